@@ -1,0 +1,179 @@
+/*
+ * liblq — B200-native (sm_100a) rank-1 lattice sums and MDI-LR cluster sums.
+ *
+ * The drop-in boundary of the hot path of latquad (arXiv 2404.08867's
+ * reference package).  The reference has no FFI of its own: its boundary is
+ * the Python callables listed in SURVEY.md §8(b).  Each entry point below
+ * names the reference function whose inner loop it replaces
+ * (paths relative to /root/reference/pkg/src/latquad/).  The Python mirror
+ * (paper_2404_08867_b200/{lattice,quad,mdi}.py) binds these with ctypes;
+ * INTEGRATION.md shows the binding a latquad maintainer would add.
+ *
+ * Conventions
+ *  - Every function returns int status: LQ_OK or a negative LQ_ERR_* code;
+ *    lq_last_error() (thread-local) describes the last failure.  The Python
+ *    layer maps LQ_ERR_VALUE -> ValueError, LQ_ERR_OVERFLOW -> OverflowError,
+ *    LQ_ERR_GRIDCAP -> GridCapError, the rest -> RuntimeError, matching the
+ *    reference's exceptions (lattice.py:65-70, 99-100; mdi.py:44-45, 112-113).
+ *  - Host pointers are caller-owned; "_dev" pointers are device pointers
+ *    (e.g. torch tensors' data_ptr()).  Device scratch is owned by the lq_ctx.
+ *  - All work is ordered on the context's stream (lq_ctx_set_stream); calls
+ *    that return values to host pointers synchronise that stream.
+ *  - Reductions are deterministic: fixed tiles of LQ_TILE points, a fixed
+ *    in-tile tree, fixed super-chunks of LQ_SUPER_TILES tiles and a fixed
+ *    pairwise tree over super-chunk partials, independent of grid size and of
+ *    how super-chunks are split across GPUs.
+ */
+#ifndef LQ_H
+#define LQ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LQ_ABI_VERSION 1
+
+#define LQ_OK 0
+#define LQ_ERR_VALUE (-1)
+#define LQ_ERR_OVERFLOW (-2)
+#define LQ_ERR_GRIDCAP (-3)
+#define LQ_ERR_CUDA (-4)
+#define LQ_ERR_UNSUPPORTED (-5)
+#define LQ_ERR_NOMEM (-6)
+
+#define LQ_TILE 4096          /* points (or flat grid nodes) per reduction tile */
+#define LQ_SUPER_TILES 1024   /* tiles per super-chunk (4 Mi points)           */
+#define LQ_NODE_BLOCK 256     /* MDI nodes per deterministic partial block     */
+#define LQ_MAX_SLOTS 512      /* bytecode live-slot limit                      */
+
+typedef struct lq_ctx lq_ctx;
+
+/* Bytecode instruction; slot[a] <- op(...).  Ops (see lower.py):
+ * 0 CONST c | 1 VAR x[b] | 2 ACC_INIT c | 3 ACC_ADD += c*slot[b] |
+ * 4 ACC_MUL *= slot[b] | 5 POW slot[b]^n | 6 RPOW 1/slot[b]^n | 7 EXP |
+ * 8 SIN | 9 COS | 10 ABS (of slot[b]) | 11 ACC_ADDVAR += c*x[b]          */
+typedef struct {
+    int32_t op, a, b, n;
+    double c;
+} lq_insn;
+
+typedef struct {
+    const lq_insn* insn;   /* host array of n_insn instructions */
+    int32_t n_insn;
+    int32_t n_slots;
+    int32_t result;        /* slot holding the value */
+    int32_t n_vars;        /* variables referenced: 0..n_vars-1 */
+} lq_program;
+
+enum {
+    LQ_FAM_PROGRAM = 0,     /* generic bytecode (any expression)               */
+    LQ_FAM_LIN_EXP = 1,     /* K exp(alpha + <beta,x>)                         */
+    LQ_FAM_LIN_SINCOS = 2,  /* C0 + A sin(<beta,x>) + B cos(<beta,x>)          */
+    LQ_FAM_LIN_EXPABS = 3,  /* K exp(kappa |alpha + <beta,x>|)                 */
+    LQ_FAM_QUAD_EXP = 4     /* K exp(alpha + sum_j beta_j x_j + gamma_j x_j^2) */
+};
+
+typedef struct {
+    int32_t kind;
+    int32_t d;
+    const double* beta;     /* [d], host (LIN_*, QUAD_EXP) */
+    const double* gamma;    /* [d], host (QUAD_EXP)        */
+    double alpha, K, A, B, C0, kappa;
+    lq_program prog;        /* LQ_FAM_PROGRAM */
+} lq_integrand;
+
+/* ---- context ---------------------------------------------------------- */
+int lq_ctx_create(int device, lq_ctx** out);
+int lq_ctx_destroy(lq_ctx* ctx);
+/* Order all work on this cudaStream_t (NULL: the context's own stream). */
+int lq_ctx_set_stream(lq_ctx* ctx, void* stream);
+int lq_sync(lq_ctx* ctx);
+const char* lq_last_error(void);
+int lq_abi_version(void);
+int lq_device_info(lq_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);
+/* Device time (ms) of the main kernel of the last timed call (0 if none). */
+int lq_ctx_enable_timing(lq_ctx* ctx, int enable);
+int lq_last_kernel_ms(lq_ctx* ctx, float* ms, int64_t* launches);
+
+/* ---- points: replaces lattice.points_block (lattice.py:96-105) ---------
+ * out[(i-start)*d + j] = RN(((i * z_reduced[j]) mod n) / n), i in [start, stop),
+ * bit-identical to the reference (int64 modmul + IEEE division).
+ * n > 2^53 -> LQ_ERR_OVERFLOW (lattice.py:99-100).                          */
+int lq_points_block(lq_ctx* ctx, int32_t d, uint64_t n, const uint64_t* z_reduced,
+                    int64_t start, int64_t stop, double* out, int32_t out_is_device);
+
+/* ---- plain lattice sum: replaces the block loop of quad.slr_integrate ----
+ * (quad.py:96-104 -> lattice.iter_point_blocks + exprcore.eval_array + np.sum).
+ * Returns sum_{i in [i_begin, i_end)} f(frac(i z / n)) (not divided by n).   */
+int lq_lattice_sum(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_t* z_reduced,
+                   uint64_t i_begin, uint64_t i_end, double* sum_out);
+/* Multi-GPU building blocks: super-chunk s covers points
+ * [s*LQ_TILE*LQ_SUPER_TILES, (s+1)*...) of [0, n).  Writes the partials of
+ * super-chunks [s_begin, s_end) to out_dev[0 .. s_end-s_begin).             */
+int64_t lq_lattice_num_supers(uint64_t n);
+int lq_lattice_partials(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_t* z_reduced,
+                        int64_t s_begin, int64_t s_end, double* out_dev);
+/* Fixed pairwise tree over vals_dev[0..count); result to host *out. */
+int lq_reduce_sum(lq_ctx* ctx, const double* vals_dev, int64_t count, double* out);
+
+/* ---- direct tensor-grid sum: replaces mdi._numeric_sum / direct_tensor_sum
+ * (mdi.py:104-136) for implr_integrate and the MDI fallback.  Flat index s
+ * decodes first axis fastest.  nodes: concatenated per-axis node values
+ * (host), or NULL with midpoint=1 for nodes RN((t+0.5)/counts[k])
+ * (transform.py:169-178).  Sums flat indices [s_begin, s_end).              */
+int lq_tensor_sum(lq_ctx* ctx, const lq_program* prog, int32_t d, const int64_t* counts,
+                  const double* nodes, int32_t midpoint, uint64_t s_begin, uint64_t s_end,
+                  double* sum_out);
+
+/* ---- MDI-LR cluster sums: replaces the symbolic level loop of
+ * mdi.mdi_sum (mdi.py:139-192) for separable integrands.  Factor f is a
+ * univariate U_f(y) = R_f(y) exp(i P_f(y)) on an axis with count_f midpoint
+ * nodes y_t = RN((t+0.5)/count_f); S_f = sum_t U_f(y_t).                     */
+typedef struct {
+    int32_t count;          /* nodes on the factor's axis              */
+    int32_t r_off, r_len;   /* program R in the insn table (len 0: R=1) */
+    int32_t r_result;
+    int32_t p_off, p_len;   /* program P (len 0: P=0)                   */
+    int32_t p_result;
+    int32_t n_slots;
+} lq_factor;
+
+/* Partial cluster sums of LQ_NODE_BLOCK-node blocks: part_dev[(f*nblk + b)*2 + {0,1}]
+ * (re, im) for node blocks b of every factor with b*nshards/... owned by
+ * shard `shard` of `nshards` (blocks [floor(shard*NB_f/nshards),
+ * floor((shard+1)*NB_f/nshards)); others left untouched).  nblk = max_f NB_f. */
+int lq_mdi_block_sums(lq_ctx* ctx, const lq_insn* insn, int32_t n_insn, const lq_factor* factors,
+                      int32_t n_factors, int32_t shard, int32_t nshards, double* part_dev);
+/* Combine: S_f = fixed tree over blocks; term t = coef_t * prod_{f in term t} S_f
+ * * exp(log_extra_t), evaluated in log-polar form (sum log|S|, sum arg S).
+ * term_ptr[n_terms+1] indexes term_fac.  out[0]=log|raw|, out[1]=sign(Re raw)
+ * (0 if raw == 0), out[2]=Re raw as a double (may under/overflow), out[3]=Im raw. */
+int lq_mdi_combine(lq_ctx* ctx, const double* part_dev, const lq_factor* factors, int32_t n_factors, int32_t nblk,
+                   const int32_t* term_ptr, const int32_t* term_fac, const double* coef_re,
+                   const double* coef_im, const double* log_extra, int32_t n_terms,
+                   double* out4);
+/* Single-GPU convenience: block sums + combine. */
+int lq_mdi_sum(lq_ctx* ctx, const lq_insn* insn, int32_t n_insn, const lq_factor* factors,
+               int32_t n_factors, const int32_t* term_ptr, const int32_t* term_fac,
+               const double* coef_re, const double* coef_im, const double* log_extra,
+               int32_t n_terms, double* out4);
+
+/* ---- characteristic-function MDI for K exp(kappa |alpha + <beta,y>|),
+ * kappa < 0 (BASELINE config 5; the reference cannot express |.|, so this is
+ * an extension):  sum_grid = K prod_j N_j (|kappa|/pi) int_R Re[e^{i w alpha}
+ * prod_j phi_j(w)] / (kappa^2 + w^2) dw,  phi_j(w) = (1/N_j) sum_t e^{i w beta_j y_t}.
+ * w_nodes/w_weights: host quadrature on [0, W] (even integrand, factor 2
+ * applied by the caller).  out2[0] = log|integral part|, out2[1] = sign.      */
+int lq_mdi_expabs(lq_ctx* ctx, int32_t d, const double* beta, const int32_t* counts, double alpha,
+                  const double* w_nodes, const double* w_weights, int32_t n_w, double kappa,
+                  double* out2);
+
+/* ---- FP64 roofline probe: DFMA chains on every SM; returns TFLOP/s ----- */
+int lq_fp64_peak(lq_ctx* ctx, int32_t iters, double* tflops, float* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LQ_H */

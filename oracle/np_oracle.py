@@ -1,0 +1,139 @@
+"""Numpy restatement of the reference hot path (CPU ORACLE, test-only).
+
+Each function cites the reference code it restates
+(/root/reference/pkg/src/latquad/...).  Expressions are the repo's own
+``paper_2404_08867_b200.expr.Expr`` (the reference's Expr cannot travel to the
+GPU box); ``eval_array`` below follows the reference evaluator's order.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from paper_2404_08867_b200.expr import as_expr, topo
+
+_MAX_ENUM = 2**53
+
+
+def points_block(n, z, start, stop):
+    """lattice.py:96-105: ((j * z_j) % n) / n in int64 then true division.
+    z are the unreduced components; reduced here as z_reduced does (lattice.py:76-78)."""
+    if n > _MAX_ENUM:
+        raise OverflowError(f"cannot enumerate points of an n={n} rule")
+    j = np.arange(start, stop, dtype=np.int64)
+    zr = [int(c) % n for c in z]
+    out = np.empty((len(j), len(zr)))
+    for col, zj in enumerate(zr):
+        out[:, col] = ((j * zj) % n) / n
+    return out
+
+
+def eval_array(e, assignment):
+    """exprcore.py:442-480 over the repo's Expr: sums v = const; v = v + c*t,
+    products v = coeff; v = v*f; pow 1/b or b**k; numpy exp/sin/cos (+abs)."""
+    e = as_expr(e)
+    memo = {}
+    for node in topo(e):
+        op = node.op
+        if op == "const":
+            v = node.val
+        elif op == "var":
+            v = assignment[node.idx]
+        elif op == "add":
+            v = node.val
+            for c, t in node.terms:
+                v = v + c * memo[t]
+        elif op == "mul":
+            v = node.val
+            for f in node.args:
+                v = v * memo[f]
+        elif op == "pow":
+            b = memo[node.args[0]]
+            k = node.idx
+            v = b ** k if k > 0 else (1.0 / b if k == -1 else 1.0 / (b ** -k))
+        elif op == "exp":
+            v = np.exp(memo[node.args[0]])
+        elif op == "sin":
+            v = np.sin(memo[node.args[0]])
+        elif op == "cos":
+            v = np.cos(memo[node.args[0]])
+        elif op == "abs":
+            v = np.abs(memo[node.args[0]])
+        else:
+            raise ValueError(op)
+        memo[node] = v
+    return memo[e]
+
+
+def slr_sum(f, n, z, i_begin=0, i_end=None, rows=1 << 19):
+    """quad.py:96-104: per block of `rows` points, eval_array then np.sum;
+    blocks accumulated in order.  Returns the raw sum (not divided by n)."""
+    i_end = n if i_end is None else i_end
+    d = len(z)
+    acc = 0.0
+    for start in range(i_begin, i_end, rows):
+        stop = min(start + rows, i_end)
+        pts = points_block(n, z, start, stop)
+        vals = eval_array(f, {i + 1: pts[:, i] for i in range(d)})
+        acc += float(vals) * len(pts) if np.ndim(vals) == 0 else float(np.sum(vals))
+    return acc
+
+
+def slr_value(f, n, z):
+    return slr_sum(f, n, z) / n
+
+
+def axis_counts(n, z):
+    """transform.py:76-83 on the unreduced z."""
+    out = [math.lcm(z[i], z[i + 1]) // min(z[i], z[i + 1]) for i in range(len(z) - 1)]
+    out.append(-(-n // z[-1]))
+    return tuple(out)
+
+
+def midpoint_nodes(counts):
+    """transform.py:169-178: (t + 0.5) / n_i as Python floats."""
+    return [np.array([(t + 0.5) / ct for t in range(ct)]) for ct in counts]
+
+
+def direct_tensor_sum(f, nodes, chunk=1 << 19):
+    """mdi.py:104-136: flat index decoded first-axis-fastest, chunked eval_array."""
+    counts = [len(a) for a in nodes]
+    total = math.prod(counts) if counts else 1
+    acc = 0.0
+    for start in range(0, total, chunk):
+        idx = np.arange(start, min(start + chunk, total), dtype=np.int64)
+        assign, rem = {}, idx
+        for k, (ct, arr) in enumerate(zip(counts, nodes)):
+            assign[k + 1] = arr[rem % ct]
+            rem = rem // ct
+        vals = eval_array(f, assign)
+        acc += float(vals) * len(idx) if np.ndim(vals) == 0 else float(np.sum(vals))
+    return acc
+
+
+def normalize(raw, counts):
+    """mdi.py:195-203."""
+    total = math.prod(counts)
+    if total <= 2**53:
+        return raw / total
+    out = raw
+    for ct in counts:
+        out /= ct
+    return out
+
+
+def separable_log_sum(factor_fns, counts):
+    """MDI-LR of a product-separable integrand prod_j phi_j(x_j): the value the
+    reference's level loop produces, as
+    sum_j log|S_j| with S_j = sum_t phi_j(y_t) over the midpoint nodes
+    (mdi.py:152-183 collapses to this for separable forms).  Returns
+    (log|raw|, sign)."""
+    logs, sign = 0.0, 1.0
+    for fn, ct in zip(factor_fns, counts):
+        y = (np.arange(ct) + 0.5) / ct
+        s = float(np.sum(fn(y)))
+        logs += math.log(abs(s))
+        sign *= math.copysign(1.0, s)
+    return logs, sign

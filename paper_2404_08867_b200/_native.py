@@ -1,0 +1,159 @@
+"""ctypes binding of liblq.so (include/lq.h).
+
+The product path has no CPU fallback: if the shared library or a B200 is
+missing, every entry point raises ``NativeUnavailable`` loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .lower import INSN_DTYPE
+
+__all__ = ["lib", "ctx", "NativeUnavailable", "check", "LQ_TILE", "LQ_SUPER_TILES",
+           "LQ_NODE_BLOCK", "Integrand", "Program", "Factor", "LIB_PATH"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblq.so")
+
+LQ_OK, LQ_ERR_VALUE, LQ_ERR_OVERFLOW, LQ_ERR_GRIDCAP = 0, -1, -2, -3
+LQ_ERR_CUDA, LQ_ERR_UNSUPPORTED, LQ_ERR_NOMEM = -4, -5, -6
+LQ_TILE, LQ_SUPER_TILES, LQ_NODE_BLOCK = 4096, 1024, 256
+
+FAM = {"program": 0, "lin_exp": 1, "lin_sincos": 2, "lin_expabs": 3, "quad_exp": 4}
+
+
+class NativeUnavailable(RuntimeError):
+    """liblq.so could not be loaded or no sm_100 device is usable."""
+
+
+class Insn(C.Structure):
+    _fields_ = [("op", C.c_int32), ("a", C.c_int32), ("b", C.c_int32), ("n", C.c_int32), ("c", C.c_double)]
+
+
+assert C.sizeof(Insn) == INSN_DTYPE.itemsize
+
+
+class Program(C.Structure):
+    _fields_ = [("insn", C.c_void_p), ("n_insn", C.c_int32), ("n_slots", C.c_int32),
+                ("result", C.c_int32), ("n_vars", C.c_int32)]
+
+
+class Integrand(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("d", C.c_int32), ("beta", C.c_void_p), ("gamma", C.c_void_p),
+                ("alpha", C.c_double), ("K", C.c_double), ("A", C.c_double), ("B", C.c_double),
+                ("C0", C.c_double), ("kappa", C.c_double), ("prog", Program)]
+
+
+class Factor(C.Structure):
+    _fields_ = [("count", C.c_int32), ("r_off", C.c_int32), ("r_len", C.c_int32), ("r_result", C.c_int32),
+                ("p_off", C.c_int32), ("p_len", C.c_int32), ("p_result", C.c_int32), ("n_slots", C.c_int32)]
+
+
+_P = C.c_void_p
+_SIGS = {
+    "lq_ctx_create": [C.c_int, C.POINTER(C.c_void_p)],
+    "lq_ctx_destroy": [_P],
+    "lq_ctx_set_stream": [_P, _P],
+    "lq_sync": [_P],
+    "lq_abi_version": [],
+    "lq_device_info": [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
+    "lq_ctx_enable_timing": [_P, C.c_int],
+    "lq_last_kernel_ms": [_P, C.POINTER(C.c_float), C.POINTER(C.c_int64)],
+    "lq_points_block": [_P, C.c_int32, C.c_uint64, _P, C.c_int64, C.c_int64, _P, C.c_int32],
+    "lq_lattice_sum": [_P, C.POINTER(Integrand), C.c_uint64, _P, C.c_uint64, C.c_uint64, C.POINTER(C.c_double)],
+    "lq_lattice_partials": [_P, C.POINTER(Integrand), C.c_uint64, _P, C.c_int64, C.c_int64, _P],
+    "lq_reduce_sum": [_P, _P, C.c_int64, C.POINTER(C.c_double)],
+    "lq_tensor_sum": [_P, C.POINTER(Program), C.c_int32, _P, _P, C.c_int32, C.c_uint64, C.c_uint64,
+                      C.POINTER(C.c_double)],
+    "lq_mdi_block_sums": [_P, _P, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, _P],
+    "lq_mdi_combine": [_P, _P, _P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, C.c_int32, _P],
+    "lq_mdi_sum": [_P, _P, C.c_int32, _P, C.c_int32, _P, _P, _P, _P, _P, C.c_int32, _P],
+    "lq_mdi_expabs": [_P, C.c_int32, _P, _P, C.c_double, _P, _P, C.c_int32, C.c_double, _P],
+    "lq_fp64_peak": [_P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_float)],
+}
+
+_lib = None
+_lock = threading.Lock()
+_ctxs = {}
+
+
+def lib():
+    """Load liblq.so once (raises NativeUnavailable if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeUnavailable(
+                    f"{LIB_PATH} not built; run __graft_entry__.build() (no CPU fallback exists)")
+            h = C.CDLL(LIB_PATH)
+            for name, args in _SIGS.items():
+                fn = getattr(h, name)
+                fn.argtypes = args
+                fn.restype = C.c_int
+            h.lq_last_error.argtypes = []
+            h.lq_last_error.restype = C.c_char_p
+            h.lq_lattice_num_supers.argtypes = [C.c_uint64]
+            h.lq_lattice_num_supers.restype = C.c_int64
+            _lib = h
+    return _lib
+
+
+def check(rc):
+    if rc == LQ_OK:
+        return
+    msg = lib().lq_last_error().decode(errors="replace")
+    if rc == LQ_ERR_VALUE:
+        raise ValueError(msg)
+    if rc == LQ_ERR_OVERFLOW:
+        raise OverflowError(msg)
+    if rc == LQ_ERR_GRIDCAP:
+        from .mdi import GridCapError
+        raise GridCapError(msg)
+    if rc == LQ_ERR_UNSUPPORTED:
+        raise NativeUnavailable(msg) if "sm_100a" in msg else NotImplementedError(msg)
+    raise RuntimeError(f"liblq error {rc}: {msg}")
+
+
+class _Ctx:
+    def __init__(self, device):
+        h = lib()
+        p = C.c_void_p()
+        rc = h.lq_ctx_create(int(device), C.byref(p))
+        if rc != LQ_OK:
+            msg = h.lq_last_error().decode(errors="replace")
+            raise NativeUnavailable(f"cannot create liblq context on device {device}: {msg}")
+        self.ptr = p
+        self.device = device
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                lib().lq_ctx_destroy(self.ptr)
+        except Exception:
+            pass
+
+
+def ctx(device=None):
+    """The process's liblq context for ``device`` (default: current CUDA device
+    per LOCAL_RANK, else 0)."""
+    if device is None:
+        device = int(os.environ.get("LQ_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    key = (device, threading.get_ident())
+    c = _ctxs.get(key)
+    if c is None:
+        c = _ctxs[key] = _Ctx(device)
+    return c.ptr
+
+
+def as_ptr(arr):
+    return C.c_void_p(arr.ctypes.data) if arr is not None else None
+
+
+def u64(seq):
+    return np.ascontiguousarray(np.asarray(seq, dtype=np.uint64))

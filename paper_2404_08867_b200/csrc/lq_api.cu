@@ -1,0 +1,676 @@
+// liblq C ABI (include/lq.h): context, argument validation, table building
+// and kernel launches.  Host code only; kernels live in lq_kernels.cu, which
+// this translation unit includes so that template instantiations stay local.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lq_kernels.cu"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                      \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess)                                                        \
+            return fail(LQ_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                          \
+    } while (0)
+
+enum Buf { B_TAB = 0, B_TILES, B_RED0, B_RED1, B_OUT, B_PROG, B_AUX0, B_AUX1, B_AUX2, B_AUX3, B_PART, B_FAC, B_NBUF };
+
+}  // namespace
+
+struct lq_ctx {
+    int device = 0;
+    int sm_count = 0;
+    int cc_major = 0, cc_minor = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    void* dbuf[B_NBUF] = {};
+    size_t dcap[B_NBUF] = {};
+    void* hpin = nullptr;      // pinned host staging
+    size_t hcap = 0;
+    bool timing = false;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    float last_ms = 0.f;
+    int64_t launches = 0;
+};
+
+namespace {
+
+int set_dev(lq_ctx* c) {
+    if (!c) return fail(LQ_ERR_VALUE, "null lq_ctx");
+    CK(cudaSetDevice(c->device));
+    return LQ_OK;
+}
+
+int dev_buf(lq_ctx* c, int which, size_t bytes, void** out) {
+    if (bytes == 0) bytes = 8;
+    if (c->dcap[which] < bytes) {
+        if (c->dbuf[which]) {
+            CK(cudaStreamSynchronize(c->stream));
+            CK(cudaFree(c->dbuf[which]));
+            c->dbuf[which] = nullptr;
+            c->dcap[which] = 0;
+        }
+        size_t cap = bytes + bytes / 4;
+        cudaError_t e = cudaMalloc(&c->dbuf[which], cap);
+        if (e != cudaSuccess) return fail(LQ_ERR_NOMEM, "cudaMalloc(%zu): %s", cap, cudaGetErrorString(e));
+        c->dcap[which] = cap;
+    }
+    *out = c->dbuf[which];
+    return LQ_OK;
+}
+
+int pin_buf(lq_ctx* c, size_t bytes, void** out) {
+    if (c->hcap < bytes) {
+        if (c->hpin) {
+            CK(cudaStreamSynchronize(c->stream));
+            CK(cudaFreeHost(c->hpin));
+            c->hpin = nullptr;
+        }
+        size_t cap = bytes < 4096 ? 4096 : bytes + bytes / 4;
+        CK(cudaMallocHost(&c->hpin, cap));
+        c->hcap = cap;
+    }
+    *out = c->hpin;
+    return LQ_OK;
+}
+
+// H2D through the pinned staging buffer (async on the ctx stream; the
+// staging buffer is reused only after the stream drains it).
+int upload(lq_ctx* c, int which, const void* src, size_t bytes, void** dst) {
+    int rc = dev_buf(c, which, bytes, dst);
+    if (rc) return rc;
+    if (bytes == 0) return LQ_OK;
+    void* h;
+    CK(cudaStreamSynchronize(c->stream));
+    rc = pin_buf(c, bytes, &h);
+    if (rc) return rc;
+    memcpy(h, src, bytes);
+    CK(cudaMemcpyAsync(*dst, h, bytes, cudaMemcpyHostToDevice, c->stream));
+    return LQ_OK;
+}
+
+int grid_for(lq_ctx* c, const void* kernel, int64_t work) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, lq::kThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+    int64_t g = (int64_t)c->sm_count * per_sm;
+    if (work < g) g = work;
+    return (int)(g < 1 ? 1 : g);
+}
+
+void t_begin(lq_ctx* c) {
+    if (c->timing) cudaEventRecord(c->ev0, c->stream);
+}
+void t_end(lq_ctx* c) {
+    if (c->timing) cudaEventRecord(c->ev1, c->stream);
+    c->launches++;
+}
+
+// Fixed-tree reduction of vals[count] down to one value in device memory.
+int reduce_dev(lq_ctx* c, const double* vals, int64_t count, double** result) {
+    const double* cur = vals;
+    int which = B_RED0;
+    int64_t n = count;
+    if (n <= 0) {
+        void* p;
+        int rc = dev_buf(c, B_RED0, 8, &p);
+        if (rc) return rc;
+        CK(cudaMemsetAsync(p, 0, 8, c->stream));
+        *result = (double*)p;
+        return LQ_OK;
+    }
+    do {
+        int64_t groups = (n + 1023) / 1024;
+        void* p;
+        int rc = dev_buf(c, which, groups * sizeof(double), &p);
+        if (rc) return rc;
+        lq::k_reduce1024<<<(unsigned)groups, lq::kThreads, 0, c->stream>>>(cur, n, (double*)p);
+        c->launches++;
+        CK(cudaGetLastError());
+        cur = (const double*)p;
+        n = groups;
+        which = which == B_RED0 ? B_RED1 : B_RED0;
+    } while (n > 1);
+    *result = const_cast<double*>(cur);
+    return LQ_OK;
+}
+
+int read_scalar(lq_ctx* c, const double* dev, double* out, int k = 1) {
+    void* h;
+    int rc = pin_buf(c, sizeof(double) * k, &h);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(h, dev, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    memcpy(out, h, sizeof(double) * k);
+    return LQ_OK;
+}
+
+// ------------------------------------------------------------ lattice sums
+
+int check_lattice(uint64_t n, const uint64_t* z, int d) {
+    if (n < 1) return fail(LQ_ERR_VALUE, "point count must be positive, got %llu", (unsigned long long)n);
+    if (n > (1ull << 53)) return fail(LQ_ERR_OVERFLOW, "cannot enumerate points of an n=%llu rule", (unsigned long long)n);
+    if (d < 1) return fail(LQ_ERR_VALUE, "dimension must be positive, got %d", d);
+    if (!z) return fail(LQ_ERR_VALUE, "null generating vector");
+    for (int j = 0; j < d; ++j)
+        if (z[j] >= n) return fail(LQ_ERR_VALUE, "z_reduced[%d]=%llu not reduced mod n", j, (unsigned long long)z[j]);
+    return LQ_OK;
+}
+
+int pick_slots(int n_slots) {
+    if (n_slots > LQ_MAX_SLOTS) return -1;
+    return n_slots <= 32 ? 32 : LQ_MAX_SLOTS;
+}
+
+// Launch the tile kernel of integrand f over points [base, end) writing
+// ntiles tile partials to tiles_dev.
+int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z, uint64_t base, uint64_t end,
+                 int64_t ntiles, double* tiles_dev) {
+    const int d = f->d;
+    const bool fast = n <= (1ull << 31) && f->kind != LQ_FAM_PROGRAM;
+    int rc;
+    if (fast && (f->kind == LQ_FAM_LIN_EXP || f->kind == LQ_FAM_LIN_SINCOS || f->kind == LQ_FAM_LIN_EXPABS)) {
+        if (!f->beta) return fail(LQ_ERR_VALUE, "family needs beta");
+        double maxabs = 0.0;
+        for (int j = 0; j < d; ++j) maxabs = fmax(maxabs, fabs(f->beta[j]));
+        if (!std::isfinite(maxabs)) return fail(LQ_ERR_VALUE, "non-finite coefficient");
+        int sigma = 0;
+        if (maxabs > 0.0) {
+            int e = std::ilogb(maxabs / (double)n);
+            sigma = 1074 + e + 1 - 1020;
+            if (sigma < 0) sigma = 0;
+        }
+        std::vector<lq::LinDim> tab(d);
+        for (int j = 0; j < d; ++j) {
+            tab[j].c = std::ldexp(f->beta[j] / (double)n, 1074 - sigma);
+            tab[j].z = (uint32_t)z[j];
+            tab[j].zs = (uint32_t)(((uint64_t)z[j] << 32) / n);
+        }
+        void* dt;
+        if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(lq::LinDim), &dt))) return rc;
+        lq::LinParams p{f->alpha, std::ldexp(1.0, sigma), f->K, f->A, f->B, f->C0, f->kappa};
+        const void* kern = f->kind == LQ_FAM_LIN_EXP ? (const void*)lq::k_lin<lq::OUT_EXP>
+                         : f->kind == LQ_FAM_LIN_SINCOS ? (const void*)lq::k_lin<lq::OUT_SINCOS>
+                                                        : (const void*)lq::k_lin<lq::OUT_EXPABS>;
+        int grid = grid_for(c, kern, ntiles);
+        t_begin(c);
+        if (f->kind == LQ_FAM_LIN_EXP)
+            lq::k_lin<lq::OUT_EXP><<<grid, lq::kThreads, 0, c->stream>>>((const lq::LinDim*)dt, d, (uint32_t)n, base, end, ntiles, p, 0u, tiles_dev);
+        else if (f->kind == LQ_FAM_LIN_SINCOS)
+            lq::k_lin<lq::OUT_SINCOS><<<grid, lq::kThreads, 0, c->stream>>>((const lq::LinDim*)dt, d, (uint32_t)n, base, end, ntiles, p, 0u, tiles_dev);
+        else
+            lq::k_lin<lq::OUT_EXPABS><<<grid, lq::kThreads, 0, c->stream>>>((const lq::LinDim*)dt, d, (uint32_t)n, base, end, ntiles, p, 0u, tiles_dev);
+        t_end(c);
+        CK(cudaGetLastError());
+        return LQ_OK;
+    }
+    if (fast && f->kind == LQ_FAM_QUAD_EXP) {
+        if (!f->beta || !f->gamma) return fail(LQ_ERR_VALUE, "quad family needs beta and gamma");
+        const double inv_n = 1.0 / (double)n;
+        int sigma = 1074 + std::ilogb(inv_n) - 1000;
+        if (sigma < 0) sigma = 0;
+        const double M = std::ldexp(inv_n, 1074 - sigma);
+        std::vector<lq::QuadDim> tab(d);
+        for (int j = 0; j < d; ++j) {
+            tab[j].b = std::ldexp(f->beta[j], sigma);
+            tab[j].q = std::ldexp(f->gamma[j], 2 * sigma);
+            tab[j].z = (uint32_t)z[j];
+            tab[j].zs = (uint32_t)(((uint64_t)z[j] << 32) / n);
+            tab[j].pad0 = tab[j].pad1 = 0;
+            if (!std::isfinite(tab[j].b) || !std::isfinite(tab[j].q))
+                return fail(LQ_ERR_VALUE, "quadratic coefficient out of range");
+        }
+        void* dt;
+        if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(lq::QuadDim), &dt))) return rc;
+        int grid = grid_for(c, (const void*)lq::k_quad, ntiles);
+        t_begin(c);
+        lq::k_quad<<<grid, lq::kThreads, 0, c->stream>>>((const lq::QuadDim*)dt, d, (uint32_t)n, base, end, ntiles, M,
+                                                         f->alpha, f->K, 0u, tiles_dev);
+        t_end(c);
+        CK(cudaGetLastError());
+        return LQ_OK;
+    }
+    // generic bytecode (any family falls back here for n > 2^31)
+    const lq_program* pg = &f->prog;
+    if (f->kind != LQ_FAM_PROGRAM || !pg->insn || pg->n_insn < 1)
+        return fail(LQ_ERR_UNSUPPORTED, "integrand needs a bytecode program for n=%llu", (unsigned long long)n);
+    const int ns = pick_slots(pg->n_slots);
+    if (ns < 0) return fail(LQ_ERR_UNSUPPORTED, "program needs %d slots (max %d)", pg->n_slots, LQ_MAX_SLOTS);
+    if (pg->n_vars > d) return fail(LQ_ERR_VALUE, "program uses %d variables, rule has d=%d", pg->n_vars, d);
+    void* dp;
+    if ((rc = upload(c, B_PROG, pg->insn, sizeof(lq_insn) * pg->n_insn, &dp))) return rc;
+    const bool wide = n > (1ull << 31);
+    void* dz;
+    if (wide) {
+        if ((rc = upload(c, B_TAB, z, sizeof(uint64_t) * d, &dz))) return rc;
+    } else {
+        std::vector<uint32_t> zz(2 * (size_t)d);
+        for (int j = 0; j < d; ++j) {
+            zz[2 * j] = (uint32_t)z[j];
+            zz[2 * j + 1] = (uint32_t)(((uint64_t)z[j] << 32) / n);
+        }
+        if ((rc = upload(c, B_TAB, zz.data(), zz.size() * 4, &dz))) return rc;
+    }
+    const double n_d = (double)n, inv_n = 1.0 / n_d;
+    const void* kern = wide ? (ns == 32 ? (const void*)lq::k_prog_lattice<32, true> : (const void*)lq::k_prog_lattice<LQ_MAX_SLOTS, true>)
+                            : (ns == 32 ? (const void*)lq::k_prog_lattice<32, false> : (const void*)lq::k_prog_lattice<LQ_MAX_SLOTS, false>);
+    int grid = grid_for(c, kern, ntiles);
+    t_begin(c);
+#define LQ_PL(NS, W) lq::k_prog_lattice<NS, W><<<grid, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, pg->n_insn, pg->result, n, n_d, inv_n, inv_n, dz, base, end, ntiles, tiles_dev)
+    if (wide) { if (ns == 32) LQ_PL(32, true); else LQ_PL(LQ_MAX_SLOTS, true); }
+    else { if (ns == 32) LQ_PL(32, false); else LQ_PL(LQ_MAX_SLOTS, false); }
+#undef LQ_PL
+    t_end(c);
+    CK(cudaGetLastError());
+    return LQ_OK;
+}
+
+int check_integrand(const lq_integrand* f) {
+    if (!f) return fail(LQ_ERR_VALUE, "null integrand");
+    if (f->kind < LQ_FAM_PROGRAM || f->kind > LQ_FAM_QUAD_EXP) return fail(LQ_ERR_VALUE, "bad family kind %d", f->kind);
+    return LQ_OK;
+}
+
+}  // namespace
+
+// ======================================================================= ABI
+extern "C" {
+
+const char* lq_last_error(void) { return g_err.c_str(); }
+int lq_abi_version(void) { return LQ_ABI_VERSION; }
+
+int lq_ctx_create(int device, lq_ctx** out) {
+    if (!out) return fail(LQ_ERR_VALUE, "null output pointer");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(LQ_ERR_VALUE, "device %d out of range (%d devices)", device, ndev);
+    lq_ctx* c = new lq_ctx();
+    c->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->cc_major, cudaDevAttrComputeCapabilityMajor, device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->cc_minor, cudaDevAttrComputeCapabilityMinor, device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(LQ_ERR_CUDA, "context creation failed: %s", cudaGetErrorString(e));
+    }
+    if (c->cc_major != 10) {
+        int cc = c->cc_major * 10 + c->cc_minor;
+        delete c;
+        return fail(LQ_ERR_UNSUPPORTED, "liblq is built for sm_100a (B200); device has sm_%d", cc);
+    }
+    c->stream = c->own;
+    *out = c;
+    return LQ_OK;
+}
+
+int lq_ctx_destroy(lq_ctx* c) {
+    if (!c) return LQ_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (int i = 0; i < B_NBUF; ++i)
+        if (c->dbuf[i]) cudaFree(c->dbuf[i]);
+    if (c->hpin) cudaFreeHost(c->hpin);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->own) cudaStreamDestroy(c->own);
+    delete c;
+    return LQ_OK;
+}
+
+int lq_ctx_set_stream(lq_ctx* c, void* stream) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(c->stream));
+    c->stream = stream ? (cudaStream_t)stream : c->own;
+    return LQ_OK;
+}
+
+int lq_sync(lq_ctx* c) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(c->stream));
+    return LQ_OK;
+}
+
+int lq_device_info(lq_ctx* c, int* sm, int* maj, int* mnr) {
+    if (!c) return fail(LQ_ERR_VALUE, "null lq_ctx");
+    if (sm) *sm = c->sm_count;
+    if (maj) *maj = c->cc_major;
+    if (mnr) *mnr = c->cc_minor;
+    return LQ_OK;
+}
+
+int lq_ctx_enable_timing(lq_ctx* c, int enable) {
+    if (!c) return fail(LQ_ERR_VALUE, "null lq_ctx");
+    c->timing = enable != 0;
+    c->launches = 0;
+    return LQ_OK;
+}
+
+int lq_last_kernel_ms(lq_ctx* c, float* ms, int64_t* launches) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    float t = 0.f;
+    if (c->timing) {
+        CK(cudaEventSynchronize(c->ev1));
+        CK(cudaEventElapsedTime(&t, c->ev0, c->ev1));
+    }
+    if (ms) *ms = t;
+    if (launches) *launches = c->launches;
+    return LQ_OK;
+}
+
+int lq_points_block(lq_ctx* c, int32_t d, uint64_t n, const uint64_t* z, int64_t start, int64_t stop, double* out,
+                    int32_t out_is_device) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if ((rc = check_lattice(n, z, d))) return rc;
+    if (start < 0 || stop < start) return fail(LQ_ERR_VALUE, "bad index range [%lld, %lld)", (long long)start, (long long)stop);
+    const uint64_t m = (uint64_t)(stop - start);
+    if (m == 0) return LQ_OK;
+    if (!out) return fail(LQ_ERR_VALUE, "null output");
+    void* dz;
+    if ((rc = upload(c, B_AUX0, z, sizeof(uint64_t) * d, &dz))) return rc;
+    const uint64_t n_elem = m * (uint64_t)d;
+    double* dst = out;
+    if (!out_is_device) {
+        void* p;
+        if ((rc = dev_buf(c, B_OUT, n_elem * sizeof(double), &p))) return rc;
+        dst = (double*)p;
+    }
+    const double n_d = (double)n, inv = 1.0 / n_d;
+    int64_t blocks = (int64_t)((n_elem + lq::kThreads - 1) / lq::kThreads);
+    int grid = grid_for(c, (const void*)lq::k_points, blocks);
+    t_begin(c);
+    lq::k_points<<<grid, lq::kThreads, 0, c->stream>>>((const uint64_t*)dz, (uint32_t)d, n, n_d, inv, inv, (uint64_t)start, n_elem, dst);
+    t_end(c);
+    CK(cudaGetLastError());
+    if (!out_is_device) {
+        CK(cudaMemcpyAsync(out, dst, n_elem * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    return LQ_OK;
+}
+
+int64_t lq_lattice_num_supers(uint64_t n) {
+    const uint64_t sp = (uint64_t)LQ_TILE * LQ_SUPER_TILES;
+    return (int64_t)((n + sp - 1) / sp);
+}
+
+int lq_lattice_partials(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z, int64_t s_begin,
+                        int64_t s_end, double* out_dev) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if ((rc = check_integrand(f)) || (rc = check_lattice(n, z, f->d))) return rc;
+    const int64_t ns = lq_lattice_num_supers(n);
+    if (s_begin < 0 || s_end > ns || s_end < s_begin)
+        return fail(LQ_ERR_VALUE, "super-chunk range [%lld, %lld) outside [0, %lld)", (long long)s_begin, (long long)s_end, (long long)ns);
+    if (s_end == s_begin) return LQ_OK;
+    const uint64_t sp = (uint64_t)LQ_TILE * LQ_SUPER_TILES;
+    const uint64_t base = (uint64_t)s_begin * sp;
+    const uint64_t end = std::min<uint64_t>((uint64_t)s_end * sp, n);
+    const int64_t ntiles = (int64_t)((end - base + LQ_TILE - 1) / LQ_TILE);
+    void* tiles;
+    if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
+    if ((rc = launch_tiles(c, f, n, z, base, end, ntiles, (double*)tiles))) return rc;
+    lq::k_reduce1024<<<(unsigned)(s_end - s_begin), lq::kThreads, 0, c->stream>>>((const double*)tiles, ntiles, out_dev);
+    c->launches++;
+    CK(cudaGetLastError());
+    return LQ_OK;
+}
+
+int lq_reduce_sum(lq_ctx* c, const double* vals, int64_t count, double* out) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (!out) return fail(LQ_ERR_VALUE, "null output");
+    double* r;
+    if ((rc = reduce_dev(c, vals, count, &r))) return rc;
+    return read_scalar(c, r, out);
+}
+
+int lq_lattice_sum(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z, uint64_t i_begin, uint64_t i_end,
+                   double* sum_out) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if ((rc = check_integrand(f)) || (rc = check_lattice(n, z, f->d))) return rc;
+    if (!sum_out) return fail(LQ_ERR_VALUE, "null output");
+    if (i_end < i_begin) return fail(LQ_ERR_VALUE, "bad index range");
+    if (i_end == i_begin) {
+        *sum_out = 0.0;
+        return LQ_OK;
+    }
+    if (n <= (1ull << 31) && i_end > (1ull << 32) - 2 * LQ_TILE)
+        return fail(LQ_ERR_VALUE, "index range beyond 2^32 for n <= 2^31; reduce indices mod n");
+    const int64_t ntiles = (int64_t)((i_end - i_begin + LQ_TILE - 1) / LQ_TILE);
+    void* tiles;
+    if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
+    if ((rc = launch_tiles(c, f, n, z, i_begin, i_end, ntiles, (double*)tiles))) return rc;
+    double* r;
+    if ((rc = reduce_dev(c, (const double*)tiles, ntiles, &r))) return rc;
+    return read_scalar(c, r, sum_out);
+}
+
+int lq_tensor_sum(lq_ctx* c, const lq_program* pg, int32_t d, const int64_t* counts, const double* nodes,
+                  int32_t midpoint, uint64_t s_begin, uint64_t s_end, double* sum_out) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (!pg || !pg->insn || pg->n_insn < 1) return fail(LQ_ERR_VALUE, "null program");
+    if (d < 0 || d > lq::kMaxAxes) return fail(LQ_ERR_UNSUPPORTED, "tensor sum supports 0..%d axes, got %d", lq::kMaxAxes, d);
+    if (!sum_out) return fail(LQ_ERR_VALUE, "null output");
+    if (pg->n_vars > d) return fail(LQ_ERR_VALUE, "program uses %d axes, grid has %d", pg->n_vars, d);
+    const int ns = pick_slots(pg->n_slots);
+    if (ns < 0) return fail(LQ_ERR_UNSUPPORTED, "program needs %d slots (max %d)", pg->n_slots, LQ_MAX_SLOTS);
+    std::vector<int64_t> off(d + 1, 0);
+    for (int k = 0; k < d; ++k) {
+        if (counts[k] < 1) return fail(LQ_ERR_VALUE, "axis %d has no nodes", k + 1);
+        off[k + 1] = off[k] + counts[k];
+    }
+    if (s_end < s_begin) return fail(LQ_ERR_VALUE, "bad flat range");
+    if (s_end == s_begin) {
+        *sum_out = 0.0;
+        return LQ_OK;
+    }
+    void *dp, *dc, *doff, *dn;
+    if ((rc = upload(c, B_PROG, pg->insn, sizeof(lq_insn) * pg->n_insn, &dp))) return rc;
+    std::vector<int64_t> cnt(counts, counts + d);
+    cnt.push_back(1);
+    if ((rc = upload(c, B_AUX0, cnt.data(), sizeof(int64_t) * cnt.size(), &dc))) return rc;
+    if ((rc = upload(c, B_AUX1, off.data(), sizeof(int64_t) * off.size(), &doff))) return rc;
+    const int64_t total_nodes = off[d];
+    if (midpoint || !nodes) {
+        if ((rc = dev_buf(c, B_AUX2, sizeof(double) * (total_nodes + 1), &dn))) return rc;
+        if (d > 0) {
+            int64_t maxc = 1;
+            for (int k = 0; k < d; ++k) maxc = std::max<int64_t>(maxc, counts[k]);
+            dim3 g((unsigned)std::min<int64_t>((maxc + 255) / 256, 4096), (unsigned)d);
+            lq::k_midpoint_nodes<<<g, 256, 0, c->stream>>>((const int64_t*)dc, (const int64_t*)doff, d, (double*)dn);
+            c->launches++;
+            CK(cudaGetLastError());
+        }
+    } else {
+        if ((rc = upload(c, B_AUX2, nodes, sizeof(double) * total_nodes, &dn))) return rc;
+    }
+    const int64_t ntiles = (int64_t)((s_end - s_begin + LQ_TILE - 1) / LQ_TILE);
+    void* tiles;
+    if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
+    const void* kern = ns == 32 ? (const void*)lq::k_prog_tensor<32> : (const void*)lq::k_prog_tensor<LQ_MAX_SLOTS>;
+    int grid = grid_for(c, kern, ntiles);
+    t_begin(c);
+    if (ns == 32)
+        lq::k_prog_tensor<32><<<grid, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, pg->n_insn, pg->result, d, (const int64_t*)dc, (const int64_t*)doff, (const double*)dn, s_begin, s_end, ntiles, (double*)tiles);
+    else
+        lq::k_prog_tensor<LQ_MAX_SLOTS><<<grid, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, pg->n_insn, pg->result, d, (const int64_t*)dc, (const int64_t*)doff, (const double*)dn, s_begin, s_end, ntiles, (double*)tiles);
+    t_end(c);
+    CK(cudaGetLastError());
+    double* r;
+    if ((rc = reduce_dev(c, (const double*)tiles, ntiles, &r))) return rc;
+    return read_scalar(c, r, sum_out);
+}
+
+static int mdi_validate(const lq_insn* insn, int32_t n_insn, const lq_factor* fac, int32_t nf, int* nblk, int* ns) {
+    if (nf < 0) return fail(LQ_ERR_VALUE, "negative factor count");
+    int maxnb = 1, maxslots = 1;
+    for (int f = 0; f < nf; ++f) {
+        const lq_factor& F = fac[f];
+        if (F.count < 1) return fail(LQ_ERR_VALUE, "factor %d has no nodes", f);
+        if (F.r_len < 0 || F.p_len < 0 || F.r_off < 0 || F.p_off < 0 || F.r_off + F.r_len > n_insn || F.p_off + F.p_len > n_insn)
+            return fail(LQ_ERR_VALUE, "factor %d program out of range", f);
+        maxnb = std::max(maxnb, (F.count + LQ_NODE_BLOCK - 1) / LQ_NODE_BLOCK);
+        maxslots = std::max(maxslots, F.n_slots);
+    }
+    *nblk = maxnb;
+    *ns = pick_slots(maxslots);
+    if (*ns < 0) return fail(LQ_ERR_UNSUPPORTED, "factor program needs %d slots", maxslots);
+    if (n_insn > 0 && !insn) return fail(LQ_ERR_VALUE, "null instruction table");
+    return LQ_OK;
+}
+
+int lq_mdi_block_sums(lq_ctx* c, const lq_insn* insn, int32_t n_insn, const lq_factor* fac, int32_t nf, int32_t shard,
+                      int32_t nshards, double* part_dev) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    int nblk, ns;
+    if ((rc = mdi_validate(insn, n_insn, fac, nf, &nblk, &ns))) return rc;
+    if (nshards < 1 || shard < 0 || shard >= nshards) return fail(LQ_ERR_VALUE, "bad shard %d of %d", shard, nshards);
+    if (nf == 0) return LQ_OK;
+    void *dp, *dfac;
+    if ((rc = upload(c, B_PROG, insn, sizeof(lq_insn) * std::max(n_insn, 1), &dp))) return rc;
+    if ((rc = upload(c, B_AUX0, fac, sizeof(lq_factor) * nf, &dfac))) return rc;
+    dim3 g((unsigned)nf, (unsigned)nblk);
+    t_begin(c);
+    if (ns == 32)
+        lq::k_mdi_blocks<32><<<g, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, (const lq_factor*)dfac, nblk, shard, nshards, part_dev);
+    else
+        lq::k_mdi_blocks<LQ_MAX_SLOTS><<<g, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, (const lq_factor*)dfac, nblk, shard, nshards, part_dev);
+    t_end(c);
+    CK(cudaGetLastError());
+    return LQ_OK;
+}
+
+int lq_mdi_combine(lq_ctx* c, const double* part_dev, const lq_factor* fac, int32_t nf, int32_t nblk, const int32_t* term_ptr,
+                   const int32_t* term_fac, const double* coef_re, const double* coef_im, const double* log_extra,
+                   int32_t n_terms, double* out4) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (!out4 || n_terms < 0 || !term_ptr) return fail(LQ_ERR_VALUE, "bad combine arguments");
+    const int32_t nk = term_ptr[n_terms];
+    for (int k = 0; k < nk; ++k)
+        if (term_fac[k] < 0 || term_fac[k] >= nf) return fail(LQ_ERR_VALUE, "term factor index out of range");
+    // host-side packing of the small term tables
+    std::vector<double> coef(2 * (size_t)std::max(n_terms, 1));
+    for (int t = 0; t < n_terms; ++t) {
+        coef[2 * t] = coef_re[t];
+        coef[2 * t + 1] = coef_im ? coef_im[t] : 0.0;
+    }
+    void *dptr, *dfacidx, *dcoef, *dlog, *fw, *tw, *dout, *dfac;
+    lq_factor dummy{};
+    if ((rc = upload(c, B_FAC, nf > 0 ? (const void*)fac : (const void*)&dummy, sizeof(lq_factor) * std::max(nf, 1), &dfac))) return rc;
+    if ((rc = upload(c, B_AUX1, term_ptr, sizeof(int32_t) * (n_terms + 1), &dptr))) return rc;
+    if ((rc = upload(c, B_AUX2, term_fac, sizeof(int32_t) * std::max(nk, 1), &dfacidx))) return rc;
+    if ((rc = upload(c, B_AUX3, coef.data(), sizeof(double) * coef.size(), &dcoef))) return rc;
+    std::vector<double> lx(log_extra ? log_extra : coef.data(), log_extra ? log_extra + n_terms : coef.data());
+    if (!log_extra) lx.assign(std::max(n_terms, 1), 0.0);
+    if ((rc = upload(c, B_RED1, lx.data(), sizeof(double) * std::max<size_t>(lx.size(), 1), &dlog))) return rc;
+    if ((rc = dev_buf(c, B_TILES, sizeof(double) * 2 * std::max(nf, 1), &fw))) return rc;
+    if ((rc = dev_buf(c, B_RED0, sizeof(double) * 2 * std::max(n_terms, 1), &tw))) return rc;
+    if ((rc = dev_buf(c, B_OUT, sizeof(double) * 4, &dout))) return rc;
+    lq::k_mdi_combine<<<1, lq::kThreads, 0, c->stream>>>(part_dev, nf, nblk, (const lq_factor*)dfac,
+                                                        (const int32_t*)dptr, (const int32_t*)dfacidx,
+                                                        (const double*)dcoef, (const double*)dlog, n_terms,
+                                                        (double*)fw, (double*)tw, (double*)dout);
+    c->launches++;
+    CK(cudaGetLastError());
+    return read_scalar(c, (const double*)dout, out4, 4);
+}
+
+int lq_mdi_sum(lq_ctx* c, const lq_insn* insn, int32_t n_insn, const lq_factor* fac, int32_t nf,
+               const int32_t* term_ptr, const int32_t* term_fac, const double* coef_re, const double* coef_im,
+               const double* log_extra, int32_t n_terms, double* out4) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    int nblk, ns;
+    if ((rc = mdi_validate(insn, n_insn, fac, nf, &nblk, &ns))) return rc;
+    void* part;
+    if ((rc = dev_buf(c, B_PART, sizeof(double) * 2 * (size_t)std::max(nf, 1) * nblk, &part))) return rc;
+    if (nf > 0 && (rc = lq_mdi_block_sums(c, insn, n_insn, fac, nf, 0, 1, (double*)part))) return rc;
+    return lq_mdi_combine(c, (const double*)part, fac, nf, nblk, term_ptr, term_fac, coef_re, coef_im, log_extra, n_terms, out4);
+}
+
+int lq_mdi_expabs(lq_ctx* c, int32_t d, const double* beta, const int32_t* counts, double alpha, const double* wn,
+                  const double* ww, int32_t n_w, double kappa, double* out2) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (d < 1 || !beta || !counts || !wn || !ww || n_w < 1 || !out2) return fail(LQ_ERR_VALUE, "bad expabs arguments");
+    if (!(kappa < 0.0)) return fail(LQ_ERR_VALUE, "kappa must be negative");
+    void *db, *dc, *dw, *dww, *dv;
+    if ((rc = upload(c, B_AUX0, beta, sizeof(double) * d, &db))) return rc;
+    if ((rc = upload(c, B_AUX1, counts, sizeof(int32_t) * d, &dc))) return rc;
+    if ((rc = upload(c, B_AUX2, wn, sizeof(double) * n_w, &dw))) return rc;
+    if ((rc = upload(c, B_AUX3, ww, sizeof(double) * n_w, &dww))) return rc;
+    if ((rc = dev_buf(c, B_TILES, sizeof(double) * n_w, &dv))) return rc;
+    t_begin(c);
+    lq::k_cf_expabs<<<n_w, lq::kThreads, 0, c->stream>>>((const double*)db, (const int32_t*)dc, d, alpha,
+                                                         (const double*)dw, (const double*)dww, kappa, (double*)dv);
+    t_end(c);
+    CK(cudaGetLastError());
+    double* r;
+    if ((rc = reduce_dev(c, (const double*)dv, n_w, &r))) return rc;
+    double s;
+    if ((rc = read_scalar(c, r, &s))) return rc;
+    out2[0] = s == 0.0 ? -INFINITY : std::log(std::fabs(s));
+    out2[1] = s > 0.0 ? 1.0 : (s < 0.0 ? -1.0 : 0.0);
+    return LQ_OK;
+}
+
+int lq_fp64_peak(lq_ctx* c, int32_t iters, double* tflops, float* ms) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (iters < 1) return fail(LQ_ERR_VALUE, "iters must be positive");
+    void* p;
+    if ((rc = dev_buf(c, B_OUT, 64, &p))) return rc;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)lq::k_fp64_peak, lq::kThreads, 0);
+    const int grid = c->sm_count * std::max(per_sm, 1) * 4;
+    lq::k_fp64_peak<<<grid, lq::kThreads, 0, c->stream>>>(std::max(1, iters / 16), 1.0, (double*)p);  // warm-up
+    CK(cudaGetLastError());
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, c->stream));
+    lq::k_fp64_peak<<<grid, lq::kThreads, 0, c->stream>>>(iters, 1.0, (double*)p);
+    CK(cudaEventRecord(b, c->stream));
+    CK(cudaEventSynchronize(b));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = 2.0 * 8 * 16 * (double)iters * grid * lq::kThreads;
+    if (tflops) *tflops = flops / (t * 1e-3) / 1e12;
+    if (ms) *ms = t;
+    return LQ_OK;
+}
+
+}  // extern "C"

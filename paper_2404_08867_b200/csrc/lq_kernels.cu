@@ -1,0 +1,427 @@
+// liblq kernels (sm_100a).  See include/lq.h for the ABI and DESIGN.md for
+// the roofline of each kernel.
+#include "lq_device.cuh"
+
+namespace lq {
+
+// ============================================================ points_block
+// out[e], e = row*d + col, = RN(((start+row) * z[col] mod n) / n).
+// Flat mapping keeps the HBM writes fully coalesced (the kernel is bound by
+// the 8 B/coordinate store); the residue comes from one FP64-estimated
+// modmul per element.
+__global__ void __launch_bounds__(kThreads) k_points(const uint64_t* __restrict__ z, uint32_t d, uint64_t n,
+                                                     double n_d, double inv_n, double ninv_mm,
+                                                     uint64_t start, uint64_t n_elem, double* __restrict__ out) {
+    for (uint64_t e = blockIdx.x * (uint64_t)kThreads + threadIdx.x; e < n_elem;
+         e += (uint64_t)gridDim.x * kThreads) {
+        uint64_t row = e / d;
+        uint32_t col = (uint32_t)(e - row * d);
+        uint64_t i = start + row;
+        uint64_t r = mulmod_u64(i % n, __ldg(z + col), n, ninv_mm);
+        out[e] = exact_div((double)r, n_d, inv_n);
+    }
+}
+
+// ============================================================ family sums
+// Per-dimension record of the linear-form kernels.
+struct LinDim {
+    double c;       // beta_j / n * 2^(1074 - sigma): multiplies the denormal 2^-1074 r
+    uint32_t z;     // z_j mod n
+    uint32_t zs;    // floor(z * 2^32 / n)  (Shoup)
+};
+
+struct QuadDim {
+    double b;       // beta_j * 2^sigma
+    double q;       // gamma_j * 2^(2 sigma)
+    uint32_t z, zs;
+    uint32_t pad0, pad1;
+};
+
+struct LinParams {
+    double alpha, scale, K, A, B, C0, kappa;
+};
+
+enum : int { OUT_EXP = 0, OUT_SINCOS = 1, OUT_EXPABS = 2 };
+
+template <int OUTER>
+__device__ __forceinline__ double outer_fn(double acc, const LinParams& p) {
+    if (OUTER == OUT_EXP) return p.K * exp(fma(acc, p.scale, p.alpha));
+    if (OUTER == OUT_EXPABS) return p.K * exp(p.kappa * fabs(fma(acc, p.scale, p.alpha)));
+    double s, c;
+    sincos(acc * p.scale, &s, &c);
+    return p.C0 + p.A * s + p.B * c;
+}
+
+// Plain lattice sum of f = outer(alpha + <beta, x>), n <= 2^31.
+// Tile = 256 threads x 16 consecutive points.  Dimension-outer loop: per
+// (thread, j) one Shoup modmul gives the first residue, then each of the 16
+// points costs IADD + VIADDMNMX (next residue) + one DFMA with the residue
+// read as a denormal -- x_j/n folded into the coefficient, no conversion, no
+// division.  tile_out[t] = sum over tile t (fixed tree).
+template <int OUTER>
+__global__ void __launch_bounds__(kThreads, 2) k_lin(const LinDim* __restrict__ dims, int d, uint32_t n,
+                                                      uint64_t base, uint64_t end, int64_t ntiles,
+                                                      LinParams prm, uint32_t hmask,
+                                                      double* __restrict__ tile_out) {
+    __shared__ double sh[8];
+    uint32_t H[kPts];
+    #pragma unroll
+    for (int k = 0; k < kPts; ++k) H[k] = (threadIdx.x + k) & hmask;   // opaque zeros
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t i0_64 = base + (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kPts;
+        const uint32_t i0 = (uint32_t)i0_64;   // < 2^32 (n <= 2^31)
+        double acc[kPts];
+        #pragma unroll
+        for (int p = 0; p < kPts; ++p) acc[p] = 0.0;
+        #pragma unroll 1
+        for (int j = 0; j < d; ++j) {
+            const LinDim dm = dims[j];
+            const uint32_t zm = dm.z - n;
+            uint32_t r = mulmod_shoup(i0, dm.z, dm.zs, n);
+            #pragma unroll
+            for (int p = 0; p < kPts; ++p) {
+                acc[p] = fma(dm.c, denorm_of(r, H[p]), acc[p]);
+                r = step_mod(r, dm.z, zm);
+            }
+        }
+        double s = 0.0;
+        #pragma unroll
+        for (int p = 0; p < kPts; ++p) {
+            double f = outer_fn<OUTER>(acc[p], prm);
+            s += (i0_64 + p < end) ? f : 0.0;
+        }
+        s = block_sum(s, sh);
+        if (threadIdx.x == 0) tile_out[tile] = s;
+    }
+}
+
+// Plain lattice sum of f = K exp(alpha + sum_j b_j x_j + q_j x_j^2), n <= 2^31.
+// Per point-dim: residue step (2 int ops), xs = denormal * M (exact scale),
+// t = q xs + b, acc += t xs: 3 FP64 ops (FP64-pipe bound).
+__global__ void __launch_bounds__(kThreads, 2) k_quad(const QuadDim* __restrict__ dims, int d, uint32_t n,
+                                                       uint64_t base, uint64_t end, int64_t ntiles,
+                                                       double M, double alpha, double K, uint32_t hmask,
+                                                       double* __restrict__ tile_out) {
+    __shared__ double sh[8];
+    uint32_t H[kPts];
+    #pragma unroll
+    for (int k = 0; k < kPts; ++k) H[k] = (threadIdx.x + k) & hmask;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t i0_64 = base + (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kPts;
+        const uint32_t i0 = (uint32_t)i0_64;
+        double acc[kPts];
+        #pragma unroll
+        for (int p = 0; p < kPts; ++p) acc[p] = 0.0;
+        #pragma unroll 1
+        for (int j = 0; j < d; ++j) {
+            const QuadDim dm = dims[j];
+            const uint32_t zm = dm.z - n;
+            uint32_t r = mulmod_shoup(i0, dm.z, dm.zs, n);
+            #pragma unroll
+            for (int p = 0; p < kPts; ++p) {
+                const double xs = denorm_of(r, H[p]) * M;
+                acc[p] = fma(fma(dm.q, xs, dm.b), xs, acc[p]);
+                r = step_mod(r, dm.z, zm);
+            }
+        }
+        double s = 0.0;
+        #pragma unroll
+        for (int p = 0; p < kPts; ++p) {
+            double f = K * exp(alpha + acc[p]);
+            s += (i0_64 + p < end) ? f : 0.0;
+        }
+        s = block_sum(s, sh);
+        if (threadIdx.x == 0) tile_out[tile] = s;
+    }
+}
+
+// ============================================================ generic bytecode
+struct LatSrc32 {   // n <= 2^31: Shoup modmul per variable access
+    uint32_t i, n;
+    double n_d, inv_n;
+    const uint2* zz;   // (z, zs)
+    __device__ __forceinline__ double x(int b) const {
+        const uint2 t = __ldg(zz + b);
+        return exact_div((double)mulmod_shoup(i, t.x, t.y, n), n_d, inv_n);
+    }
+};
+
+struct LatSrc64 {   // n < 2^53
+    uint64_t i, n;
+    double n_d, inv_n, ninv_mm;
+    const uint64_t* z;
+    __device__ __forceinline__ double x(int b) const {
+        return exact_div((double)mulmod_u64(i, __ldg(z + b), n, ninv_mm), n_d, inv_n);
+    }
+};
+
+template <int NS, bool WIDE>
+__global__ void __launch_bounds__(kThreads) k_prog_lattice(const lq_insn* __restrict__ prog, int n_insn, int result,
+                                                          uint64_t n, double n_d, double inv_n, double ninv_mm,
+                                                          const void* __restrict__ ztab, uint64_t base, uint64_t end,
+                                                          int64_t ntiles, double* __restrict__ tile_out) {
+    __shared__ double sh[8];
+    double slot[NS];
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t i0 = base + (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kPts;
+        double s = 0.0;
+        for (int p = 0; p < kPts; ++p) {
+            const uint64_t i = i0 + p;
+            double f = 0.0;
+            if (i < end) {
+                if (WIDE) {
+                    LatSrc64 src{i % n, n, n_d, inv_n, ninv_mm, (const uint64_t*)ztab};
+                    f = run_program<NS>(prog, n_insn, result, src, slot);
+                } else {
+                    LatSrc32 src{(uint32_t)i, (uint32_t)n, n_d, inv_n, (const uint2*)ztab};
+                    f = run_program<NS>(prog, n_insn, result, src, slot);
+                }
+            }
+            s += f;
+        }
+        s = block_sum(s, sh);
+        if (threadIdx.x == 0) tile_out[tile] = s;
+    }
+}
+
+// ============================================================ tensor grid
+constexpr int kMaxAxes = 128;
+
+struct TensorSrc {
+    const double* nodes;
+    const int64_t* off;
+    const uint32_t* digit;
+    __device__ __forceinline__ double x(int b) const { return __ldg(nodes + off[b] + digit[b]); }
+};
+
+// Direct sum over the tensor grid, flat index s = s_1 + s_2 n_1 + ... (first
+// axis fastest, mdi.py:118-124).  Each thread decodes its first index and
+// advances an odometer over its 16 consecutive nodes.
+template <int NS>
+__global__ void __launch_bounds__(kThreads) k_prog_tensor(const lq_insn* __restrict__ prog, int n_insn, int result,
+                                                          int d, const int64_t* __restrict__ counts,
+                                                          const int64_t* __restrict__ off,
+                                                          const double* __restrict__ nodes,
+                                                          uint64_t base, uint64_t end, int64_t ntiles,
+                                                          double* __restrict__ tile_out) {
+    __shared__ double sh[8];
+    double slot[NS];
+    uint32_t digit[kMaxAxes];
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t s0 = base + (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kPts;
+        uint64_t rem = s0;
+        for (int k = 0; k < d; ++k) {
+            const uint64_t c = (uint64_t)counts[k];
+            digit[k] = (uint32_t)(rem % c);
+            rem /= c;
+        }
+        TensorSrc src{nodes, off, digit};
+        double s = 0.0;
+        for (int p = 0; p < kPts; ++p) {
+            if (s0 + p < end) s += run_program<NS>(prog, n_insn, result, src, slot);
+            for (int k = 0; k < d; ++k) {   // odometer
+                if (++digit[k] < (uint64_t)counts[k]) break;
+                digit[k] = 0;
+            }
+        }
+        s = block_sum(s, sh);
+        if (threadIdx.x == 0) tile_out[tile] = s;
+    }
+}
+
+__global__ void k_midpoint_nodes(const int64_t* __restrict__ counts, const int64_t* __restrict__ off, int d,
+                                 double* __restrict__ nodes) {
+    // nodes of axis k: RN((t + 0.5) / n_k), transform.py:177
+    const int k = blockIdx.y;
+    if (k >= d) return;
+    const int64_t c = counts[k];
+    const double cd = (double)c, inv = 1.0 / cd;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < c; t += (int64_t)gridDim.x * blockDim.x)
+        nodes[off[k] + t] = exact_div((double)t + 0.5, cd, inv);
+}
+
+// ============================================================ MDI cluster sums
+struct UnivSrc {
+    double y;
+    __device__ __forceinline__ double x(int) const { return y; }
+};
+
+// One CTA per (factor, node block): evaluates U_f(y_t) = R(y_t) e^{i P(y_t)}
+// on the block's 256 midpoint nodes and writes the (re, im) block sums.
+template <int NS>
+__global__ void __launch_bounds__(kThreads) k_mdi_blocks(const lq_insn* __restrict__ insn,
+                                                         const lq_factor* __restrict__ fac, int nblk,
+                                                         int shard, int nshards, double* __restrict__ part) {
+    __shared__ double sh[8];
+    double slot[NS];
+    const int f = blockIdx.x, b = blockIdx.y;
+    const lq_factor F = fac[f];
+    const int NB = (F.count + LQ_NODE_BLOCK - 1) / LQ_NODE_BLOCK;
+    const int b_lo = (int)(((int64_t)shard * NB) / nshards), b_hi = (int)(((int64_t)(shard + 1) * NB) / nshards);
+    if (b < b_lo || b >= b_hi) return;
+    const int t = b * LQ_NODE_BLOCK + threadIdx.x;
+    double re = 0.0, im = 0.0;
+    if (t < F.count) {
+        const double cd = (double)F.count;
+        UnivSrc src{exact_div((double)t + 0.5, cd, 1.0 / cd)};
+        double R = F.r_len ? run_program<NS>(insn + F.r_off, F.r_len, F.r_result, src, slot) : 1.0;
+        if (F.p_len) {
+            double P = run_program<NS>(insn + F.p_off, F.p_len, F.p_result, src, slot);
+            double sn, cs;
+            sincos(P, &sn, &cs);
+            re = R * cs;
+            im = R * sn;
+        } else {
+            re = R;
+        }
+    }
+    re = block_sum(re, sh);
+    im = block_sum(im, sh);
+    if (threadIdx.x == 0) {
+        part[((int64_t)f * nblk + b) * 2 + 0] = re;
+        part[((int64_t)f * nblk + b) * 2 + 1] = im;
+    }
+}
+
+// Single-CTA combine in log-polar form (fixed order everywhere).
+__global__ void __launch_bounds__(kThreads) k_mdi_combine(const double* __restrict__ part, int n_factors, int nblk,
+                                                          const lq_factor* __restrict__ fac,
+                                                          const int32_t* __restrict__ term_ptr,
+                                                          const int32_t* __restrict__ term_fac,
+                                                          const double* __restrict__ coef,   // [n_terms][2]
+                                                          const double* __restrict__ log_extra, int n_terms,
+                                                          double* __restrict__ fwork,   // [n_factors][2]
+                                                          double* __restrict__ twork,   // [n_terms][2]
+                                                          double* __restrict__ out4) {
+    __shared__ double sh[8];
+    __shared__ double sM;
+    for (int f = threadIdx.x; f < n_factors; f += kThreads) {
+        const int NB = (fac[f].count + LQ_NODE_BLOCK - 1) / LQ_NODE_BLOCK;
+        double re = 0.0, im = 0.0;
+        for (int b = 0; b < NB; ++b) {
+            re += part[((int64_t)f * nblk + b) * 2 + 0];
+            im += part[((int64_t)f * nblk + b) * 2 + 1];
+        }
+        fwork[2 * f + 0] = log(hypot(re, im));
+        fwork[2 * f + 1] = atan2(im, re);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_terms; t += kThreads) {
+        double L = log(hypot(coef[2 * t], coef[2 * t + 1])) + log_extra[t];
+        double ph = atan2(coef[2 * t + 1], coef[2 * t]);
+        for (int k = term_ptr[t]; k < term_ptr[t + 1]; ++k) {
+            L += fwork[2 * term_fac[k] + 0];
+            ph += fwork[2 * term_fac[k] + 1];
+        }
+        twork[2 * t + 0] = L;
+        twork[2 * t + 1] = ph;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double M = -INFINITY;
+        for (int t = 0; t < n_terms; ++t) M = fmax(M, twork[2 * t]);
+        sM = M;
+    }
+    __syncthreads();
+    const double M = sM;
+    double sre = 0.0, sim = 0.0;
+    if (M > -INFINITY) {
+        for (int t = threadIdx.x; t < n_terms; t += kThreads) {
+            const double m = exp(twork[2 * t] - M);
+            double sn, cs;
+            sincos(twork[2 * t + 1], &sn, &cs);
+            sre += m * cs;
+            sim += m * sn;
+        }
+    }
+    sre = block_sum(sre, sh);
+    sim = block_sum(sim, sh);
+    if (threadIdx.x == 0) {
+        if (M == -INFINITY || sre == 0.0) {
+            out4[0] = -INFINITY; out4[1] = 0.0; out4[2] = 0.0; out4[3] = 0.0;
+        } else {
+            out4[0] = M + log(fabs(sre));
+            out4[1] = sre > 0.0 ? 1.0 : -1.0;
+            out4[2] = sre * exp(M);
+            out4[3] = sim * exp(M);
+        }
+    }
+}
+
+// ============================================================ CF (exp-abs) MDI
+// One CTA per frequency node w: each warp forms phi_j(w) = sum_t e^{i w beta_j y_t}
+// for its directions j (lanes over t), accumulating log|phi_j| and arg phi_j;
+// the 8 warps' (log, arg) partials combine in fixed order.  val[k] =
+// weight_k * |kappa|/(kappa^2+w^2) * exp(sum log|phi|) cos(w alpha + sum arg).
+__global__ void __launch_bounds__(kThreads) k_cf_expabs(const double* __restrict__ beta, const int32_t* __restrict__ counts,
+                                                        int d, double alpha, const double* __restrict__ wn,
+                                                        const double* __restrict__ ww, double kappa,
+                                                        double* __restrict__ val) {
+    __shared__ double sl[8], sa[8];
+    const int k = blockIdx.x;
+    const double w = wn[k];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double lsum = 0.0, asum = 0.0;
+    for (int j = warp; j < d; j += kThreads / 32) {
+        const int N = counts[j];
+        const double cd = (double)N, inv = 1.0 / cd, th = w * beta[j];
+        double re = 0.0, im = 0.0;
+        for (int t = lane; t < N; t += 32) {
+            const double y = exact_div((double)t + 0.5, cd, inv);
+            double sn, cs;
+            sincos(th * y, &sn, &cs);
+            re += cs;
+            im += sn;
+        }
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            re += __shfl_xor_sync(0xffffffffu, re, o);
+            im += __shfl_xor_sync(0xffffffffu, im, o);
+        }
+        lsum += log(hypot(re, im) * inv);
+        asum += atan2(im, re);
+    }
+    if (lane == 0) { sl[warp] = lsum; sa[warp] = asum; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double L = 0.0, A = 0.0;
+        for (int q = 0; q < kThreads / 32; ++q) { L += sl[q]; A += sa[q]; }
+        const double ak = fabs(kappa);
+        val[k] = ww[k] * ak / (kappa * kappa + w * w) * exp(L) * cos(w * alpha + A);
+    }
+}
+
+// ============================================================ reductions
+// Fixed pairwise tree over groups of 1024 consecutive values (zero padded):
+// out[g] = tree(vals[1024 g .. 1024 g + 1023]).  1024 threads, 4 per thread... here
+// 256 threads each fold 4 adjacent values in a fixed order first.
+__global__ void __launch_bounds__(kThreads) k_reduce1024(const double* __restrict__ v, int64_t count,
+                                                         double* __restrict__ out) {
+    __shared__ double sh[8];
+    const int64_t g = blockIdx.x;
+    const int64_t i = g * 1024 + (int64_t)threadIdx.x * 4;
+    double a[4];
+    #pragma unroll
+    for (int q = 0; q < 4; ++q) a[q] = (i + q < count) ? v[i + q] : 0.0;
+    double s = (a[0] + a[1]) + (a[2] + a[3]);
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) out[g] = s;
+}
+
+// ============================================================ FP64 probe
+__global__ void __launch_bounds__(kThreads) k_fp64_peak(int iters, double seed, double* out) {
+    double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+           a6 = a0 + 6, a7 = a0 + 7;
+    const double m = 0.999999, c = 1e-7;
+    for (int it = 0; it < iters; ++it) {
+        #pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+            a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+        }
+    }
+    double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.678) out[0] = s;   // keep the chains live
+}
+
+}  // namespace lq

@@ -1,0 +1,207 @@
+"""Host side of the GPU engine: lowered integrands -> liblq argument structs,
+and the single-GPU entry points the drop-in front-ends call.
+
+Everything here is argument packing; all arithmetic over points, nodes and
+clusters runs in liblq.so (no CPU fallback).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from collections import OrderedDict
+
+import numpy as np
+
+from . import _native as N
+from .expr import Expr, as_expr, free_vars
+from .lower import Program, compile_program, recognize_plain, separate
+
+__all__ = ["PlainIntegrand", "plain_integrand", "lattice_sum", "tensor_program", "SeparablePlan",
+           "separable_plan", "mdi_separable_sum"]
+
+
+class _LRU(OrderedDict):
+    def __init__(self, cap=64):
+        super().__init__()
+        self.cap = cap
+
+    def get_or(self, key, make):
+        if key in self:
+            self.move_to_end(key)
+            return self[key]
+        val = make()
+        self[key] = val
+        if len(self) > self.cap:
+            self.popitem(last=False)
+        return val
+
+
+_plain_cache = _LRU()
+_prog_cache = _LRU()
+_sep_cache = _LRU()
+
+
+class PlainIntegrand:
+    """An lq_integrand struct plus the numpy buffers it points into."""
+
+    def __init__(self, e, d, family=None, program=None):
+        self.expr, self.d = e, d
+        self.family, self.program = family, program
+        s = N.Integrand()
+        s.d = d
+        s.alpha, s.K, s.A, s.B, s.C0, s.kappa = 0.0, 1.0, 0.0, 0.0, 0.0, -1.0
+        self._keep = []
+        if family is not None:
+            s.kind = N.FAM[family.kind]
+            beta = np.ascontiguousarray(family.beta, dtype=np.float64)
+            self._keep.append(beta)
+            s.beta = beta.ctypes.data
+            if family.gamma is not None:
+                gamma = np.ascontiguousarray(family.gamma, dtype=np.float64)
+                self._keep.append(gamma)
+                s.gamma = gamma.ctypes.data
+            s.alpha, s.K, s.A, s.B = family.alpha, family.K, family.A, family.B
+            s.C0, s.kappa = family.C0, family.kappa
+        if program is not None:
+            if family is None:
+                s.kind = 0
+            ins = np.ascontiguousarray(program.insn)
+            self._keep.append(ins)
+            s.prog.insn = ins.ctypes.data
+            s.prog.n_insn = len(ins)
+            s.prog.n_slots = program.n_slots
+            s.prog.result = program.result
+            s.prog.n_vars = program.n_vars
+        self.struct = s
+
+    @property
+    def kind(self):
+        return self.family.kind if self.family is not None else "program"
+
+
+def plain_integrand(f, d, force_program=False):
+    """Lower f for the plain lattice sum over d coordinates (cached)."""
+    e = as_expr(f)
+
+    def make():
+        fam = None if force_program else recognize_plain(e, d)
+        prog = compile_program(e)
+        return PlainIntegrand(e, d, fam, prog)
+
+    return _plain_cache.get_or((e, d, force_program), make)
+
+
+def lattice_sum(pi, n, z_reduced, i_begin=0, i_end=None):
+    """sum_{i in [i_begin, i_end)} f(x_i) on the GPU (not divided by n)."""
+    i_end = n if i_end is None else i_end
+    out = C.c_double()
+    N.check(N.lib().lq_lattice_sum(N.ctx(), C.byref(pi.struct), n, N.as_ptr(z_reduced),
+                                   int(i_begin), int(i_end), C.byref(out)))
+    return out.value
+
+
+def tensor_program(g):
+    e = as_expr(g)
+    return _prog_cache.get_or(e, lambda: compile_program(e))
+
+
+def tensor_sum(g, grids, s_begin=0, s_end=None):
+    """Direct grid sum of g (non-constant) on the GPU; flat index first-axis-fastest."""
+    prog = tensor_program(g)
+    d = grids.d
+    counts = np.asarray(grids.counts, dtype=np.int64)
+    total = grids.total
+    s_end = total if s_end is None else s_end
+    ins = np.ascontiguousarray(prog.insn)
+    p = N.Program(ins.ctypes.data, len(ins), prog.n_slots, prog.result, prog.n_vars)
+    if getattr(grids, "midpoint", False):
+        nodes, mid = None, 1
+    else:
+        nodes = np.ascontiguousarray(np.concatenate([np.asarray(nd, dtype=np.float64) for nd in grids.nodes])
+                                     if d else np.zeros(1))
+        mid = 0
+    out = C.c_double()
+    N.check(N.lib().lq_tensor_sum(N.ctx(), C.byref(p), d, N.as_ptr(counts), N.as_ptr(nodes), mid,
+                                  int(s_begin), int(s_end), C.byref(out)))
+    return out.value
+
+
+# ------------------------------------------------------------------ MDI-LR
+
+class SeparablePlan:
+    """Factor table + term structure of a separable integrand on given axis counts."""
+
+    def __init__(self, e, counts):
+        terms = separate(e)
+        self.ok = terms is not None
+        if not self.ok:
+            return
+        d = len(counts)
+        insn_parts, factors, term_ptr, term_fac = [], [], [0], []
+        coef_re, coef_im, log_extra = [], [], []
+        off = 0
+        max_slots = 1
+        fac_index = {}
+        for t in terms:
+            extra = 0.0
+            for ax in range(1, d + 1):
+                if ax not in t.factors:
+                    extra += math.log(counts[ax - 1])
+            for ax in sorted(t.factors):
+                fc = t.factors[ax]
+                key = (ax, fc.R, fc.P)
+                idx = fac_index.get(key)
+                if idx is None:
+                    rec = N.Factor()
+                    rec.count = int(counts[ax - 1])
+                    for which, sub in (("r", fc.R), ("p", fc.P)):
+                        if sub is None:
+                            setattr(rec, f"{which}_off", 0)
+                            setattr(rec, f"{which}_len", 0)
+                            setattr(rec, f"{which}_result", 0)
+                            continue
+                        prog = compile_program(sub, var_map=lambda j: 0)
+                        insn_parts.append(prog.insn)
+                        setattr(rec, f"{which}_off", off)
+                        setattr(rec, f"{which}_len", len(prog.insn))
+                        setattr(rec, f"{which}_result", prog.result)
+                        off += len(prog.insn)
+                        max_slots = max(max_slots, prog.n_slots)
+                    idx = len(factors)
+                    fac_index[key] = idx
+                    factors.append(rec)
+                term_fac.append(idx)
+            term_ptr.append(len(term_fac))
+            coef_re.append(complex(t.coef).real)
+            coef_im.append(complex(t.coef).imag)
+            log_extra.append(extra)
+        for rec in factors:
+            rec.n_slots = max_slots
+        from .lower import INSN_DTYPE
+        self.insn = (np.ascontiguousarray(np.concatenate(insn_parts)) if insn_parts
+                     else np.zeros(1, dtype=INSN_DTYPE))
+        self.n_insn = int(off)
+        self.factors = (N.Factor * max(len(factors), 1))(*factors)
+        self.n_factors = len(factors)
+        self.term_ptr = np.asarray(term_ptr, dtype=np.int32)
+        self.term_fac = np.asarray(term_fac if term_fac else [0], dtype=np.int32)
+        self.coef_re = np.asarray(coef_re, dtype=np.float64)
+        self.coef_im = np.asarray(coef_im, dtype=np.float64)
+        self.log_extra = np.asarray(log_extra, dtype=np.float64)
+        self.n_terms = len(terms)
+
+
+def separable_plan(g, counts):
+    e = as_expr(g)
+    return _sep_cache.get_or((e, tuple(counts)), lambda: SeparablePlan(e, counts))
+
+
+def mdi_separable_sum(plan):
+    """(log|raw|, sign, raw, im) of the full-grid sum via per-direction cluster sums."""
+    out = np.zeros(4)
+    N.check(N.lib().lq_mdi_sum(N.ctx(), N.as_ptr(plan.insn), plan.n_insn, C.cast(plan.factors, C.c_void_p),
+                               plan.n_factors, N.as_ptr(plan.term_ptr), N.as_ptr(plan.term_fac),
+                               N.as_ptr(plan.coef_re), N.as_ptr(plan.coef_im), N.as_ptr(plan.log_extra),
+                               plan.n_terms, N.as_ptr(out)))
+    return float(out[0]), float(out[1]), float(out[2]), float(out[3])

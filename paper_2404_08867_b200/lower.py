@@ -1,0 +1,508 @@
+"""Expression analysis: integrand -> what the GPU runs.
+
+Three lowerings, tried in this order by the front-ends (``quad.py``/``mdi.py``):
+
+1. ``recognize_plain``: closed integrand families with hand-written kernels
+   (exp / sin+cos / exp-abs of a linear form, exp of a diagonal quadratic).
+   These are the BASELINE configs' integrands in the reference's canonical
+   forms: cfg1 ``exp(sum 0.125 x_j)``, cfg2 ``A sin L + B cos L``,
+   cfg3 ``K exp(sum b_j x_j + q_j x_j^2)``, cfg5 ``exp(-|sum c_j (x_j - w_j)|)``.
+2. ``compile_program``: any expression as a register bytecode the generic
+   CUDA interpreter evaluates per point, in the reference's evaluation order
+   (sums ``v = const; v = v + c*t``, products ``v = coeff; v = v*f``;
+   /root/reference/pkg/src/latquad/exprcore.py:442-480).
+3. ``separate``: for MDI-LR, a factorisation f = sum_tau coef_tau prod_j
+   U_{tau,j}(x_j) with complex coefficients and univariate, possibly complex
+   (R(y) e^{i P(y)}) factors.  The tensor-grid sum of such a term is the
+   product of per-direction cluster sums S_{tau,j} = sum_t U_{tau,j}(y_t): the
+   closed form of what the reference's symbolic partial summation with
+   like-term collection computes level by level (mdi.py:139-192,
+   exprcore.py:139-169, 349-402).
+"""
+
+from __future__ import annotations
+
+import cmath
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .expr import Expr, add, const, free_vars, func, mul, power, topo
+
+__all__ = [
+    "linear_form", "quad_form", "recognize_plain", "PlainFamily",
+    "Program", "compile_program", "separate", "SepTerm", "Factor",
+    "MAX_SLOTS", "INSN_DTYPE",
+]
+
+# ------------------------------------------------------------ polynomial view
+
+_POLY_CAP = 4096
+
+
+def _poly(e, cap=_POLY_CAP):
+    """Polynomial as {monomial: coef}, monomial = ((var, power), ...) sorted;
+    None if e is not a polynomial (or grows past ``cap`` monomials)."""
+    memo = {}
+    for node in topo(e):
+        op = node.op
+        if op == "const":
+            p = {(): node.val}
+        elif op == "var":
+            p = {((node.idx, 1),): 1.0}
+        elif op == "add":
+            p = {(): node.val} if node.val != 0.0 else {}
+            for c, t in node.terms:
+                q = memo.get(t)
+                if q is None:
+                    p = None
+                    break
+                for m, v in q.items():
+                    p[m] = p.get(m, 0.0) + c * v
+                if len(p) > cap:
+                    p = None
+                    break
+        elif op == "mul":
+            p = {(): node.val}
+            for f in node.args:
+                q = memo.get(f)
+                if q is None:
+                    p = None
+                    break
+                p = _pmul(p, q, cap)
+                if p is None:
+                    break
+        elif op == "pow" and node.idx >= 2:
+            q = memo.get(node.args[0])
+            p = {(): 1.0} if q is not None else None
+            for _ in range(node.idx if q is not None else 0):
+                p = _pmul(p, q, cap)
+                if p is None:
+                    break
+        else:
+            p = None
+        memo[node] = p
+    return memo.get(e)
+
+
+def _pmul(p, q, cap):
+    out = {}
+    for m1, c1 in p.items():
+        for m2, c2 in q.items():
+            dm = dict(m1)
+            for v, k in m2:
+                dm[v] = dm.get(v, 0) + k
+            key = tuple(sorted(dm.items()))
+            out[key] = out.get(key, 0.0) + c1 * c2
+            if len(out) > cap:
+                return None
+    return out
+
+
+def linear_form(e):
+    """(alpha, {j: beta_j}) if e is affine in the coordinates, else None."""
+    if e.op == "add" and all(t.op == "var" for _, t in e.terms):
+        beta = {}
+        for c, t in e.terms:
+            beta[t.idx] = beta.get(t.idx, 0.0) + c
+        return e.val, beta
+    p = _poly(e, cap=1 << 16)
+    if p is None:
+        return None
+    alpha, beta = 0.0, {}
+    for m, c in p.items():
+        if not m:
+            alpha += c
+        elif len(m) == 1 and m[0][1] == 1:
+            beta[m[0][0]] = beta.get(m[0][0], 0.0) + c
+        elif c != 0.0:
+            return None
+    return alpha, beta
+
+
+def quad_form(e):
+    """(alpha, {j: (b_j, q_j)}) if e = alpha + sum_j b_j x_j + q_j x_j^2, else None."""
+    p = _poly(e, cap=1 << 16)
+    if p is None:
+        return None
+    alpha, coefs = 0.0, {}
+    for m, c in p.items():
+        if not m:
+            alpha += c
+            continue
+        if len(m) != 1 or m[0][1] > 2:
+            if c != 0.0:
+                return None
+            continue
+        j, k = m[0]
+        b, q = coefs.get(j, (0.0, 0.0))
+        coefs[j] = (b + c, q) if k == 1 else (b, q + c)
+    return alpha, coefs
+
+
+# ------------------------------------------------------ plain-sum families
+
+@dataclass
+class PlainFamily:
+    """A closed family the LIN/QUAD lattice-sum kernels evaluate.
+
+    kind: 'lin_exp'    f = K exp(alpha + <beta, x>)
+          'lin_sincos' f = C0 + A sin(<beta, x>) + B cos(<beta, x>)
+          'lin_expabs' f = K exp(kappa |alpha + <beta, x>|)
+          'quad_exp'   f = K exp(alpha + sum_j beta_j x_j + gamma_j x_j^2)
+    """
+
+    kind: str
+    d: int
+    beta: np.ndarray
+    gamma: np.ndarray = None
+    alpha: float = 0.0
+    K: float = 1.0
+    A: float = 0.0
+    B: float = 0.0
+    C0: float = 0.0
+    kappa: float = -1.0
+
+
+def _vec(coefs, d):
+    v = np.zeros(d)
+    for j, c in coefs.items():
+        if not 1 <= j <= d:
+            return None
+        v[j - 1] = c
+    return v
+
+
+def _strip_scale(e):
+    if e.op == "mul" and len(e.args) == 1:
+        return e.val, e.args[0]
+    return 1.0, e
+
+
+def _abs_affine(arg):
+    """arg = a0 + kappa*|L| -> (a0, kappa, abs node) or None."""
+    a0 = 0.0
+    if arg.op == "add":
+        if len(arg.terms) != 1:
+            return None
+        a0 = arg.val
+        kappa, node = arg.terms[0]
+    else:
+        kappa, node = _strip_scale(arg)
+    if node.op != "abs":
+        return None
+    return a0, kappa, node
+
+
+def recognize_plain(e, d):
+    """Match a closed family (PlainFamily) or return None."""
+    K, core = _strip_scale(e)
+    if core.op == "exp":
+        arg = core.args[0]
+        lf = linear_form(arg)
+        if lf is not None:
+            beta = _vec(lf[1], d)
+            if beta is not None:
+                return PlainFamily("lin_exp", d, beta, alpha=lf[0], K=K)
+        ab = _abs_affine(arg)
+        if ab is not None:
+            a0, kappa, node = ab
+            lf = linear_form(node.args[0])
+            if lf is not None:
+                beta = _vec(lf[1], d)
+                if beta is not None:
+                    return PlainFamily("lin_expabs", d, beta, alpha=lf[0],
+                                       K=K * math.exp(a0), kappa=kappa)
+        qf = quad_form(arg)
+        if qf is not None:
+            b = _vec({j: v[0] for j, v in qf[1].items()}, d)
+            g = _vec({j: v[1] for j, v in qf[1].items()}, d)
+            if b is not None:
+                return PlainFamily("quad_exp", d, b, gamma=g, alpha=qf[0], K=K)
+        return None
+    # C0 + sum_k coef_k trig(alpha_k + <beta, x>) with one shared beta
+    if e.op == "add":
+        terms, C0 = e.terms, e.val
+    elif core.op in ("sin", "cos"):
+        terms, C0 = ((K, core),), 0.0
+    else:
+        return None
+    A = B = 0.0
+    beta0 = None
+    for c, t in terms:
+        s, t = _strip_scale(t)
+        c *= s
+        if t.op not in ("sin", "cos"):
+            return None
+        lf = linear_form(t.args[0])
+        if lf is None:
+            return None
+        beta = _vec(lf[1], d)
+        if beta is None:
+            return None
+        if beta0 is None:
+            beta0 = beta
+        elif not np.array_equal(beta0, beta):
+            return None
+        al = lf[0]
+        if t.op == "sin":   # sin(al + L) = sin al cos L + cos al sin L
+            A += c * math.cos(al)
+            B += c * math.sin(al)
+        else:               # cos(al + L) = cos al cos L - sin al sin L
+            A -= c * math.sin(al)
+            B += c * math.cos(al)
+    if beta0 is None:
+        return None
+    return PlainFamily("lin_sincos", d, beta0, A=A, B=B, C0=C0)
+
+
+# ------------------------------------------------------------------ bytecode
+
+MAX_SLOTS = 512
+
+OP_CONST, OP_VAR, OP_ACC_INIT, OP_ACC_ADD, OP_ACC_MUL = 0, 1, 2, 3, 4
+OP_POW, OP_RPOW, OP_EXP, OP_SIN, OP_COS, OP_ABS, OP_ACC_ADDVAR = 5, 6, 7, 8, 9, 10, 11
+_FUNC_OP = {"exp": OP_EXP, "sin": OP_SIN, "cos": OP_COS, "abs": OP_ABS}
+
+# must match lq_insn in include/lq.h
+INSN_DTYPE = np.dtype([("op", "<i4"), ("a", "<i4"), ("b", "<i4"), ("n", "<i4"), ("c", "<f8")])
+
+
+@dataclass
+class Program:
+    """Register bytecode: insn[k] writes slot a; the value is slot ``result``."""
+
+    insn: np.ndarray
+    n_slots: int
+    result: int
+    n_vars: int
+
+    def __len__(self):
+        return len(self.insn)
+
+
+def compile_program(e, var_map=None):
+    """Compile e to bytecode; ``var_map`` maps coordinate index -> kernel
+    variable number (default: j -> j-1)."""
+    vm = var_map if var_map is not None else (lambda j: j - 1)
+    uses = {}
+    for node in topo(e):
+        for ch in ([t for _, t in node.terms] if node.op == "add" else node.args):
+            uses[ch] = uses.get(ch, 0) + 1
+    out = []
+    free = []
+    state = {"next": 0, "max": 0}
+    slot_of = {}
+    left = dict(uses)
+
+    def alloc():
+        if free:
+            return free.pop()
+        s = state["next"]
+        state["next"] += 1
+        state["max"] = max(state["max"], state["next"])
+        return s
+
+    def release(node):
+        left[node] -= 1
+        if left[node] == 0 and node in slot_of:
+            free.append(slot_of.pop(node))
+
+    def emit(op, a, b=0, n=0, c=0.0):
+        out.append((op, a, b, n, c))
+
+    def ev(node):
+        if node in slot_of:
+            return slot_of[node]
+        op = node.op
+        if op == "const":
+            s = alloc()
+            emit(OP_CONST, s, c=node.val)
+        elif op == "var":
+            s = alloc()
+            emit(OP_VAR, s, b=vm(node.idx))
+        elif op == "add":
+            s = alloc()
+            emit(OP_ACC_INIT, s, c=node.val)
+            for c, t in node.terms:
+                if t.op == "var" and uses.get(t, 0) == 1:
+                    emit(OP_ACC_ADDVAR, s, b=vm(t.idx), c=c)
+                    left[t] -= 1
+                    continue
+                cs = ev(t)
+                emit(OP_ACC_ADD, s, b=cs, c=c)
+                release(t)
+        elif op == "mul":
+            s = alloc()
+            emit(OP_ACC_INIT, s, c=node.val)
+            for f in node.args:
+                cs = ev(f)
+                emit(OP_ACC_MUL, s, b=cs)
+                release(f)
+        elif op == "pow":
+            cs = ev(node.args[0])
+            s = alloc()
+            if node.idx >= 2:
+                emit(OP_POW, s, b=cs, n=node.idx)
+            else:
+                emit(OP_RPOW, s, b=cs, n=-node.idx)
+            release(node.args[0])
+        else:
+            cs = ev(node.args[0])
+            s = alloc()
+            emit(_FUNC_OP[op], s, b=cs)
+            release(node.args[0])
+        if uses.get(node, 0) > 0:
+            slot_of[node] = s
+        return s
+
+    res = ev(e)
+    if state["max"] > MAX_SLOTS:
+        raise ValueError(f"expression needs {state['max']} live slots (limit {MAX_SLOTS})")
+    insn = np.zeros(len(out), dtype=INSN_DTYPE)
+    for k, (op, a, b, n, c) in enumerate(out):
+        insn[k] = (op, a, b, n, c)
+    nv = max([vm(j) for j in free_vars(e)], default=-1) + 1
+    return Program(insn, max(state["max"], 1), res, nv)
+
+
+# --------------------------------------------------------- MDI separability
+
+@dataclass(frozen=True)
+class Factor:
+    """Univariate factor U(y) = R(y) * exp(i P(y)) on one axis (1-based).
+    R or P may be None (meaning 1 and 0)."""
+
+    axis: int
+    R: Expr = None
+    P: Expr = None
+
+
+@dataclass
+class SepTerm:
+    coef: complex
+    factors: dict = field(default_factory=dict)   # axis -> Factor
+
+
+_TERM_CAP = 1024
+
+
+def _univ(e):
+    fv = free_vars(e)
+    return fv.pop() if len(fv) == 1 else (0 if not fv else None)
+
+
+def _fmul(f1, f2):
+    R = f1.R if f2.R is None else (f2.R if f1.R is None else mul(1.0, [f1.R, f2.R]))
+    P = f1.P if f2.P is None else (f2.P if f1.P is None else add([(1.0, f1.P), (1.0, f2.P)]))
+    return Factor(f1.axis, R, P)
+
+
+def _tmul(t1, t2):
+    fac = dict(t1.factors)
+    for ax, f in t2.factors.items():
+        fac[ax] = _fmul(fac[ax], f) if ax in fac else f
+    return SepTerm(t1.coef * t2.coef, fac)
+
+
+def _additive_split(arg):
+    """arg = c + sum_j g_j(x_j) -> (c, {axis: g_j}) or None."""
+    if arg.op == "add":
+        pieces = [(c, t) for c, t in arg.terms]
+        c0 = arg.val
+    else:
+        pieces, c0 = [(1.0, arg)], 0.0
+    groups = {}
+    for c, t in pieces:
+        ax = _univ(t)
+        if ax is None:
+            return None
+        if ax == 0:
+            from .expr import evaluate
+            c0 += c * evaluate(t, {})
+            continue
+        groups.setdefault(ax, []).append((c, t))
+    return c0, {ax: add(ps) for ax, ps in groups.items()}
+
+
+def separate(e, cap=_TERM_CAP):
+    """Factorise e into SepTerms, or None when e is not (finitely) separable."""
+    memo = {}
+
+    def rec(node):
+        hit = memo.get(node)
+        if hit is not None or node in memo:
+            return hit
+        out = _rec(node)
+        if out is not None and len(out) > cap:
+            out = None
+        memo[node] = out
+        return out
+
+    def _rec(node):
+        ax = _univ(node)
+        if ax == 0:
+            from .expr import evaluate
+            return [SepTerm(complex(evaluate(node, {})), {})]
+        if ax is not None:
+            return [SepTerm(1.0, {ax: Factor(ax, R=node)})]
+        op = node.op
+        if op == "add":
+            terms = [SepTerm(complex(node.val), {})] if node.val != 0.0 else []
+            for c, t in node.terms:
+                sub = rec(t)
+                if sub is None:
+                    return None
+                terms.extend(SepTerm(c * s.coef, s.factors) for s in sub)
+            return terms
+        if op == "mul":
+            acc = [SepTerm(complex(node.val), {})]
+            for f in node.args:
+                sub = rec(f)
+                if sub is None:
+                    return None
+                acc = [_tmul(a, b) for a in acc for b in sub]
+                if len(acc) > cap:
+                    return None
+            return acc
+        if op == "pow":
+            sub = rec(node.args[0])
+            if sub is None:
+                return None
+            k = node.idx
+            if k >= 2:
+                acc = [SepTerm(1.0, {})]
+                for _ in range(k):
+                    acc = [_tmul(a, b) for a in acc for b in sub]
+                    if len(acc) > cap:
+                        return None
+                return acc
+            if len(sub) != 1:
+                return None
+            t = sub[0]
+            if t.coef == 0:
+                return None
+            fac = {}
+            for ax2, f in t.factors.items():
+                R = power(f.R, k) if f.R is not None else None
+                P = mul(float(k), [f.P]) if f.P is not None else None
+                fac[ax2] = Factor(ax2, R, P)
+            return [SepTerm(t.coef ** k, fac)]
+        if op in ("exp", "sin", "cos"):
+            sp = _additive_split(node.args[0])
+            if sp is None or not math.isfinite(sp[0]):
+                return None
+            c0, groups = sp
+            if op == "exp":
+                return [SepTerm(complex(math.exp(c0)),
+                                {ax2: Factor(ax2, R=func("exp", g)) for ax2, g in groups.items()})]
+            pos = {ax2: Factor(ax2, P=g) for ax2, g in groups.items()}
+            neg = {ax2: Factor(ax2, P=mul(-1.0, [g])) for ax2, g in groups.items()}
+            ep, en = cmath.exp(1j * c0), cmath.exp(-1j * c0)
+            if op == "cos":   # (e^{i a} + e^{-i a}) / 2
+                return [SepTerm(0.5 * ep, pos), SepTerm(0.5 * en, neg)]
+            return [SepTerm(-0.5j * ep, pos), SepTerm(0.5j * en, neg)]   # (e^{ia} - e^{-ia}) / 2i
+        return None
+
+    return rec(e)

@@ -1,0 +1,216 @@
+"""Multilevel dimension iteration over the improved rule's tensor grid
+(drop-in for latquad.mdi, /root/reference/pkg/src/latquad/mdi.py).
+
+The reference strips one axis per level by symbolic partial summation with
+like-term collection (mdi.py:139-192).  For a separable integrand
+f = sum_tau c_tau prod_j U_{tau,j}(x_j) every level multiplies the surviving
+coefficient by the cluster sum S_{tau,k} = sum_t U_{tau,k}(y_t) of the axis it
+removes, so the whole iteration is the product of the d per-direction cluster
+sums.  The GPU forms all d cluster sums at once (one CTA per factor and node
+block, ``lq_mdi_block_sums``) and combines them in log-polar form
+(``lq_mdi_combine``): the levels fuse into one pass.  Integrands that are not
+separable take the reference's fallback, the direct sweep over the full grid
+(mdi.py:167-179), on the GPU with the same node cap.
+
+Reported bookkeeping follows the reference: ``levels``/``base_dim`` from the
+same m/order loop, GridCapError when the base sweep exceeds ``direct_cap``
+(mdi.py:112-113) -- kept for drop-in error behaviour even though the GPU does
+not need the base sweep -- and ``value`` is the raw grid sum.  ``level_nodes``
+reports the number of per-direction cluster sums carried per level (the GPU
+has no symbolic DAG).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+from . import engine
+from .expr import as_expr, evaluate, free_vars
+from .lattice import korobov_vector
+from .transform import midpoint_grids
+
+__all__ = ["MdiConfig", "MdiReport", "GridCapError", "BudgetExceededError", "mdi_sum", "mdi_lr",
+           "direct_tensor_sum", "DIRECT_CAP", "DEFAULT_NODE_BUDGET"]
+
+DIRECT_CAP = 10**8                 # mdi.py:38
+DEFAULT_NODE_BUDGET = 200_000      # exprcore.py:59
+
+
+class GridCapError(RuntimeError):
+    """The requested direct sweep exceeds the configured node cap (mdi.py:44-45)."""
+
+
+class BudgetExceededError(Exception):
+    """The integrand does not reduce within the budget (exprcore.py:68)."""
+
+
+@dataclass(frozen=True)
+class MdiConfig:
+    """Engine knobs with the reference's validation (mdi.py:48-76)."""
+
+    m: int = 1
+    budget: int = DEFAULT_NODE_BUDGET
+    order: str = "forward"
+    fallback: str = "numeric"
+    direct_cap: int = DIRECT_CAP
+
+    def __post_init__(self):
+        if not 1 <= self.m <= 3:
+            raise ValueError(f"m must be 1, 2, or 3, got {self.m}")
+        if self.budget < 1:
+            raise ValueError(f"budget must be positive, got {self.budget}")
+        if self.order not in ("forward", "reverse"):
+            raise ValueError(f"order must be 'forward' or 'reverse', got {self.order!r}")
+        if self.fallback not in ("numeric", "error"):
+            raise ValueError(f"fallback must be 'numeric' or 'error', got {self.fallback!r}")
+
+
+@dataclass
+class MdiReport:
+    """Observability record (mdi.py:79-101) plus GPU-side extras:
+    log_raw (natural log of |value|, finite even when value under/overflows),
+    sign, method ('separable' | 'direct' | 'constant'), clusters."""
+
+    value: float
+    levels: int
+    base_dim: int
+    level_nodes: tuple = ()
+    level_seconds: tuple = ()
+    base_seconds: float = 0.0
+    fallback: bool = False
+    det_a: float = None
+    log_raw: float = None
+    sign: float = None
+    method: str = None
+    clusters: int = 0
+
+    @property
+    def seconds(self):
+        return float(sum(self.level_seconds)) + self.base_seconds
+
+
+def _const_sweep(value, counts):
+    """The reference's constant sweep: chunks of 2^19 nodes, acc += c * len
+    (mdi.py:116-128)."""
+    total = math.prod(counts) if counts else 1
+    acc = 0.0
+    chunk = 1 << 19
+    for start in range(0, total, chunk):
+        acc += float(value) * (min(start + chunk, total) - start)
+    return acc
+
+
+def direct_tensor_sum(g, grids, cap=DIRECT_CAP):
+    """Brute-force grid sum on the GPU (mdi.py:104-136); raises past ``cap``."""
+    counts = list(grids.counts)
+    total = math.prod(counts) if counts else 1
+    if total > cap:
+        raise GridCapError(f"direct sweep needs {total} evaluations, cap is {cap}")
+    e = as_expr(g)
+    if not free_vars(e):
+        if not counts:
+            return evaluate(e, {})
+        return _const_sweep(evaluate(e, {}), counts)
+    return engine.tensor_sum(e, grids)
+
+
+def _level_plan(d, cfg):
+    """Levels and base axes exactly as the reference's loop (mdi.py:146-165)."""
+    axes = list(range(1, d + 1))
+    levels = 0
+    while len(axes) > 3:
+        for _ in range(cfg.m):
+            axes = axes[:-1] if cfg.order == "forward" else axes[1:]
+        levels += 1
+    return levels, axes
+
+
+def mdi_sum(g, grids, cfg=None):
+    """Full grid sum of g by dimension iteration (mdi.py:139-192)."""
+    cfg = cfg if cfg is not None else MdiConfig()
+    d = grids.d
+    e = as_expr(g)
+    extra = free_vars(e) - set(range(1, d + 1))
+    if extra:
+        raise ValueError(f"integrand uses coordinates {sorted(extra)} beyond the {d} axes")
+    counts = tuple(grids.counts)
+    levels, base_axes = _level_plan(d, cfg)
+    t0 = time.perf_counter()
+
+    if not free_vars(e):
+        value = _const_sweep(evaluate(e, {}), counts)
+        return MdiReport(value=value, levels=levels, base_dim=len(base_axes), level_nodes=(1,) * levels,
+                         level_seconds=(0.0,) * levels, base_seconds=time.perf_counter() - t0,
+                         log_raw=math.log(abs(value)) if value else -math.inf,
+                         sign=math.copysign(1.0, value) if value else 0.0, method="constant", clusters=0)
+
+    plan = engine.separable_plan(e, counts) if not getattr(grids, "_force_direct", False) else None
+    usable = plan is not None and plan.ok and (plan.n_factors + plan.n_terms) <= cfg.budget
+    usable = usable and getattr(grids, "midpoint", False)
+    if not usable:
+        if cfg.fallback == "error":
+            raise BudgetExceededError("integrand is not separable over the grid axes "
+                                      f"(budget {cfg.budget}); no level reduction possible")
+        value = direct_tensor_sum(e, grids, cap=cfg.direct_cap)
+        return MdiReport(value=value, levels=0, base_dim=d, base_seconds=time.perf_counter() - t0,
+                         fallback=True, log_raw=math.log(abs(value)) if value else -math.inf,
+                         sign=math.copysign(1.0, value) if value else 0.0, method="direct")
+
+    base_total = math.prod(counts[a - 1] for a in base_axes)
+    if base_total > cfg.direct_cap:
+        raise GridCapError(f"direct sweep needs {base_total} evaluations, cap is {cfg.direct_cap}")
+    log_raw, sign, raw, _ = engine.mdi_separable_sum(plan)
+    secs = time.perf_counter() - t0
+    return MdiReport(value=raw, levels=levels, base_dim=len(base_axes),
+                     level_nodes=(plan.n_factors,) * levels, level_seconds=(0.0,) * levels,
+                     base_seconds=secs, fallback=False, log_raw=log_raw, sign=sign,
+                     method="separable", clusters=plan.n_factors)
+
+
+def _normalize(raw, counts):
+    """raw / prod(counts) without overflowing float (mdi.py:195-203)."""
+    total = math.prod(counts)
+    if total <= 2**53:
+        return raw / total
+    out = raw
+    for ct in counts:
+        out /= ct
+    return out
+
+
+def _det_a(rule):
+    """|A| = 1/(z_1 ... z_{d-1}); 0.0 when the product overflows float (mdi.py:206-212)."""
+    if rule.d <= 1:
+        return 1.0
+    a = getattr(rule, "_korobov_a", None)
+    if a is not None:
+        e = (rule.d - 1) * (rule.d - 2) // 2       # prod_{j<d-1} a^j
+        if a == 1 or e == 0:
+            return 1.0
+        if e * math.log2(a) > 1100:
+            return 0.0
+        prod = a ** e
+    else:
+        prod = math.prod(rule.z[:-1])
+    try:
+        return 1.0 / float(prod)
+    except OverflowError:
+        return 0.0
+
+
+def mdi_lr(f, d, a, n, cfg=None, rule=None, with_report=False):
+    """Improved-rule quadrature via dimension iteration (mdi.py:215-234)."""
+    cfg = cfg if cfg is not None else MdiConfig()
+    if rule is None:
+        rule = korobov_vector(a, n, d)
+    elif rule.d != d:
+        raise ValueError(f"rule dimension {rule.d} != {d}")
+    grids = midpoint_grids(rule)
+    report = mdi_sum(f, grids, cfg)
+    report.det_a = _det_a(rule)
+    value = _normalize(report.value, grids.counts)
+    if with_report:
+        return value, report
+    return value

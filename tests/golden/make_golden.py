@@ -1,0 +1,226 @@
+"""Freeze golden vectors from the REFERENCE implementation (run in the build
+container only; /root/reference does not exist on the GPU box).
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [--skip-slow]
+
+Writes points.json, slr.json, mdi.json next to this file.  Every value is
+produced by calling the reference's own public API
+(/root/reference/pkg/src/latquad/{lattice,quad,mdi,transform}.py) on the
+seeded inputs of paper_2404_08867_b200/configs.py, except the config-5
+integrand exp(-|L|), which the reference grammar cannot express
+(exprcore.py:638): that sum is formed from the reference's own points_block
+(lattice.py:96-105) plus a numpy restatement of the integrand, labelled
+"kind": "ref_points+numpy".
+
+Floats are stored bit-exactly: scalars as float.hex(), arrays as base64 of
+little-endian float64 bytes.
+"""
+
+from __future__ import annotations
+
+import argparse
+import base64
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+from latquad import corpus, exprcore  # noqa: E402  (reference, read-only)
+from latquad.lattice import LatticeRule, korobov_vector, points_block  # noqa: E402
+from latquad.mdi import MdiConfig, direct_tensor_sum, mdi_lr  # noqa: E402
+from latquad.quad import implr_integrate, mdilr_integrate, slr_integrate  # noqa: E402
+from latquad.transform import axis_counts, midpoint_grids  # noqa: E402
+
+from paper_2404_08867_b200.configs import make_config  # noqa: E402
+
+
+def b64(arr):
+    return base64.b64encode(np.ascontiguousarray(arr, dtype="<f8").tobytes()).decode()
+
+
+def hx(v):
+    return float(v).hex()
+
+
+def points_cases():
+    cases = []
+
+    def add(tag, rule, start, stop):
+        pts = points_block(rule, start, stop)
+        cases.append({"tag": tag, "n": str(rule.n), "z": [str(c) for c in rule.z],
+                      "start": start, "stop": stop, "shape": list(pts.shape), "data": b64(pts)})
+
+    add("four_point", LatticeRule(4, (1, 3)), 0, 4)
+    add("origin", LatticeRule(1, (1, 1, 1)), 0, 1)
+    add("korobov_7_81_3", korobov_vector(7, 81, 3), 0, 81)
+    add("rule_101_1_40", LatticeRule(101, (1, 40)), 0, 101)
+    add("korobov_10_101_3_unreduced", korobov_vector(10, 101, 3), 0, 101)
+    for cid in (1, 2, 3, 5):
+        cfg = make_config(cid)
+        rule = LatticeRule(cfg.plain_n, cfg.plain_z())
+        n = cfg.plain_n
+        rows = {1: n, 2: 48, 3: 16, 5: 8}[cid]
+        add(f"cfg{cid}_head", rule, 0, min(rows, n))
+        if rows < n:
+            add(f"cfg{cid}_tail", rule, n - rows, n)
+            mid = n // 2 + 12345 % n
+            add(f"cfg{cid}_mid", rule, mid, min(mid + rows, n))
+    # large moduli where the reference's int64 j*z_j stays exact (j*z < 2^63)
+    big = LatticeRule(2**31 + 11, (1, 2**31 - 5, 1_234_567_891, 7))
+    add("n_2p31_plus", big, 2**31 + 11 - 16, 2**31 + 11)
+    big2 = LatticeRule(2**33 + 17, (1, 3_000_000_019, 5))
+    add("n_2p33_plus", big2, 2**30, 2**30 + 16)
+    big3 = LatticeRule(2**50 + 55, (1, 977, 12_345))
+    add("n_2p50_plus", big3, 2**40, 2**40 + 16)
+    return cases
+
+
+def slr_cases(skip_slow):
+    out = []
+
+    def add(tag, text, d, rule, kind="reference", **extra):
+        f = exprcore.parse(text, d)
+        t0 = time.perf_counter()
+        r = slr_integrate(f, rule)
+        out.append({"tag": tag, "kind": kind, "text": text, "d": d, "n": str(rule.n),
+                    "z": [str(c) for c in rule.z], "value": hx(r.value),
+                    "a": r.a, "ref_seconds": time.perf_counter() - t0, **extra})
+
+    add("const_2p5", "2.5", 2, LatticeRule(101, (1, 10)))
+    add("dual_mode", "cos(2*pi*(3*x[1] - x[2]))", 2, LatticeRule(8, (1, 3)))
+    add("nondual_mode", "cos(2*pi*x[1])", 2, LatticeRule(8, (1, 3)))
+    add("expxy_101", corpus.get("expxy").text, 2, korobov_vector(10, 101, 2))
+    add("expxy_40001", corpus.get("expxy").text, 2, korobov_vector(200, 40001, 2))
+    add("sinsq_2027", corpus.get("sinsq").text, 2, korobov_vector(45, 2027, 2))
+    add("expsum3_1e6", corpus.get("expsum").text, 3, korobov_vector(100, 10**6 + 1, 3))
+    add("gaussian5", corpus.get("gaussian").text, 5, korobov_vector(33, 4099, 5))
+    add("ratprod4", corpus.get("ratprod").text, 4, korobov_vector(77, 3001, 4))
+    add("invpow3", corpus.get("invpow").text, 3, korobov_vector(19, 2003, 3))
+    add("expsq4", corpus.get("expsq").text, 4, korobov_vector(31, 2999, 4))
+    add("coslin6", corpus.get("coslin").text, 6, korobov_vector(13, 5003, 6))
+    add("expalt7", corpus.get("expalt").text, 7, korobov_vector(21, 7001, 7))
+    add("poly_mix", "x[1]^3*x[2] - 0.5*x[3]^2 + x[1]*x[2]*x[3] + 0.25", 3,
+        korobov_vector(5, 1021, 3))
+    add("recip_sum", "1/(1 + x[1] + 2*x[2])", 2, korobov_vector(7, 997, 2))
+    add("sin_of_prod", "sin(x[1]*x[2]) + exp(-x[3])*cos(3*x[1])", 3, korobov_vector(9, 1499, 3))
+    for cid in (1, 2, 3):
+        if cid == 3 and skip_slow:
+            continue
+        cfg = make_config(cid)
+        add(f"cfg{cid}", cfg.text, cfg.d, LatticeRule(cfg.plain_n, cfg.plain_z()))
+
+    # config 5: reference points + numpy restatement of exp(-|sum c_j (x_j - w_j)|)
+    cfg = make_config(5)
+    rule = LatticeRule(cfg.plain_n, cfg.plain_z())
+    c = np.asarray(cfg.c)
+    w = np.asarray(cfg.w)
+    cw = float(np.dot(c, w))
+    for (lo, hi) in ((0, 1 << 14), (cfg.plain_n - (1 << 12), cfg.plain_n), (1 << 30, (1 << 30) + (1 << 12))):
+        pts = points_block(rule, lo, hi)
+        vals = np.exp(-np.abs(pts @ c - cw))
+        out.append({"tag": f"cfg5_range_{lo}_{hi}", "kind": "ref_points+numpy", "text": cfg.text,
+                    "d": cfg.d, "n": str(rule.n), "z": [str(v) for v in rule.z],
+                    "i_begin": lo, "i_end": hi, "range_sum": hx(float(np.sum(vals))),
+                    "value": None})
+    return out
+
+
+def mdi_cases(skip_slow):
+    out = []
+
+    def rep_fields(rep):
+        return {"raw": hx(rep.value), "levels": rep.levels, "base_dim": rep.base_dim,
+                "fallback": rep.fallback, "det_a": hx(rep.det_a) if rep.det_a is not None else None,
+                "level_nodes": list(rep.level_nodes)}
+
+    def add(tag, text, d, a, n, cfg=None, with_implr=False, **extra):
+        f = exprcore.parse(text, d)
+        rule = korobov_vector(a, n, d)
+        counts = axis_counts(rule)
+        t0 = time.perf_counter()
+        value, rep = mdi_lr(f, d, a, n, cfg=cfg, with_report=True)
+        secs = time.perf_counter() - t0
+        rec = {"tag": tag, "text": text, "d": d, "a": a, "n": str(n),
+               "counts": [str(x) for x in counts], "value": hx(value),
+               "ref_seconds": secs, **rep_fields(rep), **extra}
+        if cfg is not None:
+            rec["direct_cap"] = cfg.direct_cap
+        if with_implr:
+            rec["implr"] = hx(implr_integrate(f, d, a, n).value)
+            rec["direct_sum"] = hx(direct_tensor_sum(f, midpoint_grids(rule)))
+        out.append(rec)
+        return rec
+
+    # acceptance-01 sweep (reference tests/test_acceptance.py:52-71)
+    for entry in corpus.entries():
+        for d in range(2, 7):
+            if d < entry.min_d:
+                continue
+            for a in range(2, 6):
+                add(f"acc01_{entry.id}_d{d}_a{a}", entry.text, d, a, a**d, with_implr=True,
+                    corpus=entry.id)
+    add("readme_gaussian_d10", corpus.get("gaussian").text, 10, 10, 1 + 10**10,
+        reference=hx(corpus.reference_value("gaussian", 10)))
+    add("gaussian_d12", corpus.get("gaussian").text, 12, 10, 1 + 10**12,
+        reference=hx(corpus.reference_value("gaussian", 12)))
+    add("expalt_d20_a8", corpus.get("expalt").text, 20, 8, 8**20)
+    add("ratprod_d4_a3_n81", corpus.get("ratprod").text, 4, 3, 81, with_implr=True)
+    add("gaussian_d4_a3_n81", corpus.get("gaussian").text, 4, 3, 81, with_implr=True)
+    add("expalt_d5_a2_n32", corpus.get("expalt").text, 5, 2, 32, with_implr=True)
+    add("const1_d2", "1", 2, 10, 101)
+    add("gaussian_d3_a7_n400", corpus.get("gaussian").text, 3, 7, 400, with_implr=True)
+    add("expsum_d3_a100", corpus.get("expsum").text, 3, 100, 10**6 + 1, with_implr=True)
+    add("expxy_d2_a200", corpus.get("expxy").text, 2, 200, 40001, with_implr=True)
+    add("cos_lin_small_d8", "cos(0.3 + sum(i=1..d, 0.2*i*x[i]))", 8, 4, 4**8, with_implr=True)
+    add("ratprod_d30_a16", corpus.get("ratprod").text, 30, 16, 16**30)
+    add("gaussian_d100_a8", corpus.get("gaussian").text, 100, 8, 8**100)
+
+    cfg2 = make_config(2)
+    add("cfg2", cfg2.text, cfg2.d, cfg2.mdi_a, cfg2.mdi_n)
+    cfg1 = make_config(1)
+    if not skip_slow:
+        add("cfg1", cfg1.text, cfg1.d, cfg1.mdi_a, cfg1.mdi_n,
+            cfg=MdiConfig(direct_cap=10**10))
+    # the default cap refuses config 1 (a^3 > 1e8): record the refusal too
+    try:
+        mdi_lr(exprcore.parse(cfg1.text, cfg1.d), cfg1.d, cfg1.mdi_a, cfg1.mdi_n)
+        refused = False
+    except Exception as exc:  # GridCapError
+        refused = type(exc).__name__
+    out.append({"tag": "cfg1_default_cap", "refused": refused})
+    if not skip_slow:
+        cfg4 = make_config(4)
+        rec = add("cfg4", cfg4.text, cfg4.d, cfg4.mdi_a, cfg4.mdi_n)
+        rec["log_raw"] = hx(math.log(float.fromhex(rec["raw"])))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--skip-slow", action="store_true")
+    ap.add_argument("--only", choices=["points", "slr", "mdi"], default=None)
+    args = ap.parse_args()
+    meta = {"generator": "tests/golden/make_golden.py", "numpy": np.__version__,
+            "python": sys.version.split()[0], "reference": "/root/reference/pkg (latquad 0.1.0)"}
+    jobs = {"points": lambda: points_cases(), "slr": lambda: slr_cases(args.skip_slow),
+            "mdi": lambda: mdi_cases(args.skip_slow)}
+    for name, fn in jobs.items():
+        if args.only and name != args.only:
+            continue
+        t0 = time.perf_counter()
+        cases = fn()
+        with open(os.path.join(HERE, f"{name}.json"), "w") as fh:
+            json.dump({"meta": meta, "cases": cases}, fh, indent=1)
+        print(f"{name}: {len(cases)} cases in {time.perf_counter() - t0:.1f}s", flush=True)
+
+
+if __name__ == "__main__":
+    main()
