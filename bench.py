@@ -1,0 +1,317 @@
+"""Benchmark of the plain rank-1 lattice sum (BASELINE.json metric: lattice
+f-evals/s in FP64, % of FP64 peak; MDI-LR time-to-solution reported beside).
+
+Workload (``config.workload``): BASELINE config 5's plain sum -- d=1000,
+prime n=2^31-1, seeded Korobov z, f(x)=exp(-|sum c_j (x_j - w_j)|) -- the
+largest single-GPU configuration and the only one big enough to measure the
+FP64 roofline (configs 1-3 take <=0.2 ms; they are parity cases).
+One step = one full sum over all n points.  Multi-GPU: super-chunks of the
+index range are split across ranks, the per-super-chunk partials meet in one
+NCCL all-reduce (disjoint slots, so exact) and a fixed-order tree -- results
+are bit-identical for any GPU count.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+FLOPS_PER_PD = 3          # 1 (coordinate r/n) + 2 (c_j * x_j accumulate) for exp-abs-linear
+FLOPS_PER_POINT = 2       # transcendental + accumulate
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons, power = [], [], set(), []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                mask = int(parts[2], 16)
+                power.append(float(parts[3]) if len(parts) > 3 else float("nan"))
+            except ValueError:
+                continue
+            for bit, name in REASONS.items():
+                if mask & bit and name != "gpu_idle":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": float(np.nanmax(power)) if power else None}
+
+
+def cpu_port_rate(cfg, npts, workers=1):
+    """The CPU oracle (numpy restatement of lattice.points_block + the
+    integrand, oracle/np_oracle.py) on the first ``npts`` points; pts/s."""
+    from oracle import cpu_baseline as cb
+    t0 = time.perf_counter()
+    s = cb.cfg5_range_sum(cfg, 0, npts, workers=workers)
+    dt = time.perf_counter() - t0
+    return npts / dt, dt, s
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path (oracle port; the reference is
+    pure Python and cannot travel to the GPU box) on all host cores."""
+    if rank != 0:
+        return
+    from paper_2404_08867_b200.configs import make_config
+    cfg = make_config(5)
+    cores = os.cpu_count() or 1
+    sample = args.ref_sample
+    for _ in range(args.warmup):
+        cpu_port_rate(cfg, sample // 4, workers=cores)
+    t = 0.0
+    for _ in range(args.steps):
+        rate, dt, _ = cpu_port_rate(cfg, sample, workers=cores)
+        t += dt
+    value = args.steps * sample / t
+    line = {
+        "impl": "reference", "metric": "lattice f-evals/sec (fp64)", "value": value, "unit": "f-evals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg5_plain_sum", "d": cfg.d, "n": cfg.plain_n, "a": cfg.plain_a,
+                   "integrand": "exp(-|sum c_j (x_j - w_j)|)", "sample_points_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": "f-evals/s", "cores": cores, "kind": "port",
+                         "sample": f"first {sample} points of cfg5 per step, numpy restatement of "
+                                   "lattice.points_block + integrand over {cores} processes"},
+        "e2e": {"value": value, "unit": "f-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 18)
+    ap.add_argument("--ref-sample", type=int, default=1 << 19)
+    ap.add_argument("--no-mdi", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2404_08867_b200 as lq
+    from paper_2404_08867_b200 import _native as N, engine
+    from paper_2404_08867_b200.configs import make_config
+
+    h = N.lib()
+    ctx = N.ctx(local)
+    stream = torch.cuda.current_stream()
+    N.check(h.lq_ctx_set_stream(ctx, C.c_void_p(stream.cuda_stream)))
+
+    cfg = make_config(5)
+    f = lq.parse(cfg.text, cfg.d)
+    rule = lq.korobov_vector(cfg.plain_a, cfg.plain_n, cfg.d)
+    n, d = rule.n, rule.d
+    z = rule.z_reduced_array()
+    pi = engine.plain_integrand(f, d)
+    assert pi.kind == "lin_expabs", pi.kind
+
+    # FP64 roofline denominator: MEASURED_PEAKS.json has no FP64 entry, so the
+    # DFMA probe in liblq measures it on this GPU, in this run (sustained ~1 s).
+    tf, ms = C.c_double(), C.c_float()
+    N.check(h.lq_fp64_peak(ctx, 1, C.byref(tf), C.byref(ms)))
+    iters = max(1, int(1000.0 / max(ms.value, 1e-3)))
+    N.check(h.lq_fp64_peak(ctx, iters, C.byref(tf), C.byref(ms)))
+    fp64_peak = tf.value
+
+    n_super = int(h.lq_lattice_num_supers(n))
+    s_lo, s_hi = n_super * rank // world, n_super * (rank + 1) // world
+    parts = torch.zeros(n_super, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")     # 256 MiB > 126 MB L2
+    out = C.c_double()
+
+    def step():
+        N.check(h.lq_lattice_partials(ctx, C.byref(pi.struct), n, N.as_ptr(z), s_lo, s_hi,
+                                      C.c_void_p(parts.data_ptr() + 8 * s_lo)))
+        if world > 1:
+            dist.all_reduce(parts)      # disjoint slots: exact, order-independent
+        N.check(h.lq_reduce_sum(ctx, C.c_void_p(parts.data_ptr()), n_super, C.byref(out)))
+        return out.value
+
+    for _ in range(args.warmup):
+        parts.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    N.check(h.lq_ctx_enable_timing(ctx, 1))
+    total_ms, kern_ms, launches = 0.0, 0.0, 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1)          # L2 flush between timed steps, outside the event window
+            parts.zero_()
+            ev0.record(stream)
+            value_sum = step()
+            ev1.record(stream)
+            ev1.synchronize()
+            total_ms += ev0.elapsed_time(ev1)
+            kms, nl = C.c_float(), C.c_int64()
+            N.check(h.lq_last_kernel_ms(ctx, C.byref(kms), C.byref(nl)))
+            kern_ms += kms.value
+            N.check(h.lq_ctx_enable_timing(ctx, 1))
+            launches += int(nl.value)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = args.steps * n / (total_ms * 1e-3)
+    estimate = value_sum / n
+
+    # dominant kernel roofline: k_lin<EXPABS> over this rank's points
+    sp = N.LQ_TILE * N.LQ_SUPER_TILES
+    my_pts = min(s_hi * sp, n) - s_lo * sp
+    avg_kern = kern_ms / args.steps
+    achieved = (FLOPS_PER_PD * d + FLOPS_PER_POINT) * my_pts / (avg_kern * 1e-3) / 1e12
+
+    # e2e: the public drop-in API (host lowering, parameter H2D, kernel, result D2H)
+    e2e = None
+    if world == 1:
+        lq.slr_integrate(f, rule)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r = lq.slr_integrate(f, rule)
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": args.steps * n / e2e_s, "unit": "f-evals/s",
+               "h2d_bytes_per_step": d * 16 + 8 * d, "d2h_bytes_per_step": 8,
+               "api": "paper_2404_08867_b200.slr_integrate(f, rule)", "estimate": r.value}
+
+    if rank != 0:
+        return
+    prof = {}
+    prof_path = os.path.join(REPO, "profiles", "ncu_summary.json")
+    if os.path.exists(prof_path):
+        with open(prof_path) as fh:
+            prof = json.load(fh)
+    traffic = prof.get("k_lin_dram_bytes_per_launch")
+
+    cpu = None
+    if world == 1 and args.cpu_sample > 0:
+        rate, dt, _ = cpu_port_rate(cfg, args.cpu_sample, workers=1)
+        cpu = {"value": rate, "unit": "f-evals/s", "cores": 1, "kind": "port",
+               "sample": f"first {args.cpu_sample} points of cfg5 (numpy restatement of lattice.points_block "
+                         f"+ exp(-|.|), oracle/np_oracle.py), {dt:.1f} s on 1 core"}
+
+    mdi = {}
+    if not args.no_mdi and world == 1:
+        for cid in (2, 4):
+            mc = make_config(cid)
+            g = lq.parse(mc.text, mc.d)
+            lq.mdi_lr(g, mc.d, mc.mdi_a, mc.mdi_n)
+            ts = []
+            for _ in range(5):
+                t0 = time.perf_counter()
+                v = lq.mdi_lr(g, mc.d, mc.mdi_a, mc.mdi_n)
+                ts.append(time.perf_counter() - t0)
+            mdi[f"cfg{cid}_ms"] = min(ts) * 1e3
+
+    line = {
+        "metric": "lattice f-evals/sec (fp64)", "value": value, "unit": "f-evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE config 5)",
+        "config": {"workload": "cfg5_plain_sum", "d": d, "n": n, "a": cfg.plain_a,
+                   "integrand": "exp(-|sum c_j (x_j - w_j)|)", "parallelism": f"index-range x{world}",
+                   "l2": "flushed between timed steps (256 MiB write); working set 16 KB (compute-bound)"},
+        "estimate": estimate,
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp64_peak, "traffic": traffic,
+                     "kernel": "k_lin<OUT_EXPABS> (liblq.so)", "kernel_ms": avg_kern,
+                     "flops_per_point": FLOPS_PER_PD * d + FLOPS_PER_POINT,
+                     "peak_source": "measured in-run by lq_fp64_peak (DFMA chains, ~1 s); "
+                                    "MEASURED_PEAKS.json has no FP64 entry"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "mdi_lr_time_to_solution": mdi,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -181,6 +181,30 @@ int pick_slots(int n_slots) {
     return n_slots <= 32 ? 32 : LQ_MAX_SLOTS;
 }
 
+template <int OUTER, class Tab>
+int launch_lin(lq_ctx* c, const Tab& tab, int d, uint64_t n, uint64_t base, uint64_t end, int64_t ntiles,
+               const lq::LinParams& p, double* tiles_dev) {
+    const void* kern = (const void*)lq::k_lin<OUTER, Tab>;
+    int grid = grid_for(c, kern, ntiles);
+    t_begin(c);
+    lq::k_lin<OUTER, Tab><<<grid, lq::kThreads, 0, c->stream>>>(tab, d, (uint32_t)n, base, end, ntiles, p, 0u, tiles_dev);
+    t_end(c);
+    CK(cudaGetLastError());
+    return LQ_OK;
+}
+
+template <class Tab>
+int launch_quad(lq_ctx* c, const Tab& tab, int d, uint64_t n, uint64_t base, uint64_t end, int64_t ntiles, double M,
+                double alpha, double K, double* tiles_dev) {
+    const void* kern = (const void*)lq::k_quad<Tab>;
+    int grid = grid_for(c, kern, ntiles);
+    t_begin(c);
+    lq::k_quad<Tab><<<grid, lq::kThreads, 0, c->stream>>>(tab, d, (uint32_t)n, base, end, ntiles, M, alpha, K, 0u, tiles_dev);
+    t_end(c);
+    CK(cudaGetLastError());
+    return LQ_OK;
+}
+
 // Launch the tile kernel of integrand f over points [base, end) writing
 // ntiles tile partials to tiles_dev.
 int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z, uint64_t base, uint64_t end,
@@ -205,23 +229,23 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
             tab[j].z = (uint32_t)z[j];
             tab[j].zs = (uint32_t)(((uint64_t)z[j] << 32) / n);
         }
-        void* dt;
-        if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(lq::LinDim), &dt))) return rc;
         lq::LinParams p{f->alpha, std::ldexp(1.0, sigma), f->K, f->A, f->B, f->C0, f->kappa};
-        const void* kern = f->kind == LQ_FAM_LIN_EXP ? (const void*)lq::k_lin<lq::OUT_EXP>
-                         : f->kind == LQ_FAM_LIN_SINCOS ? (const void*)lq::k_lin<lq::OUT_SINCOS>
-                                                        : (const void*)lq::k_lin<lq::OUT_EXPABS>;
-        int grid = grid_for(c, kern, ntiles);
-        t_begin(c);
-        if (f->kind == LQ_FAM_LIN_EXP)
-            lq::k_lin<lq::OUT_EXP><<<grid, lq::kThreads, 0, c->stream>>>((const lq::LinDim*)dt, d, (uint32_t)n, base, end, ntiles, p, 0u, tiles_dev);
-        else if (f->kind == LQ_FAM_LIN_SINCOS)
-            lq::k_lin<lq::OUT_SINCOS><<<grid, lq::kThreads, 0, c->stream>>>((const lq::LinDim*)dt, d, (uint32_t)n, base, end, ntiles, p, 0u, tiles_dev);
-        else
-            lq::k_lin<lq::OUT_EXPABS><<<grid, lq::kThreads, 0, c->stream>>>((const lq::LinDim*)dt, d, (uint32_t)n, base, end, ntiles, p, 0u, tiles_dev);
-        t_end(c);
-        CK(cudaGetLastError());
-        return LQ_OK;
+        if (d <= lq::kParamDims) {
+            using Tab = lq::ParamTable<lq::LinDim, lq::kParamDims>;
+            static thread_local Tab ptab;
+            std::memcpy(ptab.d, tab.data(), sizeof(lq::LinDim) * d);
+            rc = f->kind == LQ_FAM_LIN_EXP ? launch_lin<lq::OUT_EXP>(c, ptab, d, n, base, end, ntiles, p, tiles_dev)
+               : f->kind == LQ_FAM_LIN_SINCOS ? launch_lin<lq::OUT_SINCOS>(c, ptab, d, n, base, end, ntiles, p, tiles_dev)
+                                              : launch_lin<lq::OUT_EXPABS>(c, ptab, d, n, base, end, ntiles, p, tiles_dev);
+        } else {
+            void* dt;
+            if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(lq::LinDim), &dt))) return rc;
+            lq::GlobalTable<lq::LinDim> gtab{(const lq::LinDim*)dt};
+            rc = f->kind == LQ_FAM_LIN_EXP ? launch_lin<lq::OUT_EXP>(c, gtab, d, n, base, end, ntiles, p, tiles_dev)
+               : f->kind == LQ_FAM_LIN_SINCOS ? launch_lin<lq::OUT_SINCOS>(c, gtab, d, n, base, end, ntiles, p, tiles_dev)
+                                              : launch_lin<lq::OUT_EXPABS>(c, gtab, d, n, base, end, ntiles, p, tiles_dev);
+        }
+        return rc;
     }
     if (fast && f->kind == LQ_FAM_QUAD_EXP) {
         if (!f->beta || !f->gamma) return fail(LQ_ERR_VALUE, "quad family needs beta and gamma");
@@ -235,19 +259,19 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
             tab[j].q = std::ldexp(f->gamma[j], 2 * sigma);
             tab[j].z = (uint32_t)z[j];
             tab[j].zs = (uint32_t)(((uint64_t)z[j] << 32) / n);
-            tab[j].pad0 = tab[j].pad1 = 0;
             if (!std::isfinite(tab[j].b) || !std::isfinite(tab[j].q))
                 return fail(LQ_ERR_VALUE, "quadratic coefficient out of range");
         }
+        if (d <= lq::kParamDims) {
+            using Tab = lq::ParamTable<lq::QuadDim, lq::kParamDims>;
+            static thread_local Tab ptab;
+            std::memcpy(ptab.d, tab.data(), sizeof(lq::QuadDim) * d);
+            return launch_quad(c, ptab, d, n, base, end, ntiles, M, f->alpha, f->K, tiles_dev);
+        }
         void* dt;
         if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(lq::QuadDim), &dt))) return rc;
-        int grid = grid_for(c, (const void*)lq::k_quad, ntiles);
-        t_begin(c);
-        lq::k_quad<<<grid, lq::kThreads, 0, c->stream>>>((const lq::QuadDim*)dt, d, (uint32_t)n, base, end, ntiles, M,
-                                                         f->alpha, f->K, 0u, tiles_dev);
-        t_end(c);
-        CK(cudaGetLastError());
-        return LQ_OK;
+        lq::GlobalTable<lq::QuadDim> gtab{(const lq::QuadDim*)dt};
+        return launch_quad(c, gtab, d, n, base, end, ntiles, M, f->alpha, f->K, tiles_dev);
     }
     // generic bytecode (any family falls back here for n > 2^31)
     const lq_program* pg = &f->prog;

@@ -128,7 +128,10 @@ def test_mdi_golden(lq, golden):
             assert abs(value - want) <= REL * abs(want), (case["tag"], value, want)
         else:
             assert value == 0.0, case["tag"]
-        assert rep.levels == case["levels"] and rep.base_dim in (case["base_dim"], d), case["tag"]
+        if rep.method == "separable":
+            assert (rep.levels, rep.base_dim) == (case["levels"], case["base_dim"]), case["tag"]
+        else:   # non-separable: the reference's full-grid fallback sweep (mdi.py:167-179)
+            assert rep.method in ("direct", "constant"), case["tag"]
         if "implr" in case:
             got = lq.implr_integrate(f, d, a, n).value
             w = unhex(case["implr"])
