@@ -181,28 +181,48 @@ int pick_slots(int n_slots) {
     return n_slots <= 32 ? 32 : LQ_MAX_SLOTS;
 }
 
-template <int OUTER, class Tab>
-int launch_lin(lq_ctx* c, const Tab& tab, int d, uint64_t n, uint64_t base, uint64_t end, int64_t ntiles,
-               const lq::LinParams& p, double* tiles_dev) {
-    const void* kern = (const void*)lq::k_lin<OUTER, Tab>;
-    int grid = grid_for(c, kern, ntiles);
+template <int OUTER, class Args>
+int launch_lin(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev) {
     t_begin(c);
-    lq::k_lin<OUTER, Tab><<<grid, lq::kThreads, 0, c->stream>>>(tab, d, (uint32_t)n, base, end, ntiles, p, 0u, tiles_dev);
+    lq::k_lin<OUTER, Args><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, 0u, tiles_dev);
     t_end(c);
     CK(cudaGetLastError());
     return LQ_OK;
 }
 
-template <class Tab>
-int launch_quad(lq_ctx* c, const Tab& tab, int d, uint64_t n, uint64_t base, uint64_t end, int64_t ntiles, double M,
-                double alpha, double K, double* tiles_dev) {
-    const void* kern = (const void*)lq::k_quad<Tab>;
-    int grid = grid_for(c, kern, ntiles);
+template <class Args>
+int launch_quad(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev) {
     t_begin(c);
-    lq::k_quad<Tab><<<grid, lq::kThreads, 0, c->stream>>>(tab, d, (uint32_t)n, base, end, ntiles, M, alpha, K, 0u, tiles_dev);
+    lq::k_quad<Args><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, 0u, tiles_dev);
     t_end(c);
     CK(cudaGetLastError());
     return LQ_OK;
+}
+
+template <class A>
+void fill_head(A& a, int d, uint64_t n, uint64_t base, uint64_t end, double alpha, double scale, double K, double A_,
+               double B, double C0, double kappa, double M) {
+    a.d = d; a.n = (uint32_t)n; a.base = base; a.end = end;
+    a.alpha = alpha; a.scale = scale; a.K = K; a.A = A_; a.B = B; a.C0 = C0; a.kappa = kappa; a.M = M;
+}
+
+template <int OUTER>
+int lin_dispatch(lq_ctx* c, const std::vector<lq::LinDim>& tab, int d, uint64_t n, uint64_t base, uint64_t end,
+                 int64_t ntiles, const lq_integrand* f, double scale, double* tiles_dev) {
+    if (d <= lq::kParamDims) {
+        using Args = lq::FamArgs<lq::LinDim, lq::kParamDims>;
+        static thread_local Args args;
+        fill_head(args, d, n, base, end, f->alpha, scale, f->K, f->A, f->B, f->C0, f->kappa, 0.0);
+        std::memcpy(args.dims, tab.data(), sizeof(lq::LinDim) * d);
+        return launch_lin<OUTER>(c, args, ntiles, tiles_dev);
+    }
+    void* dt;
+    int rc;
+    if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(lq::LinDim), &dt))) return rc;
+    lq::FamArgsG<lq::LinDim> args;
+    fill_head(args, d, n, base, end, f->alpha, scale, f->K, f->A, f->B, f->C0, f->kappa, 0.0);
+    args.dims = (const lq::LinDim*)dt;
+    return launch_lin<OUTER>(c, args, ntiles, tiles_dev);
 }
 
 // Launch the tile kernel of integrand f over points [base, end) writing
@@ -229,23 +249,10 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
             tab[j].z = (uint32_t)z[j];
             tab[j].zs = (uint32_t)(((uint64_t)z[j] << 32) / n);
         }
-        lq::LinParams p{f->alpha, std::ldexp(1.0, sigma), f->K, f->A, f->B, f->C0, f->kappa};
-        if (d <= lq::kParamDims) {
-            using Tab = lq::ParamTable<lq::LinDim, lq::kParamDims>;
-            static thread_local Tab ptab;
-            std::memcpy(ptab.d, tab.data(), sizeof(lq::LinDim) * d);
-            rc = f->kind == LQ_FAM_LIN_EXP ? launch_lin<lq::OUT_EXP>(c, ptab, d, n, base, end, ntiles, p, tiles_dev)
-               : f->kind == LQ_FAM_LIN_SINCOS ? launch_lin<lq::OUT_SINCOS>(c, ptab, d, n, base, end, ntiles, p, tiles_dev)
-                                              : launch_lin<lq::OUT_EXPABS>(c, ptab, d, n, base, end, ntiles, p, tiles_dev);
-        } else {
-            void* dt;
-            if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(lq::LinDim), &dt))) return rc;
-            lq::GlobalTable<lq::LinDim> gtab{(const lq::LinDim*)dt};
-            rc = f->kind == LQ_FAM_LIN_EXP ? launch_lin<lq::OUT_EXP>(c, gtab, d, n, base, end, ntiles, p, tiles_dev)
-               : f->kind == LQ_FAM_LIN_SINCOS ? launch_lin<lq::OUT_SINCOS>(c, gtab, d, n, base, end, ntiles, p, tiles_dev)
-                                              : launch_lin<lq::OUT_EXPABS>(c, gtab, d, n, base, end, ntiles, p, tiles_dev);
-        }
-        return rc;
+        const double scale = std::ldexp(1.0, sigma);
+        if (f->kind == LQ_FAM_LIN_EXP) return lin_dispatch<lq::OUT_EXP>(c, tab, d, n, base, end, ntiles, f, scale, tiles_dev);
+        if (f->kind == LQ_FAM_LIN_SINCOS) return lin_dispatch<lq::OUT_SINCOS>(c, tab, d, n, base, end, ntiles, f, scale, tiles_dev);
+        return lin_dispatch<lq::OUT_EXPABS>(c, tab, d, n, base, end, ntiles, f, scale, tiles_dev);
     }
     if (fast && f->kind == LQ_FAM_QUAD_EXP) {
         if (!f->beta || !f->gamma) return fail(LQ_ERR_VALUE, "quad family needs beta and gamma");
@@ -263,15 +270,18 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
                 return fail(LQ_ERR_VALUE, "quadratic coefficient out of range");
         }
         if (d <= lq::kParamDims) {
-            using Tab = lq::ParamTable<lq::QuadDim, lq::kParamDims>;
-            static thread_local Tab ptab;
-            std::memcpy(ptab.d, tab.data(), sizeof(lq::QuadDim) * d);
-            return launch_quad(c, ptab, d, n, base, end, ntiles, M, f->alpha, f->K, tiles_dev);
+            using Args = lq::FamArgs<lq::QuadDim, lq::kParamDims>;
+            static thread_local Args args;
+            fill_head(args, d, n, base, end, f->alpha, 1.0, f->K, 0, 0, 0, 0, M);
+            std::memcpy(args.dims, tab.data(), sizeof(lq::QuadDim) * d);
+            return launch_quad(c, args, ntiles, tiles_dev);
         }
         void* dt;
         if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(lq::QuadDim), &dt))) return rc;
-        lq::GlobalTable<lq::QuadDim> gtab{(const lq::QuadDim*)dt};
-        return launch_quad(c, gtab, d, n, base, end, ntiles, M, f->alpha, f->K, tiles_dev);
+        lq::FamArgsG<lq::QuadDim> args;
+        fill_head(args, d, n, base, end, f->alpha, 1.0, f->K, 0, 0, 0, 0, M);
+        args.dims = (const lq::QuadDim*)dt;
+        return launch_quad(c, args, ntiles, tiles_dev);
     }
     // generic bytecode (any family falls back here for n > 2^31)
     const lq_program* pg = &f->prog;

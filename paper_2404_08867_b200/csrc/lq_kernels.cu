@@ -60,100 +60,111 @@ __device__ __noinline__ double quad_outer(double acc, double alpha, double K) { 
 // (LDCU), which frees the vector register file ports for the residue chain
 // (measured +30% over LDG-fed operands).
 constexpr int kParamDims = 1024;
-template <class T, int N>
-struct ParamTable {
-    T d[N];
+
+// Kernel arguments: everything the j-loop reads is warp-uniform and lives in
+// kernel parameter space, so ptxas keeps the loop counter and per-dimension
+// constants in uniform registers (LDCU + UR operands).
+template <class Dim, int N>
+struct FamArgs {
+    int d;
+    uint32_t n;
+    uint64_t base, end;
+    double alpha, scale, K, A, B, C0, kappa, M;
+    Dim dims[N];
 };
 
-template <class T>
-struct GlobalTable {
-    const T* __restrict__ d;
+template <class Dim>
+struct FamArgsG {   // d > kParamDims: per-dimension records in global memory
+    int d;
+    uint32_t n;
+    uint64_t base, end;
+    double alpha, scale, K, A, B, C0, kappa, M;
+    const Dim* __restrict__ dims;
 };
 
 // Plain lattice sum of f = outer(alpha + <beta, x>), n <= 2^31.
-// Tile = 256 threads x 16 consecutive points.  Dimension-outer loop: per
-// (thread, j) one Shoup modmul gives the first residue, then each of the 16
-// points costs VIADD + VIADDMNMX (next residue) + one DFMA with the residue
-// read as a denormal -- x_j/n folded into the coefficient, no conversion, no
-// division.  tile_out[t] = sum over tile t (fixed tree).
-template <int OUTER, class Tab>
-__global__ void __launch_bounds__(kThreads, 2) k_lin(const __grid_constant__ Tab dims, int d, uint32_t n,
-                                                      uint64_t base, uint64_t end, int64_t ntiles,
-                                                      LinParams prm, uint32_t hmask,
+// One CTA per tile of 256 threads x 16 consecutive points.  Dimension-outer
+// loop: per (thread, j) one Shoup modmul gives the first residue, then each of
+// the 16 points costs VIADD + VIADDMNMX (next residue) + one DFMA with the
+// residue read as a denormal -- x_j/n folded into the coefficient, no
+// conversion, no division.  tile_out[t] = sum over tile t
+// (fixed tree).
+template <int OUTER, class Args>
+__global__ void __launch_bounds__(kThreads, 2) k_lin(const __grid_constant__ Args a, uint32_t hmask,
                                                       double* __restrict__ tile_out) {
     __shared__ double sh[8];
     uint32_t H[kPts];
     #pragma unroll
     for (int k = 0; k < kPts; ++k) H[k] = (threadIdx.x + k) & hmask;   // opaque zeros
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t i0_64 = base + (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kPts;
-        const uint32_t i0 = (uint32_t)i0_64;   // < 2^32 (n <= 2^31)
-        double acc[kPts];
-        #pragma unroll
-        for (int p = 0; p < kPts; ++p) acc[p] = 0.0;
-        #pragma unroll 1
-        for (int j = 0; j < d; ++j) {
-            const double c = dims.d[j].c;
-            const uint32_t z = dims.d[j].z;
-            const uint32_t zm = z - n;
-            uint32_t r = mulmod_shoup(i0, z, dims.d[j].zs, n);
-            #pragma unroll
-            for (int p = 0; p < kPts; ++p) {
-                acc[p] = fma(c, denorm_of(r, H[p]), acc[p]);
-                r = step_mod(r, z, zm);
-            }
-        }
-        double s = 0.0;
+    const int64_t tile = blockIdx.x;
+    const uint64_t i0_64 = a.base + (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kPts;
+    const uint32_t i0 = (uint32_t)i0_64;   // < 2^32 (n <= 2^31)
+    const uint32_t n = a.n;
+    double acc[kPts];
+    #pragma unroll
+    for (int p = 0; p < kPts; ++p) acc[p] = 0.0;
+    #pragma unroll 1
+    for (int j = 0; j < a.d; ++j) {
+        const double c = a.dims[j].c;
+        const uint32_t z = a.dims[j].z;
+        const uint32_t zm = z - n;
+        uint32_t r = mulmod_shoup(i0, z, a.dims[j].zs, n);
         #pragma unroll
         for (int p = 0; p < kPts; ++p) {
-            double f = outer_fn<OUTER>(acc[p], prm);
-            s += (i0_64 + p < end) ? f : 0.0;
+            acc[p] = fma(c, denorm_of(r, H[p]), acc[p]);
+            r = step_mod(r, z, zm);
         }
-        s = block_sum(s, sh);
-        if (threadIdx.x == 0) tile_out[tile] = s;
     }
+    const LinParams prm{a.alpha, a.scale, a.K, a.A, a.B, a.C0, a.kappa};
+    double s = 0.0;
+    #pragma unroll
+    for (int p = 0; p < kPts; ++p) {
+        double f = outer_fn<OUTER>(acc[p], prm);
+        s += (i0_64 + p < a.end) ? f : 0.0;
+    }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) tile_out[tile] = s;
 }
 
 // Plain lattice sum of f = K exp(alpha + sum_j b_j x_j + q_j x_j^2), n <= 2^31.
 // Per point-dim: residue step (2 int ops), xs = denormal * M (exact scale),
 // t = q xs + b, acc += t xs: 3 FP64 ops (FP64-pipe bound).
-template <class Tab>
-__global__ void __launch_bounds__(kThreads, 2) k_quad(const __grid_constant__ Tab dims, int d, uint32_t n,
-                                                       uint64_t base, uint64_t end, int64_t ntiles,
-                                                       double M, double alpha, double K, uint32_t hmask,
+template <class Args>
+__global__ void __launch_bounds__(kThreads, 2) k_quad(const __grid_constant__ Args a, uint32_t hmask,
                                                        double* __restrict__ tile_out) {
     __shared__ double sh[8];
     uint32_t H[kPts];
     #pragma unroll
     for (int k = 0; k < kPts; ++k) H[k] = (threadIdx.x + k) & hmask;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t i0_64 = base + (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kPts;
-        const uint32_t i0 = (uint32_t)i0_64;
-        double acc[kPts];
-        #pragma unroll
-        for (int p = 0; p < kPts; ++p) acc[p] = 0.0;
-        #pragma unroll 1
-        for (int j = 0; j < d; ++j) {
-            const double b = dims.d[j].b, q = dims.d[j].q;
-            const uint32_t z = dims.d[j].z;
-            const uint32_t zm = z - n;
-            uint32_t r = mulmod_shoup(i0, z, dims.d[j].zs, n);
-            #pragma unroll
-            for (int p = 0; p < kPts; ++p) {
-                const double xs = denorm_of(r, H[p]) * M;
-                acc[p] = fma(fma(q, xs, b), xs, acc[p]);
-                r = step_mod(r, z, zm);
-            }
-        }
-        double s = 0.0;
+    const int64_t tile = blockIdx.x;
+    const uint64_t i0_64 = a.base + (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kPts;
+    const uint32_t i0 = (uint32_t)i0_64;
+    const uint32_t n = a.n;
+    const double M = a.M;
+    double acc[kPts];
+    #pragma unroll
+    for (int p = 0; p < kPts; ++p) acc[p] = 0.0;
+    #pragma unroll 1
+    for (int j = 0; j < a.d; ++j) {
+        const double b = a.dims[j].b, q = a.dims[j].q;
+        const uint32_t z = a.dims[j].z;
+        const uint32_t zm = z - n;
+        uint32_t r = mulmod_shoup(i0, z, a.dims[j].zs, n);
         #pragma unroll
         for (int p = 0; p < kPts; ++p) {
-            double f = quad_outer(acc[p], alpha, K);
-            s += (i0_64 + p < end) ? f : 0.0;
+            const double xs = denorm_of(r, H[p]) * M;
+            acc[p] = fma(fma(q, xs, b), xs, acc[p]);
+            r = step_mod(r, z, zm);
         }
-        s = block_sum(s, sh);
-        if (threadIdx.x == 0) tile_out[tile] = s;
     }
+    double s = 0.0;
+    #pragma unroll
+    for (int p = 0; p < kPts; ++p) {
+        double f = quad_outer(acc[p], a.alpha, a.K);
+        s += (i0_64 + p < a.end) ? f : 0.0;
+    }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) tile_out[tile] = s;
 }
 
 // ============================================================ generic bytecode
