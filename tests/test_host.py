@@ -1,0 +1,272 @@
+"""CPU: host-side logic of the drop-in (parser, lowering, bookkeeping, ABI)."""
+
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st
+
+import paper_2404_08867_b200 as lq
+from paper_2404_08867_b200 import expr as E
+from paper_2404_08867_b200 import lower as L
+from paper_2404_08867_b200.configs import make_config
+from paper_2404_08867_b200.mdi import _det_a, _level_plan, _normalize
+from paper_2404_08867_b200.transform import axis_counts, midpoint_grids
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+# ---------------------------------------------------------------- parser
+
+def test_parser_quirks_match_reference_grammar():
+    x = E.var(1)
+    assert E.evaluate(lq.parse("-x[1]^2", 1), {1: 3.0}) == 9.0          # (-a)^k, exprcore.py:591-603
+    assert E.evaluate(lq.parse("x[1]/4", 1), {1: 2.0}) == 0.5
+    assert E.evaluate(lq.parse("2/(1+x[1])", 1), {1: 1.0}) == 1.0
+    assert E.evaluate(lq.parse("sum(i=1..d, i*x[i])", 3), {1: 1, 2: 1, 3: 1}) == 6.0
+    assert E.evaluate(lq.parse("prod(i=1..d, x[i]^(i))", 3), {1: 2, 2: 2, 3: 2}) == 64.0
+    assert E.evaluate(lq.parse("exp(sum(i=1..d, (-1)^(i+1)*x[i]))", 2), {1: 1.0, 2: 1.0}) == 1.0
+    assert E.evaluate(lq.parse("2*pi + e", 1), {}) == 2 * math.pi + math.e
+    assert E.evaluate(lq.parse("abs(x[1]-1)", 1), {1: 0.25}) == 0.75     # extension
+    for bad in ("x[0]", "x[3]", "foo(1)", "x[1]/x[2]", "(1", "1 $ 2", "x[1]/0"):
+        with pytest.raises(lq.ParseError):
+            lq.parse(bad, 2)
+
+
+def test_repr_float_literals_round_trip():
+    cfg = make_config(2)
+    f = lq.parse(cfg.text, cfg.d)
+    fam = L.recognize_plain(f, cfg.d)
+    assert fam.kind == "lin_sincos"
+    assert np.array_equal(fam.beta, np.asarray(cfg.c))
+
+
+def test_reference_expr_adapter_duck_typing():
+    class R:   # minimal stand-in for a latquad Expr node (exprcore.py:80-91)
+        def __init__(self, kind, value=0.0, index=0, children=()):
+            self.kind, self.value, self.index, self.children = kind, value, index, children
+    x1, x2 = R("var", index=1), R("var", index=2)
+    s = R("sum", 0.5, 0, ((x1, 2.0), (x2, -1.0)))
+    e = R("exp", children=(s,))
+    p = R("prod", 3.0, 0, (e, R("pow", 0.0, -1, (x2,))))
+    got = E.as_expr(p)
+    assert E.evaluate(got, {1: 0.3, 2: 0.7}) == pytest.approx(3.0 * math.exp(0.5 + 0.6 - 0.7) / 0.7, rel=1e-15)
+
+
+# ------------------------------------------------------------- lowering
+
+@pytest.mark.parametrize("cid,kind", [(1, "lin_exp"), (2, "lin_sincos"), (3, "quad_exp"), (5, "lin_expabs")])
+def test_config_families_recognised(cid, kind):
+    cfg = make_config(cid)
+    fam = L.recognize_plain(lq.parse(cfg.text, cfg.d), cfg.d)
+    assert fam is not None and fam.kind == kind
+
+
+def _family_value(fam, x):
+    if fam.kind == "lin_exp":
+        return fam.K * math.exp(fam.alpha + float(fam.beta @ x))
+    if fam.kind == "lin_sincos":
+        L_ = float(fam.beta @ x)
+        return fam.C0 + fam.A * math.sin(L_) + fam.B * math.cos(L_)
+    if fam.kind == "lin_expabs":
+        return fam.K * math.exp(fam.kappa * abs(fam.alpha + float(fam.beta @ x)))
+    return fam.K * math.exp(fam.alpha + float(fam.beta @ x) + float(fam.gamma @ (x * x)))
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 5])
+def test_family_parameters_reproduce_the_integrand(cid):
+    cfg = make_config(cid)
+    f = lq.parse(cfg.text, cfg.d)
+    fam = L.recognize_plain(f, cfg.d)
+    rng = np.random.default_rng(cid)
+    for _ in range(5):
+        x = rng.uniform(0, 1, cfg.d)
+        want = E.evaluate(f, {j + 1: x[j] for j in range(cfg.d)})
+        assert _family_value(fam, x) == pytest.approx(want, rel=1e-12, abs=1e-14)
+
+
+def _run_bytecode(prog, xs):
+    """Python interpreter of the liblq bytecode (mirror of lq_device.cuh::run_program)."""
+    slot = [0.0] * prog.n_slots
+    for op, a, b, n, c in prog.insn.tolist():
+        if op == L.OP_CONST or op == L.OP_ACC_INIT:
+            slot[a] = c
+        elif op == L.OP_VAR:
+            slot[a] = xs[b]
+        elif op == L.OP_ACC_ADD:
+            slot[a] = slot[a] + c * slot[b]
+        elif op == L.OP_ACC_ADDVAR:
+            slot[a] = slot[a] + c * xs[b]
+        elif op == L.OP_ACC_MUL:
+            slot[a] = slot[a] * slot[b]
+        elif op == L.OP_POW:
+            slot[a] = slot[b] ** n
+        elif op == L.OP_RPOW:
+            slot[a] = 1.0 / (slot[b] ** n)
+        else:
+            slot[a] = {L.OP_EXP: math.exp, L.OP_SIN: math.sin, L.OP_COS: math.cos, L.OP_ABS: abs}[op](slot[b])
+    return slot[prog.result]
+
+
+CORPUS_LIKE = [
+    ("x[2]*exp(x[1]*x[2])/(e-2)", 2), ("sin(2*pi + sum(i=1..d, x[i]^2))", 4),
+    ("exp(sum(i=1..d, x[i])) / (e-1)^d", 3), ("0.3989422804014327*exp(-sum(i=1..d, x[i]^2)/2)", 5),
+    ("prod(i=1..d, 1/(0.81 + (x[i]-0.6)^2))", 4), ("(1 + sum(i=1..d, x[i]))^(-(d+1))", 3),
+    ("cos(2*pi + sum(i=1..d, 2*x[i]))", 6), ("x[1]^3*x[2] - 0.5*x[3]^2 + x[1]*x[2]*x[3] + 0.25", 3),
+    ("exp(-abs(0.3*x[1] - 0.2*x[2] + 0.1))", 2), ("(x[1] + x[2])^2 * (x[1] - x[2])^-2", 2),
+]
+
+
+@pytest.mark.parametrize("text,d", CORPUS_LIKE)
+def test_bytecode_matches_host_evaluation(text, d):
+    f = lq.parse(text, d)
+    prog = L.compile_program(f)
+    rng = np.random.default_rng(len(text))
+    for _ in range(10):
+        x = rng.uniform(0.05, 0.95, d)
+        want = E.evaluate(f, {j + 1: x[j] for j in range(d)})
+        assert _run_bytecode(prog, list(x)) == pytest.approx(want, rel=1e-13, abs=1e-300)
+    assert prog.n_slots <= L.MAX_SLOTS
+
+
+def _sep_eval(terms, x):
+    tot = 0j
+    for t in terms:
+        v = complex(t.coef)
+        for ax, fc in t.factors.items():
+            R = E.evaluate(fc.R, {ax: x[ax - 1]}) if fc.R is not None else 1.0
+            P = E.evaluate(fc.P, {ax: x[ax - 1]}) if fc.P is not None else 0.0
+            v *= R * complex(math.cos(P), math.sin(P))
+        tot += v
+    return tot
+
+
+@pytest.mark.parametrize("text,d", [t for t in CORPUS_LIKE if "abs" not in t[0] and "^(-(d+1))" not in t[0]
+                                    and "exp(x[1]*x[2])" not in t[0] and "^-2" not in t[0]])
+def test_separation_is_exact(text, d):
+    f = lq.parse(text, d)
+    terms = L.separate(f)
+    assert terms is not None
+    rng = np.random.default_rng(d)
+    for _ in range(6):
+        x = rng.uniform(0, 1, d)
+        want = E.evaluate(f, {j + 1: x[j] for j in range(d)})
+        got = _sep_eval(terms, x)
+        assert abs(got.imag) <= 1e-12 * max(1.0, abs(want))
+        assert got.real == pytest.approx(want, rel=1e-12, abs=1e-12)
+
+
+def test_non_separable_detected():
+    for text, d in [("x[2]*exp(x[1]*x[2])", 2), ("(1 + x[1] + x[2])^(-3)", 2), ("exp(-abs(x[1] - x[2]))", 2)]:
+        assert L.separate(lq.parse(text, d)) is None
+
+
+_coef = st.floats(min_value=-2, max_value=2, allow_nan=False)
+
+
+@given(st.lists(st.tuples(st.integers(1, 4), st.integers(1, 3), _coef), min_size=1, max_size=6), _coef)
+@settings(max_examples=40, deadline=None)
+def test_separation_random_polynomials(monos, c0):
+    pairs = [(c, E.power(E.var(i), k)) for i, k, c in monos]
+    f = E.add(pairs, c0)
+    terms = L.separate(f)
+    assert terms is not None
+    x = np.linspace(0.1, 0.9, 4)
+    want = E.evaluate(f, {j + 1: x[j] for j in range(4)})
+    assert _sep_eval(terms, x).real == pytest.approx(want, rel=1e-12, abs=1e-12)
+
+
+# ---------------------------------------------------- rules and bookkeeping
+
+def test_lattice_rule_validation_mirrors_reference():
+    with pytest.raises(ValueError):
+        lq.LatticeRule(0, (1,))
+    with pytest.raises(ValueError):
+        lq.LatticeRule(5, ())
+    with pytest.raises(ValueError):
+        lq.LatticeRule(5, (1, 0))
+    r = lq.korobov_vector(7, 81, 3)
+    assert r.z == (1, 7, 49) and r.z_reduced == (1, 7, 49)
+    big = lq.korobov_vector(10, 101, 3)
+    assert big.z == (1, 10, 100) and not big.is_grid_type
+    assert lq.LatticeRule(4, (1, 2)).is_grid_type
+    assert len({lq.LatticeRule(8, (1, 3)), lq.LatticeRule(8, (1, 3))}) == 1
+    with pytest.raises(ValueError):
+        lq.korobov_vector(0, 11, 2)
+    with pytest.raises(ValueError):
+        lq.korobov_vector(11, 11, 2)
+    cfg = make_config(5)
+    rule = lq.korobov_vector(cfg.plain_a, cfg.plain_n, cfg.d)
+    assert rule.z_reduced == tuple(c % rule.n for c in rule.z[:0]) + cfg.plain_z()
+
+
+def test_axis_counts_closed_form_equals_lcm_form():
+    for a, n, d in [(3, 81, 4), (10, 1 + 10**10, 10), (478, 1009, 8), (64, 64**100, 100), (1, 11, 4)]:
+        kor = lq.korobov_vector(a, n, d)
+        plain = lq.LatticeRule(n, kor.z)
+        assert axis_counts(kor) == axis_counts(plain)
+    assert midpoint_grids(lq.korobov_vector(2, 8, 3)).nodes == ((0.25, 0.75),) * 2 + ((0.25, 0.75),)
+
+
+def test_level_plan_matches_reference_reports(golden):
+    for case in golden["mdi"]:
+        if "levels" not in case:
+            continue
+        levels, base = _level_plan(case["d"], lq.MdiConfig())
+        assert (levels, len(base)) == (case["levels"], case["base_dim"]), case["tag"]
+
+
+def test_mdiconfig_validation():
+    for kw in ({"m": 0}, {"m": 4}, {"budget": 0}, {"order": "sideways"}, {"fallback": "retry"}):
+        with pytest.raises(ValueError):
+            lq.MdiConfig(**kw)
+    cfg = lq.MdiConfig()
+    assert cfg.m == 1 and cfg.order == "forward" and cfg.fallback == "numeric"
+
+
+def test_det_a_and_normalize(golden):
+    for case in golden["mdi"]:
+        if case.get("det_a") is None:
+            continue
+        rule = lq.korobov_vector(case["a"], int(case["n"]), case["d"])
+        assert _det_a(rule) == float.fromhex(case["det_a"]), case["tag"]
+        counts = axis_counts(rule)
+        assert _normalize(float.fromhex(case["raw"]), counts) == float.fromhex(case["value"])
+
+
+def test_quadrature_result_validation():
+    with pytest.raises(ValueError):
+        lq.QuadratureResult(method="slr", value=1.0, points=0, d=1, n=1)
+    with pytest.raises(ValueError):
+        lq.QuadratureResult(method="slr", value=1.0, points=1, d=1, n=1, rel_error=-0.1)
+
+
+# -------------------------------------------------------------- C ABI
+
+def test_library_exports_every_declared_symbol():
+    from paper_2404_08867_b200 import _native
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("liblq.so not built")
+    header = open(os.path.join(REPO, "include", "lq.h")).read()
+    names = set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(lq_\w+)\s*\(", header, re.M))
+    assert len(names) >= 18
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    for name in sorted(names):
+        assert hasattr(lib, name), name
+    h = _native.lib()
+    assert h.lq_abi_version() == 1
+    assert h.lq_lattice_num_supers(2**31 - 1) == 512
+
+
+def test_error_mapping_without_gpu():
+    from paper_2404_08867_b200 import _native
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("liblq.so not built")
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check")
+    with pytest.raises(_native.NativeUnavailable):
+        _native.ctx(0)
