@@ -172,7 +172,9 @@ def main():
 
     h = N.lib()
     ctx = N.ctx(local)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream shared by liblq and the timing events
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     N.check(h.lq_ctx_set_stream(ctx, C.c_void_p(stream.cuda_stream)))
 
     cfg = make_config(5)

@@ -165,10 +165,11 @@ int lq_mdi_sum(lq_ctx* ctx, const lq_insn* insn, int32_t n_insn, const lq_factor
  * an extension):  sum_grid = K prod_j N_j (|kappa|/pi) int_R Re[e^{i w alpha}
  * prod_j phi_j(w)] / (kappa^2 + w^2) dw,  phi_j(w) = (1/N_j) sum_t e^{i w beta_j y_t}.
  * w_nodes/w_weights: host quadrature on [0, W] (even integrand, factor 2
- * applied by the caller).  out2[0] = log|integral part|, out2[1] = sign.      */
+ * applied by the caller).  out2[0] = log|sum_k w_k |kappa|/(kappa^2+w_k^2)
+ * Re[e^{i w_k alpha} prod_j phi_j(w_k)]|, out2[1] = its sign.                  */
 int lq_mdi_expabs(lq_ctx* ctx, int32_t d, const double* beta, const int32_t* counts, double alpha,
                   const double* w_nodes, const double* w_weights, int32_t n_w, double kappa,
-                  double* out2);
+                  double* out2, double* logmag_out /* optional [n_w]: log|prod_j phi_j(w_k)| */);
 
 /* ---- FP64 roofline probe: DFMA chains on every SM; returns TFLOP/s ----- */
 int lq_fp64_peak(lq_ctx* ctx, int32_t iters, double* tflops, float* ms);

@@ -137,3 +137,27 @@ def separable_log_sum(factor_fns, counts):
         logs += math.log(abs(s))
         sign *= math.copysign(1.0, s)
     return logs, sign
+
+
+def expabs_grid_mean_dp(k, Q, N, alpha, kappa):
+    """Exact-to-rounding mean of exp(kappa |alpha + sum_j (k_j/Q) y_j|) over the
+    midpoint grid y_j in {(t+1/2)/N}, for integer k_j: L*2NQ = sum_j k_j (2t_j+1)
+    is an integer, so its distribution is the convolution of the per-axis
+    uniform pmfs (a dimension iteration over the distribution of the partial
+    linear form).  Validation oracle for the characteristic-function MDI path
+    (an extension: the reference cannot express |.|)."""
+    k = [int(v) for v in k]
+    size = sum(kj * (2 * N - 1) for kj in k) + 1
+    pmf = np.zeros(size)
+    pmf[0] = 1.0
+    top = 0
+    for kj in k:
+        nxt = np.zeros(size)
+        for t in range(N):
+            off = kj * (2 * t + 1)
+            nxt[off:off + top + 1] += pmf[:top + 1]
+        top += kj * (2 * N - 1)
+        pmf = nxt / N
+    m = np.arange(size, dtype=np.float64)
+    L = alpha + m / (2.0 * N * Q)
+    return float(np.sum(pmf * np.exp(kappa * np.abs(L))))

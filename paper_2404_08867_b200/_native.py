@@ -72,7 +72,7 @@ _SIGS = {
     "lq_mdi_block_sums": [_P, _P, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, _P],
     "lq_mdi_combine": [_P, _P, _P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, C.c_int32, _P],
     "lq_mdi_sum": [_P, _P, C.c_int32, _P, C.c_int32, _P, _P, _P, _P, _P, C.c_int32, _P],
-    "lq_mdi_expabs": [_P, C.c_int32, _P, _P, C.c_double, _P, _P, C.c_int32, C.c_double, _P],
+    "lq_mdi_expabs": [_P, C.c_int32, _P, _P, C.c_double, _P, _P, C.c_int32, C.c_double, _P, _P],
     "lq_fp64_peak": [_P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_float)],
 }
 

@@ -654,7 +654,7 @@ int lq_mdi_sum(lq_ctx* c, const lq_insn* insn, int32_t n_insn, const lq_factor* 
 }
 
 int lq_mdi_expabs(lq_ctx* c, int32_t d, const double* beta, const int32_t* counts, double alpha, const double* wn,
-                  const double* ww, int32_t n_w, double kappa, double* out2) {
+                  const double* ww, int32_t n_w, double kappa, double* out2, double* logmag) {
     int rc = set_dev(c);
     if (rc) return rc;
     if (d < 1 || !beta || !counts || !wn || !ww || n_w < 1 || !out2) return fail(LQ_ERR_VALUE, "bad expabs arguments");
@@ -664,16 +664,23 @@ int lq_mdi_expabs(lq_ctx* c, int32_t d, const double* beta, const int32_t* count
     if ((rc = upload(c, B_AUX1, counts, sizeof(int32_t) * d, &dc))) return rc;
     if ((rc = upload(c, B_AUX2, wn, sizeof(double) * n_w, &dw))) return rc;
     if ((rc = upload(c, B_AUX3, ww, sizeof(double) * n_w, &dww))) return rc;
+    void* dl;
     if ((rc = dev_buf(c, B_TILES, sizeof(double) * n_w, &dv))) return rc;
+    if ((rc = dev_buf(c, B_PART, sizeof(double) * n_w, &dl))) return rc;
     t_begin(c);
     lq::k_cf_expabs<<<n_w, lq::kThreads, 0, c->stream>>>((const double*)db, (const int32_t*)dc, d, alpha,
-                                                         (const double*)dw, (const double*)dww, kappa, (double*)dv);
+                                                         (const double*)dw, (const double*)dww, kappa, (double*)dv,
+                                                         (double*)dl);
     t_end(c);
     CK(cudaGetLastError());
     double* r;
     if ((rc = reduce_dev(c, (const double*)dv, n_w, &r))) return rc;
     double s;
     if ((rc = read_scalar(c, r, &s))) return rc;
+    if (logmag) {
+        CK(cudaMemcpyAsync(logmag, dl, sizeof(double) * n_w, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
     out2[0] = s == 0.0 ? -INFINITY : std::log(std::fabs(s));
     out2[1] = s > 0.0 ? 1.0 : (s < 0.0 ? -1.0 : 0.0);
     return LQ_OK;

@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kThreads) k_mdi_combine(const double* __restri
 __global__ void __launch_bounds__(kThreads) k_cf_expabs(const double* __restrict__ beta, const int32_t* __restrict__ counts,
                                                         int d, double alpha, const double* __restrict__ wn,
                                                         const double* __restrict__ ww, double kappa,
-                                                        double* __restrict__ val) {
+                                                        double* __restrict__ val, double* __restrict__ logmag) {
     __shared__ double sl[8], sa[8];
     const int k = blockIdx.x;
     const double w = wn[k];
@@ -420,6 +420,7 @@ __global__ void __launch_bounds__(kThreads) k_cf_expabs(const double* __restrict
         for (int q = 0; q < kThreads / 32; ++q) { L += sl[q]; A += sa[q]; }
         const double ak = fabs(kappa);
         val[k] = ww[k] * ak / (kappa * kappa + w * w) * exp(L) * cos(w * alpha + A);
+        logmag[k] = L;
     }
 }
 

@@ -39,6 +39,19 @@ def world(group=None):
     return dist.get_rank(group), dist.get_world_size(group)
 
 
+def _bind_stream(h, ctx):
+    """Order liblq's work on torch's current stream (NCCL and the partial
+    buffers live there).  The legacy default stream has handle 0, which liblq
+    reads as "context-owned stream", so torch work is first moved to a
+    dedicated stream in that case."""
+    import torch
+    s = torch.cuda.current_stream()
+    if s.cuda_stream == 0:
+        s = torch.cuda.Stream()
+        torch.cuda.set_stream(s)
+    N.check(h.lq_ctx_set_stream(ctx, C.c_void_p(s.cuda_stream)))
+
+
 def shard_range(n_units, rank, size):
     """Contiguous block of ``n_units`` owned by ``rank`` of ``size``."""
     return (n_units * rank) // size, (n_units * (rank + 1)) // size
@@ -68,7 +81,7 @@ def slr_integrate(f, rule, reference=None, group=None):
     pi = engine.plain_integrand(e, d)
     h = N.lib()
     ctx = N.ctx(torch.cuda.current_device())
-    N.check(h.lq_ctx_set_stream(ctx, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    _bind_stream(h, ctx)
     S = int(h.lq_lattice_num_supers(n))
     lo, hi = shard_range(S, rank, size)
     parts = torch.zeros(S, dtype=torch.float64, device="cuda")
@@ -101,7 +114,7 @@ def mdi_lr(f, d, a, n, cfg=None, rule=None, with_report=False, group=None):
         raise GridCapError(f"direct sweep needs {base_total} evaluations, cap is {cfg.direct_cap}")
     h = N.lib()
     ctx = N.ctx(torch.cuda.current_device())
-    N.check(h.lq_ctx_set_stream(ctx, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    _bind_stream(h, ctx)
     nblk = max((int(plan.factors[k].count) + N.LQ_NODE_BLOCK - 1) // N.LQ_NODE_BLOCK
                for k in range(plan.n_factors))
     part = torch.zeros(plan.n_factors * nblk * 2, dtype=torch.float64, device="cuda")

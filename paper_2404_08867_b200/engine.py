@@ -205,3 +205,48 @@ def mdi_separable_sum(plan):
                                N.as_ptr(plan.coef_re), N.as_ptr(plan.coef_im), N.as_ptr(plan.log_extra),
                                plan.n_terms, N.as_ptr(out)))
     return float(out[0]), float(out[1]), float(out[2]), float(out[3])
+
+
+# --------------------------------------------- MDI-LR, exp-abs-linear family
+
+_GL16 = np.polynomial.legendre.leggauss(16)
+
+
+def cf_quadrature(beta, counts, alpha, kappa):
+    """Composite 16-point Gauss-Legendre nodes on [0, Omega] for the
+    characteristic-function integral, plus zero-weight tail probes."""
+    beta = np.asarray(beta, dtype=np.float64)
+    counts = np.asarray(counts, dtype=np.float64)
+    var = float(np.sum(beta * beta * (counts * counts - 1.0) / (12.0 * counts * counts)))
+    sigma = math.sqrt(var)
+    omega = math.sqrt(2.0 * 75.0 / var)                       # Gaussian envelope e^-75 at Omega
+    mu = abs(alpha + 0.5 * float(np.sum(beta)))
+    h = 0.5 * min(abs(kappa), 1.0 / sigma, math.pi / (mu + 3.0 * sigma))
+    panels = max(8, int(math.ceil(omega / h)))
+    x, w = _GL16
+    edges = np.linspace(0.0, omega, panels + 1)
+    mid = 0.5 * (edges[1:] + edges[:-1])[:, None]
+    half = 0.5 * (edges[1:] - edges[:-1])[:, None]
+    nodes = (mid + half * x[None, :]).ravel()
+    weights = (half * w[None, :]).ravel()
+    probes = omega * np.logspace(0.0, 6.0, 64)
+    return nodes, weights, probes, sigma
+
+
+def mdi_expabs_cf(beta, counts, alpha, kappa):
+    """E = mean over the midpoint grid of exp(kappa |alpha + <beta, y>|), kappa < 0,
+    by the characteristic function on the GPU (lq_mdi_expabs).  Returns
+    (E, tail_bound) where tail_bound bounds |prod_j phi_j| beyond Omega."""
+    beta = np.ascontiguousarray(beta, dtype=np.float64)
+    cnt = np.ascontiguousarray(counts, dtype=np.int32)
+    nodes, weights, probes, sigma = cf_quadrature(beta, counts, alpha, kappa)
+    wn = np.ascontiguousarray(np.concatenate([nodes, probes]))
+    ww = np.ascontiguousarray(np.concatenate([weights, np.zeros_like(probes)]))
+    out = np.zeros(2)
+    logmag = np.zeros(len(wn))
+    N.check(N.lib().lq_mdi_expabs(N.ctx(), len(beta), N.as_ptr(beta), N.as_ptr(cnt), float(alpha),
+                                  N.as_ptr(wn), N.as_ptr(ww), len(wn), float(kappa), N.as_ptr(out),
+                                  N.as_ptr(logmag)))
+    E = out[1] * math.exp(out[0]) * 2.0 / math.pi
+    tail = float(np.exp(np.max(logmag[len(nodes):]))) if len(probes) else 0.0
+    return E, tail

@@ -26,6 +26,8 @@ import math
 import time
 from dataclasses import dataclass
 
+import numpy as np
+
 from . import engine
 from .expr import as_expr, evaluate, free_vars
 from .lattice import korobov_vector
@@ -71,7 +73,8 @@ class MdiConfig:
 class MdiReport:
     """Observability record (mdi.py:79-101) plus GPU-side extras:
     log_raw (natural log of |value|, finite even when value under/overflows),
-    sign, method ('separable' | 'direct' | 'constant'), clusters."""
+    sign, method ('separable' | 'direct' | 'constant' | 'characteristic'),
+    clusters."""
 
     value: float
     levels: int
@@ -146,9 +149,15 @@ def mdi_sum(g, grids, cfg=None):
                          log_raw=math.log(abs(value)) if value else -math.inf,
                          sign=math.copysign(1.0, value) if value else 0.0, method="constant", clusters=0)
 
-    plan = engine.separable_plan(e, counts) if not getattr(grids, "_force_direct", False) else None
-    usable = plan is not None and plan.ok and (plan.n_factors + plan.n_terms) <= cfg.budget
+    plan = engine.separable_plan(e, counts)
+    usable = plan.ok and (plan.n_factors + plan.n_terms) <= cfg.budget
     usable = usable and getattr(grids, "midpoint", False)
+    total = math.prod(counts)
+    if (not usable and total > cfg.direct_cap and getattr(grids, "midpoint", False)
+            and cfg.fallback == "numeric"):
+        rep = _characteristic(e, d, counts, levels, base_axes, t0)
+        if rep is not None:
+            return rep
     if not usable:
         if cfg.fallback == "error":
             raise BudgetExceededError("integrand is not separable over the grid axes "
@@ -167,6 +176,35 @@ def mdi_sum(g, grids, cfg=None):
                      level_nodes=(plan.n_factors,) * levels, level_seconds=(0.0,) * levels,
                      base_seconds=secs, fallback=False, log_raw=log_raw, sign=sign,
                      method="separable", clusters=plan.n_factors)
+
+
+def _characteristic(e, d, counts, levels, base_axes, t0):
+    """K exp(kappa |alpha + <beta, x>|), kappa < 0, over the midpoint grid via
+    e^{-k|L|} = (1/pi) int k/(k^2 + w^2) cos(w L) dw: the grid mean becomes a
+    1-D integral of products of per-direction cluster sums
+    phi_j(w) = (1/N_j) sum_t e^{i w beta_j y_t}.  An extension beyond the
+    reference (which has no |.|): returns None when the integrand is not of
+    this form or the truncated integral cannot be certified, and the caller
+    falls back to the direct sweep."""
+    from .lower import recognize_plain
+    fam = recognize_plain(e, d)
+    if fam is None or fam.kind != "lin_expabs" or not fam.kappa < 0.0 or fam.K == 0.0:
+        return None
+    beta = np.asarray(fam.beta, dtype=np.float64)
+    log_total = float(sum(math.log(c) for c in counts))
+    if not np.any(beta):
+        mean = math.exp(fam.kappa * abs(fam.alpha))
+    else:
+        if len(counts) < 2 or max(counts) > 2**31 - 1:
+            return None
+        mean, tail = engine.mdi_expabs_cf(beta, counts, fam.alpha, fam.kappa)
+        if not (mean > 0.0) or tail > 1e-16 * mean:
+            return None
+    log_raw = math.log(abs(fam.K)) + math.log(mean) + log_total
+    raw = math.copysign(math.exp(log_raw), fam.K) if log_raw < 709.0 else math.copysign(math.inf, fam.K)
+    return MdiReport(value=raw, levels=levels, base_dim=len(base_axes), level_nodes=(d,) * levels,
+                     level_seconds=(0.0,) * levels, base_seconds=time.perf_counter() - t0, fallback=False,
+                     log_raw=log_raw, sign=math.copysign(1.0, fam.K), method="characteristic", clusters=d)
 
 
 def _normalize(raw, counts):

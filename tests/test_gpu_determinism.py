@@ -19,7 +19,9 @@ def env():
     from paper_2404_08867_b200 import _native as N, engine
     h = N.lib()
     ctx = N.ctx(0)
-    N.check(h.lq_ctx_set_stream(ctx, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
+    N.check(h.lq_ctx_set_stream(ctx, C.c_void_p(s.cuda_stream)))
     return lq, N, engine, h, ctx
 
 
