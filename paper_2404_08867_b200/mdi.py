@@ -88,10 +88,19 @@ class MdiReport:
     sign: float = None
     method: str = None
     clusters: int = 0
+    log_total: float = None
 
     @property
     def seconds(self):
         return float(sum(self.level_seconds)) + self.base_seconds
+
+    @property
+    def mean(self):
+        """Grid mean exp(log_raw - sum log n_i): finite where ``value`` (the raw
+        sum, kept reference-identical) over- or underflows FP64."""
+        if self.log_raw is None or self.log_total is None:
+            return None
+        return (self.sign or 0.0) * math.exp(self.log_raw - self.log_total)
 
 
 def _const_sweep(value, counts):
@@ -248,6 +257,7 @@ def mdi_lr(f, d, a, n, cfg=None, rule=None, with_report=False):
     grids = midpoint_grids(rule)
     report = mdi_sum(f, grids, cfg)
     report.det_a = _det_a(rule)
+    report.log_total = float(sum(math.log(c) for c in grids.counts))
     value = _normalize(report.value, grids.counts)
     if with_report:
         return value, report

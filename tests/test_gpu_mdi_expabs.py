@@ -3,8 +3,9 @@ function (extension beyond the reference, which has no |.|; SURVEY §8c marks
 config 5's MDI-LR parity as unpinned).  Validated against an exact
 dimension-iteration oracle over the distribution of the linear form
 (oracle.np_oracle.expabs_grid_mean_dp), which needs rational beta_j = k_j/Q:
-Q = 4096 and N = 8 put the lattice revival of the characteristic function at
-w = 2 pi 2NQ ~ 4e5, far beyond where the integrand matters."""
+Q = 4096 and N >= 8 put the lattice revival of the characteristic function at
+w = 2 pi 2NQ >= 4e5, whose leftover (a property of the rational surrogate, not
+of real beta) stays below the 1e-10 bar."""
 
 import math
 
@@ -15,11 +16,11 @@ pytestmark = pytest.mark.gpu
 
 
 def _text(k, Q, alpha, kappa):
-    terms = " + ".join(f"{kj / Q!r}*x[{j + 1}]" for j, kj in enumerate(k))
+    terms = " + ".join(f"{float(kj) / Q!r}*x[{j + 1}]" for j, kj in enumerate(k))
     return f"exp({kappa!r}*abs({terms} + {alpha!r}))"
 
 
-@pytest.mark.parametrize("d,N,kappa,shift,seed", [(40, 8, -1.0, 0.0, 1), (40, 8, -2.5, 0.7, 2),
+@pytest.mark.parametrize("d,N,kappa,shift,seed", [(40, 8, -1.0, 0.0, 1), (32, 16, -2.5, 0.7, 2),
                                                   (64, 8, -1.0, -1.3, 3), (32, 16, -0.5, 0.2, 4)])
 def test_characteristic_function_matches_exact_oracle(d, N, kappa, shift, seed):
     import paper_2404_08867_b200 as lq
@@ -42,6 +43,8 @@ def test_config5_mdi_runs_and_is_plausible():
     f = lq.parse(cfg.text, cfg.d)
     value, rep = lq.mdi_lr(f, cfg.d, cfg.mdi_a, cfg.mdi_n, with_report=True)
     assert rep.method == "characteristic"
+    assert value == math.inf       # raw sum 512^1000 * mean overflows FP64, as the reference's would
+    value = rep.mean                # the finite grid mean, from log_raw
     # the midpoint-grid mean and the plain-lattice mean both approximate the same
     # integral; their difference is quadrature error, not arithmetic error
     plain = 0.9200283162987288   # slr_integrate on cfg5's n = 2^31-1 lattice (bench estimate)
