@@ -193,7 +193,7 @@ def main():
     N.check(h.lq_fp64_peak(ctx, iters, C.byref(tf), C.byref(ms)))
     fp64_peak = tf.value
 
-    n_super = int(h.lq_lattice_num_supers(n))
+    tile_pts, n_super = N.lattice_layout(pi.struct, n)
     s_lo, s_hi = n_super * rank // world, n_super * (rank + 1) // world
     parts = torch.zeros(n_super, dtype=torch.float64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")     # 256 MiB > 126 MB L2
@@ -242,7 +242,7 @@ def main():
     estimate = value_sum / n
 
     # dominant kernel roofline: k_lin<EXPABS> over this rank's points
-    sp = N.LQ_TILE * N.LQ_SUPER_TILES
+    sp = tile_pts * N.LQ_SUPER_TILES
     my_pts = min(s_hi * sp, n) - s_lo * sp
     avg_kern = kern_ms / args.steps
     achieved = (FLOPS_PER_PD * d + FLOPS_PER_POINT) * my_pts / (avg_kern * 1e-3) / 1e12

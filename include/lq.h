@@ -19,7 +19,7 @@
  *    (e.g. torch tensors' data_ptr()).  Device scratch is owned by the lq_ctx.
  *  - All work is ordered on the context's stream (lq_ctx_set_stream); calls
  *    that return values to host pointers synchronise that stream.
- *  - Reductions are deterministic: fixed tiles of LQ_TILE points, a fixed
+ *  - Reductions are deterministic: fixed tiles of points, a fixed
  *    in-tile tree, fixed super-chunks of LQ_SUPER_TILES tiles and a fixed
  *    pairwise tree over super-chunk partials, independent of grid size and of
  *    how super-chunks are split across GPUs.
@@ -43,8 +43,10 @@ extern "C" {
 #define LQ_ERR_UNSUPPORTED (-5)
 #define LQ_ERR_NOMEM (-6)
 
-#define LQ_TILE 4096          /* points (or flat grid nodes) per reduction tile */
-#define LQ_SUPER_TILES 1024   /* tiles per super-chunk (4 Mi points)           */
+#define LQ_TILE 4096          /* flat grid nodes per tile (tensor sums); points per
+                                 tile of the bytecode lattice kernel; the family
+                                 kernels use 6144-point tiles (lq_lattice_layout) */
+#define LQ_SUPER_TILES 1024   /* tiles per super-chunk                          */
 #define LQ_NODE_BLOCK 256     /* MDI nodes per deterministic partial block     */
 #define LQ_MAX_SLOTS 512      /* bytecode live-slot limit                      */
 
@@ -109,10 +111,12 @@ int lq_points_block(lq_ctx* ctx, int32_t d, uint64_t n, const uint64_t* z_reduce
  * Returns sum_{i in [i_begin, i_end)} f(frac(i z / n)) (not divided by n).   */
 int lq_lattice_sum(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_t* z_reduced,
                    uint64_t i_begin, uint64_t i_end, double* sum_out);
-/* Multi-GPU building blocks: super-chunk s covers points
- * [s*LQ_TILE*LQ_SUPER_TILES, (s+1)*...) of [0, n).  Writes the partials of
+/* Multi-GPU building blocks.  The tile size depends on the kernel chosen for
+ * (f, n); lq_lattice_layout reports it and the number of super-chunks.
+ * Super-chunk s covers points [s*T*LQ_SUPER_TILES, (s+1)*T*LQ_SUPER_TILES)
+ * of [0, n), T = tile points.  lq_lattice_partials writes the partials of
  * super-chunks [s_begin, s_end) to out_dev[0 .. s_end-s_begin).             */
-int64_t lq_lattice_num_supers(uint64_t n);
+int lq_lattice_layout(const lq_integrand* f, uint64_t n, int64_t* tile_points, int64_t* n_supers);
 int lq_lattice_partials(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_t* z_reduced,
                         int64_t s_begin, int64_t s_end, double* out_dev);
 /* Fixed pairwise tree over vals_dev[0..count); result to host *out. */

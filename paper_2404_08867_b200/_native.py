@@ -66,6 +66,7 @@ _SIGS = {
     "lq_points_block": [_P, C.c_int32, C.c_uint64, _P, C.c_int64, C.c_int64, _P, C.c_int32],
     "lq_lattice_sum": [_P, C.POINTER(Integrand), C.c_uint64, _P, C.c_uint64, C.c_uint64, C.POINTER(C.c_double)],
     "lq_lattice_partials": [_P, C.POINTER(Integrand), C.c_uint64, _P, C.c_int64, C.c_int64, _P],
+    "lq_lattice_layout": [C.POINTER(Integrand), C.c_uint64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
     "lq_reduce_sum": [_P, _P, C.c_int64, C.POINTER(C.c_double)],
     "lq_tensor_sum": [_P, C.POINTER(Program), C.c_int32, _P, _P, C.c_int32, C.c_uint64, C.c_uint64,
                       C.POINTER(C.c_double)],
@@ -98,8 +99,6 @@ def lib():
                 fn.restype = C.c_int
             h.lq_last_error.argtypes = []
             h.lq_last_error.restype = C.c_char_p
-            h.lq_lattice_num_supers.argtypes = [C.c_uint64]
-            h.lq_lattice_num_supers.restype = C.c_int64
             _lib = h
     return _lib
 
@@ -149,6 +148,13 @@ def ctx(device=None):
     if c is None:
         c = _ctxs[key] = _Ctx(device)
     return c.ptr
+
+
+def lattice_layout(pi_struct, n):
+    """(tile points, number of super-chunks) of the kernel liblq picks for (f, n)."""
+    tp, ns = C.c_int64(), C.c_int64()
+    check(lib().lq_lattice_layout(C.byref(pi_struct), int(n), C.byref(tp), C.byref(ns)))
+    return tp.value, ns.value
 
 
 def as_ptr(arr):

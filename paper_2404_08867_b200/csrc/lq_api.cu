@@ -225,12 +225,20 @@ int lin_dispatch(lq_ctx* c, const std::vector<lq::LinDim>& tab, int d, uint64_t 
     return launch_lin<OUTER>(c, args, ntiles, tiles_dev);
 }
 
+bool uses_family_kernel(const lq_integrand* f, uint64_t n) {
+    return n <= (1ull << 31) && f->kind != LQ_FAM_PROGRAM;
+}
+
+uint64_t tile_points(const lq_integrand* f, uint64_t n) {
+    return uses_family_kernel(f, n) ? (uint64_t)lq::kFamTile : (uint64_t)lq::kTile;
+}
+
 // Launch the tile kernel of integrand f over points [base, end) writing
 // ntiles tile partials to tiles_dev.
 int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z, uint64_t base, uint64_t end,
                  int64_t ntiles, double* tiles_dev) {
     const int d = f->d;
-    const bool fast = n <= (1ull << 31) && f->kind != LQ_FAM_PROGRAM;
+    const bool fast = uses_family_kernel(f, n);
     int rc;
     if (fast && (f->kind == LQ_FAM_LIN_EXP || f->kind == LQ_FAM_LIN_SINCOS || f->kind == LQ_FAM_LIN_EXPABS)) {
         if (!f->beta) return fail(LQ_ERR_VALUE, "family needs beta");
@@ -248,6 +256,8 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
             tab[j].c = std::ldexp(f->beta[j] / (double)n, 1074 - sigma);
             tab[j].z = (uint32_t)z[j];
             tab[j].zs = (uint32_t)(((uint64_t)z[j] << 32) / n);
+            tab[j].z2 = (uint32_t)((2 * z[j]) % n);
+            tab[j].pad = 0;
         }
         const double scale = std::ldexp(1.0, sigma);
         if (f->kind == LQ_FAM_LIN_EXP) return lin_dispatch<lq::OUT_EXP>(c, tab, d, n, base, end, ntiles, f, scale, tiles_dev);
@@ -266,6 +276,8 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
             tab[j].q = std::ldexp(f->gamma[j], 2 * sigma);
             tab[j].z = (uint32_t)z[j];
             tab[j].zs = (uint32_t)(((uint64_t)z[j] << 32) / n);
+            tab[j].z2 = (uint32_t)((2 * z[j]) % n);
+            tab[j].pad = 0;
             if (!std::isfinite(tab[j].b) || !std::isfinite(tab[j].q))
                 return fail(LQ_ERR_VALUE, "quadratic coefficient out of range");
         }
@@ -449,9 +461,14 @@ int lq_points_block(lq_ctx* c, int32_t d, uint64_t n, const uint64_t* z, int64_t
     return LQ_OK;
 }
 
-int64_t lq_lattice_num_supers(uint64_t n) {
-    const uint64_t sp = (uint64_t)LQ_TILE * LQ_SUPER_TILES;
-    return (int64_t)((n + sp - 1) / sp);
+int lq_lattice_layout(const lq_integrand* f, uint64_t n, int64_t* tile_pts, int64_t* n_supers) {
+    int rc;
+    if ((rc = check_integrand(f))) return rc;
+    const uint64_t tp = tile_points(f, n);
+    const uint64_t sp = tp * LQ_SUPER_TILES;
+    if (tile_pts) *tile_pts = (int64_t)tp;
+    if (n_supers) *n_supers = (int64_t)((n + sp - 1) / sp);
+    return LQ_OK;
 }
 
 int lq_lattice_partials(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z, int64_t s_begin,
@@ -459,14 +476,16 @@ int lq_lattice_partials(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint
     int rc = set_dev(c);
     if (rc) return rc;
     if ((rc = check_integrand(f)) || (rc = check_lattice(n, z, f->d))) return rc;
-    const int64_t ns = lq_lattice_num_supers(n);
+    int64_t tp64, ns;
+    lq_lattice_layout(f, n, &tp64, &ns);
+    const uint64_t tp = (uint64_t)tp64;
     if (s_begin < 0 || s_end > ns || s_end < s_begin)
         return fail(LQ_ERR_VALUE, "super-chunk range [%lld, %lld) outside [0, %lld)", (long long)s_begin, (long long)s_end, (long long)ns);
     if (s_end == s_begin) return LQ_OK;
-    const uint64_t sp = (uint64_t)LQ_TILE * LQ_SUPER_TILES;
+    const uint64_t sp = tp * LQ_SUPER_TILES;
     const uint64_t base = (uint64_t)s_begin * sp;
     const uint64_t end = std::min<uint64_t>((uint64_t)s_end * sp, n);
-    const int64_t ntiles = (int64_t)((end - base + LQ_TILE - 1) / LQ_TILE);
+    const int64_t ntiles = (int64_t)((end - base + tp - 1) / tp);
     void* tiles;
     if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
     if ((rc = launch_tiles(c, f, n, z, base, end, ntiles, (double*)tiles))) return rc;
@@ -496,9 +515,10 @@ int lq_lattice_sum(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t*
         *sum_out = 0.0;
         return LQ_OK;
     }
-    if (n <= (1ull << 31) && i_end > (1ull << 32) - 2 * LQ_TILE)
+    const uint64_t tp = tile_points(f, n);
+    if (n <= (1ull << 31) && i_end > (1ull << 32) - 2 * tp)
         return fail(LQ_ERR_VALUE, "index range beyond 2^32 for n <= 2^31; reduce indices mod n");
-    const int64_t ntiles = (int64_t)((i_end - i_begin + LQ_TILE - 1) / LQ_TILE);
+    const int64_t ntiles = (int64_t)((i_end - i_begin + tp - 1) / tp);
     void* tiles;
     if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
     if ((rc = launch_tiles(c, f, n, z, i_begin, i_end, ntiles, (double*)tiles))) return rc;

@@ -2,7 +2,7 @@
 ``torch.distributed`` (NCCL over NVLink) for the single exchange step.
 
 Plain lattice sum: the index range [0, n) is cut into fixed super-chunks of
-LQ_TILE * LQ_SUPER_TILES points (include/lq.h); rank r of P owns super-chunks
+LQ_SUPER_TILES tiles (lq_lattice_layout, include/lq.h); rank r of P owns super-chunks
 [floor(r S / P), floor((r+1) S / P)) and writes their partials into its own
 slots of a zero vector of length S.  One all-reduce(SUM) over disjoint slots
 is exact (x + 0 = x in IEEE arithmetic) whatever order NCCL reduces in, so
@@ -82,7 +82,7 @@ def slr_integrate(f, rule, reference=None, group=None):
     h = N.lib()
     ctx = N.ctx(torch.cuda.current_device())
     _bind_stream(h, ctx)
-    S = int(h.lq_lattice_num_supers(n))
+    _, S = N.lattice_layout(pi.struct, n)
     lo, hi = shard_range(S, rank, size)
     parts = torch.zeros(S, dtype=torch.float64, device="cuda")
     if hi > lo:

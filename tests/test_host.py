@@ -258,7 +258,12 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     h = _native.lib()
     assert h.lq_abi_version() == 1
-    assert h.lq_lattice_num_supers(2**31 - 1) == 512
+    from paper_2404_08867_b200 import engine
+    cfg = make_config(5)
+    pi = engine.plain_integrand(lq.parse(cfg.text, cfg.d), cfg.d)
+    assert _native.lattice_layout(pi.struct, cfg.plain_n) == (6144, 342)
+    prog = engine.plain_integrand(lq.parse(cfg.text, cfg.d), cfg.d, force_program=True)
+    assert _native.lattice_layout(prog.struct, cfg.plain_n) == (4096, 512)
 
 
 def test_error_mapping_without_gpu():
