@@ -47,7 +47,7 @@ class Expr:
     'exp', 'sin', 'cos', 'abs' (args = (arg,)).
     """
 
-    __slots__ = ("op", "val", "idx", "args", "terms", "_key", "_hash")
+    __slots__ = ("op", "val", "idx", "args", "terms", "_key", "_hash", "_fv")
 
     def __init__(self, op, val=0.0, idx=0, args=(), terms=()):
         self.op = op
@@ -61,6 +61,7 @@ class Expr:
             key = (op, self.val, self.idx, tuple(a._key for a in self.args))
         self._key = key
         self._hash = hash(key)
+        self._fv = None
 
     def __hash__(self):
         return self._hash
@@ -254,7 +255,10 @@ def node_count(e):
 
 
 def free_vars(e):
-    return {n.idx for n in topo(e) if n.op == "var"}
+    """Set of 1-based coordinate indices in e (cached on the node)."""
+    if e._fv is None:
+        e._fv = frozenset(n.idx for n in topo(e) if n.op == "var")
+    return set(e._fv)
 
 
 def evaluate(e, assignment):

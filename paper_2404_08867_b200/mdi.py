@@ -129,13 +129,12 @@ def direct_tensor_sum(g, grids, cap=DIRECT_CAP):
 
 
 def _level_plan(d, cfg):
-    """Levels and base axes exactly as the reference's loop (mdi.py:146-165)."""
-    axes = list(range(1, d + 1))
-    levels = 0
-    while len(axes) > 3:
-        for _ in range(cfg.m):
-            axes = axes[:-1] if cfg.order == "forward" else axes[1:]
-        levels += 1
+    """Levels and base axes of the reference's loop (mdi.py:146-165): strip
+    m axes per level while more than 3 remain, from the end ("forward") or the
+    start ("reverse")."""
+    levels = -(-(d - 3) // cfg.m) if d > 3 else 0
+    base = d - levels * cfg.m
+    axes = list(range(1, base + 1)) if cfg.order == "forward" else list(range(d - base + 1, d + 1))
     return levels, axes
 
 
