@@ -54,7 +54,19 @@ def main():
             fl = (FLOPS_PER_PD[cid] * cfg.d + 2) * pts
             print(f"cfg{cid} {pi.kind:10s} n={n} d={cfg.d}: kernel {kms:.3f} ms wall {wall*1e3:.3f} ms "
                   f"{pts/kms*1e3:.3e} pts/s {pd/kms*1e3:.3e} pd/s {fl/kms*1e-9:.2f} TF  value={s/n!r}")
-    for cid, cap in ((2, None), (4, None), (1, 10**10)):
+    # steady-state rate of the Gaussian family kernel on a large lattice
+    cfg = make_config(3)
+    f = lq.parse(cfg.text, cfg.d)
+    big = lq.korobov_vector(cfg.plain_a, 2**31 - 1, cfg.d)
+    pi = engine.plain_integrand(f, cfg.d)
+    engine.lattice_sum(pi, big.n, big.z_reduced_array(), 0, 1 << 27)
+    engine.lattice_sum(pi, big.n, big.z_reduced_array(), 0, 1 << 27)
+    kms = C.c_float(); nl = C.c_int64()
+    N.check(h.lq_last_kernel_ms(ctx, C.byref(kms), C.byref(nl)))
+    pd = (1 << 27) * cfg.d
+    print(f"quad_exp big-n d=300 2^27 pts: kernel {kms.value:.3f} ms {pd/kms.value*1e3:.3e} pd/s "
+          f"{(5*cfg.d+2)*(1<<27)/kms.value*1e-9:.2f} TF")
+    for cid, cap in ((2, None), (4, None), (1, 10**10), (5, None)):
         cfg = make_config(cid)
         f = lq.parse(cfg.text, cfg.d)
         mc = lq.MdiConfig(direct_cap=cap) if cap else None
