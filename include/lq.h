@@ -175,6 +175,25 @@ int lq_mdi_expabs(lq_ctx* ctx, int32_t d, const double* beta, const int32_t* cou
                   const double* w_nodes, const double* w_weights, int32_t n_w, double kappa,
                   double* out2, double* logmag_out /* optional [n_w]: log|prod_j phi_j(w_k)| */);
 
+/* ---- lattice quality measures and constructions (
+ * lattice.py:140-311).  B_alpha and the factors 1 + g_j (B + beta) follow
+ * numpy's operation order.  n <= 2^31.                                       */
+/* sum over i in [i_begin, i_end) of prod_j (1 + g_j (B_alpha(x_ij) + beta)):
+ * shift_avg_wce_sq (g = weights, beta = anchor constant) and p_alpha
+ * (g = sign (2 pi)^alpha / alpha!, beta = 0).                               */
+int lq_bprod_sum(lq_ctx* ctx, int32_t alpha, int32_t d, uint64_t n, const uint64_t* z_reduced,
+                 const double* g, double beta, uint64_t i_begin, uint64_t i_end, double* sum_out);
+/* cbc_construct (lattice.py:259-289): z_1 = 1, then for each s the candidate
+ * minimising the shift-averaged worst-case error, ties to the earliest
+ * (strict improvement with 1e-9 relative head-room, lattice.py:248-252).    */
+int lq_cbc_construct(lq_ctx* ctx, uint64_t n, int32_t d, const double* gamma, double beta,
+                     const int64_t* candidates, int64_t n_candidates, int64_t* z_out);
+/* korobov_search building block (lattice.py:292-311): for each candidate a,
+ * sum_k prod_j (1 + gamma_j (B_2(x_kj) + beta)) over the Korobov rule
+ * z = (1, a, ..., a^(d-1)).                                                 */
+int lq_korobov_values(lq_ctx* ctx, uint64_t n, int32_t d, const double* gamma, double beta,
+                      const int64_t* candidates, int64_t n_candidates, double* sums_out);
+
 /* ---- FP64 roofline probe: DFMA chains on every SM; returns TFLOP/s ----- */
 int lq_fp64_peak(lq_ctx* ctx, int32_t iters, double* tflops, float* ms);
 

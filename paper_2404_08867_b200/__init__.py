@@ -13,6 +13,8 @@ from .transform import AxisGridSet, axis_counts, midpoint_grids
 from .mdi import (DEFAULT_NODE_BUDGET, DIRECT_CAP, BudgetExceededError, GridCapError, MdiConfig,
                   MdiReport, direct_tensor_sum, mdi_lr, mdi_sum)
 from .quad import QuadratureResult, implr_integrate, mdilr_integrate, slr_integrate
+from .quality import (QualityWarning, WeightModel, bernoulli_poly, cbc_construct, korobov_search, p_alpha,
+                      shift_avg_wce_sq)
 
 __version__ = "0.1.0"
 
@@ -23,5 +25,7 @@ __all__ = [
     "DEFAULT_NODE_BUDGET", "DIRECT_CAP", "BudgetExceededError", "GridCapError", "MdiConfig",
     "MdiReport", "direct_tensor_sum", "mdi_lr", "mdi_sum",
     "QuadratureResult", "implr_integrate", "mdilr_integrate", "slr_integrate",
+    "QualityWarning", "WeightModel", "bernoulli_poly", "cbc_construct", "korobov_search", "p_alpha",
+    "shift_avg_wce_sq",
     "__version__",
 ]

@@ -75,6 +75,10 @@ _SIGS = {
     "lq_mdi_sum": [_P, _P, C.c_int32, _P, C.c_int32, _P, _P, _P, _P, _P, C.c_int32, _P],
     "lq_mdi_expabs": [_P, C.c_int32, _P, _P, C.c_double, _P, _P, C.c_int32, C.c_double, _P, _P],
     "lq_fp64_peak": [_P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_float)],
+    "lq_bprod_sum": [_P, C.c_int32, C.c_int32, C.c_uint64, _P, _P, C.c_double, C.c_uint64, C.c_uint64,
+                     C.POINTER(C.c_double)],
+    "lq_cbc_construct": [_P, C.c_uint64, C.c_int32, _P, C.c_double, _P, C.c_int64, _P],
+    "lq_korobov_values": [_P, C.c_uint64, C.c_int32, _P, C.c_double, _P, C.c_int64, _P],
 }
 
 _lib = None

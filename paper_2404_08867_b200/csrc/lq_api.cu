@@ -735,3 +735,158 @@ int lq_fp64_peak(lq_ctx* c, int32_t iters, double* tflops, float* ms) {
 }
 
 }  // extern "C"
+
+// ============================================================ quality measures
+namespace {
+
+int b2_table(lq_ctx* c, uint32_t n, double** out) {
+    void* p;
+    int rc;
+    if ((rc = dev_buf(c, B_AUX2, sizeof(double) * n, &p))) return rc;
+    const double nd = (double)n;
+    lq::k_b2_table<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, c->stream>>>(n, nd, 1.0 / nd, (double*)p);
+    c->launches++;
+    CK(cudaGetLastError());
+    *out = (double*)p;
+    return LQ_OK;
+}
+
+bool improves(double val, double best) { return val < best - 1e-9 * std::fabs(best); }   // lattice.py:248-252
+
+constexpr size_t kSmemTable = 200 * 1024;
+
+template <class K>
+int persistent_grid(lq_ctx* c, K kern, size_t smem) {
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kern, lq::kThreads, smem);
+    return c->sm_count * std::max(per_sm, 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+int lq_bprod_sum(lq_ctx* c, int32_t alpha, int32_t d, uint64_t n, const uint64_t* z, const double* g, double beta,
+                 uint64_t i_begin, uint64_t i_end, double* sum_out) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (alpha != 2 && alpha != 4) return fail(LQ_ERR_VALUE, "alpha must be 2 or 4, got %d", alpha);
+    if ((rc = check_lattice(n, z, d))) return rc;
+    if (n > (1ull << 31)) return fail(LQ_ERR_UNSUPPORTED, "quality sums support n <= 2^31");
+    if (!g || !sum_out || i_end < i_begin) return fail(LQ_ERR_VALUE, "bad arguments");
+    if (i_end == i_begin) {
+        *sum_out = 0.0;
+        return LQ_OK;
+    }
+    std::vector<lq::QDim> tab(d);
+    for (int j = 0; j < d; ++j) {
+        tab[j].z = (uint32_t)z[j];
+        tab[j].zs = (uint32_t)(((uint64_t)z[j] << 32) / n);
+        tab[j].g = g[j];
+    }
+    void* dt;
+    if ((rc = upload(c, B_TAB, tab.data(), sizeof(lq::QDim) * d, &dt))) return rc;
+    const int64_t ntiles = (int64_t)((i_end - i_begin + lq::kTile - 1) / lq::kTile);
+    void* tiles;
+    if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
+    const double nd = (double)n;
+    t_begin(c);
+    if (alpha == 2)
+        lq::k_bprod<2><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>((const lq::QDim*)dt, d, (uint32_t)n, nd, 1.0 / nd, beta, i_begin, i_end, (double*)tiles);
+    else
+        lq::k_bprod<4><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>((const lq::QDim*)dt, d, (uint32_t)n, nd, 1.0 / nd, beta, i_begin, i_end, (double*)tiles);
+    t_end(c);
+    CK(cudaGetLastError());
+    double* r;
+    if ((rc = reduce_dev(c, (const double*)tiles, ntiles, &r))) return rc;
+    return read_scalar(c, r, sum_out);
+}
+
+int lq_cbc_construct(lq_ctx* c, uint64_t n, int32_t d, const double* gamma, double beta, const int64_t* cands,
+                     int64_t ncand, int64_t* z_out) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (n < 2 || n > (1ull << 31)) return fail(LQ_ERR_VALUE, "CBC supports 2 <= n <= 2^31, got %llu", (unsigned long long)n);
+    if (d < 1 || !gamma || !z_out) return fail(LQ_ERR_VALUE, "bad arguments");
+    if (d > 1 && (ncand < 1 || !cands)) return fail(LQ_ERR_VALUE, "no candidates");
+    for (int64_t k = 0; k < ncand; ++k)
+        if (cands[k] < 1 || (uint64_t)cands[k] >= n) return fail(LQ_ERR_VALUE, "candidate out of range");
+    double* b2;
+    if ((rc = b2_table(c, (uint32_t)n, &b2))) return rc;
+    void *basev, *dc, *dv;
+    if ((rc = dev_buf(c, B_AUX3, sizeof(double) * n, &basev))) return rc;
+    lq::k_cbc_init<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, c->stream>>>((uint32_t)n, b2, gamma[0], beta, (double*)basev);
+    c->launches++;
+    CK(cudaGetLastError());
+    z_out[0] = 1;
+    if (d == 1) return lq_sync(c);
+    if ((rc = upload(c, B_AUX0, cands, sizeof(int64_t) * ncand, &dc))) return rc;
+    if ((rc = dev_buf(c, B_OUT, sizeof(double) * ncand, &dv))) return rc;
+    std::vector<double> vals(ncand);
+    const bool smem = sizeof(double) * n <= kSmemTable;
+    const size_t shbytes = smem ? sizeof(double) * n : 0;
+    const int grid = smem ? persistent_grid(c, lq::k_cbc_eval<true>, shbytes) : persistent_grid(c, lq::k_cbc_eval<false>, 0);
+    double anchor = 1.0 + gamma[0] * beta;
+    for (int s = 1; s < d; ++s) {
+        const double g = gamma[s];
+        anchor *= 1.0 + g * beta;
+        t_begin(c);
+        if (smem)
+            lq::k_cbc_eval<true><<<std::min<int64_t>(grid, ncand), lq::kThreads, shbytes, c->stream>>>((uint32_t)n, b2, (const double*)basev, g, beta, (const int64_t*)dc, ncand, (double*)dv);
+        else
+            lq::k_cbc_eval<false><<<std::min<int64_t>(grid, ncand), lq::kThreads, 0, c->stream>>>((uint32_t)n, b2, (const double*)basev, g, beta, (const int64_t*)dc, ncand, (double*)dv);
+        t_end(c);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(vals.data(), dv, sizeof(double) * ncand, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        int64_t best = -1;
+        double best_val = INFINITY;
+        for (int64_t k = 0; k < ncand; ++k) {
+            const double val = vals[k] / (double)n - anchor;
+            if (best < 0 || improves(val, best_val)) {
+                best = k;
+                best_val = val;
+            }
+        }
+        z_out[s] = cands[best];
+        lq::k_cbc_update<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, c->stream>>>((uint32_t)n, b2, g, beta, (uint32_t)cands[best], (double*)basev);
+        c->launches++;
+        CK(cudaGetLastError());
+    }
+    return lq_sync(c);
+}
+
+int lq_korobov_values(lq_ctx* c, uint64_t n, int32_t d, const double* gamma, double beta, const int64_t* cands,
+                      int64_t ncand, double* sums_out) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (n < 2 || n > (1ull << 31)) return fail(LQ_ERR_VALUE, "Korobov search supports 2 <= n <= 2^31");
+    if (d < 1 || !gamma || !sums_out || ncand < 0) return fail(LQ_ERR_VALUE, "bad arguments");
+    if (ncand == 0) return LQ_OK;
+    for (int64_t k = 0; k < ncand; ++k)
+        if (cands[k] < 1 || (uint64_t)cands[k] >= n) return fail(LQ_ERR_VALUE, "candidate out of range");
+    double* b2;
+    if ((rc = b2_table(c, (uint32_t)n, &b2))) return rc;
+    void *dg, *dc, *dv;
+    if ((rc = upload(c, B_AUX1, gamma, sizeof(double) * d, &dg))) return rc;
+    if ((rc = upload(c, B_AUX0, cands, sizeof(int64_t) * ncand, &dc))) return rc;
+    if ((rc = dev_buf(c, B_OUT, sizeof(double) * ncand, &dv))) return rc;
+    const bool smem = sizeof(double) * n <= kSmemTable;
+    const size_t shbytes = smem ? sizeof(double) * n : 0;
+    const int grid = smem ? persistent_grid(c, lq::k_korobov<true>, shbytes) : persistent_grid(c, lq::k_korobov<false>, 0);
+    t_begin(c);
+    if (smem)
+        lq::k_korobov<true><<<std::min<int64_t>(grid, ncand), lq::kThreads, shbytes, c->stream>>>((uint32_t)n, d, b2, (const double*)dg, beta, (const int64_t*)dc, ncand, (double*)dv);
+    else
+        lq::k_korobov<false><<<std::min<int64_t>(grid, ncand), lq::kThreads, 0, c->stream>>>((uint32_t)n, d, b2, (const double*)dg, beta, (const int64_t*)dc, ncand, (double*)dv);
+    t_end(c);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(sums_out, dv, sizeof(double) * ncand, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return LQ_OK;
+}
+
+}  // extern "C"

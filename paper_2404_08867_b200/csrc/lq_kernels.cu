@@ -479,3 +479,147 @@ __global__ void __launch_bounds__(kThreads) k_fp64_peak(int iters, double seed, 
 }
 
 }  // namespace lq
+
+namespace lq {
+
+// ============================================================ quality measures
+// Bernoulli polynomials in numpy's operation order (lattice.py:140-149):
+// B2 = (x - 1/2)^2 - 1/12, B4 = ((x - 2) x + 1) x x - 1/30, each op rounded
+// (no contraction), so per-point factors match the reference bit for bit.
+__device__ __forceinline__ double bern2(double x) {
+    const double t = __dsub_rn(x, 0.5);
+    return __dsub_rn(__dmul_rn(t, t), 1.0 / 12.0);
+}
+
+__device__ __forceinline__ double bern4(double x) {
+    return __dsub_rn(__dmul_rn(__dmul_rn(__dadd_rn(__dmul_rn(__dsub_rn(x, 2.0), x), 1.0), x), x), 1.0 / 30.0);
+}
+
+// 1 + g (B + beta), as numpy evaluates `1.0 + g * (B + beta)`
+__device__ __forceinline__ double bfactor(double B, double g, double beta) {
+    return __dadd_rn(1.0, __dmul_rn(g, __dadd_rn(B, beta)));
+}
+
+struct QDim {
+    uint32_t z, zs;   // z mod n, Shoup constant
+    double g;         // weight gamma_j (or the p_alpha coefficient)
+};
+
+// sum over points of prod_j (1 + g_j (B_alpha(x_j) + beta)), x_j = RN(r/n)
+// exactly: shift_avg_wce_sq (lattice.py:225-245) and p_alpha (:167-181).
+template <int ALPHA>
+__global__ void __launch_bounds__(kThreads) k_bprod(const QDim* __restrict__ dims, int d, uint32_t n, double n_d,
+                                                    double inv_n, double beta, uint64_t base, uint64_t end,
+                                                    double* __restrict__ tile_out) {
+    __shared__ double sh[8];
+    const uint64_t i0_64 = base + (uint64_t)blockIdx.x * kTile + (uint64_t)threadIdx.x * kPts;
+    const uint32_t i0 = (uint32_t)i0_64;
+    double prod[kPts];
+    #pragma unroll
+    for (int p = 0; p < kPts; ++p) prod[p] = 1.0;
+    for (int j = 0; j < d; ++j) {
+        const QDim dm = dims[j];
+        const uint32_t zm = dm.z - n;
+        uint32_t r = mulmod_shoup(i0 % n, dm.z, dm.zs, n);
+        #pragma unroll
+        for (int p = 0; p < kPts; ++p) {
+            const double x = exact_div((double)r, n_d, inv_n);
+            const double B = ALPHA == 2 ? bern2(x) : bern4(x);
+            prod[p] = __dmul_rn(prod[p], bfactor(B, dm.g, beta));
+            r = step_mod(r, dm.z, zm);
+        }
+    }
+    double s = 0.0;
+    #pragma unroll
+    for (int p = 0; p < kPts; ++p) s += (i0_64 + p < end) ? prod[p] : 0.0;
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
+}
+
+// B2 of every residue: b2[r] = B2(RN(r/n)), as bernoulli_poly(np.arange(n)/n, 2)
+// (lattice.py:272).
+__global__ void k_b2_table(uint32_t n, double n_d, double inv_n, double* __restrict__ b2) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+        b2[r] = bern2(exact_div((double)r, n_d, inv_n));
+}
+
+// CBC base column: base[k] = 1 + gamma_1 (b2[k] + beta) (lattice.py:274)
+__global__ void k_cbc_init(uint32_t n, const double* __restrict__ b2, double g, double beta,
+                           double* __restrict__ basev) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        basev[k] = bfactor(b2[k], g, beta);
+}
+
+// CBC candidate sweep (lattice.py:280-287): for every candidate c,
+// val[c] = sum_k base[k] * (1 + g (b2[(k c) mod n] + beta)).  Persistent CTAs
+// hold the B2 table in shared memory when it fits and walk the candidates.
+template <bool SMEM>
+__global__ void __launch_bounds__(kThreads) k_cbc_eval(uint32_t n, const double* __restrict__ b2g,
+                                                       const double* __restrict__ basev, double g, double beta,
+                                                       const int64_t* __restrict__ cands, int64_t ncand,
+                                                       double* __restrict__ vals) {
+    extern __shared__ double b2s[];
+    __shared__ double sh[8];
+    const double* b2 = b2g;
+    if (SMEM) {
+        for (uint32_t r = threadIdx.x; r < n; r += kThreads) b2s[r] = b2g[r];
+        __syncthreads();
+        b2 = b2s;
+    }
+    for (int64_t ci = blockIdx.x; ci < ncand; ci += gridDim.x) {
+        const uint32_t c = (uint32_t)cands[ci];
+        const uint32_t step = (uint32_t)(((uint64_t)c * kThreads) % n), stepm = step - n;
+        uint32_t r = (uint32_t)(((uint64_t)threadIdx.x * c) % n);
+        double s = 0.0;
+        for (uint32_t k = threadIdx.x; k < n; k += kThreads) {
+            s += __dmul_rn(basev[k], bfactor(b2[r], g, beta));
+            r = step_mod(r, step, stepm);
+        }
+        s = block_sum(s, sh);
+        if (threadIdx.x == 0) vals[ci] = s;
+    }
+}
+
+__global__ void k_cbc_update(uint32_t n, const double* __restrict__ b2, double g, double beta, uint32_t c,
+                             double* __restrict__ basev) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint32_t r = (uint32_t)(((uint64_t)k * c) % n);
+        basev[k] = __dmul_rn(basev[k], bfactor(b2[r], g, beta));
+    }
+}
+
+// Korobov search (lattice.py:292-311): for every candidate a, sum over points
+// k of prod_j (1 + g_j (b2[k a^j mod n] + beta)); residues advance along j by
+// a Shoup modmul with the candidate's constant.
+template <bool SMEM>
+__global__ void __launch_bounds__(kThreads) k_korobov(uint32_t n, int d, const double* __restrict__ b2g,
+                                                      const double* __restrict__ gam, double beta,
+                                                      const int64_t* __restrict__ cands, int64_t ncand,
+                                                      double* __restrict__ vals) {
+    extern __shared__ double b2s[];
+    __shared__ double sh[8];
+    const double* b2 = b2g;
+    if (SMEM) {
+        for (uint32_t r = threadIdx.x; r < n; r += kThreads) b2s[r] = b2g[r];
+        __syncthreads();
+        b2 = b2s;
+    }
+    for (int64_t ci = blockIdx.x; ci < ncand; ci += gridDim.x) {
+        const uint32_t a = (uint32_t)(cands[ci] % n);
+        const uint32_t as = (uint32_t)(((uint64_t)a << 32) / n);
+        double s = 0.0;
+        for (uint32_t k = threadIdx.x; k < n; k += kThreads) {
+            uint32_t r = k;
+            double prod = 1.0;
+            for (int j = 0; j < d; ++j) {
+                prod = __dmul_rn(prod, bfactor(b2[r], __ldg(gam + j), beta));
+                r = mulmod_shoup(r, a, as, n);
+            }
+            s += prod;
+        }
+        s = block_sum(s, sh);
+        if (threadIdx.x == 0) vals[ci] = s;
+    }
+}
+
+}  // namespace lq

@@ -31,6 +31,11 @@ def unb64(s, shape):
 
 
 @pytest.fixture(scope="session")
+def golden_quality():
+    return load_golden("quality")
+
+
+@pytest.fixture(scope="session")
 def golden():
     return {k: load_golden(k) for k in ("points", "slr", "mdi")}
 

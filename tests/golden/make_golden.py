@@ -34,7 +34,8 @@ sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, REPO)
 
 from latquad import corpus, exprcore  # noqa: E402  (reference, read-only)
-from latquad.lattice import LatticeRule, korobov_vector, points_block  # noqa: E402
+from latquad.lattice import (LatticeRule, WeightModel, cbc_construct, korobov_search,  # noqa: E402
+                             korobov_vector, p_alpha, points_block, shift_avg_wce_sq)
 from latquad.mdi import MdiConfig, direct_tensor_sum, mdi_lr  # noqa: E402
 from latquad.quad import implr_integrate, mdilr_integrate, slr_integrate  # noqa: E402
 from latquad.transform import axis_counts, midpoint_grids  # noqa: E402
@@ -203,15 +204,57 @@ def mdi_cases(skip_slow):
     return out
 
 
+def quality_cases():
+    """Lattice quality measures and constructions (lattice.py:140-311),
+    SURVEY.md §8(f) item 3."""
+    import warnings
+    out = []
+
+    def rule_rec(rule):
+        return {"n": str(rule.n), "z": [str(c) for c in rule.z]}
+
+    rules = [LatticeRule(5, (1,)), LatticeRule(8, (1, 3)), LatticeRule(13, (1, 5)), LatticeRule(4, (1, 2)),
+             korobov_vector(7, 81, 3), korobov_vector(76, 1009, 6), korobov_vector(1234, 10007, 8),
+             korobov_vector(29, 4099, 12), korobov_vector(3, 2**20 + 7, 5), LatticeRule(8191, (1, 4000, 77, 5))]
+    for rule in rules:
+        for alpha in (2, 4):
+            with warnings.catch_warnings(record=True) as w:
+                warnings.simplefilter("always")
+                v = p_alpha(rule, alpha)
+            out.append({"tag": f"p_alpha{alpha}", **rule_rec(rule), "alpha": alpha, "value": hx(v),
+                        "warned": bool(w)})
+        for wm in (None, WeightModel.anchored([1.0 / (j + 1) for j in range(rule.d)], 0.7),
+                   WeightModel.unanchored([0.9 ** j for j in range(rule.d)])):
+            v = shift_avg_wce_sq(rule, wm)
+            out.append({"tag": "wce", **rule_rec(rule), "value": hx(v),
+                        "gamma": None if wm is None else [hx(g) for g in wm.gamma],
+                        "beta": None if wm is None else hx(wm.beta)})
+    for n, d in ((8, 3), (13, 3), (101, 5), (257, 6), (1009, 4), (4001, 3)):
+        t0 = time.perf_counter()
+        z = cbc_construct(n, d).z
+        out.append({"tag": "cbc", "n": n, "d": d, "z": list(z), "ref_seconds": time.perf_counter() - t0})
+        wm = WeightModel.anchored([0.5 ** j for j in range(d)], 1.0)
+        z = cbc_construct(n, d, wm).z
+        out.append({"tag": "cbc_anchored", "n": n, "d": d, "z": list(z),
+                    "gamma": [hx(g) for g in wm.gamma], "beta": hx(wm.beta)})
+    for n, d, crit in ((13, 3, "wce"), (101, 4, "wce"), (101, 4, "p2"), (1009, 6, "wce"), (1009, 6, "p2"),
+                       (2003, 8, "wce")):
+        t0 = time.perf_counter()
+        r = korobov_search(n, d, criterion=crit)
+        out.append({"tag": "korobov_search", "n": n, "d": d, "criterion": crit, "a": r.z[1] if d > 1 else 1,
+                    "ref_seconds": time.perf_counter() - t0})
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
-    ap.add_argument("--only", choices=["points", "slr", "mdi"], default=None)
+    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality"], default=None)
     args = ap.parse_args()
     meta = {"generator": "tests/golden/make_golden.py", "numpy": np.__version__,
             "python": sys.version.split()[0], "reference": "/root/reference/pkg (latquad 0.1.0)"}
     jobs = {"points": lambda: points_cases(), "slr": lambda: slr_cases(args.skip_slow),
-            "mdi": lambda: mdi_cases(args.skip_slow)}
+            "mdi": lambda: mdi_cases(args.skip_slow), "quality": quality_cases}
     for name, fn in jobs.items():
         if args.only and name != args.only:
             continue
