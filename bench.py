@@ -134,7 +134,7 @@ def run_reference(args, rank, world):
                    "integrand": "exp(-|sum c_j (x_j - w_j)|)", "sample_points_per_step": sample},
         "cpu_baseline": {"value": value, "unit": "f-evals/s", "cores": cores, "kind": "port",
                          "sample": f"first {sample} points of cfg5 per step, numpy restatement of "
-                                   "lattice.points_block + integrand over {cores} processes"},
+                                   f"lattice.points_block + integrand over {cores} processes"},
         "e2e": {"value": value, "unit": "f-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -146,8 +146,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 18)
-    ap.add_argument("--ref-sample", type=int, default=1 << 19)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 21)
+    ap.add_argument("--ref-sample", type=int, default=1 << 21)
     ap.add_argument("--no-mdi", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -248,19 +248,31 @@ def main():
     achieved = (FLOPS_PER_PD * d + FLOPS_PER_POINT) * my_pts / (avg_kern * 1e-3) / 1e12
 
     # e2e: the public drop-in API (host lowering, parameter H2D, kernel, result D2H)
-    e2e = None
-    if world == 1:
-        lq.slr_integrate(f, rule)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            r = lq.slr_integrate(f, rule)
-        e2e_s = time.perf_counter() - t0
-        e2e = {"value": args.steps * n / e2e_s, "unit": "f-evals/s",
-               "h2d_bytes_per_step": d * 16 + 8 * d, "d2h_bytes_per_step": 8,
-               "api": "paper_2404_08867_b200.slr_integrate(f, rule)", "estimate": r.value}
+    # e2e: the public drop-in API (host lowering, parameter upload, kernel,
+    # exchange, result D2H); multi-GPU through distributed.slr_integrate
+    from paper_2404_08867_b200 import distributed
+    api = lq.slr_integrate if world == 1 else distributed.slr_integrate
+    api(f, rule)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = api(f, rule)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": args.steps * n / e2e_s, "unit": "f-evals/s",
+           "h2d_bytes_per_step": d * 24, "d2h_bytes_per_step": 8,
+           "api": ("paper_2404_08867_b200.slr_integrate(f, rule)" if world == 1
+                   else "paper_2404_08867_b200.distributed.slr_integrate(f, rule)"),
+           "estimate": r.value}
 
     if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
         return
     prof = {}
     prof_path = os.path.join(REPO, "profiles", "ncu_summary.json")
@@ -274,7 +286,8 @@ def main():
         rate, dt, _ = cpu_port_rate(cfg, args.cpu_sample, workers=1)
         cpu = {"value": rate, "unit": "f-evals/s", "cores": 1, "kind": "port",
                "sample": f"first {args.cpu_sample} points of cfg5 (numpy restatement of lattice.points_block "
-                         f"+ exp(-|.|), oracle/np_oracle.py), {dt:.1f} s on 1 core"}
+                         f"+ exp(-|.|), oracle/np_oracle.py), {dt:.1f} s on 1 core; "
+                         f"{os.cpu_count()} host cores, numpy {np.__version__}"}
 
     mdi = {}
     if not args.no_mdi and world == 1:
