@@ -181,22 +181,63 @@ int pick_slots(int n_slots) {
     return n_slots <= 32 ? 32 : LQ_MAX_SLOTS;
 }
 
-template <int OUTER, class Args>
-int launch_lin(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev) {
+uint64_t tile_points(const lq_integrand* f, uint64_t n);
+bool uses_family_kernel(const lq_integrand* f, uint64_t n);
+
+// Dimension split of the family kernels: lattices with fewer tiles than
+// ~4 waves of CTAs run each tile on a cluster of S CTAs that split the
+// dimensions (k_fam<S>).  S depends on (n, d) only, so every GPU of a
+// multi-GPU run uses the same reduction structure.
+int fam_split(uint64_t n, int d) {
+    const uint64_t tiles = (n + lq::kFamTile - 1) / lq::kFamTile;
+    const uint64_t want = 148ull * 2 * 4;
+    int S = 1;
+    while (S < 8 && tiles * S < want && d / (2 * S) >= 16) S *= 2;
+    return S;
+}
+
+template <int KIND, int OUTER, class Args, int S>
+int launch_fam_s(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev) {
+    auto kern = lq::k_fam<KIND, OUTER, Args, S>;
+    const size_t smem = S > 1 ? sizeof(double) * lq::kFamPts * lq::kThreads : 0;
+    if (S > 1) {
+        static bool attr_set = false;   // per template instance
+        if (!attr_set) {
+            CK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr_set = true;
+        }
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ntiles, S, 1);
+    cfg.blockDim = dim3(lq::kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = S;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = S > 1 ? 1 : 0;
     t_begin(c);
-    lq::k_lin<OUTER, Args><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, 0u, tiles_dev);
+    CK(cudaLaunchKernelEx(&cfg, kern, args, 0u, tiles_dev));
     t_end(c);
     CK(cudaGetLastError());
     return LQ_OK;
 }
 
-template <class Args>
-int launch_quad(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev) {
-    t_begin(c);
-    lq::k_quad<Args><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, 0u, tiles_dev);
-    t_end(c);
-    CK(cudaGetLastError());
-    return LQ_OK;
+template <int KIND, int OUTER, class Args>
+int launch_fam(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev, uint64_t n_total) {
+    switch (fam_split(n_total, args.d)) {
+        case 1: return launch_fam_s<KIND, OUTER, Args, 1>(c, args, ntiles, tiles_dev);
+        case 2: return launch_fam_s<KIND, OUTER, Args, 2>(c, args, ntiles, tiles_dev);
+        case 4: return launch_fam_s<KIND, OUTER, Args, 4>(c, args, ntiles, tiles_dev);
+        default: return launch_fam_s<KIND, OUTER, Args, 8>(c, args, ntiles, tiles_dev);
+    }
+}
+
+uint64_t tile_points(const lq_integrand* f, uint64_t n) {
+    return uses_family_kernel(f, n) ? (uint64_t)lq::kFamTile : (uint64_t)lq::kTile;
 }
 
 template <class A>
@@ -214,7 +255,7 @@ int lin_dispatch(lq_ctx* c, const std::vector<lq::LinDim>& tab, int d, uint64_t 
         static thread_local Args args;
         fill_head(args, d, n, base, end, f->alpha, scale, f->K, f->A, f->B, f->C0, f->kappa, 0.0);
         std::memcpy(args.dims, tab.data(), sizeof(lq::LinDim) * d);
-        return launch_lin<OUTER>(c, args, ntiles, tiles_dev);
+        return launch_fam<lq::FAM_LIN, OUTER>(c, args, ntiles, tiles_dev, n);
     }
     void* dt;
     int rc;
@@ -222,16 +263,14 @@ int lin_dispatch(lq_ctx* c, const std::vector<lq::LinDim>& tab, int d, uint64_t 
     lq::FamArgsG<lq::LinDim> args;
     fill_head(args, d, n, base, end, f->alpha, scale, f->K, f->A, f->B, f->C0, f->kappa, 0.0);
     args.dims = (const lq::LinDim*)dt;
-    return launch_lin<OUTER>(c, args, ntiles, tiles_dev);
+    return launch_fam<lq::FAM_LIN, OUTER>(c, args, ntiles, tiles_dev, n);
 }
 
 bool uses_family_kernel(const lq_integrand* f, uint64_t n) {
     return n <= (1ull << 31) && f->kind != LQ_FAM_PROGRAM;
 }
 
-uint64_t tile_points(const lq_integrand* f, uint64_t n) {
-    return uses_family_kernel(f, n) ? (uint64_t)lq::kFamTile : (uint64_t)lq::kTile;
-}
+uint64_t tile_points(const lq_integrand* f, uint64_t n);
 
 // Launch the tile kernel of integrand f over points [base, end) writing
 // ntiles tile partials to tiles_dev.
@@ -286,14 +325,14 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
             static thread_local Args args;
             fill_head(args, d, n, base, end, f->alpha, 1.0, f->K, 0, 0, 0, 0, M);
             std::memcpy(args.dims, tab.data(), sizeof(lq::QuadDim) * d);
-            return launch_quad(c, args, ntiles, tiles_dev);
+            return launch_fam<lq::FAM_QUAD, 0>(c, args, ntiles, tiles_dev, n);
         }
         void* dt;
         if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(lq::QuadDim), &dt))) return rc;
         lq::FamArgsG<lq::QuadDim> args;
         fill_head(args, d, n, base, end, f->alpha, 1.0, f->K, 0, 0, 0, 0, M);
         args.dims = (const lq::QuadDim*)dt;
-        return launch_quad(c, args, ntiles, tiles_dev);
+        return launch_fam<lq::FAM_QUAD, 0>(c, args, ntiles, tiles_dev, n);
     }
     // generic bytecode (any family falls back here for n > 2^31)
     const lq_program* pg = &f->prog;

@@ -1,6 +1,10 @@
 // liblq kernels (sm_100a).  See include/lq.h for the ABI and DESIGN.md for
 // the roofline of each kernel.
+#include <cooperative_groups.h>
+
 #include "lq_device.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace lq {
 
@@ -98,10 +102,70 @@ struct FamArgsG {   // d > kParamDims: per-dimension records in global memory
 // residue read as a denormal -- x_j/n folded into the coefficient, no
 // conversion, no division.  tile_out[t] = sum over tile t
 // (fixed tree).
-template <int OUTER, class Args>
-__global__ void __launch_bounds__(kThreads, 2) k_lin(const __grid_constant__ Args a, uint32_t hmask,
+enum : int { FAM_LIN = 0, FAM_QUAD = 1 };
+
+// Accumulate dimensions [j0, j1) of the family's per-point inner sum for the
+// P consecutive points starting at i0 (two residue chains: even/odd points).
+//  LIN:  acc += c_j * (2^-1074 r)                 (one DFMA per point-dim)
+//  QUAD: xs = (2^-1074 r) * M; acc += (q_j xs + b_j) xs   (three FP64 ops)
+template <int KIND, class Args, int P>
+__device__ __forceinline__ void fam_accumulate(const Args& a, uint32_t i0, int j0, int j1, const uint32_t (&H)[P],
+                                               double (&acc)[P]) {
+    const uint32_t n = a.n;
+    #pragma unroll 1
+    for (int j = j0; j < j1; ++j) {
+        const uint32_t z = a.dims[j].z, zm = z - n;
+        const uint32_t z2 = a.dims[j].z2, z2m = z2 - n;
+        uint32_t r0 = mulmod_shoup(i0, z, a.dims[j].zs, n);
+        uint32_t r1 = step_mod(r0, z, zm);
+        if constexpr (KIND == FAM_LIN) {
+            const double c = a.dims[j].c;
+            #pragma unroll
+            for (int p = 0; p < P; p += 2) {
+                acc[p] = fma(c, denorm_of(r0, H[p]), acc[p]);
+                acc[p + 1] = fma(c, denorm_of(r1, H[p + 1]), acc[p + 1]);
+                if (p + 2 < P) {
+                    r0 = step_mod(r0, z2, z2m);
+                    r1 = step_mod(r1, z2, z2m);
+                }
+            }
+        } else {
+            const double b = a.dims[j].b, q = a.dims[j].q, M = a.M;
+            #pragma unroll
+            for (int p = 0; p < P; p += 2) {
+                const double x0 = denorm_of(r0, H[p]) * M, x1 = denorm_of(r1, H[p + 1]) * M;
+                acc[p] = fma(fma(q, x0, b), x0, acc[p]);
+                acc[p + 1] = fma(fma(q, x1, b), x1, acc[p + 1]);
+                if (p + 2 < P) {
+                    r0 = step_mod(r0, z2, z2m);
+                    r1 = step_mod(r1, z2, z2m);
+                }
+            }
+        }
+    }
+}
+
+template <int KIND, int OUTER, class Args>
+__device__ __forceinline__ double fam_outer(double acc, const Args& a) {
+    if constexpr (KIND == FAM_QUAD) {
+        return quad_outer(acc, a.alpha, a.K);
+    } else {
+        const LinParams prm{a.alpha, a.scale, a.K, a.A, a.B, a.C0, a.kappa};
+        return outer_fn<OUTER>(acc, prm);
+    }
+}
+
+// Plain lattice sum of a closed family, n <= 2^31: one tile of 256 threads x
+// 24 consecutive points per CTA (S == 1), or per cluster of S CTAs (S > 1, small
+// n): CTA rank s of the cluster accumulates the s-th slice of the dimensions,
+// parks its partial inner sums in shared memory, and rank 0 adds the S slices
+// in rank order through distributed shared memory before the outer function.
+// tile_out[t] = sum over tile t (fixed tree).
+template <int KIND, int OUTER, class Args, int S>
+__global__ void __launch_bounds__(kThreads, 2) k_fam(const __grid_constant__ Args a, uint32_t hmask,
                                                       double* __restrict__ tile_out) {
     constexpr int P = kFamPts;
+    extern __shared__ double part[];   // [P][kThreads] when S > 1
     __shared__ double sh[8];
     uint32_t H[P];
     #pragma unroll
@@ -109,79 +173,35 @@ __global__ void __launch_bounds__(kThreads, 2) k_lin(const __grid_constant__ Arg
     const int64_t tile = blockIdx.x;
     const uint64_t i0_64 = a.base + (uint64_t)tile * kFamTile + (uint64_t)threadIdx.x * P;
     const uint32_t i0 = (uint32_t)i0_64;   // < 2^32 (n <= 2^31)
-    const uint32_t n = a.n;
     double acc[P];
     #pragma unroll
     for (int p = 0; p < P; ++p) acc[p] = 0.0;
-    #pragma unroll 1
-    for (int j = 0; j < a.d; ++j) {
-        const double c = a.dims[j].c;
-        const uint32_t z = a.dims[j].z, zm = z - n;
-        const uint32_t z2 = a.dims[j].z2, z2m = z2 - n;
-        uint32_t r0 = mulmod_shoup(i0, z, a.dims[j].zs, n);
-        uint32_t r1 = step_mod(r0, z, zm);
+    int rank = 0;
+    if constexpr (S == 1) {
+        fam_accumulate<KIND>(a, i0, 0, a.d, H, acc);
+    } else {
+        cg::cluster_group cluster = cg::this_cluster();
+        rank = (int)cluster.block_rank();
+        fam_accumulate<KIND>(a, i0, (int)((int64_t)a.d * rank / S), (int)((int64_t)a.d * (rank + 1) / S), H, acc);
         #pragma unroll
-        for (int p = 0; p < P; p += 2) {
-            acc[p] = fma(c, denorm_of(r0, H[p]), acc[p]);
-            acc[p + 1] = fma(c, denorm_of(r1, H[p + 1]), acc[p + 1]);
-            if (p + 2 < P) {
-                r0 = step_mod(r0, z2, z2m);
-                r1 = step_mod(r1, z2, z2m);
+        for (int p = 0; p < P; ++p) part[p * kThreads + threadIdx.x] = acc[p];
+        cluster.sync();
+        if (rank == 0) {
+            #pragma unroll
+            for (int p = 0; p < P; ++p) {
+                double v = acc[p];
+                #pragma unroll
+                for (int r = 1; r < S; ++r) v += cluster.map_shared_rank(part, r)[p * kThreads + threadIdx.x];
+                acc[p] = v;
             }
         }
+        cluster.sync();   // peers keep their shared memory until rank 0 has read it
     }
-    const LinParams prm{a.alpha, a.scale, a.K, a.A, a.B, a.C0, a.kappa};
+    if (rank != 0) return;
     double s = 0.0;
     #pragma unroll
     for (int p = 0; p < P; ++p) {
-        double f = outer_fn<OUTER>(acc[p], prm);
-        s += (i0_64 + p < a.end) ? f : 0.0;
-    }
-    s = block_sum(s, sh);
-    if (threadIdx.x == 0) tile_out[tile] = s;
-}
-
-// Plain lattice sum of f = K exp(alpha + sum_j b_j x_j + q_j x_j^2), n <= 2^31.
-// Per point-dim: residue step (2 int ops), xs = denormal * M (exact scale),
-// t = q xs + b, acc += t xs: 3 FP64 ops (FP64-pipe bound).
-template <class Args>
-__global__ void __launch_bounds__(kThreads, 2) k_quad(const __grid_constant__ Args a, uint32_t hmask,
-                                                       double* __restrict__ tile_out) {
-    constexpr int P = kFamPts;
-    __shared__ double sh[8];
-    uint32_t H[P];
-    #pragma unroll
-    for (int k = 0; k < P; ++k) H[k] = (threadIdx.x + k) & hmask;
-    const int64_t tile = blockIdx.x;
-    const uint64_t i0_64 = a.base + (uint64_t)tile * kFamTile + (uint64_t)threadIdx.x * P;
-    const uint32_t i0 = (uint32_t)i0_64;
-    const uint32_t n = a.n;
-    const double M = a.M;
-    double acc[P];
-    #pragma unroll
-    for (int p = 0; p < P; ++p) acc[p] = 0.0;
-    #pragma unroll 1
-    for (int j = 0; j < a.d; ++j) {
-        const double b = a.dims[j].b, q = a.dims[j].q;
-        const uint32_t z = a.dims[j].z, zm = z - n;
-        const uint32_t z2 = a.dims[j].z2, z2m = z2 - n;
-        uint32_t r0 = mulmod_shoup(i0, z, a.dims[j].zs, n);
-        uint32_t r1 = step_mod(r0, z, zm);
-        #pragma unroll
-        for (int p = 0; p < P; p += 2) {
-            const double x0 = denorm_of(r0, H[p]) * M, x1 = denorm_of(r1, H[p + 1]) * M;
-            acc[p] = fma(fma(q, x0, b), x0, acc[p]);
-            acc[p + 1] = fma(fma(q, x1, b), x1, acc[p + 1]);
-            if (p + 2 < P) {
-                r0 = step_mod(r0, z2, z2m);
-                r1 = step_mod(r1, z2, z2m);
-            }
-        }
-    }
-    double s = 0.0;
-    #pragma unroll
-    for (int p = 0; p < P; ++p) {
-        double f = quad_outer(acc[p], a.alpha, a.K);
+        double f = fam_outer<KIND, OUTER>(acc[p], a);
         s += (i0_64 + p < a.end) ? f : 0.0;
     }
     s = block_sum(s, sh);
