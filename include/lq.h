@@ -142,6 +142,9 @@ typedef struct {
     int32_t p_off, p_len;   /* program P (len 0: P=0)                   */
     int32_t p_result;
     int32_t n_slots;
+    int32_t node_off;       /* < 0: midpoint nodes RN((t+0.5)/count); else
+                               nodes[node_off + t] of the nodes table      */
+    int32_t reserved;
 } lq_factor;
 
 /* Partial cluster sums of LQ_NODE_BLOCK-node blocks: part_dev[(f*nblk + b)*2 + {0,1}]
@@ -149,7 +152,8 @@ typedef struct {
  * shard `shard` of `nshards` (blocks [floor(shard*NB_f/nshards),
  * floor((shard+1)*NB_f/nshards)); others left untouched).  nblk = max_f NB_f. */
 int lq_mdi_block_sums(lq_ctx* ctx, const lq_insn* insn, int32_t n_insn, const lq_factor* factors,
-                      int32_t n_factors, int32_t shard, int32_t nshards, double* part_dev);
+                      int32_t n_factors, const double* nodes, int64_t n_nodes, int32_t shard,
+                      int32_t nshards, double* part_dev);
 /* Combine: S_f = fixed tree over blocks; term t = coef_t * prod_{f in term t} S_f
  * * exp(log_extra_t), evaluated in log-polar form (sum log|S|, sum arg S).
  * term_ptr[n_terms+1] indexes term_fac.  out[0]=log|raw|, out[1]=sign(Re raw)
@@ -160,7 +164,7 @@ int lq_mdi_combine(lq_ctx* ctx, const double* part_dev, const lq_factor* factors
                    double* out4);
 /* Single-GPU convenience: block sums + combine. */
 int lq_mdi_sum(lq_ctx* ctx, const lq_insn* insn, int32_t n_insn, const lq_factor* factors,
-               int32_t n_factors, const int32_t* term_ptr, const int32_t* term_fac,
+               int32_t n_factors, const double* nodes, int64_t n_nodes, const int32_t* term_ptr, const int32_t* term_fac,
                const double* coef_re, const double* coef_im, const double* log_extra,
                int32_t n_terms, double* out4);
 

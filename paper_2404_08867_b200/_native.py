@@ -50,7 +50,8 @@ class Integrand(C.Structure):
 
 class Factor(C.Structure):
     _fields_ = [("count", C.c_int32), ("r_off", C.c_int32), ("r_len", C.c_int32), ("r_result", C.c_int32),
-                ("p_off", C.c_int32), ("p_len", C.c_int32), ("p_result", C.c_int32), ("n_slots", C.c_int32)]
+                ("p_off", C.c_int32), ("p_len", C.c_int32), ("p_result", C.c_int32), ("n_slots", C.c_int32),
+                ("node_off", C.c_int32), ("reserved", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -70,9 +71,9 @@ _SIGS = {
     "lq_reduce_sum": [_P, _P, C.c_int64, C.POINTER(C.c_double)],
     "lq_tensor_sum": [_P, C.POINTER(Program), C.c_int32, _P, _P, C.c_int32, C.c_uint64, C.c_uint64,
                       C.POINTER(C.c_double)],
-    "lq_mdi_block_sums": [_P, _P, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, _P],
+    "lq_mdi_block_sums": [_P, _P, C.c_int32, _P, C.c_int32, _P, C.c_int64, C.c_int32, C.c_int32, _P],
     "lq_mdi_combine": [_P, _P, _P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, C.c_int32, _P],
-    "lq_mdi_sum": [_P, _P, C.c_int32, _P, C.c_int32, _P, _P, _P, _P, _P, C.c_int32, _P],
+    "lq_mdi_sum": [_P, _P, C.c_int32, _P, C.c_int32, _P, C.c_int64, _P, _P, _P, _P, _P, C.c_int32, _P],
     "lq_mdi_expabs": [_P, C.c_int32, _P, _P, C.c_double, _P, _P, C.c_int32, C.c_double, _P, _P],
     "lq_fp64_peak": [_P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_float)],
     "lq_bprod_sum": [_P, C.c_int32, C.c_int32, C.c_uint64, _P, _P, C.c_double, C.c_uint64, C.c_uint64,

@@ -32,7 +32,7 @@ int fail(int code, const char* fmt, ...) {
                         __FILE__, __LINE__);                                          \
     } while (0)
 
-enum Buf { B_TAB = 0, B_TILES, B_RED0, B_RED1, B_OUT, B_PROG, B_AUX0, B_AUX1, B_AUX2, B_AUX3, B_PART, B_FAC, B_NBUF };
+enum Buf { B_TAB = 0, B_TILES, B_RED0, B_RED1, B_OUT, B_PROG, B_AUX0, B_AUX1, B_AUX2, B_AUX3, B_PART, B_FAC, B_NODES, B_NBUF };
 
 }  // namespace
 
@@ -336,7 +336,7 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
     }
     // generic bytecode (any family falls back here for n > 2^31)
     const lq_program* pg = &f->prog;
-    if (f->kind != LQ_FAM_PROGRAM || !pg->insn || pg->n_insn < 1)
+    if (!pg->insn || pg->n_insn < 1)
         return fail(LQ_ERR_UNSUPPORTED, "integrand needs a bytecode program for n=%llu", (unsigned long long)n);
     const int ns = pick_slots(pg->n_slots);
     if (ns < 0) return fail(LQ_ERR_UNSUPPORTED, "program needs %d slots (max %d)", pg->n_slots, LQ_MAX_SLOTS);
@@ -641,23 +641,27 @@ static int mdi_validate(const lq_insn* insn, int32_t n_insn, const lq_factor* fa
     return LQ_OK;
 }
 
-int lq_mdi_block_sums(lq_ctx* c, const lq_insn* insn, int32_t n_insn, const lq_factor* fac, int32_t nf, int32_t shard,
-                      int32_t nshards, double* part_dev) {
+int lq_mdi_block_sums(lq_ctx* c, const lq_insn* insn, int32_t n_insn, const lq_factor* fac, int32_t nf,
+                      const double* nodes, int64_t n_nodes, int32_t shard, int32_t nshards, double* part_dev) {
     int rc = set_dev(c);
     if (rc) return rc;
     int nblk, ns;
     if ((rc = mdi_validate(insn, n_insn, fac, nf, &nblk, &ns))) return rc;
     if (nshards < 1 || shard < 0 || shard >= nshards) return fail(LQ_ERR_VALUE, "bad shard %d of %d", shard, nshards);
     if (nf == 0) return LQ_OK;
-    void *dp, *dfac;
+    for (int f = 0; f < nf; ++f)
+        if (fac[f].node_off >= 0 && (!nodes || (int64_t)fac[f].node_off + fac[f].count > n_nodes))
+            return fail(LQ_ERR_VALUE, "factor %d node table out of range", f);
+    void *dp, *dfac, *dn = nullptr;
     if ((rc = upload(c, B_PROG, insn, sizeof(lq_insn) * std::max(n_insn, 1), &dp))) return rc;
     if ((rc = upload(c, B_AUX0, fac, sizeof(lq_factor) * nf, &dfac))) return rc;
+    if (nodes && n_nodes > 0 && (rc = upload(c, B_NODES, nodes, sizeof(double) * n_nodes, &dn))) return rc;
     dim3 g((unsigned)nf, (unsigned)nblk);
     t_begin(c);
     if (ns == 32)
-        lq::k_mdi_blocks<32><<<g, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, (const lq_factor*)dfac, nblk, shard, nshards, part_dev);
+        lq::k_mdi_blocks<32><<<g, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, (const lq_factor*)dfac, (const double*)dn, nblk, shard, nshards, part_dev);
     else
-        lq::k_mdi_blocks<LQ_MAX_SLOTS><<<g, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, (const lq_factor*)dfac, nblk, shard, nshards, part_dev);
+        lq::k_mdi_blocks<LQ_MAX_SLOTS><<<g, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, (const lq_factor*)dfac, (const double*)dn, nblk, shard, nshards, part_dev);
     t_end(c);
     CK(cudaGetLastError());
     return LQ_OK;
@@ -700,7 +704,7 @@ int lq_mdi_combine(lq_ctx* c, const double* part_dev, const lq_factor* fac, int3
 }
 
 int lq_mdi_sum(lq_ctx* c, const lq_insn* insn, int32_t n_insn, const lq_factor* fac, int32_t nf,
-               const int32_t* term_ptr, const int32_t* term_fac, const double* coef_re, const double* coef_im,
+               const double* nodes, int64_t n_nodes, const int32_t* term_ptr, const int32_t* term_fac, const double* coef_re, const double* coef_im,
                const double* log_extra, int32_t n_terms, double* out4) {
     int rc = set_dev(c);
     if (rc) return rc;
@@ -708,7 +712,7 @@ int lq_mdi_sum(lq_ctx* c, const lq_insn* insn, int32_t n_insn, const lq_factor* 
     if ((rc = mdi_validate(insn, n_insn, fac, nf, &nblk, &ns))) return rc;
     void* part;
     if ((rc = dev_buf(c, B_PART, sizeof(double) * 2 * (size_t)std::max(nf, 1) * nblk, &part))) return rc;
-    if (nf > 0 && (rc = lq_mdi_block_sums(c, insn, n_insn, fac, nf, 0, 1, (double*)part))) return rc;
+    if (nf > 0 && (rc = lq_mdi_block_sums(c, insn, n_insn, fac, nf, nodes, n_nodes, 0, 1, (double*)part))) return rc;
     return lq_mdi_combine(c, (const double*)part, fac, nf, nblk, term_ptr, term_fac, coef_re, coef_im, log_extra, n_terms, out4);
 }
 

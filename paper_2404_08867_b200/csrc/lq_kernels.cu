@@ -323,7 +323,8 @@ struct UnivSrc {
 // on the block's 256 midpoint nodes and writes the (re, im) block sums.
 template <int NS>
 __global__ void __launch_bounds__(kThreads) k_mdi_blocks(const lq_insn* __restrict__ insn,
-                                                         const lq_factor* __restrict__ fac, int nblk,
+                                                         const lq_factor* __restrict__ fac,
+                                                         const double* __restrict__ nodes, int nblk,
                                                          int shard, int nshards, double* __restrict__ part) {
     __shared__ double sh[8];
     double slot[NS];
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(kThreads) k_mdi_blocks(const lq_insn* __restri
     double re = 0.0, im = 0.0;
     if (t < F.count) {
         const double cd = (double)F.count;
-        UnivSrc src{exact_div((double)t + 0.5, cd, 1.0 / cd)};
+        UnivSrc src{F.node_off < 0 ? exact_div((double)t + 0.5, cd, 1.0 / cd) : nodes[F.node_off + t]};
         double R = F.r_len ? run_program<NS>(insn + F.r_off, F.r_len, F.r_result, src, slot) : 1.0;
         if (F.p_len) {
             double P = run_program<NS>(insn + F.p_off, F.p_len, F.p_result, src, slot);

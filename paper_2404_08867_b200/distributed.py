@@ -119,7 +119,7 @@ def mdi_lr(f, d, a, n, cfg=None, rule=None, with_report=False, group=None):
                for k in range(plan.n_factors))
     part = torch.zeros(plan.n_factors * nblk * 2, dtype=torch.float64, device="cuda")
     N.check(h.lq_mdi_block_sums(ctx, N.as_ptr(plan.insn), plan.n_insn, C.cast(plan.factors, C.c_void_p),
-                                plan.n_factors, rank, size, C.c_void_p(part.data_ptr())))
+                                plan.n_factors, None, 0, rank, size, C.c_void_p(part.data_ptr())))
     exchange_disjoint(part, group)
     out = np.zeros(4)
     N.check(h.lq_mdi_combine(ctx, C.c_void_p(part.data_ptr()), C.cast(plan.factors, C.c_void_p), plan.n_factors,

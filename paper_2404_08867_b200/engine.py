@@ -132,7 +132,7 @@ def tensor_sum(g, grids, s_begin=0, s_end=None):
 class SeparablePlan:
     """Factor table + term structure of a separable integrand on given axis counts."""
 
-    def __init__(self, e, counts):
+    def __init__(self, e, counts, nodes=None):
         terms = separate(e)
         self.ok = terms is not None
         if not self.ok:
@@ -143,6 +143,14 @@ class SeparablePlan:
         off = 0
         max_slots = 1
         fac_index = {}
+        if nodes is not None:
+            node_offs = np.concatenate([[0], np.cumsum([len(nd) for nd in nodes])]).astype(np.int64)
+            if node_offs[-1] >= 2**31:
+                raise ValueError("node table too large")
+            self.nodes = np.ascontiguousarray(np.concatenate([np.asarray(nd, dtype=np.float64) for nd in nodes]))
+        else:
+            node_offs = None
+            self.nodes = None
         for t in terms:
             extra = 0.0
             for ax in range(1, d + 1):
@@ -155,6 +163,7 @@ class SeparablePlan:
                 if idx is None:
                     rec = N.Factor()
                     rec.count = int(counts[ax - 1])
+                    rec.node_off = -1 if node_offs is None else int(node_offs[ax - 1])
                     for which, sub in (("r", fc.R), ("p", fc.P)):
                         if sub is None:
                             setattr(rec, f"{which}_off", 0)
@@ -192,16 +201,20 @@ class SeparablePlan:
         self.n_terms = len(terms)
 
 
-def separable_plan(g, counts):
+def separable_plan(g, counts, nodes=None):
+    """Factorised plan on midpoint nodes (nodes=None) or explicit per-axis node tuples."""
     e = as_expr(g)
-    return _sep_cache.get_or((e, tuple(counts)), lambda: SeparablePlan(e, counts))
+    key = (e, tuple(counts), None if nodes is None else tuple(tuple(nd) for nd in nodes))
+    return _sep_cache.get_or(key, lambda: SeparablePlan(e, counts, nodes))
 
 
 def mdi_separable_sum(plan):
     """(log|raw|, sign, raw, im) of the full-grid sum via per-direction cluster sums."""
     out = np.zeros(4)
+    n_nodes = 0 if plan.nodes is None else len(plan.nodes)
     N.check(N.lib().lq_mdi_sum(N.ctx(), N.as_ptr(plan.insn), plan.n_insn, C.cast(plan.factors, C.c_void_p),
-                               plan.n_factors, N.as_ptr(plan.term_ptr), N.as_ptr(plan.term_fac),
+                               plan.n_factors, N.as_ptr(plan.nodes), n_nodes,
+                               N.as_ptr(plan.term_ptr), N.as_ptr(plan.term_fac),
                                N.as_ptr(plan.coef_re), N.as_ptr(plan.coef_im), N.as_ptr(plan.log_extra),
                                plan.n_terms, N.as_ptr(out)))
     return float(out[0]), float(out[1]), float(out[2]), float(out[3])

@@ -157,9 +157,9 @@ def mdi_sum(g, grids, cfg=None):
                          log_raw=math.log(abs(value)) if value else -math.inf,
                          sign=math.copysign(1.0, value) if value else 0.0, method="constant", clusters=0)
 
-    plan = engine.separable_plan(e, counts)
+    midpoint = getattr(grids, "midpoint", False)
+    plan = engine.separable_plan(e, counts, None if midpoint else grids.nodes)
     usable = plan.ok and (plan.n_factors + plan.n_terms) <= cfg.budget
-    usable = usable and getattr(grids, "midpoint", False)
     total = math.prod(counts)
     if (not usable and total > cfg.direct_cap and getattr(grids, "midpoint", False)
             and cfg.fallback == "numeric"):

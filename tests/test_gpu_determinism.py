@@ -92,13 +92,13 @@ def test_mdi_sharded_blocks_bit_identical(env):
     nblk = 4
     ref = np.zeros(4)
     N.check(h.lq_mdi_sum(ctx, N.as_ptr(plan.insn), plan.n_insn, C.cast(plan.factors, C.c_void_p), plan.n_factors,
-                         N.as_ptr(plan.term_ptr), N.as_ptr(plan.term_fac), N.as_ptr(plan.coef_re),
+                         None, 0, N.as_ptr(plan.term_ptr), N.as_ptr(plan.term_fac), N.as_ptr(plan.coef_re),
                          N.as_ptr(plan.coef_im), N.as_ptr(plan.log_extra), plan.n_terms, N.as_ptr(ref)))
     for shards in (2, 3, 4):
         part = torch.zeros(plan.n_factors * nblk * 2, dtype=torch.float64, device="cuda")
         for r in range(shards):
             N.check(h.lq_mdi_block_sums(ctx, N.as_ptr(plan.insn), plan.n_insn, C.cast(plan.factors, C.c_void_p),
-                                        plan.n_factors, r, shards, C.c_void_p(part.data_ptr())))
+                                        plan.n_factors, None, 0, r, shards, C.c_void_p(part.data_ptr())))
         out = np.zeros(4)
         N.check(h.lq_mdi_combine(ctx, C.c_void_p(part.data_ptr()), C.cast(plan.factors, C.c_void_p),
                                  plan.n_factors, nblk, N.as_ptr(plan.term_ptr), N.as_ptr(plan.term_fac),
