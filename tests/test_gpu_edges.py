@@ -78,7 +78,9 @@ def test_wide_modulus_points_and_sum(lq):
     f = lq.parse("cos(x[1] + 2*x[2] - x[3])", 3)
     pi = engine.plain_integrand(f, 3)
     s = engine.lattice_sum(pi, n, rule.z_reduced_array(), 2**35, 2**35 + 8192)
-    pts = orc.points_block(n, list(z), 2**35, 2**35 + 8192)
+    # exact residues in Python ints: numpy's int64 j*z would wrap here (as the
+    # reference's points_block silently does for n past ~3e9)
+    pts = np.array([[float((i * zj) % n) / n for zj in z] for i in range(2**35, 2**35 + 8192)])
     ref = float(np.sum(np.cos(pts[:, 0] + 2 * pts[:, 1] - pts[:, 2])))
     assert abs(s - ref) <= 1e-12 * abs(ref)
 
