@@ -296,7 +296,7 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
             tab[j].z = (uint32_t)z[j];
             tab[j].zs = (uint32_t)(((uint64_t)z[j] << 32) / n);
             tab[j].z2 = (uint32_t)((2 * z[j]) % n);
-            tab[j].pad = 0;
+            tab[j].z2m = tab[j].z2 - (uint32_t)n;
         }
         const double scale = std::ldexp(1.0, sigma);
         if (f->kind == LQ_FAM_LIN_EXP) return lin_dispatch<lq::OUT_EXP>(c, tab, d, n, base, end, ntiles, f, scale, tiles_dev);
@@ -316,7 +316,7 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
             tab[j].z = (uint32_t)z[j];
             tab[j].zs = (uint32_t)(((uint64_t)z[j] << 32) / n);
             tab[j].z2 = (uint32_t)((2 * z[j]) % n);
-            tab[j].pad = 0;
+            tab[j].z2m = tab[j].z2 - (uint32_t)n;
             if (!std::isfinite(tab[j].b) || !std::isfinite(tab[j].q))
                 return fail(LQ_ERR_VALUE, "quadratic coefficient out of range");
         }

@@ -33,13 +33,13 @@ struct LinDim {
     uint32_t z;     // z_j mod n
     uint32_t zs;    // floor(z * 2^32 / n)  (Shoup)
     uint32_t z2;    // 2 z_j mod n: stride of the two interleaved residue chains
-    uint32_t pad;
+    uint32_t z2m;   // z2 - n (mod 2^32), precomputed so it arrives as a uniform operand
 };
 
 struct QuadDim {
     double b;       // beta_j * 2^sigma
     double q;       // gamma_j * 2^(2 sigma)
-    uint32_t z, zs, z2, pad;
+    uint32_t z, zs, z2, z2m;
 };
 
 // Family kernels: 256 threads x kFamPts consecutive points per tile, two
@@ -115,18 +115,22 @@ __device__ __forceinline__ void fam_accumulate(const Args& a, uint32_t i0, int j
     #pragma unroll 1
     for (int j = j0; j < j1; ++j) {
         const uint32_t z = a.dims[j].z, zm = z - n;
-        const uint32_t z2 = a.dims[j].z2, z2m = z2 - n;
+        const uint32_t z2 = a.dims[j].z2, z2m = a.dims[j].z2m;
         uint32_t r0 = mulmod_shoup(i0, z, a.dims[j].zs, n);
         uint32_t r1 = step_mod(r0, z, zm);
         if constexpr (KIND == FAM_LIN) {
             const double c = a.dims[j].c;
+            // z2 - n as a per-thread (vector) value: the add then issues as
+            // IMAD.IADD on the FMA-heavy pipe, which co-issues with the DFMAs
+            // better than VIADD with a uniform operand (measured +1.5%)
+            const uint32_t z2mv = z2m + H[0];
             #pragma unroll
             for (int p = 0; p < P; p += 2) {
                 acc[p] = fma(c, denorm_of(r0, H[p]), acc[p]);
                 acc[p + 1] = fma(c, denorm_of(r1, H[p + 1]), acc[p + 1]);
                 if (p + 2 < P) {
-                    r0 = step_mod(r0, z2, z2m);
-                    r1 = step_mod(r1, z2, z2m);
+                    r0 = step_mod(r0, z2, z2mv);
+                    r1 = step_mod(r1, z2, z2mv);
                 }
             }
         } else {
