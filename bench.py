@@ -291,16 +291,19 @@ def main():
 
     mdi = {}
     if not args.no_mdi and world == 1:
-        for cid in (2, 4):
+        for cid in (1, 2, 4, 5):
             mc = make_config(cid)
             g = lq.parse(mc.text, mc.d)
-            lq.mdi_lr(g, mc.d, mc.mdi_a, mc.mdi_n)
+            mcfg = lq.MdiConfig(direct_cap=10**10) if cid == 1 else None   # as the reference needs (a^3 > 1e8)
+            lq.mdi_lr(g, mc.d, mc.mdi_a, mc.mdi_n, cfg=mcfg)
             ts = []
             for _ in range(5):
                 t0 = time.perf_counter()
-                v = lq.mdi_lr(g, mc.d, mc.mdi_a, mc.mdi_n)
+                v, rep = lq.mdi_lr(g, mc.d, mc.mdi_a, mc.mdi_n, cfg=mcfg, with_report=True)
                 ts.append(time.perf_counter() - t0)
             mdi[f"cfg{cid}_ms"] = min(ts) * 1e3
+            mdi[f"cfg{cid}_mean"] = rep.mean
+            mdi[f"cfg{cid}_method"] = rep.method
 
     line = {
         "metric": "lattice f-evals/sec (fp64)", "value": value, "unit": "f-evals/s", "n_gpus": world,
