@@ -51,6 +51,7 @@ extern "C" {
 #define LQ_MAX_SLOTS 512      /* bytecode live-slot limit                      */
 
 typedef struct lq_ctx lq_ctx;
+typedef struct lq_jit lq_jit;   /* an NVRTC-compiled integrand module (lq_jit_create) */
 
 /* Bytecode instruction; slot[a] <- op(...).  Ops (see lower.py):
  * 0 CONST c | 1 VAR x[b] | 2 ACC_INIT c | 3 ACC_ADD += c*slot[b] |
@@ -67,6 +68,7 @@ typedef struct {
     int32_t n_slots;
     int32_t result;        /* slot holding the value */
     int32_t n_vars;        /* variables referenced: 0..n_vars-1 */
+    lq_jit* jit;           /* optional: compiled straight-line version (NULL: interpret) */
 } lq_program;
 
 enum {
@@ -197,6 +199,15 @@ int lq_cbc_construct(lq_ctx* ctx, uint64_t n, int32_t d, const double* gamma, do
  * z = (1, a, ..., a^(d-1)).                                                 */
 int lq_korobov_values(lq_ctx* ctx, uint64_t n, int32_t d, const double* gamma, double beta,
                       const int64_t* candidates, int64_t n_candidates, double* sums_out);
+
+/* ---- JIT: the lowering step before the path ------
+ * Compile CUDA source that defines extern "C" kernels lq_jit_lattice and/or
+ * lq_jit_tensor (generated from an expression by paper_2404_08867_b200/jit.py)
+ * with NVRTC for sm_100a.  Attach the handle to lq_program.jit: lattice and
+ * tensor sums then launch the compiled kernel instead of the interpreter,
+ * with the same tiles and reduction tree.  NVRTC is loaded with dlopen.     */
+int lq_jit_create(const char* source, const char* name, lq_jit** out, char* log, int64_t log_cap);
+int lq_jit_destroy(lq_jit* jit);
 
 /* ---- FP64 roofline probe: DFMA chains on every SM; returns TFLOP/s ----- */
 int lq_fp64_peak(lq_ctx* ctx, int32_t iters, double* tflops, float* ms);

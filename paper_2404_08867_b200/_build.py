@@ -40,7 +40,7 @@ def build_native(force=False, verbose=False):
     if not force and not _stale(LIB, _sources()):
         return LIB
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *NVCC_FLAGS, "-o", tmp, os.path.join(CSRC, "lq_api.cu")]
+    cmd = [NVCC, *NVCC_FLAGS, "-o", tmp, os.path.join(CSRC, "lq_api.cu"), os.path.join(CSRC, "lq_jit.cu"), "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

@@ -39,7 +39,7 @@ assert C.sizeof(Insn) == INSN_DTYPE.itemsize
 
 class Program(C.Structure):
     _fields_ = [("insn", C.c_void_p), ("n_insn", C.c_int32), ("n_slots", C.c_int32),
-                ("result", C.c_int32), ("n_vars", C.c_int32)]
+                ("result", C.c_int32), ("n_vars", C.c_int32), ("jit", C.c_void_p)]
 
 
 class Integrand(C.Structure):
@@ -80,6 +80,8 @@ _SIGS = {
                      C.POINTER(C.c_double)],
     "lq_cbc_construct": [_P, C.c_uint64, C.c_int32, _P, C.c_double, _P, C.c_int64, _P],
     "lq_korobov_values": [_P, C.c_uint64, C.c_int32, _P, C.c_double, _P, C.c_int64, _P],
+    "lq_jit_create": [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_int64],
+    "lq_jit_destroy": [_P],
 }
 
 _lib = None

@@ -36,6 +36,19 @@ enum Buf { B_TAB = 0, B_TILES, B_RED0, B_RED1, B_OUT, B_PROG, B_AUX0, B_AUX1, B_
 
 }  // namespace
 
+int lq_internal_fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+cudaKernel_t lq_jit_lattice_kernel(const lq_jit* j);
+cudaKernel_t lq_jit_tensor_kernel(const lq_jit* j);
+
 struct lq_ctx {
     int device = 0;
     int sm_count = 0;
@@ -356,6 +369,15 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
         if ((rc = upload(c, B_TAB, zz.data(), zz.size() * 4, &dz))) return rc;
     }
     const double n_d = (double)n, inv_n = 1.0 / n_d;
+    if (cudaKernel_t jk = lq_jit_lattice_kernel(pg->jit)) {
+        const void* ztab = dz;
+        int wide_i = wide ? 1 : 0;
+        void* args[] = {(void*)&ztab, (void*)&n, (void*)&n_d, (void*)&inv_n, (void*)&base, (void*)&end, (void*)&wide_i, (void*)&tiles_dev};
+        t_begin(c);
+        CK(cudaLaunchKernel((const void*)jk, dim3((unsigned)ntiles), dim3(lq::kThreads), args, 0, c->stream));
+        t_end(c);
+        return LQ_OK;
+    }
     const void* kern = wide ? (ns == 32 ? (const void*)lq::k_prog_lattice<32, true> : (const void*)lq::k_prog_lattice<LQ_MAX_SLOTS, true>)
                             : (ns == 32 ? (const void*)lq::k_prog_lattice<32, false> : (const void*)lq::k_prog_lattice<LQ_MAX_SLOTS, false>);
     int grid = grid_for(c, kern, ntiles);
@@ -612,7 +634,12 @@ int lq_tensor_sum(lq_ctx* c, const lq_program* pg, int32_t d, const int64_t* cou
     const void* kern = ns == 32 ? (const void*)lq::k_prog_tensor<32> : (const void*)lq::k_prog_tensor<LQ_MAX_SLOTS>;
     int grid = grid_for(c, kern, ntiles);
     t_begin(c);
-    if (ns == 32)
+    if (cudaKernel_t jk = lq_jit_tensor_kernel(pg->jit)) {
+        const void *pc = dc, *po = doff, *pn = dn;
+        void* tp = tiles;
+        void* args[] = {(void*)&d, (void*)&pc, (void*)&po, (void*)&pn, (void*)&s_begin, (void*)&s_end, (void*)&tp};
+        CK(cudaLaunchKernel((const void*)jk, dim3((unsigned)ntiles), dim3(lq::kThreads), args, 0, c->stream));
+    } else if (ns == 32)
         lq::k_prog_tensor<32><<<grid, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, pg->n_insn, pg->result, d, (const int64_t*)dc, (const int64_t*)doff, (const double*)dn, s_begin, s_end, ntiles, (double*)tiles);
     else
         lq::k_prog_tensor<LQ_MAX_SLOTS><<<grid, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, pg->n_insn, pg->result, d, (const int64_t*)dc, (const int64_t*)doff, (const double*)dn, s_begin, s_end, ntiles, (double*)tiles);

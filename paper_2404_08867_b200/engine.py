@@ -92,9 +92,21 @@ def plain_integrand(f, d, force_program=False):
     return _plain_cache.get_or((e, d, force_program), make)
 
 
+def attach_jit(pi, n, npts):
+    """Give an interpreted plain-sum integrand its NVRTC-compiled kernel when
+    the work is large enough to pay for the compile (jit.py)."""
+    from . import jit
+    interpreted = pi.family is None or n > 2**31
+    if interpreted and not pi.struct.prog.jit and jit.jit_wanted(npts * max(len(pi.program), 1)):
+        h = jit.compile_expr(pi.expr)
+        if h:
+            pi.struct.prog.jit = h
+
+
 def lattice_sum(pi, n, z_reduced, i_begin=0, i_end=None):
     """sum_{i in [i_begin, i_end)} f(x_i) on the GPU (not divided by n)."""
     i_end = n if i_end is None else i_end
+    attach_jit(pi, n, max(0, int(i_end) - int(i_begin)))
     out = C.c_double()
     N.check(N.lib().lq_lattice_sum(N.ctx(), C.byref(pi.struct), n, N.as_ptr(z_reduced),
                                    int(i_begin), int(i_end), C.byref(out)))
@@ -114,7 +126,11 @@ def tensor_sum(g, grids, s_begin=0, s_end=None):
     total = grids.total
     s_end = total if s_end is None else s_end
     ins = np.ascontiguousarray(prog.insn)
-    p = N.Program(ins.ctypes.data, len(ins), prog.n_slots, prog.result, prog.n_vars)
+    from . import jit
+    jh = None
+    if jit.jit_wanted((int(s_end) - int(s_begin)) * max(len(ins), 1)) and d <= 128:
+        jh = jit.compile_expr(as_expr(g), n_axes=max(d, 1))
+    p = N.Program(ins.ctypes.data, len(ins), prog.n_slots, prog.result, prog.n_vars, jh)
     if getattr(grids, "midpoint", False):
         nodes, mid = None, 1
     else:

@@ -1,0 +1,226 @@
+"""Expression -> CUDA source for NVRTC (the lowering step before the path,
+SURVEY.md §8(f) item 1).
+
+An integrand outside the closed families becomes straight-line device code in
+the reference's evaluation order (sums ``v = const; v = v + c*t``, products
+``v = coeff; v = v*f``, /root/reference/pkg/src/latquad/exprcore.py:442-480),
+with every constant as an exact hex literal and every coordinate fetched once
+per point.  liblq compiles it for sm_100a (``lq_jit_create``) and launches it
+with the same tiles and fixed reduction tree as the bytecode interpreter it
+replaces, so the two agree to rounding and the JIT is purely a speed-up.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from . import _native as N
+from .expr import topo
+
+__all__ = ["source_for", "compile_expr", "jit_wanted", "JIT_THRESHOLD"]
+
+_PRELUDE = r"""
+typedef unsigned int u32;
+typedef unsigned long long u64;
+typedef long long i64;
+struct LqZZ { u32 z, zs; };
+
+__device__ __forceinline__ double lq_exact_div(double a, double b, double inv) {
+    double q = a * inv;
+    double e = fma(-q, b, a);
+    return fma(e, inv, q);
+}
+__device__ __forceinline__ u32 lq_shoup(u32 x, u32 z, u32 zs, u32 n) {
+    u32 q = __umulhi(x, zs);
+    u32 r = x * z - q * n;
+    u32 t = r - n;
+    return t < r ? t : r;
+}
+__device__ __forceinline__ u64 lq_mulmod64(u64 a, u64 b, u64 n, double ninv) {
+    u64 lo = a * b;
+    double qd = (double)a * (double)b * ninv;
+    u64 q = qd <= 0.0 ? 0ull : (u64)qd;
+    i64 r = (i64)(lo - q * n);
+    while (r < 0) r += (i64)n;
+    while (r >= (i64)n) r -= (i64)n;
+    return (u64)r;
+}
+__device__ __forceinline__ double lq_block_sum(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < 8 ? sh[lane] : 0.0;
+        for (int o = 4; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    return v;
+}
+__device__ __forceinline__ double lq_ipow(double b, int k) { return k == 2 ? b * b : pow(b, (double)k); }
+
+struct LqLat32 {
+    u32 i, n; double nd, inv; const LqZZ* zz;
+    __device__ __forceinline__ double operator()(int j) const {
+        const LqZZ t = zz[j];
+        return lq_exact_div((double)lq_shoup(i, t.z, t.zs, n), nd, inv);
+    }
+};
+struct LqLat64 {
+    u64 i, n; double nd, inv; const u64* z;
+    __device__ __forceinline__ double operator()(int j) const {
+        return lq_exact_div((double)lq_mulmod64(i, __ldg(z + j), n, inv), nd, inv);
+    }
+};
+struct LqTen {
+    const double* nodes; const i64* off; const u32* digit;
+    __device__ __forceinline__ double operator()(int j) const { return __ldg(nodes + off[j] + digit[j]); }
+};
+"""
+
+_KERNELS = r"""
+// plain lattice sum: 256 threads x 16 consecutive points per tile (the
+// interpreter's tiling, so partials line up with k_prog_lattice)
+extern "C" __global__ void __launch_bounds__(256) lq_jit_lattice(const void* zt, u64 n, double nd, double inv,
+                                                                u64 base, u64 end, int wide, double* tile_out) {
+    __shared__ double sh[8];
+    const u64 i0 = base + (u64)blockIdx.x * 4096ull + (u64)threadIdx.x * 16ull;
+    double s = 0.0;
+    for (int p = 0; p < 16; ++p) {
+        const u64 i = i0 + p;
+        if (i < end) {
+            if (wide) {
+                LqLat64 x{i % n, n, nd, inv, (const u64*)zt};
+                s += lq_f(x);
+            } else {
+                LqLat32 x{(u32)i, (u32)n, nd, inv, (const LqZZ*)zt};
+                s += lq_f(x);
+            }
+        }
+    }
+    s = lq_block_sum(s, sh);
+    if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
+}
+
+// direct tensor-grid sum, flat index first axis fastest (odometer per thread)
+extern "C" __global__ void __launch_bounds__(256) lq_jit_tensor(int d, const i64* counts, const i64* off,
+                                                               const double* nodes, u64 base, u64 end,
+                                                               double* tile_out) {
+    __shared__ double sh[8];
+    u32 digit[LQ_AXES];
+    const u64 s0 = base + (u64)blockIdx.x * 4096ull + (u64)threadIdx.x * 16ull;
+    u64 rem = s0;
+    for (int k = 0; k < d; ++k) {
+        const u64 c = (u64)counts[k];
+        digit[k] = (u32)(rem % c);
+        rem /= c;
+    }
+    LqTen x{nodes, off, digit};
+    double s = 0.0;
+    for (int p = 0; p < 16; ++p) {
+        if (s0 + p < end) s += lq_f(x);
+        for (int k = 0; k < d; ++k) {
+            if (++digit[k] < (u64)counts[k]) break;
+            digit[k] = 0;
+        }
+    }
+    s = lq_block_sum(s, sh);
+    if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
+}
+"""
+
+
+def _lit(v):
+    v = float(v)
+    if v != v or v in (float("inf"), float("-inf")):
+        return {"inf": "(1.0/0.0)", "-inf": "(-1.0/0.0)"}.get(repr(v), "(0.0/0.0)")
+    return v.hex()
+
+
+def source_for(e, var_map=None, n_axes=1):
+    """CUDA source of an expression: ``lq_f(x)`` plus both kernel bodies."""
+    vm = var_map if var_map is not None else (lambda j: j - 1)
+    names = {}
+    lines = []
+    for k, node in enumerate(topo(e)):
+        t = f"t{k}"
+        names[node] = t
+        op = node.op
+        if op == "const":
+            lines.append(f"    const double {t} = {_lit(node.val)};")
+        elif op == "var":
+            lines.append(f"    const double {t} = x({vm(node.idx)});")
+        elif op == "add":
+            lines.append(f"    double {t} = {_lit(node.val)};")
+            for c, ch in node.terms:
+                lines.append(f"    {t} = {t} + {_lit(c)} * {names[ch]};")
+        elif op == "mul":
+            lines.append(f"    double {t} = {_lit(node.val)};")
+            for ch in node.args:
+                lines.append(f"    {t} = {t} * {names[ch]};")
+        elif op == "pow":
+            b = names[node.args[0]]
+            if node.idx >= 2:
+                lines.append(f"    const double {t} = lq_ipow({b}, {node.idx});")
+            else:
+                k_ = -node.idx
+                inner = b if k_ == 1 else f"lq_ipow({b}, {k_})"
+                lines.append(f"    const double {t} = 1.0 / ({inner});")
+        else:
+            fn = {"exp": "exp", "sin": "sin", "cos": "cos", "abs": "fabs"}[op]
+            lines.append(f"    const double {t} = {fn}({names[node.args[0]]});")
+    body = "\n".join(lines)
+    fdef = (f"template <class X> __device__ __forceinline__ double lq_f(const X& x) {{\n{body}\n"
+            f"    return {names[e]};\n}}\n")
+    return _PRELUDE + fdef + f"#define LQ_AXES {max(1, int(n_axes))}\n" + _KERNELS
+
+
+class _Module:
+    def __init__(self, src):
+        log = C.create_string_buffer(4096)
+        h = C.c_void_p()
+        N.check(N.lib().lq_jit_create(src.encode(), b"lq_jit.cu", C.byref(h), log, len(log)))
+        self.handle = h
+
+    def __del__(self):
+        try:
+            if self.handle:
+                N.lib().lq_jit_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_cache = {}
+_lock = threading.Lock()
+
+
+# interpreter instruction-points above which compiling pays for itself
+# (NVRTC takes ~0.3 s per expression; the interpreter runs ~2e9 insn-points/s)
+JIT_THRESHOLD = 1e9
+
+
+def jit_wanted(work):
+    """LQ_JIT=0 never, =always for any size, default: only past JIT_THRESHOLD."""
+    mode = os.environ.get("LQ_JIT", "auto")
+    if mode == "0":
+        return False
+    return mode == "always" or work >= JIT_THRESHOLD
+
+
+def compile_expr(e, n_axes=1):
+    """Compiled module handle (int) for e, cached per process, or None if NVRTC
+    is unavailable (the bytecode interpreter then runs -- still on the GPU)."""
+    key = (e, int(n_axes))
+    with _lock:
+        mod = _cache.get(key)
+        if mod is None:
+            try:
+                mod = _Module(source_for(e, n_axes=n_axes))
+            except N.NativeUnavailable:
+                mod = False
+            except NotImplementedError:
+                mod = False
+            _cache[key] = mod
+    return mod.handle.value if mod else None

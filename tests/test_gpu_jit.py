@@ -1,0 +1,77 @@
+"""GPU: NVRTC-compiled integrands (jit.py) agree with the bytecode
+interpreter and with the reference's golden values."""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import unhex
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lq():
+    import paper_2404_08867_b200 as m
+    return m
+
+
+def _rule(lq, c):
+    return lq.LatticeRule(int(c["n"]), tuple(int(v) for v in c["z"]))
+
+
+def test_jit_plain_sums_match_interpreter_and_reference(lq, golden, monkeypatch):
+    from paper_2404_08867_b200 import engine
+    checked = 0
+    for case in golden["slr"]:
+        if case["value"] is None or case["tag"].startswith("cfg") or case["tag"] == "const_2p5":
+            continue
+        d = case["d"]
+        f = lq.parse(case["text"], d)
+        rule = _rule(lq, case)
+        z = rule.z_reduced_array()
+        monkeypatch.setenv("LQ_JIT", "0")
+        interp = engine.plain_integrand(f, d, force_program=True)
+        a = engine.lattice_sum(interp, rule.n, z)
+        assert not interp.struct.prog.jit
+        monkeypatch.setenv("LQ_JIT", "always")
+        engine._plain_cache.clear()
+        jitted = engine.plain_integrand(f, d, force_program=True)
+        b = engine.lattice_sum(jitted, rule.n, z)
+        assert jitted.struct.prog.jit, case["tag"]
+        want = unhex(case["value"]) * rule.n
+        assert abs(a - b) <= 1e-13 * max(abs(a), 1.0), case["tag"]
+        assert abs(b - want) <= 1e-10 * max(abs(want), 1e-3 * rule.n), case["tag"]
+        checked += 1
+    assert checked >= 12
+
+
+def test_jit_tensor_sums_match_reference(lq, golden, monkeypatch):
+    monkeypatch.setenv("LQ_JIT", "always")
+    checked = 0
+    for case in golden["mdi"]:
+        if "implr" not in case or not case["tag"].startswith(("acc01_expxy", "acc01_invpow", "acc01_sinsq")):
+            continue
+        f = lq.parse(case["text"], case["d"])
+        got = lq.implr_integrate(f, case["d"], case["a"], int(case["n"])).value
+        w = unhex(case["implr"])
+        assert abs(got - w) <= 1e-12 * abs(w), case["tag"]
+        checked += 1
+    assert checked >= 30
+
+
+def test_jit_wide_modulus(lq, monkeypatch):
+    from paper_2404_08867_b200 import engine
+    monkeypatch.setenv("LQ_JIT", "always")
+    n = 2**40 + 15
+    z = (1, 123456789013, 2**39 + 7)
+    f = lq.parse("x[2]*exp(x[1]*x[3]) + sin(x[1]^2)", 3)
+    pi = engine.plain_integrand(f, 3, force_program=True)
+    lo = 2**35
+    s = engine.lattice_sum(pi, n, np.asarray(z, dtype=np.uint64), lo, lo + 8192)
+    assert pi.struct.prog.jit
+    pts = np.array([[float((i * zj) % n) / n for zj in z] for i in range(lo, lo + 8192)])
+    ref = float(np.sum(pts[:, 1] * np.exp(pts[:, 0] * pts[:, 2]) + np.sin(pts[:, 0] ** 2)))
+    assert abs(s - ref) <= 1e-12 * abs(ref)
