@@ -83,8 +83,8 @@ int lq_jit_create(const char* source, const char* name, lq_jit** out, char* log,
     nvrtcProgram_ prog = nullptr;
     if (g_nvrtc.create(&prog, source, name ? name : "lq_jit.cu", 0, nullptr, nullptr) != 0)
         return lq_internal_fail(LQ_ERR_CUDA, "nvrtcCreateProgram failed");
-    const char* opts[] = {"--gpu-architecture=sm_100a", "-O3", "-std=c++17", "--fmad=true", "-lineinfo"};
-    const int rc = g_nvrtc.compile(prog, 5, opts);
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=true", "-lineinfo"};
+    const int rc = g_nvrtc.compile(prog, 4, opts);
     size_t ls = 0;
     g_nvrtc.log_size(prog, &ls);
     std::string lg(ls + 1, '\0');

@@ -33,6 +33,7 @@ def test_jit_plain_sums_match_interpreter_and_reference(lq, golden, monkeypatch)
         rule = _rule(lq, case)
         z = rule.z_reduced_array()
         monkeypatch.setenv("LQ_JIT", "0")
+        engine._plain_cache.clear()
         interp = engine.plain_integrand(f, d, force_program=True)
         a = engine.lattice_sum(interp, rule.n, z)
         assert not interp.struct.prog.jit

@@ -30,10 +30,16 @@ def main():
         cfg = make_config(cid)
         f = lq.parse(cfg.text, cfg.d)
         rule = lq.korobov_vector(cfg.plain_a, cfg.plain_n, cfg.d)
-        for force in (False, True):
+        for force in (False, True, "jit"):
             if force and cid == 5:
                 continue
-            pi = engine.plain_integrand(f, cfg.d, force_program=force)
+            if force == "jit":
+                os.environ["LQ_JIT"] = "always"
+                engine._plain_cache.clear()
+            else:
+                os.environ["LQ_JIT"] = "0"
+                engine._plain_cache.clear()
+            pi = engine.plain_integrand(f, cfg.d, force_program=bool(force))
             z = rule.z_reduced_array()
             n = rule.n
             end = n if cid != 5 else n
@@ -52,7 +58,8 @@ def main():
             pts = end
             pd = pts * cfg.d
             fl = (FLOPS_PER_PD[cid] * cfg.d + 2) * pts
-            print(f"cfg{cid} {pi.kind:10s} n={n} d={cfg.d}: kernel {kms:.3f} ms wall {wall*1e3:.3f} ms "
+            kind = pi.kind + ("+jit" if pi.struct.prog.jit and pi.family is None else "")
+            print(f"cfg{cid} {kind:10s} n={n} d={cfg.d}: kernel {kms:.3f} ms wall {wall*1e3:.3f} ms "
                   f"{pts/kms*1e3:.3e} pts/s {pd/kms*1e3:.3e} pd/s {fl/kms*1e-9:.2f} TF  value={s/n!r}")
     # steady-state rate of the Gaussian family kernel on a large lattice
     cfg = make_config(3)
