@@ -17,7 +17,7 @@ from .lower import INSN_DTYPE
 __all__ = ["lib", "ctx", "NativeUnavailable", "check", "LQ_TILE", "LQ_SUPER_TILES",
            "LQ_NODE_BLOCK", "Integrand", "Program", "Factor", "LIB_PATH"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblq.so")
+LIB_PATH = os.environ.get("LQ_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblq.so")
 
 LQ_OK, LQ_ERR_VALUE, LQ_ERR_OVERFLOW, LQ_ERR_GRIDCAP = 0, -1, -2, -3
 LQ_ERR_CUDA, LQ_ERR_UNSUPPORTED, LQ_ERR_NOMEM = -4, -5, -6

@@ -201,8 +201,9 @@ bool uses_family_kernel(const lq_integrand* f, uint64_t n);
 // ~4 waves of CTAs run each tile on a cluster of S CTAs that split the
 // dimensions (k_fam<S>).  S depends on (n, d) only, so every GPU of a
 // multi-GPU run uses the same reduction structure.
-int fam_split(uint64_t n, int d) {
-    const uint64_t tiles = (n + lq::kFamTile - 1) / lq::kFamTile;
+int fam_split(uint64_t n, int d, int kind) {
+    const uint64_t tp = (uint64_t)lq::kThreads * lq::fam_pts(kind);
+    const uint64_t tiles = (n + tp - 1) / tp;
     const uint64_t want = 148ull * 2 * 4;
     int S = 1;
     while (S < 8 && tiles * S < want && d / (2 * S) >= 16) S *= 2;
@@ -212,7 +213,7 @@ int fam_split(uint64_t n, int d) {
 template <int KIND, int OUTER, class Args, int S>
 int launch_fam_s(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev) {
     auto kern = lq::k_fam<KIND, OUTER, Args, S>;
-    const size_t smem = S > 1 ? sizeof(double) * lq::kFamPts * lq::kThreads : 0;
+    const size_t smem = S > 1 ? sizeof(double) * lq::fam_pts(KIND) * lq::kThreads : 0;
     if (S > 1) {
         static bool attr_set = false;   // per template instance
         if (!attr_set) {
@@ -241,7 +242,7 @@ int launch_fam_s(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev)
 
 template <int KIND, int OUTER, class Args>
 int launch_fam(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev, uint64_t n_total) {
-    switch (fam_split(n_total, args.d)) {
+    switch (fam_split(n_total, args.d, KIND)) {
         case 1: return launch_fam_s<KIND, OUTER, Args, 1>(c, args, ntiles, tiles_dev);
         case 2: return launch_fam_s<KIND, OUTER, Args, 2>(c, args, ntiles, tiles_dev);
         case 4: return launch_fam_s<KIND, OUTER, Args, 4>(c, args, ntiles, tiles_dev);
@@ -250,7 +251,8 @@ int launch_fam(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev, u
 }
 
 uint64_t tile_points(const lq_integrand* f, uint64_t n) {
-    return uses_family_kernel(f, n) ? (uint64_t)lq::kFamTile : (uint64_t)lq::kTile;
+    if (!uses_family_kernel(f, n)) return (uint64_t)lq::kTile;
+    return (uint64_t)lq::kThreads * lq::fam_pts(f->kind == LQ_FAM_QUAD_EXP ? lq::FAM_QUAD : lq::FAM_LIN);
 }
 
 template <class A>

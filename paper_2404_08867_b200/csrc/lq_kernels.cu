@@ -48,6 +48,11 @@ struct QuadDim {
 // (measured 8.1e12 vs 7.6e12 pd/s for 16 points, one chain).
 constexpr int kFamPts = 24;
 constexpr int kFamTile = kThreads * kFamPts;
+#ifndef LQ_QUAD_PTS
+#define LQ_QUAD_PTS 24
+#endif
+constexpr int kQuadPts = LQ_QUAD_PTS;     // points per thread of the Gaussian family
+__host__ __device__ constexpr int fam_pts(int kind) { return kind == 1 ? kQuadPts : kFamPts; }
 
 struct LinParams {
     double alpha, scale, K, A, B, C0, kappa;
@@ -168,14 +173,14 @@ __device__ __forceinline__ double fam_outer(double acc, const Args& a) {
 template <int KIND, int OUTER, class Args, int S>
 __global__ void __launch_bounds__(kThreads, 2) k_fam(const __grid_constant__ Args a, uint32_t hmask,
                                                       double* __restrict__ tile_out) {
-    constexpr int P = kFamPts;
+    constexpr int P = fam_pts(KIND);
     extern __shared__ double part[];   // [P][kThreads] when S > 1
     __shared__ double sh[8];
     uint32_t H[P];
     #pragma unroll
     for (int k = 0; k < P; ++k) H[k] = (threadIdx.x + k) & hmask;   // opaque zeros
     const int64_t tile = blockIdx.x;
-    const uint64_t i0_64 = a.base + (uint64_t)tile * kFamTile + (uint64_t)threadIdx.x * P;
+    const uint64_t i0_64 = a.base + (uint64_t)tile * (kThreads * P) + (uint64_t)threadIdx.x * P;
     const uint32_t i0 = (uint32_t)i0_64;   // < 2^32 (n <= 2^31)
     double acc[P];
     #pragma unroll

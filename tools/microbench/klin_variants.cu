@@ -33,9 +33,13 @@ __global__ void __launch_bounds__(256, MINB) kv(const __grid_constant__ Args a, 
         r[0] = mulmod_shoup(i0, z, a.dims[j].zs, n);
         uint32_t zc = z, zcm = zm;
         if (CH >= 2) {
-            zc = a.dims[j].z2;
+            uint32_t zz = 0;
+#pragma unroll
+            for (int q = 0; q < CH; ++q) zz = __viaddmin_u32(zz, z, zz + zm);
+            zc = zz;
             zcm = zc - n;
-            r[1] = step_mod(r[0], z, zm);
+#pragma unroll
+            for (int q = 1; q < CH; ++q) r[q] = step_mod(r[q - 1], z, zm);
         }
 #pragma unroll
         for (int p = 0; p < P; p += CH) {
@@ -101,13 +105,13 @@ int main() {
     }
     double* dout;
     cudaMalloc(&dout, 8 << 20);
-    run("P16 CH1 minb2", kv<16, 1, 2>, 16, a, npts, dout);
     run("P24 CH2 minb2", kv<24, 2, 2>, 24, a, npts, dout);
-    run("P24 CH1 minb2", kv<24, 1, 2>, 24, a, npts, dout);
-    run("P20 CH2 minb2", kv<20, 2, 2>, 20, a, npts, dout);
-    run("P20 CH1 minb2", kv<20, 1, 2>, 20, a, npts, dout);
-    run("P28 CH2 minb2", kv<28, 2, 2>, 28, a, npts, dout);
-    run("P22 CH2 minb2", kv<22, 2, 2>, 22, a, npts, dout);
-    run("P18 CH2 minb2", kv<18, 2, 2>, 18, a, npts, dout);
+    run("P24 CH3 minb2", kv<24, 3, 2>, 24, a, npts, dout);
+    run("P24 CH4 minb2", kv<24, 4, 2>, 24, a, npts, dout);
+    run("P30 CH3 minb2", kv<30, 3, 2>, 30, a, npts, dout);
+    run("P32 CH4 minb2", kv<32, 4, 2>, 32, a, npts, dout);
+    run("P32 CH2 minb1", kv<32, 2, 1>, 32, a, npts, dout);
+    run("P20 CH4 minb2", kv<20, 4, 2>, 20, a, npts, dout);
+    run("P16 CH4 minb3", kv<16, 4, 3>, 16, a, npts, dout);
     return 0;
 }
