@@ -30,6 +30,7 @@ sys.path.insert(0, REPO)
 
 import numpy as np  # noqa: E402
 
+METRIC = "lattice f-evals/sec (fp64) & MDI-LR time-to-solution; % of FP64 peak"   # BASELINE.json
 FLOPS_PER_PD = 3          # 1 (coordinate r/n) + 2 (c_j * x_j accumulate) for exp-abs-linear
 FLOPS_PER_POINT = 2       # transcendental + accumulate
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
@@ -127,7 +128,7 @@ def run_reference(args, rank, world):
         t += dt
     value = args.steps * sample / t
     line = {
-        "impl": "reference", "metric": "lattice f-evals/sec (fp64)", "value": value, "unit": "f-evals/s",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "f-evals/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "cfg5_plain_sum", "d": cfg.d, "n": cfg.plain_n, "a": cfg.plain_a,
@@ -303,10 +304,23 @@ def main():
                 ts.append(time.perf_counter() - t0)
             mdi[f"cfg{cid}_ms"] = min(ts) * 1e3
             mdi[f"cfg{cid}_mean"] = rep.mean
+            mdi[f"cfg{cid}_log_mean"] = rep.log_raw - rep.log_total
             mdi[f"cfg{cid}_method"] = rep.method
+        # the small BASELINE plain-sum configs (parity cases; launch/latency bound)
+        for cid in (1, 2, 3):
+            pc = make_config(cid)
+            g = lq.parse(pc.text, pc.d)
+            prule = lq.korobov_vector(pc.plain_a, pc.plain_n, pc.d)
+            lq.slr_integrate(g, prule)
+            ts = []
+            for _ in range(5):
+                t0 = time.perf_counter()
+                lq.slr_integrate(g, prule)
+                ts.append(time.perf_counter() - t0)
+            mdi[f"plain_cfg{cid}_e2e_ms"] = min(ts) * 1e3
 
     line = {
-        "metric": "lattice f-evals/sec (fp64)", "value": value, "unit": "f-evals/s", "n_gpus": world,
+        "metric": METRIC, "value": value, "unit": "f-evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE config 5)",
@@ -325,6 +339,9 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "mdi_lr_time_to_solution": mdi,
+        "notes": ("workload = BASELINE config 5 plain sum (largest single-GPU config; configs 1-3 are "
+                  "sub-millisecond parity cases, timed end to end under mdi_lr_time_to_solution.plain_*); "
+                  "roofline bound is the FP64 pipe (no tensor-core or HBM-bound work on this path)"),
     }
     print(json.dumps(line), flush=True)
     if world > 1:

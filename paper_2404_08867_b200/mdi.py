@@ -102,6 +102,13 @@ class MdiReport:
             return None
         return (self.sign or 0.0) * math.exp(self.log_raw - self.log_total)
 
+    @property
+    def log_mean(self):
+        """log |grid mean| (finite even when ``mean`` underflows, e.g. config 4)."""
+        if self.log_raw is None or self.log_total is None:
+            return None
+        return self.log_raw - self.log_total
+
 
 def _const_sweep(value, counts):
     """The reference's constant sweep: chunks of 2^19 nodes, acc += c * len
