@@ -163,16 +163,24 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    # one process per GPU; LQ_DIST_BACKEND=gloo lets the multi-rank logic be
+    # exercised with several ranks sharing one GPU (no kernel waits on another)
+    dev = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("LQ_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
 
     import paper_2404_08867_b200 as lq
     from paper_2404_08867_b200 import _native as N, engine
     from paper_2404_08867_b200.configs import make_config
+    from paper_2404_08867_b200.distributed import exchange_disjoint
 
     h = N.lib()
-    ctx = N.ctx(local)
+    ctx = N.ctx(dev)
     # a dedicated (non-default) stream shared by liblq and the timing events
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -204,7 +212,7 @@ def main():
         N.check(h.lq_lattice_partials(ctx, C.byref(pi.struct), n, N.as_ptr(z), s_lo, s_hi,
                                       C.c_void_p(parts.data_ptr() + 8 * s_lo)))
         if world > 1:
-            dist.all_reduce(parts)      # disjoint slots: exact, order-independent
+            exchange_disjoint(parts)    # disjoint slots: exact, order-independent
         N.check(h.lq_reduce_sum(ctx, C.c_void_p(parts.data_ptr()), n_super, C.byref(out)))
         return out.value
 
@@ -219,7 +227,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev) as clocks:
         for _ in range(args.steps):
             flush.fill_(1)          # L2 flush between timed steps, outside the event window
             parts.zero_()
@@ -236,7 +244,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     value = args.steps * n / (total_ms * 1e-3)
@@ -262,7 +270,7 @@ def main():
         r = api(f, rule)
     e2e_s = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = {"value": args.steps * n / e2e_s, "unit": "f-evals/s",

@@ -60,10 +60,15 @@ def shard_range(n_units, rank, size):
 def exchange_disjoint(vec, group=None):
     """All-reduce(SUM) of a vector whose slots each have exactly one non-zero
     writer: exact and order-independent.  Works on CUDA (nccl) and CPU (gloo)
-    tensors."""
+    tensors; CUDA tensors on a gloo group are staged through the host."""
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(vec, group=group)
+        if vec.is_cuda and dist.get_backend(group) != "nccl":
+            host = vec.cpu()
+            dist.all_reduce(host, group=group)
+            vec.copy_(host)
+        else:
+            dist.all_reduce(vec, group=group)
     return vec
 
 
