@@ -511,11 +511,26 @@ int lq_points_block(lq_ctx* c, int32_t d, uint64_t n, const uint64_t* z, int64_t
         dst = (double*)p;
     }
     const double n_d = (double)n, inv = 1.0 / n_d;
-    int64_t blocks = (int64_t)((n_elem + lq::kThreads - 1) / lq::kThreads);
-    int grid = grid_for(c, (const void*)lq::k_points, blocks);
-    t_begin(c);
-    lq::k_points<<<grid, lq::kThreads, 0, c->stream>>>((const uint64_t*)dz, (uint32_t)d, n, n_d, inv, inv, (uint64_t)start, n_elem, dst);
-    t_end(c);
+    if (n <= (1ull << 31)) {
+        std::vector<uint32_t> zz(2 * (size_t)d);
+        for (int j = 0; j < d; ++j) {
+            zz[2 * j] = (uint32_t)z[j];
+            zz[2 * j + 1] = (uint32_t)(((uint64_t)z[j] << 32) / n);
+        }
+        void* dzz;
+        if ((rc = upload(c, B_TAB, zz.data(), zz.size() * 4, &dzz))) return rc;
+        dim3 g((unsigned)((m + lq::kPtRows - 1) / lq::kPtRows), (unsigned)((d + lq::kPtCols - 1) / lq::kPtCols));
+        if ((m + lq::kPtRows - 1) / lq::kPtRows > 0x7fffffffull) return fail(LQ_ERR_VALUE, "point block too large");
+        t_begin(c);
+        lq::k_points_tiled<<<g, lq::kThreads, 0, c->stream>>>((const uint2*)dzz, (uint32_t)d, (uint32_t)n, n_d, inv, (uint64_t)start, m, dst);
+        t_end(c);
+    } else {
+        int64_t blocks = (int64_t)((n_elem + lq::kThreads - 1) / lq::kThreads);
+        int grid = grid_for(c, (const void*)lq::k_points, blocks);
+        t_begin(c);
+        lq::k_points<<<grid, lq::kThreads, 0, c->stream>>>((const uint64_t*)dz, (uint32_t)d, n, n_d, inv, inv, (uint64_t)start, n_elem, dst);
+        t_end(c);
+    }
     CK(cudaGetLastError());
     if (!out_is_device) {
         CK(cudaMemcpyAsync(out, dst, n_elem * sizeof(double), cudaMemcpyDeviceToHost, c->stream));

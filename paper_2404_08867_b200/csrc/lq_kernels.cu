@@ -26,6 +26,39 @@ __global__ void __launch_bounds__(kThreads) k_points(const uint64_t* __restrict_
     }
 }
 
+// points_block for n <= 2^31, HBM-write bound: a CTA owns a 64-row x 64-column
+// tile; thread (c, g) walks column c for 16 consecutive rows with the
+// two-instruction residue step (one Shoup modmul per thread), rounds each
+// coordinate exactly (Markstein) into shared memory, and the tile leaves as
+// 64-double contiguous row segments (coalesced 512 B stores).
+constexpr int kPtRows = 64, kPtCols = 64;
+__global__ void __launch_bounds__(kThreads) k_points_tiled(const uint2* __restrict__ zz, uint32_t d, uint32_t n,
+                                                           double n_d, double inv_n, uint64_t start, uint64_t m,
+                                                           double* __restrict__ out) {
+    __shared__ double tile[kPtRows][kPtCols + 1];
+    const uint64_t row0 = (uint64_t)blockIdx.x * kPtRows;
+    const uint32_t col0 = blockIdx.y * kPtCols;
+    const uint32_t c = threadIdx.x & (kPtCols - 1), g = threadIdx.x / kPtCols;   // 4 row groups of 16
+    const uint32_t col = col0 + c;
+    if (col < d) {
+        const uint2 t = __ldg(zz + col);
+        const uint32_t zm = t.x - n;
+        const uint64_t i0 = start + row0 + (uint64_t)g * 16;
+        uint32_t r = mulmod_shoup((uint32_t)(i0 % n), t.x, t.y, n);
+        #pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            tile[g * 16 + k][c] = exact_div((double)r, n_d, inv_n);
+            r = step_mod(r, t.x, zm);
+        }
+    }
+    __syncthreads();
+    const uint32_t ncols = min(kPtCols, d - col0);
+    for (int rr = threadIdx.x / kPtCols; rr < kPtRows; rr += kThreads / kPtCols) {
+        const uint64_t row = row0 + rr;
+        if (row < m && c < ncols) out[row * d + col0 + c] = tile[rr][c];
+    }
+}
+
 // ============================================================ family sums
 // Per-dimension record of the linear-form kernels.
 struct LinDim {
