@@ -62,3 +62,30 @@ def test_lattice_subcommands(capsys):
     assert "a=390" in capsys.readouterr().out            # korobov_search(1009, 6) in the reference
     assert cli.cli_main(["lattice", "cbc", "--n", "101", "--dim", "5"]) == 0
     assert "z=(1, 39, 18, 37, 43)" in capsys.readouterr().out
+
+
+def test_fit_power_law_and_cli(tmp_path, capsys):
+    import sys
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from paper_2404_08867_b200 import fits
+    path = tmp_path / "runs.csv"
+    for a, d in ((4, 10), (6, 10), (8, 10), (10, 10), (12, 10), (8, 4), (8, 6), (8, 12)):
+        t = 1e-6 * a ** 2 * d ** 1.5 * (1.0 + 0.01 * ((a * d) % 7))
+        cli.append_csv(cli.RunRecord("mdilr", "gaussian", d, 1 + a ** d, a, 0.5, seconds=t), path)
+    rows = fits.read_rows(path)
+    res = fits.fit_power_law([r for r in rows if r["d"] == 8 or r["a"] == 8], "N^2*d^q")
+    assert abs(res.exponent - 1.5) < 0.05 and res.r_squared > 0.99
+    assert cli.cli_main(["fit", "--in", str(path), "--dim", "10"]) == 0
+    assert "best=" in capsys.readouterr().out
+    try:   # same numbers as the reference's own fit where it is importable (build container)
+        from latquad.bench import fit_power_law as ref_fit
+    except ImportError:
+        return
+    for model in fits.MODELS:
+        sub = [r for r in rows if r["d"] == 10]
+        try:
+            want = ref_fit(sub, model)
+        except Exception:
+            continue
+        got = fits.fit_power_law(sub, model)
+        assert abs(got.exponent - want.exponent) < 1e-12 and abs(got.r_squared - want.r_squared) < 1e-12
