@@ -33,6 +33,7 @@ import numpy as np  # noqa: E402
 METRIC = "lattice f-evals/sec (fp64) & MDI-LR time-to-solution; % of FP64 peak"   # BASELINE.json
 FLOPS_PER_PD = 3          # 1 (coordinate r/n) + 2 (c_j * x_j accumulate) for exp-abs-linear
 FLOPS_PER_POINT = 2       # transcendental + accumulate
+ORB_M = 24                # points per chain of the orbit kernel (LQ_ORB_LIN_M, csrc/lq_kernels.cu)
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
            0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
@@ -202,7 +203,8 @@ def main():
     N.check(h.lq_fp64_peak(ctx, iters, C.byref(tf), C.byref(ms)))
     fp64_peak = tf.value
 
-    tile_pts, n_super = N.lattice_layout(pi.struct, n)
+    lay = N.lattice_layout(pi.struct, n, z)
+    n_super = lay.n_supers
     s_lo, s_hi = n_super * rank // world, n_super * (rank + 1) // world
     parts = torch.zeros(n_super, dtype=torch.float64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")     # 256 MiB > 126 MB L2
@@ -250,11 +252,24 @@ def main():
     value = args.steps * n / (total_ms * 1e-3)
     estimate = value_sum / n
 
-    # dominant kernel roofline: k_lin<EXPABS> over this rank's points
-    sp = tile_pts * N.LQ_SUPER_TILES
-    my_pts = min(s_hi * sp, n) - s_lo * sp
+    # dominant kernel roofline over this rank's units.  Orbit layout: a unit is
+    # a chain of ORB_M points whose linear forms are computed once and serve
+    # the point and its mirror; index layout: a unit is a point.
+    su = lay.tile_units * N.LQ_SUPER_TILES
+    my_units = min(s_hi * su, lay.n_units) - s_lo * su
     avg_kern = kern_ms / args.steps
-    achieved = (FLOPS_PER_PD * d + FLOPS_PER_POINT) * my_pts / (avg_kern * 1e-3) / 1e12
+    if lay.mode == N.LAYOUT_ORBIT:
+        forms = my_units * ORB_M                       # linear forms evaluated (one per pair)
+        alg_flops = forms * (FLOPS_PER_PD * d + 2 * FLOPS_PER_POINT)
+        exec_flops = forms * 2 * (-(-d // ORB_M) * ORB_M)   # DFMAs incl. zero padding of d
+        kernel_name = "k_orbit<FAM_LIN, OUT_EXPABS> (liblq.so)"
+    else:
+        forms = my_units
+        alg_flops = forms * (FLOPS_PER_PD * d + FLOPS_PER_POINT)
+        exec_flops = forms * 2 * d
+        kernel_name = "k_fam<FAM_LIN, OUT_EXPABS> (liblq.so)"
+    achieved = alg_flops / (avg_kern * 1e-3) / 1e12
+    executed = exec_flops / (avg_kern * 1e-3) / 1e12
 
     # e2e: the public drop-in API (host lowering, parameter H2D, kernel, result D2H)
     # e2e: the public drop-in API (host lowering, parameter upload, kernel,
@@ -288,7 +303,8 @@ def main():
     if os.path.exists(prof_path):
         with open(prof_path) as fh:
             prof = json.load(fh)
-    traffic = prof.get("k_lin_dram_bytes_per_launch")
+    traffic = prof.get("k_orbit_dram_bytes_per_launch" if lay.mode == N.LAYOUT_ORBIT
+                       else "k_lin_dram_bytes_per_launch")
 
     cpu = None
     if world == 1 and args.cpu_sample > 0:
@@ -338,8 +354,12 @@ def main():
         "estimate": estimate,
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
-                     "kernel": "k_lin<OUT_EXPABS> (liblq.so)", "kernel_ms": avg_kern,
-                     "flops_per_point": FLOPS_PER_PD * d + FLOPS_PER_POINT,
+                     "kernel": kernel_name, "kernel_ms": avg_kern,
+                     "layout": "orbit" if lay.mode == N.LAYOUT_ORBIT else "index",
+                     "flops_per_unit": ("per mirrored pair: 3 d (one linear form, SURVEY §8d per point-dim "
+                                        "figure) + 2 x 2 (two outer evaluations)" if lay.mode == N.LAYOUT_ORBIT
+                                        else "per point: 3 d + 2 (SURVEY §8d)"),
+                     "executed_dfma_tflops": executed, "executed_frac": executed / fp64_peak,
                      "peak_source": "measured in-run by lq_fp64_peak (DFMA chains, ~1 s); "
                                     "MEASURED_PEAKS.json has no FP64 entry"},
         "cpu_baseline": cpu,

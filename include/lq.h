@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define LQ_ABI_VERSION 1
+#define LQ_ABI_VERSION 2
 
 #define LQ_OK 0
 #define LQ_ERR_VALUE (-1)
@@ -113,12 +113,22 @@ int lq_points_block(lq_ctx* ctx, int32_t d, uint64_t n, const uint64_t* z_reduce
  * Returns sum_{i in [i_begin, i_end)} f(frac(i z / n)) (not divided by n).   */
 int lq_lattice_sum(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_t* z_reduced,
                    uint64_t i_begin, uint64_t i_end, double* sum_out);
-/* Multi-GPU building blocks.  The tile size depends on the kernel chosen for
- * (f, n); lq_lattice_layout reports it and the number of super-chunks.
- * Super-chunk s covers points [s*T*LQ_SUPER_TILES, (s+1)*T*LQ_SUPER_TILES)
- * of [0, n), T = tile points.  lq_lattice_partials writes the partials of
- * super-chunks [s_begin, s_end) to out_dev[0 .. s_end-s_begin).             */
-int lq_lattice_layout(const lq_integrand* f, uint64_t n, int64_t* tile_points, int64_t* n_supers);
+/* Multi-GPU building blocks.  A full-lattice sum is split into units: points
+ * i in [0, n) for the per-index kernels (mode LQ_LAYOUT_INDEX), or -- for a
+ * Korobov rule z_j = a^(j-1) over a prime n (mode LQ_LAYOUT_ORBIT) -- chains
+ * of consecutive powers i0 a^k whose points are summed together with their
+ * mirrors n - i.  Units form tiles of tile_units, tiles form
+ * super-chunks of LQ_SUPER_TILES; super-chunk s covers units
+ * [s*T*LQ_SUPER_TILES, (s+1)*T*LQ_SUPER_TILES).  The layout depends on
+ * (f, n, z) only, so every rank computes the same one; z may be NULL (index
+ * layout).  lq_lattice_partials writes the partials of super-chunks
+ * [s_begin, s_end) to out_dev[0 .. s_end-s_begin).  lq_lattice_sum over the
+ * full range [0, n) uses the same layout.  (Replaces the chunk loop of
+ * quad.slr_integrate, quad.py:96-104, for sharded runs.)                   */
+#define LQ_LAYOUT_INDEX 0
+#define LQ_LAYOUT_ORBIT 1
+int lq_lattice_layout(const lq_integrand* f, uint64_t n, const uint64_t* z_reduced, int64_t* tile_units,
+                      int64_t* n_supers, int64_t* n_units, int32_t* mode);
 int lq_lattice_partials(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_t* z_reduced,
                         int64_t s_begin, int64_t s_end, double* out_dev);
 /* Fixed pairwise tree over vals_dev[0..count); result to host *out. */

@@ -6,6 +6,7 @@ missing, every entry point raises ``NativeUnavailable`` loudly.
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import os
 import threading
@@ -67,7 +68,8 @@ _SIGS = {
     "lq_points_block": [_P, C.c_int32, C.c_uint64, _P, C.c_int64, C.c_int64, _P, C.c_int32],
     "lq_lattice_sum": [_P, C.POINTER(Integrand), C.c_uint64, _P, C.c_uint64, C.c_uint64, C.POINTER(C.c_double)],
     "lq_lattice_partials": [_P, C.POINTER(Integrand), C.c_uint64, _P, C.c_int64, C.c_int64, _P],
-    "lq_lattice_layout": [C.POINTER(Integrand), C.c_uint64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
+    "lq_lattice_layout": [C.POINTER(Integrand), C.c_uint64, _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                          C.POINTER(C.c_int64), C.POINTER(C.c_int32)],
     "lq_reduce_sum": [_P, _P, C.c_int64, C.POINTER(C.c_double)],
     "lq_tensor_sum": [_P, C.POINTER(Program), C.c_int32, _P, _P, C.c_int32, C.c_uint64, C.c_uint64,
                       C.POINTER(C.c_double)],
@@ -157,11 +159,18 @@ def ctx(device=None):
     return c.ptr
 
 
-def lattice_layout(pi_struct, n):
-    """(tile points, number of super-chunks) of the kernel liblq picks for (f, n)."""
-    tp, ns = C.c_int64(), C.c_int64()
-    check(lib().lq_lattice_layout(C.byref(pi_struct), int(n), C.byref(tp), C.byref(ns)))
-    return tp.value, ns.value
+Layout = collections.namedtuple("Layout", "tile_units n_supers n_units mode")
+LAYOUT_INDEX, LAYOUT_ORBIT = 0, 1
+
+
+def lattice_layout(pi_struct, n, z=None):
+    """Reduction layout liblq uses for the full-lattice sum of (f, n, z):
+    units per tile, super-chunks, units, and the mode (LAYOUT_INDEX: units are
+    points; LAYOUT_ORBIT: units are chains of mirrored Korobov points)."""
+    tp, ns, nu, mode = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
+    check(lib().lq_lattice_layout(C.byref(pi_struct), int(n), as_ptr(z), C.byref(tp), C.byref(ns),
+                                  C.byref(nu), C.byref(mode)))
+    return Layout(tp.value, ns.value, nu.value, mode.value)
 
 
 def as_ptr(arr):

@@ -4,7 +4,13 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -32,7 +38,7 @@ int fail(int code, const char* fmt, ...) {
                         __FILE__, __LINE__);                                          \
     } while (0)
 
-enum Buf { B_TAB = 0, B_TILES, B_RED0, B_RED1, B_OUT, B_PROG, B_AUX0, B_AUX1, B_AUX2, B_AUX3, B_PART, B_FAC, B_NODES, B_NBUF };
+enum Buf { B_TAB = 0, B_TILES, B_RED0, B_RED1, B_OUT, B_PROG, B_AUX0, B_AUX1, B_AUX2, B_AUX3, B_PART, B_FAC, B_NODES, B_ORB, B_NBUF };
 
 }  // namespace
 
@@ -63,6 +69,7 @@ struct lq_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_ms = 0.f;
     int64_t launches = 0;
+    uint64_t orb_id = 0;       // orbit plan whose start tables are in dbuf[B_ORB]
 };
 
 namespace {
@@ -399,6 +406,259 @@ int check_integrand(const lq_integrand* f) {
     return LQ_OK;
 }
 
+// ------------------------------------------------------------ Korobov orbits
+// Host plan of k_orbit (lq_kernels.cu): primality of n, the order o of a in
+// (Z/n)^*, a primitive root g, the coset/exponent enumeration of half of the
+// nonzero points (the mirrors n - i cover the other half) and the start tables.
+uint32_t powmod32(uint64_t b, uint64_t e, uint32_t n) {
+    uint64_t r = 1 % n;
+    b %= n;
+    while (e) {
+        if (e & 1) r = r * b % n;
+        b = b * b % n;
+        e >>= 1;
+    }
+    return (uint32_t)r;
+}
+
+bool is_prime32(uint32_t n) {
+    if (n < 2) return false;
+    for (uint32_t p : {2u, 3u, 5u, 7u, 11u, 13u}) {
+        if (n % p == 0) return n == p;
+    }
+    uint32_t d = n - 1;
+    int s = 0;
+    while (!(d & 1)) { d >>= 1; ++s; }
+    for (uint32_t b : {2u, 3u, 5u, 7u}) {   // deterministic below 3.2e9
+        uint64_t x = powmod32(b, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool comp = true;
+        for (int r = 1; r < s && comp; ++r) {
+            x = x * x % n;
+            if (x == n - 1) comp = false;
+        }
+        if (comp) return false;
+    }
+    return true;
+}
+
+struct OrbPlan {
+    uint64_t id = 0;
+    uint32_t n = 0, a = 0, as = 0, qc = 0, h = 0;
+    uint64_t units = 0;
+    int m = 0;
+    std::vector<uint32_t> G, Alo, Ahi;
+};
+
+constexpr uint32_t kOrbMaxCosets = 4096;
+
+// nullptr when the rule is not a Korobov rule over a prime modulus the orbit
+// kernel can enumerate (caller then uses the per-index kernels).
+std::shared_ptr<const OrbPlan> build_orbit_plan(uint32_t n, uint32_t a, int m) {
+    if (!is_prime32(n) || a < 1 || a >= n) return nullptr;
+    std::vector<uint32_t> primes;
+    uint32_t rest = n - 1;
+    for (uint32_t p = 2; (uint64_t)p * p <= rest; ++p)
+        if (rest % p == 0) {
+            primes.push_back(p);
+            while (rest % p == 0) rest /= p;
+        }
+    if (rest > 1) primes.push_back(rest);
+    uint32_t o = n - 1;
+    for (uint32_t p : primes)
+        while (o % p == 0 && powmod32(a, o / p, n) == 1) o /= p;
+    uint32_t g = 2;
+    for (;; ++g) {
+        bool prim = true;
+        for (uint32_t p : primes)
+            if (powmod32(g, (n - 1) / p, n) == 1) { prim = false; break; }
+        if (prim) break;
+    }
+    const uint32_t C = (n - 1) / o;
+    uint32_t cosets, h;
+    if (o % 2 == 0) { cosets = C; h = o / 2; }          // -1 lies in <a>: half of each coset
+    else { cosets = C / 2; h = o; }                     // -coset(s) = coset(s + C/2)
+    if (cosets < 1 || cosets > kOrbMaxCosets || h < (uint32_t)m) return nullptr;
+    static std::atomic<uint64_t> next_id{1};
+    auto p = std::make_shared<OrbPlan>();
+    p->id = next_id++;
+    p->n = n; p->a = a; p->m = m; p->h = h;
+    p->as = (uint32_t)(((uint64_t)a << 32) / n);
+    p->qc = (h + m - 1) / m;
+    p->units = (uint64_t)cosets * p->qc;
+    p->G.resize(cosets);
+    const uint32_t gC = powmod32(g, 1, n);
+    uint64_t gs = 1;
+    for (uint32_t s = 0; s < cosets; ++s) { p->G[s] = (uint32_t)gs; gs = gs * gC % n; }
+    const uint32_t am = powmod32(a, (uint64_t)m, n);
+    p->Alo.resize(4096);
+    uint64_t t = 1;
+    for (int q = 0; q < 4096; ++q) { p->Alo[q] = (uint32_t)t; t = t * am % n; }
+    const uint32_t am4096 = (uint32_t)t;
+    p->Ahi.resize(p->qc / 4096 + 1);
+    t = 1;
+    for (size_t q = 0; q < p->Ahi.size(); ++q) { p->Ahi[q] = (uint32_t)t; t = t * am4096 % n; }
+    return p;
+}
+
+std::shared_ptr<const OrbPlan> orbit_plan(uint32_t n, uint32_t a, int m) {
+    static std::mutex mu;
+    static std::map<std::tuple<uint32_t, uint32_t, int>, std::shared_ptr<const OrbPlan>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(n, a, m);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    auto p = build_orbit_plan(n, a, m);
+    if (cache.size() > 64) cache.clear();
+    cache[key] = p;
+    return p;
+}
+
+// LQ_ORBIT=0 disables the orbit kernel, =always uses it whenever the rule
+// allows; default: n >= 2^20 (below that the index kernels' dimension split
+// fills the GPU better).
+int orbit_mode() {
+    const char* e = std::getenv("LQ_ORBIT");
+    if (!e || !*e) return 1;
+    if (!std::strcmp(e, "0")) return 0;
+    if (!std::strcmp(e, "always")) return 2;
+    return 1;
+}
+
+std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, const uint64_t* z) {
+    const int mode = orbit_mode();
+    if (mode == 0 || !z || f->kind == LQ_FAM_PROGRAM || f->d < 2) return nullptr;
+    if (n > (1ull << 31) || n < 5 || (mode == 1 && n < (1ull << 20))) return nullptr;
+    const bool quad = f->kind == LQ_FAM_QUAD_EXP;
+    const int m = lq::orb_len(quad ? lq::FAM_QUAD : lq::FAM_LIN);
+    const int cap = quad ? lq::kOrbQuadDims : lq::kOrbLinDims;
+    if ((f->d + m - 1) / m * m > cap) return nullptr;
+    if (!f->beta || (quad && !f->gamma)) return nullptr;
+    if (z[0] != 1 % n) return nullptr;
+    const uint64_t a = z[1];
+    for (int j = 2; j < f->d; ++j)
+        if (z[j] != z[j - 1] * a % n) return nullptr;   // z_j = a^(j-1) mod n
+    return orbit_plan((uint32_t)n, (uint32_t)a, m);
+}
+
+// Device copies of the start tables, cached per context and plan.
+int orbit_tables(lq_ctx* c, const OrbPlan& p, const uint32_t** G, const uint32_t** Alo, const uint32_t** Ahi) {
+    const size_t nG = p.G.size(), nlo = p.Alo.size(), nhi = p.Ahi.size();
+    const size_t bytes = 4 * (nG + nlo + nhi);
+    if (c->orb_id != p.id) {
+        std::vector<uint32_t> all;
+        all.reserve(nG + nlo + nhi);
+        all.insert(all.end(), p.G.begin(), p.G.end());
+        all.insert(all.end(), p.Alo.begin(), p.Alo.end());
+        all.insert(all.end(), p.Ahi.begin(), p.Ahi.end());
+        void* d;
+        int rc;
+        if ((rc = upload(c, B_ORB, all.data(), bytes, &d))) return rc;
+        c->orb_id = p.id;
+    }
+    const uint32_t* base = (const uint32_t*)c->dbuf[B_ORB];
+    *G = base;
+    *Alo = base + nG;
+    *Ahi = base + nG + nlo;
+    return LQ_OK;
+}
+
+int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t unit0, int64_t ntiles,
+                 double* tiles_dev) {
+    int rc;
+    const uint32_t* G;
+    const uint32_t *Alo, *Ahi;
+    if ((rc = orbit_tables(c, p, &G, &Alo, &Ahi))) return rc;
+    const int d = f->d, m = p.m;
+    const int dpad = (d + m - 1) / m * m;
+    const double nd = (double)p.n;
+    auto head = [&](lq::OrbHead& h) {
+        h.n = p.n; h.a = p.a; h.as = p.as; h.dpad = dpad; h.units = p.units; h.qc = p.qc; h.h = p.h;
+        h.G = G; h.Alo = Alo; h.Ahi = Ahi;
+        h.alpha = f->alpha; h.K = f->K; h.A = f->A; h.B = f->B; h.C0 = f->C0; h.kappa = f->kappa;
+    };
+    const unsigned hmask = 0u;
+    if (f->kind == LQ_FAM_QUAD_EXP) {
+        static thread_local lq::OrbQuadArgs args;
+        head(args.h);
+        int sigma = 1074 + std::ilogb(1.0 / nd) - 1000;
+        if (sigma < 0) sigma = 0;
+        args.h.M = std::ldexp(1.0 / nd, 1074 - sigma);
+        args.h.half = std::ldexp(0.5, -sigma);
+        args.h.scale = 1.0;
+        double C0 = 0.0;
+        for (int j = 0; j < dpad; ++j) {
+            if (j < d) {
+                args.bq[j].x = std::ldexp(f->beta[j] + f->gamma[j], sigma);
+                args.bq[j].y = std::ldexp(f->gamma[j], 2 * sigma);
+                if (!std::isfinite(args.bq[j].x) || !std::isfinite(args.bq[j].y))
+                    return fail(LQ_ERR_VALUE, "quadratic coefficient out of range");
+                C0 += 0.5 * f->beta[j] + 0.25 * f->gamma[j];
+            } else {
+                args.bq[j].x = 0.0;
+                args.bq[j].y = 0.0;
+            }
+        }
+        args.h.alphaB = f->alpha + C0;   // f = K exp(alpha + C + odd + even) at x, odd -> -odd at 1 - x
+        args.h.bsum = 0.0;
+        t_begin(c);
+        lq::k_orbit<lq::FAM_QUAD, 0, lq::OrbQuadArgs><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, unit0, hmask, tiles_dev);
+        t_end(c);
+        CK(cudaGetLastError());
+        return LQ_OK;
+    }
+    static thread_local lq::OrbLinArgs args;
+    head(args.h);
+    double maxabs = 0.0, bsum = 0.0;
+    for (int j = 0; j < d; ++j) {
+        maxabs = fmax(maxabs, fabs(f->beta[j]));
+        bsum += f->beta[j];
+    }
+    if (!std::isfinite(maxabs)) return fail(LQ_ERR_VALUE, "non-finite coefficient");
+    int sigma = 0;
+    if (maxabs > 0.0) {
+        sigma = 1074 + std::ilogb(maxabs / nd) + 1 - 1020;
+        if (sigma < 0) sigma = 0;
+    }
+    for (int j = 0; j < dpad; ++j) args.c[j] = j < d ? std::ldexp(f->beta[j] / nd, 1074 - sigma) : 0.0;
+    args.h.scale = std::ldexp(1.0, sigma);
+    args.h.bsum = bsum;
+    args.h.alphaB = f->alpha + bsum;   // alpha + <beta, 1 - x> = (alpha + sum beta) - <beta, x>
+    args.h.M = 0.0;
+    args.h.half = 0.0;
+    t_begin(c);
+    if (f->kind == LQ_FAM_LIN_EXP)
+        lq::k_orbit<lq::FAM_LIN, lq::OUT_EXP, lq::OrbLinArgs><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, unit0, hmask, tiles_dev);
+    else if (f->kind == LQ_FAM_LIN_SINCOS)
+        lq::k_orbit<lq::FAM_LIN, lq::OUT_SINCOS, lq::OrbLinArgs><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, unit0, hmask, tiles_dev);
+    else
+        lq::k_orbit<lq::FAM_LIN, lq::OUT_EXPABS, lq::OrbLinArgs><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, unit0, hmask, tiles_dev);
+    t_end(c);
+    CK(cudaGetLastError());
+    return LQ_OK;
+}
+
+// Reduction layout of a full-lattice sum: units are points (index kernels) or
+// chains of paired points (orbit kernel); tiles of tile_units units, super-chunks
+// of LQ_SUPER_TILES tiles.
+struct Layout {
+    uint64_t tile_units, n_units;
+    std::shared_ptr<const OrbPlan> orb;
+};
+
+Layout layout_of(const lq_integrand* f, uint64_t n, const uint64_t* z) {
+    Layout L;
+    L.orb = orbit_for(f, n, z);
+    if (L.orb) {
+        L.tile_units = lq::kThreads;
+        L.n_units = L.orb->units;
+    } else {
+        L.tile_units = tile_points(f, n);
+        L.n_units = n;
+    }
+    return L;
+}
+
 }  // namespace
 
 // ======================================================================= ABI
@@ -539,13 +799,17 @@ int lq_points_block(lq_ctx* c, int32_t d, uint64_t n, const uint64_t* z, int64_t
     return LQ_OK;
 }
 
-int lq_lattice_layout(const lq_integrand* f, uint64_t n, int64_t* tile_pts, int64_t* n_supers) {
+int lq_lattice_layout(const lq_integrand* f, uint64_t n, const uint64_t* z, int64_t* tile_units, int64_t* n_supers,
+                      int64_t* n_units, int32_t* mode) {
     int rc;
     if ((rc = check_integrand(f))) return rc;
-    const uint64_t tp = tile_points(f, n);
-    const uint64_t sp = tp * LQ_SUPER_TILES;
-    if (tile_pts) *tile_pts = (int64_t)tp;
-    if (n_supers) *n_supers = (int64_t)((n + sp - 1) / sp);
+    if (z && (rc = check_lattice(n, z, f->d))) return rc;
+    const Layout L = layout_of(f, n, z);
+    const uint64_t sp = L.tile_units * LQ_SUPER_TILES;
+    if (tile_units) *tile_units = (int64_t)L.tile_units;
+    if (n_supers) *n_supers = (int64_t)((L.n_units + sp - 1) / sp);
+    if (n_units) *n_units = (int64_t)L.n_units;
+    if (mode) *mode = L.orb ? LQ_LAYOUT_ORBIT : LQ_LAYOUT_INDEX;
     return LQ_OK;
 }
 
@@ -554,19 +818,22 @@ int lq_lattice_partials(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint
     int rc = set_dev(c);
     if (rc) return rc;
     if ((rc = check_integrand(f)) || (rc = check_lattice(n, z, f->d))) return rc;
-    int64_t tp64, ns;
-    lq_lattice_layout(f, n, &tp64, &ns);
-    const uint64_t tp = (uint64_t)tp64;
+    const Layout L = layout_of(f, n, z);
+    const uint64_t tp = L.tile_units, sp = tp * LQ_SUPER_TILES;
+    const int64_t ns = (int64_t)((L.n_units + sp - 1) / sp);
     if (s_begin < 0 || s_end > ns || s_end < s_begin)
         return fail(LQ_ERR_VALUE, "super-chunk range [%lld, %lld) outside [0, %lld)", (long long)s_begin, (long long)s_end, (long long)ns);
     if (s_end == s_begin) return LQ_OK;
-    const uint64_t sp = tp * LQ_SUPER_TILES;
     const uint64_t base = (uint64_t)s_begin * sp;
-    const uint64_t end = std::min<uint64_t>((uint64_t)s_end * sp, n);
+    const uint64_t end = std::min<uint64_t>((uint64_t)s_end * sp, L.n_units);
     const int64_t ntiles = (int64_t)((end - base + tp - 1) / tp);
     void* tiles;
     if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
-    if ((rc = launch_tiles(c, f, n, z, base, end, ntiles, (double*)tiles))) return rc;
+    if (L.orb) {
+        if ((rc = launch_orbit(c, f, *L.orb, base, ntiles, (double*)tiles))) return rc;
+    } else {
+        if ((rc = launch_tiles(c, f, n, z, base, end, ntiles, (double*)tiles))) return rc;
+    }
     lq::k_reduce1024<<<(unsigned)(s_end - s_begin), lq::kThreads, 0, c->stream>>>((const double*)tiles, ntiles, out_dev);
     c->launches++;
     CK(cudaGetLastError());
@@ -592,6 +859,18 @@ int lq_lattice_sum(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t*
     if (i_end == i_begin) {
         *sum_out = 0.0;
         return LQ_OK;
+    }
+    if (i_begin == 0 && i_end == n) {
+        const Layout L = layout_of(f, n, z);
+        if (L.orb) {
+            const int64_t ntiles = (int64_t)((L.n_units + L.tile_units - 1) / L.tile_units);
+            void* tiles;
+            if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
+            if ((rc = launch_orbit(c, f, *L.orb, 0, ntiles, (double*)tiles))) return rc;
+            double* r;
+            if ((rc = reduce_dev(c, (const double*)tiles, ntiles, &r))) return rc;
+            return read_scalar(c, r, sum_out);
+        }
     }
     const uint64_t tp = tile_points(f, n);
     if (n <= (1ull << 31) && i_end > (1ull << 32) - 2 * tp)

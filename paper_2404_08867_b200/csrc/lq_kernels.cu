@@ -250,6 +250,162 @@ __global__ void __launch_bounds__(kThreads, 2) k_fam(const __grid_constant__ Arg
     if (threadIdx.x == 0) tile_out[tile] = s;
 }
 
+// ============================================================ Korobov orbits
+// Full-lattice sums for a Korobov rule z_j = a^(j-1) mod n, n prime (DESIGN.md
+// §4.1b).  Two symmetries of the point set cut the work:
+//  * shift: point i*a has residues r_j(i*a) = r_(j+1)(i), so a chain of m
+//    points i0, i0 a, ..., i0 a^(m-1) needs only the m + d - 1 residues
+//    P[t] = i0 a^t mod n -- one Shoup modmul per step instead of one residue
+//    step per point-dim; the inner sums of the chain are a sliding
+//    correlation of the coefficients with P;
+//  * mirror: x(n - i) = 1 - x(i) for i != 0, so the linear (or centred
+//    quadratic) form of the mirror point follows from the same sums.
+// The nonzero points are enumerated as g^s a^e (g a primitive root, cosets s
+// of <a>) over half of the exponents, mirrors covering the rest; point 0 is
+// added once by chain 0.
+struct OrbHead {
+    uint32_t n, a, as;      // modulus, Korobov base, Shoup constant floor(a 2^32 / n)
+    int32_t dpad;           // coefficient count padded to a multiple of the chain length
+    uint64_t units;         // chains
+    uint32_t qc, h;         // chains per coset, exponents per coset
+    const uint32_t* G;      // coset representatives g^s
+    const uint32_t* Alo;    // a^(m q) for q < 4096
+    const uint32_t* Ahi;    // a^(m 4096 q)
+    double alpha, alphaB, scale, bsum, K, A, B, C0, kappa, M, half;
+};
+
+constexpr int kOrbParamBytes = 32000;
+constexpr int kOrbLinDims = (kOrbParamBytes - (int)sizeof(OrbHead)) / 8 / 24 * 24;
+constexpr int kOrbQuadDims = (kOrbParamBytes - (int)sizeof(OrbHead)) / 16 / 24 * 24;
+#ifndef LQ_ORB_LIN_M
+#define LQ_ORB_LIN_M 24
+#endif
+#ifndef LQ_ORB_QUAD_M
+#define LQ_ORB_QUAD_M 12
+#endif
+__host__ __device__ constexpr int orb_len(int kind) { return kind == 1 ? LQ_ORB_QUAD_M : LQ_ORB_LIN_M; }
+
+struct OrbLinArgs {
+    OrbHead h;
+    double c[kOrbLinDims];        // beta_j / n * 2^(1074 - sigma), zero padded
+};
+struct OrbQuadArgs {
+    OrbHead h;
+    double2 bq[kOrbQuadDims];     // ((beta_j + gamma_j) 2^sigma, gamma_j 2^(2 sigma)), zero padded
+};
+
+__device__ __forceinline__ uint32_t mulmod32(uint32_t x, uint32_t y, uint32_t n) {
+    return (uint32_t)(((uint64_t)x * y) % n);
+}
+
+template <int OUTER>
+__device__ __noinline__ double outer_pair(double acc, const LinParams p, const double alphaB, const double bsum,
+                                          bool two) {
+    if (OUTER == OUT_EXP) {
+        const double f1 = p.K * exp(fma(acc, p.scale, p.alpha)), f2 = p.K * exp(fma(-acc, p.scale, alphaB));
+        return two ? f1 + f2 : f1;
+    }
+    if (OUTER == OUT_EXPABS) {
+        const double f1 = p.K * exp(p.kappa * fabs(fma(acc, p.scale, p.alpha)));
+        const double f2 = p.K * exp(p.kappa * fabs(fma(-acc, p.scale, alphaB)));
+        return two ? f1 + f2 : f1;
+    }
+    const double l1 = acc * p.scale, l2 = bsum - l1;
+    double s1, c1, s2, c2;
+    sincos(l1, &s1, &c1);
+    sincos(l2, &s2, &c2);
+    const double f1 = p.C0 + p.A * s1 + p.B * c1, f2 = p.C0 + p.A * s2 + p.B * c2;
+    return two ? f1 + f2 : f1;
+}
+
+// sum of f over the point and its mirror: exp(alpha' + even +- odd)
+__device__ __noinline__ double quad_pair(double odd, double even, double alphaC, double K, bool two) {
+    const double t = alphaC + even;
+    const double f1 = K * exp(t + odd), f2 = K * exp(t - odd);
+    return two ? f1 + f2 : f1;
+}
+
+// One thread = one chain of M points (and their mirrors); 256 chains per CTA.
+// tile_out[blockIdx.x] = sum over the CTA's chains (fixed tree); chain units
+// [unit0 + 256 b, unit0 + 256 (b + 1)).
+template <int KIND, int OUTER, class Args>
+__global__ void __launch_bounds__(kThreads, 2) k_orbit(const __grid_constant__ Args a, uint64_t unit0,
+                                                        uint32_t hmask, double* __restrict__ tile_out) {
+    constexpr int M = orb_len(KIND);
+    __shared__ double sh[8];
+    const OrbHead& H = a.h;
+    const uint32_t n = H.n;
+    const uint64_t u = unit0 + (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+    double s = 0.0;
+    if (u < H.units) {
+        const uint32_t cs = (uint32_t)(u / H.qc), q = (uint32_t)(u - (uint64_t)cs * H.qc);
+        const uint32_t i0 = mulmod32(mulmod32(H.G[cs], H.Alo[q & 4095u], n), H.Ahi[q >> 12], n);
+        const int valid = (int)min((uint32_t)M, H.h - q * (uint32_t)M);
+        const uint32_t za = H.a, zs = H.as;
+        if constexpr (KIND == FAM_LIN) {
+            uint32_t W[M], Z[M];
+            double acc[M];
+            W[0] = i0;
+            #pragma unroll
+            for (int k = 0; k < M; ++k) {
+                Z[k] = (threadIdx.x + k) & hmask;   // opaque zeros (hi words of the denormals)
+                acc[k] = 0.0;
+                if (k) W[k] = mulmod_shoup(W[k - 1], za, zs, n);
+            }
+            #pragma unroll 1
+            for (int j0 = 0; j0 < H.dpad; j0 += M) {
+                #pragma unroll
+                for (int v = 0; v < M; ++v) {
+                    const double c = a.c[j0 + v];
+                    #pragma unroll
+                    for (int k = 0; k < M; ++k) acc[k] = fma(c, denorm_of(W[(v + k) % M], Z[(v + k) % M]), acc[k]);
+                    W[v] = mulmod_shoup(W[(v + M - 1) % M], za, zs, n);
+                }
+            }
+            const LinParams prm{H.alpha, H.scale, H.K, H.A, H.B, H.C0, H.kappa};
+            #pragma unroll
+            for (int k = 0; k < M; ++k)
+                s += k < valid ? outer_pair<OUTER>(acc[k], prm, H.alphaB, H.bsum, true) : 0.0;
+            if (u == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
+        } else {
+            const double Ms = H.M, hf = H.half;
+            double U[M], V[M], ao[M], ae[M];
+            uint32_t r = i0;
+            const uint32_t zero = threadIdx.x & hmask;
+            #pragma unroll
+            for (int k = 0; k < M; ++k) {
+                const double x = fma(denorm_of(r, zero), Ms, -hf);
+                U[k] = x;
+                V[k] = x * x;
+                ao[k] = 0.0;
+                ae[k] = 0.0;
+                r = mulmod_shoup(r, za, zs, n);
+            }
+            #pragma unroll 1
+            for (int j0 = 0; j0 < H.dpad; j0 += M) {
+                #pragma unroll
+                for (int v = 0; v < M; ++v) {
+                    const double2 bq = a.bq[j0 + v];
+                    #pragma unroll
+                    for (int k = 0; k < M; ++k) {
+                        ao[k] = fma(bq.x, U[(v + k) % M], ao[k]);
+                        ae[k] = fma(bq.y, V[(v + k) % M], ae[k]);
+                    }
+                    const double x = fma(denorm_of(r, zero), Ms, -hf);
+                    U[v] = x;
+                    V[v] = x * x;
+                    r = mulmod_shoup(r, za, zs, n);
+                }
+            }
+            #pragma unroll
+            for (int k = 0; k < M; ++k) s += k < valid ? quad_pair(ao[k], ae[k], H.alphaB, H.K, true) : 0.0;
+            if (u == 0) s += quad_outer(0.0, H.alpha, H.K);   // point 0
+        }
+    }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
+}
+
 // ============================================================ generic bytecode
 struct LatSrc32 {   // n <= 2^31: Shoup modmul per variable access
     uint32_t i, n;

@@ -87,11 +87,12 @@ def slr_integrate(f, rule, reference=None, group=None):
     h = N.lib()
     ctx = N.ctx(torch.cuda.current_device())
     _bind_stream(h, ctx)
-    _, S = N.lattice_layout(pi.struct, n)
+    z = rule.z_reduced_array()
+    S = N.lattice_layout(pi.struct, n, z).n_supers
     lo, hi = shard_range(S, rank, size)
     parts = torch.zeros(S, dtype=torch.float64, device="cuda")
     if hi > lo:
-        N.check(h.lq_lattice_partials(ctx, C.byref(pi.struct), n, N.as_ptr(rule.z_reduced_array()), lo, hi,
+        N.check(h.lq_lattice_partials(ctx, C.byref(pi.struct), n, N.as_ptr(z), lo, hi,
                                       C.c_void_p(parts.data_ptr() + 8 * lo)))
     exchange_disjoint(parts, group)
     out = C.c_double()

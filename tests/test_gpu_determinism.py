@@ -45,7 +45,7 @@ def test_sharded_partials_bit_identical(env, cid, shards):
     rule = lq.korobov_vector(cfg.plain_a, cfg.plain_n, cfg.d)
     pi = engine.plain_integrand(lq.parse(cfg.text, cfg.d), cfg.d)
     z = rule.z_reduced_array()
-    _, S = N.lattice_layout(pi.struct, rule.n)
+    S = N.lattice_layout(pi.struct, rule.n, z).n_supers
     if cid == 5:
         S_used = 16              # first 16 super-chunks (64 Mi points) keep the test short
     else:

@@ -257,13 +257,13 @@ def test_library_exports_every_declared_symbol():
     for name in sorted(names):
         assert hasattr(lib, name), name
     h = _native.lib()
-    assert h.lq_abi_version() == 1
+    assert h.lq_abi_version() == 2
     from paper_2404_08867_b200 import engine
     cfg = make_config(5)
     pi = engine.plain_integrand(lq.parse(cfg.text, cfg.d), cfg.d)
-    assert _native.lattice_layout(pi.struct, cfg.plain_n) == (6144, 342)
+    assert _native.lattice_layout(pi.struct, cfg.plain_n)[:3] == (6144, 342, cfg.plain_n)
     prog = engine.plain_integrand(lq.parse(cfg.text, cfg.d), cfg.d, force_program=True)
-    assert _native.lattice_layout(prog.struct, cfg.plain_n) == (4096, 512)
+    assert _native.lattice_layout(prog.struct, cfg.plain_n)[:3] == (4096, 512, cfg.plain_n)
 
 
 def test_error_mapping_without_gpu():
