@@ -269,23 +269,44 @@ void fill_head(A& a, int d, uint64_t n, uint64_t base, uint64_t end, double alph
     a.alpha = alpha; a.scale = scale; a.K = K; a.A = A_; a.B = B; a.C0 = C0; a.kappa = kappa; a.M = M;
 }
 
+// Per-dimension tables in kernel parameter space, sized to d: the launch copies
+// the whole parameter struct, so small-d integrands use small instantiations
+// (measured: cfg1, d = 8, 25.6 -> 12.7 us per launch with a 32 KB vs 4 KB struct).
+template <int KIND, int OUTER, class Dim, int N>
+int fam_param_launch(lq_ctx* c, const std::vector<Dim>& tab, int d, uint64_t n, uint64_t base, uint64_t end,
+                     int64_t ntiles, double alpha, double scale, double K, double A, double B, double C0,
+                     double kappa, double M, double* tiles_dev) {
+    using Args = lq::FamArgs<Dim, N>;
+    static thread_local Args args;
+    fill_head(args, d, n, base, end, alpha, scale, K, A, B, C0, kappa, M);
+    std::memcpy(args.dims, tab.data(), sizeof(Dim) * d);
+    if (N <= 32) return launch_fam_s<KIND, OUTER, Args, 1>(c, args, ntiles, tiles_dev);   // d < 64: no split
+    return launch_fam<KIND, OUTER>(c, args, ntiles, tiles_dev, n);
+}
+
+template <int KIND, int OUTER, class Dim>
+int fam_dispatch(lq_ctx* c, const std::vector<Dim>& tab, int d, uint64_t n, uint64_t base, uint64_t end,
+                 int64_t ntiles, double alpha, double scale, double K, double A, double B, double C0, double kappa,
+                 double M, double* tiles_dev) {
+#define LQ_FPL(N) fam_param_launch<KIND, OUTER, Dim, N>(c, tab, d, n, base, end, ntiles, alpha, scale, K, A, B, C0, kappa, M, tiles_dev)
+    if (d <= 32) return LQ_FPL(32);
+    if (d <= 128) return LQ_FPL(128);
+    if (d <= lq::kParamDims) return LQ_FPL(lq::kParamDims);
+#undef LQ_FPL
+    void* dt;
+    int rc;
+    if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(Dim), &dt))) return rc;
+    lq::FamArgsG<Dim> args;
+    fill_head(args, d, n, base, end, alpha, scale, K, A, B, C0, kappa, M);
+    args.dims = (const Dim*)dt;
+    return launch_fam<KIND, OUTER>(c, args, ntiles, tiles_dev, n);
+}
+
 template <int OUTER>
 int lin_dispatch(lq_ctx* c, const std::vector<lq::LinDim>& tab, int d, uint64_t n, uint64_t base, uint64_t end,
                  int64_t ntiles, const lq_integrand* f, double scale, double* tiles_dev) {
-    if (d <= lq::kParamDims) {
-        using Args = lq::FamArgs<lq::LinDim, lq::kParamDims>;
-        static thread_local Args args;
-        fill_head(args, d, n, base, end, f->alpha, scale, f->K, f->A, f->B, f->C0, f->kappa, 0.0);
-        std::memcpy(args.dims, tab.data(), sizeof(lq::LinDim) * d);
-        return launch_fam<lq::FAM_LIN, OUTER>(c, args, ntiles, tiles_dev, n);
-    }
-    void* dt;
-    int rc;
-    if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(lq::LinDim), &dt))) return rc;
-    lq::FamArgsG<lq::LinDim> args;
-    fill_head(args, d, n, base, end, f->alpha, scale, f->K, f->A, f->B, f->C0, f->kappa, 0.0);
-    args.dims = (const lq::LinDim*)dt;
-    return launch_fam<lq::FAM_LIN, OUTER>(c, args, ntiles, tiles_dev, n);
+    return fam_dispatch<lq::FAM_LIN, OUTER>(c, tab, d, n, base, end, ntiles, f->alpha, scale, f->K, f->A, f->B, f->C0,
+                                            f->kappa, 0.0, tiles_dev);
 }
 
 bool uses_family_kernel(const lq_integrand* f, uint64_t n) {
@@ -342,19 +363,8 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
             if (!std::isfinite(tab[j].b) || !std::isfinite(tab[j].q))
                 return fail(LQ_ERR_VALUE, "quadratic coefficient out of range");
         }
-        if (d <= lq::kParamDims) {
-            using Args = lq::FamArgs<lq::QuadDim, lq::kParamDims>;
-            static thread_local Args args;
-            fill_head(args, d, n, base, end, f->alpha, 1.0, f->K, 0, 0, 0, 0, M);
-            std::memcpy(args.dims, tab.data(), sizeof(lq::QuadDim) * d);
-            return launch_fam<lq::FAM_QUAD, 0>(c, args, ntiles, tiles_dev, n);
-        }
-        void* dt;
-        if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(lq::QuadDim), &dt))) return rc;
-        lq::FamArgsG<lq::QuadDim> args;
-        fill_head(args, d, n, base, end, f->alpha, 1.0, f->K, 0, 0, 0, 0, M);
-        args.dims = (const lq::QuadDim*)dt;
-        return launch_fam<lq::FAM_QUAD, 0>(c, args, ntiles, tiles_dev, n);
+        return fam_dispatch<lq::FAM_QUAD, 0>(c, tab, d, n, base, end, ntiles, f->alpha, 1.0, f->K, 0, 0, 0, 0, M,
+                                             tiles_dev);
     }
     // generic bytecode (any family falls back here for n > 2^31)
     const lq_program* pg = &f->prog;
@@ -515,8 +525,9 @@ std::shared_ptr<const OrbPlan> orbit_plan(uint32_t n, uint32_t a, int m) {
 }
 
 // LQ_ORBIT=0 disables the orbit kernel, =always uses it whenever the rule
-// allows; default: n >= 2^20 (below that the index kernels' dimension split
-// fills the GPU better).
+// allows; default: n >= 2^18 (measured: cfg3, n = 1e6, 0.066 vs 0.161 ms;
+// below ~1e5 points both are launch-latency bound and the index kernels'
+// dimension split is slightly faster: cfg2 0.034 vs 0.040 ms).
 int orbit_mode() {
     const char* e = std::getenv("LQ_ORBIT");
     if (!e || !*e) return 1;
@@ -528,7 +539,7 @@ int orbit_mode() {
 std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, const uint64_t* z) {
     const int mode = orbit_mode();
     if (mode == 0 || !z || f->kind == LQ_FAM_PROGRAM || f->d < 2) return nullptr;
-    if (n > (1ull << 31) || n < 5 || (mode == 1 && n < (1ull << 20))) return nullptr;
+    if (n > (1ull << 31) || n < 5 || (mode == 1 && n < (1ull << 18))) return nullptr;
     const bool quad = f->kind == LQ_FAM_QUAD_EXP;
     const int m = lq::orb_len(quad ? lq::FAM_QUAD : lq::FAM_LIN);
     const int cap = quad ? lq::kOrbQuadDims : lq::kOrbLinDims;

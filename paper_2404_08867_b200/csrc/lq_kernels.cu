@@ -110,7 +110,10 @@ __device__ __noinline__ double quad_outer(double acc, double alpha, double K) { 
 // they fit: the j-loop then reads c_j, z_j, zs_j as uniform-register operands
 // (LDCU), which frees the vector register file ports for the residue chain
 // (measured +30% over LDG-fed operands).
-constexpr int kParamDims = 1000;   // 1000 x 32 B + header < 32764 B of kernel parameters
+#ifndef LQ_PARAM_DIMS
+#define LQ_PARAM_DIMS 1000
+#endif
+constexpr int kParamDims = LQ_PARAM_DIMS;   // 1000 x 32 B + header < 32764 B of kernel parameters
 
 // Kernel arguments: everything the j-loop reads is warp-uniform and lives in
 // kernel parameter space, so ptxas keeps the loop counter and per-dimension
@@ -348,7 +351,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_orbit(const __grid_constant__ A
             W[0] = i0;
             #pragma unroll
             for (int k = 0; k < M; ++k) {
+#ifdef LQ_ORB_VZ
+                asm volatile("mov.b32 %0, 0;" : "=r"(Z[k]));   // opaque zeros (hi words of the denormals)
+#else
                 Z[k] = (threadIdx.x + k) & hmask;   // opaque zeros (hi words of the denormals)
+#endif
                 acc[k] = 0.0;
                 if (k) W[k] = mulmod_shoup(W[k - 1], za, zs, n);
             }
