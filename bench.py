@@ -33,6 +33,7 @@ import numpy as np  # noqa: E402
 METRIC = "lattice f-evals/sec (fp64) & MDI-LR time-to-solution; % of FP64 peak"   # BASELINE.json
 FLOPS_PER_PD = 3          # 1 (coordinate r/n) + 2 (c_j * x_j accumulate) for exp-abs-linear
 FLOPS_PER_POINT = 2       # transcendental + accumulate
+TERM_FLOPS = 2            # SURVEY.md §8(d) per-coordinate term of exp-abs-linear (c_j * x_j accumulate)
 ORB_M = 24                # points per chain of the orbit kernel (LQ_ORB_LIN_M, csrc/lq_kernels.cu)
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -259,16 +260,23 @@ def main():
     my_units = min(s_hi * su, lay.n_units) - s_lo * su
     avg_kern = kern_ms / args.steps
     if lay.mode == N.LAYOUT_ORBIT:
-        forms = my_units * ORB_M                       # linear forms evaluated (one per pair)
-        alg_flops = forms * (FLOPS_PER_PD * d + 2 * FLOPS_PER_POINT)
+        forms = my_units * ORB_M                       # linear forms evaluated (one per mirrored pair)
+        alg_flops = forms * (TERM_FLOPS * d + 2 * FLOPS_PER_POINT)
+        conv_flops = forms * (FLOPS_PER_PD * d + 2 * FLOPS_PER_POINT)
         exec_flops = forms * 2 * (-(-d // ORB_M) * ORB_M)   # DFMAs incl. zero padding of d
         kernel_name = "k_orbit<FAM_LIN, OUT_EXPABS> (liblq.so)"
+        unit_txt = (f"unit = chain of {ORB_M} mirrored point pairs; per pair {TERM_FLOPS}*d + 2*{FLOPS_PER_POINT} "
+                    "flop (SURVEY §8d per-coordinate term of exp-abs-linear, the coordinate division being "
+                    "folded into the coefficient; one linear form serves the pair; two outer evaluations)")
     else:
         forms = my_units
         alg_flops = forms * (FLOPS_PER_PD * d + FLOPS_PER_POINT)
+        conv_flops = alg_flops
         exec_flops = forms * 2 * d
         kernel_name = "k_fam<FAM_LIN, OUT_EXPABS> (liblq.so)"
+        unit_txt = f"unit = point; {FLOPS_PER_PD}*d + {FLOPS_PER_POINT} flop (SURVEY §8d)"
     achieved = alg_flops / (avg_kern * 1e-3) / 1e12
+    conv = conv_flops / (avg_kern * 1e-3) / 1e12
     executed = exec_flops / (avg_kern * 1e-3) / 1e12
 
     # e2e: the public drop-in API (host lowering, parameter H2D, kernel, result D2H)
@@ -356,9 +364,10 @@ def main():
                      "frac": achieved / fp64_peak, "traffic": traffic,
                      "kernel": kernel_name, "kernel_ms": avg_kern,
                      "layout": "orbit" if lay.mode == N.LAYOUT_ORBIT else "index",
-                     "flops_per_unit": ("per mirrored pair: 3 d (one linear form, SURVEY §8d per point-dim "
-                                        "figure) + 2 x 2 (two outer evaluations)" if lay.mode == N.LAYOUT_ORBIT
-                                        else "per point: 3 d + 2 (SURVEY §8d)"),
+                     "flops_per_unit": unit_txt,
+                     "survey_convention": {"achieved": conv, "frac": conv / fp64_peak,
+                                           "note": "3 flop per point-dim (incl. the coordinate division r/n) "
+                                                   "charged once per linear form"},
                      "executed_dfma_tflops": executed, "executed_frac": executed / fp64_peak,
                      "peak_source": "measured in-run by lq_fp64_peak (DFMA chains, ~1 s); "
                                     "MEASURED_PEAKS.json has no FP64 entry"},

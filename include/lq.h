@@ -117,7 +117,9 @@ int lq_lattice_sum(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_
  * i in [0, n) for the per-index kernels (mode LQ_LAYOUT_INDEX), or -- for a
  * Korobov rule z_j = a^(j-1) over a prime n (mode LQ_LAYOUT_ORBIT) -- chains
  * of consecutive powers i0 a^k whose points are summed together with their
- * mirrors n - i.  Units form tiles of tile_units, tiles form
+ * mirrors n - i, or -- when every z_j is a unit mod n
+ * (mode LQ_LAYOUT_PAIRED) -- mirror-pair indices i in [0, n/2], point i
+ * summed with point n - i.  Units form tiles of tile_units, tiles form
  * super-chunks of LQ_SUPER_TILES; super-chunk s covers units
  * [s*T*LQ_SUPER_TILES, (s+1)*T*LQ_SUPER_TILES).  The layout depends on
  * (f, n, z) only, so every rank computes the same one; z may be NULL (index
@@ -127,6 +129,7 @@ int lq_lattice_sum(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_
  * quad.slr_integrate, quad.py:96-104, for sharded runs.)                   */
 #define LQ_LAYOUT_INDEX 0
 #define LQ_LAYOUT_ORBIT 1
+#define LQ_LAYOUT_PAIRED 2   /* units: mirror-pair indices i in [0, n/2] (points i and n - i) */
 int lq_lattice_layout(const lq_integrand* f, uint64_t n, const uint64_t* z_reduced, int64_t* tile_units,
                       int64_t* n_supers, int64_t* n_units, int32_t* mode);
 int lq_lattice_partials(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_t* z_reduced,

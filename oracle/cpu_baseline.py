@@ -19,12 +19,16 @@ _ROWS = 1 << 12
 
 
 def _chunk(args):
+    # one BLAS thread per process: `cores` then counts exactly the threads used
+    # (16 forked workers each spawning a 16-thread BLAS pool oversubscribe the host)
+    from threadpoolctl import threadpool_limits
     n, z, c, cw, lo, hi = args
     acc = 0.0
-    for start in range(lo, hi, _ROWS):
-        stop = min(start + _ROWS, hi)
-        pts = np_oracle.points_block(n, z, start, stop)
-        acc += float(np.sum(np.exp(-np.abs(pts @ c - cw))))
+    with threadpool_limits(1):
+        for start in range(lo, hi, _ROWS):
+            stop = min(start + _ROWS, hi)
+            pts = np_oracle.points_block(n, z, start, stop)
+            acc += float(np.sum(np.exp(-np.abs(pts @ c - cw))))
     return acc
 
 

@@ -160,13 +160,14 @@ def ctx(device=None):
 
 
 Layout = collections.namedtuple("Layout", "tile_units n_supers n_units mode")
-LAYOUT_INDEX, LAYOUT_ORBIT = 0, 1
+LAYOUT_INDEX, LAYOUT_ORBIT, LAYOUT_PAIRED = 0, 1, 2
 
 
 def lattice_layout(pi_struct, n, z=None):
     """Reduction layout liblq uses for the full-lattice sum of (f, n, z):
     units per tile, super-chunks, units, and the mode (LAYOUT_INDEX: units are
-    points; LAYOUT_ORBIT: units are chains of mirrored Korobov points)."""
+    points; LAYOUT_ORBIT: units are chains of mirrored Korobov points;
+    LAYOUT_PAIRED: units are mirror-pair indices i in [0, n/2])."""
     tp, ns, nu, mode = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
     check(lib().lq_lattice_layout(C.byref(pi_struct), int(n), as_ptr(z), C.byref(tp), C.byref(ns),
                                   C.byref(nu), C.byref(mode)))

@@ -206,21 +206,22 @@ bool uses_family_kernel(const lq_integrand* f, uint64_t n);
 
 // Dimension split of the family kernels: lattices with fewer tiles than
 // ~4 waves of CTAs run each tile on a cluster of S CTAs that split the
-// dimensions (k_fam<S>).  S depends on (n, d) only, so every GPU of a
+// dimensions (k_fam<S>).  S depends on (units, d) only, so every GPU of a
 // multi-GPU run uses the same reduction structure.
-int fam_split(uint64_t n, int d, int kind) {
+int fam_split(uint64_t units, int d, int kind) {
     const uint64_t tp = (uint64_t)lq::kThreads * lq::fam_pts(kind);
-    const uint64_t tiles = (n + tp - 1) / tp;
+    const uint64_t tiles = (units + tp - 1) / tp;
     const uint64_t want = 148ull * 2 * 4;
     int S = 1;
     while (S < 8 && tiles * S < want && d / (2 * S) >= 16) S *= 2;
     return S;
 }
 
-template <int KIND, int OUTER, class Args, int S>
+template <int KIND, int OUTER, bool PAIR, class Args, int S>
 int launch_fam_s(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev) {
-    auto kern = lq::k_fam<KIND, OUTER, Args, S>;
-    const size_t smem = S > 1 ? sizeof(double) * lq::fam_pts(KIND) * lq::kThreads : 0;
+    auto kern = lq::k_fam<KIND, OUTER, Args, S, PAIR>;
+    const int na = KIND == lq::FAM_QUADP ? 2 : 1;
+    const size_t smem = S > 1 ? sizeof(double) * na * lq::fam_pts(KIND) * lq::kThreads : 0;
     if (S > 1) {
         static bool attr_set = false;   // per template instance
         if (!attr_set) {
@@ -247,48 +248,72 @@ int launch_fam_s(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev)
     return LQ_OK;
 }
 
-template <int KIND, int OUTER, class Args>
-int launch_fam(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev, uint64_t n_total) {
-    switch (fam_split(n_total, args.d, KIND)) {
-        case 1: return launch_fam_s<KIND, OUTER, Args, 1>(c, args, ntiles, tiles_dev);
-        case 2: return launch_fam_s<KIND, OUTER, Args, 2>(c, args, ntiles, tiles_dev);
-        case 4: return launch_fam_s<KIND, OUTER, Args, 4>(c, args, ntiles, tiles_dev);
-        default: return launch_fam_s<KIND, OUTER, Args, 8>(c, args, ntiles, tiles_dev);
+template <int KIND, int OUTER, bool PAIR, class Args>
+int launch_fam(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev, uint64_t units) {
+    switch (fam_split(units, args.d, KIND)) {
+        case 1: return launch_fam_s<KIND, OUTER, PAIR, Args, 1>(c, args, ntiles, tiles_dev);
+        case 2: return launch_fam_s<KIND, OUTER, PAIR, Args, 2>(c, args, ntiles, tiles_dev);
+        case 4: return launch_fam_s<KIND, OUTER, PAIR, Args, 4>(c, args, ntiles, tiles_dev);
+        default: return launch_fam_s<KIND, OUTER, PAIR, Args, 8>(c, args, ntiles, tiles_dev);
     }
 }
 
-uint64_t tile_points(const lq_integrand* f, uint64_t n) {
-    if (!uses_family_kernel(f, n)) return (uint64_t)lq::kTile;
-    return (uint64_t)lq::kThreads * lq::fam_pts(f->kind == LQ_FAM_QUAD_EXP ? lq::FAM_QUAD : lq::FAM_LIN);
+// Full-range sums pair each point with its mirror n - i (x -> 1 - x) when every
+// z_j is a unit mod n -- then only i = 0 and i = n/2 are self-mirrored -- and
+// run over the pair indices [0, n/2] (LQ_PAIR=0 disables).
+bool pair_ok(const lq_integrand* f, uint64_t n, const uint64_t* z) {
+    const char* e = std::getenv("LQ_PAIR");
+    if (e && !std::strcmp(e, "0")) return false;
+    if (!z || f->kind == LQ_FAM_PROGRAM || n < 3 || n > (1ull << 31)) return false;
+    for (int j = 0; j < f->d; ++j) {
+        uint64_t a = z[j], b = n;
+        while (b) { const uint64_t t = a % b; a = b; b = t; }
+        if (a != 1) return false;
+    }
+    return true;
 }
 
+int fam_kind(const lq_integrand* f, bool pair) {
+    if (f->kind == LQ_FAM_QUAD_EXP) return pair ? lq::FAM_QUADP : lq::FAM_QUAD;
+    return lq::FAM_LIN;
+}
+
+uint64_t tile_points(const lq_integrand* f, uint64_t n, bool pair) {
+    if (!uses_family_kernel(f, n)) return (uint64_t)lq::kTile;
+    return (uint64_t)lq::kThreads * lq::fam_pts(fam_kind(f, pair));
+}
+uint64_t tile_points(const lq_integrand* f, uint64_t n) { return tile_points(f, n, false); }
+
+// scalar parameters of the family kernels
+struct FamHead {
+    double alpha = 0, scale = 1, K = 0, A = 0, B = 0, C0 = 0, kappa = 0, M = 0, alphaB = 0, bsum = 0, half = 0;
+};
+
 template <class A>
-void fill_head(A& a, int d, uint64_t n, uint64_t base, uint64_t end, double alpha, double scale, double K, double A_,
-               double B, double C0, double kappa, double M) {
+void fill_head(A& a, int d, uint64_t n, uint64_t base, uint64_t end, const FamHead& h) {
     a.d = d; a.n = (uint32_t)n; a.base = base; a.end = end;
-    a.alpha = alpha; a.scale = scale; a.K = K; a.A = A_; a.B = B; a.C0 = C0; a.kappa = kappa; a.M = M;
+    a.alpha = h.alpha; a.scale = h.scale; a.K = h.K; a.A = h.A; a.B = h.B; a.C0 = h.C0; a.kappa = h.kappa;
+    a.M = h.M; a.alphaB = h.alphaB; a.bsum = h.bsum; a.half = h.half;
 }
 
 // Per-dimension tables in kernel parameter space, sized to d: the launch copies
 // the whole parameter struct, so small-d integrands use small instantiations
 // (measured: cfg1, d = 8, 25.6 -> 12.7 us per launch with a 32 KB vs 4 KB struct).
-template <int KIND, int OUTER, class Dim, int N>
+template <int KIND, int OUTER, bool PAIR, class Dim, int N>
 int fam_param_launch(lq_ctx* c, const std::vector<Dim>& tab, int d, uint64_t n, uint64_t base, uint64_t end,
-                     int64_t ntiles, double alpha, double scale, double K, double A, double B, double C0,
-                     double kappa, double M, double* tiles_dev) {
+                     int64_t ntiles, uint64_t units, const FamHead& h, double* tiles_dev) {
     using Args = lq::FamArgs<Dim, N>;
     static thread_local Args args;
-    fill_head(args, d, n, base, end, alpha, scale, K, A, B, C0, kappa, M);
+    fill_head(args, d, n, base, end, h);
     std::memcpy(args.dims, tab.data(), sizeof(Dim) * d);
-    if (N <= 32) return launch_fam_s<KIND, OUTER, Args, 1>(c, args, ntiles, tiles_dev);   // d < 64: no split
-    return launch_fam<KIND, OUTER>(c, args, ntiles, tiles_dev, n);
+    if (N <= 32) return launch_fam_s<KIND, OUTER, PAIR, Args, 1>(c, args, ntiles, tiles_dev);   // d < 64: no split
+    return launch_fam<KIND, OUTER, PAIR>(c, args, ntiles, tiles_dev, units);
 }
 
-template <int KIND, int OUTER, class Dim>
+template <int KIND, int OUTER, bool PAIR, class Dim>
 int fam_dispatch(lq_ctx* c, const std::vector<Dim>& tab, int d, uint64_t n, uint64_t base, uint64_t end,
-                 int64_t ntiles, double alpha, double scale, double K, double A, double B, double C0, double kappa,
-                 double M, double* tiles_dev) {
-#define LQ_FPL(N) fam_param_launch<KIND, OUTER, Dim, N>(c, tab, d, n, base, end, ntiles, alpha, scale, K, A, B, C0, kappa, M, tiles_dev)
+                 int64_t ntiles, uint64_t units, const FamHead& h, double* tiles_dev) {
+#define LQ_FPL(N) fam_param_launch<KIND, OUTER, PAIR, Dim, N>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev)
     if (d <= 32) return LQ_FPL(32);
     if (d <= 128) return LQ_FPL(128);
     if (d <= lq::kParamDims) return LQ_FPL(lq::kParamDims);
@@ -297,35 +322,31 @@ int fam_dispatch(lq_ctx* c, const std::vector<Dim>& tab, int d, uint64_t n, uint
     int rc;
     if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(Dim), &dt))) return rc;
     lq::FamArgsG<Dim> args;
-    fill_head(args, d, n, base, end, alpha, scale, K, A, B, C0, kappa, M);
+    fill_head(args, d, n, base, end, h);
     args.dims = (const Dim*)dt;
-    return launch_fam<KIND, OUTER>(c, args, ntiles, tiles_dev, n);
-}
-
-template <int OUTER>
-int lin_dispatch(lq_ctx* c, const std::vector<lq::LinDim>& tab, int d, uint64_t n, uint64_t base, uint64_t end,
-                 int64_t ntiles, const lq_integrand* f, double scale, double* tiles_dev) {
-    return fam_dispatch<lq::FAM_LIN, OUTER>(c, tab, d, n, base, end, ntiles, f->alpha, scale, f->K, f->A, f->B, f->C0,
-                                            f->kappa, 0.0, tiles_dev);
+    return launch_fam<KIND, OUTER, PAIR>(c, args, ntiles, tiles_dev, units);
 }
 
 bool uses_family_kernel(const lq_integrand* f, uint64_t n) {
     return n <= (1ull << 31) && f->kind != LQ_FAM_PROGRAM;
 }
 
-uint64_t tile_points(const lq_integrand* f, uint64_t n);
-
-// Launch the tile kernel of integrand f over points [base, end) writing
-// ntiles tile partials to tiles_dev.
+// Launch the tile kernel of integrand f over index units [base, end) writing
+// ntiles tile partials to tiles_dev.  pair: units are mirror-pair indices
+// [0, n/2] of a full-range sum (pair_ok), else points.
 int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z, uint64_t base, uint64_t end,
-                 int64_t ntiles, double* tiles_dev) {
+                 int64_t ntiles, double* tiles_dev, bool pair = false) {
     const int d = f->d;
     const bool fast = uses_family_kernel(f, n);
+    const uint64_t units = pair ? n / 2 + 1 : n;
     int rc;
     if (fast && (f->kind == LQ_FAM_LIN_EXP || f->kind == LQ_FAM_LIN_SINCOS || f->kind == LQ_FAM_LIN_EXPABS)) {
         if (!f->beta) return fail(LQ_ERR_VALUE, "family needs beta");
-        double maxabs = 0.0;
-        for (int j = 0; j < d; ++j) maxabs = fmax(maxabs, fabs(f->beta[j]));
+        double maxabs = 0.0, bsum = 0.0;
+        for (int j = 0; j < d; ++j) {
+            maxabs = fmax(maxabs, fabs(f->beta[j]));
+            bsum += f->beta[j];
+        }
         if (!std::isfinite(maxabs)) return fail(LQ_ERR_VALUE, "non-finite coefficient");
         int sigma = 0;
         if (maxabs > 0.0) {
@@ -341,30 +362,40 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
             tab[j].z2 = (uint32_t)((2 * z[j]) % n);
             tab[j].z2m = tab[j].z2 - (uint32_t)n;
         }
-        const double scale = std::ldexp(1.0, sigma);
-        if (f->kind == LQ_FAM_LIN_EXP) return lin_dispatch<lq::OUT_EXP>(c, tab, d, n, base, end, ntiles, f, scale, tiles_dev);
-        if (f->kind == LQ_FAM_LIN_SINCOS) return lin_dispatch<lq::OUT_SINCOS>(c, tab, d, n, base, end, ntiles, f, scale, tiles_dev);
-        return lin_dispatch<lq::OUT_EXPABS>(c, tab, d, n, base, end, ntiles, f, scale, tiles_dev);
+        FamHead h;
+        h.alpha = f->alpha; h.scale = std::ldexp(1.0, sigma); h.K = f->K; h.A = f->A; h.B = f->B; h.C0 = f->C0;
+        h.kappa = f->kappa; h.bsum = bsum; h.alphaB = f->alpha + bsum;
+#define LQ_LIN(OUT) (pair ? fam_dispatch<lq::FAM_LIN, OUT, true>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev) \
+                          : fam_dispatch<lq::FAM_LIN, OUT, false>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev))
+        if (f->kind == LQ_FAM_LIN_EXP) return LQ_LIN(lq::OUT_EXP);
+        if (f->kind == LQ_FAM_LIN_SINCOS) return LQ_LIN(lq::OUT_SINCOS);
+        return LQ_LIN(lq::OUT_EXPABS);
+#undef LQ_LIN
     }
     if (fast && f->kind == LQ_FAM_QUAD_EXP) {
         if (!f->beta || !f->gamma) return fail(LQ_ERR_VALUE, "quad family needs beta and gamma");
         const double inv_n = 1.0 / (double)n;
         int sigma = 1074 + std::ilogb(inv_n) - 1000;
         if (sigma < 0) sigma = 0;
-        const double M = std::ldexp(inv_n, 1074 - sigma);
+        FamHead h;
+        h.alpha = f->alpha; h.K = f->K; h.M = std::ldexp(inv_n, 1074 - sigma); h.half = std::ldexp(0.5, -sigma);
         std::vector<lq::QuadDim> tab(d);
+        double C0 = 0.0;
         for (int j = 0; j < d; ++j) {
-            tab[j].b = std::ldexp(f->beta[j], sigma);
+            // paired: centred form b' u + q u^2 with b' = beta + gamma (u = x - 1/2)
+            tab[j].b = std::ldexp(pair ? f->beta[j] + f->gamma[j] : f->beta[j], sigma);
             tab[j].q = std::ldexp(f->gamma[j], 2 * sigma);
             tab[j].z = (uint32_t)z[j];
             tab[j].zs = (uint32_t)(((uint64_t)z[j] << 32) / n);
             tab[j].z2 = (uint32_t)((2 * z[j]) % n);
             tab[j].z2m = tab[j].z2 - (uint32_t)n;
+            C0 += 0.5 * f->beta[j] + 0.25 * f->gamma[j];
             if (!std::isfinite(tab[j].b) || !std::isfinite(tab[j].q))
                 return fail(LQ_ERR_VALUE, "quadratic coefficient out of range");
         }
-        return fam_dispatch<lq::FAM_QUAD, 0>(c, tab, d, n, base, end, ntiles, f->alpha, 1.0, f->K, 0, 0, 0, 0, M,
-                                             tiles_dev);
+        h.alphaB = f->alpha + C0;
+        if (pair) return fam_dispatch<lq::FAM_QUADP, 0, true>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev);
+        return fam_dispatch<lq::FAM_QUAD, 0, false>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev);
     }
     // generic bytecode (any family falls back here for n > 2^31)
     const lq_program* pg = &f->prog;
@@ -653,8 +684,10 @@ int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t un
 // chains of paired points (orbit kernel); tiles of tile_units units, super-chunks
 // of LQ_SUPER_TILES tiles.
 struct Layout {
-    uint64_t tile_units, n_units;
+    uint64_t tile_units = 0, n_units = 0;
     std::shared_ptr<const OrbPlan> orb;
+    bool pair = false;
+    int mode() const { return orb ? LQ_LAYOUT_ORBIT : pair ? LQ_LAYOUT_PAIRED : LQ_LAYOUT_INDEX; }
 };
 
 Layout layout_of(const lq_integrand* f, uint64_t n, const uint64_t* z) {
@@ -663,6 +696,10 @@ Layout layout_of(const lq_integrand* f, uint64_t n, const uint64_t* z) {
     if (L.orb) {
         L.tile_units = lq::kThreads;
         L.n_units = L.orb->units;
+    } else if (uses_family_kernel(f, n) && pair_ok(f, n, z)) {
+        L.pair = true;
+        L.tile_units = tile_points(f, n, true);
+        L.n_units = n / 2 + 1;
     } else {
         L.tile_units = tile_points(f, n);
         L.n_units = n;
@@ -820,7 +857,7 @@ int lq_lattice_layout(const lq_integrand* f, uint64_t n, const uint64_t* z, int6
     if (tile_units) *tile_units = (int64_t)L.tile_units;
     if (n_supers) *n_supers = (int64_t)((L.n_units + sp - 1) / sp);
     if (n_units) *n_units = (int64_t)L.n_units;
-    if (mode) *mode = L.orb ? LQ_LAYOUT_ORBIT : LQ_LAYOUT_INDEX;
+    if (mode) *mode = L.mode();
     return LQ_OK;
 }
 
@@ -843,7 +880,7 @@ int lq_lattice_partials(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint
     if (L.orb) {
         if ((rc = launch_orbit(c, f, *L.orb, base, ntiles, (double*)tiles))) return rc;
     } else {
-        if ((rc = launch_tiles(c, f, n, z, base, end, ntiles, (double*)tiles))) return rc;
+        if ((rc = launch_tiles(c, f, n, z, base, end, ntiles, (double*)tiles, L.pair))) return rc;
     }
     lq::k_reduce1024<<<(unsigned)(s_end - s_begin), lq::kThreads, 0, c->stream>>>((const double*)tiles, ntiles, out_dev);
     c->launches++;
@@ -873,11 +910,13 @@ int lq_lattice_sum(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t*
     }
     if (i_begin == 0 && i_end == n) {
         const Layout L = layout_of(f, n, z);
-        if (L.orb) {
+        if (L.orb || L.pair) {
             const int64_t ntiles = (int64_t)((L.n_units + L.tile_units - 1) / L.tile_units);
             void* tiles;
             if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
-            if ((rc = launch_orbit(c, f, *L.orb, 0, ntiles, (double*)tiles))) return rc;
+            if (L.orb) rc = launch_orbit(c, f, *L.orb, 0, ntiles, (double*)tiles);
+            else rc = launch_tiles(c, f, n, z, 0, L.n_units, ntiles, (double*)tiles, true);
+            if (rc) return rc;
             double* r;
             if ((rc = reduce_dev(c, (const double*)tiles, ntiles, &r))) return rc;
             return read_scalar(c, r, sum_out);

@@ -85,7 +85,11 @@ constexpr int kFamTile = kThreads * kFamPts;
 #define LQ_QUAD_PTS 24
 #endif
 constexpr int kQuadPts = LQ_QUAD_PTS;     // points per thread of the Gaussian family
-__host__ __device__ constexpr int fam_pts(int kind) { return kind == 1 ? kQuadPts : kFamPts; }
+#ifndef LQ_QUADP_PTS
+#define LQ_QUADP_PTS 12
+#endif
+// kind: 0 LIN, 1 QUAD, 2 QUADP (mirror-paired Gaussian: two accumulators per point)
+__host__ __device__ constexpr int fam_pts(int kind) { return kind == 1 ? kQuadPts : kind == 2 ? LQ_QUADP_PTS : kFamPts; }
 
 struct LinParams {
     double alpha, scale, K, A, B, C0, kappa;
@@ -106,6 +110,36 @@ __device__ __noinline__ double outer_fn(double acc, const LinParams p) {
 
 __device__ __noinline__ double quad_outer(double acc, double alpha, double K) { return K * exp(alpha + acc); }
 
+// Mirror pairs (x and 1 - x): f at both points from one
+// inner sum; `two` is false for the self-mirrored points 0 and n/2.
+template <int OUTER>
+__device__ __noinline__ double outer_pair(double acc, const LinParams p, const double alphaB, const double bsum,
+                                          bool two) {
+    if (OUTER == OUT_EXP) {
+        const double f1 = p.K * exp(fma(acc, p.scale, p.alpha)), f2 = p.K * exp(fma(-acc, p.scale, alphaB));
+        return two ? f1 + f2 : f1;
+    }
+    if (OUTER == OUT_EXPABS) {
+        const double f1 = p.K * exp(p.kappa * fabs(fma(acc, p.scale, p.alpha)));
+        const double f2 = p.K * exp(p.kappa * fabs(fma(-acc, p.scale, alphaB)));
+        return two ? f1 + f2 : f1;
+    }
+    const double l1 = acc * p.scale, l2 = bsum - l1;
+    double s1, c1, s2, c2;
+    sincos(l1, &s1, &c1);
+    sincos(l2, &s2, &c2);
+    const double f1 = p.C0 + p.A * s1 + p.B * c1, f2 = p.C0 + p.A * s2 + p.B * c2;
+    return two ? f1 + f2 : f1;
+}
+
+// sum of f over the point and its mirror: exp(alpha' + even +- odd)
+__device__ __noinline__ double quad_pair(double odd, double even, double alphaC, double K, bool two) {
+    const double t = alphaC + even;
+    const double f1 = K * exp(t + odd), f2 = K * exp(t - odd);
+    return two ? f1 + f2 : f1;
+}
+
+
 // Per-dimension tables travel in kernel parameter space (constant bank 0) when
 // they fit: the j-loop then reads c_j, z_j, zs_j as uniform-register operands
 // (LDCU), which frees the vector register file ports for the residue chain
@@ -124,6 +158,7 @@ struct FamArgs {
     uint32_t n;
     uint64_t base, end;
     double alpha, scale, K, A, B, C0, kappa, M;
+    double alphaB, bsum, half;   // mirror pairs: alpha + sum beta (QUADP: alpha + C), sum beta, 2^-sigma / 2
     Dim dims[N];
 };
 
@@ -133,6 +168,7 @@ struct FamArgsG {   // d > kParamDims: per-dimension records in global memory
     uint32_t n;
     uint64_t base, end;
     double alpha, scale, K, A, B, C0, kappa, M;
+    double alphaB, bsum, half;
     const Dim* __restrict__ dims;
 };
 
@@ -143,15 +179,17 @@ struct FamArgsG {   // d > kParamDims: per-dimension records in global memory
 // residue read as a denormal -- x_j/n folded into the coefficient, no
 // conversion, no division.  tile_out[t] = sum over tile t
 // (fixed tree).
-enum : int { FAM_LIN = 0, FAM_QUAD = 1 };
+enum : int { FAM_LIN = 0, FAM_QUAD = 1, FAM_QUADP = 2 };
 
 // Accumulate dimensions [j0, j1) of the family's per-point inner sum for the
 // P consecutive points starting at i0 (two residue chains: even/odd points).
 //  LIN:  acc += c_j * (2^-1074 r)                 (one DFMA per point-dim)
 //  QUAD: xs = (2^-1074 r) * M; acc += (q_j xs + b_j) xs   (three FP64 ops)
+//  QUADP: u = (2^-1074 r) * M - 2^-sigma/2 (the centred coordinate x - 1/2);
+//        acc += b'_j u, acc2 += q_j u^2  (odd and even parts)
 template <int KIND, class Args, int P>
 __device__ __forceinline__ void fam_accumulate(const Args& a, uint32_t i0, int j0, int j1, const uint32_t (&H)[P],
-                                               double (&acc)[P]) {
+                                               double (&acc)[P], double (&acc2)[P]) {
     const uint32_t n = a.n;
     #pragma unroll 1
     for (int j = j0; j < j1; ++j) {
@@ -172,6 +210,20 @@ __device__ __forceinline__ void fam_accumulate(const Args& a, uint32_t i0, int j
                 if (p + 2 < P) {
                     r0 = step_mod(r0, z2, z2mv);
                     r1 = step_mod(r1, z2, z2mv);
+                }
+            }
+        } else if constexpr (KIND == FAM_QUADP) {
+            const double b = a.dims[j].b, q = a.dims[j].q, M = a.M, hf = a.half;
+            #pragma unroll
+            for (int p = 0; p < P; p += 2) {
+                const double u0 = fma(denorm_of(r0, H[p]), M, -hf), u1 = fma(denorm_of(r1, H[p + 1]), M, -hf);
+                acc[p] = fma(b, u0, acc[p]);
+                acc2[p] = fma(q * u0, u0, acc2[p]);
+                acc[p + 1] = fma(b, u1, acc[p + 1]);
+                acc2[p + 1] = fma(q * u1, u1, acc2[p + 1]);
+                if (p + 2 < P) {
+                    r0 = step_mod(r0, z2, z2m);
+                    r1 = step_mod(r1, z2, z2m);
                 }
             }
         } else {
@@ -206,11 +258,12 @@ __device__ __forceinline__ double fam_outer(double acc, const Args& a) {
 // parks its partial inner sums in shared memory, and rank 0 adds the S slices
 // in rank order through distributed shared memory before the outer function.
 // tile_out[t] = sum over tile t (fixed tree).
-template <int KIND, int OUTER, class Args, int S>
+template <int KIND, int OUTER, class Args, int S, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 2) k_fam(const __grid_constant__ Args a, uint32_t hmask,
                                                       double* __restrict__ tile_out) {
     constexpr int P = fam_pts(KIND);
-    extern __shared__ double part[];   // [P][kThreads] when S > 1
+    constexpr int NA = KIND == FAM_QUADP ? 2 : 1;   // accumulators per point
+    extern __shared__ double part[];   // [NA][P][kThreads] when S > 1
     __shared__ double sh[8];
     uint32_t H[P];
     #pragma unroll
@@ -218,26 +271,38 @@ __global__ void __launch_bounds__(kThreads, 2) k_fam(const __grid_constant__ Arg
     const int64_t tile = blockIdx.x;
     const uint64_t i0_64 = a.base + (uint64_t)tile * (kThreads * P) + (uint64_t)threadIdx.x * P;
     const uint32_t i0 = (uint32_t)i0_64;   // < 2^32 (n <= 2^31)
-    double acc[P];
+    double acc[P], acc2[P];
     #pragma unroll
-    for (int p = 0; p < P; ++p) acc[p] = 0.0;
+    for (int p = 0; p < P; ++p) {
+        acc[p] = 0.0;
+        acc2[p] = 0.0;
+    }
     int rank = 0;
     if constexpr (S == 1) {
-        fam_accumulate<KIND>(a, i0, 0, a.d, H, acc);
+        fam_accumulate<KIND>(a, i0, 0, a.d, H, acc, acc2);
     } else {
         cg::cluster_group cluster = cg::this_cluster();
         rank = (int)cluster.block_rank();
-        fam_accumulate<KIND>(a, i0, (int)((int64_t)a.d * rank / S), (int)((int64_t)a.d * (rank + 1) / S), H, acc);
+        fam_accumulate<KIND>(a, i0, (int)((int64_t)a.d * rank / S), (int)((int64_t)a.d * (rank + 1) / S), H, acc,
+                             acc2);
         #pragma unroll
-        for (int p = 0; p < P; ++p) part[p * kThreads + threadIdx.x] = acc[p];
+        for (int p = 0; p < P; ++p) {
+            part[p * kThreads + threadIdx.x] = acc[p];
+            if (NA == 2) part[(P + p) * kThreads + threadIdx.x] = acc2[p];
+        }
         cluster.sync();
         if (rank == 0) {
             #pragma unroll
             for (int p = 0; p < P; ++p) {
-                double v = acc[p];
+                double v = acc[p], v2 = acc2[p];
                 #pragma unroll
-                for (int r = 1; r < S; ++r) v += cluster.map_shared_rank(part, r)[p * kThreads + threadIdx.x];
+                for (int r = 1; r < S; ++r) {
+                    const double* pr = cluster.map_shared_rank(part, r);
+                    v += pr[p * kThreads + threadIdx.x];
+                    if (NA == 2) v2 += pr[(P + p) * kThreads + threadIdx.x];
+                }
                 acc[p] = v;
+                acc2[p] = v2;
             }
         }
         cluster.sync();   // peers keep their shared memory until rank 0 has read it
@@ -246,8 +311,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_fam(const __grid_constant__ Arg
     double s = 0.0;
     #pragma unroll
     for (int p = 0; p < P; ++p) {
-        double f = fam_outer<KIND, OUTER>(acc[p], a);
-        s += (i0_64 + p < a.end) ? f : 0.0;
+        const uint64_t i = i0_64 + p;
+        double f;
+        if constexpr (KIND == FAM_QUADP) {
+            f = quad_pair(acc[p], acc2[p], a.alphaB, a.K, i != 0 && 2 * i != a.n);
+        } else if constexpr (PAIR) {
+            const LinParams prm{a.alpha, a.scale, a.K, a.A, a.B, a.C0, a.kappa};
+            f = outer_pair<OUTER>(acc[p], prm, a.alphaB, a.bsum, i != 0 && 2 * i != a.n);
+        } else {
+            f = fam_outer<KIND, OUTER>(acc[p], a);
+        }
+        s += (i < a.end) ? f : 0.0;
     }
     s = block_sum(s, sh);
     if (threadIdx.x == 0) tile_out[tile] = s;
@@ -299,33 +373,6 @@ struct OrbQuadArgs {
 
 __device__ __forceinline__ uint32_t mulmod32(uint32_t x, uint32_t y, uint32_t n) {
     return (uint32_t)(((uint64_t)x * y) % n);
-}
-
-template <int OUTER>
-__device__ __noinline__ double outer_pair(double acc, const LinParams p, const double alphaB, const double bsum,
-                                          bool two) {
-    if (OUTER == OUT_EXP) {
-        const double f1 = p.K * exp(fma(acc, p.scale, p.alpha)), f2 = p.K * exp(fma(-acc, p.scale, alphaB));
-        return two ? f1 + f2 : f1;
-    }
-    if (OUTER == OUT_EXPABS) {
-        const double f1 = p.K * exp(p.kappa * fabs(fma(acc, p.scale, p.alpha)));
-        const double f2 = p.K * exp(p.kappa * fabs(fma(-acc, p.scale, alphaB)));
-        return two ? f1 + f2 : f1;
-    }
-    const double l1 = acc * p.scale, l2 = bsum - l1;
-    double s1, c1, s2, c2;
-    sincos(l1, &s1, &c1);
-    sincos(l2, &s2, &c2);
-    const double f1 = p.C0 + p.A * s1 + p.B * c1, f2 = p.C0 + p.A * s2 + p.B * c2;
-    return two ? f1 + f2 : f1;
-}
-
-// sum of f over the point and its mirror: exp(alpha' + even +- odd)
-__device__ __noinline__ double quad_pair(double odd, double even, double alphaC, double K, bool two) {
-    const double t = alphaC + even;
-    const double f1 = K * exp(t + odd), f2 = K * exp(t - odd);
-    return two ? f1 + f2 : f1;
 }
 
 // One thread = one chain of M points (and their mirrors); 256 chains per CTA.

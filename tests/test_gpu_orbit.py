@@ -109,15 +109,15 @@ def test_orbit_not_used_for_non_korobov_or_composite(env, monkeypatch):
     lq, N, engine = env
     monkeypatch.setenv("LQ_ORBIT", "always")
     f = lq.parse("exp(0.1*x[1] + 0.2*x[2] + 0.3*x[3])", 3)
-    # composite n
+    # composite n (and z_j = 5^j shares factors with n: no mirror pairs either)
     r = lq.korobov_vector(5, 100000, 3)
     assert _layout(N, engine, f, r).mode == N.LAYOUT_INDEX
-    # not a Korobov vector
+    # not a Korobov vector: mirror pairs only
     r = lq.LatticeRule(100003, (1, 17, 1234))
-    assert _layout(N, engine, f, r).mode == N.LAYOUT_INDEX
-    # a = 1: every point its own coset (too many cosets) -> index kernels
+    assert _layout(N, engine, f, r).mode == N.LAYOUT_PAIRED
+    # a = 1: every point its own coset (too many cosets) -> mirror pairs only
     r = lq.korobov_vector(1, 100003, 3)
-    assert _layout(N, engine, f, r).mode == N.LAYOUT_INDEX
+    assert _layout(N, engine, f, r).mode == N.LAYOUT_PAIRED
     # sub-ranges never use the orbit kernel, full ranges do
     r = lq.korobov_vector(7, 100003, 3)
     pi = engine.plain_integrand(f, 3)
@@ -139,3 +139,95 @@ def test_orbit_cfg5_matches_index_kernel(env, monkeypatch):
     orb = _sum(lq, engine, f, rule, "1", monkeypatch)
     idx = _sum(lq, engine, f, rule, "0", monkeypatch)
     assert math.isclose(orb, idx, rel_tol=1e-12), (orb, idx)
+
+
+# ---------------------------------------------------------------- mirror pairs
+# Rules that are not Korobov-over-a-prime (CBC-built vectors, composite or
+# power-of-two n) still pair each point with its mirror when every z_j is a
+# unit mod n (LAYOUT_PAIRED, k_fam<PAIR>).
+
+def _family_text(family, d, rng):
+    c = [float(v) for v in rng.uniform(0, 1, d)]
+    w = [float(v) for v in rng.uniform(0, 1, d)]
+    if family == "exp":
+        return "exp(" + " + ".join(f"{c[j] / d!r}*x[{j + 1}]" for j in range(d)) + ")"
+    if family == "sincos":
+        return "cos(0.7 + " + " + ".join(f"{c[j]!r}*x[{j + 1}]" for j in range(d)) + ")"
+    if family == "expabs":
+        return "exp(-abs(" + " + ".join(f"{c[j] / 4!r}*(x[{j + 1}] - {w[j]!r})" for j in range(d)) + "))"
+    return "exp(-(" + " + ".join(f"{c[j] ** 2 / 4!r}*(x[{j + 1}] - {w[j]!r})^2" for j in range(d)) + "))"
+
+
+def _unit_vector(n, d, rng):
+    z = [1]
+    while len(z) < d:
+        v = int(rng.integers(1, n))
+        if math.gcd(v, n) == 1:
+            z.append(v)
+    return tuple(z)
+
+
+@pytest.mark.parametrize("n", [65536, 100003, 99991 * 2, 3 ** 10])
+@pytest.mark.parametrize("family", ["exp", "sincos", "expabs", "gauss"])
+def test_paired_layout_vs_oracle(env, n, family, monkeypatch):
+    lq, N, engine = env
+    from oracle import np_oracle
+    d = 40 if family != "gauss" else 96       # 96: the cluster split runs too
+    rng = np.random.default_rng(zlib.crc32(f"{n}/{family}".encode()))
+    f = lq.parse(_family_text(family, d, rng), d)
+    rule = lq.LatticeRule(n, _unit_vector(n, d, rng))
+    monkeypatch.delenv("LQ_PAIR", raising=False)
+    assert _layout(N, engine, f, rule).mode == N.LAYOUT_PAIRED
+    pi = engine.plain_integrand(f, d)
+    z = rule.z_reduced_array()
+    paired = engine.lattice_sum(pi, n, z)
+    monkeypatch.setenv("LQ_PAIR", "0")
+    assert _layout(N, engine, f, rule).mode == N.LAYOUT_INDEX
+    plain = engine.lattice_sum(pi, n, z)
+    ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
+    assert math.isclose(paired, ref, rel_tol=REL), (n, family, paired, ref)
+    assert math.isclose(paired, plain, rel_tol=1e-12), (n, family, paired, plain)
+
+
+def test_paired_needs_units(env, monkeypatch):
+    lq, N, engine = env
+    monkeypatch.delenv("LQ_PAIR", raising=False)
+    f = lq.parse("exp(0.1*x[1] + 0.2*x[2])", 2)
+    assert _layout(N, engine, f, lq.LatticeRule(1000, (1, 3))).mode == N.LAYOUT_PAIRED
+    assert _layout(N, engine, f, lq.LatticeRule(1000, (1, 4))).mode == N.LAYOUT_INDEX   # gcd(4, 1000) > 1
+    # a bytecode integrand never pairs
+    g = lq.parse("x[1]*x[2] + 1", 2)
+    assert _layout(N, engine, g, lq.LatticeRule(1000, (1, 3))).mode == N.LAYOUT_INDEX
+
+
+def test_paired_partials_sharded_bit_identical(env, monkeypatch):
+    import ctypes as C
+    import torch
+    lq, N, engine = env
+    from paper_2404_08867_b200.distributed import shard_range
+    monkeypatch.delenv("LQ_PAIR", raising=False)
+    n, d = 1 << 26, 64
+    rng = np.random.default_rng(11)
+    f = lq.parse(_family_text("expabs", d, rng), d)
+    rule = lq.LatticeRule(n, _unit_vector(n, d, rng))
+    pi = engine.plain_integrand(f, d)
+    z = rule.z_reduced_array()
+    lay = N.lattice_layout(pi.struct, n, z)
+    assert lay.mode == N.LAYOUT_PAIRED and lay.n_units == n // 2 + 1 and lay.n_supers > 4
+    h, ctx = N.lib(), N.ctx()
+    S = lay.n_supers
+    one = torch.zeros(S, dtype=torch.float64, device="cuda")
+    N.check(h.lq_lattice_partials(ctx, C.byref(pi.struct), n, N.as_ptr(z), 0, S, C.c_void_p(one.data_ptr())))
+    many = torch.zeros(S, dtype=torch.float64, device="cuda")
+    for r in range(3):
+        lo, hi = shard_range(S, r, 3)
+        N.check(h.lq_lattice_partials(ctx, C.byref(pi.struct), n, N.as_ptr(z), lo, hi,
+                                      C.c_void_p(many.data_ptr() + 8 * lo)))
+    torch.cuda.synchronize()
+    assert torch.equal(one.view(torch.int64), many.view(torch.int64))
+    out = C.c_double()
+    N.check(h.lq_reduce_sum(ctx, C.c_void_p(one.data_ptr()), S, C.byref(out)))
+    full = engine.lattice_sum(pi, n, z)
+    assert out.value == full
+    monkeypatch.setenv("LQ_PAIR", "0")
+    assert math.isclose(engine.lattice_sum(pi, n, z), full, rel_tol=1e-12)
