@@ -555,10 +555,9 @@ std::shared_ptr<const OrbPlan> orbit_plan(uint32_t n, uint32_t a, int m) {
     return p;
 }
 
-// LQ_ORBIT=0 disables the orbit kernel, =always uses it whenever the rule
-// allows; default: n >= 2^18 (measured: cfg3, n = 1e6, 0.066 vs 0.161 ms;
-// below ~1e5 points both are launch-latency bound and the index kernels'
-// dimension split is slightly faster: cfg2 0.034 vs 0.040 ms).
+// LQ_ORBIT=0 disables the orbit kernel; otherwise it runs whenever the rule
+// allows (measured kernel ms, orbit vs mirror-paired index kernel: cfg1
+// 0.0119 / 0.0125, cfg2 0.0231 / 0.0244, cfg3 0.053 / 0.127, cfg5 67.9 / 134.8).
 int orbit_mode() {
     const char* e = std::getenv("LQ_ORBIT");
     if (!e || !*e) return 1;
@@ -570,7 +569,7 @@ int orbit_mode() {
 std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, const uint64_t* z) {
     const int mode = orbit_mode();
     if (mode == 0 || !z || f->kind == LQ_FAM_PROGRAM || f->d < 2) return nullptr;
-    if (n > (1ull << 31) || n < 5 || (mode == 1 && n < (1ull << 18))) return nullptr;
+    if (n > (1ull << 31) || n < 5) return nullptr;
     const bool quad = f->kind == LQ_FAM_QUAD_EXP;
     const int m = lq::orb_len(quad ? lq::FAM_QUAD : lq::FAM_LIN);
     const int cap = quad ? lq::kOrbQuadDims : lq::kOrbLinDims;
@@ -605,6 +604,42 @@ int orbit_tables(lq_ctx* c, const OrbPlan& p, const uint32_t** G, const uint32_t
     return LQ_OK;
 }
 
+// Kernel-parameter structs sized to the padded dimension (the launch copies
+// the whole struct: 32 KB costs ~13 us per launch).
+template <int N>
+int orbit_quad(lq_ctx* c, const lq::OrbHead& head, const std::vector<double2>& bq, uint64_t unit0, int64_t ntiles,
+               double* tiles_dev) {
+    using Args = lq::OrbQuadArgs<N>;
+    static thread_local Args args;
+    args.h = head;
+    std::memcpy(args.bq, bq.data(), sizeof(double2) * bq.size());
+    t_begin(c);
+    lq::k_orbit<lq::FAM_QUAD, 0, Args><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, unit0, 0u, tiles_dev);
+    t_end(c);
+    CK(cudaGetLastError());
+    return LQ_OK;
+}
+
+template <int N>
+int orbit_lin(lq_ctx* c, const lq::OrbHead& head, const std::vector<double>& cv, int outer, uint64_t unit0,
+              int64_t ntiles, double* tiles_dev) {
+    using Args = lq::OrbLinArgs<N>;
+    static thread_local Args args;
+    args.h = head;
+    std::memcpy(args.c, cv.data(), sizeof(double) * cv.size());
+    const dim3 g((unsigned)ntiles), b(lq::kThreads);
+    t_begin(c);
+    if (outer == lq::OUT_EXP)
+        lq::k_orbit<lq::FAM_LIN, lq::OUT_EXP, Args><<<g, b, 0, c->stream>>>(args, unit0, 0u, tiles_dev);
+    else if (outer == lq::OUT_SINCOS)
+        lq::k_orbit<lq::FAM_LIN, lq::OUT_SINCOS, Args><<<g, b, 0, c->stream>>>(args, unit0, 0u, tiles_dev);
+    else
+        lq::k_orbit<lq::FAM_LIN, lq::OUT_EXPABS, Args><<<g, b, 0, c->stream>>>(args, unit0, 0u, tiles_dev);
+    t_end(c);
+    CK(cudaGetLastError());
+    return LQ_OK;
+}
+
 int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t unit0, int64_t ntiles,
                  double* tiles_dev) {
     int rc;
@@ -614,43 +649,36 @@ int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t un
     const int d = f->d, m = p.m;
     const int dpad = (d + m - 1) / m * m;
     const double nd = (double)p.n;
-    auto head = [&](lq::OrbHead& h) {
-        h.n = p.n; h.a = p.a; h.as = p.as; h.dpad = dpad; h.units = p.units; h.qc = p.qc; h.h = p.h;
-        h.G = G; h.Alo = Alo; h.Ahi = Ahi;
-        h.alpha = f->alpha; h.K = f->K; h.A = f->A; h.B = f->B; h.C0 = f->C0; h.kappa = f->kappa;
-    };
-    const unsigned hmask = 0u;
+    lq::OrbHead h;
+    h.n = p.n; h.a = p.a; h.as = p.as; h.dpad = dpad; h.units = p.units; h.qc = p.qc; h.h = p.h;
+    h.G = G; h.Alo = Alo; h.Ahi = Ahi;
+    h.alpha = f->alpha; h.K = f->K; h.A = f->A; h.B = f->B; h.C0 = f->C0; h.kappa = f->kappa;
     if (f->kind == LQ_FAM_QUAD_EXP) {
-        static thread_local lq::OrbQuadArgs args;
-        head(args.h);
         int sigma = 1074 + std::ilogb(1.0 / nd) - 1000;
         if (sigma < 0) sigma = 0;
-        args.h.M = std::ldexp(1.0 / nd, 1074 - sigma);
-        args.h.half = std::ldexp(0.5, -sigma);
-        args.h.scale = 1.0;
+        h.M = std::ldexp(1.0 / nd, 1074 - sigma);
+        h.half = std::ldexp(0.5, -sigma);
+        h.scale = 1.0;
+        std::vector<double2> bq(dpad);
         double C0 = 0.0;
         for (int j = 0; j < dpad; ++j) {
             if (j < d) {
-                args.bq[j].x = std::ldexp(f->beta[j] + f->gamma[j], sigma);
-                args.bq[j].y = std::ldexp(f->gamma[j], 2 * sigma);
-                if (!std::isfinite(args.bq[j].x) || !std::isfinite(args.bq[j].y))
+                bq[j].x = std::ldexp(f->beta[j] + f->gamma[j], sigma);
+                bq[j].y = std::ldexp(f->gamma[j], 2 * sigma);
+                if (!std::isfinite(bq[j].x) || !std::isfinite(bq[j].y))
                     return fail(LQ_ERR_VALUE, "quadratic coefficient out of range");
                 C0 += 0.5 * f->beta[j] + 0.25 * f->gamma[j];
             } else {
-                args.bq[j].x = 0.0;
-                args.bq[j].y = 0.0;
+                bq[j].x = 0.0;
+                bq[j].y = 0.0;
             }
         }
-        args.h.alphaB = f->alpha + C0;   // f = K exp(alpha + C + odd + even) at x, odd -> -odd at 1 - x
-        args.h.bsum = 0.0;
-        t_begin(c);
-        lq::k_orbit<lq::FAM_QUAD, 0, lq::OrbQuadArgs><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, unit0, hmask, tiles_dev);
-        t_end(c);
-        CK(cudaGetLastError());
-        return LQ_OK;
+        h.alphaB = f->alpha + C0;   // f = K exp(alpha + C + odd + even) at x, odd -> -odd at 1 - x
+        h.bsum = 0.0;
+        if (dpad <= 120) return orbit_quad<120>(c, h, bq, unit0, ntiles, tiles_dev);
+        if (dpad <= 504) return orbit_quad<504>(c, h, bq, unit0, ntiles, tiles_dev);
+        return orbit_quad<lq::kOrbQuadDims>(c, h, bq, unit0, ntiles, tiles_dev);
     }
-    static thread_local lq::OrbLinArgs args;
-    head(args.h);
     double maxabs = 0.0, bsum = 0.0;
     for (int j = 0; j < d; ++j) {
         maxabs = fmax(maxabs, fabs(f->beta[j]));
@@ -662,22 +690,17 @@ int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t un
         sigma = 1074 + std::ilogb(maxabs / nd) + 1 - 1020;
         if (sigma < 0) sigma = 0;
     }
-    for (int j = 0; j < dpad; ++j) args.c[j] = j < d ? std::ldexp(f->beta[j] / nd, 1074 - sigma) : 0.0;
-    args.h.scale = std::ldexp(1.0, sigma);
-    args.h.bsum = bsum;
-    args.h.alphaB = f->alpha + bsum;   // alpha + <beta, 1 - x> = (alpha + sum beta) - <beta, x>
-    args.h.M = 0.0;
-    args.h.half = 0.0;
-    t_begin(c);
-    if (f->kind == LQ_FAM_LIN_EXP)
-        lq::k_orbit<lq::FAM_LIN, lq::OUT_EXP, lq::OrbLinArgs><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, unit0, hmask, tiles_dev);
-    else if (f->kind == LQ_FAM_LIN_SINCOS)
-        lq::k_orbit<lq::FAM_LIN, lq::OUT_SINCOS, lq::OrbLinArgs><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, unit0, hmask, tiles_dev);
-    else
-        lq::k_orbit<lq::FAM_LIN, lq::OUT_EXPABS, lq::OrbLinArgs><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, unit0, hmask, tiles_dev);
-    t_end(c);
-    CK(cudaGetLastError());
-    return LQ_OK;
+    std::vector<double> cv(dpad);
+    for (int j = 0; j < dpad; ++j) cv[j] = j < d ? std::ldexp(f->beta[j] / nd, 1074 - sigma) : 0.0;
+    h.scale = std::ldexp(1.0, sigma);
+    h.bsum = bsum;
+    h.alphaB = f->alpha + bsum;   // alpha + <beta, 1 - x> = (alpha + sum beta) - <beta, x>
+    h.M = 0.0;
+    h.half = 0.0;
+    const int outer = f->kind == LQ_FAM_LIN_EXP ? lq::OUT_EXP : f->kind == LQ_FAM_LIN_SINCOS ? lq::OUT_SINCOS : lq::OUT_EXPABS;
+    if (dpad <= 120) return orbit_lin<120>(c, h, cv, outer, unit0, ntiles, tiles_dev);
+    if (dpad <= 1008) return orbit_lin<1008>(c, h, cv, outer, unit0, ntiles, tiles_dev);
+    return orbit_lin<lq::kOrbLinDims>(c, h, cv, outer, unit0, ntiles, tiles_dev);
 }
 
 // Reduction layout of a full-lattice sum: units are points (index kernels) or

@@ -362,13 +362,15 @@ constexpr int kOrbQuadDims = (kOrbParamBytes - (int)sizeof(OrbHead)) / 16 / 24 *
 #endif
 __host__ __device__ constexpr int orb_len(int kind) { return kind == 1 ? LQ_ORB_QUAD_M : LQ_ORB_LIN_M; }
 
+template <int N = kOrbLinDims>
 struct OrbLinArgs {
     OrbHead h;
-    double c[kOrbLinDims];        // beta_j / n * 2^(1074 - sigma), zero padded
+    double c[N];                  // beta_j / n * 2^(1074 - sigma), zero padded
 };
+template <int N = kOrbQuadDims>
 struct OrbQuadArgs {
     OrbHead h;
-    double2 bq[kOrbQuadDims];     // ((beta_j + gamma_j) 2^sigma, gamma_j 2^(2 sigma)), zero padded
+    double2 bq[N];                // ((beta_j + gamma_j) 2^sigma, gamma_j 2^(2 sigma)), zero padded
 };
 
 __device__ __forceinline__ uint32_t mulmod32(uint32_t x, uint32_t y, uint32_t n) {
