@@ -1126,10 +1126,21 @@ int lq_mdi_expabs(lq_ctx* c, int32_t d, const double* beta, const int32_t* count
     void* dl;
     if ((rc = dev_buf(c, B_TILES, sizeof(double) * n_w, &dv))) return rc;
     if ((rc = dev_buf(c, B_PART, sizeof(double) * n_w, &dl))) return rc;
+    // closed-form Dirichlet sums (default) or the direct N-term sums (LQ_CF_DIRECT=1)
+    const char* direct = std::getenv("LQ_CF_DIRECT");
     t_begin(c);
-    lq::k_cf_expabs<<<n_w, lq::kThreads, 0, c->stream>>>((const double*)db, (const int32_t*)dc, d, alpha,
-                                                         (const double*)dw, (const double*)dww, kappa, (double*)dv,
-                                                         (double*)dl);
+    if (direct && !std::strcmp(direct, "1")) {
+        lq::k_cf_expabs<<<n_w, lq::kThreads, 0, c->stream>>>((const double*)db, (const int32_t*)dc, d, alpha,
+                                                             (const double*)dw, (const double*)dww, kappa,
+                                                             (double*)dv, (double*)dl);
+    } else {
+        double bsum = 0.0;
+        for (int j = 0; j < d; ++j) bsum += beta[j];
+        lq::k_cf_expabs_closed<<<n_w, lq::kThreads, 0, c->stream>>>((const double*)db, (const int32_t*)dc, d,
+                                                                    alpha + 0.5 * bsum, (const double*)dw,
+                                                                    (const double*)dww, kappa, (double*)dv,
+                                                                    (double*)dl);
+    }
     t_end(c);
     CK(cudaGetLastError());
     double* r;

@@ -720,6 +720,37 @@ __global__ void __launch_bounds__(kThreads) k_cf_expabs(const double* __restrict
     }
 }
 
+// Closed form of the same cluster sums on the midpoint grid y_t = (t + 1/2)/N:
+// (1/N) sum_t e^{i th y_t} = e^{i th/2} sin(th/2) / (N sin(th/(2N))) (Dirichlet
+// kernel), so each (w, j) costs two sines instead of N sincos; the phases sum
+// to w (sum beta)/2 + pi (number of negative ratios), folded into alpha_half =
+// alpha + (sum beta)/2 on the host.  One CTA per frequency node, threads over j.
+__global__ void __launch_bounds__(kThreads) k_cf_expabs_closed(const double* __restrict__ beta,
+                                                               const int32_t* __restrict__ counts, int d,
+                                                               double alpha_half, const double* __restrict__ wn,
+                                                               const double* __restrict__ ww, double kappa,
+                                                               double* __restrict__ val, double* __restrict__ logmag) {
+    __shared__ double sh[8];
+    const int k = blockIdx.x;
+    const double w = wn[k];
+    double lsum = 0.0, neg = 0.0;
+    for (int j = threadIdx.x; j < d; j += kThreads) {
+        const double cd = (double)counts[j], h = 0.5 * w * beta[j];
+        double r = 1.0;
+        if (h != 0.0) r = sin(h) / (cd * sin(h / cd));
+        lsum += log(fabs(r));
+        neg += r < 0.0 ? 1.0 : 0.0;
+    }
+    lsum = block_sum(lsum, sh);
+    neg = block_sum(neg, sh);
+    if (threadIdx.x == 0) {
+        const double ak = fabs(kappa);
+        const double c = cos(w * alpha_half);
+        val[k] = ww[k] * ak / (kappa * kappa + w * w) * exp(lsum) * (fmod(neg, 2.0) != 0.0 ? -c : c);
+        logmag[k] = lsum;
+    }
+}
+
 // ============================================================ reductions
 // Fixed pairwise tree over groups of 1024 consecutive values (zero padded):
 // out[g] = tree(vals[1024 g .. 1024 g + 1023]).  1024 threads, 4 per thread... here

@@ -40,6 +40,12 @@ class _LRU(OrderedDict):
 _plain_cache = _LRU()
 _prog_cache = _LRU()
 _sep_cache = _LRU()
+_fam_cache = _LRU()
+
+
+def plain_family(e, d):
+    """lower.recognize_plain(e, d), cached per (expression, d)."""
+    return _fam_cache.get_or((e, d), lambda: recognize_plain(e, d))
 
 
 class PlainIntegrand:

@@ -201,8 +201,7 @@ def _characteristic(e, d, counts, levels, base_axes, t0):
     reference (which has no |.|): returns None when the integrand is not of
     this form or the truncated integral cannot be certified, and the caller
     falls back to the direct sweep."""
-    from .lower import recognize_plain
-    fam = recognize_plain(e, d)
+    fam = engine.plain_family(e, d)
     if fam is None or fam.kind != "lin_expabs" or not fam.kappa < 0.0 or fam.K == 0.0:
         return None
     beta = np.asarray(fam.beta, dtype=np.float64)

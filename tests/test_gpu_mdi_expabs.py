@@ -20,9 +20,12 @@ def _text(k, Q, alpha, kappa):
     return f"exp({kappa!r}*abs({terms} + {alpha!r}))"
 
 
+@pytest.mark.parametrize("direct", ["0", "1"])
 @pytest.mark.parametrize("d,N,kappa,shift,seed", [(40, 8, -1.0, 0.0, 1), (32, 16, -2.5, 0.7, 2),
                                                   (64, 8, -1.0, -1.3, 3), (32, 16, -0.5, 0.2, 4)])
-def test_characteristic_function_matches_exact_oracle(d, N, kappa, shift, seed):
+def test_characteristic_function_matches_exact_oracle(d, N, kappa, shift, seed, direct, monkeypatch):
+    # direct = "1": per-node sums (k_cf_expabs); "0": closed-form Dirichlet sums (k_cf_expabs_closed)
+    monkeypatch.setenv("LQ_CF_DIRECT", direct)
     import paper_2404_08867_b200 as lq
     from oracle.np_oracle import expabs_grid_mean_dp
     Q = 4096
@@ -57,3 +60,16 @@ def test_small_non_separable_grid_still_takes_the_direct_sweep():
     f = lq.parse("exp(-abs(x[1] - x[2] + 0.1))", 2)
     value, rep = lq.mdi_lr(f, 2, 10, 101, with_report=True)
     assert rep.method == "direct"
+
+
+def test_config5_closed_form_equals_direct_sums(monkeypatch):
+    import paper_2404_08867_b200 as lq
+    from paper_2404_08867_b200.configs import make_config
+    cfg = make_config(5)
+    f = lq.parse(cfg.text, cfg.d)
+    monkeypatch.setenv("LQ_CF_DIRECT", "1")
+    _, a = lq.mdi_lr(f, cfg.d, cfg.mdi_a, cfg.mdi_n, with_report=True)
+    monkeypatch.setenv("LQ_CF_DIRECT", "0")
+    _, b = lq.mdi_lr(f, cfg.d, cfg.mdi_a, cfg.mdi_n, with_report=True)
+    assert a.method == b.method == "characteristic"
+    assert math.isclose(a.mean, b.mean, rel_tol=1e-12), (a.mean, b.mean)
