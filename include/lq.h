@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define LQ_ABI_VERSION 2
+#define LQ_ABI_VERSION 3
 
 #define LQ_OK 0
 #define LQ_ERR_VALUE (-1)
@@ -76,15 +76,18 @@ enum {
     LQ_FAM_LIN_EXP = 1,     /* K exp(alpha + <beta,x>)                         */
     LQ_FAM_LIN_SINCOS = 2,  /* C0 + A sin(<beta,x>) + B cos(<beta,x>)          */
     LQ_FAM_LIN_EXPABS = 3,  /* K exp(kappa |alpha + <beta,x>|)                 */
-    LQ_FAM_QUAD_EXP = 4     /* K exp(alpha + sum_j beta_j x_j + gamma_j x_j^2) */
+    LQ_FAM_QUAD_EXP = 4,    /* K exp(alpha + sum_j beta_j x_j + gamma_j x_j^2) */
+    LQ_FAM_LIN_POW = 5,     /* K (alpha + <beta,x>)^power, integer power       */
+    LQ_FAM_QUAD_SINCOS = 6  /* C0 + A sin(Q) + B cos(Q), Q = sum_j beta_j x_j + gamma_j x_j^2 */
 };
 
 typedef struct {
     int32_t kind;
     int32_t d;
-    const double* beta;     /* [d], host (LIN_*, QUAD_EXP) */
-    const double* gamma;    /* [d], host (QUAD_EXP)        */
+    const double* beta;     /* [d], host (LIN_*, QUAD_*) */
+    const double* gamma;    /* [d], host (QUAD_*)        */
     double alpha, K, A, B, C0, kappa;
+    double power;           /* LIN_POW: integer-valued exponent */
     lq_program prog;        /* LQ_FAM_PROGRAM */
 } lq_integrand;
 

@@ -24,7 +24,8 @@ LQ_OK, LQ_ERR_VALUE, LQ_ERR_OVERFLOW, LQ_ERR_GRIDCAP = 0, -1, -2, -3
 LQ_ERR_CUDA, LQ_ERR_UNSUPPORTED, LQ_ERR_NOMEM = -4, -5, -6
 LQ_TILE, LQ_SUPER_TILES, LQ_NODE_BLOCK = 4096, 1024, 256
 
-FAM = {"program": 0, "lin_exp": 1, "lin_sincos": 2, "lin_expabs": 3, "quad_exp": 4}
+ABI_VERSION = 3   # LQ_ABI_VERSION of include/lq.h these ctypes structs match
+FAM = {"program": 0, "lin_exp": 1, "lin_sincos": 2, "lin_expabs": 3, "quad_exp": 4, "lin_pow": 5, "quad_sincos": 6}
 
 
 class NativeUnavailable(RuntimeError):
@@ -46,7 +47,7 @@ class Program(C.Structure):
 class Integrand(C.Structure):
     _fields_ = [("kind", C.c_int32), ("d", C.c_int32), ("beta", C.c_void_p), ("gamma", C.c_void_p),
                 ("alpha", C.c_double), ("K", C.c_double), ("A", C.c_double), ("B", C.c_double),
-                ("C0", C.c_double), ("kappa", C.c_double), ("prog", Program)]
+                ("C0", C.c_double), ("kappa", C.c_double), ("power", C.c_double), ("prog", Program)]
 
 
 class Factor(C.Structure):
@@ -108,6 +109,9 @@ def lib():
                 fn.restype = C.c_int
             h.lq_last_error.argtypes = []
             h.lq_last_error.restype = C.c_char_p
+            got = h.lq_abi_version()
+            if got != ABI_VERSION:
+                raise NativeUnavailable(f"{LIB_PATH} has ABI {got}, these bindings need {ABI_VERSION}; rebuild it")
             _lib = h
     return _lib
 

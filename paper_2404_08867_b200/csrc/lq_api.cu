@@ -204,6 +204,16 @@ int pick_slots(int n_slots) {
 uint64_t tile_points(const lq_integrand* f, uint64_t n);
 bool uses_family_kernel(const lq_integrand* f, uint64_t n);
 
+bool is_quad_kind(int k) { return k == LQ_FAM_QUAD_EXP || k == LQ_FAM_QUAD_SINCOS; }
+bool is_lin_kind(int k) {
+    return k == LQ_FAM_LIN_EXP || k == LQ_FAM_LIN_SINCOS || k == LQ_FAM_LIN_EXPABS || k == LQ_FAM_LIN_POW;
+}
+int lin_outer(int k) {
+    return k == LQ_FAM_LIN_EXP ? lq::OUT_EXP : k == LQ_FAM_LIN_SINCOS ? lq::OUT_SINCOS
+         : k == LQ_FAM_LIN_EXPABS ? lq::OUT_EXPABS : lq::OUT_POW;
+}
+int quad_outer_of(int k) { return k == LQ_FAM_QUAD_SINCOS ? lq::OUT_SINCOS : lq::OUT_EXP; }
+
 // Dimension split of the family kernels: lattices with fewer tiles than
 // ~4 waves of CTAs run each tile on a cluster of S CTAs that split the
 // dimensions (k_fam<S>).  S depends on (units, d) only, so every GPU of a
@@ -274,7 +284,7 @@ bool pair_ok(const lq_integrand* f, uint64_t n, const uint64_t* z) {
 }
 
 int fam_kind(const lq_integrand* f, bool pair) {
-    if (f->kind == LQ_FAM_QUAD_EXP) return pair ? lq::FAM_QUADP : lq::FAM_QUAD;
+    if (is_quad_kind(f->kind)) return pair ? lq::FAM_QUADP : lq::FAM_QUAD;
     return lq::FAM_LIN;
 }
 
@@ -286,14 +296,14 @@ uint64_t tile_points(const lq_integrand* f, uint64_t n) { return tile_points(f, 
 
 // scalar parameters of the family kernels
 struct FamHead {
-    double alpha = 0, scale = 1, K = 0, A = 0, B = 0, C0 = 0, kappa = 0, M = 0, alphaB = 0, bsum = 0, half = 0;
+    double alpha = 0, scale = 1, K = 0, A = 0, B = 0, C0 = 0, kappa = 0, M = 0, alphaB = 0, bsum = 0, half = 0, pw = 0;
 };
 
 template <class A>
 void fill_head(A& a, int d, uint64_t n, uint64_t base, uint64_t end, const FamHead& h) {
     a.d = d; a.n = (uint32_t)n; a.base = base; a.end = end;
     a.alpha = h.alpha; a.scale = h.scale; a.K = h.K; a.A = h.A; a.B = h.B; a.C0 = h.C0; a.kappa = h.kappa;
-    a.M = h.M; a.alphaB = h.alphaB; a.bsum = h.bsum; a.half = h.half;
+    a.M = h.M; a.alphaB = h.alphaB; a.bsum = h.bsum; a.half = h.half; a.pw = h.pw;
 }
 
 // Per-dimension tables in kernel parameter space, sized to d: the launch copies
@@ -340,7 +350,7 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
     const bool fast = uses_family_kernel(f, n);
     const uint64_t units = pair ? n / 2 + 1 : n;
     int rc;
-    if (fast && (f->kind == LQ_FAM_LIN_EXP || f->kind == LQ_FAM_LIN_SINCOS || f->kind == LQ_FAM_LIN_EXPABS)) {
+    if (fast && is_lin_kind(f->kind)) {
         if (!f->beta) return fail(LQ_ERR_VALUE, "family needs beta");
         double maxabs = 0.0, bsum = 0.0;
         for (int j = 0; j < d; ++j) {
@@ -364,21 +374,25 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
         }
         FamHead h;
         h.alpha = f->alpha; h.scale = std::ldexp(1.0, sigma); h.K = f->K; h.A = f->A; h.B = f->B; h.C0 = f->C0;
-        h.kappa = f->kappa; h.bsum = bsum; h.alphaB = f->alpha + bsum;
+        h.kappa = f->kappa; h.bsum = bsum; h.alphaB = f->alpha + bsum; h.pw = f->power;
 #define LQ_LIN(OUT) (pair ? fam_dispatch<lq::FAM_LIN, OUT, true>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev) \
                           : fam_dispatch<lq::FAM_LIN, OUT, false>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev))
-        if (f->kind == LQ_FAM_LIN_EXP) return LQ_LIN(lq::OUT_EXP);
-        if (f->kind == LQ_FAM_LIN_SINCOS) return LQ_LIN(lq::OUT_SINCOS);
-        return LQ_LIN(lq::OUT_EXPABS);
+        switch (lin_outer(f->kind)) {
+            case lq::OUT_EXP: return LQ_LIN(lq::OUT_EXP);
+            case lq::OUT_SINCOS: return LQ_LIN(lq::OUT_SINCOS);
+            case lq::OUT_EXPABS: return LQ_LIN(lq::OUT_EXPABS);
+            default: return LQ_LIN(lq::OUT_POW);
+        }
 #undef LQ_LIN
     }
-    if (fast && f->kind == LQ_FAM_QUAD_EXP) {
+    if (fast && is_quad_kind(f->kind)) {
         if (!f->beta || !f->gamma) return fail(LQ_ERR_VALUE, "quad family needs beta and gamma");
         const double inv_n = 1.0 / (double)n;
         int sigma = 1074 + std::ilogb(inv_n) - 1000;
         if (sigma < 0) sigma = 0;
         FamHead h;
-        h.alpha = f->alpha; h.K = f->K; h.M = std::ldexp(inv_n, 1074 - sigma); h.half = std::ldexp(0.5, -sigma);
+        h.alpha = f->alpha; h.K = f->K; h.A = f->A; h.B = f->B; h.C0 = f->C0;
+        h.M = std::ldexp(inv_n, 1074 - sigma); h.half = std::ldexp(0.5, -sigma);
         std::vector<lq::QuadDim> tab(d);
         double C0 = 0.0;
         for (int j = 0; j < d; ++j) {
@@ -394,8 +408,12 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
                 return fail(LQ_ERR_VALUE, "quadratic coefficient out of range");
         }
         h.alphaB = f->alpha + C0;
-        if (pair) return fam_dispatch<lq::FAM_QUADP, 0, true>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev);
-        return fam_dispatch<lq::FAM_QUAD, 0, false>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev);
+        if (quad_outer_of(f->kind) == lq::OUT_SINCOS) {
+            if (pair) return fam_dispatch<lq::FAM_QUADP, lq::OUT_SINCOS, true>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev);
+            return fam_dispatch<lq::FAM_QUAD, lq::OUT_SINCOS, false>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev);
+        }
+        if (pair) return fam_dispatch<lq::FAM_QUADP, lq::OUT_EXP, true>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev);
+        return fam_dispatch<lq::FAM_QUAD, lq::OUT_EXP, false>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev);
     }
     // generic bytecode (any family falls back here for n > 2^31)
     const lq_program* pg = &f->prog;
@@ -443,7 +461,9 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
 
 int check_integrand(const lq_integrand* f) {
     if (!f) return fail(LQ_ERR_VALUE, "null integrand");
-    if (f->kind < LQ_FAM_PROGRAM || f->kind > LQ_FAM_QUAD_EXP) return fail(LQ_ERR_VALUE, "bad family kind %d", f->kind);
+    if (f->kind < LQ_FAM_PROGRAM || f->kind > LQ_FAM_QUAD_SINCOS) return fail(LQ_ERR_VALUE, "bad family kind %d", f->kind);
+    if (f->kind == LQ_FAM_LIN_POW && (f->power != std::floor(f->power) || std::fabs(f->power) > 1e6))
+        return fail(LQ_ERR_VALUE, "LIN_POW needs an integer power, got %g", f->power);
     return LQ_OK;
 }
 
@@ -570,7 +590,7 @@ std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, cons
     const int mode = orbit_mode();
     if (mode == 0 || !z || f->kind == LQ_FAM_PROGRAM || f->d < 2) return nullptr;
     if (n > (1ull << 31) || n < 5) return nullptr;
-    const bool quad = f->kind == LQ_FAM_QUAD_EXP;
+    const bool quad = is_quad_kind(f->kind);
     const int m = lq::orb_len(quad ? lq::FAM_QUAD : lq::FAM_LIN);
     const int cap = quad ? lq::kOrbQuadDims : lq::kOrbLinDims;
     if ((f->d + m - 1) / m * m > cap) return nullptr;
@@ -607,14 +627,18 @@ int orbit_tables(lq_ctx* c, const OrbPlan& p, const uint32_t** G, const uint32_t
 // Kernel-parameter structs sized to the padded dimension (the launch copies
 // the whole struct: 32 KB costs ~13 us per launch).
 template <int N>
-int orbit_quad(lq_ctx* c, const lq::OrbHead& head, const std::vector<double2>& bq, uint64_t unit0, int64_t ntiles,
-               double* tiles_dev) {
+int orbit_quad(lq_ctx* c, const lq::OrbHead& head, const std::vector<double2>& bq, int outer, uint64_t unit0,
+               int64_t ntiles, double* tiles_dev) {
     using Args = lq::OrbQuadArgs<N>;
     static thread_local Args args;
     args.h = head;
     std::memcpy(args.bq, bq.data(), sizeof(double2) * bq.size());
+    const dim3 g((unsigned)ntiles), b(lq::kThreads);
     t_begin(c);
-    lq::k_orbit<lq::FAM_QUAD, 0, Args><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, unit0, 0u, tiles_dev);
+    if (outer == lq::OUT_SINCOS)
+        lq::k_orbit<lq::FAM_QUAD, lq::OUT_SINCOS, Args><<<g, b, 0, c->stream>>>(args, unit0, 0u, tiles_dev);
+    else
+        lq::k_orbit<lq::FAM_QUAD, lq::OUT_EXP, Args><<<g, b, 0, c->stream>>>(args, unit0, 0u, tiles_dev);
     t_end(c);
     CK(cudaGetLastError());
     return LQ_OK;
@@ -633,8 +657,10 @@ int orbit_lin(lq_ctx* c, const lq::OrbHead& head, const std::vector<double>& cv,
         lq::k_orbit<lq::FAM_LIN, lq::OUT_EXP, Args><<<g, b, 0, c->stream>>>(args, unit0, 0u, tiles_dev);
     else if (outer == lq::OUT_SINCOS)
         lq::k_orbit<lq::FAM_LIN, lq::OUT_SINCOS, Args><<<g, b, 0, c->stream>>>(args, unit0, 0u, tiles_dev);
-    else
+    else if (outer == lq::OUT_EXPABS)
         lq::k_orbit<lq::FAM_LIN, lq::OUT_EXPABS, Args><<<g, b, 0, c->stream>>>(args, unit0, 0u, tiles_dev);
+    else
+        lq::k_orbit<lq::FAM_LIN, lq::OUT_POW, Args><<<g, b, 0, c->stream>>>(args, unit0, 0u, tiles_dev);
     t_end(c);
     CK(cudaGetLastError());
     return LQ_OK;
@@ -652,8 +678,9 @@ int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t un
     lq::OrbHead h;
     h.n = p.n; h.a = p.a; h.as = p.as; h.dpad = dpad; h.units = p.units; h.qc = p.qc; h.h = p.h;
     h.G = G; h.Alo = Alo; h.Ahi = Ahi;
-    h.alpha = f->alpha; h.K = f->K; h.A = f->A; h.B = f->B; h.C0 = f->C0; h.kappa = f->kappa;
-    if (f->kind == LQ_FAM_QUAD_EXP) {
+    h.alpha = f->alpha; h.K = f->K; h.A = f->A; h.B = f->B; h.C0 = f->C0; h.kappa = f->kappa; h.pw = f->power;
+    if (is_quad_kind(f->kind)) {
+        const int outer = quad_outer_of(f->kind);
         int sigma = 1074 + std::ilogb(1.0 / nd) - 1000;
         if (sigma < 0) sigma = 0;
         h.M = std::ldexp(1.0 / nd, 1074 - sigma);
@@ -675,9 +702,9 @@ int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t un
         }
         h.alphaB = f->alpha + C0;   // f = K exp(alpha + C + odd + even) at x, odd -> -odd at 1 - x
         h.bsum = 0.0;
-        if (dpad <= 120) return orbit_quad<120>(c, h, bq, unit0, ntiles, tiles_dev);
-        if (dpad <= 504) return orbit_quad<504>(c, h, bq, unit0, ntiles, tiles_dev);
-        return orbit_quad<lq::kOrbQuadDims>(c, h, bq, unit0, ntiles, tiles_dev);
+        if (dpad <= 120) return orbit_quad<120>(c, h, bq, outer, unit0, ntiles, tiles_dev);
+        if (dpad <= 504) return orbit_quad<504>(c, h, bq, outer, unit0, ntiles, tiles_dev);
+        return orbit_quad<lq::kOrbQuadDims>(c, h, bq, outer, unit0, ntiles, tiles_dev);
     }
     double maxabs = 0.0, bsum = 0.0;
     for (int j = 0; j < d; ++j) {
@@ -697,7 +724,7 @@ int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t un
     h.alphaB = f->alpha + bsum;   // alpha + <beta, 1 - x> = (alpha + sum beta) - <beta, x>
     h.M = 0.0;
     h.half = 0.0;
-    const int outer = f->kind == LQ_FAM_LIN_EXP ? lq::OUT_EXP : f->kind == LQ_FAM_LIN_SINCOS ? lq::OUT_SINCOS : lq::OUT_EXPABS;
+    const int outer = lin_outer(f->kind);
     if (dpad <= 120) return orbit_lin<120>(c, h, cv, outer, unit0, ntiles, tiles_dev);
     if (dpad <= 1008) return orbit_lin<1008>(c, h, cv, outer, unit0, ntiles, tiles_dev);
     return orbit_lin<lq::kOrbLinDims>(c, h, cv, outer, unit0, ntiles, tiles_dev);

@@ -92,53 +92,61 @@ constexpr int kQuadPts = LQ_QUAD_PTS;     // points per thread of the Gaussian f
 __host__ __device__ constexpr int fam_pts(int kind) { return kind == 1 ? kQuadPts : kind == 2 ? LQ_QUADP_PTS : kFamPts; }
 
 struct LinParams {
-    double alpha, scale, K, A, B, C0, kappa;
+    double alpha, scale, K, A, B, C0, kappa, pw;
 };
 
-enum : int { OUT_EXP = 0, OUT_SINCOS = 1, OUT_EXPABS = 2 };
+// Outer functions g(s) of the families' inner sums s:
+//   EXP K e^s | SINCOS C0 + A sin s + B cos s | EXPABS K e^(kappa |s|) | POW K s^pw
+enum : int { OUT_EXP = 0, OUT_SINCOS = 1, OUT_EXPABS = 2, OUT_POW = 3 };
+
+// numpy's b**k for integer k (exprcore.py:466-468; square for k == 2, libm pow
+// otherwise; a negative k is 1 / b**(-k), as the reference's pow nodes).
+__device__ __forceinline__ double int_pow(double b, double k) {
+    if (k >= 0.0) return k == 2.0 ? b * b : pow(b, k);
+    return 1.0 / (k == -1.0 ? b : k == -2.0 ? b * b : pow(b, -k));
+}
+
+template <int OUTER>
+__device__ __forceinline__ double outer_val(double s, const LinParams& p) {
+    if (OUTER == OUT_EXP) return p.K * exp(s);
+    if (OUTER == OUT_EXPABS) return p.K * exp(p.kappa * fabs(s));
+    if (OUTER == OUT_POW) return p.K * int_pow(s, p.pw);
+    double sn, cs;
+    sincos(s, &sn, &cs);
+    return p.C0 + p.A * sn + p.B * cs;
+}
 
 // Outer functions run once per point (not per point-dim): kept out of line so
 // their temporaries do not inflate the register budget of the j-loop.
+// Linear families: s = alpha + acc * scale (alpha = 0 for SINCOS, folded into A, B).
 template <int OUTER>
 __device__ __noinline__ double outer_fn(double acc, const LinParams p) {
-    if (OUTER == OUT_EXP) return p.K * exp(fma(acc, p.scale, p.alpha));
-    if (OUTER == OUT_EXPABS) return p.K * exp(p.kappa * fabs(fma(acc, p.scale, p.alpha)));
-    double s, c;
-    sincos(acc * p.scale, &s, &c);
-    return p.C0 + p.A * s + p.B * c;
+    return outer_val<OUTER>(fma(acc, p.scale, p.alpha), p);
 }
 
-__device__ __noinline__ double quad_outer(double acc, double alpha, double K) { return K * exp(alpha + acc); }
+// Quadratic families: s = alpha + acc.
+template <int OUTER>
+__device__ __noinline__ double quad_outer(double acc, const LinParams p) {
+    return outer_val<OUTER>(p.alpha + acc, p);
+}
 
 // Mirror pairs (x and 1 - x): f at both points from one
 // inner sum; `two` is false for the self-mirrored points 0 and n/2.
+// Linear: s(1 - x) = (alpha + sum beta) - acc * scale.
 template <int OUTER>
-__device__ __noinline__ double outer_pair(double acc, const LinParams p, const double alphaB, const double bsum,
-                                          bool two) {
-    if (OUTER == OUT_EXP) {
-        const double f1 = p.K * exp(fma(acc, p.scale, p.alpha)), f2 = p.K * exp(fma(-acc, p.scale, alphaB));
-        return two ? f1 + f2 : f1;
-    }
-    if (OUTER == OUT_EXPABS) {
-        const double f1 = p.K * exp(p.kappa * fabs(fma(acc, p.scale, p.alpha)));
-        const double f2 = p.K * exp(p.kappa * fabs(fma(-acc, p.scale, alphaB)));
-        return two ? f1 + f2 : f1;
-    }
-    const double l1 = acc * p.scale, l2 = bsum - l1;
-    double s1, c1, s2, c2;
-    sincos(l1, &s1, &c1);
-    sincos(l2, &s2, &c2);
-    const double f1 = p.C0 + p.A * s1 + p.B * c1, f2 = p.C0 + p.A * s2 + p.B * c2;
+__device__ __noinline__ double outer_pair(double acc, const LinParams p, const double alphaB, bool two) {
+    const double f1 = outer_val<OUTER>(fma(acc, p.scale, p.alpha), p);
+    const double f2 = outer_val<OUTER>(fma(-acc, p.scale, alphaB), p);
     return two ? f1 + f2 : f1;
 }
 
-// sum of f over the point and its mirror: exp(alpha' + even +- odd)
-__device__ __noinline__ double quad_pair(double odd, double even, double alphaC, double K, bool two) {
+// Quadratic, centred form: s = alphaC + even +- odd at x and 1 - x.
+template <int OUTER>
+__device__ __noinline__ double quad_pair(double odd, double even, double alphaC, const LinParams p, bool two) {
     const double t = alphaC + even;
-    const double f1 = K * exp(t + odd), f2 = K * exp(t - odd);
+    const double f1 = outer_val<OUTER>(t + odd, p), f2 = outer_val<OUTER>(t - odd, p);
     return two ? f1 + f2 : f1;
 }
-
 
 // Per-dimension tables travel in kernel parameter space (constant bank 0) when
 // they fit: the j-loop then reads c_j, z_j, zs_j as uniform-register operands
@@ -159,6 +167,7 @@ struct FamArgs {
     uint64_t base, end;
     double alpha, scale, K, A, B, C0, kappa, M;
     double alphaB, bsum, half;   // mirror pairs: alpha + sum beta (QUADP: alpha + C), sum beta, 2^-sigma / 2
+    double pw;                   // OUT_POW exponent
     Dim dims[N];
 };
 
@@ -169,6 +178,7 @@ struct FamArgsG {   // d > kParamDims: per-dimension records in global memory
     uint64_t base, end;
     double alpha, scale, K, A, B, C0, kappa, M;
     double alphaB, bsum, half;
+    double pw;
     const Dim* __restrict__ dims;
 };
 
@@ -242,14 +252,15 @@ __device__ __forceinline__ void fam_accumulate(const Args& a, uint32_t i0, int j
     }
 }
 
+template <class Args>
+__device__ __forceinline__ LinParams lin_params(const Args& a) {
+    return LinParams{a.alpha, a.scale, a.K, a.A, a.B, a.C0, a.kappa, a.pw};
+}
+
 template <int KIND, int OUTER, class Args>
 __device__ __forceinline__ double fam_outer(double acc, const Args& a) {
-    if constexpr (KIND == FAM_QUAD) {
-        return quad_outer(acc, a.alpha, a.K);
-    } else {
-        const LinParams prm{a.alpha, a.scale, a.K, a.A, a.B, a.C0, a.kappa};
-        return outer_fn<OUTER>(acc, prm);
-    }
+    if constexpr (KIND == FAM_QUAD) return quad_outer<OUTER>(acc, lin_params(a));
+    else return outer_fn<OUTER>(acc, lin_params(a));
 }
 
 // Plain lattice sum of a closed family, n <= 2^31: one tile of 256 threads x
@@ -314,10 +325,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_fam(const __grid_constant__ Arg
         const uint64_t i = i0_64 + p;
         double f;
         if constexpr (KIND == FAM_QUADP) {
-            f = quad_pair(acc[p], acc2[p], a.alphaB, a.K, i != 0 && 2 * i != a.n);
+            f = quad_pair<OUTER>(acc[p], acc2[p], a.alphaB, lin_params(a), i != 0 && 2 * i != a.n);
         } else if constexpr (PAIR) {
-            const LinParams prm{a.alpha, a.scale, a.K, a.A, a.B, a.C0, a.kappa};
-            f = outer_pair<OUTER>(acc[p], prm, a.alphaB, a.bsum, i != 0 && 2 * i != a.n);
+            f = outer_pair<OUTER>(acc[p], lin_params(a), a.alphaB, i != 0 && 2 * i != a.n);
         } else {
             f = fam_outer<KIND, OUTER>(acc[p], a);
         }
@@ -348,7 +358,7 @@ struct OrbHead {
     const uint32_t* G;      // coset representatives g^s
     const uint32_t* Alo;    // a^(m q) for q < 4096
     const uint32_t* Ahi;    // a^(m 4096 q)
-    double alpha, alphaB, scale, bsum, K, A, B, C0, kappa, M, half;
+    double alpha, alphaB, scale, bsum, K, A, B, C0, kappa, M, half, pw;
 };
 
 constexpr int kOrbParamBytes = 32000;
@@ -418,10 +428,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_orbit(const __grid_constant__ A
                     W[v] = mulmod_shoup(W[(v + M - 1) % M], za, zs, n);
                 }
             }
-            const LinParams prm{H.alpha, H.scale, H.K, H.A, H.B, H.C0, H.kappa};
+            const LinParams prm{H.alpha, H.scale, H.K, H.A, H.B, H.C0, H.kappa, H.pw};
             #pragma unroll
             for (int k = 0; k < M; ++k)
-                s += k < valid ? outer_pair<OUTER>(acc[k], prm, H.alphaB, H.bsum, true) : 0.0;
+                s += k < valid ? outer_pair<OUTER>(acc[k], prm, H.alphaB, true) : 0.0;
             if (u == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
         } else {
             const double Ms = H.M, hf = H.half;
@@ -454,8 +464,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_orbit(const __grid_constant__ A
                 }
             }
             #pragma unroll
-            for (int k = 0; k < M; ++k) s += k < valid ? quad_pair(ao[k], ae[k], H.alphaB, H.K, true) : 0.0;
-            if (u == 0) s += quad_outer(0.0, H.alpha, H.K);   // point 0
+            const LinParams prm{H.alpha, H.scale, H.K, H.A, H.B, H.C0, H.kappa, H.pw};
+            #pragma unroll
+            for (int k = 0; k < M; ++k) s += k < valid ? quad_pair<OUTER>(ao[k], ae[k], H.alphaB, prm, true) : 0.0;
+            if (u == 0) s += quad_outer<OUTER>(0.0, prm);   // point 0
         }
     }
     s = block_sum(s, sh);

@@ -68,7 +68,7 @@ class PlainIntegrand:
                 self._keep.append(gamma)
                 s.gamma = gamma.ctypes.data
             s.alpha, s.K, s.A, s.B = family.alpha, family.K, family.A, family.B
-            s.C0, s.kappa = family.C0, family.kappa
+            s.C0, s.kappa, s.power = family.C0, family.kappa, float(family.power)
         if program is not None:
             if family is None:
                 s.kind = 0

@@ -147,10 +147,12 @@ def quad_form(e):
 class PlainFamily:
     """A closed family the LIN/QUAD lattice-sum kernels evaluate.
 
-    kind: 'lin_exp'    f = K exp(alpha + <beta, x>)
-          'lin_sincos' f = C0 + A sin(<beta, x>) + B cos(<beta, x>)
-          'lin_expabs' f = K exp(kappa |alpha + <beta, x>|)
-          'quad_exp'   f = K exp(alpha + sum_j beta_j x_j + gamma_j x_j^2)
+    kind: 'lin_exp'     f = K exp(alpha + <beta, x>)
+          'lin_sincos'  f = C0 + A sin(<beta, x>) + B cos(<beta, x>)
+          'lin_expabs'  f = K exp(kappa |alpha + <beta, x>|)
+          'lin_pow'     f = K (alpha + <beta, x>)^power, integer power
+          'quad_exp'    f = K exp(alpha + sum_j beta_j x_j + gamma_j x_j^2)
+          'quad_sincos' f = C0 + A sin(Q) + B cos(Q), Q = sum_j beta_j x_j + gamma_j x_j^2
     """
 
     kind: str
@@ -163,6 +165,7 @@ class PlainFamily:
     B: float = 0.0
     C0: float = 0.0
     kappa: float = -1.0
+    power: int = 0
 
 
 def _vec(coefs, d):
@@ -221,40 +224,67 @@ def recognize_plain(e, d):
             if b is not None:
                 return PlainFamily("quad_exp", d, b, gamma=g, alpha=qf[0], K=K)
         return None
-    # C0 + sum_k coef_k trig(alpha_k + <beta, x>) with one shared beta
+    if core.op == "pow":
+        # K (alpha + <beta, x>)^k: the reference's pow node (integer k, negative
+        # k meaning 1 / b^-k; exprcore.py:466-468)
+        lf = linear_form(core.args[0])
+        if lf is not None and core.idx != 0:
+            beta = _vec(lf[1], d)
+            if beta is not None:
+                return PlainFamily("lin_pow", d, beta, alpha=lf[0], K=K, power=int(core.idx))
+        return None
+    # C0 + sum_k coef_k trig(alpha_k + F(x)) with one shared form F: linear
+    # (lin_sincos) or diagonal quadratic (quad_sincos)
     if e.op == "add":
         terms, C0 = e.terms, e.val
     elif core.op in ("sin", "cos"):
         terms, C0 = ((K, core),), 0.0
     else:
         return None
+    for form, kind in ((linear_form, "lin_sincos"), (quad_form, "quad_sincos")):
+        fam = _trig_family(terms, C0, d, form, kind)
+        if fam is not None:
+            return fam
+    return None
+
+
+def _trig_family(terms, C0, d, form, kind):
     A = B = 0.0
-    beta0 = None
+    key0 = None
     for c, t in terms:
         s, t = _strip_scale(t)
         c *= s
         if t.op not in ("sin", "cos"):
             return None
-        lf = linear_form(t.args[0])
-        if lf is None:
+        ff = form(t.args[0])
+        if ff is None:
             return None
-        beta = _vec(lf[1], d)
-        if beta is None:
+        al, coefs = ff
+        if kind == "lin_sincos":
+            beta = _vec(coefs, d)
+            if beta is None:
+                return None
+            key = (beta, None)
+        else:
+            beta = _vec({j: v[0] for j, v in coefs.items()}, d)
+            gamma = _vec({j: v[1] for j, v in coefs.items()}, d)
+            if beta is None:
+                return None
+            key = (beta, gamma)
+        if key0 is None:
+            key0 = key
+        elif not (np.array_equal(key0[0], key[0]) and
+                  (key[1] is None or np.array_equal(key0[1], key[1]))):
             return None
-        if beta0 is None:
-            beta0 = beta
-        elif not np.array_equal(beta0, beta):
-            return None
-        al = lf[0]
         if t.op == "sin":   # sin(al + L) = sin al cos L + cos al sin L
             A += c * math.cos(al)
             B += c * math.sin(al)
         else:               # cos(al + L) = cos al cos L - sin al sin L
             A -= c * math.sin(al)
             B += c * math.cos(al)
-    if beta0 is None:
+    if key0 is None:
         return None
-    return PlainFamily("lin_sincos", d, beta0, A=A, B=B, C0=C0)
+    return PlainFamily(kind, d, key0[0], gamma=key0[1], A=A, B=B, C0=C0)
 
 
 # ------------------------------------------------------------------ bytecode

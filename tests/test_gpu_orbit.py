@@ -70,7 +70,7 @@ def test_orbit_configs_vs_oracle(env, cid, monkeypatch):
 
 
 @pytest.mark.parametrize("kind", ["primitive", "odd_order", "even_order_cosets"])
-@pytest.mark.parametrize("family", ["exp", "sincos", "expabs", "gauss"])
+@pytest.mark.parametrize("family", ["exp", "sincos", "expabs", "gauss", "pow", "qtrig"])
 def test_orbit_group_structures(env, kind, family, monkeypatch):
     # prime n = 100003, n - 1 = 2 * 3 * 7 * 2381; a chosen for each coset structure
     lq, N, engine = env
@@ -83,16 +83,7 @@ def test_orbit_group_structures(env, kind, family, monkeypatch):
     o = _order(a, n)
     assert (o == n - 1) if kind == "primitive" else (o % 2 == (1 if kind == "odd_order" else 0))
     rng = np.random.default_rng(zlib.crc32(f"{kind}/{family}".encode()))
-    c = [float(v) for v in rng.uniform(0, 1, d)]
-    w = [float(v) for v in rng.uniform(0, 1, d)]
-    if family == "exp":
-        text = "exp(" + " + ".join(f"{c[j] / d!r}*x[{j + 1}]" for j in range(d)) + ")"
-    elif family == "sincos":
-        text = "cos(0.7 + " + " + ".join(f"{c[j]!r}*x[{j + 1}]" for j in range(d)) + ")"
-    elif family == "expabs":
-        text = "exp(-abs(" + " + ".join(f"{c[j] / 4!r}*(x[{j + 1}] - {w[j]!r})" for j in range(d)) + "))"
-    else:
-        text = "exp(-(" + " + ".join(f"{c[j] ** 2 / 4!r}*(x[{j + 1}] - {w[j]!r})^2" for j in range(d)) + "))"
+    text = _family_text(family, d, rng)
     f = lq.parse(text, d)
     rule = lq.korobov_vector(a, n, d)
     monkeypatch.setenv("LQ_ORBIT", "always")
@@ -155,6 +146,10 @@ def _family_text(family, d, rng):
         return "cos(0.7 + " + " + ".join(f"{c[j]!r}*x[{j + 1}]" for j in range(d)) + ")"
     if family == "expabs":
         return "exp(-abs(" + " + ".join(f"{c[j] / 4!r}*(x[{j + 1}] - {w[j]!r})" for j in range(d)) + "))"
+    if family == "pow":
+        return "(1.5 + " + " + ".join(f"{c[j] / d!r}*x[{j + 1}]" for j in range(d)) + ")^(-3)"
+    if family == "qtrig":
+        return "0.5 + sin(0.3 + " + " + ".join(f"{c[j] ** 2 / 4!r}*(x[{j + 1}] - {w[j]!r})^2" for j in range(d)) + ")"
     return "exp(-(" + " + ".join(f"{c[j] ** 2 / 4!r}*(x[{j + 1}] - {w[j]!r})^2" for j in range(d)) + "))"
 
 
@@ -168,11 +163,11 @@ def _unit_vector(n, d, rng):
 
 
 @pytest.mark.parametrize("n", [65536, 100003, 99991 * 2, 3 ** 10])
-@pytest.mark.parametrize("family", ["exp", "sincos", "expabs", "gauss"])
+@pytest.mark.parametrize("family", ["exp", "sincos", "expabs", "gauss", "pow", "qtrig"])
 def test_paired_layout_vs_oracle(env, n, family, monkeypatch):
     lq, N, engine = env
     from oracle import np_oracle
-    d = 40 if family != "gauss" else 96       # 96: the cluster split runs too
+    d = 96 if family in ("gauss", "qtrig") else 40       # 96: the cluster split runs too
     rng = np.random.default_rng(zlib.crc32(f"{n}/{family}".encode()))
     f = lq.parse(_family_text(family, d, rng), d)
     rule = lq.LatticeRule(n, _unit_vector(n, d, rng))
@@ -231,3 +226,23 @@ def test_paired_partials_sharded_bit_identical(env, monkeypatch):
     assert out.value == full
     monkeypatch.setenv("LQ_PAIR", "0")
     assert math.isclose(engine.lattice_sum(pi, n, z), full, rel_tol=1e-12)
+
+
+@pytest.mark.parametrize("family,kind", [("pow", "lin_pow"), ("qtrig", "quad_sincos")])
+def test_new_families_match_bytecode(env, family, kind, monkeypatch):
+    # the family kernels against the bytecode interpreter on a sub-range (index
+    # layout) and on the full lattice (orbit layout)
+    lq, N, engine = env
+    d, n = 50, 1000003
+    rng = np.random.default_rng(9)
+    f = lq.parse(_family_text(family, d, rng), d)
+    rule = lq.korobov_vector(76543, n, d)
+    fam = engine.plain_integrand(f, d)
+    prog = engine.plain_integrand(f, d, force_program=True)
+    assert fam.kind == kind
+    z = rule.z_reduced_array()
+    monkeypatch.setenv("LQ_JIT", "0")
+    for lo, hi in ((0, n), (12345, 400000)):
+        a = engine.lattice_sum(fam, n, z, lo, hi)
+        b = engine.lattice_sum(prog, n, z, lo, hi)
+        assert math.isclose(a, b, rel_tol=1e-12), (family, lo, hi, a, b)

@@ -257,7 +257,8 @@ def test_library_exports_every_declared_symbol():
     for name in sorted(names):
         assert hasattr(lib, name), name
     h = _native.lib()
-    assert h.lq_abi_version() == 2
+    want = int(re.search(r"#define LQ_ABI_VERSION (\d+)", header).group(1))
+    assert h.lq_abi_version() == want == _native.ABI_VERSION
     from paper_2404_08867_b200 import engine
     cfg = make_config(5)
     pi = engine.plain_integrand(lq.parse(cfg.text, cfg.d), cfg.d)
