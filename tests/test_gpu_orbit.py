@@ -246,3 +246,30 @@ def test_new_families_match_bytecode(env, family, kind, monkeypatch):
         a = engine.lattice_sum(fam, n, z, lo, hi)
         b = engine.lattice_sum(prog, n, z, lo, hi)
         assert math.isclose(a, b, rel_tol=1e-12), (family, lo, hi, a, b)
+
+
+@pytest.mark.parametrize("n,d,a", [(5, 3, 2), (7, 1, 3), (2, 4, 1), (3, 2, 2), (4, 3, 3), (1009, 4100, 478),
+                                   (100003, 4100, 7)])
+def test_layout_edges_vs_index_kernel(env, n, d, a, monkeypatch):
+    # tiny moduli (self-mirrored points, no orbit), d = 1, and d beyond the
+    # parameter-space tables (global-memory tables): every layout liblq picks
+    # equals the plain per-index sum
+    lq, N, engine = env
+    rng = np.random.default_rng(n + d)
+    f = lq.parse(_family_text("expabs", d, rng), d)
+    rule = lq.korobov_vector(a, n, d)
+    pi = engine.plain_integrand(f, d)
+    z = rule.z_reduced_array()
+    monkeypatch.delenv("LQ_PAIR", raising=False)
+    monkeypatch.delenv("LQ_ORBIT", raising=False)
+    lay = N.lattice_layout(pi.struct, n, z)
+    got = engine.lattice_sum(pi, n, z)
+    monkeypatch.setenv("LQ_PAIR", "0")
+    monkeypatch.setenv("LQ_ORBIT", "0")
+    assert N.lattice_layout(pi.struct, n, z).mode == N.LAYOUT_INDEX
+    want = engine.lattice_sum(pi, n, z)
+    assert math.isclose(got, want, rel_tol=1e-12), (n, d, lay, got, want)
+    if n * d <= 200000:
+        from oracle import np_oracle
+        ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
+        assert math.isclose(got, ref, rel_tol=REL), (n, d, got, ref)
