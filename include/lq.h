@@ -78,7 +78,8 @@ enum {
     LQ_FAM_LIN_EXPABS = 3,  /* K exp(kappa |alpha + <beta,x>|)                 */
     LQ_FAM_QUAD_EXP = 4,    /* K exp(alpha + sum_j beta_j x_j + gamma_j x_j^2) */
     LQ_FAM_LIN_POW = 5,     /* K (alpha + <beta,x>)^power, integer power       */
-    LQ_FAM_QUAD_SINCOS = 6  /* C0 + A sin(Q) + B cos(Q), Q = sum_j beta_j x_j + gamma_j x_j^2 */
+    LQ_FAM_QUAD_SINCOS = 6, /* C0 + A sin(Q) + B cos(Q), Q = sum_j beta_j x_j + gamma_j x_j^2 */
+    LQ_FAM_PROD_QUAD = 7    /* K prod_j ((x_j - beta_j)^2 + gamma_j)^power; gamma_j = NaN: no factor */
 };
 
 typedef struct {

@@ -25,7 +25,7 @@ LQ_ERR_CUDA, LQ_ERR_UNSUPPORTED, LQ_ERR_NOMEM = -4, -5, -6
 LQ_TILE, LQ_SUPER_TILES, LQ_NODE_BLOCK = 4096, 1024, 256
 
 ABI_VERSION = 3   # LQ_ABI_VERSION of include/lq.h these ctypes structs match
-FAM = {"program": 0, "lin_exp": 1, "lin_sincos": 2, "lin_expabs": 3, "quad_exp": 4, "lin_pow": 5, "quad_sincos": 6}
+FAM = {"program": 0, "lin_exp": 1, "lin_sincos": 2, "lin_expabs": 3, "quad_exp": 4, "lin_pow": 5, "quad_sincos": 6, "prod_quad": 7}
 
 
 class NativeUnavailable(RuntimeError):

@@ -274,7 +274,7 @@ int launch_fam(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev, u
 bool pair_ok(const lq_integrand* f, uint64_t n, const uint64_t* z) {
     const char* e = std::getenv("LQ_PAIR");
     if (e && !std::strcmp(e, "0")) return false;
-    if (!z || f->kind == LQ_FAM_PROGRAM || n < 3 || n > (1ull << 31)) return false;
+    if (!z || f->kind == LQ_FAM_PROGRAM || f->kind == LQ_FAM_PROD_QUAD || n < 3 || n > (1ull << 31)) return false;
     for (int j = 0; j < f->d; ++j) {
         uint64_t a = z[j], b = n;
         while (b) { const uint64_t t = a % b; a = b; b = t; }
@@ -285,6 +285,7 @@ bool pair_ok(const lq_integrand* f, uint64_t n, const uint64_t* z) {
 
 int fam_kind(const lq_integrand* f, bool pair) {
     if (is_quad_kind(f->kind)) return pair ? lq::FAM_QUADP : lq::FAM_QUAD;
+    if (f->kind == LQ_FAM_PROD_QUAD) return lq::FAM_PROD;
     return lq::FAM_LIN;
 }
 
@@ -339,6 +340,71 @@ int fam_dispatch(lq_ctx* c, const std::vector<Dim>& tab, int d, uint64_t n, uint
 
 bool uses_family_kernel(const lq_integrand* f, uint64_t n) {
     return n <= (1ull << 31) && f->kind != LQ_FAM_PROGRAM;
+}
+
+// Product family (k_prod).  The coordinate comes out of the denormal residue
+// as x 2^-g (g >= 51 - log2 n keeps 2^(1074-g)/n finite), so every scaled
+// factor carries 2^-2g; the running product is renormalised every R factors,
+// R the largest power of two <= 16 that keeps R worst-case scaled factors
+// inside 2^(+-1000).
+int launch_prod(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z, uint64_t base, uint64_t end,
+                int64_t ntiles, double* tiles_dev) {
+    if (!f->beta || !f->gamma) return fail(LQ_ERR_VALUE, "product family needs beta (w) and gamma (c)");
+    const int g = std::max(0, 51 - std::ilogb((double)n));
+    const double m = std::ldexp(1.0 / (double)n, 1074 - g);
+    if (!std::isfinite(m)) return fail(LQ_ERR_UNSUPPORTED, "product family: scale overflow for n=%llu", (unsigned long long)n);
+    std::vector<lq::ProdDim> tab;
+    double worst = 0.0;
+    for (int j = 0; j < f->d; ++j) {
+        const double w = f->beta[j], cj = f->gamma[j];
+        if (std::isnan(cj)) continue;
+        const double dist = w < 0.0 ? -w : (w > 1.0 ? w - 1.0 : 0.0);
+        const double fmin = cj + dist * dist, fmax = cj + std::fmax(w * w, (1.0 - w) * (1.0 - w));
+        if (!(fmin > 0.0) || !std::isfinite(fmax))
+            return fail(LQ_ERR_UNSUPPORTED, "product factor %d spans [%g, %g]", j + 1, fmin, fmax);
+        worst = std::fmax(worst, std::fmax(std::fabs(std::log2(fmin) - 2 * g), std::fabs(std::log2(fmax) - 2 * g)));
+        lq::ProdDim r;
+        r.m = m;
+        r.w = std::ldexp(w, -g);
+        r.c = std::ldexp(cj, -2 * g);
+        if (cj != 0.0 && !std::isnormal(r.c))
+            return fail(LQ_ERR_UNSUPPORTED, "product factor %d out of the scaled range", j + 1);
+        r.z = (uint32_t)z[j];
+        r.zs = (uint32_t)(((uint64_t)z[j] << 32) / n);
+        r.z2 = (uint32_t)((2 * z[j]) % n);
+        r.z2m = r.z2 - (uint32_t)n;
+        tab.push_back(r);
+    }
+    int R = 16;
+    while (R > 1 && R * (worst + 1.0) > 1000.0) R /= 2;
+    if ((worst + 1.0) > 1000.0) return fail(LQ_ERR_UNSUPPORTED, "product factors span more than 2^1000");
+    const int64_t off = 2ll * g * (int64_t)tab.size();
+    if (off > (1ll << 30)) return fail(LQ_ERR_UNSUPPORTED, "product exponent offset too large");
+    const int nf = (int)tab.size();
+    auto head = [&](auto& a) {
+        a.nf = nf; a.n = (uint32_t)n; a.base = base; a.end = end; a.K = f->K; a.pw = f->power; a.off = (int32_t)off;
+        a.rmask = R - 1;
+    };
+    if (nf <= lq::kProdParamDims) {
+        static thread_local lq::ProdArgs<lq::kProdParamDims> args;
+        head(args);
+        std::memcpy(args.dims, tab.data(), sizeof(lq::ProdDim) * nf);
+        t_begin(c);
+        lq::k_prod<<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, 0u, tiles_dev);
+        t_end(c);
+    } else {
+        void* dt;
+        int rc;
+        if ((rc = upload(c, B_TAB, tab.data(), tab.size() * sizeof(lq::ProdDim), &dt))) return rc;
+        lq::ProdArgsG args;
+        head(args);
+        args.dims = (const lq::ProdDim*)dt;
+        t_begin(c);
+        lq::k_prod<<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, 0u, tiles_dev);
+        t_end(c);
+    }
+    CK(cudaGetLastError());
+    return LQ_OK;
 }
 
 // Launch the tile kernel of integrand f over index units [base, end) writing
@@ -415,6 +481,7 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
         if (pair) return fam_dispatch<lq::FAM_QUADP, lq::OUT_EXP, true>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev);
         return fam_dispatch<lq::FAM_QUAD, lq::OUT_EXP, false>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev);
     }
+    if (fast && f->kind == LQ_FAM_PROD_QUAD) return launch_prod(c, f, n, z, base, end, ntiles, tiles_dev);
     // generic bytecode (any family falls back here for n > 2^31)
     const lq_program* pg = &f->prog;
     if (!pg->insn || pg->n_insn < 1)
@@ -461,8 +528,9 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
 
 int check_integrand(const lq_integrand* f) {
     if (!f) return fail(LQ_ERR_VALUE, "null integrand");
-    if (f->kind < LQ_FAM_PROGRAM || f->kind > LQ_FAM_QUAD_SINCOS) return fail(LQ_ERR_VALUE, "bad family kind %d", f->kind);
-    if (f->kind == LQ_FAM_LIN_POW && (f->power != std::floor(f->power) || std::fabs(f->power) > 1e6))
+    if (f->kind < LQ_FAM_PROGRAM || f->kind > LQ_FAM_PROD_QUAD) return fail(LQ_ERR_VALUE, "bad family kind %d", f->kind);
+    if ((f->kind == LQ_FAM_LIN_POW || f->kind == LQ_FAM_PROD_QUAD) &&
+        (f->power != std::floor(f->power) || std::fabs(f->power) > 1e6))
         return fail(LQ_ERR_VALUE, "LIN_POW needs an integer power, got %g", f->power);
     return LQ_OK;
 }
@@ -588,7 +656,7 @@ int orbit_mode() {
 
 std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, const uint64_t* z) {
     const int mode = orbit_mode();
-    if (mode == 0 || !z || f->kind == LQ_FAM_PROGRAM || f->d < 2) return nullptr;
+    if (mode == 0 || !z || f->kind == LQ_FAM_PROGRAM || f->kind == LQ_FAM_PROD_QUAD || f->d < 2) return nullptr;
     if (n > (1ull << 31) || n < 5) return nullptr;
     const bool quad = is_quad_kind(f->kind);
     const int m = lq::orb_len(quad ? lq::FAM_QUAD : lq::FAM_LIN);

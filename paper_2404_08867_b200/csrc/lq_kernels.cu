@@ -88,8 +88,12 @@ constexpr int kQuadPts = LQ_QUAD_PTS;     // points per thread of the Gaussian f
 #ifndef LQ_QUADP_PTS
 #define LQ_QUADP_PTS 12
 #endif
-// kind: 0 LIN, 1 QUAD, 2 QUADP (mirror-paired Gaussian: two accumulators per point)
-__host__ __device__ constexpr int fam_pts(int kind) { return kind == 1 ? kQuadPts : kind == 2 ? LQ_QUADP_PTS : kFamPts; }
+// kind: 0 LIN, 1 QUAD, 2 QUADP (mirror-paired Gaussian: two accumulators per
+// point), 3 PROD (product family: a running product and its exponent per point)
+constexpr int kProdPts = 16;
+__host__ __device__ constexpr int fam_pts(int kind) {
+    return kind == 1 ? kQuadPts : kind == 2 ? LQ_QUADP_PTS : kind == 3 ? kProdPts : kFamPts;
+}
 
 struct LinParams {
     double alpha, scale, K, A, B, C0, kappa, pw;
@@ -189,7 +193,7 @@ struct FamArgsG {   // d > kParamDims: per-dimension records in global memory
 // residue read as a denormal -- x_j/n folded into the coefficient, no
 // conversion, no division.  tile_out[t] = sum over tile t
 // (fixed tree).
-enum : int { FAM_LIN = 0, FAM_QUAD = 1, FAM_QUADP = 2 };
+enum : int { FAM_LIN = 0, FAM_QUAD = 1, FAM_QUADP = 2, FAM_PROD = 3 };
 
 // Accumulate dimensions [j0, j1) of the family's per-point inner sum for the
 // P consecutive points starting at i0 (two residue chains: even/odd points).
@@ -335,6 +339,103 @@ __global__ void __launch_bounds__(kThreads, 2) k_fam(const __grid_constant__ Arg
     }
     s = block_sum(s, sh);
     if (threadIdx.x == 0) tile_out[tile] = s;
+}
+
+// ============================================================ product family
+// f = K prod_j ((x_j - w_j)^2 + c_j)^p (Genz product peak, config 4's
+// integrand, corpus ratprod).  Per point-dim: t = x 2^-g - w_j 2^-g and
+// D *= t*t + c_j 2^-2g -- the coordinate is again the denormal residue times a
+// scale, so three FP64 ops and the two-op residue step.  D is renormalised to
+// [1, 2) every R factors (host-chosen so R scaled factors cannot leave
+// 2^(+-1000)) with its exponent kept in an integer.
+struct ProdDim {
+    double m;       // 2^(1074 - g) / n: denormal residue -> x 2^-g
+    double w;       // w_j 2^-g
+    double c;       // c_j 2^-2g
+    uint32_t z, zs, z2, z2m;
+};
+
+template <int N>
+struct ProdArgs {
+    int nf;              // factors (dimensions that carry one)
+    uint32_t n;
+    uint64_t base, end;
+    double K, pw;
+    int32_t off;         // 2 g nf: D_true = D 2^(E + off)
+    int32_t rmask;       // renormalise after factor j when (j & rmask) == rmask
+    ProdDim dims[N];
+};
+
+struct ProdArgsG {   // more factors than kProdParamDims: records in global memory
+    int nf;
+    uint32_t n;
+    uint64_t base, end;
+    double K, pw;
+    int32_t off, rmask;
+    const ProdDim* __restrict__ dims;
+};
+
+constexpr int kProdParamDims = 780;   // 780 x 40 B + header < 32 KB
+
+__device__ __forceinline__ void renorm(double& D, int& E) {
+    const int hi = __double2hiint(D), lo = __double2loint(D);
+    const int e = (hi >> 20) - 1023;   // D > 0 normal
+    D = __hiloint2double(hi - (e << 20), lo);
+    E += e;
+}
+
+__device__ __noinline__ double prod_outer(double D, int E, double K, double pw, int off) {
+    renorm(D, E);
+    return ldexp(K * int_pow(D, pw), (int)pw * (E + off));
+}
+
+template <class Args>
+__global__ void __launch_bounds__(kThreads, 2) k_prod(const __grid_constant__ Args a, uint32_t hmask,
+                                                       double* __restrict__ tile_out) {
+    constexpr int P = kProdPts;
+    __shared__ double sh[8];
+    uint32_t H[P];
+    #pragma unroll
+    for (int k = 0; k < P; ++k) H[k] = (threadIdx.x + k) & hmask;   // opaque zeros
+    const uint64_t i0_64 = a.base + (uint64_t)blockIdx.x * (kThreads * P) + (uint64_t)threadIdx.x * P;
+    const uint32_t i0 = (uint32_t)i0_64, n = a.n;
+    double D[P];
+    int E[P];
+    #pragma unroll
+    for (int p = 0; p < P; ++p) {
+        D[p] = 1.0;
+        E[p] = 0;
+    }
+    #pragma unroll 1
+    for (int j = 0; j < a.nf; ++j) {
+        const ProdDim& q = a.dims[j];
+        const uint32_t z = q.z, z2 = q.z2, z2m = q.z2m;
+        const double m = q.m, w = q.w, c = q.c;
+        uint32_t r0 = mulmod_shoup(i0, z, q.zs, n);
+        uint32_t r1 = step_mod(r0, z, z - n);
+        #pragma unroll
+        for (int p = 0; p < P; p += 2) {
+            const double t0 = fma(denorm_of(r0, H[p]), m, -w), t1 = fma(denorm_of(r1, H[p + 1]), m, -w);
+            D[p] *= fma(t0, t0, c);
+            D[p + 1] *= fma(t1, t1, c);
+            if (p + 2 < P) {
+                r0 = step_mod(r0, z2, z2m);
+                r1 = step_mod(r1, z2, z2m);
+            }
+        }
+        if ((j & a.rmask) == a.rmask) {
+            #pragma unroll
+            for (int p = 0; p < P; ++p) renorm(D[p], E[p]);
+        }
+    }
+    double s = 0.0;
+    #pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const double f = prod_outer(D[p], E[p], a.K, a.pw, a.off);
+        s += (i0_64 + p < a.end) ? f : 0.0;
+    }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
 }
 
 // ============================================================ Korobov orbits

@@ -153,6 +153,7 @@ class PlainFamily:
           'lin_pow'     f = K (alpha + <beta, x>)^power, integer power
           'quad_exp'    f = K exp(alpha + sum_j beta_j x_j + gamma_j x_j^2)
           'quad_sincos' f = C0 + A sin(Q) + B cos(Q), Q = sum_j beta_j x_j + gamma_j x_j^2
+          'prod_quad'   f = K prod_j ((x_j - beta_j)^2 + gamma_j)^power  (gamma_j NaN: no factor)
     """
 
     kind: str
@@ -198,8 +199,73 @@ def _abs_affine(arg):
     return a0, kappa, node
 
 
+def _shifted_square(base):
+    """base = c0 + k (x_j + s)^2 (the parser's form of c0 + k (x_j - w)^2) ->
+    (j, w, c) with the factor equal to k ((x_j - w)^2 + c), plus k; or None."""
+    if base.op != "add" or len(base.terms) != 1:
+        return None
+    k, sq = base.terms[0]
+    if sq.op != "pow" or sq.idx != 2 or k == 0.0:
+        return None
+    inner = sq.args[0]
+    if inner.op == "var":
+        j, s = inner.idx, 0.0
+    elif inner.op == "add" and len(inner.terms) == 1 and inner.terms[0][0] == 1.0 and inner.terms[0][1].op == "var":
+        j, s = inner.terms[0][1].idx, inner.val
+    else:
+        return None
+    return j, -s, base.val / k, k
+
+
+def _prod_family(K, factors, d):
+    """K prod_j (c_j + k_j (x_j - w_j)^2)^p over distinct coordinates, every
+    factor bounded away from 0 on [0, 1] (Genz product peak, config 4)."""
+    if not factors:
+        return None
+    p = None
+    w = np.zeros(d)
+    c = np.full(d, np.nan)
+    for fct in factors:
+        base, k = (fct.args[0], fct.idx) if fct.op == "pow" else (fct, 1)
+        if k == 0:
+            return None
+        if not free_vars(base):
+            return None
+        m = _shifted_square(base)
+        if m is None:
+            qf = quad_form(base)     # a + b x + q x^2, accepted when completing the square is benign
+            if qf is None or len(qf[1]) != 1:
+                return None
+            (j, (b, q)), = qf[1].items()
+            if q == 0.0:
+                return None
+            wj, cq = -b / (2.0 * q), qf[0] / q
+            cj = cq - wj * wj
+            if not (abs(cj) >= 1e-4 * abs(cq)):   # completing the square loses <= 1e4 ulp of c
+                return None
+            m = (j, wj, cj, q)
+        j, wj, cj, kq = m
+        if not 1 <= j <= d or not np.isnan(c[j - 1]):
+            return None
+        if p is None:
+            p = k
+        elif p != k:
+            return None
+        dist = max(-wj, wj - 1.0, 0.0)
+        fmin, fmax = cj + dist * dist, cj + max(wj * wj, (1.0 - wj) ** 2)
+        if not (fmin > 0.0) or not math.isfinite(fmax) or math.log2(fmax / fmin) > 58.0:
+            return None
+        w[j - 1], c[j - 1] = wj, cj
+        K *= kq ** k
+    if p is None or not math.isfinite(K):
+        return None
+    return PlainFamily("prod_quad", d, w, gamma=c, K=K, power=int(p))
+
+
 def recognize_plain(e, d):
     """Match a closed family (PlainFamily) or return None."""
+    if e.op == "mul" and len(e.args) > 1:
+        return _prod_family(e.val, e.args, d)
     K, core = _strip_scale(e)
     if core.op == "exp":
         arg = core.args[0]
@@ -232,7 +298,7 @@ def recognize_plain(e, d):
             beta = _vec(lf[1], d)
             if beta is not None:
                 return PlainFamily("lin_pow", d, beta, alpha=lf[0], K=K, power=int(core.idx))
-        return None
+        return _prod_family(K, (core,), d)
     # C0 + sum_k coef_k trig(alpha_k + F(x)) with one shared form F: linear
     # (lin_sincos) or diagonal quadratic (quad_sincos)
     if e.op == "add":

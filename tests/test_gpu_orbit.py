@@ -273,3 +273,51 @@ def test_layout_edges_vs_index_kernel(env, n, d, a, monkeypatch):
         from oracle import np_oracle
         ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
         assert math.isclose(got, ref, rel_tol=REL), (n, d, got, ref)
+
+
+@pytest.mark.parametrize("text,d", [
+    ("prod(i=1..d, 1/(0.81 + (x[i]-0.6)^2))", 10),                                   # corpus ratprod
+    ("(0.81 + x[1]^2 - 1.2*x[1])^(-2) * (2 + x[2]^2)^(-2) * 3", 2),
+    ("prod(i=1..d, (0.3 + (x[i]-0.25)^2))", 40),
+    ("prod(i=1..d, 1/(0.0001 + (x[i]-0.5)^2))", 6),                                  # sharp peaks
+])
+def test_product_family_vs_bytecode_and_oracle(env, text, d, monkeypatch):
+    lq, N, engine = env
+    from oracle import np_oracle
+    f = lq.parse(text, d)
+    fam = engine.plain_integrand(f, d)
+    assert fam.kind == "prod_quad"
+    prog = engine.plain_integrand(f, d, force_program=True)
+    monkeypatch.setenv("LQ_JIT", "0")
+    for n, a in ((10007, 1234), (1000003, 76543)):
+        rule = lq.korobov_vector(a, n, d)
+        z = rule.z_reduced_array()
+        got = engine.lattice_sum(fam, n, z)
+        want = engine.lattice_sum(prog, n, z)
+        assert math.isclose(got, want, rel_tol=1e-12), (text, n, got, want)
+        if n * d <= 200000:
+            ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
+            assert math.isclose(got, ref, rel_tol=REL), (text, n, got, ref)
+
+
+def test_product_family_config4_integrand(env, monkeypatch):
+    # config 4's product peak: factors ~ 10^2..10^5, so the running product needs
+    # the exponent renormalisation.  All 500 factors underflow the sum to 0.0 in
+    # FP64 (reference-identical): the first 90 factors keep
+    # it representable (~1e-248).
+    lq, N, engine = env
+    from paper_2404_08867_b200.configs import make_config
+    cfg = make_config(4)
+    d = 90
+    text = " * ".join(cfg.text.split(" * ")[:d])
+    f = lq.parse(text, d)
+    fam = engine.plain_integrand(f, d)
+    assert fam.kind == "prod_quad"
+    prog = engine.plain_integrand(f, d, force_program=True)
+    monkeypatch.setenv("LQ_JIT", "0")
+    for n, a in ((100003, 3), (1 << 20, 5)):
+        rule = lq.korobov_vector(a, n, d)
+        z = rule.z_reduced_array()
+        got = engine.lattice_sum(fam, rule.n, z)
+        want = engine.lattice_sum(prog, rule.n, z)
+        assert got > 0.0 and math.isclose(got, want, rel_tol=1e-11), (n, got, want)
