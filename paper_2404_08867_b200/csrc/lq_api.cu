@@ -364,7 +364,6 @@ int launch_prod(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z,
             return fail(LQ_ERR_UNSUPPORTED, "product factor %d spans [%g, %g]", j + 1, fmin, fmax);
         worst = std::fmax(worst, std::fmax(std::fabs(std::log2(fmin) - 2 * g), std::fabs(std::log2(fmax) - 2 * g)));
         lq::ProdDim r;
-        r.m = m;
         r.w = std::ldexp(w, -g);
         r.c = std::ldexp(cj, -2 * g);
         if (cj != 0.0 && !std::isnormal(r.c))
@@ -382,7 +381,8 @@ int launch_prod(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z,
     if (off > (1ll << 30)) return fail(LQ_ERR_UNSUPPORTED, "product exponent offset too large");
     const int nf = (int)tab.size();
     auto head = [&](auto& a) {
-        a.nf = nf; a.n = (uint32_t)n; a.base = base; a.end = end; a.K = f->K; a.pw = f->power; a.off = (int32_t)off;
+        a.nf = nf; a.n = (uint32_t)n; a.base = base; a.end = end; a.K = f->K; a.pw = f->power; a.m = m;
+        a.off = (int32_t)off;
         a.rmask = R - 1;
     };
     if (nf <= lq::kProdParamDims) {

@@ -349,7 +349,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_fam(const __grid_constant__ Arg
 // [1, 2) every R factors (host-chosen so R scaled factors cannot leave
 // 2^(+-1000)) with its exponent kept in an integer.
 struct ProdDim {
-    double m;       // 2^(1074 - g) / n: denormal residue -> x 2^-g
     double w;       // w_j 2^-g
     double c;       // c_j 2^-2g
     uint32_t z, zs, z2, z2m;
@@ -361,6 +360,7 @@ struct ProdArgs {
     uint32_t n;
     uint64_t base, end;
     double K, pw;
+    double m;            // 2^(1074 - g) / n: denormal residue -> x 2^-g
     int32_t off;         // 2 g nf: D_true = D 2^(E + off)
     int32_t rmask;       // renormalise after factor j when (j & rmask) == rmask
     ProdDim dims[N];
@@ -370,12 +370,12 @@ struct ProdArgsG {   // more factors than kProdParamDims: records in global memo
     int nf;
     uint32_t n;
     uint64_t base, end;
-    double K, pw;
+    double K, pw, m;
     int32_t off, rmask;
     const ProdDim* __restrict__ dims;
 };
 
-constexpr int kProdParamDims = 780;   // 780 x 40 B + header < 32 KB
+constexpr int kProdParamDims = 1000;  // 1000 x 32 B + header < 32 KB
 
 __device__ __forceinline__ void renorm(double& D, int& E) {
     const int hi = __double2hiint(D), lo = __double2loint(D);
@@ -406,12 +406,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_prod(const __grid_constant__ Ar
         D[p] = 1.0;
         E[p] = 0;
     }
+    // m is the same for every factor: one vector register for the whole loop,
+    // so each FP64 op below has at most one uniform operand (w_j or c_j) and
+    // the per-factor records stay LDCU/UR operands
+    double m;
+    asm("mov.b64 %0, %1;" : "=d"(m) : "d"(a.m));
     #pragma unroll 1
     for (int j = 0; j < a.nf; ++j) {
-        const ProdDim& q = a.dims[j];
-        const uint32_t z = q.z, z2 = q.z2, z2m = q.z2m;
-        const double m = q.m, w = q.w, c = q.c;
-        uint32_t r0 = mulmod_shoup(i0, z, q.zs, n);
+        const uint32_t z = a.dims[j].z, z2 = a.dims[j].z2, z2m = a.dims[j].z2m;
+        const double w = a.dims[j].w, c = a.dims[j].c;
+        uint32_t r0 = mulmod_shoup(i0, z, a.dims[j].zs, n);
         uint32_t r1 = step_mod(r0, z, z - n);
         #pragma unroll
         for (int p = 0; p < P; p += 2) {
