@@ -141,6 +141,13 @@ int lq_lattice_partials(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const ui
 /* Fixed pairwise tree over vals_dev[0..count); result to host *out. */
 int lq_reduce_sum(lq_ctx* ctx, const double* vals_dev, int64_t count, double* out);
 
+/* ---- Monte Carlo: replaces quad.mc_integrate's loop (quad.py:79-93).  Sums
+ * f over points [i_begin, i_end) of numpy's default_rng(seed).random((n, d))
+ * stream, reproduced bit for bit on the device: PCG64 state/increment as
+ * (lo, hi) words of bit_generator.state after seeding (host bookkeeping).   */
+int lq_mc_sum(lq_ctx* ctx, const lq_program* prog, int32_t d, uint64_t n, const uint64_t* state,
+              const uint64_t* inc, uint64_t i_begin, uint64_t i_end, double* sum_out);
+
 /* ---- direct tensor-grid sum: replaces mdi._numeric_sum / direct_tensor_sum
  * (mdi.py:104-136) for implr_integrate and the MDI fallback.  Flat index s
  * decodes first axis fastest.  nodes: concatenated per-axis node values

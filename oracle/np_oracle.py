@@ -85,6 +85,43 @@ def slr_value(f, n, z):
     return slr_sum(f, n, z) / n
 
 
+def mc_value(f, d, n, seed=0, rows=1 << 19):
+    """quad.py:79-93: numpy default_rng(seed).random((rows, d)) blocks,
+    eval_array, float(np.sum) accumulated per block, divided by n."""
+    rng = np.random.default_rng(seed)
+    acc, done = 0.0, 0
+    while done < n:
+        m = min(rows, n - done)
+        pts = rng.random((m, d))
+        vals = eval_array(f, {i + 1: pts[:, i] for i in range(d)})
+        acc += float(vals) * m if np.ndim(vals) == 0 else float(np.sum(vals))
+        done += m
+    return acc / n
+
+
+PCG64_MULT = 0x2360ED051FC65DA44385DF649FCCF645   # numpy's PCG_DEFAULT_MULTIPLIER_128
+
+
+def pcg64_draw(state, inc, k):
+    """Draw k (0-based) of numpy's PCG64 stream from (state, inc), by the affine
+    jump s_k = M^(k+1) s + inc (M^k + ... + 1) and the XSL-RR output -- the
+    restatement the device generator (lq_mc_sum) follows."""
+    mask = (1 << 128) - 1
+    A, C = 1, 0
+    PA, PC = PCG64_MULT, inc
+    e = k + 1
+    while e:
+        if e & 1:
+            A, C = (PA * A) & mask, (PA * C + PC) & mask
+        PA, PC = (PA * PA) & mask, (PA * PC + PC) & mask
+        e >>= 1
+    s = (A * state + C) & mask
+    rot = s >> 122
+    x = ((s >> 64) ^ s) & ((1 << 64) - 1)
+    out = ((x >> rot) | (x << ((64 - rot) & 63))) & ((1 << 64) - 1)
+    return (out >> 11) * (1.0 / 9007199254740992.0)
+
+
 def axis_counts(n, z):
     """transform.py:76-83 on the unreduced z."""
     out = [math.lcm(z[i], z[i + 1]) // min(z[i], z[i + 1]) for i in range(len(z) - 1)]

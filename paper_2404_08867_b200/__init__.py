@@ -12,7 +12,7 @@ from .lattice import LatticeRule, iter_point_blocks, korobov_vector, lattice_poi
 from .transform import AxisGridSet, axis_counts, midpoint_grids
 from .mdi import (DEFAULT_NODE_BUDGET, DIRECT_CAP, BudgetExceededError, GridCapError, MdiConfig,
                   MdiReport, direct_tensor_sum, mdi_lr, mdi_sum)
-from .quad import QuadratureResult, implr_integrate, mdilr_integrate, slr_integrate
+from .quad import QuadratureResult, implr_integrate, mc_integrate, mdilr_integrate, slr_integrate
 from .quality import (QualityWarning, WeightModel, bernoulli_poly, cbc_construct, korobov_search, p_alpha,
                       shift_avg_wce_sq)
 
@@ -24,7 +24,7 @@ __all__ = [
     "AxisGridSet", "axis_counts", "midpoint_grids",
     "DEFAULT_NODE_BUDGET", "DIRECT_CAP", "BudgetExceededError", "GridCapError", "MdiConfig",
     "MdiReport", "direct_tensor_sum", "mdi_lr", "mdi_sum",
-    "QuadratureResult", "implr_integrate", "mdilr_integrate", "slr_integrate",
+    "QuadratureResult", "implr_integrate", "mc_integrate", "mdilr_integrate", "slr_integrate",
     "QualityWarning", "WeightModel", "bernoulli_poly", "cbc_construct", "korobov_search", "p_alpha",
     "shift_avg_wce_sq",
     "__version__",

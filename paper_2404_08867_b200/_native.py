@@ -72,6 +72,8 @@ _SIGS = {
     "lq_lattice_layout": [C.POINTER(Integrand), C.c_uint64, _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                           C.POINTER(C.c_int64), C.POINTER(C.c_int32)],
     "lq_reduce_sum": [_P, _P, C.c_int64, C.POINTER(C.c_double)],
+    "lq_mc_sum": [_P, C.POINTER(Program), C.c_int32, C.c_uint64, _P, _P, C.c_uint64, C.c_uint64,
+                  C.POINTER(C.c_double)],
     "lq_tensor_sum": [_P, C.POINTER(Program), C.c_int32, _P, _P, C.c_int32, C.c_uint64, C.c_uint64,
                       C.POINTER(C.c_double)],
     "lq_mdi_block_sums": [_P, _P, C.c_int32, _P, C.c_int32, _P, C.c_int64, C.c_int32, C.c_int32, _P],

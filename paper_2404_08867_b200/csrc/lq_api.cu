@@ -1052,6 +1052,69 @@ int lq_lattice_sum(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t*
     return read_scalar(c, r, sum_out);
 }
 
+// Monte Carlo over numpy's PCG64 stream (quad.mc_integrate, quad.py:79-93).
+int lq_mc_sum(lq_ctx* c, const lq_program* pg, int32_t d, uint64_t n, const uint64_t* state, const uint64_t* inc,
+              uint64_t i_begin, uint64_t i_end, double* sum_out) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (!pg || !pg->insn || pg->n_insn < 1) return fail(LQ_ERR_VALUE, "null program");
+    if (!state || !inc || !sum_out) return fail(LQ_ERR_VALUE, "null argument");
+    if (d < 1) return fail(LQ_ERR_VALUE, "dimension must be positive, got %d", d);
+    if (n < 1) return fail(LQ_ERR_VALUE, "sample count must be >= 1, got %llu", (unsigned long long)n);
+    if (i_end > n || i_end < i_begin) return fail(LQ_ERR_VALUE, "bad point range");
+    if (pg->n_vars > d) return fail(LQ_ERR_VALUE, "program uses %d variables, d=%d", pg->n_vars, d);
+    if ((unsigned __int128)n * (unsigned)d >= ((unsigned __int128)1 << 64))
+        return fail(LQ_ERR_OVERFLOW, "n*d draws exceed 2^64");
+    const int ns = pick_slots(pg->n_slots);
+    if (ns < 0) return fail(LQ_ERR_UNSUPPORTED, "program needs %d slots (max %d)", pg->n_slots, LQ_MAX_SLOTS);
+    if (i_end == i_begin) {
+        *sum_out = 0.0;
+        return LQ_OK;
+    }
+    typedef unsigned __int128 u128;
+    const u128 M = ((u128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;   // PCG_DEFAULT_MULTIPLIER_128
+    const u128 I = ((u128)inc[1] << 64) | inc[0];
+    auto pack = [](u128 A, u128 C) {
+        return lq::Jump{(uint64_t)A, (uint64_t)(A >> 64), (uint64_t)C, (uint64_t)(C >> 64)};
+    };
+    std::vector<lq::Jump> tab(d + 1 + 64);
+    u128 A = 1, C = 0;   // b draws: A_b = M^b, C_b = inc (M^(b-1) + ... + 1)
+    for (int b = 0; b <= d; ++b) {
+        tab[b] = pack(A, C);
+        C = M * C + I;
+        A = M * A;
+    }
+    u128 PA = M, PC = I;   // 2^k draws
+    for (int k = 0; k < 64; ++k) {
+        tab[d + 1 + k] = pack(PA, PC);
+        PC = PA * PC + PC;
+        PA = PA * PA;
+    }
+    void *dp, *dt;
+    if ((rc = upload(c, B_PROG, pg->insn, sizeof(lq_insn) * pg->n_insn, &dp))) return rc;
+    if ((rc = upload(c, B_AUX0, tab.data(), sizeof(lq::Jump) * tab.size(), &dt))) return rc;
+    const int64_t ntiles = (int64_t)((i_end - i_begin + lq::kTile - 1) / lq::kTile);
+    void* tiles;
+    if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
+    const lq::Jump* jt = (const lq::Jump*)dt;
+    const void* kern = ns == 32 ? (const void*)lq::k_prog_mc<32> : (const void*)lq::k_prog_mc<LQ_MAX_SLOTS>;
+    const int grid = grid_for(c, kern, ntiles);
+    t_begin(c);
+    if (ns == 32)
+        lq::k_prog_mc<32><<<grid, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, pg->n_insn, pg->result, d, jt,
+                                                                 jt + d + 1, state[0], state[1], i_begin, i_end,
+                                                                 ntiles, (double*)tiles);
+    else
+        lq::k_prog_mc<LQ_MAX_SLOTS><<<grid, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, pg->n_insn, pg->result,
+                                                                          d, jt, jt + d + 1, state[0], state[1],
+                                                                          i_begin, i_end, ntiles, (double*)tiles);
+    t_end(c);
+    CK(cudaGetLastError());
+    double* r;
+    if ((rc = reduce_dev(c, (const double*)tiles, ntiles, &r))) return rc;
+    return read_scalar(c, r, sum_out);
+}
+
 int lq_tensor_sum(lq_ctx* c, const lq_program* pg, int32_t d, const int64_t* counts, const double* nodes,
                   int32_t midpoint, uint64_t s_begin, uint64_t s_end, double* sum_out) {
     int rc = set_dev(c);

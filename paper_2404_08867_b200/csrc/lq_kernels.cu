@@ -628,6 +628,70 @@ __global__ void __launch_bounds__(kThreads) k_prog_lattice(const lq_insn* __rest
     }
 }
 
+// ============================================================ Monte Carlo
+// quad.mc_integrate (quad.py:79-93) draws numpy's default_rng(seed).random((rows, d))
+// row-major: PCG64 (128-bit LCG s <- M s + inc, XSL-RR 128/64 output of the new
+// state), random() = (out >> 11) 2^-53.  Draw k of the stream is an affine
+// jump of the seed state, so every coordinate is generated in place: thread
+// state S = state before its point's first draw, coordinate b = output of
+// A_(b+1) S + C_(b+1) (host-computed jump table), next point S <- A_d S + C_d.
+typedef unsigned __int128 u128;
+
+struct Jump {        // s -> A s + C (mod 2^128)
+    uint64_t alo, ahi, clo, chi;
+};
+
+__device__ __forceinline__ u128 jump_apply(const Jump& j, u128 s) {
+    const u128 A = ((u128)j.ahi << 64) | j.alo, C = ((u128)j.chi << 64) | j.clo;
+    return A * s + C;
+}
+
+__device__ __forceinline__ double pcg_double(u128 s) {
+    const uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+    const unsigned rot = (unsigned)(hi >> 58);
+    const uint64_t x = hi ^ lo;
+    const uint64_t out = (x >> rot) | (x << ((64u - rot) & 63u));
+    return (double)(out >> 11) * (1.0 / 9007199254740992.0);
+}
+
+struct McSrc {
+    u128 S;
+    const Jump* __restrict__ jt;   // jt[b] advances by b draws, b = 0..d
+    __device__ __forceinline__ double x(int b) const {
+        const Jump j = jt[b + 1];
+        return pcg_double(jump_apply(j, S));
+    }
+};
+
+// Points [base, end) in tiles of 4096 (256 threads x 16 consecutive points).
+// pow2[k] jumps by 2^k draws (k < 64).
+template <int NS>
+__global__ void __launch_bounds__(kThreads) k_prog_mc(const lq_insn* __restrict__ prog, int n_insn, int result, int d,
+                                                      const Jump* __restrict__ jt, const Jump* __restrict__ pow2,
+                                                      uint64_t s0lo, uint64_t s0hi, uint64_t base, uint64_t end,
+                                                      int64_t ntiles, double* __restrict__ tile_out) {
+    __shared__ double sh[8];
+    double slot[NS];
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t i0 = base + (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kPts;
+        u128 S = ((u128)s0hi << 64) | s0lo;
+        const uint64_t k0 = i0 * (uint64_t)d;   // draws before point i0
+        for (int k = 0; k < 64; ++k)
+            if ((k0 >> k) & 1ull) S = jump_apply(pow2[k], S);
+        const Jump jd = jt[d];
+        double s = 0.0;
+        for (int p = 0; p < kPts; ++p) {
+            if (i0 + p < end) {
+                McSrc src{S, jt};
+                s += run_program<NS>(prog, n_insn, result, src, slot);
+            }
+            S = jump_apply(jd, S);
+        }
+        s = block_sum(s, sh);
+        if (threadIdx.x == 0) tile_out[tile] = s;
+    }
+}
+
 // ============================================================ tensor grid
 constexpr int kMaxAxes = 128;
 

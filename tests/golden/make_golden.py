@@ -37,7 +37,7 @@ from latquad import corpus, exprcore  # noqa: E402  (reference, read-only)
 from latquad.lattice import (LatticeRule, WeightModel, cbc_construct, korobov_search,  # noqa: E402
                              korobov_vector, p_alpha, points_block, shift_avg_wce_sq)
 from latquad.mdi import MdiConfig, direct_tensor_sum, mdi_lr  # noqa: E402
-from latquad.quad import implr_integrate, mdilr_integrate, slr_integrate  # noqa: E402
+from latquad.quad import implr_integrate, mc_integrate, mdilr_integrate, slr_integrate  # noqa: E402
 from latquad.transform import axis_counts, midpoint_grids  # noqa: E402
 
 from paper_2404_08867_b200.configs import make_config  # noqa: E402
@@ -246,15 +246,37 @@ def quality_cases():
     return out
 
 
+def mc_cases():
+    """quad.mc_integrate (quad.py:79-93): numpy default_rng(seed) streams; the
+    first rows of the stream are frozen too, so the device generator is pinned
+    point by point, not only through the mean."""
+    out = []
+
+    def add(tag, text, d, n, seed):
+        f = exprcore.parse(text, d)
+        r = mc_integrate(f, d, n, seed=seed)
+        first = np.random.default_rng(seed).random((min(n, 64), d))
+        out.append({"tag": tag, "text": text, "d": d, "n": n, "seed": seed, "value": hx(r.value),
+                    "first_rows": b64(first), "first_shape": list(first.shape)})
+
+    add("expxy_101_s0", corpus.get("expxy").text, 2, 101, 0)
+    add("expxy_40001_s7", corpus.get("expxy").text, 2, 40001, 7)
+    add("sinsq_10001_s1", corpus.get("sinsq").text, 2, 10001, 1)
+    add("gaussian5_70000_s3", corpus.get("gaussian").text, 5, 70000, 3)
+    add("ratprod7_600000_s11", corpus.get("ratprod").text, 7, 600000, 11)   # > one 2^19-row block
+    add("const_2p5", "2.5", 3, 1000, 0)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
-    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality"], default=None)
+    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc"], default=None)
     args = ap.parse_args()
     meta = {"generator": "tests/golden/make_golden.py", "numpy": np.__version__,
             "python": sys.version.split()[0], "reference": "/root/reference/pkg (latquad 0.1.0)"}
     jobs = {"points": lambda: points_cases(), "slr": lambda: slr_cases(args.skip_slow),
-            "mdi": lambda: mdi_cases(args.skip_slow), "quality": quality_cases}
+            "mdi": lambda: mdi_cases(args.skip_slow), "quality": quality_cases, "mc": mc_cases}
     for name, fn in jobs.items():
         if args.only and name != args.only:
             continue

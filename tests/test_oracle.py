@@ -93,3 +93,21 @@ def test_configs_are_seeded_as_documented(golden):
         assert case["text"] == cfg.text
         assert int(case["z"][1]) == cfg.plain_a
     assert make_config(3).plain_a == 811507
+
+
+def test_mc_oracle_pinned_to_reference():
+    # quad.mc_integrate values and the first rows of each stream, frozen from the reference
+    import numpy as np
+    import paper_2404_08867_b200 as lq
+    from conftest import load_golden, unb64, unhex
+    from oracle import np_oracle
+    for case in load_golden("mc"):
+        f = lq.parse(case["text"], case["d"])
+        got = np_oracle.mc_value(f, case["d"], case["n"], case["seed"])
+        assert abs(got - unhex(case["value"])) <= 1e-13 * abs(unhex(case["value"])), case["tag"]
+        first = unb64(case["first_rows"], case["first_shape"])
+        st = np.random.default_rng(case["seed"]).bit_generator.state["state"]
+        d = case["d"]
+        for i in (0, 1, first.shape[0] - 1):
+            for j in range(d):
+                assert np_oracle.pcg64_draw(st["state"], st["inc"], i * d + j) == first[i, j], (case["tag"], i, j)
