@@ -268,15 +268,31 @@ def mc_cases():
     return out
 
 
+def suite_cases():
+    """Rows of the reference's benchmark suites (bench.py:104-211) that run in
+    seconds here: test1, test2, test3, test5 (values, reference values, status)."""
+    from latquad import bench as rbench
+    out = []
+    for suite in ("test1", "test2", "test3", "test5"):
+        for spec in rbench.suite_specs(suite):
+            rec = rbench._run_row(spec, 0, False)
+            out.append({"suite": suite, "method": rec.method, "integrand": rec.integrand, "d": rec.d,
+                        "n": str(rec.n), "a": rec.a, "status": rec.status,
+                        "value": None if rec.value is None else hx(rec.value),
+                        "reference": None if rec.reference is None else hx(rec.reference)})
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
-    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc"], default=None)
+    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites"], default=None)
     args = ap.parse_args()
     meta = {"generator": "tests/golden/make_golden.py", "numpy": np.__version__,
             "python": sys.version.split()[0], "reference": "/root/reference/pkg (latquad 0.1.0)"}
     jobs = {"points": lambda: points_cases(), "slr": lambda: slr_cases(args.skip_slow),
-            "mdi": lambda: mdi_cases(args.skip_slow), "quality": quality_cases, "mc": mc_cases}
+            "mdi": lambda: mdi_cases(args.skip_slow), "quality": quality_cases, "mc": mc_cases,
+            "suites": suite_cases}
     for name, fn in jobs.items():
         if args.only and name != args.only:
             continue

@@ -89,3 +89,17 @@ def test_fit_power_law_and_cli(tmp_path, capsys):
             continue
         got = fits.fit_power_law(sub, model)
         assert abs(got.exponent - want.exponent) < 1e-12 and abs(got.r_squared - want.r_squared) < 1e-12
+
+
+def test_suite_specs_match_reference_rows():
+    from paper_2404_08867_b200 import suites
+    from conftest import load_golden
+    # every frozen reference row appears, in order, in our suite grids
+    rows = load_golden("suites")
+    for suite in ("test1", "test2", "test3", "test5"):
+        want = [(r["method"], r["integrand"], r["d"], int(r["n"]), r["a"]) for r in rows if r["suite"] == suite]
+        assert suites.suite_specs(suite) == want, suite
+    assert len(suites.suite_specs("test4")) == 10 and len(suites.suite_specs("test4", unbounded=True)) == 14
+    assert len(suites.suite_specs("test7")) == 42
+    with pytest.raises(ValueError):
+        suites.suite_specs("test9")
