@@ -133,3 +133,19 @@ def test_mdi_policies(lq):
     for m in (1, 2, 3):
         rep = lq.mdi_sum(g, grids, lq.MdiConfig(m=m))
         assert rep.levels == math.ceil((7 - rep.base_dim) / m) and 1 <= rep.base_dim <= 3
+
+
+def test_mdi_m_order_invariance_and_huge_grid(lq):
+    # the reference's TestMdiSum.test_m_and_order_invariance / test_huge_grid_normalization
+    from paper_2404_08867_b200 import corpus
+    f = corpus.corpus_expr("sinsq", 6)
+    grids = lq.midpoint_grids(lq.korobov_vector(3, 3**6, 6))
+    base = lq.mdi_sum(f, grids, lq.MdiConfig(m=1)).value
+    for m in (1, 2, 3):
+        for order in ("forward", "reverse"):
+            got = lq.mdi_sum(f, grids, lq.MdiConfig(m=m, order=order)).value
+            assert got == pytest.approx(base, rel=1e-12)
+    g = corpus.corpus_expr("expalt", 20)
+    got = lq.mdi_lr(g, 20, 8, 8**20)
+    ref = corpus.reference_value("expalt", 20)
+    assert math.isfinite(got) and abs(got - ref) / abs(ref) < 2e-2

@@ -77,3 +77,28 @@ def test_mc_errors(lq):
         lq.mc_integrate(lq.parse("x[1]", 1), 1, 0)
     r = lq.mc_integrate(lq.parse("2.5", 3), 3, 1000)
     assert r.value == 2.5
+
+
+def test_mc_seed_determinism_and_three_sigma(lq):
+    # the reference's own Monte-Carlo checks (tests/test_quad.py TestMonteCarlo)
+    from paper_2404_08867_b200 import corpus
+    f = corpus.corpus_expr("gaussian", 3)
+    a = lq.mc_integrate(f, d=3, n=4096, seed=11)
+    b = lq.mc_integrate(f, d=3, n=4096, seed=11)
+    c = lq.mc_integrate(f, d=3, n=4096, seed=12)
+    assert a.value == b.value and a.value != c.value
+    r = lq.mc_integrate(lq.parse("x[1]", 1), d=1, n=10**6, seed=0)
+    assert abs(r.value - 0.5) <= 3.0 * (1.0 / math.sqrt(12.0)) / 1e3
+    r = lq.mc_integrate(corpus.corpus_expr("expsum", 3), d=3, n=10**4, seed=5, reference=1.0)
+    assert r.rel_error == pytest.approx(abs(r.value - 1.0))
+
+
+def test_mc_error_slope(lq):
+    # acceptance check 10 of the reference: mean |error| ~ n^-1/2
+    from paper_2404_08867_b200 import corpus
+    f = corpus.corpus_expr("gaussian", 2)
+    ref = corpus.reference_value("gaussian", 2)
+    ns = [10**3, 10**4, 10**5]
+    means = [np.mean([lq.mc_integrate(f, 2, n, seed=s, reference=ref).rel_error for s in range(16)]) for n in ns]
+    slope = float(np.polyfit(np.log(ns), np.log(means), 1)[0])
+    assert abs(slope + 0.5) <= 0.15, slope
