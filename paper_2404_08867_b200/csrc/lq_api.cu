@@ -347,13 +347,19 @@ bool uses_family_kernel(const lq_integrand* f, uint64_t n) {
 // factor carries 2^-2g; the running product is renormalised every R factors,
 // R the largest power of two <= 16 that keeps R worst-case scaled factors
 // inside 2^(+-1000).
-int launch_prod(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z, uint64_t base, uint64_t end,
-                int64_t ntiles, double* tiles_dev) {
+struct ProdScale {
+    int g = 0, R = 16;
+    double m = 0.0;
+    int64_t off = 0;
+    std::vector<int> dims;            // coordinates carrying a factor
+    std::vector<double> w, c;         // scaled w_j 2^-g, c_j 2^-2g
+};
+
+int prod_scale(const lq_integrand* f, uint64_t n, ProdScale& ps) {
     if (!f->beta || !f->gamma) return fail(LQ_ERR_VALUE, "product family needs beta (w) and gamma (c)");
-    const int g = std::max(0, 51 - std::ilogb((double)n));
-    const double m = std::ldexp(1.0 / (double)n, 1074 - g);
-    if (!std::isfinite(m)) return fail(LQ_ERR_UNSUPPORTED, "product family: scale overflow for n=%llu", (unsigned long long)n);
-    std::vector<lq::ProdDim> tab;
+    ps.g = std::max(0, 51 - std::ilogb((double)n));
+    ps.m = std::ldexp(1.0 / (double)n, 1074 - ps.g);
+    if (!std::isfinite(ps.m)) return fail(LQ_ERR_UNSUPPORTED, "product family: scale overflow for n=%llu", (unsigned long long)n);
     double worst = 0.0;
     for (int j = 0; j < f->d; ++j) {
         const double w = f->beta[j], cj = f->gamma[j];
@@ -362,23 +368,41 @@ int launch_prod(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z,
         const double fmin = cj + dist * dist, fmax = cj + std::fmax(w * w, (1.0 - w) * (1.0 - w));
         if (!(fmin > 0.0) || !std::isfinite(fmax))
             return fail(LQ_ERR_UNSUPPORTED, "product factor %d spans [%g, %g]", j + 1, fmin, fmax);
-        worst = std::fmax(worst, std::fmax(std::fabs(std::log2(fmin) - 2 * g), std::fabs(std::log2(fmax) - 2 * g)));
-        lq::ProdDim r;
-        r.w = std::ldexp(w, -g);
-        r.c = std::ldexp(cj, -2 * g);
-        if (cj != 0.0 && !std::isnormal(r.c))
+        worst = std::fmax(worst, std::fmax(std::fabs(std::log2(fmin) - 2 * ps.g), std::fabs(std::log2(fmax) - 2 * ps.g)));
+        const double cs = std::ldexp(cj, -2 * ps.g);
+        if (cj != 0.0 && !std::isnormal(cs))
             return fail(LQ_ERR_UNSUPPORTED, "product factor %d out of the scaled range", j + 1);
+        ps.dims.push_back(j);
+        ps.w.push_back(std::ldexp(w, -ps.g));
+        ps.c.push_back(cs);
+    }
+    ps.R = 16;
+    while (ps.R > 1 && ps.R * (worst + 1.0) > 1000.0) ps.R /= 2;
+    if ((worst + 1.0) > 1000.0) return fail(LQ_ERR_UNSUPPORTED, "product factors span more than 2^1000");
+    ps.off = 2ll * ps.g * (int64_t)ps.dims.size();
+    if (ps.off > (1ll << 30)) return fail(LQ_ERR_UNSUPPORTED, "product exponent offset too large");
+    return LQ_OK;
+}
+
+int launch_prod(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z, uint64_t base, uint64_t end,
+                int64_t ntiles, double* tiles_dev) {
+    ProdScale ps;
+    int rc0 = prod_scale(f, n, ps);
+    if (rc0) return rc0;
+    std::vector<lq::ProdDim> tab(ps.dims.size());
+    for (size_t k = 0; k < ps.dims.size(); ++k) {
+        const int j = ps.dims[k];
+        lq::ProdDim& r = tab[k];
+        r.w = ps.w[k];
+        r.c = ps.c[k];
         r.z = (uint32_t)z[j];
         r.zs = (uint32_t)(((uint64_t)z[j] << 32) / n);
         r.z2 = (uint32_t)((2 * z[j]) % n);
         r.z2m = r.z2 - (uint32_t)n;
-        tab.push_back(r);
     }
-    int R = 16;
-    while (R > 1 && R * (worst + 1.0) > 1000.0) R /= 2;
-    if ((worst + 1.0) > 1000.0) return fail(LQ_ERR_UNSUPPORTED, "product factors span more than 2^1000");
-    const int64_t off = 2ll * g * (int64_t)tab.size();
-    if (off > (1ll << 30)) return fail(LQ_ERR_UNSUPPORTED, "product exponent offset too large");
+    const double m = ps.m;
+    const int64_t off = ps.off;
+    const int R = ps.R;
     const int nf = (int)tab.size();
     auto head = [&](auto& a) {
         a.nf = nf; a.n = (uint32_t)n; a.base = base; a.end = end; a.K = f->K; a.pw = f->power; a.m = m;
@@ -576,6 +600,7 @@ struct OrbPlan {
     uint32_t n = 0, a = 0, as = 0, qc = 0, h = 0;
     uint64_t units = 0;
     int m = 0;
+    bool mirror = true;
     std::vector<uint32_t> G, Alo, Ahi;
 };
 
@@ -583,7 +608,9 @@ constexpr uint32_t kOrbMaxCosets = 4096;
 
 // nullptr when the rule is not a Korobov rule over a prime modulus the orbit
 // kernel can enumerate (caller then uses the per-index kernels).
-std::shared_ptr<const OrbPlan> build_orbit_plan(uint32_t n, uint32_t a, int m) {
+// mirror: enumerate half of the nonzero points (their mirrors n - i are summed
+// with them); otherwise every nonzero point once (product family).
+std::shared_ptr<const OrbPlan> build_orbit_plan(uint32_t n, uint32_t a, int m, bool mirror) {
     if (!is_prime32(n) || a < 1 || a >= n) return nullptr;
     std::vector<uint32_t> primes;
     uint32_t rest = n - 1;
@@ -605,13 +632,14 @@ std::shared_ptr<const OrbPlan> build_orbit_plan(uint32_t n, uint32_t a, int m) {
     }
     const uint32_t C = (n - 1) / o;
     uint32_t cosets, h;
-    if (o % 2 == 0) { cosets = C; h = o / 2; }          // -1 lies in <a>: half of each coset
+    if (!mirror) { cosets = C; h = o; }                 // every coset, every exponent
+    else if (o % 2 == 0) { cosets = C; h = o / 2; }     // -1 lies in <a>: half of each coset
     else { cosets = C / 2; h = o; }                     // -coset(s) = coset(s + C/2)
     if (cosets < 1 || cosets > kOrbMaxCosets || h < (uint32_t)m) return nullptr;
     static std::atomic<uint64_t> next_id{1};
     auto p = std::make_shared<OrbPlan>();
     p->id = next_id++;
-    p->n = n; p->a = a; p->m = m; p->h = h;
+    p->n = n; p->a = a; p->m = m; p->h = h; p->mirror = mirror;
     p->as = (uint32_t)(((uint64_t)a << 32) / n);
     p->qc = (h + m - 1) / m;
     p->units = (uint64_t)cosets * p->qc;
@@ -630,14 +658,14 @@ std::shared_ptr<const OrbPlan> build_orbit_plan(uint32_t n, uint32_t a, int m) {
     return p;
 }
 
-std::shared_ptr<const OrbPlan> orbit_plan(uint32_t n, uint32_t a, int m) {
+std::shared_ptr<const OrbPlan> orbit_plan(uint32_t n, uint32_t a, int m, bool mirror) {
     static std::mutex mu;
-    static std::map<std::tuple<uint32_t, uint32_t, int>, std::shared_ptr<const OrbPlan>> cache;
+    static std::map<std::tuple<uint32_t, uint32_t, int, bool>, std::shared_ptr<const OrbPlan>> cache;
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(n, a, m);
+    auto key = std::make_tuple(n, a, m, mirror);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
-    auto p = build_orbit_plan(n, a, m);
+    auto p = build_orbit_plan(n, a, m, mirror);
     if (cache.size() > 64) cache.clear();
     cache[key] = p;
     return p;
@@ -656,18 +684,22 @@ int orbit_mode() {
 
 std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, const uint64_t* z) {
     const int mode = orbit_mode();
-    if (mode == 0 || !z || f->kind == LQ_FAM_PROGRAM || f->kind == LQ_FAM_PROD_QUAD || f->d < 2) return nullptr;
+    if (mode == 0 || !z || f->kind == LQ_FAM_PROGRAM || f->d < 2) return nullptr;
     if (n > (1ull << 31) || n < 5) return nullptr;
+    const bool prod = f->kind == LQ_FAM_PROD_QUAD;
     const bool quad = is_quad_kind(f->kind);
-    const int m = lq::orb_len(quad ? lq::FAM_QUAD : lq::FAM_LIN);
-    const int cap = quad ? lq::kOrbQuadDims : lq::kOrbLinDims;
+    const int m = prod ? lq::kOrbProdM : lq::orb_len(quad ? lq::FAM_QUAD : lq::FAM_LIN);
+    const int cap = prod ? lq::kOrbProdDims : quad ? lq::kOrbQuadDims : lq::kOrbLinDims;
     if ((f->d + m - 1) / m * m > cap) return nullptr;
-    if (!f->beta || (quad && !f->gamma)) return nullptr;
+    if (!f->beta || ((quad || prod) && !f->gamma)) return nullptr;
+    if (prod)
+        for (int j = 0; j < f->d; ++j)
+            if (std::isnan(f->gamma[j])) return nullptr;   // every coordinate must carry a factor
     if (z[0] != 1 % n) return nullptr;
     const uint64_t a = z[1];
     for (int j = 2; j < f->d; ++j)
         if (z[j] != z[j - 1] * a % n) return nullptr;   // z_j = a^(j-1) mod n
-    return orbit_plan((uint32_t)n, (uint32_t)a, m);
+    return orbit_plan((uint32_t)n, (uint32_t)a, m, !prod);
 }
 
 // Device copies of the start tables, cached per context and plan.
@@ -734,6 +766,23 @@ int orbit_lin(lq_ctx* c, const lq::OrbHead& head, const std::vector<double>& cv,
     return LQ_OK;
 }
 
+template <int N>
+int orbit_prod(lq_ctx* c, const lq::OrbHead& head, const std::vector<double2>& wc, int nf, int off, int rmask,
+               uint64_t unit0, int64_t ntiles, double* tiles_dev) {
+    using Args = lq::OrbProdArgs<N>;
+    static thread_local Args args;
+    args.h = head;
+    args.nf = nf;
+    args.off = off;
+    args.rmask = rmask;
+    std::memcpy(args.wc, wc.data(), sizeof(double2) * wc.size());
+    t_begin(c);
+    lq::k_orbit_prod<Args><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, unit0, 0u, tiles_dev);
+    t_end(c);
+    CK(cudaGetLastError());
+    return LQ_OK;
+}
+
 int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t unit0, int64_t ntiles,
                  double* tiles_dev) {
     int rc;
@@ -747,6 +796,16 @@ int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t un
     h.n = p.n; h.a = p.a; h.as = p.as; h.dpad = dpad; h.units = p.units; h.qc = p.qc; h.h = p.h;
     h.G = G; h.Alo = Alo; h.Ahi = Ahi;
     h.alpha = f->alpha; h.K = f->K; h.A = f->A; h.B = f->B; h.C0 = f->C0; h.kappa = f->kappa; h.pw = f->power;
+    if (f->kind == LQ_FAM_PROD_QUAD) {
+        ProdScale ps;
+        if ((rc = prod_scale(f, p.n, ps))) return rc;
+        h.M = ps.m;
+        std::vector<double2> wc(dpad);
+        for (int j = 0; j < dpad; ++j) wc[j] = j < d ? make_double2(ps.w[j], ps.c[j]) : make_double2(0.0, 1.0);
+        if (dpad <= 128) return orbit_prod<128>(c, h, wc, d, (int)ps.off, ps.R - 1, unit0, ntiles, tiles_dev);
+        if (dpad <= 512) return orbit_prod<512>(c, h, wc, d, (int)ps.off, ps.R - 1, unit0, ntiles, tiles_dev);
+        return orbit_prod<lq::kOrbProdDims>(c, h, wc, d, (int)ps.off, ps.R - 1, unit0, ntiles, tiles_dev);
+    }
     if (is_quad_kind(f->kind)) {
         const int outer = quad_outer_of(f->kind);
         int sigma = 1074 + std::ilogb(1.0 / nd) - 1000;

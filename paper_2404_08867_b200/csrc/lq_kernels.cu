@@ -515,14 +515,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_orbit(const __grid_constant__ A
             W[0] = i0;
             #pragma unroll
             for (int k = 0; k < M; ++k) {
-#ifdef LQ_ORB_VZ
-                asm volatile("mov.b32 %0, 0;" : "=r"(Z[k]));   // opaque zeros (hi words of the denormals)
-#else
                 Z[k] = (threadIdx.x + k) & hmask;   // opaque zeros (hi words of the denormals)
-#endif
                 acc[k] = 0.0;
                 if (k) W[k] = mulmod_shoup(W[k - 1], za, zs, n);
             }
+            // (a window of denormal doubles, as in k_orbit_prod, measured 70.4 vs
+            // 67.9 ms on cfg5: ptxas then loses the residue-major schedule)
             #pragma unroll 1
             for (int j0 = 0; j0 < H.dpad; j0 += M) {
                 #pragma unroll
@@ -573,6 +571,87 @@ __global__ void __launch_bounds__(kThreads, 2) k_orbit(const __grid_constant__ A
             #pragma unroll
             for (int k = 0; k < M; ++k) s += k < valid ? quad_pair<OUTER>(ao[k], ae[k], H.alphaB, prm, true) : 0.0;
             if (u == 0) s += quad_outer<OUTER>(0.0, prm);   // point 0
+        }
+    }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
+}
+
+// Product family over Korobov orbits (no mirror pairs: a factor's mirror has
+// the other shift 1 - w_j): the plan enumerates every nonzero point once,
+// chains of kOrbProdM points share the residue window as in k_orbit, and each
+// point keeps its running product and exponent as in k_prod.
+constexpr int kOrbProdM = 16;
+constexpr int kOrbProdDims = (kOrbParamBytes - (int)sizeof(OrbHead) - 16) / 16 / kOrbProdM * kOrbProdM;
+
+template <int N>
+struct OrbProdArgs {
+    OrbHead h;                  // uses n, a, as, dpad, units, qc, h, G, Alo, Ahi, K, pw, M (= 2^(1074-g)/n)
+    int32_t nf, off, rmask;     // factors (= d), as ProdArgs
+    double2 wc[N];              // (w_j 2^-g, c_j 2^-2g); entries past nf are skipped
+};
+
+template <class Args>
+__global__ void __launch_bounds__(kThreads, 2) k_orbit_prod(const __grid_constant__ Args a, uint64_t unit0,
+                                                             uint32_t hmask, double* __restrict__ tile_out) {
+    constexpr int M = kOrbProdM;
+    __shared__ double sh[8];
+    const OrbHead& H = a.h;
+    const uint32_t n = H.n;
+    const uint64_t u = unit0 + (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+    double s = 0.0;
+    if (u < H.units) {
+        const uint32_t cs = (uint32_t)(u / H.qc), q = (uint32_t)(u - (uint64_t)cs * H.qc);
+        const uint32_t i0 = mulmod32(mulmod32(H.G[cs], H.Alo[q & 4095u], n), H.Ahi[q >> 12], n);
+        const int valid = (int)min((uint32_t)M, H.h - q * (uint32_t)M);
+        const uint32_t za = H.a, zs = H.as;
+        // the residue window is kept as denormal doubles X = {r, 0}: a new
+        // residue is written straight into the low word of its slot, so the
+        // DFMAs read the pair without per-use moves
+        const uint32_t zero = threadIdx.x & hmask;
+        double X[M], D[M];
+        int E[M];
+        uint32_t r = i0;
+        #pragma unroll
+        for (int k = 0; k < M; ++k) {
+            X[k] = denorm_of(r, zero);
+            D[k] = 1.0;
+            E[k] = 0;
+            if (k + 1 < M) r = mulmod_shoup(r, za, zs, n);
+        }
+        double m;
+        asm("mov.b64 %0, %1;" : "=d"(m) : "d"(H.M));   // one vector register: a single uniform operand per op
+        #pragma unroll 1
+        for (int j0 = 0; j0 < H.dpad; j0 += M) {
+            #pragma unroll
+            for (int v = 0; v < M; ++v) {
+                const double2 wc = a.wc[j0 + v];
+                if (j0 + v < a.nf) {   // uniform: the padded tail of the last block is skipped
+                    #pragma unroll
+                    for (int k = 0; k < M; ++k) {
+                        const double t = fma(X[(v + k) % M], m, -wc.x);
+                        D[k] *= fma(t, t, wc.y);
+                    }
+                }
+                r = mulmod_shoup(r, za, zs, n);
+                X[v] = denorm_of(r, zero);
+                if (((j0 + v) & a.rmask) == a.rmask) {
+                    #pragma unroll
+                    for (int k = 0; k < M; ++k) renorm(D[k], E[k]);
+                }
+            }
+        }
+        #pragma unroll
+        for (int k = 0; k < M; ++k) s += k < valid ? prod_outer(D[k], E[k], H.K, H.pw, a.off) : 0.0;
+        if (u == 0) {   // point 0 (x = 0): the same factors at t = -w_j
+            double D0 = 1.0;
+            int E0 = 0;
+            for (int j = 0; j < a.nf; ++j) {
+                const double2 wc = a.wc[j];
+                D0 *= fma(wc.x, wc.x, wc.y);
+                if ((j & a.rmask) == a.rmask) renorm(D0, E0);
+            }
+            s += prod_outer(D0, E0, H.K, H.pw, a.off);
         }
     }
     s = block_sum(s, sh);
