@@ -22,6 +22,7 @@ has no symbolic DAG).
 
 from __future__ import annotations
 
+import functools
 import math
 import time
 from dataclasses import dataclass
@@ -252,6 +253,11 @@ def _det_a(rule):
         return 0.0
 
 
+@functools.lru_cache(maxsize=64)
+def _log_total(counts):
+    return float(sum(math.log(c) for c in counts))
+
+
 def mdi_lr(f, d, a, n, cfg=None, rule=None, with_report=False):
     """Improved-rule quadrature via dimension iteration (mdi.py:215-234)."""
     cfg = cfg if cfg is not None else MdiConfig()
@@ -262,7 +268,7 @@ def mdi_lr(f, d, a, n, cfg=None, rule=None, with_report=False):
     grids = midpoint_grids(rule)
     report = mdi_sum(f, grids, cfg)
     report.det_a = _det_a(rule)
-    report.log_total = float(sum(math.log(c) for c in grids.counts))
+    report.log_total = _log_total(grids.counts)
     value = _normalize(report.value, grids.counts)
     if with_report:
         return value, report
