@@ -296,8 +296,14 @@ def main():
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
+    # H2D per call: the kernel-parameter struct (coefficient table + header);
+    # the orbit start tables are uploaded once per context and plan
+    if lay.mode == N.LAYOUT_ORBIT:
+        h2d = 8 * (-(-d // ORB_M) * ORB_M) + 152 + 24          # OrbLinArgs<1008> + launch arguments
+    else:
+        h2d = 24 * d + 112 + 16                                # FamArgs<LinDim, 1000> + launch arguments
     e2e = {"value": args.steps * n / e2e_s, "unit": "f-evals/s",
-           "h2d_bytes_per_step": d * 24, "d2h_bytes_per_step": 8,
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8,
            "api": ("paper_2404_08867_b200.slr_integrate(f, rule)" if world == 1
                    else "paper_2404_08867_b200.distributed.slr_integrate(f, rule)"),
            "estimate": r.value}
