@@ -321,3 +321,42 @@ def test_product_family_config4_integrand(env, monkeypatch):
         got = engine.lattice_sum(fam, rule.n, z)
         want = engine.lattice_sum(prog, rule.n, z)
         assert got > 0.0 and math.isclose(got, want, rel_tol=1e-11), (n, got, want)
+
+
+def test_randomised_layouts_agree(env, monkeypatch):
+    # random primes, Korobov parameters, dimensions and families: the orbit,
+    # mirror-paired and plain index layouts give the same sums
+    lq, N, engine = env
+    rng = np.random.default_rng(2024)
+
+    def is_prime(m):
+        if m < 2:
+            return False
+        p = 2
+        while p * p <= m:
+            if m % p == 0:
+                return False
+            p += 1
+        return True
+
+    fams = ["exp", "sincos", "expabs", "gauss", "pow", "qtrig"]
+    for trial in range(24):
+        n = int(rng.integers(20000, 2000000))
+        while not is_prime(n):
+            n += 1
+        a = int(rng.integers(2, n - 1))
+        d = int(rng.integers(2, 160))
+        fam = fams[trial % len(fams)]
+        f = lq.parse(_family_text(fam, d, rng), d)
+        rule = lq.korobov_vector(a, n, d)
+        pi = engine.plain_integrand(f, d)
+        z = rule.z_reduced_array()
+        vals = {}
+        for orb, pair in (("1", "1"), ("0", "1"), ("0", "0")):
+            monkeypatch.setenv("LQ_ORBIT", orb)
+            monkeypatch.setenv("LQ_PAIR", pair)
+            mode = N.lattice_layout(pi.struct, n, z).mode
+            vals[mode] = engine.lattice_sum(pi, n, z)
+        base = vals[N.LAYOUT_INDEX]
+        for mode, v in vals.items():
+            assert math.isclose(v, base, rel_tol=1e-11, abs_tol=1e-9 * n), (trial, fam, n, a, d, mode, v, base)
