@@ -1004,10 +1004,12 @@ int lq_points_block(lq_ctx* c, int32_t d, uint64_t n, const uint64_t* z, int64_t
         }
         void* dzz;
         if ((rc = upload(c, B_TAB, zz.data(), zz.size() * 4, &dzz))) return rc;
-        dim3 g((unsigned)((m + lq::kPtRows - 1) / lq::kPtRows), (unsigned)((d + lq::kPtCols - 1) / lq::kPtCols));
-        if ((m + lq::kPtRows - 1) / lq::kPtRows > 0x7fffffffull) return fail(LQ_ERR_VALUE, "point block too large");
+        const uint64_t row_tiles = (m + lq::kPtRows - 1) / lq::kPtRows;
+        const uint32_t col_tiles = (uint32_t)((d + lq::kPtCols - 1) / lq::kPtCols);
+        if (row_tiles * col_tiles > 0x7fffffffull) return fail(LQ_ERR_VALUE, "point block too large");
         t_begin(c);
-        lq::k_points_tiled<<<g, lq::kThreads, 0, c->stream>>>((const uint2*)dzz, (uint32_t)d, (uint32_t)n, n_d, inv, (uint64_t)start, m, dst);
+        lq::k_points_tiled<<<(unsigned)(row_tiles * col_tiles), lq::kThreads, 0, c->stream>>>(
+            (const uint2*)dzz, (uint32_t)d, (uint32_t)n, n_d, inv, (uint64_t)start, m, col_tiles, dst);
         t_end(c);
     } else {
         int64_t blocks = (int64_t)((n_elem + lq::kThreads - 1) / lq::kThreads);

