@@ -38,7 +38,7 @@ int fail(int code, const char* fmt, ...) {
                         __FILE__, __LINE__);                                          \
     } while (0)
 
-enum Buf { B_TAB = 0, B_TILES, B_RED0, B_RED1, B_OUT, B_PROG, B_AUX0, B_AUX1, B_AUX2, B_AUX3, B_PART, B_FAC, B_NODES, B_ORB, B_NBUF };
+enum Buf { B_TAB = 0, B_TILES, B_RED0, B_RED1, B_OUT, B_PROG, B_AUX0, B_AUX1, B_AUX2, B_AUX3, B_PART, B_FAC, B_NODES, B_ORB, B_FFTW, B_FFTH, B_NBUF };
 
 }  // namespace
 
@@ -70,6 +70,7 @@ struct lq_ctx {
     float last_ms = 0.f;
     int64_t launches = 0;
     uint64_t orb_id = 0;       // orbit plan whose start tables are in dbuf[B_ORB]
+    bool fft_w = false;        // twiddles computed in dbuf[B_FFTW]
 };
 
 namespace {
@@ -602,6 +603,7 @@ struct OrbPlan {
     int m = 0;
     bool mirror = true;
     std::vector<uint32_t> G, Alo, Ahi;
+    std::vector<uint32_t> apow;   // FFT plans: (a^t mod n, Shoup constant) pairs, t < kFftN
 };
 
 constexpr uint32_t kOrbMaxCosets = 4096;
@@ -658,14 +660,25 @@ std::shared_ptr<const OrbPlan> build_orbit_plan(uint32_t n, uint32_t a, int m, b
     return p;
 }
 
-std::shared_ptr<const OrbPlan> orbit_plan(uint32_t n, uint32_t a, int m, bool mirror) {
+std::shared_ptr<const OrbPlan> orbit_plan(uint32_t n, uint32_t a, int m, bool mirror, bool fft = false) {
     static std::mutex mu;
-    static std::map<std::tuple<uint32_t, uint32_t, int, bool>, std::shared_ptr<const OrbPlan>> cache;
+    static std::map<std::tuple<uint32_t, uint32_t, int, bool, bool>, std::shared_ptr<const OrbPlan>> cache;
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(n, a, m, mirror);
+    auto key = std::make_tuple(n, a, m, mirror, fft);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     auto p = build_orbit_plan(n, a, m, mirror);
+    if (p && fft) {
+        auto q = std::make_shared<OrbPlan>(*p);
+        q->apow.resize(2 * lq::kFftN);
+        uint64_t t = 1 % n;
+        for (int k = 0; k < lq::kFftN; ++k) {
+            q->apow[2 * k] = (uint32_t)t;
+            q->apow[2 * k + 1] = (uint32_t)((t << 32) / n);
+            t = t * a % n;
+        }
+        p = q;
+    }
     if (cache.size() > 64) cache.clear();
     cache[key] = p;
     return p;
@@ -682,7 +695,22 @@ int orbit_mode() {
     return 1;
 }
 
-std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, const uint64_t* z) {
+// The FFT form (k_orbit_fft) for the linear families when d is large enough
+// for O(log N) per point to beat O(d) and the lattice is large enough to fill
+// the GPU with 4096-point tiles: LQ_FFT=0 disables, =always forces.
+// (cfg2, n = 10^4, d = 100: FFT 0.029 ms vs direct orbit 0.022 ms.)
+constexpr int kFftMinD = 96;
+constexpr uint64_t kFftMinN = 1ull << 20;
+bool fft_wanted(const lq_integrand* f, uint64_t n) {
+    const char* e = std::getenv("LQ_FFT");
+    if (e && !std::strcmp(e, "0")) return false;
+    if (!is_lin_kind(f->kind) || f->d > lq::kFftN / 2) return false;
+    if (e && !std::strcmp(e, "always")) return f->d >= 2;
+    return f->d >= kFftMinD && n >= kFftMinN;
+}
+
+std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, const uint64_t* z, bool* fft = nullptr) {
+    if (fft) *fft = false;
     const int mode = orbit_mode();
     if (mode == 0 || !z || f->kind == LQ_FAM_PROGRAM || f->d < 2) return nullptr;
     if (n > (1ull << 31) || n < 5) return nullptr;
@@ -699,19 +727,30 @@ std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, cons
     const uint64_t a = z[1];
     for (int j = 2; j < f->d; ++j)
         if (z[j] != z[j - 1] * a % n) return nullptr;   // z_j = a^(j-1) mod n
+    if (fft && fft_wanted(f, n)) {
+        auto p = orbit_plan((uint32_t)n, (uint32_t)a, lq::kFftN - f->d + 1, true, true);
+        if (p) {
+            *fft = true;
+            return p;
+        }
+    }
     return orbit_plan((uint32_t)n, (uint32_t)a, m, !prod);
 }
 
 // Device copies of the start tables, cached per context and plan.
-int orbit_tables(lq_ctx* c, const OrbPlan& p, const uint32_t** G, const uint32_t** Alo, const uint32_t** Ahi) {
-    const size_t nG = p.G.size(), nlo = p.Alo.size(), nhi = p.Ahi.size();
-    const size_t bytes = 4 * (nG + nlo + nhi);
+int orbit_tables(lq_ctx* c, const OrbPlan& p, const uint32_t** G, const uint32_t** Alo, const uint32_t** Ahi,
+                 const uint2** apow = nullptr) {
+    const size_t nG = p.G.size(), nlo = p.Alo.size(), nhi = p.Ahi.size(), np = p.apow.size();
+    const size_t pad = (nG + nlo + nhi) & 1;   // keep apow 8-byte aligned
+    const size_t bytes = 4 * (nG + nlo + nhi + pad + np);
     if (c->orb_id != p.id) {
         std::vector<uint32_t> all;
-        all.reserve(nG + nlo + nhi);
+        all.reserve(nG + nlo + nhi + pad + np);
         all.insert(all.end(), p.G.begin(), p.G.end());
         all.insert(all.end(), p.Alo.begin(), p.Alo.end());
         all.insert(all.end(), p.Ahi.begin(), p.Ahi.end());
+        if (pad) all.push_back(0);
+        all.insert(all.end(), p.apow.begin(), p.apow.end());
         void* d;
         int rc;
         if ((rc = upload(c, B_ORB, all.data(), bytes, &d))) return rc;
@@ -721,6 +760,7 @@ int orbit_tables(lq_ctx* c, const OrbPlan& p, const uint32_t** G, const uint32_t
     *G = base;
     *Alo = base + nG;
     *Ahi = base + nG + nlo;
+    if (apow) *apow = (const uint2*)(base + nG + nlo + nhi + pad);
     return LQ_OK;
 }
 
@@ -778,6 +818,59 @@ int orbit_prod(lq_ctx* c, const lq::OrbHead& head, const std::vector<double2>& w
     std::memcpy(args.wc, wc.data(), sizeof(double2) * wc.size());
     t_begin(c);
     lq::k_orbit_prod<Args><<<(unsigned)ntiles, lq::kThreads, 0, c->stream>>>(args, unit0, 0u, tiles_dev);
+    t_end(c);
+    CK(cudaGetLastError());
+    return LQ_OK;
+}
+
+int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t unit0, int64_t ntiles,
+                     double* tiles_dev) {
+    int rc;
+    const uint32_t *G, *Alo, *Ahi;
+    const uint2* apow;
+    if ((rc = orbit_tables(c, p, &G, &Alo, &Ahi, &apow))) return rc;
+    const int d = f->d;
+    const size_t smem = sizeof(double2) * lq::kFftPad;
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute((const void*)lq::k_fft_coeffs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft<lq::OUT_EXP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft<lq::OUT_SINCOS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft<lq::OUT_EXPABS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft<lq::OUT_POW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    void *W, *Hc, *dc;
+    if ((rc = dev_buf(c, B_FFTW, sizeof(double2) * lq::kFftN, &W))) return rc;
+    if (!c->fft_w) {
+        lq::k_fft_twiddles<<<lq::kFftN / lq::kThreads, lq::kThreads, 0, c->stream>>>((double2*)W);
+        CK(cudaGetLastError());
+        c->fft_w = true;
+    }
+    const double nd = (double)p.n;
+    std::vector<double> cv(d);
+    double bsum = 0.0;
+    for (int j = 0; j < d; ++j) {
+        cv[j] = f->beta[j] / nd;
+        bsum += f->beta[j];
+    }
+    if ((rc = upload(c, B_AUX0, cv.data(), sizeof(double) * d, &dc))) return rc;
+    if ((rc = dev_buf(c, B_FFTH, sizeof(double2) * lq::kFftN, &Hc))) return rc;
+    lq::k_fft_coeffs<<<1, lq::kThreads, smem, c->stream>>>((const double*)dc, d, (const double2*)W, (double2*)Hc);
+    CK(cudaGetLastError());
+    lq::FftHead h;
+    h.n = p.n; h.B = (uint32_t)p.m; h.units = p.units; h.qc = p.qc; h.h = p.h;
+    h.G = G; h.Alo = Alo; h.Ahi = Ahi; h.apow = apow; h.W = (const double2*)W; h.Hc = (const double2*)Hc;
+    h.alpha = f->alpha; h.alphaB = f->alpha + bsum; h.K = f->K; h.A = f->A; h.Bc = f->B; h.C0 = f->C0;
+    h.kappa = f->kappa; h.pw = f->power;
+    const dim3 g((unsigned)ntiles), b(lq::kThreads);
+    t_begin(c);
+    switch (lin_outer(f->kind)) {
+        case lq::OUT_EXP: lq::k_orbit_fft<lq::OUT_EXP><<<g, b, smem, c->stream>>>(h, unit0, tiles_dev); break;
+        case lq::OUT_SINCOS: lq::k_orbit_fft<lq::OUT_SINCOS><<<g, b, smem, c->stream>>>(h, unit0, tiles_dev); break;
+        case lq::OUT_EXPABS: lq::k_orbit_fft<lq::OUT_EXPABS><<<g, b, smem, c->stream>>>(h, unit0, tiles_dev); break;
+        default: lq::k_orbit_fft<lq::OUT_POW><<<g, b, smem, c->stream>>>(h, unit0, tiles_dev); break;
+    }
     t_end(c);
     CK(cudaGetLastError());
     return LQ_OK;
@@ -863,15 +956,17 @@ int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t un
 struct Layout {
     uint64_t tile_units = 0, n_units = 0;
     std::shared_ptr<const OrbPlan> orb;
-    bool pair = false;
-    int mode() const { return orb ? LQ_LAYOUT_ORBIT : pair ? LQ_LAYOUT_PAIRED : LQ_LAYOUT_INDEX; }
+    bool pair = false, fft = false;
+    int mode() const {
+        return orb ? (fft ? LQ_LAYOUT_ORBIT_FFT : LQ_LAYOUT_ORBIT) : pair ? LQ_LAYOUT_PAIRED : LQ_LAYOUT_INDEX;
+    }
 };
 
 Layout layout_of(const lq_integrand* f, uint64_t n, const uint64_t* z) {
     Layout L;
-    L.orb = orbit_for(f, n, z);
+    L.orb = orbit_for(f, n, z, &L.fft);
     if (L.orb) {
-        L.tile_units = lq::kThreads;
+        L.tile_units = L.fft ? 2 : lq::kThreads;   // FFT form: two chains per CTA
         L.n_units = L.orb->units;
     } else if (uses_family_kernel(f, n) && pair_ok(f, n, z)) {
         L.pair = true;
@@ -1057,7 +1152,8 @@ int lq_lattice_partials(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint
     void* tiles;
     if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
     if (L.orb) {
-        if ((rc = launch_orbit(c, f, *L.orb, base, ntiles, (double*)tiles))) return rc;
+        if ((rc = L.fft ? launch_orbit_fft(c, f, *L.orb, base, ntiles, (double*)tiles)
+                        : launch_orbit(c, f, *L.orb, base, ntiles, (double*)tiles))) return rc;
     } else {
         if ((rc = launch_tiles(c, f, n, z, base, end, ntiles, (double*)tiles, L.pair))) return rc;
     }
@@ -1093,7 +1189,8 @@ int lq_lattice_sum(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t*
             const int64_t ntiles = (int64_t)((L.n_units + L.tile_units - 1) / L.tile_units);
             void* tiles;
             if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
-            if (L.orb) rc = launch_orbit(c, f, *L.orb, 0, ntiles, (double*)tiles);
+            if (L.orb) rc = L.fft ? launch_orbit_fft(c, f, *L.orb, 0, ntiles, (double*)tiles)
+                                  : launch_orbit(c, f, *L.orb, 0, ntiles, (double*)tiles);
             else rc = launch_tiles(c, f, n, z, 0, L.n_units, ntiles, (double*)tiles, true);
             if (rc) return rc;
             double* r;

@@ -3,6 +3,7 @@
 #include <cooperative_groups.h>
 
 #include "lq_device.cuh"
+#include "lq_fft.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -674,6 +675,101 @@ __global__ void __launch_bounds__(kThreads, 2) k_orbit_prod(const __grid_constan
             s += prod_outer(D0, E0, H.K, H.pw, a.off);
         }
     }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
+}
+
+// ---------------------------------------------------- Korobov orbits, FFT form
+// The chain sums L_k = sum_j c_j P[k + j] (k < B) are a correlation of the
+// coefficients with the residue sequence P[t] = i0 a^t mod n, t < N = B + d - 1:
+// one forward FFT of P, a product with conj(FFT(c)), one inverse FFT give all
+// B linear forms of a chain (overlap-save), O(log N) FP64 work per point
+// instead of O(d).  Two chains ride in one complex FFT
+// (real and imaginary parts); c is real, so their correlations separate.
+struct FftHead {
+    uint32_t n, B;                     // modulus, chain length N - d + 1
+    uint64_t units;                    // chains
+    uint32_t qc, h;                    // chains per coset, exponents per coset
+    const uint32_t* G;                 // coset representatives
+    const uint32_t* Alo;               // a^(B q), q < 4096
+    const uint32_t* Ahi;               // a^(B 4096 q)
+    const uint2* apow;                 // (a^t mod n, floor(a^t 2^32 / n)), t < N
+    const double2* W;                  // e^{-2 pi i k / N}
+    const double2* Hc;                 // conj(FFT(c zero-padded)) / N, c_j = beta_j / n
+    double alpha, alphaB, K, A, Bc, C0, kappa, pw;
+};
+
+__global__ void __launch_bounds__(kThreads) k_fft_twiddles(double2* __restrict__ W) {
+    for (int k = blockIdx.x * kThreads + threadIdx.x; k < kFftN; k += gridDim.x * kThreads) {
+        double sn, cs;
+        sincospi(-2.0 * (double)k / (double)kFftN, &sn, &cs);
+        W[k] = make_double2(cs, sn);
+    }
+}
+
+// Hc = conj(FFT(c_pad)) / N, one CTA.
+__global__ void __launch_bounds__(kThreads) k_fft_coeffs(const double* __restrict__ c, int d,
+                                                          const double2* __restrict__ W, double2* __restrict__ Hc) {
+    extern __shared__ double2 buf[];
+    for (int t = threadIdx.x; t < kFftN; t += kThreads) buf[fpad(t)] = make_double2(t < d ? c[t] : 0.0, 0.0);
+    __syncthreads();
+    fft4096(buf, W);
+    const double inv = 1.0 / (double)kFftN;
+    for (int t = threadIdx.x; t < kFftN; t += kThreads) {
+        const double2 v = buf[fpad(t)];
+        Hc[t] = make_double2(v.x * inv, -v.y * inv);
+    }
+}
+
+__device__ __forceinline__ uint32_t fft_chain_start(const FftHead& a, uint64_t u, int& valid) {
+    const uint32_t n = a.n;
+    const uint32_t cs = (uint32_t)(u / a.qc), q = (uint32_t)(u - (uint64_t)cs * a.qc);
+    valid = (int)min(a.B, a.h - q * a.B);
+    return mulmod32(mulmod32(a.G[cs], a.Alo[q & 4095u], n), a.Ahi[q >> 12], n);
+}
+
+// One CTA = two chains (units 2b, 2b + 1 after unit0); tile_out[b] = their sum.
+template <int OUTER>
+__global__ void __launch_bounds__(kThreads, 2) k_orbit_fft(const __grid_constant__ FftHead a, uint64_t unit0,
+                                                         double* __restrict__ tile_out) {
+    extern __shared__ double2 buf[];   // kFftPad
+    __shared__ double sh[8];
+    const uint32_t n = a.n;
+    const uint64_t u0 = unit0 + 2ull * blockIdx.x, u1 = u0 + 1;
+    int v0 = 0, v1 = 0;
+    const uint32_t s0 = u0 < a.units ? fft_chain_start(a, u0, v0) : 0u;
+    const uint32_t s1 = u1 < a.units ? fft_chain_start(a, u1, v1) : 0u;
+    // residues of both chains straight into the registers of the first pass:
+    // thread j holds positions j + 256 r
+    double2 v[16];
+    #pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const int t = threadIdx.x + r * kThreads;
+        const uint2 ap = __ldg(a.apow + t);
+        v[r] = make_double2((double)mulmod_shoup(s0, ap.x, ap.y, n), (double)mulmod_shoup(s1, ap.x, ap.y, n));
+    }
+    fft4096_regs(v, buf, a.W);
+    // Y = X conj(C) / N, conjugated so that the forward transform inverts it;
+    // the last forward pass left positions j + 256 r in this thread, which are
+    // exactly the inputs of the first inverse pass
+    #pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const double2 y = cmul(v[r], __ldg(a.Hc + threadIdx.x + r * kThreads));
+        v[r] = make_double2(y.x, -y.y);
+    }
+    // inverse transform; its last pass writes the correlations to shared memory
+    // so the out-of-line outer function runs with no transform state live
+    fft_pass<false, true>(v, buf, 1, a.W);
+    fft_pass<true, true>(v, buf, 16, a.W);
+    fft_pass<true, true>(v, buf, 256, a.W);
+    const LinParams prm{a.alpha, 1.0, a.K, a.A, a.Bc, a.C0, a.kappa, a.pw};
+    double s = 0.0;
+    for (int k = threadIdx.x; k < v0 || k < v1; k += kThreads) {
+        const double2 y = buf[fpad(k)];             // conj of the correlation: (L0, -L1)
+        if (k < v0) s += outer_pair<OUTER>(y.x, prm, a.alphaB, true);
+        if (k < v1) s += outer_pair<OUTER>(-y.y, prm, a.alphaB, true);
+    }
+    if (u0 == 0 && threadIdx.x == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
     s = block_sum(s, sh);
     if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
 }

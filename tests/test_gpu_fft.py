@@ -1,0 +1,70 @@
+"""FFT form of the Korobov chain sums (k_orbit_fft) against
+the direct orbit kernel and the oracle.  The correlation through an FFT is
+exact up to rounding (~1e-14 relative on the linear forms), so sums agree with
+the direct kernels to 1e-12 and with the oracle to the north-star 1e-10."""
+
+import math
+import zlib
+
+import numpy as np
+import pytest
+
+from test_gpu_orbit import _family_text, _order
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def env():
+    import paper_2404_08867_b200 as lq
+    from paper_2404_08867_b200 import _native as N, engine
+    N.lib()
+    return lq, N, engine
+
+
+def _sums(engine, N, pi, n, z, monkeypatch):
+    out = {}
+    for fft in ("always", "0"):
+        monkeypatch.setenv("LQ_FFT", fft)
+        out[N.lattice_layout(pi.struct, n, z).mode] = engine.lattice_sum(pi, n, z)
+    return out
+
+
+@pytest.mark.parametrize("family", ["exp", "sincos", "expabs", "pow"])
+@pytest.mark.parametrize("n,d,kind", [(100003, 37, "primitive"), (100003, 200, "odd_order"),
+                                      (1000003, 600, "even_order_cosets"), (1000003, 2048, "primitive")])
+def test_fft_matches_direct_orbit_and_oracle(env, family, n, d, kind, monkeypatch):
+    lq, N, engine = env
+    from oracle import np_oracle
+    fac = {100003: (2, 3, 7, 2381), 1000003: (2, 3, 166667)}[n]
+    g = 2
+    while any(pow(g, (n - 1) // p, n) == 1 for p in fac):
+        g += 1
+    a = {"primitive": g, "odd_order": pow(g, 2, n), "even_order_cosets": pow(g, 3, n)}[kind]
+    rng = np.random.default_rng(zlib.crc32(f"{family}/{n}/{d}".encode()))
+    f = lq.parse(_family_text(family, d, rng), d)
+    rule = lq.korobov_vector(a, n, d)
+    pi = engine.plain_integrand(f, d)
+    z = rule.z_reduced_array()
+    got = _sums(engine, N, pi, n, z, monkeypatch)
+    assert set(got) == {N.LAYOUT_ORBIT_FFT, N.LAYOUT_ORBIT}, got.keys()
+    fft, direct = got[N.LAYOUT_ORBIT_FFT], got[N.LAYOUT_ORBIT]
+    assert math.isclose(fft, direct, rel_tol=1e-12, abs_tol=1e-12 * n), (family, n, d, fft, direct)
+    if n * d <= 3_000_000:
+        ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
+        assert math.isclose(fft, ref, rel_tol=REL, abs_tol=1e-10 * n), (family, n, d, fft, ref)
+
+
+def test_fft_cfg5(env, monkeypatch):
+    # the headline lattice through the FFT form vs the direct orbit kernel
+    lq, N, engine = env
+    from paper_2404_08867_b200.configs import make_config
+    cfg = make_config(5)
+    f = lq.parse(cfg.text, cfg.d)
+    rule = lq.korobov_vector(cfg.plain_a, cfg.plain_n, cfg.d)
+    pi = engine.plain_integrand(f, cfg.d)
+    got = _sums(engine, N, pi, rule.n, rule.z_reduced_array(), monkeypatch)
+    fft, direct = got[N.LAYOUT_ORBIT_FFT], got[N.LAYOUT_ORBIT]
+    assert math.isclose(fft, direct, rel_tol=1e-12), (fft, direct)

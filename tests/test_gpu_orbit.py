@@ -60,6 +60,7 @@ def test_orbit_configs_vs_oracle(env, cid, monkeypatch):
     f = lq.parse(cfg.text, cfg.d)
     rule = lq.korobov_vector(cfg.plain_a, cfg.plain_n, cfg.d)
     monkeypatch.setenv("LQ_ORBIT", "always")
+    monkeypatch.setenv("LQ_FFT", "0")          # the direct orbit kernel (the FFT form: test_gpu_fft.py)
     assert _layout(N, engine, f, rule).mode == N.LAYOUT_ORBIT
     orb = _sum(lq, engine, f, rule, "always", monkeypatch)
     idx = _sum(lq, engine, f, rule, "0", monkeypatch)
@@ -126,6 +127,7 @@ def test_orbit_cfg5_matches_index_kernel(env, monkeypatch):
     f = lq.parse(cfg.text, cfg.d)
     rule = lq.korobov_vector(cfg.plain_a, cfg.plain_n, cfg.d)
     monkeypatch.delenv("LQ_ORBIT", raising=False)
+    monkeypatch.setenv("LQ_FFT", "0")          # the direct orbit kernel (the FFT form: test_gpu_fft.py)
     assert _layout(N, engine, f, rule).mode == N.LAYOUT_ORBIT
     orb = _sum(lq, engine, f, rule, "1", monkeypatch)
     idx = _sum(lq, engine, f, rule, "0", monkeypatch)
