@@ -35,6 +35,7 @@ FLOPS_PER_PD = 3          # 1 (coordinate r/n) + 2 (c_j * x_j 
 FLOPS_PER_POINT = 2       # transcendental + accumulate
 TERM_FLOPS = 2            # SURVEY.md §8(d) per-coordinate term of exp-abs-linear (c_j * x_j accumulate)
 ORB_M = 24                # points per chain of the orbit kernel (LQ_ORB_LIN_M, csrc/lq_kernels.cu)
+FFT_N = 4096              # transform length of the FFT-form orbit kernel (kFftN, csrc/lq_fft.cuh)
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
            0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
@@ -259,7 +260,18 @@ def main():
     su = lay.tile_units * N.LQ_SUPER_TILES
     my_units = min(s_hi * su, lay.n_units) - s_lo * su
     avg_kern = kern_ms / args.steps
-    if lay.mode == N.LAYOUT_ORBIT:
+    if lay.mode == N.LAYOUT_ORBIT_FFT:
+        B = FFT_N - d + 1                              # points per chain (overlap-save block)
+        forms = my_units * B                           # linear forms (one per mirrored pair)
+        fft_flops = 2 * 5 * FFT_N * int(math.log2(FFT_N)) + 6 * FFT_N   # fwd + inv complex FFT + spectrum product
+        alg_flops = (my_units / 2) * fft_flops + forms * 2 * FLOPS_PER_POINT
+        conv_flops = forms * (FLOPS_PER_PD * d + 2 * FLOPS_PER_POINT)
+        exec_flops = alg_flops
+        kernel_name = "k_orbit_fft<OUT_EXPABS> (liblq.so)"
+        unit_txt = (f"unit = chain of {B} mirrored point pairs, two chains per {FFT_N}-point complex FFT tile; "
+                    f"per tile 2 x 5 N log2 N (forward + inverse FFT) + 6 N (spectrum product) flop, "
+                    f"+ 2 x {FLOPS_PER_POINT} per pair (two outer evaluations)")
+    elif lay.mode == N.LAYOUT_ORBIT:
         forms = my_units * ORB_M                       # linear forms evaluated (one per mirrored pair)
         alg_flops = forms * (TERM_FLOPS * d + 2 * FLOPS_PER_POINT)
         conv_flops = forms * (FLOPS_PER_PD * d + 2 * FLOPS_PER_POINT)
@@ -298,7 +310,9 @@ def main():
         e2e_s = float(t.item())
     # H2D per call: the kernel-parameter struct (coefficient table + header);
     # the orbit start tables are uploaded once per context and plan
-    if lay.mode == N.LAYOUT_ORBIT:
+    if lay.mode == N.LAYOUT_ORBIT_FFT:
+        h2d = 8 * d + 136 + 16 + 24                          # coefficients + FftHead + launch arguments
+    elif lay.mode == N.LAYOUT_ORBIT:
         h2d = 8 * (-(-d // ORB_M) * ORB_M) + 152 + 24          # OrbLinArgs<1008> + launch arguments
     else:
         h2d = 24 * d + 112 + 16                                # FamArgs<LinDim, 1000> + launch arguments
@@ -317,8 +331,8 @@ def main():
     if os.path.exists(prof_path):
         with open(prof_path) as fh:
             prof = json.load(fh)
-    traffic = prof.get("k_orbit_dram_bytes_per_launch" if lay.mode == N.LAYOUT_ORBIT
-                       else "k_lin_dram_bytes_per_launch")
+    traffic = prof.get({N.LAYOUT_ORBIT_FFT: "k_orbit_fft_dram_bytes_per_launch",
+                        N.LAYOUT_ORBIT: "k_orbit_dram_bytes_per_launch"}.get(lay.mode, "k_lin_dram_bytes_per_launch"))
 
     cpu = None
     if world == 1 and args.cpu_sample > 0:
@@ -369,11 +383,17 @@ def main():
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
                      "kernel": kernel_name, "kernel_ms": avg_kern,
-                     "layout": "orbit" if lay.mode == N.LAYOUT_ORBIT else "index",
+                     "layout": {N.LAYOUT_ORBIT_FFT: "orbit-fft", N.LAYOUT_ORBIT: "orbit",
+                                N.LAYOUT_PAIRED: "paired"}.get(lay.mode, "index"),
                      "flops_per_unit": unit_txt,
                      "survey_convention": {"achieved": conv, "frac": conv / fp64_peak,
-                                           "note": "3 flop per point-dim (incl. the coordinate division r/n) "
-                                                   "charged once per linear form"},
+                                           "note": ("3 flop per point-dim (incl. the coordinate division r/n) "
+                                                    "charged once per linear form"
+                                                    + ("; i.e. what the direct O(d) evaluation of the same linear "
+                                                       "forms would have to sustain" if lay.mode == N.LAYOUT_ORBIT_FFT
+                                                       else ""))},
+                     "fp64_pipe_busy_ncu": prof.get({N.LAYOUT_ORBIT_FFT: "k_orbit_fft", N.LAYOUT_ORBIT: "k_orbit"}
+                                                    .get(lay.mode, "k_fam_index_kernel"), {}).get("fp64_pipe_pct_of_peak"),
                      "executed_dfma_tflops": executed, "executed_frac": executed / fp64_peak,
                      "peak_source": "measured in-run by lq_fp64_peak (DFMA chains, ~1 s); "
                                     "MEASURED_PEAKS.json has no FP64 entry"},
