@@ -856,14 +856,14 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     }
     if ((rc = upload(c, B_AUX0, cv.data(), sizeof(double) * d, &dc))) return rc;
     if ((rc = dev_buf(c, B_FFTH, sizeof(double2) * lq::kFftN, &Hc))) return rc;
-    lq::k_fft_coeffs<<<1, lq::kThreads, smem, c->stream>>>((const double*)dc, d, (const double2*)W, (double2*)Hc);
+    lq::k_fft_coeffs<<<1, lq::kFftThreads, smem, c->stream>>>((const double*)dc, d, (const double2*)W, (double2*)Hc);
     CK(cudaGetLastError());
     lq::FftHead h;
     h.n = p.n; h.B = (uint32_t)p.m; h.units = p.units; h.qc = p.qc; h.h = p.h;
     h.G = G; h.Alo = Alo; h.Ahi = Ahi; h.apow = apow; h.W = (const double2*)W; h.Hc = (const double2*)Hc;
     h.alpha = f->alpha; h.alphaB = f->alpha + bsum; h.K = f->K; h.A = f->A; h.Bc = f->B; h.C0 = f->C0;
     h.kappa = f->kappa; h.pw = f->power;
-    const dim3 g((unsigned)ntiles), b(lq::kThreads);
+    const dim3 g((unsigned)ntiles), b(lq::kFftThreads);
     t_begin(c);
     switch (lin_outer(f->kind)) {
         case lq::OUT_EXP: lq::k_orbit_fft<lq::OUT_EXP><<<g, b, smem, c->stream>>>(h, unit0, tiles_dev); break;

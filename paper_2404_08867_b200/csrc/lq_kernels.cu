@@ -707,15 +707,15 @@ __global__ void __launch_bounds__(kThreads) k_fft_twiddles(double2* __restrict__
     }
 }
 
-// Hc = conj(FFT(c_pad)) / N, one CTA.
-__global__ void __launch_bounds__(kThreads) k_fft_coeffs(const double* __restrict__ c, int d,
-                                                          const double2* __restrict__ W, double2* __restrict__ Hc) {
+// Hc = conj(FFT(c_pad)) / N, one CTA of kFftThreads.
+__global__ void __launch_bounds__(kFftThreads) k_fft_coeffs(const double* __restrict__ c, int d,
+                                                             const double2* __restrict__ W, double2* __restrict__ Hc) {
     extern __shared__ double2 buf[];
-    for (int t = threadIdx.x; t < kFftN; t += kThreads) buf[fpad(t)] = make_double2(t < d ? c[t] : 0.0, 0.0);
+    for (int t = threadIdx.x; t < kFftN; t += kFftThreads) buf[fpad(t)] = make_double2(t < d ? c[t] : 0.0, 0.0);
     __syncthreads();
     fft4096(buf, W);
     const double inv = 1.0 / (double)kFftN;
-    for (int t = threadIdx.x; t < kFftN; t += kThreads) {
+    for (int t = threadIdx.x; t < kFftN; t += kFftThreads) {
         const double2 v = buf[fpad(t)];
         Hc[t] = make_double2(v.x * inv, -v.y * inv);
     }
@@ -728,49 +728,69 @@ __device__ __forceinline__ uint32_t fft_chain_start(const FftHead& a, uint64_t u
     return mulmod32(mulmod32(a.G[cs], a.Alo[q & 4095u], n), a.Ahi[q >> 12], n);
 }
 
+// Deterministic CTA sum for NT threads (fixed tree).  Result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ double block_sum_n(double v, double* sh /* >= NT / 32 */) {
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < (NT / 32) ? sh[lane] : 0.0;
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    return v;
+}
+
 // One CTA = two chains (units 2b, 2b + 1 after unit0); tile_out[b] = their sum.
 template <int OUTER>
-__global__ void __launch_bounds__(kThreads, 2) k_orbit_fft(const __grid_constant__ FftHead a, uint64_t unit0,
-                                                         double* __restrict__ tile_out) {
+__global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_constant__ FftHead a, uint64_t unit0,
+                                                               double* __restrict__ tile_out) {
+    constexpr int R = kFftR;
     extern __shared__ double2 buf[];   // kFftPad
-    __shared__ double sh[8];
+    __shared__ double sh[32];
     const uint32_t n = a.n;
     const uint64_t u0 = unit0 + 2ull * blockIdx.x, u1 = u0 + 1;
     int v0 = 0, v1 = 0;
     const uint32_t s0 = u0 < a.units ? fft_chain_start(a, u0, v0) : 0u;
     const uint32_t s1 = u1 < a.units ? fft_chain_start(a, u1, v1) : 0u;
     // residues of both chains straight into the registers of the first pass:
-    // thread j holds positions j + 256 r
-    double2 v[16];
+    // thread j holds positions j + (N/R) r
+    double2 v[R];
     #pragma unroll
-    for (int r = 0; r < 16; ++r) {
-        const int t = threadIdx.x + r * kThreads;
+    for (int r = 0; r < R; ++r) {
+        const int t = threadIdx.x + r * kFftThreads;
         const uint2 ap = __ldg(a.apow + t);
         v[r] = make_double2((double)mulmod_shoup(s0, ap.x, ap.y, n), (double)mulmod_shoup(s1, ap.x, ap.y, n));
     }
-    fft4096_regs(v, buf, a.W);
+    fft4096_regs<false>(v, buf, a.W);
     // Y = X conj(C) / N, conjugated so that the forward transform inverts it;
-    // the last forward pass left positions j + 256 r in this thread, which are
-    // exactly the inputs of the first inverse pass
+    // the last forward pass left positions j + (N/R) r in this thread, which
+    // are exactly the inputs of the first inverse pass
     #pragma unroll
-    for (int r = 0; r < 16; ++r) {
-        const double2 y = cmul(v[r], __ldg(a.Hc + threadIdx.x + r * kThreads));
+    for (int r = 0; r < R; ++r) {
+        const double2 y = cmul(v[r], __ldg(a.Hc + threadIdx.x + r * kFftThreads));
         v[r] = make_double2(y.x, -y.y);
     }
     // inverse transform; its last pass writes the correlations to shared memory
     // so the out-of-line outer function runs with no transform state live
-    fft_pass<false, true>(v, buf, 1, a.W);
-    fft_pass<true, true>(v, buf, 16, a.W);
-    fft_pass<true, true>(v, buf, 256, a.W);
+    fft4096_regs<true>(v, buf, a.W);
     const LinParams prm{a.alpha, 1.0, a.K, a.A, a.Bc, a.C0, a.kappa, a.pw};
     double s = 0.0;
-    for (int k = threadIdx.x; k < v0 || k < v1; k += kThreads) {
+    #pragma unroll 1
+    for (int k = threadIdx.x; k < v0 || k < v1; k += kFftThreads) {
         const double2 y = buf[fpad(k)];             // conj of the correlation: (L0, -L1)
-        if (k < v0) s += outer_pair<OUTER>(y.x, prm, a.alphaB, true);
-        if (k < v1) s += outer_pair<OUTER>(-y.y, prm, a.alphaB, true);
+        // inlined (no call): nothing else is live here
+        const double l0 = y.x, l1 = -y.y;
+        const double f00 = outer_val<OUTER>(l0 + prm.alpha, prm), f01 = outer_val<OUTER>(a.alphaB - l0, prm);
+        const double f10 = outer_val<OUTER>(l1 + prm.alpha, prm), f11 = outer_val<OUTER>(a.alphaB - l1, prm);
+        s += (k < v0 ? f00 + f01 : 0.0) + (k < v1 ? f10 + f11 : 0.0);
     }
     if (u0 == 0 && threadIdx.x == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
-    s = block_sum(s, sh);
+    s = block_sum_n<kFftThreads>(s, sh);
     if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
 }
 
