@@ -721,11 +721,17 @@ __global__ void __launch_bounds__(kFftThreads) k_fft_coeffs(const double* __rest
     }
 }
 
-__device__ __forceinline__ uint32_t fft_chain_start(const FftHead& a, uint64_t u, int& valid) {
+__device__ __forceinline__ uint32_t fft_chain_start(const FftHead& a, uint64_t u) {
     const uint32_t n = a.n;
     const uint32_t cs = (uint32_t)(u / a.qc), q = (uint32_t)(u - (uint64_t)cs * a.qc);
-    valid = (int)min(a.B, a.h - q * a.B);
     return mulmod32(mulmod32(a.G[cs], a.Alo[q & 4095u], n), a.Ahi[q >> 12], n);
+}
+
+// points of chain u that belong to the enumeration (the last chain of a coset is short)
+__device__ __forceinline__ int fft_chain_valid(const FftHead& a, uint64_t u) {
+    if (u >= a.units) return 0;
+    const uint32_t q = (uint32_t)(u % a.qc);
+    return (int)min(a.B, a.h - q * a.B);
 }
 
 // Deterministic CTA sum for NT threads (fixed tree).  Result valid in thread 0.
@@ -754,9 +760,8 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
     __shared__ double sh[32];
     const uint32_t n = a.n;
     const uint64_t u0 = unit0 + 2ull * blockIdx.x, u1 = u0 + 1;
-    int v0 = 0, v1 = 0;
-    const uint32_t s0 = u0 < a.units ? fft_chain_start(a, u0, v0) : 0u;
-    const uint32_t s1 = u1 < a.units ? fft_chain_start(a, u1, v1) : 0u;
+    const uint32_t s0 = u0 < a.units ? fft_chain_start(a, u0) : 0u;
+    const uint32_t s1 = u1 < a.units ? fft_chain_start(a, u1) : 0u;
     // residues of both chains straight into the registers of the first pass:
     // thread j holds positions j + (N/R) r
     double2 v[R];
@@ -779,6 +784,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
     // so the out-of-line outer function runs with no transform state live
     fft4096_regs<true>(v, buf, a.W);
     const LinParams prm{a.alpha, 1.0, a.K, a.A, a.Bc, a.C0, a.kappa, a.pw};
+    const int v0 = fft_chain_valid(a, u0), v1 = fft_chain_valid(a, u1);   // recomputed: not live across the FFTs
     double s = 0.0;
     #pragma unroll 1
     for (int k = threadIdx.x; k < v0 || k < v1; k += kFftThreads) {
