@@ -830,7 +830,7 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     const uint2* apow;
     if ((rc = orbit_tables(c, p, &G, &Alo, &Ahi, &apow))) return rc;
     const int d = f->d;
-    const size_t smem = sizeof(double2) * lq::kFftPad;
+    const size_t smem = lq::kFftSmem;
     static bool attr = false;
     if (!attr) {
         CK(cudaFuncSetAttribute((const void*)lq::k_fft_coeffs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -4,7 +4,9 @@
 // 19.7 vs 14.5 ms on cfg5), one R-point butterfly per thread per pass.
 //
 // Shared-memory layout: element i lives at i + i / R (one pad slot per R), so
-// the stride-R stores of the first pass spread over the banks.
+// the stride-R stores of the first pass spread over the banks.  Radix-16
+// twiddles come from two small shared tables, Wlo[i] = W^i and W4[i] = W^(4i)
+// for i < 768 (24 KB): W^(r s) = Wlo[(r mod 4) s] W4[(r div 4) s].
 #pragma once
 #include <cstdint>
 
@@ -19,6 +21,16 @@ constexpr int kFftR = LQ_FFT_RADIX;
 constexpr int kFftThreads = kFftN / kFftR;
 constexpr int kFftLogR = kFftR == 16 ? 4 : 3;
 constexpr int kFftPad = kFftN + kFftN / kFftR;   // padded shared-memory length (double2)
+constexpr int kFftTw = 768;                       // entries of each radix-16 twiddle table
+constexpr int kFftSmem = (kFftPad + (kFftR == 16 ? 2 * kFftTw : 0)) * 16;   // bytes per CTA
+
+// Load the radix-16 twiddle tables (Wlo, W4) from the global W into tw[0 .. 2*768).
+__device__ __forceinline__ void fft_load_twiddles(double2* __restrict__ tw, const double2* __restrict__ W) {
+    for (int i = threadIdx.x; i < kFftTw; i += kFftThreads) {
+        tw[i] = __ldg(W + i);
+        tw[kFftTw + i] = __ldg(W + 4 * i);
+    }
+}
 
 __device__ __forceinline__ int fpad(int i) { return i + (i >> kFftLogR); }
 
@@ -87,7 +99,8 @@ __host__ __device__ constexpr int dft_slot(int k) {
 }
 
 // One Stockham pass (sub-transform length Ns -> R Ns).  Thread j < N/R owns
-// inputs j + (N/R) r, r < R.  W[k] = e^{-2 pi i k / N}.
+// inputs j + (N/R) r, r < R.  W: R = 16 -> the shared tables of
+// fft_load_twiddles; R = 8 -> the global table e^{-2 pi i k / N}.
 //  * the inputs come from shared memory (LOAD) or are already in v;
 //  * the outputs go to shared memory (STORE; positions (j / Ns) R Ns + j % Ns
 //    + r Ns) or -- for the last pass, Ns = N/R, whose outputs are exactly
@@ -105,13 +118,15 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[kFftR], double2* __restric
     if (Ns > 1) {
         const int step = k * (kFftN / (Ns * kFftR));
         if constexpr (kFftR == 16) {
-            // W^(r step), r = r0 + 4 r1, as W^(r0 step) W^(4 r1 step): six table
-            // loads instead of fifteen (fewer live registers, no spills)
+            // W^(r step), r = r0 + 4 r1, as W^(r0 step) W^(4 r1 step): six
+            // shared-table loads instead of fifteen global ones (q step < 768)
+            const double2* __restrict__ Wlo = W;
+            const double2* __restrict__ W4 = W + kFftTw;
             double2 lo[4], hi[4];
             #pragma unroll
             for (int q = 1; q < 4; ++q) {
-                lo[q] = __ldg(W + ((q * step) & (kFftN - 1)));
-                hi[q] = __ldg(W + ((4 * q * step) & (kFftN - 1)));
+                lo[q] = Wlo[q * step];
+                hi[q] = W4[q * step];
             }
             #pragma unroll
             for (int r = 1; r < 16; ++r) {

@@ -711,9 +711,11 @@ __global__ void __launch_bounds__(kThreads) k_fft_twiddles(double2* __restrict__
 __global__ void __launch_bounds__(kFftThreads) k_fft_coeffs(const double* __restrict__ c, int d,
                                                              const double2* __restrict__ W, double2* __restrict__ Hc) {
     extern __shared__ double2 buf[];
+    double2* tw = buf + kFftPad;
+    fft_load_twiddles(tw, W);
     for (int t = threadIdx.x; t < kFftN; t += kFftThreads) buf[fpad(t)] = make_double2(t < d ? c[t] : 0.0, 0.0);
     __syncthreads();
-    fft4096(buf, W);
+    fft4096(buf, kFftR == 16 ? tw : W);
     const double inv = 1.0 / (double)kFftN;
     for (int t = threadIdx.x; t < kFftN; t += kFftThreads) {
         const double2 v = buf[fpad(t)];
@@ -756,8 +758,11 @@ template <int OUTER>
 __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_constant__ FftHead a, uint64_t unit0,
                                                                double* __restrict__ tile_out) {
     constexpr int R = kFftR;
-    extern __shared__ double2 buf[];   // kFftPad
+    extern __shared__ double2 buf[];   // kFftPad, then the twiddle tables
     __shared__ double sh[32];
+    double2* tw = buf + kFftPad;
+    fft_load_twiddles(tw, a.W);          // visible after the first pass's barrier
+    const double2* Wt = kFftR == 16 ? tw : a.W;
     const uint32_t n = a.n;
     const uint64_t u0 = unit0 + 2ull * blockIdx.x, u1 = u0 + 1;
     const uint32_t s0 = u0 < a.units ? fft_chain_start(a, u0) : 0u;
@@ -771,7 +776,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
         const uint2 ap = __ldg(a.apow + t);
         v[r] = make_double2((double)mulmod_shoup(s0, ap.x, ap.y, n), (double)mulmod_shoup(s1, ap.x, ap.y, n));
     }
-    fft4096_regs<false>(v, buf, a.W);
+    fft4096_regs<false>(v, buf, Wt);
     // Y = X conj(C) / N, conjugated so that the forward transform inverts it;
     // the last forward pass left positions j + (N/R) r in this thread, which
     // are exactly the inputs of the first inverse pass
@@ -782,7 +787,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
     }
     // inverse transform; its last pass writes the correlations to shared memory
     // so the out-of-line outer function runs with no transform state live
-    fft4096_regs<true>(v, buf, a.W);
+    fft4096_regs<true>(v, buf, Wt);
     const LinParams prm{a.alpha, 1.0, a.K, a.A, a.Bc, a.C0, a.kappa, a.pw};
     const int v0 = fft_chain_valid(a, u0), v1 = fft_chain_valid(a, u1);   // recomputed: not live across the FFTs
     double s = 0.0;
