@@ -701,10 +701,22 @@ int orbit_mode() {
 // (cfg2, n = 10^4, d = 100: FFT 0.029 ms vs direct orbit 0.022 ms.)
 constexpr int kFftMinD = 96;
 constexpr uint64_t kFftMinN = 1ull << 20;
+// Accuracy guard: the FFT's norm-wise error on a linear form is about
+// eps log2(N) ||c||_2 ||P||_2 <= 1.2e-16 * 12 * ||beta||_2 * sqrt(N)
+// (c = beta / n, residues < n); the FFT form is used only while that bound
+// stays below 1e-11 absolute on the linear forms (||beta||_2 <= ~100), where
+// the direct kernels' own rounding is of the same order.
+bool fft_accurate(const lq_integrand* f) {
+    double s2 = 0.0;
+    for (int j = 0; j < f->d; ++j) s2 += f->beta[j] * f->beta[j];
+    const double bound = 1.2e-16 * 12.0 * std::sqrt(s2) * std::sqrt((double)lq::kFftN);
+    return std::isfinite(bound) && bound <= 1e-11;
+}
+
 bool fft_wanted(const lq_integrand* f, uint64_t n) {
     const char* e = std::getenv("LQ_FFT");
     if (e && !std::strcmp(e, "0")) return false;
-    if (!is_lin_kind(f->kind) || f->d > lq::kFftN / 2) return false;
+    if (!is_lin_kind(f->kind) || f->d > lq::kFftN / 2 || !f->beta || !fft_accurate(f)) return false;
     if (e && !std::strcmp(e, "always")) return f->d >= 2;
     return f->d >= kFftMinD && n >= kFftMinN;
 }

@@ -276,3 +276,27 @@ def test_error_mapping_without_gpu():
         pytest.skip("CPU-only check")
     with pytest.raises(_native.NativeUnavailable):
         _native.ctx(0)
+
+
+def test_layout_selection_without_gpu():
+    # host-side layout decisions (no GPU needed): FFT form for cfg5, the
+    # accuracy guard keeps huge-coefficient linear forms on the direct orbit
+    # kernel, non-Korobov rules get mirror pairs, composite moduli index tiles
+    import numpy as np
+    from paper_2404_08867_b200 import _native, engine
+    cfg = make_config(5)
+    pi = engine.plain_integrand(lq.parse(cfg.text, cfg.d), cfg.d)
+    rule = lq.korobov_vector(cfg.plain_a, cfg.plain_n, cfg.d)
+    lay = _native.lattice_layout(pi.struct, rule.n, rule.z_reduced_array())
+    assert lay.mode == _native.LAYOUT_ORBIT_FFT and lay.tile_units == 2
+    assert lay.n_units * (4097 - cfg.d) >= (rule.n - 1) // 2
+    d = 200
+    big = "cos(" + " + ".join(f"{30.0 + j}*x[{j + 1}]" for j in range(d)) + ")"
+    pib = engine.plain_integrand(lq.parse(big, d), d)
+    r = lq.korobov_vector(1234567, 2147483647, d)
+    assert _native.lattice_layout(pib.struct, r.n, r.z_reduced_array()).mode == _native.LAYOUT_ORBIT
+    r2 = lq.LatticeRule(1000003, tuple(int(v) for v in np.arange(1, 2 * d, 2)))
+    assert _native.lattice_layout(pib.struct, r2.n, r2.z_reduced_array()).mode == _native.LAYOUT_PAIRED
+    r3 = lq.korobov_vector(7, 1 << 20, d)
+    assert _native.lattice_layout(pib.struct, r3.n, r3.z_reduced_array()).mode in (_native.LAYOUT_PAIRED,
+                                                                                      _native.LAYOUT_INDEX)
