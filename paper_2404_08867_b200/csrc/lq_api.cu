@@ -708,7 +708,14 @@ constexpr uint64_t kFftMinN = 1ull << 20;
 // the direct kernels' own rounding is of the same order.
 bool fft_accurate(const lq_integrand* f) {
     double s2 = 0.0;
-    for (int j = 0; j < f->d; ++j) s2 += f->beta[j] * f->beta[j];
+    for (int j = 0; j < f->d; ++j) {
+        if (is_quad_kind(f->kind)) {   // centred form: b' = beta + gamma, q = gamma (|u| <= 1/2)
+            const double bp = f->beta[j] + f->gamma[j];
+            s2 += bp * bp + f->gamma[j] * f->gamma[j];
+        } else {
+            s2 += f->beta[j] * f->beta[j];
+        }
+    }
     const double bound = 1.2e-16 * 12.0 * std::sqrt(s2) * std::sqrt((double)lq::kFftN);
     return std::isfinite(bound) && bound <= 1e-11;
 }
@@ -716,7 +723,9 @@ bool fft_accurate(const lq_integrand* f) {
 bool fft_wanted(const lq_integrand* f, uint64_t n) {
     const char* e = std::getenv("LQ_FFT");
     if (e && !std::strcmp(e, "0")) return false;
-    if (!is_lin_kind(f->kind) || f->d > lq::kFftN / 2 || !f->beta || !fft_accurate(f)) return false;
+    if (!(is_lin_kind(f->kind) || is_quad_kind(f->kind)) || f->d > lq::kFftN / 2 || !f->beta) return false;
+    if (is_quad_kind(f->kind) && !f->gamma) return false;
+    if (!fft_accurate(f)) return false;
     if (e && !std::strcmp(e, "always")) return f->d >= 2;
     return f->d >= kFftMinD && n >= kFftMinN;
 }
@@ -730,7 +739,6 @@ std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, cons
     const bool quad = is_quad_kind(f->kind);
     const int m = prod ? lq::kOrbProdM : lq::orb_len(quad ? lq::FAM_QUAD : lq::FAM_LIN);
     const int cap = prod ? lq::kOrbProdDims : quad ? lq::kOrbQuadDims : lq::kOrbLinDims;
-    if ((f->d + m - 1) / m * m > cap) return nullptr;
     if (!f->beta || ((quad || prod) && !f->gamma)) return nullptr;
     if (prod)
         for (int j = 0; j < f->d; ++j)
@@ -739,13 +747,14 @@ std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, cons
     const uint64_t a = z[1];
     for (int j = 2; j < f->d; ++j)
         if (z[j] != z[j - 1] * a % n) return nullptr;   // z_j = a^(j-1) mod n
-    if (fft && fft_wanted(f, n)) {
+    if (fft && fft_wanted(f, n)) {   // the FFT form has its own dimension limit (d <= N/2)
         auto p = orbit_plan((uint32_t)n, (uint32_t)a, lq::kFftN - f->d + 1, true, true);
         if (p) {
             *fft = true;
             return p;
         }
     }
+    if ((f->d + m - 1) / m * m > cap) return nullptr;   // direct form: tables in parameter space
     return orbit_plan((uint32_t)n, (uint32_t)a, m, !prod);
 }
 
@@ -850,6 +859,9 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
         CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft<lq::OUT_SINCOS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft<lq::OUT_EXPABS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft<lq::OUT_POW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute((const void*)lq::k_fft_coeffs_pm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft_quad<lq::OUT_EXP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft_quad<lq::OUT_SINCOS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     void *W, *Hc, *dc;
@@ -860,15 +872,30 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
         c->fft_w = true;
     }
     const double nd = (double)p.n;
-    std::vector<double> cv(d);
+    const bool quad = is_quad_kind(f->kind);
     double bsum = 0.0;
-    for (int j = 0; j < d; ++j) {
-        cv[j] = f->beta[j] / nd;
-        bsum += f->beta[j];
+    if ((rc = dev_buf(c, B_FFTH, sizeof(double2) * lq::kFftN * (quad ? 2 : 1), &Hc))) return rc;
+    if (quad) {
+        // centred form: b'_j = beta_j + gamma_j, q_j = gamma_j; alpha' = alpha + sum(beta/2 + gamma/4)
+        std::vector<double> bq(2 * (size_t)d);
+        for (int j = 0; j < d; ++j) {
+            bq[j] = f->beta[j] + f->gamma[j];
+            bq[d + j] = f->gamma[j];
+            bsum += 0.5 * f->beta[j] + 0.25 * f->gamma[j];
+        }
+        if ((rc = upload(c, B_AUX0, bq.data(), sizeof(double) * bq.size(), &dc))) return rc;
+        lq::k_fft_coeffs_pm<<<1, lq::kFftThreads, smem, c->stream>>>((const double*)dc, (const double*)dc + d, d,
+                                                                    (const double2*)W, (double2*)Hc,
+                                                                    (double2*)Hc + lq::kFftN);
+    } else {
+        std::vector<double> cv(d);
+        for (int j = 0; j < d; ++j) {
+            cv[j] = f->beta[j] / nd;
+            bsum += f->beta[j];
+        }
+        if ((rc = upload(c, B_AUX0, cv.data(), sizeof(double) * d, &dc))) return rc;
+        lq::k_fft_coeffs<<<1, lq::kFftThreads, smem, c->stream>>>((const double*)dc, d, (const double2*)W, (double2*)Hc);
     }
-    if ((rc = upload(c, B_AUX0, cv.data(), sizeof(double) * d, &dc))) return rc;
-    if ((rc = dev_buf(c, B_FFTH, sizeof(double2) * lq::kFftN, &Hc))) return rc;
-    lq::k_fft_coeffs<<<1, lq::kFftThreads, smem, c->stream>>>((const double*)dc, d, (const double2*)W, (double2*)Hc);
     CK(cudaGetLastError());
     lq::FftHead h;
     h.n = p.n; h.B = (uint32_t)p.m; h.units = p.units; h.qc = p.qc; h.h = p.h;
@@ -876,6 +903,17 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     h.alpha = f->alpha; h.alphaB = f->alpha + bsum; h.K = f->K; h.A = f->A; h.Bc = f->B; h.C0 = f->C0;
     h.kappa = f->kappa; h.pw = f->power;
     const dim3 g((unsigned)ntiles), b(lq::kFftThreads);
+    if (quad) {
+        const double2* Hm = (const double2*)Hc + lq::kFftN;
+        t_begin(c);
+        if (quad_outer_of(f->kind) == lq::OUT_SINCOS)
+            lq::k_orbit_fft_quad<lq::OUT_SINCOS><<<g, b, smem, c->stream>>>(h, Hm, unit0, tiles_dev);
+        else
+            lq::k_orbit_fft_quad<lq::OUT_EXP><<<g, b, smem, c->stream>>>(h, Hm, unit0, tiles_dev);
+        t_end(c);
+        CK(cudaGetLastError());
+        return LQ_OK;
+    }
     t_begin(c);
     switch (lin_outer(f->kind)) {
         case lq::OUT_EXP: lq::k_orbit_fft<lq::OUT_EXP><<<g, b, smem, c->stream>>>(h, unit0, tiles_dev); break;
@@ -978,7 +1016,8 @@ Layout layout_of(const lq_integrand* f, uint64_t n, const uint64_t* z) {
     Layout L;
     L.orb = orbit_for(f, n, z, &L.fft);
     if (L.orb) {
-        L.tile_units = L.fft ? 2 : lq::kThreads;   // FFT form: two chains per CTA
+        // FFT form: two chains per CTA (linear families) or one (Gaussian family)
+        L.tile_units = L.fft ? (is_quad_kind(f->kind) ? 1 : 2) : lq::kThreads;
         L.n_units = L.orb->units;
     } else if (uses_family_kernel(f, n) && pair_ok(f, n, z)) {
         L.pair = true;

@@ -723,6 +723,31 @@ __global__ void __launch_bounds__(kFftThreads) k_fft_coeffs(const double* __rest
     }
 }
 
+// H+- = (conj(FFT(b)) +- conj(FFT(q))) / (2N) for the Gaussian family: b and q
+// share one transform (b + i q) and are separated by symmetry.  One CTA.
+__global__ void __launch_bounds__(kFftThreads) k_fft_coeffs_pm(const double* __restrict__ b,
+                                                                const double* __restrict__ q, int d,
+                                                                const double2* __restrict__ W,
+                                                                double2* __restrict__ Hp, double2* __restrict__ Hm) {
+    extern __shared__ double2 buf[];
+    double2* tw = buf + kFftPad;
+    fft_load_twiddles(tw, W);
+    for (int t = threadIdx.x; t < kFftN; t += kFftThreads)
+        buf[fpad(t)] = t < d ? make_double2(b[t], q[t]) : make_double2(0.0, 0.0);
+    __syncthreads();
+    fft4096(buf, kFftR == 16 ? tw : W);
+    const double h = 0.5 / (double)kFftN;
+    for (int m = threadIdx.x; m < kFftN; m += kFftThreads) {
+        const double2 x = buf[fpad(m)], xr = buf[fpad((kFftN - m) & (kFftN - 1))];
+        const double2 sb = make_double2(x.x + xr.x, x.y - xr.y);    // 2 FFT(b)[m]
+        const double2 sq = make_double2(x.y + xr.y, xr.x - x.x);    // 2 FFT(q)[m]  ((x - conj xr) / i)
+        const double2 hb = make_double2(sb.x * h, -sb.y * h);       // conj(FFT(b)) / N
+        const double2 hq = make_double2(sq.x * h, -sq.y * h);       // conj(FFT(q)) / N
+        Hp[m] = make_double2(0.5 * (hb.x + hq.x), 0.5 * (hb.y + hq.y));
+        Hm[m] = make_double2(0.5 * (hb.x - hq.x), 0.5 * (hb.y - hq.y));
+    }
+}
+
 __device__ __forceinline__ uint32_t fft_chain_start(const FftHead& a, uint64_t u) {
     const uint32_t n = a.n;
     const uint32_t cs = (uint32_t)(u / a.qc), q = (uint32_t)(u - (uint64_t)cs * a.qc);
@@ -801,6 +826,57 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
         s += (k < v0 ? f00 + f01 : 0.0) + (k < v1 ? f10 + f11 : 0.0);
     }
     if (u0 == 0 && threadIdx.x == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
+    s = block_sum_n<kFftThreads>(s, sh);
+    if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
+}
+
+// Gaussian family in FFT form: one chain per CTA.  The centred coordinates
+// u_t = P[t]/n - 1/2 and their squares ride as x = u + i u^2 in one transform;
+// with X = FFT(x), the odd/even correlations (b' with u, q with u^2) come back
+// as Re/Im of IFFT(Z), Z[m] = X[m] H+[m] + conj(X[N-m]) H-[m],
+// H+- = (conj(FFT(b')) +- conj(FFT(q))) / (2N) (spectra of the real parts
+// separated by symmetry).  Point and mirror: exp(alpha' + even +- odd).
+template <int OUTER>
+__global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft_quad(const __grid_constant__ FftHead a,
+                                                                    const double2* __restrict__ Hm,
+                                                                    uint64_t unit0, double* __restrict__ tile_out) {
+    constexpr int R = kFftR;
+    extern __shared__ double2 buf[];   // kFftPad, then the twiddle tables
+    __shared__ double sh[32];
+    double2* tw = buf + kFftPad;
+    fft_load_twiddles(tw, a.W);
+    const double2* Wt = kFftR == 16 ? tw : a.W;
+    const uint32_t n = a.n;
+    const uint64_t u0 = unit0 + blockIdx.x;
+    const uint32_t s0 = u0 < a.units ? fft_chain_start(a, u0) : 0u;
+    const double inv_n = 1.0 / (double)n;
+    double2 v[R];
+    #pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int t = threadIdx.x + r * kFftThreads;
+        const uint2 ap = __ldg(a.apow + t);
+        const double u = fma((double)mulmod_shoup(s0, ap.x, ap.y, n), inv_n, -0.5);
+        v[r] = make_double2(u, u * u);
+    }
+    fft4096_regs<true>(v, buf, Wt);        // X in shared memory, natural order
+    #pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int m = threadIdx.x + r * kFftThreads;
+        const double2 x = buf[fpad(m)], xr = buf[fpad((kFftN - m) & (kFftN - 1))];
+        const double2 z = cadd(cmul(x, __ldg(a.Hc + m)), cmul(make_double2(xr.x, -xr.y), __ldg(Hm + m)));
+        v[r] = make_double2(z.x, -z.y);     // conjugated: the forward transform inverts it
+    }
+    fft4096_regs<true>(v, buf, Wt);        // (first pass stores only after its barrier)
+    const LinParams prm{a.alpha, 1.0, a.K, a.A, a.Bc, a.C0, a.kappa, a.pw};
+    const int v0 = fft_chain_valid(a, u0);
+    double s = 0.0;
+    #pragma unroll 1
+    for (int k = threadIdx.x; k < v0; k += kFftThreads) {
+        const double2 y = buf[fpad(k)];    // conj: (odd, -even)
+        const double t = a.alphaB - y.y;
+        s += outer_val<OUTER>(t + y.x, prm) + outer_val<OUTER>(t - y.x, prm);
+    }
+    if (u0 == 0 && threadIdx.x == 0) s += quad_outer<OUTER>(0.0, prm);   // point 0
     s = block_sum_n<kFftThreads>(s, sh);
     if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
 }
