@@ -793,13 +793,18 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
     const uint32_t s0 = u0 < a.units ? fft_chain_start(a, u0) : 0u;
     const uint32_t s1 = u1 < a.units ? fft_chain_start(a, u1) : 0u;
     // residues of both chains straight into the registers of the first pass:
-    // thread j holds positions j + (N/R) r
+    // thread j holds positions t = j + (N/R) r, P[t] = s a^j (a^(N/R))^r --
+    // one table load per thread, then a Shoup step per position
     double2 v[R];
-    #pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int t = threadIdx.x + r * kFftThreads;
-        const uint2 ap = __ldg(a.apow + t);
-        v[r] = make_double2((double)mulmod_shoup(s0, ap.x, ap.y, n), (double)mulmod_shoup(s1, ap.x, ap.y, n));
+    {
+        const uint2 aj = __ldg(a.apow + threadIdx.x), as = __ldg(a.apow + kFftThreads);
+        uint32_t p0 = mulmod_shoup(s0, aj.x, aj.y, n), p1 = mulmod_shoup(s1, aj.x, aj.y, n);
+        #pragma unroll
+        for (int r = 0; r < R; ++r) {
+            v[r] = make_double2((double)p0, (double)p1);
+            p0 = mulmod_shoup(p0, as.x, as.y, n);
+            p1 = mulmod_shoup(p1, as.x, as.y, n);
+        }
     }
     fft4096_regs<false>(v, buf, Wt);
     // Y = X conj(C) / N, conjugated so that the forward transform inverts it;
