@@ -168,7 +168,7 @@ def mdi_sum(g, grids, cfg=None):
     midpoint = getattr(grids, "midpoint", False)
     plan = engine.separable_plan(e, counts, None if midpoint else grids.nodes)
     usable = plan.ok and (plan.n_factors + plan.n_terms) <= cfg.budget
-    total = math.prod(counts)
+    total = _total(tuple(counts))
     if (not usable and total > cfg.direct_cap and getattr(grids, "midpoint", False)
             and cfg.fallback == "numeric"):
         rep = _characteristic(e, d, counts, levels, base_axes, t0)
@@ -206,7 +206,7 @@ def _characteristic(e, d, counts, levels, base_axes, t0):
     if fam is None or fam.kind != "lin_expabs" or not fam.kappa < 0.0 or fam.K == 0.0:
         return None
     beta = np.asarray(fam.beta, dtype=np.float64)
-    log_total = float(sum(math.log(c) for c in counts))
+    log_total = _log_total(tuple(counts))
     if not np.any(beta):
         mean = math.exp(fam.kappa * abs(fam.alpha))
     else:
@@ -224,7 +224,7 @@ def _characteristic(e, d, counts, levels, base_axes, t0):
 
 def _normalize(raw, counts):
     """raw / prod(counts) without overflowing float (mdi.py:195-203)."""
-    total = math.prod(counts)
+    total = _total(tuple(counts))
     if total <= 2**53:
         return raw / total
     out = raw
@@ -256,6 +256,12 @@ def _det_a(rule):
 @functools.lru_cache(maxsize=64)
 def _log_total(counts):
     return float(sum(math.log(c) for c in counts))
+
+
+@functools.lru_cache(maxsize=64)
+def _total(counts):
+    """prod(counts) as an exact integer (thousands of bits at d = 1000), cached."""
+    return math.prod(counts) if counts else 1
 
 
 def mdi_lr(f, d, a, n, cfg=None, rule=None, with_report=False):

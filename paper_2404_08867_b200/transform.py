@@ -22,7 +22,7 @@ class AxisGridSet:
     RN((t + 0.5) / n_i) is regenerated on the GPU -- and materialise the
     tuples only when ``nodes`` is read."""
 
-    __slots__ = ("counts", "n", "z", "_nodes", "midpoint")
+    __slots__ = ("counts", "n", "z", "_nodes", "midpoint", "_total")
 
     def __init__(self, nodes, counts, n, z, midpoint=False):
         counts = tuple(int(c) for c in counts)
@@ -38,6 +38,7 @@ class AxisGridSet:
         self.z = z
         self._nodes = nodes
         self.midpoint = midpoint
+        self._total = None
 
     @property
     def nodes(self):
@@ -51,7 +52,9 @@ class AxisGridSet:
 
     @property
     def total(self):
-        return math.prod(self.counts)
+        if self._total is None:
+            self._total = math.prod(self.counts)
+        return self._total
 
     def node_arrays(self):
         return [np.asarray(nd, dtype=float) for nd in self.nodes]
@@ -83,5 +86,10 @@ def axis_counts(rule):
 
 
 def midpoint_grids(rule):
-    """Open grids: nodes (t + 1/2)/n_i with the rule's axis counts (transform.py:169-178)."""
-    return AxisGridSet(None, axis_counts(rule), rule.n, rule.z, midpoint=True)
+    """Open grids: nodes (t + 1/2)/n_i with the rule's axis counts (transform.py:169-178).
+    Immutable, so one grid set is kept per (immutable) rule object."""
+    g = rule.__dict__.get("_midpoint_grids")
+    if g is None:
+        g = AxisGridSet(None, axis_counts(rule), rule.n, rule.z, midpoint=True)
+        object.__setattr__(rule, "_midpoint_grids", g)
+    return g
