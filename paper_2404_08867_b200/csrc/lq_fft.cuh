@@ -5,8 +5,7 @@
 //
 // Shared-memory layout: element i lives at i + i / R (one pad slot per R), so
 // the stride-R stores of the first pass spread over the banks.  Radix-16
-// twiddles come from two small shared tables, Wlo[i] = W^i and W4[i] = W^(4i)
-// for i < 768 (24 KB): W^(r s) = Wlo[(r mod 4) s] W4[(r div 4) s].
+// twiddles come from small shared tables (26 KB, see fft_load_twiddles).
 #pragma once
 #include <cstdint>
 
@@ -21,14 +20,26 @@ constexpr int kFftR = LQ_FFT_RADIX;
 constexpr int kFftThreads = kFftN / kFftR;
 constexpr int kFftLogR = kFftR == 16 ? 4 : 3;
 constexpr int kFftPad = kFftN + kFftN / kFftR;   // padded shared-memory length (double2)
-constexpr int kFftTw = 768;                       // entries of each radix-16 twiddle table
-constexpr int kFftSmem = (kFftPad + (kFftR == 16 ? 2 * kFftTw : 0)) * 16;   // bytes per CTA
+// Radix-16 twiddle tables in shared memory, laid out [q][k] so that the lanes
+// of a warp (consecutive k) read consecutive entries:
+//   pass Ns = 256: L3[q][k] = W^(q k),    H3[q][k] = W^(4 q k),   k < 256
+//   pass Ns = 16:  L2[q][k] = W^(16 q k), H2[q][k] = W^(64 q k),  k < 16
+// (q = 1..3; W = e^{-2 pi i / N}); W^(r s) = L[r mod 4] H[r div 4].
+constexpr int kFftTw3 = 3 * 256, kFftTw2 = 3 * 16;
+constexpr int kFftTwAll = 2 * kFftTw3 + 2 * kFftTw2;
+constexpr int kFftSmem = (kFftPad + (kFftR == 16 ? kFftTwAll : 0)) * 16;   // bytes per CTA
 
-// Load the radix-16 twiddle tables (Wlo, W4) from the global W into tw[0 .. 2*768).
+// Build the radix-16 tables from the global table W[k] = e^{-2 pi i k / N}.
 __device__ __forceinline__ void fft_load_twiddles(double2* __restrict__ tw, const double2* __restrict__ W) {
-    for (int i = threadIdx.x; i < kFftTw; i += kFftThreads) {
-        tw[i] = __ldg(W + i);
-        tw[kFftTw + i] = __ldg(W + 4 * i);
+    for (int i = threadIdx.x; i < kFftTw3; i += kFftThreads) {
+        const int q = i / 256 + 1, k = i & 255;
+        tw[i] = __ldg(W + q * k);
+        tw[kFftTw3 + i] = __ldg(W + ((4 * q * k) & (kFftN - 1)));
+    }
+    for (int i = threadIdx.x; i < kFftTw2; i += kFftThreads) {
+        const int q = i / 16 + 1, k = i & 15;
+        tw[2 * kFftTw3 + i] = __ldg(W + 16 * q * k);
+        tw[2 * kFftTw3 + kFftTw2 + i] = __ldg(W + ((64 * q * k) & (kFftN - 1)));
     }
 }
 
@@ -119,14 +130,14 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[kFftR], double2* __restric
         const int step = k * (kFftN / (Ns * kFftR));
         if constexpr (kFftR == 16) {
             // W^(r step), r = r0 + 4 r1, as W^(r0 step) W^(4 r1 step): six
-            // shared-table loads instead of fifteen global ones (q step < 768)
-            const double2* __restrict__ Wlo = W;
-            const double2* __restrict__ W4 = W + kFftTw;
+            // conflict-free shared-table loads instead of fifteen global ones
+            const double2* __restrict__ L = Ns == 256 ? W : W + 2 * kFftTw3;
+            const double2* __restrict__ H = Ns == 256 ? W + kFftTw3 : W + 2 * kFftTw3 + kFftTw2;
             double2 lo[4], hi[4];
             #pragma unroll
             for (int q = 1; q < 4; ++q) {
-                lo[q] = Wlo[q * step];
-                hi[q] = W4[q * step];
+                lo[q] = L[(q - 1) * Ns + k];
+                hi[q] = H[(q - 1) * Ns + k];
             }
             #pragma unroll
             for (int r = 1; r < 16; ++r) {
