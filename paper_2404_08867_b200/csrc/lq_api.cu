@@ -868,6 +868,7 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     if ((rc = dev_buf(c, B_FFTW, sizeof(double2) * lq::kFftN, &W))) return rc;
     if (!c->fft_w) {
         lq::k_fft_twiddles<<<lq::kFftN / lq::kThreads, lq::kThreads, 0, c->stream>>>((double2*)W);
+        c->launches++;
         CK(cudaGetLastError());
         c->fft_w = true;
     }
@@ -896,6 +897,7 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
         if ((rc = upload(c, B_AUX0, cv.data(), sizeof(double) * d, &dc))) return rc;
         lq::k_fft_coeffs<<<1, lq::kFftThreads, smem, c->stream>>>((const double*)dc, d, (const double2*)W, (double2*)Hc);
     }
+    c->launches++;   // the coefficient transform
     CK(cudaGetLastError());
     lq::FftHead h;
     h.n = p.n; h.B = (uint32_t)p.m; h.units = p.units; h.qc = p.qc; h.h = p.h;
