@@ -698,9 +698,10 @@ int orbit_mode() {
 // The FFT form (k_orbit_fft) for the linear families when d is large enough
 // for O(log N) per point to beat O(d) and the lattice is large enough to fill
 // the GPU with 4096-point tiles: LQ_FFT=0 disables, =always forces.
-// (cfg2, n = 10^4, d = 100: FFT 0.029 ms vs direct orbit 0.022 ms.)
+// (kernel ms, FFT vs direct orbit: cfg2, n = 10^4, d = 100: 0.023 vs 0.022;
+// cfg3, n = 10^6, d = 300: 0.018 vs 0.054.)
 constexpr int kFftMinD = 96;
-constexpr uint64_t kFftMinN = 1ull << 20;
+constexpr uint64_t kFftMinN = 1ull << 18;
 // Accuracy guard: the FFT's norm-wise error on a linear form is about
 // eps log2(N) ||c||_2 ||P||_2 <= 1.2e-16 * 12 * ||beta||_2 * sqrt(N)
 // (c = beta / n, residues < n); the FFT form is used only while that bound
