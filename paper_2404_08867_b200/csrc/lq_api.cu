@@ -176,7 +176,7 @@ int reduce_dev(lq_ctx* c, const double* vals, int64_t count, double** result) {
 }
 
 int read_scalar(lq_ctx* c, const double* dev, double* out, int k = 1) {
-    void* h;
+    void* h = nullptr;
     int rc = pin_buf(c, sizeof(double) * k, &h);
     if (rc) return rc;
     CK(cudaMemcpyAsync(h, dev, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));

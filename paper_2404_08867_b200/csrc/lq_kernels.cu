@@ -587,7 +587,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_orbit(const __grid_constant__ A
                     r = mulmod_shoup(r, za, zs, n);
                 }
             }
-            #pragma unroll
             const LinParams prm{H.alpha, H.scale, H.K, H.A, H.B, H.C0, H.kappa, H.pw};
             #pragma unroll
             for (int k = 0; k < M; ++k) s += k < valid ? quad_pair<OUTER>(ao[k], ae[k], H.alphaB, prm, true) : 0.0;
