@@ -326,8 +326,8 @@ def test_product_family_config4_integrand(env, monkeypatch):
 
 
 def test_randomised_layouts_agree(env, monkeypatch):
-    # random primes, Korobov parameters, dimensions and families: the orbit,
-    # mirror-paired and plain index layouts give the same sums
+    # random primes, Korobov parameters, dimensions and families: the FFT-form
+    # orbit, direct orbit, mirror-paired and plain index layouts give the same sums
     lq, N, engine = env
     rng = np.random.default_rng(2024)
 
@@ -354,9 +354,10 @@ def test_randomised_layouts_agree(env, monkeypatch):
         pi = engine.plain_integrand(f, d)
         z = rule.z_reduced_array()
         vals = {}
-        for orb, pair in (("1", "1"), ("0", "1"), ("0", "0")):
+        for orb, pair, fft in (("1", "1", "always"), ("1", "1", "0"), ("0", "1", "0"), ("0", "0", "0")):
             monkeypatch.setenv("LQ_ORBIT", orb)
             monkeypatch.setenv("LQ_PAIR", pair)
+            monkeypatch.setenv("LQ_FFT", fft)
             mode = N.lattice_layout(pi.struct, n, z).mode
             vals[mode] = engine.lattice_sum(pi, n, z)
         base = vals[N.LAYOUT_INDEX]
