@@ -8,7 +8,7 @@ sm_100a library ``liblq.so`` (include/lq.h).
 """
 
 from .expr import Expr, ParseError, UnassignedVariableError, as_expr, free_vars, node_count, parse
-from .lattice import LatticeRule, iter_point_blocks, korobov_vector, lattice_points, points_block
+from .lattice import LatticeRule, fibonacci_rule, iter_point_blocks, korobov_vector, lattice_points, points_block
 from .transform import AxisGridSet, axis_counts, midpoint_grids
 from .mdi import (DEFAULT_NODE_BUDGET, DIRECT_CAP, BudgetExceededError, GridCapError, MdiConfig,
                   MdiReport, direct_tensor_sum, mdi_lr, mdi_sum)
@@ -20,7 +20,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Expr", "ParseError", "UnassignedVariableError", "as_expr", "free_vars", "node_count", "parse",
-    "LatticeRule", "iter_point_blocks", "korobov_vector", "lattice_points", "points_block",
+    "LatticeRule", "fibonacci_rule", "iter_point_blocks", "korobov_vector", "lattice_points", "points_block",
     "AxisGridSet", "axis_counts", "midpoint_grids",
     "DEFAULT_NODE_BUDGET", "DIRECT_CAP", "BudgetExceededError", "GridCapError", "MdiConfig",
     "MdiReport", "direct_tensor_sum", "mdi_lr", "mdi_sum",

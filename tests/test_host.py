@@ -300,3 +300,17 @@ def test_layout_selection_without_gpu():
     r3 = lq.korobov_vector(7, 1 << 20, d)
     assert _native.lattice_layout(pib.struct, r3.n, r3.z_reduced_array()).mode in (_native.LAYOUT_PAIRED,
                                                                                       _native.LAYOUT_INDEX)
+
+
+def test_fibonacci_rule_mirrors_reference():
+    # lattice.py:120-129 and the reference's own pins (tests/test_lattice.py:85-98)
+    assert lq.fibonacci_rule(2) == lq.LatticeRule(2, (1, 1))
+    assert lq.fibonacci_rule(10) == lq.LatticeRule(89, (1, 55))
+    assert lq.fibonacci_rule(15) == lq.LatticeRule(987, (1, 610))
+    for k in range(3, 30):
+        r = lq.fibonacci_rule(k)
+        assert r.z[1] < r.n and math.gcd(r.z[1], r.n) == 1
+    with pytest.raises(ValueError):
+        lq.fibonacci_rule(1)
+    with pytest.raises(OverflowError):
+        lq.fibonacci_rule(78)
