@@ -135,6 +135,7 @@ int lq_lattice_sum(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_
 #define LQ_LAYOUT_ORBIT 1
 #define LQ_LAYOUT_PAIRED 2   /* units: mirror-pair indices i in [0, n/2] (points i and n - i) */
 #define LQ_LAYOUT_ORBIT_FFT 3 /* units: Korobov chains of 4097 - d points, two per FFT tile */
+#define LQ_LAYOUT_ORBIT_POW2 4 /* n = 2^k Korobov: units are tiles (levels of chains + the 2^m0 lattice) */
 int lq_lattice_layout(const lq_integrand* f, uint64_t n, const uint64_t* z_reduced, int64_t* tile_units,
                       int64_t* n_supers, int64_t* n_units, int32_t* mode);
 int lq_lattice_partials(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_t* z_reduced,

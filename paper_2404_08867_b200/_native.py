@@ -166,7 +166,7 @@ def ctx(device=None):
 
 
 Layout = collections.namedtuple("Layout", "tile_units n_supers n_units mode")
-LAYOUT_INDEX, LAYOUT_ORBIT, LAYOUT_PAIRED, LAYOUT_ORBIT_FFT = 0, 1, 2, 3
+LAYOUT_INDEX, LAYOUT_ORBIT, LAYOUT_PAIRED, LAYOUT_ORBIT_FFT, LAYOUT_ORBIT_POW2 = 0, 1, 2, 3, 4
 
 
 def lattice_layout(pi_struct, n, z=None):

@@ -602,6 +602,7 @@ struct OrbPlan {
     uint64_t units = 0;
     int m = 0;
     bool mirror = true;
+    bool zero = true;             // the launch covering unit 0 also adds the point x = 0
     std::vector<uint32_t> G, Alo, Ahi;
     std::vector<uint32_t> apow;   // FFT plans: (a^t mod n, Shoup constant) pairs, t < kFftN
 };
@@ -682,6 +683,101 @@ std::shared_ptr<const OrbPlan> orbit_plan(uint32_t n, uint32_t a, int m, bool mi
     if (cache.size() > 64) cache.clear();
     cache[key] = p;
     return p;
+}
+
+// ---- Korobov rules with n = 2^k.  Point i = 2^v u (u odd) has residues
+// 2^v (u a^(j-1) mod 2^m), m = k - v: level m is the unit group mod 2^m, whose
+// mirror classes {u, -u} are the cyclic group <5> (order 2^(m-2)); a = +-5^alpha
+// moves a class by alpha, so the chains i0 a^t of a level run along the cosets
+// 5^e <5^alpha> (e < 2^tau, tau = v2(alpha)).  Each level is an orbit sum with
+// modulus 2^m; the levels too short for chains, and the point 0, form the
+// lattice with modulus 2^m0, summed by the per-index kernel.
+uint64_t inv_pow2(uint64_t x, int m) {   // x odd: x^-1 mod 2^m (Newton)
+    uint64_t y = x;
+    for (int i = 0; i < 6; ++i) y *= 2 - x * y;
+    return m >= 64 ? y : (y & ((1ull << m) - 1));
+}
+
+std::shared_ptr<const OrbPlan> build_orbit_plan_pow2(int m, uint32_t a_full, int len, bool fft) {
+    if (m < 3 || m > 31) return nullptr;
+    const uint64_t n = 1ull << m, mask = n - 1;
+    const uint64_t a = a_full & mask;
+    if (!(a & 1)) return nullptr;
+    const uint64_t b = (a & 3) == 1 ? a : (n - a) & mask;   // the <5> part of +-a
+    // discrete log of b to base 5 in <5> mod 2^m, bit by bit (5^(2^i) = 1 + 2^(i+2) mod 2^(i+3))
+    uint64_t alpha = 0, cur = b, p5 = 5;   // cur = b 5^-alpha
+    for (int i = 0; i < m - 2; ++i) {
+        if ((cur & ((1ull << (i + 3)) - 1)) != 1) {
+            alpha |= 1ull << i;
+            cur = (cur * inv_pow2(p5, 64)) & mask;
+        }
+        p5 = (p5 * p5) & mask;
+    }
+    if (alpha == 0) return nullptr;                          // a = +-1 mod 2^m: no chains
+    int tau = 0;
+    while (!((alpha >> tau) & 1)) ++tau;
+    const uint64_t L = 1ull << (m - 2 - tau);                 // class-cycle length
+    const uint64_t cosets = 1ull << tau;
+    if (cosets > kOrbMaxCosets || L < (uint64_t)len) return nullptr;
+    static std::atomic<uint64_t> next_id{1ull << 40};
+    auto p = std::make_shared<OrbPlan>();
+    p->id = next_id++;
+    p->n = (uint32_t)n; p->a = (uint32_t)a; p->m = len; p->h = (uint32_t)L; p->mirror = true; p->zero = false;
+    p->as = (uint32_t)((a << 32) / n);
+    p->qc = (uint32_t)((L + len - 1) / len);
+    p->units = cosets * p->qc;
+    p->G.resize(cosets);
+    uint64_t g = 1;
+    for (uint64_t e = 0; e < cosets; ++e) { p->G[e] = (uint32_t)g; g = (g * 5) & mask; }
+    auto mulm = [&](uint64_t x, uint64_t y) { return (x * y) & mask; };
+    uint64_t am = 1;
+    for (int i = 0; i < len; ++i) am = mulm(am, a);
+    p->Alo.resize(4096);
+    uint64_t t = 1;
+    for (int q = 0; q < 4096; ++q) { p->Alo[q] = (uint32_t)t; t = mulm(t, am); }
+    const uint64_t am4096 = t;
+    p->Ahi.resize(p->qc / 4096 + 1);
+    t = 1;
+    for (size_t q = 0; q < p->Ahi.size(); ++q) { p->Ahi[q] = (uint32_t)t; t = mulm(t, am4096); }
+    if (fft) {
+        p->apow.resize(2 * lq::kFftN);
+        t = 1;
+        for (int k = 0; k < lq::kFftN; ++k) {
+            p->apow[2 * k] = (uint32_t)t;
+            p->apow[2 * k + 1] = (uint32_t)((t << 32) / n);
+            t = mulm(t, a);
+        }
+    }
+    return p;
+}
+
+struct Pow2Plan {
+    int k = 0, m0 = 0;                                  // levels m0+1 .. k; small lattice mod 2^m0
+    bool fft = false;
+    std::vector<std::shared_ptr<const OrbPlan>> levels; // m = k, k-1, ..., m0+1
+};
+
+std::shared_ptr<const Pow2Plan> pow2_plan(uint32_t a, int k, int len, bool fft) {
+    static std::mutex mu;
+    static std::map<std::tuple<uint32_t, int, int, bool>, std::shared_ptr<const Pow2Plan>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(a, k, len, fft);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    auto P = std::make_shared<Pow2Plan>();
+    P->k = k;
+    P->fft = fft;
+    int m = k;
+    for (; m >= 3; --m) {
+        auto lp = build_orbit_plan_pow2(m, a, len, fft);
+        if (!lp) break;
+        P->levels.push_back(lp);
+    }
+    P->m0 = m;
+    std::shared_ptr<const Pow2Plan> out = P->levels.empty() ? nullptr : P;
+    if (cache.size() > 64) cache.clear();
+    cache[key] = out;
+    return out;
 }
 
 // LQ_ORBIT=0 disables the orbit kernel; otherwise it runs whenever the rule
@@ -901,7 +997,7 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     c->launches++;   // the coefficient transform
     CK(cudaGetLastError());
     lq::FftHead h;
-    h.n = p.n; h.B = (uint32_t)p.m; h.units = p.units; h.qc = p.qc; h.h = p.h;
+    h.n = p.n; h.B = (uint32_t)p.m; h.units = p.units; h.qc = p.qc; h.h = p.h; h.zero = p.zero ? 1 : 0;
     h.G = G; h.Alo = Alo; h.Ahi = Ahi; h.apow = apow; h.W = (const double2*)W; h.Hc = (const double2*)Hc;
     h.alpha = f->alpha; h.alphaB = f->alpha + bsum; h.K = f->K; h.A = f->A; h.Bc = f->B; h.C0 = f->C0;
     h.kappa = f->kappa; h.pw = f->power;
@@ -940,6 +1036,7 @@ int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t un
     const double nd = (double)p.n;
     lq::OrbHead h;
     h.n = p.n; h.a = p.a; h.as = p.as; h.dpad = dpad; h.units = p.units; h.qc = p.qc; h.h = p.h;
+    h.zero = p.zero ? 1 : 0;
     h.G = G; h.Alo = Alo; h.Ahi = Ahi;
     h.alpha = f->alpha; h.K = f->K; h.A = f->A; h.B = f->B; h.C0 = f->C0; h.kappa = f->kappa; h.pw = f->power;
     if (f->kind == LQ_FAM_PROD_QUAD) {
@@ -1010,13 +1107,62 @@ struct Layout {
     uint64_t tile_units = 0, n_units = 0;
     std::shared_ptr<const OrbPlan> orb;
     bool pair = false, fft = false;
+    // n = 2^k Korobov rules: level segments of tiles, then the small lattice
+    std::shared_ptr<const Pow2Plan> p2;
+    std::vector<int64_t> seg;          // first tile of each level, of the small lattice, and the end
+    uint64_t small_n = 0, small_tp = 0;
     int mode() const {
+        if (p2) return LQ_LAYOUT_ORBIT_POW2;
         return orb ? (fft ? LQ_LAYOUT_ORBIT_FFT : LQ_LAYOUT_ORBIT) : pair ? LQ_LAYOUT_PAIRED : LQ_LAYOUT_INDEX;
     }
 };
 
+// n = 2^k Korobov rules of the linear and Gaussian families (mirror pairs).
+std::shared_ptr<const Pow2Plan> pow2_for(const lq_integrand* f, uint64_t n, const uint64_t* z, bool* fft) {
+    *fft = false;
+    if (orbit_mode() == 0 || !z || f->d < 2 || !(is_lin_kind(f->kind) || is_quad_kind(f->kind))) return nullptr;
+    if (n < (1ull << 12) || n > (1ull << 31) || (n & (n - 1))) return nullptr;
+    if (!f->beta || (is_quad_kind(f->kind) && !f->gamma)) return nullptr;
+    if (z[0] != 1) return nullptr;
+    const uint64_t a = z[1];
+    if (!(a & 1)) return nullptr;
+    for (int j = 2; j < f->d; ++j)
+        if (z[j] != z[j - 1] * a % n) return nullptr;
+    int k = 0;
+    while ((1ull << k) < n) ++k;
+    const bool quad = is_quad_kind(f->kind);
+    bool use_fft = fft_wanted(f, n);
+    int len = use_fft ? lq::kFftN - f->d + 1 : lq::orb_len(quad ? lq::FAM_QUAD : lq::FAM_LIN);
+    if (!use_fft) {
+        const int cap = quad ? lq::kOrbQuadDims : lq::kOrbLinDims;
+        if ((f->d + len - 1) / len * len > cap) return nullptr;
+    }
+    auto P = pow2_plan((uint32_t)a, k, len, use_fft);
+    if (P) *fft = use_fft;
+    return P;
+}
+
 Layout layout_of(const lq_integrand* f, uint64_t n, const uint64_t* z) {
     Layout L;
+    bool fft2 = false;
+    if ((L.p2 = pow2_for(f, n, z, &fft2))) {
+        L.fft = fft2;
+        const bool quad = is_quad_kind(f->kind);
+        const uint64_t tu = fft2 ? (quad ? 1 : 2) : lq::kThreads;
+        int64_t t = 0;
+        for (const auto& lp : L.p2->levels) {
+            L.seg.push_back(t);
+            t += (int64_t)((lp->units + tu - 1) / tu);
+        }
+        L.small_n = 1ull << L.p2->m0;
+        L.small_tp = tile_points(f, L.small_n);
+        L.seg.push_back(t);
+        t += (int64_t)((L.small_n + L.small_tp - 1) / L.small_tp);
+        L.seg.push_back(t);
+        L.tile_units = 1;                 // units are tiles
+        L.n_units = (uint64_t)t;
+        return L;
+    }
     L.orb = orbit_for(f, n, z, &L.fft);
     if (L.orb) {
         // FFT form: two chains per CTA (linear families) or one (Gaussian family)
@@ -1031,6 +1177,34 @@ Layout layout_of(const lq_integrand* f, uint64_t n, const uint64_t* z) {
         L.n_units = n;
     }
     return L;
+}
+
+// Tiles [T0, T1) of a 2^k layout into tiles_dev[0 .. T1 - T0).
+int launch_pow2_tiles(lq_ctx* c, const lq_integrand* f, const uint64_t* z, const Layout& L, int64_t T0, int64_t T1,
+                      double* tiles_dev) {
+    int rc;
+    const int nl = (int)L.p2->levels.size();
+    const bool quad = is_quad_kind(f->kind);
+    const uint64_t tu = L.fft ? (quad ? 1 : 2) : lq::kThreads;
+    for (int l = 0; l <= nl; ++l) {
+        const int64_t lo = std::max(T0, L.seg[l]), hi = std::min(T1, L.seg[l + 1]);
+        if (hi <= lo) continue;
+        double* out = tiles_dev + (lo - T0);
+        if (l < nl) {
+            const OrbPlan& lp = *L.p2->levels[l];
+            const uint64_t unit0 = (uint64_t)(lo - L.seg[l]) * tu;
+            rc = L.fft ? launch_orbit_fft(c, f, lp, unit0, hi - lo, out) : launch_orbit(c, f, lp, unit0, hi - lo, out);
+        } else {
+            // the lattice mod 2^m0: every level too short for chains, and the point 0
+            std::vector<uint64_t> zs(f->d);
+            for (int j = 0; j < f->d; ++j) zs[j] = z[j] & (L.small_n - 1);
+            const uint64_t base = (uint64_t)(lo - L.seg[l]) * L.small_tp;
+            const uint64_t end = std::min<uint64_t>((uint64_t)(hi - L.seg[l]) * L.small_tp, L.small_n);
+            rc = launch_tiles(c, f, L.small_n, zs.data(), base, end, hi - lo, out);
+        }
+        if (rc) return rc;
+    }
+    return LQ_OK;
 }
 
 }  // namespace
@@ -1205,7 +1379,9 @@ int lq_lattice_partials(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint
     const int64_t ntiles = (int64_t)((end - base + tp - 1) / tp);
     void* tiles;
     if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
-    if (L.orb) {
+    if (L.p2) {
+        if ((rc = launch_pow2_tiles(c, f, z, L, (int64_t)base, (int64_t)end, (double*)tiles))) return rc;
+    } else if (L.orb) {
         if ((rc = L.fft ? launch_orbit_fft(c, f, *L.orb, base, ntiles, (double*)tiles)
                         : launch_orbit(c, f, *L.orb, base, ntiles, (double*)tiles))) return rc;
     } else {
@@ -1239,6 +1415,15 @@ int lq_lattice_sum(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t*
     }
     if (i_begin == 0 && i_end == n) {
         const Layout L = layout_of(f, n, z);
+        if (L.p2) {
+            const int64_t ntiles = (int64_t)L.n_units;
+            void* tiles;
+            if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
+            if ((rc = launch_pow2_tiles(c, f, z, L, 0, ntiles, (double*)tiles))) return rc;
+            double* r;
+            if ((rc = reduce_dev(c, (const double*)tiles, ntiles, &r))) return rc;
+            return read_scalar(c, r, sum_out);
+        }
         if (L.orb || L.pair) {
             const int64_t ntiles = (int64_t)((L.n_units + L.tile_units - 1) / L.tile_units);
             void* tiles;

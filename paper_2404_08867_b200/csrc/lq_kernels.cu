@@ -485,6 +485,7 @@ struct OrbHead {
     const uint32_t* Alo;    // a^(m q) for q < 4096
     const uint32_t* Ahi;    // a^(m 4096 q)
     double alpha, alphaB, scale, bsum, K, A, B, C0, kappa, M, half, pw;
+    int32_t zero;           // unit 0 also adds the point x = 0 (not for the levels of n = 2^k)
 };
 
 constexpr int kOrbParamBytes = 32000;
@@ -556,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_orbit(const __grid_constant__ A
             #pragma unroll
             for (int k = 0; k < M; ++k)
                 s += k < valid ? outer_pair<OUTER>(acc[k], prm, H.alphaB, true) : 0.0;
-            if (u == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
+            if (u == 0 && H.zero) s += outer_fn<OUTER>(0.0, prm);   // point 0
         } else {
             const double Ms = H.M, hf = H.half;
             double U[M], V[M], ao[M], ae[M];
@@ -590,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_orbit(const __grid_constant__ A
             const LinParams prm{H.alpha, H.scale, H.K, H.A, H.B, H.C0, H.kappa, H.pw};
             #pragma unroll
             for (int k = 0; k < M; ++k) s += k < valid ? quad_pair<OUTER>(ao[k], ae[k], H.alphaB, prm, true) : 0.0;
-            if (u == 0) s += quad_outer<OUTER>(0.0, prm);   // point 0
+            if (u == 0 && H.zero) s += quad_outer<OUTER>(0.0, prm);   // point 0
         }
     }
     s = block_sum(s, sh);
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_orbit_prod(const __grid_constan
         }
         #pragma unroll
         for (int k = 0; k < M; ++k) s += k < valid ? prod_outer(D[k], E[k], H.K, H.pw, a.off) : 0.0;
-        if (u == 0) {   // point 0 (x = 0): the same factors at t = -w_j
+        if (u == 0 && H.zero) {   // point 0 (x = 0): the same factors at t = -w_j
             double D0 = 1.0;
             int E0 = 0;
             for (int j = 0; j < a.nf; ++j) {
@@ -696,6 +697,7 @@ struct FftHead {
     const double2* W;                  // e^{-2 pi i k / N}
     const double2* Hc;                 // conj(FFT(c zero-padded)) / N, c_j = beta_j / n
     double alpha, alphaB, K, A, Bc, C0, kappa, pw;
+    int32_t zero;                      // unit 0 also adds the point x = 0
 };
 
 __global__ void __launch_bounds__(kThreads) k_fft_twiddles(double2* __restrict__ W) {
@@ -837,7 +839,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
         const double f10 = outer_val<OUTER>(l1 + prm.alpha, prm), f11 = outer_val<OUTER>(a.alphaB - l1, prm);
         s += (k < v0 ? f00 + f01 : 0.0) + (k < v1 ? f10 + f11 : 0.0);
     }
-    if (u0 == 0 && threadIdx.x == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
+    if (u0 == 0 && a.zero && threadIdx.x == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
     s = block_sum_n<kFftThreads>(s, sh);
     if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
 }
@@ -888,7 +890,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft_quad(const __grid_
         const double t = a.alphaB - y.y;
         s += outer_val<OUTER>(t + y.x, prm) + outer_val<OUTER>(t - y.x, prm);
     }
-    if (u0 == 0 && threadIdx.x == 0) s += quad_outer<OUTER>(0.0, prm);   // point 0
+    if (u0 == 0 && a.zero && threadIdx.x == 0) s += quad_outer<OUTER>(0.0, prm);   // point 0
     s = block_sum_n<kFftThreads>(s, sh);
     if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
 }

@@ -363,3 +363,65 @@ def test_randomised_layouts_agree(env, monkeypatch):
         base = vals[N.LAYOUT_INDEX]
         for mode, v in vals.items():
             assert math.isclose(v, base, rel_tol=1e-11, abs_tol=1e-9 * n), (trial, fam, n, a, d, mode, v, base)
+
+
+# ---------------------------------------------------------------- n = 2^k
+@pytest.mark.parametrize("k,a,d", [(12, 5, 9), (16, 3, 37), (20, 1234567 | 1, 37), (20, 3, 200), (22, 5, 300),
+                                   (24, 12345 | 1, 600)])
+@pytest.mark.parametrize("family", ["exp", "sincos", "expabs", "pow", "gauss", "qtrig"])
+def test_pow2_levels_vs_paired(env, k, a, d, family, monkeypatch):
+    # Korobov rules with n = 2^k: orbit / FFT levels of the unit groups mod 2^m
+    # plus the small 2^m0 lattice against the mirror-paired index kernel
+    lq, N, engine = env
+    n = 1 << k
+    rng = np.random.default_rng(zlib.crc32(f"pow2/{k}/{a}/{d}/{family}".encode()))
+    f = lq.parse(_family_text(family, d, rng), d)
+    rule = lq.korobov_vector(a % n, n, d)
+    pi = engine.plain_integrand(f, d)
+    z = rule.z_reduced_array()
+    monkeypatch.delenv("LQ_ORBIT", raising=False)
+    monkeypatch.delenv("LQ_FFT", raising=False)
+    lay = N.lattice_layout(pi.struct, n, z)
+    got = engine.lattice_sum(pi, n, z)
+    monkeypatch.setenv("LQ_ORBIT", "0")
+    assert N.lattice_layout(pi.struct, n, z).mode == N.LAYOUT_PAIRED
+    want = engine.lattice_sum(pi, n, z)
+    assert lay.mode == N.LAYOUT_ORBIT_POW2, lay
+    assert math.isclose(got, want, rel_tol=1e-11, abs_tol=1e-9 * n), (k, a, d, family, got, want)
+    if n * d <= 200000:
+        from oracle import np_oracle
+        ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
+        assert math.isclose(got, ref, rel_tol=REL, abs_tol=1e-9 * n), (k, a, d, family, got, ref)
+
+
+def test_pow2_partials_sharded_bit_identical(env, monkeypatch):
+    # the 2^k layout through the multi-GPU building blocks: shards of tiles
+    # (levels and the small lattice) reproduce the one-launch sum bit for bit
+    import ctypes as C
+    import torch
+    lq, N, engine = env
+    from paper_2404_08867_b200.configs import make_config
+    from paper_2404_08867_b200.distributed import shard_range
+    monkeypatch.delenv("LQ_ORBIT", raising=False)
+    cfg = make_config(5)
+    f = lq.parse(cfg.text, cfg.d)
+    n = 1 << 26
+    rule = lq.korobov_vector((cfg.plain_a | 1) % n, n, cfg.d)
+    pi = engine.plain_integrand(f, cfg.d)
+    z = rule.z_reduced_array()
+    lay = N.lattice_layout(pi.struct, n, z)
+    assert lay.mode == N.LAYOUT_ORBIT_POW2 and lay.n_supers >= 3
+    h, ctx = N.lib(), N.ctx()
+    S = lay.n_supers
+    one = torch.zeros(S, dtype=torch.float64, device="cuda")
+    N.check(h.lq_lattice_partials(ctx, C.byref(pi.struct), n, N.as_ptr(z), 0, S, C.c_void_p(one.data_ptr())))
+    many = torch.zeros(S, dtype=torch.float64, device="cuda")
+    for r in range(3):
+        lo, hi = shard_range(S, r, 3)
+        N.check(h.lq_lattice_partials(ctx, C.byref(pi.struct), n, N.as_ptr(z), lo, hi,
+                                      C.c_void_p(many.data_ptr() + 8 * lo)))
+    torch.cuda.synchronize()
+    assert torch.equal(one.view(torch.int64), many.view(torch.int64))
+    out = C.c_double()
+    N.check(h.lq_reduce_sum(ctx, C.c_void_p(one.data_ptr()), S, C.byref(out)))
+    assert out.value == engine.lattice_sum(pi, n, z)

@@ -281,7 +281,7 @@ def test_error_mapping_without_gpu():
 def test_layout_selection_without_gpu():
     # host-side layout decisions (no GPU needed): FFT form for cfg5, the
     # accuracy guard keeps huge-coefficient linear forms on the direct orbit
-    # kernel, non-Korobov rules get mirror pairs, composite moduli index tiles
+    # kernel, non-Korobov rules get mirror pairs, n = 2^k Korobov rules levels
     import numpy as np
     from paper_2404_08867_b200 import _native, engine
     cfg = make_config(5)
@@ -298,8 +298,7 @@ def test_layout_selection_without_gpu():
     r2 = lq.LatticeRule(1000003, tuple(int(v) for v in np.arange(1, 2 * d, 2)))
     assert _native.lattice_layout(pib.struct, r2.n, r2.z_reduced_array()).mode == _native.LAYOUT_PAIRED
     r3 = lq.korobov_vector(7, 1 << 20, d)
-    assert _native.lattice_layout(pib.struct, r3.n, r3.z_reduced_array()).mode in (_native.LAYOUT_PAIRED,
-                                                                                      _native.LAYOUT_INDEX)
+    assert _native.lattice_layout(pib.struct, r3.n, r3.z_reduced_array()).mode == _native.LAYOUT_ORBIT_POW2
 
 
 def test_fibonacci_rule_mirrors_reference():
@@ -314,3 +313,18 @@ def test_fibonacci_rule_mirrors_reference():
         lq.fibonacci_rule(1)
     with pytest.raises(OverflowError):
         lq.fibonacci_rule(78)
+
+
+def test_pow2_layout_without_gpu():
+    # n = 2^k Korobov rules get the level layout; even a, composite non-2^k n,
+    # or a = +-1 do not
+    from paper_2404_08867_b200 import _native, engine
+    cfg = make_config(5)
+    pi = engine.plain_integrand(lq.parse(cfg.text, cfg.d), cfg.d)
+    r = lq.korobov_vector(12345 | 1, 1 << 24, cfg.d)
+    lay = _native.lattice_layout(pi.struct, r.n, r.z_reduced_array())
+    assert lay.mode == _native.LAYOUT_ORBIT_POW2 and lay.tile_units == 1
+    r = lq.korobov_vector(1, 1 << 24, cfg.d)
+    assert _native.lattice_layout(pi.struct, r.n, r.z_reduced_array()).mode != _native.LAYOUT_ORBIT_POW2
+    r = lq.korobov_vector(12346, 1 << 24, cfg.d)
+    assert _native.lattice_layout(pi.struct, r.n, r.z_reduced_array()).mode != _native.LAYOUT_ORBIT_POW2
