@@ -69,8 +69,9 @@ struct lq_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_ms = 0.f;
     int64_t launches = 0;
-    uint64_t orb_id = 0;       // orbit plan whose start tables are in dbuf[B_ORB]
     bool fft_w = false;        // twiddles computed in dbuf[B_FFTW]
+    // device copies of orbit-plan tables by plan id (a 2^k rule has one plan per level)
+    std::map<uint64_t, std::pair<void*, size_t>> orb_tabs;
 };
 
 namespace {
@@ -861,7 +862,13 @@ int orbit_tables(lq_ctx* c, const OrbPlan& p, const uint32_t** G, const uint32_t
     const size_t nG = p.G.size(), nlo = p.Alo.size(), nhi = p.Ahi.size(), np = p.apow.size();
     const size_t pad = (nG + nlo + nhi) & 1;   // keep apow 8-byte aligned
     const size_t bytes = 4 * (nG + nlo + nhi + pad + np);
-    if (c->orb_id != p.id) {
+    auto it = c->orb_tabs.find(p.id);
+    if (it == c->orb_tabs.end()) {
+        if (c->orb_tabs.size() >= 64) {   // bounded cache: drop everything (plans are rebuilt cheaply)
+            CK(cudaStreamSynchronize(c->stream));
+            for (auto& kv : c->orb_tabs) cudaFree(kv.second.first);
+            c->orb_tabs.clear();
+        }
         std::vector<uint32_t> all;
         all.reserve(nG + nlo + nhi + pad + np);
         all.insert(all.end(), p.G.begin(), p.G.end());
@@ -869,12 +876,12 @@ int orbit_tables(lq_ctx* c, const OrbPlan& p, const uint32_t** G, const uint32_t
         all.insert(all.end(), p.Ahi.begin(), p.Ahi.end());
         if (pad) all.push_back(0);
         all.insert(all.end(), p.apow.begin(), p.apow.end());
-        void* d;
-        int rc;
-        if ((rc = upload(c, B_ORB, all.data(), bytes, &d))) return rc;
-        c->orb_id = p.id;
+        void* d = nullptr;
+        CK(cudaMalloc(&d, bytes));
+        CK(cudaMemcpy(d, all.data(), bytes, cudaMemcpyHostToDevice));   // once per (context, plan)
+        it = c->orb_tabs.emplace(p.id, std::make_pair(d, bytes)).first;
     }
-    const uint32_t* base = (const uint32_t*)c->dbuf[B_ORB];
+    const uint32_t* base = (const uint32_t*)it->second.first;
     *G = base;
     *Alo = base + nG;
     *Ahi = base + nG + nlo;
@@ -1249,6 +1256,7 @@ int lq_ctx_destroy(lq_ctx* c) {
     cudaStreamSynchronize(c->stream);
     for (int i = 0; i < B_NBUF; ++i)
         if (c->dbuf[i]) cudaFree(c->dbuf[i]);
+    for (auto& kv : c->orb_tabs) cudaFree(kv.second.first);
     if (c->hpin) cudaFreeHost(c->hpin);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
