@@ -257,7 +257,7 @@ def main():
     # dominant kernel roofline over this rank's units.  Orbit layout: a unit is
     # a chain of ORB_M points whose linear forms are computed once and serve
     # the point and its mirror; index layout: a unit is a point.
-    su = lay.tile_units * N.LQ_SUPER_TILES
+    su = lay.tile_units * lay.super_tiles
     my_units = min(s_hi * su, lay.n_units) - s_lo * su
     avg_kern = kern_ms / args.steps
     if lay.mode == N.LAYOUT_ORBIT_FFT:

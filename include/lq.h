@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define LQ_ABI_VERSION 3
+#define LQ_ABI_VERSION 4
 
 #define LQ_OK 0
 #define LQ_ERR_VALUE (-1)
@@ -124,8 +124,9 @@ int lq_lattice_sum(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_
  * mirrors n - i, or -- when every z_j is a unit mod n
  * (mode LQ_LAYOUT_PAIRED) -- mirror-pair indices i in [0, n/2], point i
  * summed with point n - i.  Units form tiles of tile_units, tiles form
- * super-chunks of LQ_SUPER_TILES; super-chunk s covers units
- * [s*T*LQ_SUPER_TILES, (s+1)*T*LQ_SUPER_TILES).  The layout depends on
+ * super-chunks of super_tiles tiles (LQ_SUPER_TILES; 256 for the FFT-form
+ * layouts, whose tiles are heavy); super-chunk s covers units
+ * [s*T*S, (s+1)*T*S), T = tile_units, S = super_tiles.  The layout depends on
  * (f, n, z) only, so every rank computes the same one; z may be NULL (index
  * layout).  lq_lattice_partials writes the partials of super-chunks
  * [s_begin, s_end) to out_dev[0 .. s_end-s_begin).  lq_lattice_sum over the
@@ -137,7 +138,7 @@ int lq_lattice_sum(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_
 #define LQ_LAYOUT_ORBIT_FFT 3 /* units: Korobov chains of 4097 - d points, two per FFT tile */
 #define LQ_LAYOUT_ORBIT_POW2 4 /* n = 2^k Korobov: units are tiles (levels of chains + the 2^m0 lattice) */
 int lq_lattice_layout(const lq_integrand* f, uint64_t n, const uint64_t* z_reduced, int64_t* tile_units,
-                      int64_t* n_supers, int64_t* n_units, int32_t* mode);
+                      int64_t* n_supers, int64_t* n_units, int32_t* mode, int64_t* super_tiles);
 int lq_lattice_partials(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_t* z_reduced,
                         int64_t s_begin, int64_t s_end, double* out_dev);
 /* Fixed pairwise tree over vals_dev[0..count); result to host *out. */

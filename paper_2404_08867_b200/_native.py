@@ -24,7 +24,7 @@ LQ_OK, LQ_ERR_VALUE, LQ_ERR_OVERFLOW, LQ_ERR_GRIDCAP = 0, -1, -2, -3
 LQ_ERR_CUDA, LQ_ERR_UNSUPPORTED, LQ_ERR_NOMEM = -4, -5, -6
 LQ_TILE, LQ_SUPER_TILES, LQ_NODE_BLOCK = 4096, 1024, 256
 
-ABI_VERSION = 3   # LQ_ABI_VERSION of include/lq.h these ctypes structs match
+ABI_VERSION = 4   # LQ_ABI_VERSION of include/lq.h these ctypes structs match
 FAM = {"program": 0, "lin_exp": 1, "lin_sincos": 2, "lin_expabs": 3, "quad_exp": 4, "lin_pow": 5, "quad_sincos": 6, "prod_quad": 7}
 
 
@@ -70,7 +70,7 @@ _SIGS = {
     "lq_lattice_sum": [_P, C.POINTER(Integrand), C.c_uint64, _P, C.c_uint64, C.c_uint64, C.POINTER(C.c_double)],
     "lq_lattice_partials": [_P, C.POINTER(Integrand), C.c_uint64, _P, C.c_int64, C.c_int64, _P],
     "lq_lattice_layout": [C.POINTER(Integrand), C.c_uint64, _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
-                          C.POINTER(C.c_int64), C.POINTER(C.c_int32)],
+                          C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int64)],
     "lq_reduce_sum": [_P, _P, C.c_int64, C.POINTER(C.c_double)],
     "lq_mc_sum": [_P, C.POINTER(Program), C.c_int32, C.c_uint64, _P, _P, C.c_uint64, C.c_uint64,
                   C.POINTER(C.c_double)],
@@ -165,7 +165,7 @@ def ctx(device=None):
     return c.ptr
 
 
-Layout = collections.namedtuple("Layout", "tile_units n_supers n_units mode")
+Layout = collections.namedtuple("Layout", "tile_units n_supers n_units mode super_tiles")
 LAYOUT_INDEX, LAYOUT_ORBIT, LAYOUT_PAIRED, LAYOUT_ORBIT_FFT, LAYOUT_ORBIT_POW2 = 0, 1, 2, 3, 4
 
 
@@ -174,10 +174,10 @@ def lattice_layout(pi_struct, n, z=None):
     units per tile, super-chunks, units, and the mode (LAYOUT_INDEX: units are
     points; LAYOUT_ORBIT: units are chains of mirrored Korobov points;
     LAYOUT_PAIRED: units are mirror-pair indices i in [0, n/2])."""
-    tp, ns, nu, mode = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
+    tp, ns, nu, mode, st = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32(), C.c_int64()
     check(lib().lq_lattice_layout(C.byref(pi_struct), int(n), as_ptr(z), C.byref(tp), C.byref(ns),
-                                  C.byref(nu), C.byref(mode)))
-    return Layout(tp.value, ns.value, nu.value, mode.value)
+                                  C.byref(nu), C.byref(mode), C.byref(st)))
+    return Layout(tp.value, ns.value, nu.value, mode.value, st.value)
 
 
 def as_ptr(arr):

@@ -1118,6 +1118,7 @@ struct Layout {
     std::shared_ptr<const Pow2Plan> p2;
     std::vector<int64_t> seg;          // first tile of each level, of the small lattice, and the end
     uint64_t small_n = 0, small_tp = 0;
+    int64_t super_tiles = LQ_SUPER_TILES;   // tiles per super-chunk (256 for the heavy FFT tiles)
     int mode() const {
         if (p2) return LQ_LAYOUT_ORBIT_POW2;
         return orb ? (fft ? LQ_LAYOUT_ORBIT_FFT : LQ_LAYOUT_ORBIT) : pair ? LQ_LAYOUT_PAIRED : LQ_LAYOUT_INDEX;
@@ -1168,12 +1169,14 @@ Layout layout_of(const lq_integrand* f, uint64_t n, const uint64_t* z) {
         L.seg.push_back(t);
         L.tile_units = 1;                 // units are tiles
         L.n_units = (uint64_t)t;
+        if (fft2) L.super_tiles = 256;
         return L;
     }
     L.orb = orbit_for(f, n, z, &L.fft);
     if (L.orb) {
         // FFT form: two chains per CTA (linear families) or one (Gaussian family)
         L.tile_units = L.fft ? (is_quad_kind(f->kind) ? 1 : 2) : lq::kThreads;
+        if (L.fft) L.super_tiles = 256;
         L.n_units = L.orb->units;
     } else if (uses_family_kernel(f, n) && pair_ok(f, n, z)) {
         L.pair = true;
@@ -1184,6 +1187,30 @@ Layout layout_of(const lq_integrand* f, uint64_t n, const uint64_t* z) {
         L.n_units = n;
     }
     return L;
+}
+
+// Super-chunk partials of tiles[0 .. ntiles) (groups of L.super_tiles) into out.
+int super_partials(lq_ctx* c, const Layout& L, const double* tiles, int64_t ntiles, int64_t groups, double* out) {
+    if (L.super_tiles == 256)
+        lq::k_reduce256<<<(unsigned)groups, lq::kThreads, 0, c->stream>>>(tiles, ntiles, out);
+    else
+        lq::k_reduce1024<<<(unsigned)groups, lq::kThreads, 0, c->stream>>>(tiles, ntiles, out);
+    c->launches++;
+    CK(cudaGetLastError());
+    return LQ_OK;
+}
+
+// Full sum of a layout's tiles: the super-chunk partials, then the fixed tree
+// over them -- the same association as lq_lattice_partials + lq_reduce_sum,
+// so one GPU and any number of ranks agree bit for bit.
+int layout_total(lq_ctx* c, const Layout& L, const double* tiles, int64_t ntiles, double** result) {
+    if (L.super_tiles == LQ_SUPER_TILES) return reduce_dev(c, tiles, ntiles, result);
+    const int64_t groups = (ntiles + L.super_tiles - 1) / L.super_tiles;
+    void* parts;
+    int rc;
+    if ((rc = dev_buf(c, B_PART, sizeof(double) * groups, &parts))) return rc;
+    if ((rc = super_partials(c, L, tiles, ntiles, groups, (double*)parts))) return rc;
+    return reduce_dev(c, (const double*)parts, groups, result);
 }
 
 // Tiles [T0, T1) of a 2^k layout into tiles_dev[0 .. T1 - T0).
@@ -1358,16 +1385,17 @@ int lq_points_block(lq_ctx* c, int32_t d, uint64_t n, const uint64_t* z, int64_t
 }
 
 int lq_lattice_layout(const lq_integrand* f, uint64_t n, const uint64_t* z, int64_t* tile_units, int64_t* n_supers,
-                      int64_t* n_units, int32_t* mode) {
+                      int64_t* n_units, int32_t* mode, int64_t* super_tiles) {
     int rc;
     if ((rc = check_integrand(f))) return rc;
     if (z && (rc = check_lattice(n, z, f->d))) return rc;
     const Layout L = layout_of(f, n, z);
-    const uint64_t sp = L.tile_units * LQ_SUPER_TILES;
+    const uint64_t sp = L.tile_units * (uint64_t)L.super_tiles;
     if (tile_units) *tile_units = (int64_t)L.tile_units;
     if (n_supers) *n_supers = (int64_t)((L.n_units + sp - 1) / sp);
     if (n_units) *n_units = (int64_t)L.n_units;
     if (mode) *mode = L.mode();
+    if (super_tiles) *super_tiles = L.super_tiles;
     return LQ_OK;
 }
 
@@ -1377,7 +1405,7 @@ int lq_lattice_partials(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint
     if (rc) return rc;
     if ((rc = check_integrand(f)) || (rc = check_lattice(n, z, f->d))) return rc;
     const Layout L = layout_of(f, n, z);
-    const uint64_t tp = L.tile_units, sp = tp * LQ_SUPER_TILES;
+    const uint64_t tp = L.tile_units, sp = tp * (uint64_t)L.super_tiles;
     const int64_t ns = (int64_t)((L.n_units + sp - 1) / sp);
     if (s_begin < 0 || s_end > ns || s_end < s_begin)
         return fail(LQ_ERR_VALUE, "super-chunk range [%lld, %lld) outside [0, %lld)", (long long)s_begin, (long long)s_end, (long long)ns);
@@ -1395,10 +1423,7 @@ int lq_lattice_partials(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint
     } else {
         if ((rc = launch_tiles(c, f, n, z, base, end, ntiles, (double*)tiles, L.pair))) return rc;
     }
-    lq::k_reduce1024<<<(unsigned)(s_end - s_begin), lq::kThreads, 0, c->stream>>>((const double*)tiles, ntiles, out_dev);
-    c->launches++;
-    CK(cudaGetLastError());
-    return LQ_OK;
+    return super_partials(c, L, (const double*)tiles, ntiles, s_end - s_begin, out_dev);
 }
 
 int lq_reduce_sum(lq_ctx* c, const double* vals, int64_t count, double* out) {
@@ -1429,7 +1454,7 @@ int lq_lattice_sum(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t*
             if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
             if ((rc = launch_pow2_tiles(c, f, z, L, 0, ntiles, (double*)tiles))) return rc;
             double* r;
-            if ((rc = reduce_dev(c, (const double*)tiles, ntiles, &r))) return rc;
+            if ((rc = layout_total(c, L, (const double*)tiles, ntiles, &r))) return rc;
             return read_scalar(c, r, sum_out);
         }
         if (L.orb || L.pair) {
@@ -1441,7 +1466,7 @@ int lq_lattice_sum(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t*
             else rc = launch_tiles(c, f, n, z, 0, L.n_units, ntiles, (double*)tiles, true);
             if (rc) return rc;
             double* r;
-            if ((rc = reduce_dev(c, (const double*)tiles, ntiles, &r))) return rc;
+            if ((rc = layout_total(c, L, (const double*)tiles, ntiles, &r))) return rc;
             return read_scalar(c, r, sum_out);
         }
     }

@@ -1265,6 +1265,18 @@ __global__ void __launch_bounds__(kThreads) k_reduce1024(const double* __restric
     if (threadIdx.x == 0) out[g] = s;
 }
 
+// Fixed tree over groups of 256 consecutive values (zero padded): the
+// super-chunk partials of layouts with heavy tiles (FFT form: 2 chains, ~12k
+// points per tile), whose super-chunks hold 256 tiles.
+__global__ void __launch_bounds__(kThreads) k_reduce256(const double* __restrict__ v, int64_t count,
+                                                        double* __restrict__ out) {
+    __shared__ double sh[8];
+    const int64_t i = blockIdx.x * (int64_t)kThreads + threadIdx.x;
+    double s = i < count ? v[i] : 0.0;
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
 // ============================================================ FP64 probe
 __global__ void __launch_bounds__(kThreads) k_fp64_peak(int iters, double seed, double* out) {
     double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,

@@ -2,7 +2,7 @@
 ``torch.distributed`` (NCCL over NVLink) for the single exchange step.
 
 Plain lattice sum: the index range [0, n) is cut into fixed super-chunks of
-LQ_SUPER_TILES tiles (lq_lattice_layout, include/lq.h); rank r of P owns super-chunks
+super_tiles tiles (lq_lattice_layout, include/lq.h); rank r of P owns super-chunks
 [floor(r S / P), floor((r+1) S / P)) and writes their partials into its own
 slots of a zero vector of length S.  One all-reduce(SUM) over disjoint slots
 is exact (x + 0 = x in IEEE arithmetic) whatever order NCCL reduces in, so
