@@ -31,6 +31,7 @@ constexpr int kFftSmem = (kFftPad + (kFftR == 16 ? kFftTwAll : 0)) * 16;   // by
 
 // Build the radix-16 tables from the global table W[k] = e^{-2 pi i k / N}.
 __device__ __forceinline__ void fft_load_twiddles(double2* __restrict__ tw, const double2* __restrict__ W) {
+    if constexpr (kFftR != 16) return;   // radix 8 reads the global table directly
     for (int i = threadIdx.x; i < kFftTw3; i += kFftThreads) {
         const int q = i / 256 + 1, k = i & 255;
         tw[i] = __ldg(W + q * k);
