@@ -38,7 +38,7 @@ int fail(int code, const char* fmt, ...) {
                         __FILE__, __LINE__);                                          \
     } while (0)
 
-enum Buf { B_TAB = 0, B_TILES, B_RED0, B_RED1, B_OUT, B_PROG, B_AUX0, B_AUX1, B_AUX2, B_AUX3, B_PART, B_FAC, B_NODES, B_ORB, B_FFTW, B_FFTH, B_NBUF };
+enum Buf { B_TAB = 0, B_TILES, B_RED0, B_RED1, B_OUT, B_PROG, B_AUX0, B_AUX1, B_AUX2, B_AUX3, B_PART, B_FAC, B_NODES, B_FFTW, B_FFTH, B_NBUF };
 
 }  // namespace
 
