@@ -114,7 +114,12 @@ int lq_points_block(lq_ctx* ctx, int32_t d, uint64_t n, const uint64_t* z_reduce
 
 /* ---- plain lattice sum: replaces the block loop of quad.slr_integrate ----
  * (quad.py:96-104 -> lattice.iter_point_blocks + exprcore.eval_array + np.sum).
- * Returns sum_{i in [i_begin, i_end)} f(frac(i z / n)) (not divided by n).   */
+ * Returns sum_{i in [i_begin, i_end)} f(frac(i z / n)) (not divided by n).
+ * A full range [0, n) uses the fastest exact enumeration lq_lattice_layout
+ * reports (Korobov chains in direct or FFT form, 2^k unit-group levels,
+ * mirror pairs, index tiles); sub-ranges use index tiles.  The choice is a
+ * function of (f, n, z) only; LQ_ORBIT=0, LQ_FFT=0|always, LQ_PAIR=0 in the
+ * environment override it (tests, comparisons).                             */
 int lq_lattice_sum(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_t* z_reduced,
                    uint64_t i_begin, uint64_t i_end, double* sum_out);
 /* Multi-GPU building blocks.  A full-lattice sum is split into units: points
