@@ -60,7 +60,7 @@ def main():
             fl = (FLOPS_PER_PD[cid] * cfg.d + 2) * pts
             kind = pi.kind + ("+jit" if pi.struct.prog.jit and pi.family is None else "")
             print(f"cfg{cid} {kind:10s} n={n} d={cfg.d}: kernel {kms:.3f} ms wall {wall*1e3:.3f} ms "
-                  f"{pts/kms*1e3:.3e} pts/s {pd/kms*1e3:.3e} pd/s {fl/kms*1e-9:.2f} TF  value={s/n!r}")
+                  f"{pts/kms*1e3:.3e} pts/s {pd/kms*1e3:.3e} pd/s {fl/kms*1e-9:.2f} TF-direct-equiv  value={s/n!r}")
     # steady-state rate of the Gaussian family kernel on a large lattice
     cfg = make_config(3)
     f = lq.parse(cfg.text, cfg.d)
