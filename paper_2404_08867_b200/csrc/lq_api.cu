@@ -606,7 +606,24 @@ struct OrbPlan {
     bool zero = true;             // the launch covering unit 0 also adds the point x = 0
     std::vector<uint32_t> G, Alo, Ahi;
     std::vector<uint32_t> apow;   // FFT plans: (a^t mod n, Shoup constant) pairs, t < kFftN
+    std::vector<uint32_t> starts; // FFT plans: first point of every chain (no divisions on the device)
 };
+
+// Chain starts of an FFT plan: starts[u] = G[u / qc] a^(m (u mod qc)) mod n.
+void fill_chain_starts(OrbPlan& p) {
+    const uint64_t n = p.n;
+    uint64_t am = 1;
+    for (int i = 0; i < p.m; ++i) am = am * p.a % n;
+    p.starts.resize(p.units);
+    size_t u = 0;
+    for (size_t cs = 0; cs < p.G.size(); ++cs) {
+        uint64_t t = p.G[cs];
+        for (uint32_t q = 0; q < p.qc; ++q, ++u) {
+            p.starts[u] = (uint32_t)t;
+            t = t * am % n;
+        }
+    }
+}
 
 constexpr uint32_t kOrbMaxCosets = 4096;
 
@@ -679,6 +696,7 @@ std::shared_ptr<const OrbPlan> orbit_plan(uint32_t n, uint32_t a, int m, bool mi
             q->apow[2 * k + 1] = (uint32_t)((t << 32) / n);
             t = t * a % n;
         }
+        fill_chain_starts(*q);
         p = q;
     }
     if (cache.size() > 64) cache.clear();
@@ -748,6 +766,7 @@ std::shared_ptr<const OrbPlan> build_orbit_plan_pow2(int m, uint32_t a_full, int
             p->apow[2 * k + 1] = (uint32_t)((t << 32) / n);
             t = mulm(t, a);
         }
+        fill_chain_starts(*p);
     }
     return p;
 }
@@ -858,10 +877,11 @@ std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, cons
 
 // Device copies of the start tables, cached per context and plan.
 int orbit_tables(lq_ctx* c, const OrbPlan& p, const uint32_t** G, const uint32_t** Alo, const uint32_t** Ahi,
-                 const uint2** apow = nullptr) {
+                 const uint2** apow = nullptr, const uint32_t** starts = nullptr) {
     const size_t nG = p.G.size(), nlo = p.Alo.size(), nhi = p.Ahi.size(), np = p.apow.size();
     const size_t pad = (nG + nlo + nhi) & 1;   // keep apow 8-byte aligned
-    const size_t bytes = 4 * (nG + nlo + nhi + pad + np);
+    const size_t ns = p.starts.size();
+    const size_t bytes = 4 * (nG + nlo + nhi + pad + np + ns);
     auto it = c->orb_tabs.find(p.id);
     if (it == c->orb_tabs.end()) {
         if (c->orb_tabs.size() >= 64) {   // bounded cache: drop everything (plans are rebuilt cheaply)
@@ -876,6 +896,7 @@ int orbit_tables(lq_ctx* c, const OrbPlan& p, const uint32_t** G, const uint32_t
         all.insert(all.end(), p.Ahi.begin(), p.Ahi.end());
         if (pad) all.push_back(0);
         all.insert(all.end(), p.apow.begin(), p.apow.end());
+        all.insert(all.end(), p.starts.begin(), p.starts.end());
         void* d = nullptr;
         CK(cudaMalloc(&d, bytes));
         CK(cudaMemcpy(d, all.data(), bytes, cudaMemcpyHostToDevice));   // once per (context, plan)
@@ -886,6 +907,7 @@ int orbit_tables(lq_ctx* c, const OrbPlan& p, const uint32_t** G, const uint32_t
     *Alo = base + nG;
     *Ahi = base + nG + nlo;
     if (apow) *apow = (const uint2*)(base + nG + nlo + nhi + pad);
+    if (starts) *starts = base + nG + nlo + nhi + pad + np;
     return LQ_OK;
 }
 
@@ -951,9 +973,9 @@ int orbit_prod(lq_ctx* c, const lq::OrbHead& head, const std::vector<double2>& w
 int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t unit0, int64_t ntiles,
                      double* tiles_dev) {
     int rc;
-    const uint32_t *G, *Alo, *Ahi;
+    const uint32_t *G, *Alo, *Ahi, *starts;
     const uint2* apow;
-    if ((rc = orbit_tables(c, p, &G, &Alo, &Ahi, &apow))) return rc;
+    if ((rc = orbit_tables(c, p, &G, &Alo, &Ahi, &apow, &starts))) return rc;
     const int d = f->d;
     const size_t smem = lq::kFftSmem;
     static bool attr = false;
@@ -1005,7 +1027,8 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     CK(cudaGetLastError());
     lq::FftHead h;
     h.n = p.n; h.B = (uint32_t)p.m; h.units = p.units; h.qc = p.qc; h.h = p.h; h.zero = p.zero ? 1 : 0;
-    h.G = G; h.Alo = Alo; h.Ahi = Ahi; h.apow = apow; h.W = (const double2*)W; h.Hc = (const double2*)Hc;
+    h.G = G; h.Alo = Alo; h.Ahi = Ahi; h.apow = apow; h.starts = starts; h.W = (const double2*)W;
+    h.Hc = (const double2*)Hc;
     h.alpha = f->alpha; h.alphaB = f->alpha + bsum; h.K = f->K; h.A = f->A; h.Bc = f->B; h.C0 = f->C0;
     h.kappa = f->kappa; h.pw = f->power;
     const dim3 g((unsigned)ntiles), b(lq::kFftThreads);

@@ -694,6 +694,7 @@ struct FftHead {
     const uint32_t* Alo;               // a^(B q), q < 4096
     const uint32_t* Ahi;               // a^(B 4096 q)
     const uint2* apow;                 // (a^t mod n, floor(a^t 2^32 / n)), t < N
+    const uint32_t* starts;            // first point of every chain
     const double2* W;                  // e^{-2 pi i k / N}
     const double2* Hc;                 // conj(FFT(c zero-padded)) / N, c_j = beta_j / n
     double alpha, alphaB, K, A, Bc, C0, kappa, pw;
@@ -757,16 +758,13 @@ __device__ __forceinline__ double2 hermitian_load(const double2* __restrict__ H,
     return make_double2(h.x, -h.y);
 }
 
-__device__ __forceinline__ uint32_t fft_chain_start(const FftHead& a, uint64_t u) {
-    const uint32_t n = a.n;
-    const uint32_t cs = (uint32_t)(u / a.qc), q = (uint32_t)(u - (uint64_t)cs * a.qc);
-    return mulmod32(mulmod32(a.G[cs], a.Alo[q & 4095u], n), a.Ahi[q >> 12], n);
-}
+// first point of chain u (host-computed table: no 64-bit divisions here)
+__device__ __forceinline__ uint32_t fft_chain_start(const FftHead& a, uint64_t u) { return __ldg(a.starts + u); }
 
 // points of chain u that belong to the enumeration (the last chain of a coset is short)
 __device__ __forceinline__ int fft_chain_valid(const FftHead& a, uint64_t u) {
     if (u >= a.units) return 0;
-    const uint32_t q = (uint32_t)(u % a.qc);
+    const uint32_t q = (uint32_t)u % a.qc;   // units < 2^32
     return (int)min(a.B, a.h - q * a.B);
 }
 
