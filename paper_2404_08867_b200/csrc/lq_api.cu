@@ -970,6 +970,52 @@ int orbit_prod(lq_ctx* c, const lq::OrbHead& head, const std::vector<double2>& w
     return LQ_OK;
 }
 
+// e^x as (c, k), c 2^k = e^x, c in [0.7, 1.5) (long double reduction on the host)
+void split_exp(long double x, double& cm, int32_t& k) {
+    const long double ln2 = 0.693147180559945309417232121458176568L;
+    const long double kk = nearbyintl(x / ln2);
+    cm = (double)expl(x - kk * ln2);
+    k = (int32_t)kk;
+}
+
+// Constants of the one-reduction point/mirror pair (lq::PairFast); false when
+// the family has no such form or some value could leave the normal range.
+// |s1| <= |alpha| + sum |beta|, |s2| <= |alphaB| + sum |beta| (x_j in [0, 1)).
+bool pair_fast_consts(const lq_integrand* f, double bsum, lq::PairFast& q) {
+    if (std::getenv("LQ_PAIRFAST") && std::string(std::getenv("LQ_PAIRFAST")) == "0") return false;
+    const int outer = lin_outer(f->kind);
+    long double babs = 0.0L;
+    for (int j = 0; j < f->d; ++j) babs += fabsl((long double)f->beta[j]);
+    const long double alpha = f->alpha, alphaB = (long double)f->alpha + (long double)bsum;
+    const long double smax = std::max(fabsl(alpha), fabsl(alphaB)) + babs;
+    const long double D = alpha + alphaB;
+    q = lq::PairFast{};
+    if (outer == lq::OUT_SINCOS) {
+        if (!std::isfinite((double)smax)) return false;
+        const long double sD = sinl(D), cD = cosl(D), A = f->A, B = f->B;
+        q.ym = 1.0; q.ya = f->alpha; q.post = 1.0;
+        q.c0 = (double)(A + B * sD - A * cD);
+        q.c1 = (double)(B + A * sD + B * cD);
+        q.c2 = (double)(2.0L * (long double)f->C0);
+        return true;
+    }
+    if (outer == lq::OUT_EXP) {
+        if (!(smax <= 700.0L)) return false;
+        q.ym = 1.0; q.ya = f->alpha; q.post = f->K;
+        split_exp(D, q.c0, q.k0);
+        return true;
+    }
+    if (outer == lq::OUT_EXPABS) {
+        const long double lam = -(long double)f->kappa;
+        if (!(lam >= 0.0L) || !(lam * smax <= 700.0L)) return false;
+        q.ym = (double)lam; q.ya = (double)(lam * alpha); q.E = (double)(lam * D); q.post = f->K;
+        split_exp(-lam * D, q.c0, q.k0);
+        split_exp(lam * D, q.c1, q.k1);
+        return true;
+    }
+    return false;
+}
+
 int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t unit0, int64_t ntiles,
                      double* tiles_dev) {
     int rc;
@@ -981,10 +1027,14 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     static bool attr = false;
     if (!attr) {
         CK(cudaFuncSetAttribute((const void*)lq::k_fft_coeffs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft<lq::OUT_EXP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft<lq::OUT_SINCOS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft<lq::OUT_EXPABS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft<lq::OUT_POW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const void* fns[] = {(const void*)lq::k_orbit_fft<lq::OUT_EXP, false>,
+                             (const void*)lq::k_orbit_fft<lq::OUT_SINCOS, false>,
+                             (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, false>,
+                             (const void*)lq::k_orbit_fft<lq::OUT_POW, false>,
+                             (const void*)lq::k_orbit_fft<lq::OUT_EXP, true>,
+                             (const void*)lq::k_orbit_fft<lq::OUT_SINCOS, true>,
+                             (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, true>};
+        for (const void* fn : fns) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute((const void*)lq::k_fft_coeffs_pm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft_quad<lq::OUT_EXP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft_quad<lq::OUT_SINCOS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1043,13 +1093,15 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
         CK(cudaGetLastError());
         return LQ_OK;
     }
+    const int outer = lin_outer(f->kind);
+    const bool fast = pair_fast_consts(f, bsum, h.pf);
     t_begin(c);
-    switch (lin_outer(f->kind)) {
-        case lq::OUT_EXP: lq::k_orbit_fft<lq::OUT_EXP><<<g, b, smem, c->stream>>>(h, unit0, tiles_dev); break;
-        case lq::OUT_SINCOS: lq::k_orbit_fft<lq::OUT_SINCOS><<<g, b, smem, c->stream>>>(h, unit0, tiles_dev); break;
-        case lq::OUT_EXPABS: lq::k_orbit_fft<lq::OUT_EXPABS><<<g, b, smem, c->stream>>>(h, unit0, tiles_dev); break;
-        default: lq::k_orbit_fft<lq::OUT_POW><<<g, b, smem, c->stream>>>(h, unit0, tiles_dev); break;
-    }
+#define LQ_FFT_LIN(O, F) lq::k_orbit_fft<O, F><<<g, b, smem, c->stream>>>(h, unit0, tiles_dev)
+    if (outer == lq::OUT_EXP) { if (fast) LQ_FFT_LIN(lq::OUT_EXP, true); else LQ_FFT_LIN(lq::OUT_EXP, false); }
+    else if (outer == lq::OUT_SINCOS) { if (fast) LQ_FFT_LIN(lq::OUT_SINCOS, true); else LQ_FFT_LIN(lq::OUT_SINCOS, false); }
+    else if (outer == lq::OUT_EXPABS) { if (fast) LQ_FFT_LIN(lq::OUT_EXPABS, true); else LQ_FFT_LIN(lq::OUT_EXPABS, false); }
+    else LQ_FFT_LIN(lq::OUT_POW, false);
+#undef LQ_FFT_LIN
     t_end(c);
     CK(cudaGetLastError());
     return LQ_OK;

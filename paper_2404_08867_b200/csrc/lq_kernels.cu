@@ -686,6 +686,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_orbit_prod(const __grid_constan
 // B linear forms of a chain (overlap-save), O(log N) FP64 work per point
 // instead of O(d).  Two chains ride in one complex FFT
 // (real and imaginary parts); c is real, so their correlations separate.
+// A point and its mirror from one range reduction.  With
+// s1 = alpha + l, s2 = alphaB - l = D - s1 and y = ym l + ya:
+//   EXP     e^s1 + e^s2 = e^y + e^D e^-y                       (y = s1)
+//   EXPABS  e^-|y| + e^-|E - y|, y = lambda s1, E = lambda D   (kappa = -lambda <= 0)
+//   SINCOS  2 C0 + A' sin y + B' cos y                         (y = s1)
+// e^z = 2^k e^r and e^-z = 2^-k e^-r share r, r^2 and the even/odd halves of
+// one Taylor polynomial; the constants are split on the host as c 2^k.  The
+// host enables it only where every value stays a normal double (|y| <= 700).
+struct PairFast {
+    double ym, ya, E;
+    double c0, c1, c2;   // EXP: e^D; EXPABS: e^-E, e^E; SINCOS: A', B', 2 C0
+    double post;         // multiplier after the sum (K; 1 for SINCOS)
+    int32_t k0, k1;      // binary exponents of c0, c1
+};
+
 struct FftHead {
     uint32_t n, B;                     // modulus, chain length N - d + 1
     uint64_t units;                    // chains
@@ -698,8 +713,52 @@ struct FftHead {
     const double2* W;                  // e^{-2 pi i k / N}
     const double2* Hc;                 // conj(FFT(c zero-padded)) / N, c_j = beta_j / n
     double alpha, alphaB, K, A, Bc, C0, kappa, pw;
+    PairFast pf;
     int32_t zero;                      // unit 0 also adds the point x = 0
 };
+
+// v 2^j by exponent arithmetic (v 2^j must be a normal double)
+__device__ __forceinline__ double scale2(double v, int j) {
+    return __hiloint2double(__double2hiint(v) + (j << 20), __double2loint(v));
+}
+
+// f(s1) + f(s2) without the factor q.post (see PairFast)
+template <int OUTER>
+__device__ __forceinline__ double pair_fast(double l, const PairFast& q) {
+    const double y = fma(l, q.ym, q.ya);
+    if constexpr (OUTER == OUT_SINCOS) {
+        double sn, cs;
+        sincos(y, &sn, &cs);
+        return fma(q.c0, sn, fma(q.c1, cs, q.c2));
+    } else {
+        const double z = OUTER == OUT_EXPABS ? -fabs(y) : y;
+        const double t = fma(z, 1.4426950408889634, 6755399441055744.0);   // 1.5 2^52: round to integer
+        const int k = __double2loint(t);
+        const double kf = t - 6755399441055744.0;
+        double r = fma(kf, -6.93147180559945286e-01, z);                    // z - k ln2, two-part ln2
+        r = fma(kf, -2.319046813846299558e-17, r);
+        const double r2 = r * r;
+        double e = fma(r2, 2.08767569878681e-09, 2.755731922398589e-07);   // sum r^2i / (2i)!, i <= 6
+        e = fma(r2, e, 2.48015873015873e-05);
+        e = fma(r2, e, 0.001388888888888889);
+        e = fma(r2, e, 0.041666666666666664);
+        e = fma(r2, e, 0.5);
+        e = fma(r2, e, 1.0);
+        double o = fma(r2, 2.505210838544172e-08, 2.7557319223985893e-06);   // sum r^2i / (2i + 1)!, i <= 5
+        o = fma(r2, o, 0.0001984126984126984);
+        o = fma(r2, o, 0.008333333333333333);
+        o = fma(r2, o, 0.16666666666666666);
+        o = fma(r2, o, 1.0);
+        const double p = fma(r, o, e), m = fma(-r, o, e);                    // e^r, e^-r
+        const double f1 = scale2(p, k);
+        if constexpr (OUTER == OUT_EXP) {
+            return f1 + scale2(m * q.c0, q.k0 - k);
+        } else {
+            const bool s1 = y >= 0.0, s2 = y <= q.E, same = s1 == s2;
+            return f1 + scale2((same ? m : p) * (s2 ? q.c0 : q.c1), (s2 ? q.k0 : q.k1) + (same ? -k : k));
+        }
+    }
+}
 
 __global__ void __launch_bounds__(kThreads) k_fft_twiddles(double2* __restrict__ W) {
     for (int k = blockIdx.x * kThreads + threadIdx.x; k < kFftN; k += gridDim.x * kThreads) {
@@ -786,7 +845,7 @@ __device__ __forceinline__ double block_sum_n(double v, double* sh /* >= NT / 32
 }
 
 // One CTA = two chains (units 2b, 2b + 1 after unit0); tile_out[b] = their sum.
-template <int OUTER>
+template <int OUTER, bool FAST>
 __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_constant__ FftHead a, uint64_t unit0,
                                                                double* __restrict__ tile_out) {
     constexpr int R = kFftR;
@@ -833,10 +892,16 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
         const double2 y = buf[fpad(k)];             // conj of the correlation: (L0, -L1)
         // inlined (no call): nothing else is live here
         const double l0 = y.x, l1 = -y.y;
-        const double f00 = outer_val<OUTER>(l0 + prm.alpha, prm), f01 = outer_val<OUTER>(a.alphaB - l0, prm);
-        const double f10 = outer_val<OUTER>(l1 + prm.alpha, prm), f11 = outer_val<OUTER>(a.alphaB - l1, prm);
-        s += (k < v0 ? f00 + f01 : 0.0) + (k < v1 ? f10 + f11 : 0.0);
+        if constexpr (FAST) {
+            const double g0 = pair_fast<OUTER>(l0, a.pf), g1 = pair_fast<OUTER>(l1, a.pf);
+            s += (k < v0 ? g0 : 0.0) + (k < v1 ? g1 : 0.0);
+        } else {
+            const double f00 = outer_val<OUTER>(l0 + prm.alpha, prm), f01 = outer_val<OUTER>(a.alphaB - l0, prm);
+            const double f10 = outer_val<OUTER>(l1 + prm.alpha, prm), f11 = outer_val<OUTER>(a.alphaB - l1, prm);
+            s += (k < v0 ? f00 + f01 : 0.0) + (k < v1 ? f10 + f11 : 0.0);
+        }
     }
+    if constexpr (FAST) s *= a.pf.post;
     if (u0 == 0 && a.zero && threadIdx.x == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
     s = block_sum_n<kFftThreads>(s, sh);
     if (threadIdx.x == 0) tile_out[blockIdx.x] = s;

@@ -85,3 +85,40 @@ def test_fft_gaussian_large(env, monkeypatch):
     got = _sums(engine, N, pi, n, rule.z_reduced_array(), monkeypatch)
     fft, direct = got[N.LAYOUT_ORBIT_FFT], got[N.LAYOUT_ORBIT]
     assert math.isclose(fft, direct, rel_tol=1e-12), (fft, direct)
+
+
+def _pair_text(family, d, rng, scale, offset):
+    c = rng.uniform(0, 1, d)
+    c = c * (scale / c.sum())
+    w = rng.uniform(0, 1, d)
+    if family == "expabs":
+        return "exp(-abs(" + " + ".join(f"{float(c[j])!r}*(x[{j + 1}] - {float(w[j])!r})" for j in range(d)) + "))"
+    sgn = np.where(rng.uniform(size=d) < 0.5, -1.0, 1.0)
+    if family == "exp":
+        return f"exp({offset!r} + " + " + ".join(f"{float(sgn[j] * c[j])!r}*x[{j + 1}]" for j in range(d)) + ")"
+    return "2.0 + 0.5*cos(1.3 + " + " + ".join(f"{float(sgn[j] * c[j])!r}*x[{j + 1}]" for j in range(d)) + ")"
+
+
+@pytest.mark.parametrize("family,scale,offset", [("expabs", 10.0, 0), ("expabs", 0.01, 0), ("expabs", 350.0, 0),
+                                                 ("expabs", 800.0, 0), ("exp", 3.0, 0.25), ("exp", 600.0, 0.25),
+                                                 ("exp", 100.0, -650.0), ("sincos", 9.0, 0), ("sincos", 400.0, 0)])
+def test_fft_pair_fast(env, family, scale, offset, monkeypatch):
+    # the one-reduction point/mirror outer (PairFast) against
+    # the two-exp form and the oracle; bounds past the normal range (|y| <= 700:
+    # expabs 800, exp offset -650) fall back to the two-exp form
+    lq, N, engine = env
+    from oracle import np_oracle
+    n, d, a = 100003, 150, 2
+    rng = np.random.default_rng(zlib.crc32(f"pair/{family}/{scale}".encode()))
+    f = lq.parse(_pair_text(family, d, rng, scale, offset), d)
+    rule = lq.korobov_vector(a, n, d)
+    pi = engine.plain_integrand(f, d)
+    z = rule.z_reduced_array()
+    monkeypatch.setenv("LQ_FFT", "always")
+    assert N.lattice_layout(pi.struct, n, z).mode == N.LAYOUT_ORBIT_FFT
+    fast = engine.lattice_sum(pi, n, z)
+    monkeypatch.setenv("LQ_PAIRFAST", "0")
+    slow = engine.lattice_sum(pi, n, z)
+    assert math.isclose(fast, slow, rel_tol=1e-13, abs_tol=1e-300), (fast, slow)
+    ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
+    assert math.isclose(fast, ref, rel_tol=REL, abs_tol=1e-300), (fast, ref)
