@@ -22,11 +22,12 @@ constexpr int kFftLogR = kFftR == 16 ? 4 : 3;
 constexpr int kFftPad = kFftN + kFftN / kFftR;   // padded shared-memory length (double2)
 // Radix-16 twiddle tables in shared memory, laid out [q][k] so that the lanes
 // of a warp (consecutive k) read consecutive entries:
-//   pass Ns = 256: L3[q][k] = W^(q k),    H3[q][k] = W^(4 q k),   k < 256
-//   pass Ns = 16:  L2[q][k] = W^(16 q k), H2[q][k] = W^(64 q k),  k < 16
-// (q = 1..3; W = e^{-2 pi i / N}); W^(r s) = L[r mod 4] H[r div 4].
-constexpr int kFftTw3 = 3 * 256, kFftTw2 = 3 * 16;
-constexpr int kFftTwAll = 2 * kFftTw3 + 2 * kFftTw2;
+//   pass Ns = 256: L3[q][k] = W^(q k), H3[q][k] = W^(4 q k), q = 1..3, k < 256;
+//                  W^(r k) = L3[r mod 4] H3[r div 4] (6 loads, 9 products)
+//   pass Ns = 16:  T2[r][k] = W^(16 r k), r = 1..15, k < 16 (all of them)
+// (W = e^{-2 pi i / N}).
+constexpr int kFftTw3 = 3 * 256, kFftTw2 = 15 * 16;
+constexpr int kFftTwAll = 2 * kFftTw3 + kFftTw2;
 constexpr int kFftSmem = (kFftPad + (kFftR == 16 ? kFftTwAll : 0)) * 16;   // bytes per CTA
 
 // Build the radix-16 tables from the global table W[k] = e^{-2 pi i k / N}.
@@ -38,9 +39,8 @@ __device__ __forceinline__ void fft_load_twiddles(double2* __restrict__ tw, cons
         tw[kFftTw3 + i] = __ldg(W + ((4 * q * k) & (kFftN - 1)));
     }
     for (int i = threadIdx.x; i < kFftTw2; i += kFftThreads) {
-        const int q = i / 16 + 1, k = i & 15;
-        tw[2 * kFftTw3 + i] = __ldg(W + 16 * q * k);
-        tw[2 * kFftTw3 + kFftTw2 + i] = __ldg(W + ((64 * q * k) & (kFftN - 1)));
+        const int r = i / 16 + 1, k = i & 15;
+        tw[2 * kFftTw3 + i] = __ldg(W + ((16 * r * k) & (kFftN - 1)));
     }
 }
 
@@ -129,11 +129,15 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[kFftR], double2* __restric
     const int k = j & (Ns - 1);
     if (Ns > 1) {
         const int step = k * (kFftN / (Ns * kFftR));
-        if constexpr (kFftR == 16) {
+        if (kFftR == 16 && Ns == 16) {
+            const double2* __restrict__ T = W + 2 * kFftTw3;
+            #pragma unroll
+            for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], T[(r - 1) * 16 + k]);
+        } else if constexpr (kFftR == 16) {
             // W^(r step), r = r0 + 4 r1, as W^(r0 step) W^(4 r1 step): six
             // conflict-free shared-table loads instead of fifteen global ones
-            const double2* __restrict__ L = Ns == 256 ? W : W + 2 * kFftTw3;
-            const double2* __restrict__ H = Ns == 256 ? W + kFftTw3 : W + 2 * kFftTw3 + kFftTw2;
+            const double2* __restrict__ L = W;
+            const double2* __restrict__ H = W + kFftTw3;
             double2 lo[4], hi[4];
             #pragma unroll
             for (int q = 1; q < 4; ++q) {
