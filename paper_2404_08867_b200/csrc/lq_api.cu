@@ -970,6 +970,11 @@ int orbit_prod(lq_ctx* c, const lq::OrbHead& head, const std::vector<double2>& w
     return LQ_OK;
 }
 
+int64_t kFftTilesPerCta = [] {
+    const char* e = std::getenv("LQ_FFT_PER_CTA");
+    return e ? std::max<int64_t>(1, std::atoll(e)) : 8;
+}();
+
 // e^x as (c, k), c 2^k = e^x, c in [0.7, 1.5) (long double reduction on the host)
 void split_exp(long double x, double& cm, int32_t& k) {
     const long double ln2 = 0.693147180559945309417232121458176568L;
@@ -1081,14 +1086,17 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     h.Hc = (const double2*)Hc;
     h.alpha = f->alpha; h.alphaB = f->alpha + bsum; h.K = f->K; h.A = f->A; h.Bc = f->B; h.C0 = f->C0;
     h.kappa = f->kappa; h.pw = f->power;
-    const dim3 g((unsigned)ntiles), b(lq::kFftThreads);
+    // several tiles per CTA once there are many waves: the twiddle fill is
+    // paid once per CTA
+    const int per = (int)std::max<int64_t>(1, std::min<int64_t>(kFftTilesPerCta, ntiles / (2 * 148 * 16)));
+    const dim3 g((unsigned)((ntiles + per - 1) / per)), b(lq::kFftThreads);
     if (quad) {
         const double2* Hm = (const double2*)Hc + lq::kFftN;
         t_begin(c);
         if (quad_outer_of(f->kind) == lq::OUT_SINCOS)
-            lq::k_orbit_fft_quad<lq::OUT_SINCOS><<<g, b, smem, c->stream>>>(h, Hm, unit0, tiles_dev);
+            lq::k_orbit_fft_quad<lq::OUT_SINCOS><<<g, b, smem, c->stream>>>(h, Hm, unit0, ntiles, per, tiles_dev);
         else
-            lq::k_orbit_fft_quad<lq::OUT_EXP><<<g, b, smem, c->stream>>>(h, Hm, unit0, tiles_dev);
+            lq::k_orbit_fft_quad<lq::OUT_EXP><<<g, b, smem, c->stream>>>(h, Hm, unit0, ntiles, per, tiles_dev);
         t_end(c);
         CK(cudaGetLastError());
         return LQ_OK;
@@ -1096,7 +1104,7 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     const int outer = lin_outer(f->kind);
     const bool fast = pair_fast_consts(f, bsum, h.pf);
     t_begin(c);
-#define LQ_FFT_LIN(O, F) lq::k_orbit_fft<O, F><<<g, b, smem, c->stream>>>(h, unit0, tiles_dev)
+#define LQ_FFT_LIN(O, F) lq::k_orbit_fft<O, F><<<g, b, smem, c->stream>>>(h, unit0, ntiles, per, tiles_dev)
     if (outer == lq::OUT_EXP) { if (fast) LQ_FFT_LIN(lq::OUT_EXP, true); else LQ_FFT_LIN(lq::OUT_EXP, false); }
     else if (outer == lq::OUT_SINCOS) { if (fast) LQ_FFT_LIN(lq::OUT_SINCOS, true); else LQ_FFT_LIN(lq::OUT_SINCOS, false); }
     else if (outer == lq::OUT_EXPABS) { if (fast) LQ_FFT_LIN(lq::OUT_EXPABS, true); else LQ_FFT_LIN(lq::OUT_EXPABS, false); }

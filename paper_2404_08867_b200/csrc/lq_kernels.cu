@@ -844,9 +844,12 @@ __device__ __forceinline__ double block_sum_n(double v, double* sh /* >= NT / 32
     return v;
 }
 
-// One CTA = two chains (units 2b, 2b + 1 after unit0); tile_out[b] = their sum.
+// Tile b = two chains (units 2b, 2b + 1 after unit0); tile_out[b] = their sum.
+// A CTA runs tiles per_cta blockIdx.x .. + per_cta - 1 (< ntiles), so the
+// twiddle tables are filled once per per_cta tiles.
 template <int OUTER, bool FAST>
 __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_constant__ FftHead a, uint64_t unit0,
+                                                               int64_t ntiles, int per_cta,
                                                                double* __restrict__ tile_out) {
     constexpr int R = kFftR;
     extern __shared__ double2 buf[];   // kFftPad, then the twiddle tables
@@ -855,7 +858,11 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
     fft_load_twiddles(tw, a.W);          // visible after the first pass's barrier
     const double2* Wt = kFftR == 16 ? tw : a.W;
     const uint32_t n = a.n;
-    const uint64_t u0 = unit0 + 2ull * blockIdx.x, u1 = u0 + 1;
+    const int64_t b0 = (int64_t)blockIdx.x * per_cta;
+    const int64_t b1 = min(b0 + per_cta, ntiles);
+    #pragma unroll 1
+    for (int64_t tb = b0; tb < b1; ++tb) {
+    const uint64_t u0 = unit0 + 2ull * (uint64_t)tb, u1 = u0 + 1;
     const uint32_t s0 = u0 < a.units ? fft_chain_start(a, u0) : 0u;
     const uint32_t s1 = u1 < a.units ? fft_chain_start(a, u1) : 0u;
     // residues of both chains straight into the registers of the first pass:
@@ -904,7 +911,8 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
     if constexpr (FAST) s *= a.pf.post;
     if (u0 == 0 && a.zero && threadIdx.x == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
     s = block_sum_n<kFftThreads>(s, sh);
-    if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
+    if (threadIdx.x == 0) tile_out[tb] = s;
+    }
 }
 
 // Gaussian family in FFT form: one chain per CTA.  The centred coordinates
@@ -916,7 +924,8 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
 template <int OUTER>
 __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft_quad(const __grid_constant__ FftHead a,
                                                                     const double2* __restrict__ Hm,
-                                                                    uint64_t unit0, double* __restrict__ tile_out) {
+                                                                    uint64_t unit0, int64_t ntiles, int per_cta,
+                                                                    double* __restrict__ tile_out) {
     constexpr int R = kFftR;
     extern __shared__ double2 buf[];   // kFftPad, then the twiddle tables
     __shared__ double sh[32];
@@ -924,7 +933,11 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft_quad(const __grid_
     fft_load_twiddles(tw, a.W);
     const double2* Wt = kFftR == 16 ? tw : a.W;
     const uint32_t n = a.n;
-    const uint64_t u0 = unit0 + blockIdx.x;
+    const int64_t b0 = (int64_t)blockIdx.x * per_cta;
+    const int64_t b1 = min(b0 + per_cta, ntiles);
+    #pragma unroll 1
+    for (int64_t tb = b0; tb < b1; ++tb) {
+    const uint64_t u0 = unit0 + (uint64_t)tb;
     const uint32_t s0 = u0 < a.units ? fft_chain_start(a, u0) : 0u;
     const double inv_n = 1.0 / (double)n;
     double2 v[R];
@@ -955,7 +968,8 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft_quad(const __grid_
     }
     if (u0 == 0 && a.zero && threadIdx.x == 0) s += quad_outer<OUTER>(0.0, prm);   // point 0
     s = block_sum_n<kFftThreads>(s, sh);
-    if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
+    if (threadIdx.x == 0) tile_out[tb] = s;
+    }
 }
 
 // ============================================================ generic bytecode
