@@ -888,27 +888,39 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
         const double2 y = cmul(v[r], hermitian_load(a.Hc, threadIdx.x + r * kFftThreads));
         v[r] = make_double2(y.x, -y.y);
     }
+    const LinParams prm{a.alpha, 1.0, a.K, a.A, a.Bc, a.C0, a.kappa, a.pw};
+    double s = 0.0;
+    if constexpr (FAST) {
+        // inverse transform with its outputs left in registers (positions
+        // j + (N/R) r, natural order): the lean pair outer runs on them
+        // directly, skipping warps whose positions are all past the chains
+        fft4096_regs<false>(v, buf, Wt);
+        const int v0 = fft_chain_valid(a, u0), v1 = fft_chain_valid(a, u1);
+        const int vmax = max(v0, v1), wbase = threadIdx.x & ~31;
+        #pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (wbase + r * kFftThreads < vmax) {
+                const int k = threadIdx.x + r * kFftThreads;
+                const double g0 = pair_fast<OUTER>(v[r].x, a.pf), g1 = pair_fast<OUTER>(-v[r].y, a.pf);
+                s += (k < v0 ? g0 : 0.0) + (k < v1 ? g1 : 0.0);
+            }
+        }
+        s *= a.pf.post;
+    } else {
     // inverse transform; its last pass writes the correlations to shared memory
     // so the out-of-line outer function runs with no transform state live
     fft4096_regs<true>(v, buf, Wt);
-    const LinParams prm{a.alpha, 1.0, a.K, a.A, a.Bc, a.C0, a.kappa, a.pw};
     const int v0 = fft_chain_valid(a, u0), v1 = fft_chain_valid(a, u1);   // recomputed: not live across the FFTs
-    double s = 0.0;
     #pragma unroll 1
     for (int k = threadIdx.x; k < v0 || k < v1; k += kFftThreads) {
         const double2 y = buf[fpad(k)];             // conj of the correlation: (L0, -L1)
         // inlined (no call): nothing else is live here
         const double l0 = y.x, l1 = -y.y;
-        if constexpr (FAST) {
-            const double g0 = pair_fast<OUTER>(l0, a.pf), g1 = pair_fast<OUTER>(l1, a.pf);
-            s += (k < v0 ? g0 : 0.0) + (k < v1 ? g1 : 0.0);
-        } else {
-            const double f00 = outer_val<OUTER>(l0 + prm.alpha, prm), f01 = outer_val<OUTER>(a.alphaB - l0, prm);
-            const double f10 = outer_val<OUTER>(l1 + prm.alpha, prm), f11 = outer_val<OUTER>(a.alphaB - l1, prm);
-            s += (k < v0 ? f00 + f01 : 0.0) + (k < v1 ? f10 + f11 : 0.0);
-        }
+        const double f00 = outer_val<OUTER>(l0 + prm.alpha, prm), f01 = outer_val<OUTER>(a.alphaB - l0, prm);
+        const double f10 = outer_val<OUTER>(l1 + prm.alpha, prm), f11 = outer_val<OUTER>(a.alphaB - l1, prm);
+        s += (k < v0 ? f00 + f01 : 0.0) + (k < v1 ? f10 + f11 : 0.0);
     }
-    if constexpr (FAST) s *= a.pf.post;
+    }
     if (u0 == 0 && a.zero && threadIdx.x == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
     s = block_sum_n<kFftThreads>(s, sh);
     if (threadIdx.x == 0) tile_out[tb] = s;
@@ -956,15 +968,18 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft_quad(const __grid_
         const double2 z = cadd(cmul(x, __ldg(a.Hc + m)), cmul(make_double2(xr.x, -xr.y), __ldg(Hm + m)));
         v[r] = make_double2(z.x, -z.y);     // conjugated: the forward transform inverts it
     }
-    fft4096_regs<true>(v, buf, Wt);        // (first pass stores only after its barrier)
+    fft4096_regs<false>(v, buf, Wt);       // (first pass stores only after its barrier); outputs stay in v
     const LinParams prm{a.alpha, 1.0, a.K, a.A, a.Bc, a.C0, a.kappa, a.pw};
-    const int v0 = fft_chain_valid(a, u0);
+    const int v0 = fft_chain_valid(a, u0), wbase = threadIdx.x & ~31;
     double s = 0.0;
-    #pragma unroll 1
-    for (int k = threadIdx.x; k < v0; k += kFftThreads) {
-        const double2 y = buf[fpad(k)];    // conj: (odd, -even)
-        const double t = a.alphaB - y.y;
-        s += outer_val<OUTER>(t + y.x, prm) + outer_val<OUTER>(t - y.x, prm);
+    #pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if (wbase + r * kFftThreads < v0) {
+            const double2 y = v[r];             // conj: (odd, -even) at position j + (N/R) r
+            const double t = a.alphaB - y.y;
+            const double g = outer_val<OUTER>(t + y.x, prm) + outer_val<OUTER>(t - y.x, prm);
+            s += threadIdx.x + r * kFftThreads < v0 ? g : 0.0;
+        }
     }
     if (u0 == 0 && a.zero && threadIdx.x == 0) s += quad_outer<OUTER>(0.0, prm);   // point 0
     s = block_sum_n<kFftThreads>(s, sh);
