@@ -80,23 +80,58 @@ __device__ __forceinline__ void dft8(double2 (&v)[8]) {
     }
 }
 
-// forward 16-point DFT (4 x 4): output k = q + 4 p in v[4 q + p]
+// forward 16-point DFT (4 x 4): output k = q + 4 p in v[4 q + p].  The
+// second-stage twiddles are fused into the butterflies (FMA "tangent" form):
+// W^2 x = c2 (x.x + x.y, x.y - x.x) and W^1 t = c1 (t.x + tan t.y, t.y - tan t.x)
+// are applied as the multiplicand of the butterfly's FMA, and a1 +- a3 =
+// W^q (x1 +- W^2q x3): 148 FP64 instructions instead of 160.
 __device__ __forceinline__ void dft16(double2 (&v)[16]) {
     #pragma unroll
     for (int n1 = 0; n1 < 4; ++n1) dft4(v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12]);
-    const double c1 = 0.92387953251128674, s1 = 0.38268343236508978;   // cos, sin(pi/8)
+    const double c1 = 0.92387953251128674, t1 = 0.41421356237309503;   // cos, tan(pi/8)
     const double c2 = 0.70710678118654757;                               // cos(pi/4)
-    v[1 + 4 * 1] = cmul(v[1 + 4 * 1], make_double2(c1, -s1));   // W16^1
-    v[1 + 4 * 2] = cmul(v[1 + 4 * 2], make_double2(c2, -c2));   // W16^2
-    v[1 + 4 * 3] = cmul(v[1 + 4 * 3], make_double2(s1, -c1));   // W16^3
-    v[2 + 4 * 1] = cmul(v[2 + 4 * 1], make_double2(c2, -c2));   // W16^2
-    v[2 + 4 * 2] = cmul_mi(v[2 + 4 * 2]);                       // W16^4
-    v[2 + 4 * 3] = cmul(v[2 + 4 * 3], make_double2(-c2, -c2));  // W16^6
-    v[3 + 4 * 1] = cmul(v[3 + 4 * 1], make_double2(s1, -c1));   // W16^3
-    v[3 + 4 * 2] = cmul(v[3 + 4 * 2], make_double2(-c2, -c2));  // W16^6
-    v[3 + 4 * 3] = cmul(v[3 + 4 * 3], make_double2(-c1, s1));   // W16^9
-    #pragma unroll
-    for (int q = 0; q < 4; ++q) dft4(v[4 * q + 0], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    dft4(v[0], v[1], v[2], v[3]);                                        // q = 0: no twiddles
+    {   // q = 2: W^2, W^4 = -i, W^6
+        const double2 a0 = v[8], x1 = v[9], x2 = v[10], x3 = v[11];
+        const double s02x = a0.x + x2.y, s02y = a0.y - x2.x, d02x = a0.x - x2.y, d02y = a0.y + x2.x;
+        const double u1 = x1.x + x1.y, w1 = x1.y - x1.x;                // W^2 x1 = c2 (u1, w1)
+        const double u3 = x3.y - x3.x, m3 = x3.x + x3.y;                // W^6 x3 = c2 (u3, -m3)
+        const double Sx = u1 + u3, Sy = w1 - m3, Dx = u1 - u3, Dy = w1 + m3;
+        v[8] = make_double2(fma(c2, Sx, s02x), fma(c2, Sy, s02y));
+        v[10] = make_double2(fma(-c2, Sx, s02x), fma(-c2, Sy, s02y));
+        v[9] = make_double2(fma(c2, Dy, d02x), fma(-c2, Dx, d02y));
+        v[11] = make_double2(fma(-c2, Dy, d02x), fma(c2, Dx, d02y));
+    }
+    {   // q = 1: W^1, W^2, W^3 = W^1 W^2
+        const double2 a0 = v[4], x1 = v[5], x2 = v[6], x3 = v[7];
+        const double u2 = x2.x + x2.y, w2 = x2.y - x2.x;
+        const double s02x = fma(c2, u2, a0.x), s02y = fma(c2, w2, a0.y);
+        const double d02x = fma(-c2, u2, a0.x), d02y = fma(-c2, w2, a0.y);
+        const double u3 = x3.x + x3.y, w3 = x3.y - x3.x;
+        const double tpx = fma(c2, u3, x1.x), tpy = fma(c2, w3, x1.y);    // x1 + W^2 x3
+        const double tmx = fma(-c2, u3, x1.x), tmy = fma(-c2, w3, x1.y);  // x1 - W^2 x3
+        const double gx = fma(t1, tpy, tpx), gy = fma(-t1, tpx, tpy);     // W^1 tp / c1
+        const double hx = fma(t1, tmy, tmx), hy = fma(-t1, tmx, tmy);     // W^1 tm / c1
+        v[4] = make_double2(fma(c1, gx, s02x), fma(c1, gy, s02y));
+        v[6] = make_double2(fma(-c1, gx, s02x), fma(-c1, gy, s02y));
+        v[5] = make_double2(fma(c1, hy, d02x), fma(-c1, hx, d02y));
+        v[7] = make_double2(fma(-c1, hy, d02x), fma(c1, hx, d02y));
+    }
+    {   // q = 3: W^3, W^6, W^9 = W^3 W^6
+        const double2 a0 = v[12], x1 = v[13], x2 = v[14], x3 = v[15];
+        const double u2 = x2.y - x2.x, w2 = -(x2.x + x2.y);            // W^6 x2 = c2 (u2, w2)
+        const double s02x = fma(c2, u2, a0.x), s02y = fma(c2, w2, a0.y);
+        const double d02x = fma(-c2, u2, a0.x), d02y = fma(-c2, w2, a0.y);
+        const double u3 = x3.y - x3.x, w3 = -(x3.x + x3.y);
+        const double tpx = fma(c2, u3, x1.x), tpy = fma(c2, w3, x1.y);    // x1 + W^6 x3
+        const double tmx = fma(-c2, u3, x1.x), tmy = fma(-c2, w3, x1.y);
+        const double gx = fma(t1, tpx, tpy), gy = fma(t1, tpy, -tpx);     // W^3 tp / c1
+        const double hx = fma(t1, tmx, tmy), hy = fma(t1, tmy, -tmx);
+        v[12] = make_double2(fma(c1, gx, s02x), fma(c1, gy, s02y));
+        v[14] = make_double2(fma(-c1, gx, s02x), fma(-c1, gy, s02y));
+        v[13] = make_double2(fma(c1, hy, d02x), fma(-c1, hx, d02y));
+        v[15] = make_double2(fma(-c1, hy, d02x), fma(c1, hx, d02y));
+    }
 }
 
 template <int R>
