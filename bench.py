@@ -291,7 +291,6 @@ def main():
     conv = conv_flops / (avg_kern * 1e-3) / 1e12
     executed = exec_flops / (avg_kern * 1e-3) / 1e12
 
-    # e2e: the public drop-in API (host lowering, parameter H2D, kernel, result D2H)
     # e2e: the public drop-in API (host lowering, parameter upload, kernel,
     # exchange, result D2H); multi-GPU through distributed.slr_integrate
     from paper_2404_08867_b200 import distributed
@@ -311,7 +310,7 @@ def main():
     # H2D per call: the kernel-parameter struct (coefficient table + header);
     # the orbit start tables are uploaded once per context and plan
     if lay.mode == N.LAYOUT_ORBIT_FFT:
-        h2d = 8 * d + 136 + 16 + 24                          # coefficients + FftHead + launch arguments
+        h2d = 8 * d + 216 + 32                               # coefficients + FftHead + launch arguments
     elif lay.mode == N.LAYOUT_ORBIT:
         h2d = 8 * (-(-d // ORB_M) * ORB_M) + 152 + 24          # OrbLinArgs<1008> + launch arguments
     else:
