@@ -254,6 +254,11 @@ def main():
     value = args.steps * n / (total_ms * 1e-3)
     estimate = value_sum / n
 
+    prof = {}
+    prof_path = os.path.join(REPO, "profiles", "ncu_summary.json")
+    if os.path.exists(prof_path):
+        with open(prof_path) as fh:
+            prof = json.load(fh)
     # dominant kernel roofline over this rank's units.  Orbit layout: a unit is
     # a chain of ORB_M points whose linear forms are computed once and serve
     # the point and its mirror; index layout: a unit is a point.
@@ -266,7 +271,9 @@ def main():
         fft_flops = 2 * 5 * FFT_N * int(math.log2(FFT_N)) + 6 * FFT_N   # fwd + inv complex FFT + spectrum product
         alg_flops = (my_units / 2) * fft_flops + forms * 2 * FLOPS_PER_POINT
         conv_flops = forms * (FLOPS_PER_PD * d + 2 * FLOPS_PER_POINT)
-        exec_flops = alg_flops
+        # FP64 flops the kernel actually executes (twiddle products, exponent
+        # arithmetic, polynomial): per tile from the committed ncu capture
+        exec_flops = (my_units / 2) * prof.get("k_orbit_fft", {}).get("fp64_flop_executed_per_tile", 0.0)
         kernel_name = "k_orbit_fft<OUT_EXPABS> (liblq.so)"
         unit_txt = (f"unit = chain of {B} mirrored point pairs, two chains per {FFT_N}-point complex FFT tile; "
                     f"per tile 2 x 5 N log2 N (forward + inverse FFT) + 6 N (spectrum product) flop, "
@@ -325,11 +332,6 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return
-    prof = {}
-    prof_path = os.path.join(REPO, "profiles", "ncu_summary.json")
-    if os.path.exists(prof_path):
-        with open(prof_path) as fh:
-            prof = json.load(fh)
     traffic = prof.get({N.LAYOUT_ORBIT_FFT: "k_orbit_fft_dram_bytes_per_launch",
                         N.LAYOUT_ORBIT: "k_orbit_dram_bytes_per_launch"}.get(lay.mode, "k_lin_dram_bytes_per_launch"))
 
