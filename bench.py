@@ -104,6 +104,18 @@ class ClockSampler:
                 "samples": len(sm), "power_w_max": float(np.nanmax(power)) if power else None}
 
 
+def cpu_model():
+    """Host CPU model name (SURVEY §8d asks for it next to the CPU baseline)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_port_rate(cfg, npts, workers=1):
     """The CPU oracle (numpy restatement of lattice.points_block + the
     integrand, oracle/np_oracle.py) on the first ``npts`` points; pts/s."""
@@ -138,7 +150,8 @@ def run_reference(args, rank, world):
                    "integrand": "exp(-|sum c_j (x_j - w_j)|)", "sample_points_per_step": sample},
         "cpu_baseline": {"value": value, "unit": "f-evals/s", "cores": cores, "kind": "port",
                          "sample": f"first {sample} points of cfg5 per step, numpy restatement of "
-                                   f"lattice.points_block + integrand over {cores} processes"},
+                                   f"lattice.points_block + integrand over {cores} processes",
+                         "cpu_model": cpu_model(), "host_cores": os.cpu_count()},
         "e2e": {"value": value, "unit": "f-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -341,7 +354,8 @@ def main():
         cpu = {"value": rate, "unit": "f-evals/s", "cores": 1, "kind": "port",
                "sample": f"first {args.cpu_sample} points of cfg5 (numpy restatement of lattice.points_block "
                          f"+ exp(-|.|), oracle/np_oracle.py), {dt:.1f} s on 1 core; "
-                         f"{os.cpu_count()} host cores, numpy {np.__version__}"}
+                         f"{os.cpu_count()} host cores, numpy {np.__version__}",
+               "cpu_model": cpu_model(), "host_cores": os.cpu_count()}
 
     mdi = {}
     if not args.no_mdi and world == 1:
