@@ -816,8 +816,18 @@ int orbit_mode() {
 // the GPU with 4096-point tiles: LQ_FFT=0 disables, =always forces.
 // (kernel ms, FFT vs direct orbit: cfg2, n = 10^4, d = 100: 0.023 vs 0.022;
 // cfg3, n = 10^6, d = 300: 0.018 vs 0.054.)
-constexpr int kFftMinD = 96;
+// Smallest d for the FFT form (tools/fft_crossover.py, direct orbit kernel vs
+// FFT form on B200): linear families pay off from d = 32 on large lattices
+// (n = 2^31 - 1: 1.20x at d = 32, 0.98x at d = 24) but only from ~d = 96 below
+// n = 2^24; SINCOS shares one sincos per mirrored pair in the FFT form and wins
+// from d = 16; the Gaussian form transforms one chain per CTA and wins from
+// d = 64.
 constexpr uint64_t kFftMinN = 1ull << 18;
+int fft_min_d(const lq_integrand* f, uint64_t n) {
+    if (is_quad_kind(f->kind)) return 64;
+    if (lin_outer(f->kind) == lq::OUT_SINCOS) return 16;
+    return n >= (1ull << 24) ? 32 : 96;
+}
 // Accuracy guard: the FFT's norm-wise error on a linear form is about
 // eps log2(N) ||c||_2 ||P||_2 <= 1.2e-16 * 12 * ||beta||_2 * sqrt(N)
 // (c = beta / n, residues < n); the FFT form is used only while that bound
@@ -844,7 +854,7 @@ bool fft_wanted(const lq_integrand* f, uint64_t n) {
     if (is_quad_kind(f->kind) && !f->gamma) return false;
     if (!fft_accurate(f)) return false;
     if (e && !std::strcmp(e, "always")) return f->d >= 2;
-    return f->d >= kFftMinD && n >= kFftMinN;
+    return f->d >= fft_min_d(f, n) && n >= kFftMinN;
 }
 
 std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, const uint64_t* z, bool* fft = nullptr) {

@@ -301,6 +301,27 @@ def test_layout_selection_without_gpu():
     assert _native.lattice_layout(pib.struct, r3.n, r3.z_reduced_array()).mode == _native.LAYOUT_ORBIT_POW2
 
 
+@pytest.mark.parametrize("fam,n,d,fft", [("expabs", 2147483647, 24, False), ("expabs", 2147483647, 32, True),
+                                         ("expabs", 1000003, 64, False), ("expabs", 1000003, 96, True),
+                                         ("sincos", 1000003, 16, True), ("sincos", 1000003, 8, False),
+                                         ("gauss", 2147483647, 48, False), ("gauss", 2147483647, 64, True),
+                                         ("expabs", 100003, 300, False)])
+def test_fft_threshold_without_gpu(fam, n, d, fft):
+    # the measured FFT-form crossovers (lq_api.cu fft_min_d, tools/fft_crossover.py)
+    from paper_2404_08867_b200 import _native, engine
+    c = [0.1 + 0.01 * (j % 7) for j in range(d)]
+    if fam == "expabs":
+        text = "exp(-abs(" + " + ".join(f"{c[j]!r}*(x[{j + 1}] - 0.5)" for j in range(d)) + "))"
+    elif fam == "sincos":
+        text = "cos(0.3 + " + " + ".join(f"{c[j]!r}*x[{j + 1}]" for j in range(d)) + ")"
+    else:
+        text = "exp(-(" + " + ".join(f"{c[j]!r}*(x[{j + 1}] - 0.5)^2" for j in range(d)) + "))"
+    pi = engine.plain_integrand(lq.parse(text, d), d)
+    r = lq.korobov_vector(76231, n, d)
+    mode = _native.lattice_layout(pi.struct, r.n, r.z_reduced_array()).mode
+    assert (mode == _native.LAYOUT_ORBIT_FFT) == fft, mode
+
+
 def test_fibonacci_rule_mirrors_reference():
     # lattice.py:120-129 and the reference's own pins (tests/test_lattice.py:85-98)
     assert lq.fibonacci_rule(2) == lq.LatticeRule(2, (1, 1))
