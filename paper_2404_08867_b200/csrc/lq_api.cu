@@ -300,13 +300,20 @@ uint64_t tile_points(const lq_integrand* f, uint64_t n) { return tile_points(f, 
 // scalar parameters of the family kernels
 struct FamHead {
     double alpha = 0, scale = 1, K = 0, A = 0, B = 0, C0 = 0, kappa = 0, M = 0, alphaB = 0, bsum = 0, half = 0, pw = 0;
+    lq::PairFast pf{};
 };
+
+bool pair_fast_consts(const lq_integrand* f, double bsum, lq::PairFast& q);
+// PairFast for kernels whose accumulator is the linear form / scale
+void pair_fast_scaled(const lq_integrand* f, double bsum, double scale, lq::PairFast& q) {
+    if (pair_fast_consts(f, bsum, q)) q.ym *= scale;   // scale = 2^sigma: exact
+}
 
 template <class A>
 void fill_head(A& a, int d, uint64_t n, uint64_t base, uint64_t end, const FamHead& h) {
     a.d = d; a.n = (uint32_t)n; a.base = base; a.end = end;
     a.alpha = h.alpha; a.scale = h.scale; a.K = h.K; a.A = h.A; a.B = h.B; a.C0 = h.C0; a.kappa = h.kappa;
-    a.M = h.M; a.alphaB = h.alphaB; a.bsum = h.bsum; a.half = h.half; a.pw = h.pw;
+    a.M = h.M; a.alphaB = h.alphaB; a.bsum = h.bsum; a.half = h.half; a.pw = h.pw; a.pf = h.pf;
 }
 
 // Per-dimension tables in kernel parameter space, sized to d: the launch copies
@@ -467,6 +474,7 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
         FamHead h;
         h.alpha = f->alpha; h.scale = std::ldexp(1.0, sigma); h.K = f->K; h.A = f->A; h.B = f->B; h.C0 = f->C0;
         h.kappa = f->kappa; h.bsum = bsum; h.alphaB = f->alpha + bsum; h.pw = f->power;
+        if (pair) pair_fast_scaled(f, bsum, h.scale, h.pf);
 #define LQ_LIN(OUT) (pair ? fam_dispatch<lq::FAM_LIN, OUT, true>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev) \
                           : fam_dispatch<lq::FAM_LIN, OUT, false>(c, tab, d, n, base, end, ntiles, units, h, tiles_dev))
         switch (lin_outer(f->kind)) {
@@ -816,17 +824,17 @@ int orbit_mode() {
 // the GPU with 4096-point tiles: LQ_FFT=0 disables, =always forces.
 // (kernel ms, FFT vs direct orbit: cfg2, n = 10^4, d = 100: 0.023 vs 0.022;
 // cfg3, n = 10^6, d = 300: 0.018 vs 0.054.)
-// Smallest d for the FFT form (tools/fft_crossover.py, direct orbit kernel vs
-// FFT form on B200): linear families pay off from d = 32 on large lattices
-// (n = 2^31 - 1: 1.20x at d = 32, 0.98x at d = 24) but only from ~d = 96 below
-// n = 2^24; SINCOS shares one sincos per mirrored pair in the FFT form and wins
-// from d = 16; the Gaussian form transforms one chain per CTA and wins from
-// d = 64.
+// Smallest d for the FFT form (tools/fft_crossover.py: the FFT form against the
+// direct orbit kernel, both with §4.1e's one-reduction pair outer): exp /
+// exp-abs / sincos from d = 49 on n >= 2^22 (n = 2^31 - 1: 0.99x at d = 48,
+// 1.21x at 56) and from d = 112 below (n = 1e6 + 3: 0.95x at 96, 1.40x at
+// 128); power (two outer evaluations in both forms, integer powers by
+// squaring) likewise (1.00x at d = 48, 1.29x at 96); the Gaussian form
+// transforms one chain per CTA and wins from d = 64.
 constexpr uint64_t kFftMinN = 1ull << 18;
 int fft_min_d(const lq_integrand* f, uint64_t n) {
     if (is_quad_kind(f->kind)) return 64;
-    if (lin_outer(f->kind) == lq::OUT_SINCOS) return 16;
-    return n >= (1ull << 24) ? 32 : 96;
+    return n >= (1ull << 22) ? 49 : 112;
 }
 // Accuracy guard: the FFT's norm-wise error on a linear form is about
 // eps log2(N) ||c||_2 ||P||_2 <= 1.2e-16 * 12 * ||beta||_2 * sqrt(N)
@@ -997,6 +1005,7 @@ void split_exp(long double x, double& cm, int32_t& k) {
 // the family has no such form or some value could leave the normal range.
 // |s1| <= |alpha| + sum |beta|, |s2| <= |alphaB| + sum |beta| (x_j in [0, 1)).
 bool pair_fast_consts(const lq_integrand* f, double bsum, lq::PairFast& q) {
+    q = lq::PairFast{};   // on = 0
     if (std::getenv("LQ_PAIRFAST") && std::string(std::getenv("LQ_PAIRFAST")) == "0") return false;
     const int outer = lin_outer(f->kind);
     long double babs = 0.0L;
@@ -1004,7 +1013,6 @@ bool pair_fast_consts(const lq_integrand* f, double bsum, lq::PairFast& q) {
     const long double alpha = f->alpha, alphaB = (long double)f->alpha + (long double)bsum;
     const long double smax = std::max(fabsl(alpha), fabsl(alphaB)) + babs;
     const long double D = alpha + alphaB;
-    q = lq::PairFast{};
     if (outer == lq::OUT_SINCOS) {
         if (!std::isfinite((double)smax)) return false;
         const long double sD = sinl(D), cD = cosl(D), A = f->A, B = f->B;
@@ -1012,12 +1020,14 @@ bool pair_fast_consts(const lq_integrand* f, double bsum, lq::PairFast& q) {
         q.c0 = (double)(A + B * sD - A * cD);
         q.c1 = (double)(B + A * sD + B * cD);
         q.c2 = (double)(2.0L * (long double)f->C0);
+        q.on = 1;
         return true;
     }
     if (outer == lq::OUT_EXP) {
         if (!(smax <= 700.0L)) return false;
         q.ym = 1.0; q.ya = f->alpha; q.post = f->K;
         split_exp(D, q.c0, q.k0);
+        q.on = 1;
         return true;
     }
     if (outer == lq::OUT_EXPABS) {
@@ -1026,6 +1036,7 @@ bool pair_fast_consts(const lq_integrand* f, double bsum, lq::PairFast& q) {
         q.ym = (double)lam; q.ya = (double)(lam * alpha); q.E = (double)(lam * D); q.post = f->K;
         split_exp(-lam * D, q.c0, q.k0);
         split_exp(lam * D, q.c1, q.k1);
+        q.on = 1;
         return true;
     }
     return false;
@@ -1090,7 +1101,7 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     }
     c->launches++;   // the coefficient transform
     CK(cudaGetLastError());
-    lq::FftHead h;
+    lq::FftHead h{};
     h.n = p.n; h.B = (uint32_t)p.m; h.units = p.units; h.qc = p.qc; h.h = p.h; h.zero = p.zero ? 1 : 0;
     h.G = G; h.Alo = Alo; h.Ahi = Ahi; h.apow = apow; h.starts = starts; h.W = (const double2*)W;
     h.Hc = (const double2*)Hc;
@@ -1134,7 +1145,7 @@ int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t un
     const int d = f->d, m = p.m;
     const int dpad = (d + m - 1) / m * m;
     const double nd = (double)p.n;
-    lq::OrbHead h;
+    lq::OrbHead h{};
     h.n = p.n; h.a = p.a; h.as = p.as; h.dpad = dpad; h.units = p.units; h.qc = p.qc; h.h = p.h;
     h.zero = p.zero ? 1 : 0;
     h.G = G; h.Alo = Alo; h.Ahi = Ahi;
@@ -1194,6 +1205,7 @@ int launch_orbit(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_t un
     h.alphaB = f->alpha + bsum;   // alpha + <beta, 1 - x> = (alpha + sum beta) - <beta, x>
     h.M = 0.0;
     h.half = 0.0;
+    pair_fast_scaled(f, bsum, h.scale, h.pf);
     const int outer = lin_outer(f->kind);
     if (dpad <= 120) return orbit_lin<120>(c, h, cv, outer, unit0, ntiles, tiles_dev);
     if (dpad <= 1008) return orbit_lin<1008>(c, h, cv, outer, unit0, ntiles, tiles_dev);

@@ -126,9 +126,24 @@ enum : int { OUT_EXP = 0, OUT_SINCOS = 1, OUT_EXPABS = 2, OUT_POW = 3 };
 
 // numpy's b**k for integer k (exprcore.py:466-468; square for k == 2, libm pow
 // otherwise; a negative k is 1 / b**(-k), as the reference's pow nodes).
+// Integer |k| <= 32 by repeated squaring (at most 9 multiplications, a few ulp
+// from libm's pow: far inside the 1e-10 parity bar, ~4x cheaper than pow).
 __device__ __forceinline__ double int_pow(double b, double k) {
-    if (k >= 0.0) return k == 2.0 ? b * b : pow(b, k);
-    return 1.0 / (k == -1.0 ? b : k == -2.0 ? b * b : pow(b, -k));
+    const double ak = fabs(k);
+    double r;
+    if (ak <= 32.0 && ak == rint(ak)) {
+        unsigned e = (unsigned)ak;
+        double x = b;
+        r = 1.0;
+        while (e) {
+            if (e & 1u) r *= x;
+            e >>= 1;
+            if (e) x *= x;
+        }
+    } else {
+        r = pow(b, ak);
+    }
+    return k >= 0.0 ? r : 1.0 / r;
 }
 
 template <int OUTER>
@@ -153,6 +168,114 @@ __device__ __noinline__ double outer_fn(double acc, const LinParams p) {
 template <int OUTER>
 __device__ __noinline__ double quad_outer(double acc, const LinParams p) {
     return outer_val<OUTER>(p.alpha + acc, p);
+}
+
+// A point and its mirror from one range reduction (DESIGN.md §4.1e).  With
+// s1 = alpha + l, s2 = alphaB - l = D - s1 and y = ym l + ya:
+//   EXP     e^s1 + e^s2 = e^y + e^D e^-y                       (y = s1)
+//   EXPABS  e^-|y| + e^-|E - y|, y = lambda s1, E = lambda D   (kappa = -lambda <= 0)
+//   SINCOS  2 C0 + A' sin y + B' cos y                         (y = s1)
+// e^z = 2^k e^r and e^-z = 2^-k e^-r share r, r^2 and the even/odd halves of
+// one Taylor polynomial; the constants are split on the host as c 2^k.  The
+// host enables it only where every value stays a normal double (|y| <= 700).
+struct PairFast {
+    double ym, ya, E;
+    double c0, c1, c2;   // EXP: e^D; EXPABS: e^-E, e^E; SINCOS: A', B', 2 C0
+    double post;         // multiplier after the sum (K; 1 for SINCOS)
+    int32_t k0, k1;      // binary exponents of c0, c1
+    int32_t on;          // the host enabled the form (else two outer evaluations)
+};
+
+// v 2^j by exponent arithmetic (v 2^j must be a normal double)
+__device__ __forceinline__ double scale2(double v, int j) {
+    return __hiloint2double(__double2hiint(v) + (j << 20), __double2loint(v));
+}
+
+// f(s1) + f(s2) without the factor q.post (see PairFast)
+template <int OUTER>
+__device__ __forceinline__ double pair_fast(double l, const PairFast& q) {
+    const double y = fma(l, q.ym, q.ya);
+    if constexpr (OUTER == OUT_SINCOS) {
+        double sn, cs;
+        sincos(y, &sn, &cs);
+        return fma(q.c0, sn, fma(q.c1, cs, q.c2));
+    } else {
+        const double z = OUTER == OUT_EXPABS ? -fabs(y) : y;
+        const double t = fma(z, 1.4426950408889634, 6755399441055744.0);   // 1.5 2^52: round to integer
+        const int k = __double2loint(t);
+        const double kf = t - 6755399441055744.0;
+        double r = fma(kf, -6.93147180559945286e-01, z);                    // z - k ln2, two-part ln2
+        r = fma(kf, -2.319046813846299558e-17, r);
+        const double r2 = r * r;
+        double e = fma(r2, 2.08767569878681e-09, 2.755731922398589e-07);   // sum r^2i / (2i)!, i <= 6
+        e = fma(r2, e, 2.48015873015873e-05);
+        e = fma(r2, e, 0.001388888888888889);
+        e = fma(r2, e, 0.041666666666666664);
+        e = fma(r2, e, 0.5);
+        e = fma(r2, e, 1.0);
+        double o = fma(r2, 2.505210838544172e-08, 2.7557319223985893e-06);   // sum r^2i / (2i + 1)!, i <= 5
+        o = fma(r2, o, 0.0001984126984126984);
+        o = fma(r2, o, 0.008333333333333333);
+        o = fma(r2, o, 0.16666666666666666);
+        o = fma(r2, o, 1.0);
+        const double p = fma(r, o, e), m = fma(-r, o, e);                    // e^r, e^-r
+        const double f1 = scale2(p, k);
+        if constexpr (OUTER == OUT_EXP) {
+            return f1 + scale2(m * q.c0, q.k0 - k);
+        } else {
+            const bool s1 = y >= 0.0, s2 = y <= q.E, same = s1 == s2;
+            return f1 + scale2((same ? m : p) * (s2 ? q.c0 : q.c1), (s2 ? q.k0 : q.k1) + (same ? -k : k));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_fft_twiddles(double2* __restrict__ W) {
+    for (int k = blockIdx.x * kThreads + threadIdx.x; k < kFftN; k += gridDim.x * kThreads) {
+        double sn, cs;
+        sincospi(-2.0 * (double)k / (double)kFftN, &sn, &cs);
+        W[k] = make_double2(cs, sn);
+    }
+}
+
+// Hc = conj(FFT(c_pad)) / N, one CTA of kFftThreads.
+__global__ void __launch_bounds__(kFftThreads) k_fft_coeffs(const double* __restrict__ c, int d,
+                                                             const double2* __restrict__ W, double2* __restrict__ Hc) {
+    extern __shared__ double2 buf[];
+    double2* tw = buf + kFftPad;
+    fft_load_twiddles(tw, W);
+    for (int t = threadIdx.x; t < kFftN; t += kFftThreads) buf[fpad(t)] = make_double2(t < d ? c[t] : 0.0, 0.0);
+    __syncthreads();
+    fft4096(buf, kFftR == 16 ? tw : W);
+    const double inv = 1.0 / (double)kFftN;
+    for (int t = threadIdx.x; t < kFftN; t += kFftThreads) {
+        const double2 v = buf[fpad(t)];
+        Hc[t] = make_double2(v.x * inv, -v.y * inv);
+    }
+}
+
+// H+- = (conj(FFT(b)) +- conj(FFT(q))) / (2N) for the Gaussian family: b and q
+// share one transform (b + i q) and are separated by symmetry.  One CTA.
+__global__ void __launch_bounds__(kFftThreads) k_fft_coeffs_pm(const double* __restrict__ b,
+                                                                const double* __restrict__ q, int d,
+                                                                const double2* __restrict__ W,
+                                                                double2* __restrict__ Hp, double2* __restrict__ Hm) {
+    extern __shared__ double2 buf[];
+    double2* tw = buf + kFftPad;
+    fft_load_twiddles(tw, W);
+    for (int t = threadIdx.x; t < kFftN; t += kFftThreads)
+        buf[fpad(t)] = t < d ? make_double2(b[t], q[t]) : make_double2(0.0, 0.0);
+    __syncthreads();
+    fft4096(buf, kFftR == 16 ? tw : W);
+    const double h = 0.5 / (double)kFftN;
+    for (int m = threadIdx.x; m < kFftN; m += kFftThreads) {
+        const double2 x = buf[fpad(m)], xr = buf[fpad((kFftN - m) & (kFftN - 1))];
+        const double2 sb = make_double2(x.x + xr.x, x.y - xr.y);    // 2 FFT(b)[m]
+        const double2 sq = make_double2(x.y + xr.y, xr.x - x.x);    // 2 FFT(q)[m]  ((x - conj xr) / i)
+        const double2 hb = make_double2(sb.x * h, -sb.y * h);       // conj(FFT(b)) / N
+        const double2 hq = make_double2(sq.x * h, -sq.y * h);       // conj(FFT(q)) / N
+        Hp[m] = make_double2(0.5 * (hb.x + hq.x), 0.5 * (hb.y + hq.y));
+        Hm[m] = make_double2(0.5 * (hb.x - hq.x), 0.5 * (hb.y - hq.y));
+    }
 }
 
 // Mirror pairs (x and 1 - x): f at both points from one
@@ -193,6 +316,7 @@ struct FamArgs {
     double alpha, scale, K, A, B, C0, kappa, M;
     double alphaB, bsum, half;   // mirror pairs: alpha + sum beta (QUADP: alpha + C), sum beta, 2^-sigma / 2
     double pw;                   // OUT_POW exponent
+    PairFast pf;                 // linear mirror pairs from one range reduction
     Dim dims[N];
 };
 
@@ -204,6 +328,7 @@ struct FamArgsG {   // d > kParamDims: per-dimension records in global memory
     double alpha, scale, K, A, B, C0, kappa, M;
     double alphaB, bsum, half;
     double pw;
+    PairFast pf;
     const Dim* __restrict__ dims;
 };
 
@@ -352,7 +477,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_fam(const __grid_constant__ Arg
         if constexpr (KIND == FAM_QUADP) {
             f = quad_pair<OUTER>(acc[p], acc2[p], a.alphaB, lin_params(a), i != 0 && 2 * i != a.n);
         } else if constexpr (PAIR) {
-            f = outer_pair<OUTER>(acc[p], lin_params(a), a.alphaB, i != 0 && 2 * i != a.n);
+            const bool two = i != 0 && 2 * i != a.n;
+            if (OUTER != OUT_POW && a.pf.on && two)   // inline: reads a.pf from parameter space
+                f = a.pf.post * pair_fast<OUTER == OUT_POW ? OUT_EXP : OUTER>(acc[p], a.pf);
+            else
+                f = outer_pair<OUTER>(acc[p], lin_params(a), a.alphaB, two);
         } else {
             f = fam_outer<KIND, OUTER>(acc[p], a);
         }
@@ -485,6 +614,7 @@ struct OrbHead {
     const uint32_t* Alo;    // a^(m q) for q < 4096
     const uint32_t* Ahi;    // a^(m 4096 q)
     double alpha, alphaB, scale, bsum, K, A, B, C0, kappa, M, half, pw;
+    PairFast pf;            // linear families: point and mirror from one range reduction
     int32_t zero;           // unit 0 also adds the point x = 0 (not for the levels of n = 2^k)
 };
 
@@ -554,9 +684,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_orbit(const __grid_constant__ A
                 }
             }
             const LinParams prm{H.alpha, H.scale, H.K, H.A, H.B, H.C0, H.kappa, H.pw};
-            #pragma unroll
-            for (int k = 0; k < M; ++k)
-                s += k < valid ? outer_pair<OUTER>(acc[k], prm, H.alphaB, true) : 0.0;
+            if (OUTER != OUT_POW && H.pf.on) {   // one range reduction per pair, inline (§4.1e)
+                double t = 0.0;
+                #pragma unroll
+                for (int k = 0; k < M; ++k)
+                    t += k < valid ? pair_fast<OUTER == OUT_POW ? OUT_EXP : OUTER>(acc[k], H.pf) : 0.0;
+                s += H.pf.post * t;
+            } else {
+                #pragma unroll
+                for (int k = 0; k < M; ++k) s += k < valid ? outer_pair<OUTER>(acc[k], prm, H.alphaB, true) : 0.0;
+            }
             if (u == 0 && H.zero) s += outer_fn<OUTER>(0.0, prm);   // point 0
         } else {
             const double Ms = H.M, hf = H.half;
@@ -686,21 +823,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_orbit_prod(const __grid_constan
 // B linear forms of a chain (overlap-save), O(log N) FP64 work per point
 // instead of O(d).  Two chains ride in one complex FFT
 // (real and imaginary parts); c is real, so their correlations separate.
-// A point and its mirror from one range reduction (DESIGN.md §4.1e).  With
-// s1 = alpha + l, s2 = alphaB - l = D - s1 and y = ym l + ya:
-//   EXP     e^s1 + e^s2 = e^y + e^D e^-y                       (y = s1)
-//   EXPABS  e^-|y| + e^-|E - y|, y = lambda s1, E = lambda D   (kappa = -lambda <= 0)
-//   SINCOS  2 C0 + A' sin y + B' cos y                         (y = s1)
-// e^z = 2^k e^r and e^-z = 2^-k e^-r share r, r^2 and the even/odd halves of
-// one Taylor polynomial; the constants are split on the host as c 2^k.  The
-// host enables it only where every value stays a normal double (|y| <= 700).
-struct PairFast {
-    double ym, ya, E;
-    double c0, c1, c2;   // EXP: e^D; EXPABS: e^-E, e^E; SINCOS: A', B', 2 C0
-    double post;         // multiplier after the sum (K; 1 for SINCOS)
-    int32_t k0, k1;      // binary exponents of c0, c1
-};
-
 struct FftHead {
     uint32_t n, B;                     // modulus, chain length N - d + 1
     uint64_t units;                    // chains
@@ -716,98 +838,6 @@ struct FftHead {
     PairFast pf;
     int32_t zero;                      // unit 0 also adds the point x = 0
 };
-
-// v 2^j by exponent arithmetic (v 2^j must be a normal double)
-__device__ __forceinline__ double scale2(double v, int j) {
-    return __hiloint2double(__double2hiint(v) + (j << 20), __double2loint(v));
-}
-
-// f(s1) + f(s2) without the factor q.post (see PairFast)
-template <int OUTER>
-__device__ __forceinline__ double pair_fast(double l, const PairFast& q) {
-    const double y = fma(l, q.ym, q.ya);
-    if constexpr (OUTER == OUT_SINCOS) {
-        double sn, cs;
-        sincos(y, &sn, &cs);
-        return fma(q.c0, sn, fma(q.c1, cs, q.c2));
-    } else {
-        const double z = OUTER == OUT_EXPABS ? -fabs(y) : y;
-        const double t = fma(z, 1.4426950408889634, 6755399441055744.0);   // 1.5 2^52: round to integer
-        const int k = __double2loint(t);
-        const double kf = t - 6755399441055744.0;
-        double r = fma(kf, -6.93147180559945286e-01, z);                    // z - k ln2, two-part ln2
-        r = fma(kf, -2.319046813846299558e-17, r);
-        const double r2 = r * r;
-        double e = fma(r2, 2.08767569878681e-09, 2.755731922398589e-07);   // sum r^2i / (2i)!, i <= 6
-        e = fma(r2, e, 2.48015873015873e-05);
-        e = fma(r2, e, 0.001388888888888889);
-        e = fma(r2, e, 0.041666666666666664);
-        e = fma(r2, e, 0.5);
-        e = fma(r2, e, 1.0);
-        double o = fma(r2, 2.505210838544172e-08, 2.7557319223985893e-06);   // sum r^2i / (2i + 1)!, i <= 5
-        o = fma(r2, o, 0.0001984126984126984);
-        o = fma(r2, o, 0.008333333333333333);
-        o = fma(r2, o, 0.16666666666666666);
-        o = fma(r2, o, 1.0);
-        const double p = fma(r, o, e), m = fma(-r, o, e);                    // e^r, e^-r
-        const double f1 = scale2(p, k);
-        if constexpr (OUTER == OUT_EXP) {
-            return f1 + scale2(m * q.c0, q.k0 - k);
-        } else {
-            const bool s1 = y >= 0.0, s2 = y <= q.E, same = s1 == s2;
-            return f1 + scale2((same ? m : p) * (s2 ? q.c0 : q.c1), (s2 ? q.k0 : q.k1) + (same ? -k : k));
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kThreads) k_fft_twiddles(double2* __restrict__ W) {
-    for (int k = blockIdx.x * kThreads + threadIdx.x; k < kFftN; k += gridDim.x * kThreads) {
-        double sn, cs;
-        sincospi(-2.0 * (double)k / (double)kFftN, &sn, &cs);
-        W[k] = make_double2(cs, sn);
-    }
-}
-
-// Hc = conj(FFT(c_pad)) / N, one CTA of kFftThreads.
-__global__ void __launch_bounds__(kFftThreads) k_fft_coeffs(const double* __restrict__ c, int d,
-                                                             const double2* __restrict__ W, double2* __restrict__ Hc) {
-    extern __shared__ double2 buf[];
-    double2* tw = buf + kFftPad;
-    fft_load_twiddles(tw, W);
-    for (int t = threadIdx.x; t < kFftN; t += kFftThreads) buf[fpad(t)] = make_double2(t < d ? c[t] : 0.0, 0.0);
-    __syncthreads();
-    fft4096(buf, kFftR == 16 ? tw : W);
-    const double inv = 1.0 / (double)kFftN;
-    for (int t = threadIdx.x; t < kFftN; t += kFftThreads) {
-        const double2 v = buf[fpad(t)];
-        Hc[t] = make_double2(v.x * inv, -v.y * inv);
-    }
-}
-
-// H+- = (conj(FFT(b)) +- conj(FFT(q))) / (2N) for the Gaussian family: b and q
-// share one transform (b + i q) and are separated by symmetry.  One CTA.
-__global__ void __launch_bounds__(kFftThreads) k_fft_coeffs_pm(const double* __restrict__ b,
-                                                                const double* __restrict__ q, int d,
-                                                                const double2* __restrict__ W,
-                                                                double2* __restrict__ Hp, double2* __restrict__ Hm) {
-    extern __shared__ double2 buf[];
-    double2* tw = buf + kFftPad;
-    fft_load_twiddles(tw, W);
-    for (int t = threadIdx.x; t < kFftN; t += kFftThreads)
-        buf[fpad(t)] = t < d ? make_double2(b[t], q[t]) : make_double2(0.0, 0.0);
-    __syncthreads();
-    fft4096(buf, kFftR == 16 ? tw : W);
-    const double h = 0.5 / (double)kFftN;
-    for (int m = threadIdx.x; m < kFftN; m += kFftThreads) {
-        const double2 x = buf[fpad(m)], xr = buf[fpad((kFftN - m) & (kFftN - 1))];
-        const double2 sb = make_double2(x.x + xr.x, x.y - xr.y);    // 2 FFT(b)[m]
-        const double2 sq = make_double2(x.y + xr.y, xr.x - x.x);    // 2 FFT(q)[m]  ((x - conj xr) / i)
-        const double2 hb = make_double2(sb.x * h, -sb.y * h);       // conj(FFT(b)) / N
-        const double2 hq = make_double2(sq.x * h, -sq.y * h);       // conj(FFT(q)) / N
-        Hp[m] = make_double2(0.5 * (hb.x + hq.x), 0.5 * (hb.y + hq.y));
-        Hm[m] = make_double2(0.5 * (hb.x - hq.x), 0.5 * (hb.y - hq.y));
-    }
-}
 
 // H[m] of a real sequence's spectrum from the lower half only: H[N - m] =
 // conj(H[m]), which halves the table's cache footprint (32 KB).
@@ -843,6 +873,7 @@ __device__ __forceinline__ double block_sum_n(double v, double* sh /* >= NT / 32
     }
     return v;
 }
+
 
 // Tile b = two chains (units 2b, 2b + 1 after unit0); tile_out[b] = their sum.
 // A CTA runs tiles per_cta blockIdx.x .. + per_cta - 1 (< ntiles), so the

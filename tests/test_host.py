@@ -301,10 +301,12 @@ def test_layout_selection_without_gpu():
     assert _native.lattice_layout(pib.struct, r3.n, r3.z_reduced_array()).mode == _native.LAYOUT_ORBIT_POW2
 
 
-@pytest.mark.parametrize("fam,n,d,fft", [("expabs", 2147483647, 24, False), ("expabs", 2147483647, 32, True),
-                                         ("expabs", 1000003, 64, False), ("expabs", 1000003, 96, True),
-                                         ("sincos", 1000003, 16, True), ("sincos", 1000003, 8, False),
+@pytest.mark.parametrize("fam,n,d,fft", [("expabs", 2147483647, 48, False), ("expabs", 2147483647, 49, True),
+                                         ("expabs", 1000003, 111, False), ("expabs", 1000003, 112, True),
+                                         ("sincos", 16777213, 56, True), ("sincos", 1000003, 96, False),
                                          ("gauss", 2147483647, 48, False), ("gauss", 2147483647, 64, True),
+                                         ("pow", 2147483647, 48, False), ("pow", 2147483647, 49, True),
+                                         ("pow", 1000003, 96, False),
                                          ("expabs", 100003, 300, False)])
 def test_fft_threshold_without_gpu(fam, n, d, fft):
     # the measured FFT-form crossovers (lq_api.cu fft_min_d, tools/fft_crossover.py)
@@ -314,6 +316,8 @@ def test_fft_threshold_without_gpu(fam, n, d, fft):
         text = "exp(-abs(" + " + ".join(f"{c[j]!r}*(x[{j + 1}] - 0.5)" for j in range(d)) + "))"
     elif fam == "sincos":
         text = "cos(0.3 + " + " + ".join(f"{c[j]!r}*x[{j + 1}]" for j in range(d)) + ")"
+    elif fam == "pow":
+        text = "(1.5 + " + " + ".join(f"{c[j] / d!r}*x[{j + 1}]" for j in range(d)) + ")^(-3)"
     else:
         text = "exp(-(" + " + ".join(f"{c[j]!r}*(x[{j + 1}] - 0.5)^2" for j in range(d)) + "))"
     pi = engine.plain_integrand(lq.parse(text, d), d)

@@ -23,6 +23,8 @@ def kernel_ms(pi, n, z, mode):
 
 def text_of(fam, d, rng):
     c = rng.uniform(0, 1, d); c *= 10 / c.sum(); w = rng.uniform(0, 1, d)
+    if fam == "pow":
+        return "(1.5 + " + " + ".join(f"{float(c[j]) / 10!r}*x[{j + 1}]" for j in range(d)) + ")^(-3)"
     if fam == "expabs":
         return "exp(-abs(" + " + ".join(f"{float(c[j])!r}*(x[{j + 1}] - {float(w[j])!r})" for j in range(d)) + "))"
     if fam == "sincos":
@@ -31,9 +33,13 @@ def text_of(fam, d, rng):
 
 
 fams = sys.argv[1].split(",") if len(sys.argv) > 1 else ["expabs"]
-for n, a in ((2147483647, 1440510675), (16777213, 1234567), (1000003, 76231)):
+ds = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [16, 24, 32, 48, 64, 96, 128]
+ns = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else [2147483647, 16777213, 1000003]
+A = {2147483647: 1440510675, 16777213: 1234567, 1000003: 76231}
+for n in ns:
+    a = A.get(n, 76231)
     for fam in fams:
-        for d in (16, 24, 32, 48, 64, 96, 128):
+        for d in ds:
             rng = np.random.default_rng(d)
             f = lq.parse(text_of(fam, d, rng), d)
             rule = lq.korobov_vector(a, n, d)
