@@ -425,3 +425,35 @@ def test_pow2_partials_sharded_bit_identical(env, monkeypatch):
     out = C.c_double()
     N.check(h.lq_reduce_sum(ctx, C.c_void_p(one.data_ptr()), S, C.byref(out)))
     assert out.value == engine.lattice_sum(pi, n, z)
+
+
+@pytest.mark.parametrize("layout", ["orbit", "paired"])
+@pytest.mark.parametrize("family,scale,offset", [("expabs", 10.0, 0.0), ("expabs", 350.0, 0.0), ("expabs", 800.0, 0.0),
+                                                 ("exp", 3.0, 0.25), ("exp", 100.0, -650.0), ("sincos", 9.0, 0.0)])
+def test_pair_fast_direct_kernels(env, layout, family, scale, offset, monkeypatch):
+    # the one-reduction point/mirror outer inlined in the
+    # direct orbit kernel and the mirror-paired index kernel, against the
+    # two-evaluation form (LQ_PAIRFAST=0) and the oracle; expabs 800 and the
+    # exp offset -650 leave the normal range and fall back
+    lq, N, engine = env
+    from oracle import np_oracle
+    from test_gpu_fft import _pair_text
+    n, d = 100003, 40
+    rng = np.random.default_rng(zlib.crc32(f"pairdirect/{family}/{scale}".encode()))
+    f = lq.parse(_pair_text(family, d, rng, scale, offset), d)
+    if layout == "orbit":
+        rule = lq.korobov_vector(2, n, d)
+        want = N.LAYOUT_ORBIT
+    else:
+        rule = lq.LatticeRule(n, _unit_vector(n, d, rng))
+        want = N.LAYOUT_PAIRED
+    pi = engine.plain_integrand(f, d)
+    z = rule.z_reduced_array()
+    monkeypatch.setenv("LQ_FFT", "0")
+    assert N.lattice_layout(pi.struct, n, z).mode == want
+    fast = engine.lattice_sum(pi, n, z)
+    monkeypatch.setenv("LQ_PAIRFAST", "0")
+    slow = engine.lattice_sum(pi, n, z)
+    assert math.isclose(fast, slow, rel_tol=1e-13, abs_tol=1e-300), (fast, slow)
+    ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
+    assert math.isclose(fast, ref, rel_tol=1e-10, abs_tol=1e-300), (fast, ref)
