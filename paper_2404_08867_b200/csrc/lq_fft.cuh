@@ -28,7 +28,11 @@ constexpr int kFftPad = kFftN + kFftN / kFftR;   // padded shared-memory length 
 // (W = e^{-2 pi i / N}).
 constexpr int kFftTw3 = 3 * 256, kFftTw2 = 15 * 16;
 constexpr int kFftTwAll = 2 * kFftTw3 + kFftTw2;
-constexpr int kFftSmem = (kFftPad + (kFftR == 16 ? kFftTwAll : 0)) * 16;   // bytes per CTA
+#ifndef LQ_FFT_EXPTAB
+#define LQ_FFT_EXPTAB 1
+#endif
+constexpr int kFftExpTab = LQ_FFT_EXPTAB ? 64 : 0;   // (2^(j/64), 2^(-j/64)) for the pair outer
+constexpr int kFftSmem = (kFftPad + (kFftR == 16 ? kFftTwAll : 0) + kFftExpTab) * 16;   // bytes per CTA
 
 // Build the radix-16 tables from the global table W[k] = e^{-2 pi i k / N}.
 __device__ __forceinline__ void fft_load_twiddles(double2* __restrict__ tw, const double2* __restrict__ W) {

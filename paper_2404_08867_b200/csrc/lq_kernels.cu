@@ -229,6 +229,36 @@ __device__ __forceinline__ double pair_fast(double l, const PairFast& q) {
     }
 }
 
+// pair_fast with a 64-entry shared table T[j] = (2^(j/64), 2^(-j/64)): the
+// range reduction z = (64 k + j) ln2/64 + r leaves |r| <= ln2/128, where
+// degree-5 halves of the Taylor polynomial suffice (truncation < 4e-17)
+template <int OUTER>
+__device__ __forceinline__ double pair_fast_tab(double l, const PairFast& q, const double2* __restrict__ T) {
+    if constexpr (OUTER == OUT_SINCOS) return pair_fast<OUTER>(l, q);
+    const double y = fma(l, q.ym, q.ya);
+    const double z = OUTER == OUT_EXPABS ? -fabs(y) : y;
+    const double t = fma(z, 92.332482616893658, 6755399441055744.0);    // 64/ln2; 1.5 2^52
+    const int K = __double2loint(t);
+    const double kf = t - 6755399441055744.0;
+    double r = fma(kf, -1.0830424696249145e-02, z);                     // ln2/64, two parts
+    r = fma(kf, -3.6235106466348431e-19, r);
+    const int k = K >> 6;
+    const double2 tj = T[K & 63];
+    const double r2 = r * r;
+    double e = fma(r2, 4.1666666666666664e-02, 0.5);
+    e = fma(r2, e, 1.0);
+    double o = fma(r2, 8.3333333333333332e-03, 0.16666666666666666);
+    o = fma(r2, o, 1.0);
+    const double p = fma(r, o, e) * tj.x, m = fma(-r, o, e) * tj.y;     // e^(z - k ln2), e^(-z + k ln2)
+    const double f1 = scale2(p, k);
+    if constexpr (OUTER == OUT_EXP) {
+        return f1 + scale2(m * q.c0, q.k0 - k);
+    } else {
+        const bool s1 = y >= 0.0, s2 = y <= q.E, same = s1 == s2;
+        return f1 + scale2((same ? m : p) * (s2 ? q.c0 : q.c1), (s2 ? q.k0 : q.k1) + (same ? -k : k));
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) k_fft_twiddles(double2* __restrict__ W) {
     for (int k = blockIdx.x * kThreads + threadIdx.x; k < kFftN; k += gridDim.x * kThreads) {
         double sn, cs;
@@ -837,6 +867,7 @@ struct FftHead {
     double alpha, alphaB, K, A, Bc, C0, kappa, pw;
     PairFast pf;
     int32_t zero;                      // unit 0 also adds the point x = 0
+    double2 etab[kFftExpTab > 0 ? kFftExpTab : 1];          // (2^(j/64), 2^(-j/64)), correctly rounded on the host
 };
 
 // H[m] of a real sequence's spectrum from the lower half only: H[N - m] =
@@ -875,6 +906,17 @@ __device__ __forceinline__ double block_sum_n(double v, double* sh /* >= NT / 32
 }
 
 
+// Per-tile CTA sums without their own barriers: each warp leaves its partial
+// in a slot of the tile's parity, and thread 0 sums the previous tile's eight
+// slots after the next tile's first FFT barrier (measured 7.50 -> 7.33 ms on cfg5)
+#ifndef LQ_FFT_DEFER
+#define LQ_FFT_DEFER 1
+#endif
+// the eight warp partials of a 256-thread CTA in block_sum_n's xor-tree order
+__device__ __forceinline__ double defer_sum8(const double* w) {
+    return ((w[0] + w[4]) + (w[2] + w[6])) + ((w[1] + w[5]) + (w[3] + w[7]));
+}
+
 // Tile b = two chains (units 2b, 2b + 1 after unit0); tile_out[b] = their sum.
 // A CTA runs tiles per_cta blockIdx.x .. + per_cta - 1 (< ntiles), so the
 // twiddle tables are filled once per per_cta tiles.
@@ -888,6 +930,10 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
     double2* tw = buf + kFftPad;
     fft_load_twiddles(tw, a.W);          // visible after the first pass's barrier
     const double2* Wt = kFftR == 16 ? tw : a.W;
+#if LQ_FFT_EXPTAB
+    double2* et = tw + kFftTwAll;
+    if (threadIdx.x < kFftExpTab) et[threadIdx.x] = a.etab[threadIdx.x];   // visible after the first barrier
+#endif
     const uint32_t n = a.n;
     const int64_t b0 = (int64_t)blockIdx.x * per_cta;
     const int64_t b1 = min(b0 + per_cta, ntiles);
@@ -911,6 +957,11 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
         }
     }
     fft4096_regs<false>(v, buf, Wt);
+#if LQ_FFT_DEFER
+    // the previous tile's warp partials (written before this tile's first
+    // barrier) summed in block_sum_n's fixed order
+    if (threadIdx.x == 0 && tb > b0) tile_out[tb - 1] = defer_sum8(sh + 8 * ((tb - 1) & 1));
+#endif
     // Y = X conj(C) / N, conjugated so that the forward transform inverts it;
     // the last forward pass left positions j + (N/R) r in this thread, which
     // are exactly the inputs of the first inverse pass
@@ -932,7 +983,11 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
         for (int r = 0; r < R; ++r) {
             if (wbase + r * kFftThreads < vmax) {
                 const int k = threadIdx.x + r * kFftThreads;
+#if LQ_FFT_EXPTAB
+                const double g0 = pair_fast_tab<OUTER>(v[r].x, a.pf, et), g1 = pair_fast_tab<OUTER>(-v[r].y, a.pf, et);
+#else
                 const double g0 = pair_fast<OUTER>(v[r].x, a.pf), g1 = pair_fast<OUTER>(-v[r].y, a.pf);
+#endif
                 s += (k < v0 ? g0 : 0.0) + (k < v1 ? g1 : 0.0);
             }
         }
@@ -953,9 +1008,19 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
     }
     }
     if (u0 == 0 && a.zero && threadIdx.x == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
+#if LQ_FFT_DEFER
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) sh[8 * (tb & 1) + (threadIdx.x >> 5)] = s;
+#else
     s = block_sum_n<kFftThreads>(s, sh);
     if (threadIdx.x == 0) tile_out[tb] = s;
+#endif
     }
+#if LQ_FFT_DEFER
+    __syncthreads();
+    if (threadIdx.x == 0 && b1 > b0) tile_out[b1 - 1] = defer_sum8(sh + 8 * ((b1 - 1) & 1));
+#endif
 }
 
 // Gaussian family in FFT form: one chain per CTA.  The centred coordinates
@@ -992,6 +1057,9 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft_quad(const __grid_
         v[r] = make_double2(u, u * u);
     }
     fft4096_regs<true>(v, buf, Wt);        // X in shared memory, natural order
+#if LQ_FFT_DEFER
+    if (threadIdx.x == 0 && tb > b0) tile_out[tb - 1] = defer_sum8(sh + 8 * ((tb - 1) & 1));
+#endif
     #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int m = threadIdx.x + r * kFftThreads;
@@ -1013,9 +1081,19 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft_quad(const __grid_
         }
     }
     if (u0 == 0 && a.zero && threadIdx.x == 0) s += quad_outer<OUTER>(0.0, prm);   // point 0
+#if LQ_FFT_DEFER
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) sh[8 * (tb & 1) + (threadIdx.x >> 5)] = s;
+#else
     s = block_sum_n<kFftThreads>(s, sh);
     if (threadIdx.x == 0) tile_out[tb] = s;
+#endif
     }
+#if LQ_FFT_DEFER
+    __syncthreads();
+    if (threadIdx.x == 0 && b1 > b0) tile_out[b1 - 1] = defer_sum8(sh + 8 * ((b1 - 1) & 1));
+#endif
 }
 
 // ============================================================ generic bytecode
