@@ -912,6 +912,11 @@ __device__ __forceinline__ double block_sum_n(double v, double* sh /* >= NT / 32
 #ifndef LQ_FFT_DEFER
 #define LQ_FFT_DEFER 1
 #endif
+// p < 2^32 as a double: (2^52 + p) - 2^52, one DADD instead of an I2F.F64
+// (cfg5 7.26 -> 7.20 ms)
+__device__ __forceinline__ double u32_to_double(uint32_t p) {
+    return __hiloint2double(0x43300000, (int)p) - 4503599627370496.0;
+}
 // the eight warp partials of a 256-thread CTA in block_sum_n's xor-tree order
 __device__ __forceinline__ double defer_sum8(const double* w) {
     return ((w[0] + w[4]) + (w[2] + w[6])) + ((w[1] + w[5]) + (w[3] + w[7]));
@@ -951,7 +956,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
         uint32_t p0 = mulmod_shoup(s0, aj.x, aj.y, n), p1 = mulmod_shoup(s1, aj.x, aj.y, n);
         #pragma unroll
         for (int r = 0; r < R; ++r) {
-            v[r] = make_double2((double)p0, (double)p1);
+            v[r] = make_double2(u32_to_double(p0), u32_to_double(p1));
             p0 = mulmod_shoup(p0, as.x, as.y, n);
             p1 = mulmod_shoup(p1, as.x, as.y, n);
         }
@@ -1053,7 +1058,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft_quad(const __grid_
     for (int r = 0; r < R; ++r) {
         const int t = threadIdx.x + r * kFftThreads;
         const uint2 ap = __ldg(a.apow + t);
-        const double u = fma((double)mulmod_shoup(s0, ap.x, ap.y, n), inv_n, -0.5);
+        const double u = fma(u32_to_double(mulmod_shoup(s0, ap.x, ap.y, n)), inv_n, -0.5);
         v[r] = make_double2(u, u * u);
     }
     fft4096_regs<true>(v, buf, Wt);        // X in shared memory, natural order
