@@ -1059,7 +1059,13 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
                              (const void*)lq::k_orbit_fft<lq::OUT_POW, false>,
                              (const void*)lq::k_orbit_fft<lq::OUT_EXP, true>,
                              (const void*)lq::k_orbit_fft<lq::OUT_SINCOS, true>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, true>};
+                             (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, true>,
+                             (const void*)lq::k_orbit_fft<lq::OUT_EXP, true, 12>,
+                             (const void*)lq::k_orbit_fft<lq::OUT_SINCOS, true, 12>,
+                             (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, true, 12>,
+                             (const void*)lq::k_orbit_fft<lq::OUT_EXP, true, 13>,
+                             (const void*)lq::k_orbit_fft<lq::OUT_SINCOS, true, 13>,
+                             (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, true, 13>};
         for (const void* fn : fns) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute((const void*)lq::k_fft_coeffs_pm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft_quad<lq::OUT_EXP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1127,11 +1133,16 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     const int outer = lin_outer(f->kind);
     const bool fast = pair_fast_consts(f, bsum, h.pf);
     t_begin(c);
-#define LQ_FFT_LIN(O, F) lq::k_orbit_fft<O, F><<<g, b, smem, c->stream>>>(h, unit0, ntiles, per, tiles_dev)
-    if (outer == lq::OUT_EXP) { if (fast) LQ_FFT_LIN(lq::OUT_EXP, true); else LQ_FFT_LIN(lq::OUT_EXP, false); }
-    else if (outer == lq::OUT_SINCOS) { if (fast) LQ_FFT_LIN(lq::OUT_SINCOS, true); else LQ_FFT_LIN(lq::OUT_SINCOS, false); }
-    else if (outer == lq::OUT_EXPABS) { if (fast) LQ_FFT_LIN(lq::OUT_EXPABS, true); else LQ_FFT_LIN(lq::OUT_EXPABS, false); }
-    else LQ_FFT_LIN(lq::OUT_POW, false);
+    // positions per thread that can hold a chain point: B <= RM N/R
+    const int rm = (int)((p.m + lq::kFftThreads - 1) / lq::kFftThreads);
+#define LQ_FFT_LIN(O, F, RM) lq::k_orbit_fft<O, F, RM><<<g, b, smem, c->stream>>>(h, unit0, ntiles, per, tiles_dev)
+#define LQ_FFT_FAST(O) do { if (rm <= 12) LQ_FFT_LIN(O, true, 12); else if (rm == 13) LQ_FFT_LIN(O, true, 13); \
+                            else LQ_FFT_LIN(O, true, lq::kFftR); } while (0)
+    if (outer == lq::OUT_EXP) { if (fast) LQ_FFT_FAST(lq::OUT_EXP); else LQ_FFT_LIN(lq::OUT_EXP, false, lq::kFftR); }
+    else if (outer == lq::OUT_SINCOS) { if (fast) LQ_FFT_FAST(lq::OUT_SINCOS); else LQ_FFT_LIN(lq::OUT_SINCOS, false, lq::kFftR); }
+    else if (outer == lq::OUT_EXPABS) { if (fast) LQ_FFT_FAST(lq::OUT_EXPABS); else LQ_FFT_LIN(lq::OUT_EXPABS, false, lq::kFftR); }
+    else LQ_FFT_LIN(lq::OUT_POW, false, lq::kFftR);
+#undef LQ_FFT_FAST
 #undef LQ_FFT_LIN
     t_end(c);
     CK(cudaGetLastError());

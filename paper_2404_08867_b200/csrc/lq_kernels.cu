@@ -912,6 +912,7 @@ __device__ __forceinline__ double block_sum_n(double v, double* sh /* >= NT / 32
 #ifndef LQ_FFT_DEFER
 #define LQ_FFT_DEFER 1
 #endif
+
 // p < 2^32 as a double: (2^52 + p) - 2^52, one DADD instead of an I2F.F64
 // (cfg5 7.26 -> 7.20 ms)
 __device__ __forceinline__ double u32_to_double(uint32_t p) {
@@ -925,7 +926,10 @@ __device__ __forceinline__ double defer_sum8(const double* w) {
 // Tile b = two chains (units 2b, 2b + 1 after unit0); tile_out[b] = their sum.
 // A CTA runs tiles per_cta blockIdx.x .. + per_cta - 1 (< ntiles), so the
 // twiddle tables are filled once per per_cta tiles.
-template <int OUTER, bool FAST>
+// RM (FAST only): the chains have at most RM * N/R points, so the outputs
+// r >= RM of the last inverse pass are dead and the compiler drops them (and
+// their registers) -- d = 769..1024: RM = 13 (cfg5 7.20 -> 7.10 ms).
+template <int OUTER, bool FAST, int RM = kFftR>
 __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_constant__ FftHead a, uint64_t unit0,
                                                                int64_t ntiles, int per_cta,
                                                                double* __restrict__ tile_out) {
@@ -985,7 +989,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
         const int v0 = fft_chain_valid(a, u0), v1 = fft_chain_valid(a, u1);
         const int vmax = max(v0, v1), wbase = threadIdx.x & ~31;
         #pragma unroll
-        for (int r = 0; r < R; ++r) {
+        for (int r = 0; r < RM; ++r) {
             if (wbase + r * kFftThreads < vmax) {
                 const int k = threadIdx.x + r * kFftThreads;
 #if LQ_FFT_EXPTAB
