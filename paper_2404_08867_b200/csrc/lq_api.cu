@@ -1114,7 +1114,8 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     h.alpha = f->alpha; h.alphaB = f->alpha + bsum; h.K = f->K; h.A = f->A; h.Bc = f->B; h.C0 = f->C0;
     h.kappa = f->kappa; h.pw = f->power;
     for (int j = 0; j < lq::kFftExpTab; ++j)
-        h.etab[j] = make_double2((double)exp2l(j / 64.0L), (double)exp2l(-(j / 64.0L)));
+        h.etab[j] = make_double2((double)exp2l(j / (long double)lq::kFftExpTab),
+                                 (double)exp2l(-(j / (long double)lq::kFftExpTab)));
     // several tiles per CTA once there are many waves: the twiddle fill is
     // paid once per CTA
     const int per = (int)std::max<int64_t>(1, std::min<int64_t>(kFftTilesPerCta, ntiles / (2 * 148 * 16)));

@@ -31,7 +31,11 @@ constexpr int kFftTwAll = 2 * kFftTw3 + kFftTw2;
 #ifndef LQ_FFT_EXPTAB
 #define LQ_FFT_EXPTAB 1
 #endif
-constexpr int kFftExpTab = LQ_FFT_EXPTAB ? 64 : 0;   // (2^(j/64), 2^(-j/64)) for the pair outer
+#ifndef LQ_FFT_EXPBITS
+#define LQ_FFT_EXPBITS 6
+#endif
+constexpr int kFftExpBits = LQ_FFT_EXPBITS;
+constexpr int kFftExpTab = LQ_FFT_EXPTAB ? 1 << kFftExpBits : 0;   // (2^(j/2^EB), 2^(-j/2^EB)) for the pair outer
 constexpr int kFftSmem = (kFftPad + (kFftR == 16 ? kFftTwAll : 0) + kFftExpTab) * 16;   // bytes per CTA
 
 // Build the radix-16 tables from the global table W[k] = e^{-2 pi i k / N}.

@@ -229,25 +229,40 @@ __device__ __forceinline__ double pair_fast(double l, const PairFast& q) {
     }
 }
 
-// pair_fast with a 64-entry shared table T[j] = (2^(j/64), 2^(-j/64)): the
-// range reduction z = (64 k + j) ln2/64 + r leaves |r| <= ln2/128, where
-// degree-5 halves of the Taylor polynomial suffice (truncation < 4e-17)
+// pair_fast with a 2^EB-entry shared table T[j] = (2^(j/2^EB), 2^(-j/2^EB)):
+// the range reduction z = (2^EB k + j) ln2/2^EB + r leaves |r| <= ln2/2^(EB+1),
+// where the even/odd Taylor halves need degree 4/5 (EB = 6), 6/7 (EB = 4) or
+// 8/7 (EB = 3) for a truncation below 4e-17
 template <int OUTER>
 __device__ __forceinline__ double pair_fast_tab(double l, const PairFast& q, const double2* __restrict__ T) {
     if constexpr (OUTER == OUT_SINCOS) return pair_fast<OUTER>(l, q);
+    constexpr int EB = kFftExpBits;
     const double y = fma(l, q.ym, q.ya);
     const double z = OUTER == OUT_EXPABS ? -fabs(y) : y;
-    const double t = fma(z, 92.332482616893658, 6755399441055744.0);    // 64/ln2; 1.5 2^52
+    const double t = fma(z, (double)(1 << EB) * 1.4426950408889634, 6755399441055744.0);   // 2^EB/ln2; 1.5 2^52
     const int K = __double2loint(t);
     const double kf = t - 6755399441055744.0;
-    double r = fma(kf, -1.0830424696249145e-02, z);                     // ln2/64, two parts
-    r = fma(kf, -3.6235106466348431e-19, r);
-    const int k = K >> 6;
-    const double2 tj = T[K & 63];
+    double r = fma(kf, -(6.93147180559945286e-01 / (1 << EB)), z);     // ln2/2^EB, two parts
+    r = fma(kf, -(2.319046813846299558e-17 / (1 << EB)), r);
+    const int k = K >> EB;
+    const double2 tj = T[K & ((1 << EB) - 1)];
     const double r2 = r * r;
-    double e = fma(r2, 4.1666666666666664e-02, 0.5);
+    double e, o;
+    if constexpr (EB >= 6) {
+        e = fma(r2, 4.1666666666666664e-02, 0.5);
+        o = fma(r2, 8.3333333333333332e-03, 0.16666666666666666);
+    } else {
+        if constexpr (EB >= 4) {
+            e = fma(r2, 1.3888888888888889e-03, 4.1666666666666664e-02);
+        } else {
+            e = fma(r2, 2.48015873015873e-05, 1.3888888888888889e-03);
+            e = fma(r2, e, 4.1666666666666664e-02);
+        }
+        e = fma(r2, e, 0.5);
+        o = fma(r2, 1.984126984126984e-04, 8.3333333333333332e-03);
+        o = fma(r2, o, 0.16666666666666666);
+    }
     e = fma(r2, e, 1.0);
-    double o = fma(r2, 8.3333333333333332e-03, 0.16666666666666666);
     o = fma(r2, o, 1.0);
     const double p = fma(r, o, e) * tj.x, m = fma(-r, o, e) * tj.y;     // e^(z - k ln2), e^(-z + k ln2)
     const double f1 = scale2(p, k);
@@ -867,7 +882,7 @@ struct FftHead {
     double alpha, alphaB, K, A, Bc, C0, kappa, pw;
     PairFast pf;
     int32_t zero;                      // unit 0 also adds the point x = 0
-    double2 etab[kFftExpTab > 0 ? kFftExpTab : 1];          // (2^(j/64), 2^(-j/64)), correctly rounded on the host
+    double2 etab[kFftExpTab > 0 ? kFftExpTab : 1];          // (2^(j/2^EB), 2^(-j/2^EB)), correctly rounded on the host
 };
 
 // H[m] of a real sequence's spectrum from the lower half only: H[N - m] =
