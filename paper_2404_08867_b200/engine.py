@@ -268,20 +268,32 @@ def cf_quadrature(beta, counts, alpha, kappa):
     return nodes, weights, probes, sigma
 
 
+_cf_cache = _LRU(16)
+
+
+def _cf_inputs(beta, counts, alpha, kappa):
+    """Contiguous device-call inputs of mdi_expabs_cf, cached per integrand and grid."""
+    beta = np.ascontiguousarray(beta, dtype=np.float64)
+    key = (beta.tobytes(), tuple(int(c) for c in counts), float(alpha), float(kappa))
+
+    def make():
+        nodes, weights, probes, _ = cf_quadrature(beta, counts, alpha, kappa)
+        wn = np.ascontiguousarray(np.concatenate([nodes, probes]))
+        ww = np.ascontiguousarray(np.concatenate([weights, np.zeros_like(probes)]))
+        return beta, np.ascontiguousarray(counts, dtype=np.int32), wn, ww, len(nodes)
+    return _cf_cache.get_or(key, make)
+
+
 def mdi_expabs_cf(beta, counts, alpha, kappa):
     """E = mean over the midpoint grid of exp(kappa |alpha + <beta, y>|), kappa < 0,
     by the characteristic function on the GPU (lq_mdi_expabs).  Returns
     (E, tail_bound) where tail_bound bounds |prod_j phi_j| beyond Omega."""
-    beta = np.ascontiguousarray(beta, dtype=np.float64)
-    cnt = np.ascontiguousarray(counts, dtype=np.int32)
-    nodes, weights, probes, sigma = cf_quadrature(beta, counts, alpha, kappa)
-    wn = np.ascontiguousarray(np.concatenate([nodes, probes]))
-    ww = np.ascontiguousarray(np.concatenate([weights, np.zeros_like(probes)]))
+    beta, cnt, wn, ww, n_nodes = _cf_inputs(beta, counts, alpha, kappa)
     out = np.zeros(2)
     logmag = np.zeros(len(wn))
     N.check(N.lib().lq_mdi_expabs(N.ctx(), len(beta), N.as_ptr(beta), N.as_ptr(cnt), float(alpha),
                                   N.as_ptr(wn), N.as_ptr(ww), len(wn), float(kappa), N.as_ptr(out),
                                   N.as_ptr(logmag)))
     E = out[1] * math.exp(out[0]) * 2.0 / math.pi
-    tail = float(np.exp(np.max(logmag[len(nodes):]))) if len(probes) else 0.0
+    tail = float(np.exp(np.max(logmag[n_nodes:]))) if len(wn) > n_nodes else 0.0
     return E, tail

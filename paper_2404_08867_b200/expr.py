@@ -47,7 +47,7 @@ class Expr:
     'exp', 'sin', 'cos', 'abs' (args = (arg,)).
     """
 
-    __slots__ = ("op", "val", "idx", "args", "terms", "_key", "_hash", "_fv")
+    __slots__ = ("op", "val", "idx", "args", "terms", "_key", "_hash", "_fv", "_fvb")
 
     def __init__(self, op, val=0.0, idx=0, args=(), terms=()):
         self.op = op
@@ -62,6 +62,7 @@ class Expr:
         self._key = key
         self._hash = hash(key)
         self._fv = None
+        self._fvb = None
 
     def __hash__(self):
         return self._hash
@@ -255,10 +256,18 @@ def node_count(e):
 
 
 def free_vars(e):
-    """Set of 1-based coordinate indices in e (cached on the node)."""
+    """Frozen set of 1-based coordinate indices in e (cached on the node)."""
     if e._fv is None:
         e._fv = frozenset(n.idx for n in topo(e) if n.op == "var")
-    return set(e._fv)
+    return e._fv
+
+
+def var_bounds(e):
+    """(min, max) of free_vars(e), or None without variables (cached on the node)."""
+    if e._fvb is None:
+        fv = free_vars(e)
+        e._fvb = (min(fv), max(fv)) if fv else ()
+    return e._fvb or None
 
 
 def evaluate(e, assignment):

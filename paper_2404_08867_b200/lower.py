@@ -486,7 +486,7 @@ _TERM_CAP = 1024
 
 def _univ(e):
     fv = free_vars(e)
-    return fv.pop() if len(fv) == 1 else (0 if not fv else None)
+    return next(iter(fv)) if len(fv) == 1 else (0 if not fv else None)
 
 
 def _fmul(f1, f2):

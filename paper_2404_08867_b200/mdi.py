@@ -30,7 +30,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import engine
-from .expr import as_expr, evaluate, free_vars
+from .expr import as_expr, evaluate, free_vars, var_bounds
 from .lattice import korobov_vector
 from .transform import midpoint_grids
 
@@ -151,10 +151,11 @@ def mdi_sum(g, grids, cfg=None):
     cfg = cfg if cfg is not None else MdiConfig()
     d = grids.d
     e = as_expr(g)
-    extra = free_vars(e) - set(range(1, d + 1))
-    if extra:
+    vb = var_bounds(e)
+    if vb and (vb[0] < 1 or vb[1] > d):
+        extra = free_vars(e) - set(range(1, d + 1))
         raise ValueError(f"integrand uses coordinates {sorted(extra)} beyond the {d} axes")
-    counts = tuple(grids.counts)
+    counts = grids.counts if isinstance(grids.counts, tuple) else tuple(grids.counts)
     levels, base_axes = _level_plan(d, cfg)
     t0 = time.perf_counter()
 
@@ -168,7 +169,7 @@ def mdi_sum(g, grids, cfg=None):
     midpoint = getattr(grids, "midpoint", False)
     plan = engine.separable_plan(e, counts, None if midpoint else grids.nodes)
     usable = plan.ok and (plan.n_factors + plan.n_terms) <= cfg.budget
-    total = _total(tuple(counts))
+    total = _total(counts)
     if (not usable and total > cfg.direct_cap and getattr(grids, "midpoint", False)
             and cfg.fallback == "numeric"):
         rep = _characteristic(e, d, counts, levels, base_axes, t0)
@@ -206,11 +207,11 @@ def _characteristic(e, d, counts, levels, base_axes, t0):
     if fam is None or fam.kind != "lin_expabs" or not fam.kappa < 0.0 or fam.K == 0.0:
         return None
     beta = np.asarray(fam.beta, dtype=np.float64)
-    log_total = _log_total(tuple(counts))
+    log_total = _log_total(counts)
     if not np.any(beta):
         mean = math.exp(fam.kappa * abs(fam.alpha))
     else:
-        if len(counts) < 2 or max(counts) > 2**31 - 1:
+        if len(counts) < 2 or _grid_facts(counts).max_count > 2**31 - 1:
             return None
         mean, tail = engine.mdi_expabs_cf(beta, counts, fam.alpha, fam.kappa)
         if not (mean > 0.0) or tail > 1e-16 * mean:
@@ -223,10 +224,17 @@ def _characteristic(e, d, counts, levels, base_axes, t0):
 
 
 def _normalize(raw, counts):
-    """raw / prod(counts) without overflowing float (mdi.py:195-203)."""
-    total = _total(tuple(counts))
-    if total <= 2**53:
-        return raw / total
+    """raw / prod(counts) without overflowing float (mdi.py:195-203).  With
+    power-of-two counts every division is exact while the running value stays
+    normal, so a normal result equals one ldexp (the running magnitude only
+    decreases); otherwise the reference's division sequence runs as is."""
+    facts = _grid_facts(counts)
+    if facts.total <= 2**53:
+        return raw / facts.total
+    if facts.shift is not None:
+        out = math.ldexp(raw, -facts.shift)
+        if raw == 0.0 or not math.isfinite(raw) or abs(out) >= 2.2250738585072014e-308:
+            return out
     out = raw
     for ct in counts:
         out /= ct
@@ -253,15 +261,44 @@ def _det_a(rule):
         return 0.0
 
 
-@functools.lru_cache(maxsize=64)
+@dataclass(frozen=True)
+class _GridFacts:
+    total: int          # prod(counts), exact (thousands of bits at d = 1000)
+    log_total: float    # sum log n_i
+    shift: int | None   # sum log2 n_i when every n_i is a power of two
+    max_count: int
+
+
+_facts_cache: dict = {}
+
+
+def _grid_facts(counts):
+    """Per-grid constants, cached by the identity of the (immutable) counts
+    tuple: a cached grid set hands the same tuple to every call, so the
+    1000-entry tuple is neither hashed nor walked again (MDI-LR
+    time-to-solution, cfg4/cfg5)."""
+    ent = _facts_cache.get(id(counts))
+    if ent is not None and ent[0] is counts:
+        return ent[1]
+    cs = tuple(counts)
+    pow2 = all(c > 0 and c & (c - 1) == 0 for c in cs)
+    facts = _GridFacts(total=math.prod(cs) if cs else 1,
+                       log_total=float(sum(math.log(c) for c in cs)),
+                       shift=sum(c.bit_length() - 1 for c in cs) if pow2 else None,
+                       max_count=max(cs) if cs else 0)
+    if len(_facts_cache) >= 64:
+        _facts_cache.clear()
+    _facts_cache[id(counts)] = (counts, facts)
+    return facts
+
+
 def _log_total(counts):
-    return float(sum(math.log(c) for c in counts))
+    return _grid_facts(counts).log_total
 
 
-@functools.lru_cache(maxsize=64)
 def _total(counts):
-    """prod(counts) as an exact integer (thousands of bits at d = 1000), cached."""
-    return math.prod(counts) if counts else 1
+    """prod(counts) as an exact integer, cached."""
+    return _grid_facts(counts).total
 
 
 def mdi_lr(f, d, a, n, cfg=None, rule=None, with_report=False):
