@@ -122,3 +122,23 @@ def test_fft_pair_fast(env, family, scale, offset, monkeypatch):
     assert math.isclose(fast, slow, rel_tol=1e-13, abs_tol=1e-300), (fast, slow)
     ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
     assert math.isclose(fast, ref, rel_tol=REL, abs_tol=1e-300), (fast, ref)
+
+
+@pytest.mark.parametrize("family", ["exp", "expabs", "sincos"])
+@pytest.mark.parametrize("d", [768, 769, 1024, 1025])
+def test_fft_position_bound_boundaries(env, family, d, monkeypatch):
+    """The compile-time bound RM on the positions a chain reaches (RM * 256 >=
+    B = 4097 - d; RM = 16 / 13 / 13 / 12 at these d) drops the dead outputs of
+    the last inverse pass: the sums must not change at the switch points."""
+    lq, N, engine = env
+    n, g = 100003, 2
+    while any(pow(g, (n - 1) // p, n) == 1 for p in (2, 3, 7, 2381)):
+        g += 1
+    rng = np.random.default_rng(zlib.crc32(f"rm/{family}/{d}".encode()))
+    f = lq.parse(_family_text(family, d, rng), d)
+    rule = lq.korobov_vector(g, n, d)
+    pi = engine.plain_integrand(f, d)
+    got = _sums(engine, N, pi, n, rule.z_reduced_array(), monkeypatch)
+    fft = got.pop(N.LAYOUT_ORBIT_FFT)
+    (direct,) = got.values()
+    assert math.isclose(fft, direct, rel_tol=1e-12, abs_tol=1e-12 * n), (family, d, fft, direct)
