@@ -65,6 +65,7 @@ struct lq_ctx {
     size_t dcap[B_NBUF] = {};
     void* hpin = nullptr;      // pinned host staging
     size_t hcap = 0;
+    size_t hoff = 0;           // uploads staged since the stream last drained: [0, hoff) may be in flight
     bool timing = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_ms = 0.f;
@@ -117,14 +118,22 @@ int pin_buf(lq_ctx* c, size_t bytes, void** out) {
 
 // H2D through the pinned staging buffer (async on the ctx stream; the
 // staging buffer is reused only after the stream drains it).
+// Consecutive uploads take consecutive slices of the staging buffer, so a
+// call's several parameter uploads cost one stream drain, not one each; the
+// slices are recycled only once the stream has drained them.
 int upload(lq_ctx* c, int which, const void* src, size_t bytes, void** dst) {
     int rc = dev_buf(c, which, bytes, dst);
     if (rc) return rc;
     if (bytes == 0) return LQ_OK;
-    void* h;
-    CK(cudaStreamSynchronize(c->stream));
-    rc = pin_buf(c, bytes, &h);
-    if (rc) return rc;
+    const size_t need = (bytes + 255) & ~(size_t)255;
+    if (c->hoff + need > c->hcap) {
+        CK(cudaStreamSynchronize(c->stream));
+        c->hoff = 0;
+        void* h;
+        if ((rc = pin_buf(c, std::max<size_t>(need, 1 << 20), &h))) return rc;
+    }
+    char* h = (char*)c->hpin + c->hoff;
+    c->hoff += need;
     memcpy(h, src, bytes);
     CK(cudaMemcpyAsync(*dst, h, bytes, cudaMemcpyHostToDevice, c->stream));
     return LQ_OK;
@@ -180,8 +189,11 @@ int read_scalar(lq_ctx* c, const double* dev, double* out, int k = 1) {
     void* h = nullptr;
     int rc = pin_buf(c, sizeof(double) * k, &h);
     if (rc) return rc;
+    // (staged uploads still in flight read their slices before this copy
+    // writes: same stream, in order)
     CK(cudaMemcpyAsync(h, dev, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    c->hoff = 0;
     memcpy(out, h, sizeof(double) * k);
     return LQ_OK;
 }
@@ -1415,6 +1427,7 @@ int lq_ctx_set_stream(lq_ctx* c, void* stream) {
     int rc = set_dev(c);
     if (rc) return rc;
     CK(cudaStreamSynchronize(c->stream));
+    c->hoff = 0;
     c->stream = stream ? (cudaStream_t)stream : c->own;
     return LQ_OK;
 }
