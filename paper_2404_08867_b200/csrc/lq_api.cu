@@ -71,6 +71,10 @@ struct lq_ctx {
     float last_ms = 0.f;
     int64_t launches = 0;
     bool fft_w = false;        // twiddles computed in dbuf[B_FFTW]
+    // coefficients whose spectrum dbuf[B_FFTH] holds (the coefficient
+    // transform is skipped when the next sum uses the same ones)
+    std::vector<double> fft_key;
+    const void* fft_key_buf = nullptr;
     // device copies of orbit-plan tables by plan id (a 2^k rule has one plan per level)
     std::map<uint64_t, std::pair<void*, size_t>> orb_tabs;
 };
@@ -1104,21 +1108,36 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
             bq[d + j] = f->gamma[j];
             bsum += 0.5 * f->beta[j] + 0.25 * f->gamma[j];
         }
-        if ((rc = upload(c, B_AUX0, bq.data(), sizeof(double) * bq.size(), &dc))) return rc;
-        lq::k_fft_coeffs_pm<<<1, lq::kFftThreads, smem, c->stream>>>((const double*)dc, (const double*)dc + d, d,
-                                                                    (const double2*)W, (double2*)Hc,
-                                                                    (double2*)Hc + lq::kFftN);
+        bq.push_back(1.0);   // key tags: the Gaussian pair of spectra, d
+        bq.push_back((double)d);
+        if (c->fft_key != bq || c->fft_key_buf != Hc) {
+            if ((rc = upload(c, B_AUX0, bq.data(), sizeof(double) * 2 * d, &dc))) return rc;
+            lq::k_fft_coeffs_pm<<<1, lq::kFftThreads, smem, c->stream>>>((const double*)dc, (const double*)dc + d, d,
+                                                                        (const double2*)W, (double2*)Hc,
+                                                                        (double2*)Hc + lq::kFftN);
+            c->launches++;   // the coefficient transform
+            CK(cudaGetLastError());
+            c->fft_key.swap(bq);
+            c->fft_key_buf = Hc;
+        }
     } else {
         std::vector<double> cv(d);
         for (int j = 0; j < d; ++j) {
             cv[j] = f->beta[j] / nd;
             bsum += f->beta[j];
         }
-        if ((rc = upload(c, B_AUX0, cv.data(), sizeof(double) * d, &dc))) return rc;
-        lq::k_fft_coeffs<<<1, lq::kFftThreads, smem, c->stream>>>((const double*)dc, d, (const double2*)W, (double2*)Hc);
+        cv.push_back(0.0);   // key tags: one real spectrum, d
+        cv.push_back((double)d);
+        if (c->fft_key != cv || c->fft_key_buf != Hc) {
+            if ((rc = upload(c, B_AUX0, cv.data(), sizeof(double) * d, &dc))) return rc;
+            lq::k_fft_coeffs<<<1, lq::kFftThreads, smem, c->stream>>>((const double*)dc, d, (const double2*)W,
+                                                                      (double2*)Hc);
+            c->launches++;   // the coefficient transform
+            CK(cudaGetLastError());
+            c->fft_key.swap(cv);
+            c->fft_key_buf = Hc;
+        }
     }
-    c->launches++;   // the coefficient transform
-    CK(cudaGetLastError());
     lq::FftHead h{};
     h.n = p.n; h.B = (uint32_t)p.m; h.units = p.units; h.qc = p.qc; h.h = p.h; h.zero = p.zero ? 1 : 0;
     h.G = G; h.Alo = Alo; h.Ahi = Ahi; h.apow = apow; h.starts = starts; h.W = (const double2*)W;
