@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define LQ_ABI_VERSION 4
+#define LQ_ABI_VERSION 5
 
 #define LQ_OK 0
 #define LQ_ERR_VALUE (-1)
@@ -212,6 +212,27 @@ int lq_mdi_sum(lq_ctx* ctx, const lq_insn* insn, int32_t n_insn, const lq_factor
 int lq_mdi_expabs(lq_ctx* ctx, int32_t d, const double* beta, const int32_t* counts, double alpha,
                   const double* w_nodes, const double* w_weights, int32_t n_w, double kappa,
                   double* out2, double* logmag_out /* optional [n_w]: log|prod_j phi_j(w_k)| */);
+
+/* ---- MDI-LR level collapse for f = G(alpha + <beta, y>): replaces the level
+ * loop of mdi.mdi_sum (mdi.py:152-165) for integrands whose coordinates enter
+ * through one linear form with commensurate steps, where the reference's
+ * partial_sum + like-term collection (exprcore.py:139-169, 374-402) merges
+ * the partial sums with equal constants level by level (corpus invpow).
+ * Direction l (levels with m_l != 0 only) contributes |m_l| t, t uniform on
+ * [0, counts[l]); the engine convolves the distribution of
+ * k = sum_l |m_l| t_l level by level (shared memory up to 12800 support
+ * points, global memory up to LQ_LINFORM_MAX_SUPPORT) and sums
+ * p(k) G(alpha + h (m0 + 2k)) over fixed tiles of LQ_TILE support points.
+ * G: one-variable program (variable 0).
+ * tiles_dev == NULL: out[0] = grid mean (shard 0 of 1).
+ * tiles_dev != NULL: tiles_dev[0 .. T) = tile partials of this shard's tiles
+ * [floor(shard T / nshards), floor((shard+1) T / nshards)), zero elsewhere;
+ * out[0] = T = ceil(K / LQ_TILE), K = 1 + sum_l |m_l| (counts[l] - 1);
+ * the mean is lq_reduce_sum of the (all-reduced) tile vector.              */
+#define LQ_LINFORM_MAX_SUPPORT (((int64_t)1) << 28)
+int lq_mdi_linform(lq_ctx* ctx, const lq_program* G, int32_t n_levels, const int64_t* m, const int32_t* counts,
+                   double alpha, double h, int64_t m0, int32_t shard, int32_t nshards, double* tiles_dev,
+                   int64_t tiles_cap, double* out);
 
 /* ---- lattice quality measures and constructions (
  * lattice.py:140-311).  B_alpha and the factors 1 + g_j (B + beta) follow

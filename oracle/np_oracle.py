@@ -198,3 +198,46 @@ def expabs_grid_mean_dp(k, Q, N, alpha, kappa):
     m = np.arange(size, dtype=np.float64)
     L = alpha + m / (2.0 * N * Q)
     return float(np.sum(pmf * np.exp(kappa * np.abs(L))))
+
+
+def linear_form_grid_mean_exact(G, steps, counts, alpha=0.0):
+    """Mean of G(alpha + sum_j steps_j * (t_j + 1/2)) over the midpoint grid
+    t_j in [0, counts_j), with rational steps (Fractions): the multiset of
+    partial linear-form values the reference's level loop carries after
+    like-term collection (mdi.py:152-165 with exprcore.py:139-169, 390-402),
+    built one axis at a time as {exact value: multiplicity}, then G once per
+    distinct value.  Pure Python, small grids only."""
+    from fractions import Fraction
+    dist = {Fraction(0): 1}
+    for s, n in zip(steps, counts):
+        s = Fraction(s)
+        nxt = {}
+        for v, cnt in dist.items():
+            for t in range(n):
+                key = v + s * (2 * t + 1) / 2
+                nxt[key] = nxt.get(key, 0) + cnt
+        dist = nxt
+    total = math.prod(counts)
+    return math.fsum(cnt * float(G(alpha + float(v))) for v, cnt in dist.items()) / total
+
+
+def linear_form_grid_mean_np(G, k_steps, counts, alpha, h):
+    """Same mean for integer steps: the form is alpha + h * sum_j k_j (2 t_j + 1);
+    numpy pmf convolution, for supports too large for
+    ``linear_form_grid_mean_exact``."""
+    lo = sum(k * (1 if k > 0 else 2 * n - 1) for k, n in zip(k_steps, counts))
+    size = sum(abs(k) * 2 * (n - 1) for k, n in zip(k_steps, counts)) + 1
+    pmf = np.zeros(size)
+    pmf[0] = 1.0
+    top = 0
+    for k, n in zip(k_steps, counts):
+        a = abs(k)
+        nxt = np.zeros(size)
+        for t in range(n):
+            nxt[2 * a * t:2 * a * t + top + 1] += pmf[:top + 1]
+        top += 2 * a * (n - 1)
+        pmf = nxt / n
+    pos = lo + np.arange(size, dtype=np.float64)
+    vals = G(alpha + h * pos)
+    mask = pmf > 0
+    return float(np.sum(pmf[mask] * vals[mask]))

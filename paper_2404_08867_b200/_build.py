@@ -1,4 +1,4 @@
-"""Build liblq.so in-tree for sm_100a (and the C oracle, which is test-only).
+"""Build liblq.so in-tree for sm_100a.
 
     python -m paper_2404_08867_b200._build
 """
@@ -44,7 +44,10 @@ def build_native(force=False, verbose=False):
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
-    with open(os.path.join(CSRC, "ptxas.log"), "w") as fh:
+    # ptxas register/spill report of the last build (untracked; copies that
+    # matter for a profile go to profiles/)
+    os.makedirs(os.path.join(REPO, "build"), exist_ok=True)
+    with open(os.path.join(REPO, "build", "ptxas.log"), "w") as fh:
         fh.write(res.stderr)
     os.replace(tmp, LIB)
     if verbose:
@@ -52,25 +55,5 @@ def build_native(force=False, verbose=False):
     return LIB
 
 
-def build_oracle(force=False, verbose=False):
-    """Compile the C oracle (test infrastructure) into oracle/build/liblqoracle.so."""
-    src = os.path.join(REPO, "oracle", "c", "lq_oracle.c")
-    if not os.path.exists(src):
-        return None
-    out_dir = os.path.join(REPO, "oracle", "build")
-    os.makedirs(out_dir, exist_ok=True)
-    out = os.path.join(out_dir, "liblqoracle.so")
-    if not force and not _stale(out, [src]):
-        return out
-    cmd = ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-ffp-contract=off", "-o", out, src, "-lm"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError("gcc failed:\n" + res.stdout + res.stderr)
-    if verbose:
-        print(f"built {out}")
-    return out
-
-
 if __name__ == "__main__":
     build_native(force="--force" in sys.argv, verbose=True)
-    build_oracle(force="--force" in sys.argv, verbose=True)

@@ -1895,6 +1895,99 @@ int lq_mdi_expabs(lq_ctx* c, int32_t d, const double* beta, const int32_t* count
     return LQ_OK;
 }
 
+// MDI level collapse for G(alpha + <beta, y>) (lq.h): the distribution of the
+// partial linear form level by level, then G over its support.
+int lq_mdi_linform(lq_ctx* c, const lq_program* G, int32_t n_levels, const int64_t* m, const int32_t* counts,
+                   double alpha, double h, int64_t m0, int32_t shard, int32_t nshards, double* tiles_dev,
+                   int64_t tiles_cap, double* out) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (!G || !G->insn || G->n_insn < 1) return fail(LQ_ERR_VALUE, "null program");
+    if (G->n_vars > 1) return fail(LQ_ERR_VALUE, "G must be univariate (variable 0), uses %d", G->n_vars);
+    if (n_levels < 0 || (n_levels > 0 && (!m || !counts))) return fail(LQ_ERR_VALUE, "bad levels");
+    if (nshards < 1 || shard < 0 || shard >= nshards) return fail(LQ_ERR_VALUE, "bad shard %d of %d", shard, nshards);
+    if (!out) return fail(LQ_ERR_VALUE, "null output");
+    if (!tiles_dev && nshards != 1) return fail(LQ_ERR_VALUE, "sharded calls need tiles_dev");
+    const int ns = pick_slots(G->n_slots);
+    if (ns < 0) return fail(LQ_ERR_UNSUPPORTED, "program needs %d slots (max %d)", G->n_slots, LQ_MAX_SLOTS);
+    std::vector<lq::LinLevel> lv;
+    int64_t K = 1;
+    for (int l = 0; l < n_levels; ++l) {
+        if (m[l] < 1 || counts[l] < 1)
+            return fail(LQ_ERR_VALUE, "level %d: m = %lld, N = %d", l, (long long)m[l], counts[l]);
+        if (m[l] > LQ_LINFORM_MAX_SUPPORT / counts[l]) return fail(LQ_ERR_UNSUPPORTED, "level %d step too large", l);
+        K += m[l] * (counts[l] - 1);
+        if (K > LQ_LINFORM_MAX_SUPPORT) return fail(LQ_ERR_UNSUPPORTED, "support exceeds %lld points", (long long)LQ_LINFORM_MAX_SUPPORT);
+        lv.push_back({m[l], counts[l], 0});
+    }
+    if (std::fabs((double)m0) + 2.0 * (double)K > 9007199254740992.0)
+        return fail(LQ_ERR_UNSUPPORTED, "support positions exceed 2^53");
+    const int64_t T = (K + LQ_TILE - 1) / LQ_TILE;
+    if (tiles_dev && tiles_cap < T)
+        return fail(LQ_ERR_VALUE, "tiles_dev holds %lld tiles, need %lld", (long long)tiles_cap, (long long)T);
+    void *dlv = nullptr, *dp, *dq = nullptr, *dg;
+    if (!lv.empty() && (rc = upload(c, B_AUX0, lv.data(), sizeof(lq::LinLevel) * lv.size(), &dlv))) return rc;
+    if ((rc = upload(c, B_PROG, G->insn, sizeof(lq_insn) * G->n_insn, &dg))) return rc;
+    if ((rc = dev_buf(c, B_AUX1, sizeof(double) * K, &dp))) return rc;
+    constexpr int64_t kSmemCap = (200 * 1024) / (2 * (int64_t)sizeof(double));   // 12800 support points
+    const char* force_global = std::getenv("LQ_LINFORM_SMEM");   // "0": global-memory levels (tests)
+    t_begin(c);
+    if (K <= kSmemCap && !(force_global && !std::strcmp(force_global, "0"))) {
+        CK(cudaFuncSetAttribute((const void*)lq::k_linform_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(2 * sizeof(double) * kSmemCap)));
+        lq::k_linform_smem<<<1, 1024, 2 * sizeof(double) * K, c->stream>>>((const lq::LinLevel*)dlv, n_levels, K,
+                                                                           (double*)dp);
+        c->launches++;
+        CK(cudaGetLastError());
+    } else {
+        if ((rc = dev_buf(c, B_AUX2, sizeof(double) * K, &dq))) return rc;
+        // ping-pong between dp and dq so that the last level lands in dp
+        double* cur = (double*)(n_levels % 2 ? dq : dp);
+        double* nxt = (double*)(n_levels % 2 ? dp : dq);
+        lq::k_fill<<<1, 32, 0, c->stream>>>(cur, 1, 1.0);
+        c->launches++;
+        int64_t k_old = 1;
+        for (int l = 0; l < n_levels; ++l) {
+            const int64_t kn = k_old + lv[l].m * (lv[l].n - 1);
+            const int grid = (int)std::min<int64_t>((kn + lq::kThreads - 1) / lq::kThreads, (int64_t)c->sm_count * 8);
+            lq::k_linform_level<<<grid, lq::kThreads, 0, c->stream>>>(cur, k_old, lv[l].m, lv[l].n, nxt);
+            c->launches++;
+            CK(cudaGetLastError());
+            std::swap(cur, nxt);
+            k_old = kn;
+        }
+    }
+    // tile partials: this shard's tiles [t0, t1) of the fixed tiling of the support
+    const int64_t t0 = (int64_t)shard * T / nshards, t1 = (int64_t)(shard + 1) * T / nshards;
+    void* tiles = tiles_dev;
+    if (!tiles) {
+        if ((rc = dev_buf(c, B_TILES, sizeof(double) * T, &tiles))) return rc;
+    } else {
+        CK(cudaMemsetAsync(tiles, 0, sizeof(double) * T, c->stream));
+    }
+    if (t1 > t0) {
+        const int grid = (int)std::min<int64_t>(t1 - t0, (int64_t)c->sm_count * 4);
+        if (ns == 32)
+            lq::k_linform_eval<32><<<grid, lq::kThreads, 0, c->stream>>>(
+                (const lq_insn*)dg, G->n_insn, G->result, (const double*)dp, K, alpha, h, (double)m0, t0, t1, 0,
+                (double*)tiles);
+        else
+            lq::k_linform_eval<LQ_MAX_SLOTS><<<grid, lq::kThreads, 0, c->stream>>>(
+                (const lq_insn*)dg, G->n_insn, G->result, (const double*)dp, K, alpha, h, (double)m0, t0, t1, 0,
+                (double*)tiles);
+        c->launches++;
+        CK(cudaGetLastError());
+    }
+    t_end(c);
+    if (tiles_dev) {
+        *out = (double)T;
+        return LQ_OK;
+    }
+    double* r;
+    if ((rc = reduce_dev(c, (const double*)tiles, T, &r))) return rc;
+    return read_scalar(c, r, out);
+}
+
 int lq_fp64_peak(lq_ctx* c, int32_t iters, double* tflops, float* ms) {
     int rc = set_dev(c);
     if (rc) return rc;

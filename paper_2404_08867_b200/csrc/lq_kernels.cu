@@ -1412,6 +1412,104 @@ __global__ void __launch_bounds__(kThreads) k_mdi_combine(const double* __restri
     }
 }
 
+// ============================================================ MDI level collapse
+// f = G(alpha + <beta, y>) on the midpoint grid with commensurate steps
+// beta_j y_t = h m_j (2t + 1): the reference's level loop strips one axis per
+// level and its like-term collection merges the partial sums whose constants
+// coincide (mdi.py:152-165, exprcore.py:139-169, 390-402), so what it carries
+// per level is the multiset of values of the partial linear form.  Here that
+// multiset is a distribution over k = sum_j |m_j| t_j (t_j uniform on
+// [0, N_j)): one convolution per direction, p'[s] = (1/N) sum_t p[s - |m| t],
+// then one pass of G over the support.  All terms are positive, so the level
+// sums carry no cancellation; four interleaved accumulators keep the rounding
+// at ~N/4 ulp per level.
+struct LinLevel {
+    int64_t m;     // |m_j| >= 1
+    int32_t n;     // N_j nodes
+    int32_t pad;
+};
+
+__device__ __forceinline__ double lin_conv_point(const double* __restrict__ p, int64_t k_old, int64_t s,
+                                                 int64_t m, int n) {
+    const int64_t t_lo = s < k_old ? 0 : (s - k_old + m) / m;   // s - m t <= k_old - 1
+    const int64_t t_hi = min((int64_t)n - 1, s / m);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t t = t_lo;
+    const double* q = p + (s - m * t_lo);
+    for (; t + 3 <= t_hi; t += 4, q -= 4 * m) {
+        a0 += q[0];
+        a1 += q[-m];
+        a2 += q[-2 * m];
+        a3 += q[-3 * m];
+    }
+    for (; t <= t_hi; ++t, q -= m) a0 += q[0];
+    return ((a0 + a1) + (a2 + a3)) / (double)n;
+}
+
+// Every level in one CTA with both distributions in shared memory (support
+// <= k_cap doubles each); the final distribution goes to p_out.
+__global__ void __launch_bounds__(1024) k_linform_smem(const LinLevel* __restrict__ lv, int n_lv, int64_t k_cap,
+                                                       double* __restrict__ p_out) {
+    extern __shared__ double lin_sm[];
+    double* a = lin_sm;
+    double* b = lin_sm + k_cap;
+    if (threadIdx.x == 0) a[0] = 1.0;
+    int64_t K = 1;
+    __syncthreads();
+    for (int l = 0; l < n_lv; ++l) {
+        const LinLevel L = lv[l];
+        const int64_t Kn = K + L.m * (L.n - 1);
+        for (int64_t s = threadIdx.x; s < Kn; s += blockDim.x) b[s] = lin_conv_point(a, K, s, L.m, L.n);
+        __syncthreads();
+        double* t = a;
+        a = b;
+        b = t;
+        K = Kn;
+    }
+    for (int64_t s = threadIdx.x; s < K; s += blockDim.x) p_out[s] = a[s];
+}
+
+__global__ void k_fill(double* __restrict__ p, int64_t count, double v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+// One level in global memory (support past the shared-memory capacity).
+__global__ void __launch_bounds__(kThreads) k_linform_level(const double* __restrict__ p, int64_t k_old,
+                                                            int64_t m, int n, double* __restrict__ q) {
+    const int64_t Kn = k_old + m * (n - 1);
+    for (int64_t s = blockIdx.x * (int64_t)kThreads + threadIdx.x; s < Kn; s += (int64_t)gridDim.x * kThreads)
+        q[s] = lin_conv_point(p, k_old, s, m, n);
+}
+
+// sum_k p[k] G(alpha + h (m0 + 2k)) over tiles of kTile support points
+// (thread-strided inside the tile, block_sum tree): tiles [t_begin, t_end),
+// partial of tile t to tiles[t - t_out0].
+template <int NS>
+__global__ void __launch_bounds__(kThreads) k_linform_eval(const lq_insn* __restrict__ prog, int n_insn, int result,
+                                                           const double* __restrict__ p, int64_t K, double alpha,
+                                                           double h, double m0, int64_t t_begin, int64_t t_end,
+                                                           int64_t t_out0, double* __restrict__ tiles) {
+    __shared__ double sh[8];
+    double slot[NS];
+    for (int64_t tile = t_begin + blockIdx.x; tile < t_end; tile += gridDim.x) {
+        double s = 0.0;
+        #pragma unroll 1
+        for (int q = 0; q < kPts; ++q) {
+            const int64_t k = tile * kTile + (int64_t)q * kThreads + threadIdx.x;
+            if (k < K) {
+                const double w = p[k];
+                if (w != 0.0) {
+                    UnivSrc src{fma(h, m0 + 2.0 * (double)k, alpha)};
+                    s += w * run_program<NS>(prog, n_insn, result, src, slot);
+                }
+            }
+        }
+        s = block_sum(s, sh);
+        if (threadIdx.x == 0) tiles[tile - t_out0] = s;
+    }
+}
+
 // ============================================================ CF (exp-abs) MDI
 // One CTA per frequency node w: each warp forms phi_j(w) = sum_t e^{i w beta_j y_t}
 // for its directions j (lanes over t), accumulating log|phi_j| and arg phi_j;

@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _native as N
 from .expr import Expr, as_expr, free_vars
-from .lower import Program, compile_program, recognize_plain, separate
+from .lower import Program, compile_program, linear_outer, recognize_plain, separate
 
 __all__ = ["PlainIntegrand", "plain_integrand", "lattice_sum", "tensor_program", "SeparablePlan",
            "separable_plan", "mdi_separable_sum"]
@@ -297,3 +297,88 @@ def mdi_expabs_cf(beta, counts, alpha, kappa):
     E = out[1] * math.exp(out[0]) * 2.0 / math.pi
     tail = float(np.exp(np.max(logmag[n_nodes:]))) if len(wn) > n_nodes else 0.0
     return E, tail
+
+
+# ------------------------------- MDI-LR level collapse, G(alpha + <beta, y>)
+
+LINFORM_MAX_SUPPORT = 1 << 28       # LQ_LINFORM_MAX_SUPPORT
+LINFORM_MAX_WORK = 2 * 10**11       # sum over levels of support x nodes (~ seconds of device time)
+_RATIO_DEN = 1 << 20
+
+
+class LinformPlan:
+    """Commensurate steps of G(<beta, y>) on the midpoint grid: direction j
+    contributes beta_j (t + 1/2)/N_j = h m_j (2t + 1), so the linear form is
+    h (m0 + 2k), k = sum_j |m_j| t_j (t_j uniform on [0, N_j)).  ``ok`` is
+    False when the steps are not commensurate within the support cap."""
+
+    def __init__(self, e, counts):
+        from fractions import Fraction
+        self.ok = False
+        lo = linear_outer(e)
+        if lo is None:
+            return
+        d = len(counts)
+        if any(not 1 <= j <= d for j in lo.beta):
+            return
+        axes = sorted(lo.beta)
+        b_ref = Fraction(lo.beta[axes[0]])
+        steps = []
+        for j in axes:
+            rho = Fraction(lo.beta[j]) / b_ref
+            if rho.denominator > _RATIO_DEN:
+                # a ratio within a few ulp of a small rational (e.g. 0.3 / 0.1)
+                approx = rho.limit_denominator(_RATIO_DEN)
+                if abs(approx - rho) > abs(rho) * Fraction(1, 1 << 50):
+                    return
+                rho = approx
+            steps.append(rho / (2 * int(counts[j - 1])))
+        den = math.lcm(*(r.denominator for r in steps))
+        nums = [int(r * den) for r in steps]
+        g = math.gcd(*nums)
+        m = [v // g for v in nums]
+        h_rat = Fraction(g, den)
+        # levels in the reference's stripping order (last axis first, mdi.py:156-159)
+        order = sorted(range(len(axes)), key=lambda i: -axes[i])
+        self.m = np.asarray([abs(m[i]) for i in order], dtype=np.int64)
+        self.n = np.asarray([int(counts[axes[i] - 1]) for i in order], dtype=np.int32)
+        self.m0 = sum(mi if mi > 0 else mi * (2 * int(counts[axes[i] - 1]) - 1) for i, mi in enumerate(m))
+        self.support = 1 + int(np.sum(self.m * (self.n.astype(np.int64) - 1)))
+        sizes = np.cumsum(self.m * (self.n.astype(np.int64) - 1)) + 1
+        work = int(np.sum(sizes * self.n))
+        if self.support > LINFORM_MAX_SUPPORT or work > LINFORM_MAX_WORK:
+            return
+        if abs(self.m0) + 2 * self.support >= 2**53:
+            return
+        self.level_support = tuple(int(v) for v in sizes)
+        self.h = float(b_ref * h_rat)
+        self.G = lo.G
+        self.prog = compile_program(lo.G)
+        self.tiles = -(-self.support // N.LQ_TILE)
+        self.ok = True
+
+    def program_struct(self):
+        ins = np.ascontiguousarray(self.prog.insn)
+        return ins, N.Program(ins.ctypes.data, len(ins), self.prog.n_slots, self.prog.result, self.prog.n_vars, None)
+
+
+_lin_cache = _LRU(32)
+
+
+def linform_plan(g, counts):
+    """LinformPlan of g on midpoint grids with these counts (cached)."""
+    e = as_expr(g)
+    return _lin_cache.get_or((e, tuple(int(c) for c in counts)), lambda: LinformPlan(e, counts))
+
+
+def mdi_linform_mean(plan, shard=0, nshards=1, tiles_dev=None):
+    """Grid mean of G(<beta, y>) via the level-collapse kernels (single GPU), or
+    this shard's tile partials into ``tiles_dev`` (a device pointer with
+    ``plan.tiles`` doubles)."""
+    ins, p = plan.program_struct()
+    out = C.c_double()
+    N.check(N.lib().lq_mdi_linform(N.ctx(), C.byref(p), len(plan.m), N.as_ptr(plan.m), N.as_ptr(plan.n), 0.0,
+                                   plan.h, int(plan.m0), shard, nshards,
+                                   None if tiles_dev is None else C.c_void_p(tiles_dev), plan.tiles,
+                                   C.byref(out)))
+    return out.value

@@ -20,6 +20,7 @@ like-term merging) keeps that analysis simple.
 from __future__ import annotations
 
 import math
+import re
 
 __all__ = [
     "Expr", "ParseError", "UnassignedVariableError",
@@ -377,259 +378,330 @@ def _from_reference(root):
 
 # --------------------------------------------------------------------- parser
 
-def _tokenize(text):
-    toks = []
-    i, n = 0, len(text)
-    while i < n:
-        ch = text[i]
-        if ch.isspace():
-            i += 1
-        elif ch.isdigit() or (ch == "." and i + 1 < n and text[i + 1].isdigit()):
-            j = i
-            while j < n and (text[j].isdigit() or (text[j] == "." and not text.startswith("..", j))):
-                j += 1
-            if j < n and text[j] in "eE" and text[i:j].count(".") <= 1:
-                k = j + 1
-                if k < n and text[k] in "+-":
-                    k += 1
-                if k < n and text[k].isdigit():
-                    while k < n and text[k].isdigit():
-                        k += 1
-                    j = k
-            toks.append(("num", text[i:j], i))
-            i = j
-        elif ch.isalpha() or ch == "_":
-            j = i
-            while j < n and (text[j].isalnum() or text[j] == "_"):
-                j += 1
-            toks.append(("name", text[i:j], i))
-            i = j
-        elif text.startswith("..", i):
-            toks.append(("sym", "..", i))
-            i += 2
-        elif ch in "+-*/^()[],=":
-            toks.append(("sym", ch, i))
-            i += 1
-        else:
-            raise ParseError(f"unexpected character {ch!r} at position {i}")
-    toks.append(("end", "", n))
-    return toks
+_TOKEN_RE = re.compile(r"""
+    (?P<ws>\s+)
+  | (?P<num>(?:\d|\.(?=\d))(?:\d|\.(?!\.))*)
+  | (?P<name>[^\W\d]\w*)
+  | (?P<sym>\.\.|[-+*/^()\[\],=])
+""", re.VERBOSE)
+_EXPONENT_RE = re.compile(r"[eE][+-]?\d+")
 
 
-_RESERVED = ("d", "x", "pi", "e", "sum", "prod") + FUNCS
+def _scan(text):
+    """Token list [(kind, text, position)] ending with ('end', '', len).  A
+    numeric literal runs over digits and single dots ('..' is the range
+    separator) and takes a decimal exponent only when it has at most one dot."""
+    out = []
+    pos = 0
+    while pos < len(text):
+        m = _TOKEN_RE.match(text, pos)
+        if m is None:
+            raise ParseError(f"character {text[pos]!r} at {pos} is not part of the grammar")
+        kind = m.lastgroup
+        end = m.end()
+        if kind == "num" and m.group().count(".") <= 1:
+            ex = _EXPONENT_RE.match(text, end)
+            if ex is not None:
+                end = ex.end()
+        if kind != "ws":
+            out.append((kind, text[pos:end], pos))
+        pos = end
+    out.append(("end", "", len(text)))
+    return out
 
 
-class _Parser:
-    def __init__(self, toks, d, env):
-        self.toks, self.pos, self.d, self.env = toks, 0, d, env
+# Binary operators of the real-valued grammar: token -> binding power.  Every
+# operator is left-associative; '^' is not here: an exponent is an integer
+# index expression applied once to a unary operand (see _Reader.power_operand).
+_BINARY = {"+": 10, "-": 10, "*": 20, "/": 20}
+_RESERVED = frozenset(("d", "x", "pi", "e", "sum", "prod") + FUNCS)
+_CONSTANTS = {"pi": math.pi, "e": math.e}
 
-    def peek(self):
-        return self.toks[self.pos]
 
-    def take(self, want=None):
-        tok = self.toks[self.pos]
-        if want is not None and tok[1] != want:
-            raise ParseError(f"expected {want!r} at position {tok[2]}, found {tok[1]!r}")
-        self.pos += 1
+class _Reader:
+    """Reads the token list into a small syntax tree once (precedence
+    climbing over _BINARY); sum/prod bodies are stored as trees and expanded
+    by _Builder per index value.  A body that does not read cleanly is kept
+    as its error and raised only if its range is non-empty, the way an
+    expansion-time parse would behave."""
+
+    def __init__(self, toks):
+        self.toks = toks
+        self.i = 0
+
+    def at(self):
+        return self.toks[self.i]
+
+    def advance(self):
+        tok = self.toks[self.i]
+        self.i += 1
         return tok
 
-    # real-valued grammar
-    def expr(self):
-        pairs = [(1.0, self.term())]
-        while self.peek()[1] in ("+", "-"):
-            sign = 1.0 if self.take()[1] == "+" else -1.0
-            pairs.append((sign, self.term()))
-        return add(pairs) if len(pairs) > 1 else pairs[0][1]
+    def expect(self, text):
+        kind, got, pos = self.toks[self.i]
+        if kind != "sym" or got != text:
+            raise ParseError(f"{text!r} expected at {pos} (got {got or 'end of input'!r})")
+        self.i += 1
 
-    def term(self):
-        node = self.factor()
-        while self.peek()[1] in ("*", "/"):
-            op = self.take()[1]
-            at = self.peek()[2]
-            rhs = self.factor()
-            if op == "*":
-                node = mul(1.0, [node, rhs])
-            elif rhs.op == "const":
-                if rhs.val == 0.0:
-                    raise ParseError(f"division by zero at position {at}")
-                node = mul(1.0 / rhs.val, [node])
-            elif node.op == "const":
-                node = mul(node.val, [power(rhs, -1)])
-            else:
-                raise ParseError(f"non-constant denominator at position {at}")
-        return node
+    def expression(self, floor=0):
+        lhs = self.power_operand()
+        while True:
+            _, op, pos = self.at()
+            bp = _BINARY.get(op)
+            if bp is None or bp <= floor or self.at()[0] != "sym":
+                return lhs
+            self.advance()
+            lhs = ("bin", op, lhs, self.expression(bp), pos)
 
-    def factor(self):
+    def power_operand(self):
         node = self.unary()
-        if self.peek()[1] == "^":
-            self.take("^")
-            node = power(node, self.ipower())
+        if self.at()[1] == "^" and self.at()[0] == "sym":
+            self.advance()
+            node = ("pow", node, self.exponent())
         return node
 
     def unary(self):
-        if self.peek()[1] == "-":
-            self.take("-")
-            return mul(-1.0, [self.base()])
-        return self.base()
+        if self.at()[1] == "-" and self.at()[0] == "sym":
+            self.advance()
+            return ("neg", self.primary())      # -a^k reads as (-a)^k
+        return self.primary()
 
-    def base(self):
-        kind, val, at = self.peek()
+    def primary(self):
+        kind, text, pos = self.advance()
         if kind == "num":
-            self.take()
             try:
-                return const(float(val))
+                return ("num", float(text))
             except ValueError:
-                raise ParseError(f"bad numeric literal {val!r} at position {at}") from None
-        if val == "(":
-            self.take("(")
-            node = self.expr()
-            self.take(")")
+                raise ParseError(f"malformed number {text!r} at {pos}") from None
+        if kind == "sym" and text == "(":
+            node = self.expression()
+            self.expect(")")
             return node
-        if kind == "name":
-            self.take()
-            if val == "pi":
-                return const(math.pi)
-            if val == "e":
-                return const(math.e)
-            if val == "x":
-                self.take("[")
-                i = self.iexpr()
-                self.take("]")
-                if not 1 <= i <= self.d:
-                    raise ParseError(f"coordinate x[{i}] outside 1..{self.d} at position {at}")
-                return var(i)
-            if val in FUNCS:
-                self.take("(")
-                arg = self.expr()
-                self.take(")")
-                return func(val, arg)
-            if val in ("sum", "prod"):
-                return self.reduction(val)
-            if val in self.env:
-                return const(float(self.env[val]))
-            if val == "d":
-                return const(float(self.d))
-            raise ParseError(f"unknown identifier {val!r} at position {at}")
-        raise ParseError(f"unexpected token {val!r} at position {at}")
+        if kind != "name":
+            raise ParseError(f"{text or 'end of input'!r} at {pos} cannot start an operand")
+        if text == "x":
+            self.expect("[")
+            idx = self.index_expression()
+            self.expect("]")
+            return ("x", idx, pos)
+        if text in FUNCS:
+            self.expect("(")
+            arg = self.expression()
+            self.expect(")")
+            return ("call", text, arg)
+        if text in ("sum", "prod"):
+            return self.reduction(text, pos)
+        return ("name", text, pos)
 
-    def reduction(self, which):
-        self.take("(")
-        kind, name, at = self.take()
-        if kind != "name" or name in _RESERVED:
-            raise ParseError(f"bad index variable {name!r} at position {at}")
-        self.take("=")
-        lo = self.iexpr()
-        self.take("..")
-        hi = self.iexpr()
-        self.take(",")
-        start = self.pos
+    def reduction(self, which, pos):
+        self.expect("(")
+        kind, var, vpos = self.advance()
+        if kind != "name" or var in _RESERVED:
+            raise ParseError(f"{var!r} at {vpos} cannot be a {which} index")
+        self.expect("=")
+        lo = self.index_expression()
+        self.expect("..")
+        hi = self.index_expression()
+        self.expect(",")
+        first = self.i
         depth = 0
-        while True:
-            k, v, p = self.toks[self.pos]
-            if k == "end":
-                raise ParseError(f"unterminated body at position {p}")
-            if v in ("(", "["):
+        while True:                       # the body runs to the ')' that closes the call
+            kind, text, tpos = self.at()
+            if kind == "end":
+                raise ParseError(f"{which} body starting at {self.toks[first][2]} is never closed")
+            if text in "([" and kind == "sym":
                 depth += 1
-            elif v in (")", "]"):
-                if depth == 0 and v == ")":
+            elif text in ")]" and kind == "sym":
+                if depth == 0 and text == ")":
                     break
                 depth -= 1
-            self.pos += 1
-        end = self.pos
-        self.take(")")
-        parts = []
-        for i in range(lo, hi + 1):
-            sub = _Parser(self.toks, self.d, {**self.env, name: i})
-            sub.pos = start
-            parts.append(sub.expr())
-            if sub.pos != end:
-                raise ParseError(f"malformed {which} body at position {at}")
-        if not parts:
-            return const(0.0 if which == "sum" else 1.0)
-        return add([(1.0, p) for p in parts]) if which == "sum" else mul(1.0, parts)
+            self.i += 1
+        last = self.i
+        self.advance()
+        sub = _Reader(self.toks[first:last] + [("end", "", self.toks[last][2])])
+        try:
+            body = sub.expression()
+            if sub.at()[0] != "end":
+                raise ParseError(f"{which} body at {pos} does not end where its call closes")
+        except ParseError as exc:
+            body = exc
+        return ("red", which, var, lo, hi, body)
 
-    # integer index arithmetic
-    def iexpr(self):
-        v = self.iterm()
-        while self.peek()[1] in ("+", "-"):
-            op = self.take()[1]
-            r = self.iterm()
-            v = v + r if op == "+" else v - r
+    # integer index expressions: + - * / (exact), ^ (right-assoc, k >= 0), unary -
+    def index_expression(self):
+        v = self.index_term()
+        while self.at()[1] in ("+", "-") and self.at()[0] == "sym":
+            op = self.advance()[1]
+            v = ("ibin", op, v, self.index_term(), None)
         return v
 
-    def iterm(self):
-        v = self.ifactor()
-        while self.peek()[1] in ("*", "/"):
-            op = self.take()[1]
-            at = self.peek()[2]
-            r = self.ifactor()
-            if op == "*":
-                v *= r
-            else:
-                if r == 0 or v % r != 0:
-                    raise ParseError(f"non-integer division in index expression at {at}")
-                v //= r
+    def index_term(self):
+        v = self.index_factor()
+        while self.at()[1] in ("*", "/") and self.at()[0] == "sym":
+            op = self.advance()[1]
+            pos = self.at()[2]
+            v = ("ibin", op, v, self.index_factor(), pos)
         return v
 
-    def ifactor(self):
-        v = self.iunary()
-        if self.peek()[1] == "^":
-            self.take("^")
-            k = self.ifactor()
-            if k < 0:
-                raise ParseError("negative power in index expression")
-            v = v ** k
+    def index_factor(self):
+        v = self.index_unary()
+        if self.at()[1] == "^" and self.at()[0] == "sym":
+            self.advance()
+            v = ("ipow", v, self.index_factor())
         return v
 
-    def iunary(self):
-        if self.peek()[1] == "-":
-            self.take("-")
-            return -self.iunary()
-        if self.peek()[1] == "(":
-            self.take("(")
-            v = self.iexpr()
-            self.take(")")
+    def index_unary(self):
+        kind, text, _ = self.at()
+        if kind == "sym" and text == "-":
+            self.advance()
+            return ("ineg", self.index_unary())
+        if kind == "sym" and text == "(":
+            self.advance()
+            v = self.index_expression()
+            self.expect(")")
             return v
-        return self.iatom()
+        return self.index_atom()
 
-    def iatom(self):
-        kind, val, at = self.take()
+    def index_atom(self):
+        kind, text, pos = self.advance()
         if kind == "num":
-            if "." in val or "e" in val or "E" in val:
-                raise ParseError(f"non-integer literal {val!r} in index expression at {at}")
-            return int(val)
+            if not text.isdigit():
+                raise ParseError(f"index expressions take integers, got {text!r} at {pos}")
+            return ("inum", int(text))
         if kind == "name":
-            if val == "d":
-                return self.d
-            if val in self.env:
-                return self.env[val]
-            raise ParseError(f"unknown index identifier {val!r} at position {at}")
-        raise ParseError(f"unexpected token {val!r} in index expression at {at}")
+            return ("iname", text, pos)
+        raise ParseError(f"{text or 'end of input'!r} at {pos} is not an index operand")
 
-    def ipower(self):
-        if self.peek()[1] == "-":
-            self.take("-")
-            return -self.ipower()
-        if self.peek()[1] == "(":
-            self.take("(")
-            v = self.iexpr()
-            self.take(")")
+    def exponent(self):
+        """An exponent is delimited: '-' exponent | '(' index expression ')' |
+        atom ['^' exponent], so 'x^2*y' is (x^2)*y."""
+        kind, text, _ = self.at()
+        if kind == "sym" and text == "-":
+            self.advance()
+            return ("ineg", self.exponent())
+        if kind == "sym" and text == "(":
+            self.advance()
+            v = self.index_expression()
+            self.expect(")")
             return v
-        v = self.iatom()
-        if self.peek()[1] == "^":
-            self.take("^")
-            k = self.ipower()
-            if k < 0:
-                raise ParseError("negative power in index expression")
-            v = v ** k
+        v = self.index_atom()
+        if self.at()[1] == "^" and self.at()[0] == "sym":
+            self.advance()
+            v = ("ipow", v, self.exponent())
         return v
+
+
+class _Builder:
+    """Syntax tree -> Expr under an environment of index values."""
+
+    def __init__(self, d):
+        self.d = d
+
+    def index(self, t, env):
+        tag = t[0]
+        if tag == "inum":
+            return t[1]
+        if tag == "iname":
+            if t[1] == "d":
+                return self.d
+            if t[1] in env:
+                return env[t[1]]
+            raise ParseError(f"{t[1]!r} at {t[2]} is not an index in scope")
+        if tag == "ineg":
+            return -self.index(t[1], env)
+        if tag == "ipow":
+            b, k = self.index(t[1], env), self.index(t[2], env)
+            if k < 0:
+                raise ParseError(f"index power {b}^{k} has a negative exponent")
+            return b ** k
+        op, a, b = t[1], self.index(t[2], env), self.index(t[3], env)
+        if op == "+":
+            return a + b
+        if op == "-":
+            return a - b
+        if op == "*":
+            return a * b
+        if b == 0 or a % b:
+            raise ParseError(f"{a}/{b} at {t[4]} is not an exact integer division")
+        return a // b
+
+    def real(self, t, env):
+        tag = t[0]
+        if tag == "num":
+            return const(t[1])
+        if tag == "name":
+            name = t[1]
+            if name in _CONSTANTS:
+                return const(_CONSTANTS[name])
+            if name in env:
+                return const(float(env[name]))
+            if name == "d":
+                return const(float(self.d))
+            raise ParseError(f"unknown name {name!r} at {t[2]}")
+        if tag == "x":
+            j = self.index(t[1], env)
+            if not 1 <= j <= self.d:
+                raise ParseError(f"x[{j}] at {t[2]} is outside the coordinates 1..{self.d}")
+            return var(j)
+        if tag == "call":
+            return func(t[1], self.real(t[2], env))
+        if tag == "neg":
+            return mul(-1.0, [self.real(t[1], env)])
+        if tag == "pow":
+            return power(self.real(t[1], env), self.index(t[2], env))
+        if tag == "red":
+            return self.reduction(t, env)
+        return self.chain(t, env)
+
+    def chain(self, t, env):
+        """A left-leaning run of one precedence level, folded iteratively (long
+        sums of thousands of terms stay off the Python stack): '+'/'-' runs
+        build one n-ary sum, '*'/'/' runs fold left to right."""
+        group = "+-" if t[1] in "+-" else "*/"
+        spine = []
+        node = t
+        while node[0] == "bin" and node[1] in group:
+            spine.append(node)
+            node = node[2]
+        acc = self.real(node, env)
+        if group == "+-":
+            pairs = [(1.0, acc)]
+            for n in reversed(spine):
+                pairs.append((1.0 if n[1] == "+" else -1.0, self.real(n[3], env)))
+            return add(pairs)
+        for n in reversed(spine):
+            rhs = self.real(n[3], env)
+            if n[1] == "*":
+                acc = mul(1.0, [acc, rhs])
+            elif rhs.op == "const":
+                # by a constant: its reciprocal as the coefficient
+                if rhs.val == 0.0:
+                    raise ParseError(f"division by zero at {n[4]}")
+                acc = mul(1.0 / rhs.val, [acc])
+            elif acc.op == "const":
+                # a constant over an expression: its -1 power
+                acc = mul(acc.val, [power(rhs, -1)])
+            else:
+                raise ParseError(f"quotient at {n[4]} has a non-constant numerator and denominator")
+        return acc
+
+    def reduction(self, t, env):
+        _, which, name, lo, hi, body = t
+        lo, hi = self.index(lo, env), self.index(hi, env)
+        if hi < lo:
+            return const(0.0 if which == "sum" else 1.0)
+        if isinstance(body, ParseError):
+            raise body
+        parts = [self.real(body, {**env, name: i}) for i in range(lo, hi + 1)]
+        return add([(1.0, p) for p in parts]) if which == "sum" else mul(1.0, parts)
 
 
 def parse(text, d):
-    """Parse source text into an Expr; ``d`` bounds x[i] (exprcore.py:759-766)."""
-    p = _Parser(_tokenize(text), int(d), {})
-    node = p.expr()
-    if p.peek()[0] != "end":
-        _, val, at = p.peek()
-        raise ParseError(f"trailing input {val!r} at position {at}")
-    return node
+    """Source text -> Expr over coordinates x[1..d] (the grammar of
+    exprcore.parse, exprcore.py:486-766, plus abs(...))."""
+    reader = _Reader(_scan(text))
+    tree = reader.expression()
+    kind, tok, pos = reader.at()
+    if kind != "end":
+        raise ParseError(f"unexpected {tok!r} at {pos} after a complete expression")
+    return _Builder(int(d)).real(tree, {})

@@ -28,12 +28,12 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .expr import Expr, add, const, free_vars, func, mul, power, topo
+from .expr import Expr, add, const, free_vars, func, mul, power, topo, var
 
 __all__ = [
     "linear_form", "quad_form", "recognize_plain", "PlainFamily",
     "Program", "compile_program", "separate", "SepTerm", "Factor",
-    "MAX_SLOTS", "INSN_DTYPE",
+    "MAX_SLOTS", "INSN_DTYPE", "LinearOuter", "linear_outer",
 ]
 
 # ------------------------------------------------------------ polynomial view
@@ -602,3 +602,83 @@ def separate(e, cap=_TERM_CAP):
         return None
 
     return rec(e)
+
+
+# ------------------------------------------- MDI: functions of one linear form
+
+@dataclass
+class LinearOuter:
+    """e = G(<beta, x>): every coordinate enters through affine forms
+    a_i + b_i <beta, x> with proportional coefficient vectors.  ``G`` is an
+    Expr in var(1) standing for s = <beta, x>; ``beta`` maps axis -> coefficient."""
+
+    G: Expr
+    beta: dict
+
+
+def _children_of(node):
+    return [t for _, t in node.terms] if node.op == "add" else list(node.args)
+
+
+def _rebuild(e, repl):
+    """e with the nodes of ``repl`` replaced (factories re-normalise)."""
+    memo = {}
+    for node in topo(e):
+        if node in repl:
+            memo[node] = repl[node]
+            continue
+        op = node.op
+        if op in ("const", "var"):
+            out = node
+        elif op == "add":
+            out = add([(c, memo[t]) for c, t in node.terms], node.val)
+        elif op == "mul":
+            out = mul(node.val, [memo[f] for f in node.args])
+        elif op == "pow":
+            out = power(memo[node.args[0]], node.idx)
+        else:
+            out = func(op, memo[node.args[0]])
+        memo[node] = out
+    return memo[e]
+
+
+def linear_outer(e, rel_tol=4.0 * 2.0**-52):
+    """Split e = G(<beta, x>) or return None (the
+    integrands whose MDI levels collapse without being separable, e.g. corpus
+    invpow (1 + sum x_i)^-(d+1)).  The maximal affine subexpressions of e must
+    share one coefficient direction: a_i + <beta_i, x> with beta_i = b_i beta."""
+    leaves = {}
+    seen = set()
+    stack = [e]
+    while stack:
+        node = stack.pop()
+        if node in seen or not free_vars(node):
+            continue
+        seen.add(node)
+        lf = linear_form(node)
+        if lf is not None:
+            leaves[node] = lf
+            continue
+        stack.extend(_children_of(node))
+    if not leaves:
+        return None
+    items = list(leaves.items())
+    beta0 = {j: c for j, c in items[0][1][1].items() if c != 0.0}
+    if not beta0:
+        return None
+    j0 = min(beta0)
+    s = var(1)
+    repl = {}
+    for node, (alpha, beta) in items:
+        beta = {j: c for j, c in beta.items() if c != 0.0}
+        if set(beta) != set(beta0):
+            return None
+        b = beta[j0] / beta0[j0]
+        for j, c in beta.items():
+            if abs(c - b * beta0[j]) > rel_tol * abs(c):
+                return None
+        repl[node] = add([(b, s)], alpha)
+    G = _rebuild(e, repl)
+    if free_vars(G) != frozenset({1}):
+        return None
+    return LinearOuter(G, beta0)

@@ -30,6 +30,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import engine
+from ._fp import blocked_const_sum, repeated_add
 from .expr import as_expr, evaluate, free_vars, var_bounds
 from .lattice import korobov_vector
 from .transform import midpoint_grids
@@ -74,8 +75,8 @@ class MdiConfig:
 class MdiReport:
     """Observability record (mdi.py:79-101) plus GPU-side extras:
     log_raw (natural log of |value|, finite even when value under/overflows),
-    sign, method ('separable' | 'direct' | 'constant' | 'characteristic'),
-    clusters."""
+    sign, method ('separable' | 'linform' | 'direct' | 'constant' |
+    'characteristic'), clusters (factor count, or support size for linform)."""
 
     value: float
     levels: int
@@ -112,14 +113,30 @@ class MdiReport:
 
 
 def _const_sweep(value, counts):
-    """The reference's constant sweep: chunks of 2^19 nodes, acc += c * len
-    (mdi.py:116-128)."""
+    """The reference's numeric sweep of a constant: chunks of 2^19 nodes,
+    acc += c * len (mdi.py:116-128), in closed form (_fp.blocked_const_sum)."""
     total = math.prod(counts) if counts else 1
-    acc = 0.0
-    chunk = 1 << 19
-    for start in range(0, total, chunk):
-        acc += float(value) * (min(start + chunk, total) - start)
-    return acc
+    return blocked_const_sum(value, total, 1 << 19)
+
+
+def _const_levels(value, counts, cfg):
+    """mdi_sum of a constant exactly as the reference's loop rounds it: each
+    level's partial_sum folds N copies of the constant into one
+    (make_sum, exprcore.py:139-153), then the base axes are swept in chunks
+    (mdi.py:167-183).  Raises GridCapError when the base sweep exceeds the cap."""
+    d = len(counts)
+    levels, base_axes = _level_plan(d, cfg)
+    stripped = [a for a in range(1, d + 1) if a not in base_axes]
+    if cfg.order == "forward":
+        stripped = stripped[::-1]
+    v = float(value)
+    for a in stripped:
+        v = repeated_add(v, counts[a - 1])
+    base = [counts[a - 1] for a in base_axes]
+    base_total = math.prod(base) if base else 1
+    if base_total > cfg.direct_cap:
+        raise GridCapError(f"direct sweep needs {base_total} evaluations, cap is {cfg.direct_cap}")
+    return (_const_sweep(v, base) if base else v), levels, base_axes
 
 
 def direct_tensor_sum(g, grids, cap=DIRECT_CAP):
@@ -160,7 +177,7 @@ def mdi_sum(g, grids, cfg=None):
     t0 = time.perf_counter()
 
     if not free_vars(e):
-        value = _const_sweep(evaluate(e, {}), counts)
+        value, levels, base_axes = _const_levels(evaluate(e, {}), counts, cfg)
         return MdiReport(value=value, levels=levels, base_dim=len(base_axes), level_nodes=(1,) * levels,
                          level_seconds=(0.0,) * levels, base_seconds=time.perf_counter() - t0,
                          log_raw=math.log(abs(value)) if value else -math.inf,
@@ -170,9 +187,16 @@ def mdi_sum(g, grids, cfg=None):
     plan = engine.separable_plan(e, counts, None if midpoint else grids.nodes)
     usable = plan.ok and (plan.n_factors + plan.n_terms) <= cfg.budget
     total = _total(counts)
-    if (not usable and total > cfg.direct_cap and getattr(grids, "midpoint", False)
-            and cfg.fallback == "numeric"):
-        rep = _characteristic(e, d, counts, levels, base_axes, t0)
+    if not usable and midpoint:
+        # non-separable integrands whose levels still collapse: exp-abs of a
+        # linear form past the direct cap by its characteristic function (an
+        # extension, the reference has no |.|), functions of one commensurate
+        # linear form by the distribution of the partial form (lq_mdi_linform)
+        if total > cfg.direct_cap and cfg.fallback == "numeric":
+            rep = _characteristic(e, d, counts, levels, base_axes, t0)
+            if rep is not None:
+                return rep
+        rep = _linform(e, counts, levels, base_axes, cfg, t0)
         if rep is not None:
             return rep
     if not usable:
@@ -193,6 +217,42 @@ def mdi_sum(g, grids, cfg=None):
                      level_nodes=(plan.n_factors,) * levels, level_seconds=(0.0,) * levels,
                      base_seconds=secs, fallback=False, log_raw=log_raw, sign=sign,
                      method="separable", clusters=plan.n_factors)
+
+
+def _linform(e, counts, levels, base_axes, cfg, t0):
+    """f = G(alpha + <beta, y>) with commensurate steps beta_j / (2 N_j): the
+    level collapse the reference's partial sums perform by like-term
+    collection (each level's partial sums take the values of the partial
+    linear form, exprcore.py:139-169, 390-402; mdi.py:152-165), here as the
+    distribution of that linear form convolved one direction per level on the
+    GPU (lq_mdi_linform), then G over its support.  None when e is not of
+    this form or its support is too large."""
+    plan = engine.linform_plan(e, counts)
+    if not plan.ok:
+        return None
+    mean = engine.mdi_linform_mean(plan)
+    log_total = _log_total(counts)
+    raw, log_raw, sign = _raw_from_mean(mean, counts, log_total)
+    stripped = plan.level_support[:levels * cfg.m:cfg.m] if cfg.m > 1 else plan.level_support[:levels]
+    return MdiReport(value=raw, levels=levels, base_dim=len(base_axes), level_nodes=tuple(stripped),
+                     level_seconds=(0.0,) * levels, base_seconds=time.perf_counter() - t0, fallback=False,
+                     log_raw=log_raw, sign=sign, method="linform", clusters=plan.support)
+
+
+def _raw_from_mean(mean, counts, log_total):
+    """Raw grid sum from the grid mean: one rounding (mean * total) while the
+    total is a double, else through logs (under/overflow like the reference's
+    float sums)."""
+    if mean == 0.0 or not math.isfinite(mean):
+        return mean, (math.log(abs(mean)) if mean else -math.inf), math.copysign(1.0, mean) if mean else 0.0
+    sign = math.copysign(1.0, mean)
+    log_raw = math.log(abs(mean)) + log_total
+    total = _total(counts)
+    if total.bit_length() <= 1000:
+        raw = mean * float(total)
+    else:
+        raw = sign * math.exp(log_raw) if log_raw < 709.7 else sign * math.inf
+    return raw, log_raw, sign
 
 
 def _characteristic(e, d, counts, levels, base_axes, t0):

@@ -283,18 +283,221 @@ def suite_cases():
     return out
 
 
+def linform_cases(skip_slow):
+    """MDI-LR of integrands that are functions of one linear form (not
+    separable): the reference's level loop collapses them by like-term
+    collection (exprcore.py:139-169, 390-402; mdi.py:152-165).  Suite test7's
+    invpow rows (bench.py:140-143, n = 1 + 8^d, a = 8) plus a few forms with
+    mixed integer coefficients; value, report fields and wall time."""
+    out = []
+
+    def add(tag, text, d, a, n, slow=False):
+        if slow and skip_slow:
+            return
+        f = exprcore.parse(text, d)
+        t0 = time.perf_counter()
+        value, rep = mdi_lr(f, d, a, n, with_report=True)
+        secs = time.perf_counter() - t0
+        out.append({"tag": tag, "text": text, "d": d, "a": a, "n": str(n), "value": hx(value),
+                    "raw": hx(rep.value), "levels": rep.levels, "base_dim": rep.base_dim,
+                    "fallback": rep.fallback, "level_nodes": list(rep.level_nodes), "ref_seconds": secs})
+        print(f"linform {tag}: {secs:.1f}s fallback={rep.fallback}", flush=True)
+
+    inv = corpus.get("invpow").text
+    for d in (4, 6, 8):
+        add(f"invpow_d{d}", inv, d, 8, 1 + 8**d)
+    add("invpow_d10", inv, 10, 8, 1 + 8**10, slow=True)
+    add("recip_mixed_d4", "1/(1 + x[1] + 2*x[2] + 3*x[3] + x[4])", 4, 5, 5**4)
+    add("recip_mixed_d5_a4", "1/(1 + x[1] + 2*x[2] - x[3] + x[4] + 2*x[5])^2", 5, 4, 4**5 + 3)
+    add("altpow_d6", "(3 + sum(i=1..d, (-1)^i*x[i]))^(-3)", 6, 3, 3**6)
+    add("sin_recip_d5", "sin(1/(1 + sum(i=1..d, x[i])))", 5, 4, 4**5)
+    add("mixed_outer_d6", "1/(1 + sum(i=1..d, x[i])) + exp(-(sum(i=1..d, x[i])/d)^2)", 6, 4, 4**6)
+    return out
+
+
+def _fft_case_sum(case):
+    """Worker: the reference's own sum of one FFT-test case: slr_integrate on
+    the parsed text, or -- for |.|, which the reference grammar lacks --
+    points_block + the numpy restatement exp(-|x c - c.w|)."""
+    key, text, params, n, a = case
+    d = text.count("x[")
+    rule = korobov_vector(a, n, d)
+    t0 = time.perf_counter()
+    if params is None:
+        value = slr_integrate(exprcore.parse(text, d), rule).value
+        kind = "reference"
+    else:
+        c = np.asarray(params["c"])
+        cw = float(np.dot(c, np.asarray(params["w"])))
+        acc = 0.0
+        for start in range(0, n, 1 << 15):
+            pts = points_block(rule, start, min(start + (1 << 15), n))
+            acc += float(np.sum(np.exp(-np.abs(pts @ c - cw))))
+        value = acc / n
+        kind = "ref_points+numpy"
+    return {"key": key, "n": n, "a": a, "d": d, "kind": kind, "value": hx(value),
+            "ref_seconds": time.perf_counter() - t0}
+
+
+def fft_cases_job(procs):
+    """Reference sums of every case of tests/test_gpu_fft.py (cases from
+    tests/fft_cases.py), so that the FFT-form kernel meets the reference and
+    not only the direct orbit kernel."""
+    import multiprocessing as mp
+    sys.path.insert(0, os.path.dirname(HERE))
+    import fft_cases
+    cases = fft_cases.all_cases()
+    with mp.Pool(procs) as pool:
+        out = pool.map(_fft_case_sum, cases, chunksize=1)
+    return out
+
+
+_PARSER_FIXED = [
+    "x[1]+x[2]*3", "-x[1]^2", "x[1]^2^2", "x[1]^-2", "2/x[1]", "x[1]/4", "x[1]/x[2]", "sum(i=1..d, x[i]^i)",
+    "prod(i=1..d, 1/(1+x[i]))", "sum(i=3..1, garbage + )", "sum(i=1..2, x[i], 2)", "x[1]^(1+1)*3", "x[1]^2*3",
+    "exp(-x[1])*sin(pi*x[2])", "--x[1]", "1..2", "1.5e3*x[1]", "2e*x[1]", "x[3]", "x[0]", "x[1.0]",
+    "sum(i=1..d, sum(j=i..d, x[i]*x[j]))", "sum(d=1..2, 1)", "x[1]^(d-1)", "x[d/2]", "x[3/2]", "x[1]^(0-2)",
+    "x[1]^((-2))", "x[1]^2^-1", "cos(2*pi + sum(i=1..d, 2*x[i]))", "(x[1]", "x[1] x[2]", "e^2*x[1]", "pi",
+    "3 - -x[1]", "x[1]^-(2)", "sum(i=1..2, x[i]", "sum(i=1..2, x[k])", "sum(i=2..1, x[k])", "sum(i=1..2, x[(i)])",
+    "1/0", "x[1]/0.0", "x[1] @ 2", ".5*x[1]", "1.2.3", "x[2^2]", "x[-1+2]", "prod(i=1..0, x[1])", "x[1]*-x[2]",
+    "(1 + sum(i=1..d, x[i]))^(-(d+1))", "abs(x[1])", "sum(i=1..3, 0.1*i*x[1])", "1/(1+x[1])/2",
+    "2/(1+x[1])*3/(x[1]+2)", "x[1]^0", "(x[1]+1)^1", "exp(x[1])^3", "sum(i=1..2, sum(i=1..2, x[i]))",
+    "x[1]^2^3^1", "2^-1*x[1]", "x[1]^ 2 * x[1] ^ 3", "sum(i=1..d, (-1)^(i+1)*x[i]^2)", "x[1]^(2^2)",
+    "sum(i=1..4/2, x[i])", "sum(i=1..d, x[i])/d", "prod(i=1..d, (x[i]-0.5)^2 + 0.1)", "sin(x[1])^-1",
+    "1e-3 + x[1]", "1E+2*x[2]", "x[1] +", "*x[1]", "sum(i=1..2 x[i])", "sum(1=1..2, x[1])", "sum(x=1..2, 1)",
+    "exp x[1]", "x[1]^x[2]", "x[1]^2.0", "x[2^-1]", "x[(1)]^(2)^2", "cos()", "sum(i=1..2, )",
+]
+
+
+def _fuzz_texts(rng, count):
+    """Random well- and ill-formed texts from a small generator of the grammar
+    (numbers, x[...] with index arithmetic, + - * / ^, exp/sin/cos, sum/prod)."""
+    def index(depth, names):
+        r = rng.random()
+        if depth > 1 or r < 0.4:
+            return rng.choice([str(rng.randint(1, 3)), "d"] + list(names))
+        op = rng.choice(["+", "-", "*", "/"])
+        return f"({index(depth + 1, names)}{op}{index(depth + 1, names)})"
+
+    def real(depth, names):
+        r = rng.random()
+        if depth > 3 or r < 0.25:
+            return rng.choice([f"x[{index(1, names)}]", repr(round(rng.uniform(-3, 3), 3)), "pi", "e", "d"]
+                              + list(names))
+        if r < 0.55:
+            return f"{real(depth + 1, names)} {rng.choice(['+', '-', '*', '/'])} {real(depth + 1, names)}"
+        if r < 0.65:
+            return f"({real(depth + 1, names)})^{rng.choice(['2', '-1', '(1+1)', '3', '-(2)', 'd'])}"
+        if r < 0.8:
+            return f"{rng.choice(['exp', 'sin', 'cos'])}({real(depth + 1, names)})"
+        if r < 0.9:
+            v = rng.choice(["i", "j", "k"])
+            return (f"{rng.choice(['sum', 'prod'])}({v}={rng.randint(0, 2)}..{rng.choice(['d', '2', '1'])}, "
+                    f"{real(depth + 1, names | {v})})")
+        return f"-{real(depth + 1, names)}"
+
+    out = []
+    for _ in range(count):
+        t = real(0, frozenset())
+        if rng.random() < 0.3:    # mutate: drop or duplicate a character
+            k = rng.randrange(len(t))
+            t = t[:k] + t[k + 1:] if rng.random() < 0.5 else t[:k] + t[k] + t[k:]
+        out.append(t)
+    return out
+
+
+def parser_cases():
+    """The reference grammar (exprcore.parse, exprcore.py:486-766) on fixed and
+    fuzzed texts: accepted texts with the reference's value (exprcore.eval) at
+    three seeded points, rejected texts with the exception type -- the
+    behaviour the product parser must reproduce (the parser must
+    be the builder's own code, pinned by a golden corpus)."""
+    import random
+    rng = random.Random(2404)
+    texts = [(t, 3) for t in _PARSER_FIXED] + [(t, 4) for t in _fuzz_texts(rng, 400)]
+    texts += [(e.text, max(3, e.min_d)) for e in corpus.entries()]
+    out = []
+    for text, d in texts:
+        rec = {"text": text, "d": d}
+        try:
+            f = exprcore.parse(text, d)
+        except Exception as exc:
+            rec["error"] = type(exc).__name__
+            out.append(rec)
+            continue
+        pts, vals = [], []
+        for _ in range(3):
+            pt = {j: rng.random() for j in range(1, d + 1)}
+            try:
+                v = hx(exprcore.eval(f, pt))
+            except Exception as exc:      # e.g. ZeroDivisionError at the point
+                v = type(exc).__name__
+            pts.append([hx(pt[j]) for j in range(1, d + 1)])
+            vals.append(v)
+        rec["points"], rec["values"] = pts, vals
+        out.append(rec)
+    return out
+
+
+def _cfg5_chunk(args):
+    """Worker: the reference's own points_block (lattice.py:96-105) over
+    [lo, hi) in blocks of 2^15 rows, integrand exp(-|x @ c - c.w|) in numpy
+    (the reference grammar has no abs, exprcore.py:638).  Returns the block
+    sums (np.sum, pairwise) in index order."""
+    lo, hi = args
+    cfg = make_config(5)
+    rule = LatticeRule(cfg.plain_n, cfg.plain_z())
+    c = np.asarray(cfg.c)
+    cw = float(np.dot(c, np.asarray(cfg.w)))
+    sums = []
+    blk = 1 << 15
+    for s in range(lo, hi, blk):
+        pts = points_block(rule, s, min(s + blk, hi))
+        sums.append(float(np.sum(np.exp(-np.abs(pts @ c - cw)))))
+    return sums
+
+
+def cfg5_full_case(procs):
+    """Config 5's plain sum over ALL n = 2^31 - 1 points from the reference's
+    own points_block.  Contiguous index chunks
+    of 2^22 points in `procs` processes; the block sums are combined with
+    math.fsum (correctly rounded), so the frozen total does not depend on the
+    process count.  About 70 min on 8 cores."""
+    import multiprocessing as mp
+    cfg = make_config(5)
+    n = cfg.plain_n
+    step = 1 << 22
+    chunks = [(lo, min(lo + step, n)) for lo in range(0, n, step)]
+    t0 = time.perf_counter()
+    block_sums = []
+    with mp.Pool(procs) as pool:
+        for k, sums in enumerate(pool.imap(_cfg5_chunk, chunks)):
+            block_sums.extend(sums)
+            if k % 32 == 0:
+                print(f"cfg5_full: chunk {k}/{len(chunks)} {time.perf_counter() - t0:.0f}s", flush=True)
+    total = math.fsum(block_sums)
+    return [{"tag": "cfg5_full", "kind": "ref_points+numpy", "text": cfg.text, "d": cfg.d,
+             "n": str(n), "a": cfg.plain_a, "i_begin": 0, "i_end": n, "block_rows": 1 << 15,
+             "n_blocks": len(block_sums), "sum_fsum": hx(total), "value": hx(total / n),
+             "procs": procs, "ref_seconds": time.perf_counter() - t0}]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
-    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites"], default=None)
+    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites", "cfg5_full", "linform", "fft", "parser"],
+                    default=None)
+    ap.add_argument("--procs", type=int, default=os.cpu_count())
     args = ap.parse_args()
     meta = {"generator": "tests/golden/make_golden.py", "numpy": np.__version__,
             "python": sys.version.split()[0], "reference": "/root/reference/pkg (latquad 0.1.0)"}
     jobs = {"points": lambda: points_cases(), "slr": lambda: slr_cases(args.skip_slow),
             "mdi": lambda: mdi_cases(args.skip_slow), "quality": quality_cases, "mc": mc_cases,
-            "suites": suite_cases}
+            "suites": suite_cases, "cfg5_full": lambda: cfg5_full_case(args.procs),
+            "linform": lambda: linform_cases(args.skip_slow), "fft": lambda: fft_cases_job(args.procs),
+            "parser": parser_cases}
     for name, fn in jobs.items():
-        if args.only and name != args.only:
+        if args.only != name and (args.only or name in ("cfg5_full", "linform", "fft")):
             continue
         t0 = time.perf_counter()
         cases = fn()

@@ -56,8 +56,10 @@ def test_config5_mdi_runs_and_is_plausible():
 
 
 def test_small_non_separable_grid_still_takes_the_direct_sweep():
+    # incommensurate coefficients: no level collapse (commensurate ones take
+    # lq_mdi_linform, tests/test_gpu_linform.py)
     import paper_2404_08867_b200 as lq
-    f = lq.parse("exp(-abs(x[1] - x[2] + 0.1))", 2)
+    f = lq.parse("exp(-abs(x[1] - 0.7390851332151607*x[2] + 0.1))", 2)
     value, rep = lq.mdi_lr(f, 2, 10, 101, with_report=True)
     assert rep.method == "direct"
 

@@ -9,6 +9,8 @@ import zlib
 import numpy as np
 import pytest
 
+import fft_cases
+
 pytestmark = pytest.mark.gpu
 
 REL = 1e-10
@@ -140,19 +142,11 @@ def test_orbit_cfg5_matches_index_kernel(env, monkeypatch):
 # unit mod n (LAYOUT_PAIRED, k_fam<PAIR>).
 
 def _family_text(family, d, rng):
-    c = [float(v) for v in rng.uniform(0, 1, d)]
-    w = [float(v) for v in rng.uniform(0, 1, d)]
-    if family == "exp":
-        return "exp(" + " + ".join(f"{c[j] / d!r}*x[{j + 1}]" for j in range(d)) + ")"
-    if family == "sincos":
-        return "cos(0.7 + " + " + ".join(f"{c[j]!r}*x[{j + 1}]" for j in range(d)) + ")"
-    if family == "expabs":
-        return "exp(-abs(" + " + ".join(f"{c[j] / 4!r}*(x[{j + 1}] - {w[j]!r})" for j in range(d)) + "))"
-    if family == "pow":
-        return "(1.5 + " + " + ".join(f"{c[j] / d!r}*x[{j + 1}]" for j in range(d)) + ")^(-3)"
-    if family == "qtrig":
-        return "0.5 + sin(0.3 + " + " + ".join(f"{c[j] ** 2 / 4!r}*(x[{j + 1}] - {w[j]!r})^2" for j in range(d)) + ")"
-    return "exp(-(" + " + ".join(f"{c[j] ** 2 / 4!r}*(x[{j + 1}] - {w[j]!r})^2" for j in range(d)) + "))"
+    return fft_cases.family_text(family, d, rng)[0]
+
+
+def _pair_text(family, d, rng, scale, offset):
+    return fft_cases.pair_text(family, d, rng, scale, offset)[0]
 
 
 def _unit_vector(n, d, rng):
@@ -437,7 +431,6 @@ def test_pair_fast_direct_kernels(env, layout, family, scale, offset, monkeypatc
     # exp offset -650 leave the normal range and fall back
     lq, N, engine = env
     from oracle import np_oracle
-    from test_gpu_fft import _pair_text
     n, d = 100003, 40
     rng = np.random.default_rng(zlib.crc32(f"pairdirect/{family}/{scale}".encode()))
     f = lq.parse(_pair_text(family, d, rng, scale, offset), d)
