@@ -164,6 +164,13 @@ int lq_mc_sum(lq_ctx* ctx, const lq_program* prog, int32_t d, uint64_t n, const 
 int lq_tensor_sum(lq_ctx* ctx, const lq_program* prog, int32_t d, const int64_t* counts,
                   const double* nodes, int32_t midpoint, uint64_t s_begin, uint64_t s_end,
                   double* sum_out);
+/* Sharded form: partials of tiles [t_begin, t_end) of the fixed tiling of
+ * [0, total) (LQ_TILE nodes per tile) into tiles_dev[t_begin .. t_end) (device);
+ * lq_reduce_sum over all ceil(total / LQ_TILE) tiles equals lq_tensor_sum over
+ * [0, total) bit for bit.  (mdi.py:104-136 sharded by flat index.) */
+int lq_tensor_partials(lq_ctx* ctx, const lq_program* prog, int32_t d, const int64_t* counts,
+                       const double* nodes, int32_t midpoint, uint64_t total, int64_t t_begin,
+                       int64_t t_end, double* tiles_dev);
 
 /* ---- MDI-LR cluster sums: replaces the symbolic level loop of
  * mdi.mdi_sum (mdi.py:139-192) for separable integrands.  Factor f is a
@@ -212,6 +219,13 @@ int lq_mdi_sum(lq_ctx* ctx, const lq_insn* insn, int32_t n_insn, const lq_factor
 int lq_mdi_expabs(lq_ctx* ctx, int32_t d, const double* beta, const int32_t* counts, double alpha,
                   const double* w_nodes, const double* w_weights, int32_t n_w, double kappa,
                   double* out2, double* logmag_out /* optional [n_w]: log|prod_j phi_j(w_k)| */);
+/* Sharded form: frequency nodes [floor(shard n_w / nshards), floor((shard+1) n_w / nshards))
+ * write their terms to out_dev[k] and log|prod_j phi_j(w_k)| to out_dev[n_w + k]
+ * (device, 2 n_w doubles, zero elsewhere); lq_reduce_sum of out_dev[0 .. n_w)
+ * after the exchange is the single-GPU sum bit for bit.                      */
+int lq_mdi_expabs_partials(lq_ctx* ctx, int32_t d, const double* beta, const int32_t* counts, double alpha,
+                           const double* w_nodes, const double* w_weights, int32_t n_w, double kappa,
+                           int32_t shard, int32_t nshards, double* out_dev);
 
 /* ---- MDI-LR level collapse for f = G(alpha + <beta, y>): replaces the level
  * loop of mdi.mdi_sum (mdi.py:152-165) for integrands whose coordinates enter

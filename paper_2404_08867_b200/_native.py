@@ -76,6 +76,10 @@ _SIGS = {
                   C.POINTER(C.c_double)],
     "lq_tensor_sum": [_P, C.POINTER(Program), C.c_int32, _P, _P, C.c_int32, C.c_uint64, C.c_uint64,
                       C.POINTER(C.c_double)],
+    "lq_tensor_partials": [_P, C.POINTER(Program), C.c_int32, _P, _P, C.c_int32, C.c_uint64, C.c_int64,
+                           C.c_int64, _P],
+    "lq_mdi_expabs_partials": [_P, C.c_int32, _P, _P, C.c_double, _P, _P, C.c_int32, C.c_double, C.c_int32,
+                               C.c_int32, _P],
     "lq_mdi_block_sums": [_P, _P, C.c_int32, _P, C.c_int32, _P, C.c_int64, C.c_int32, C.c_int32, _P],
     "lq_mdi_combine": [_P, _P, _P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, C.c_int32, _P],
     "lq_mdi_sum": [_P, _P, C.c_int32, _P, C.c_int32, _P, C.c_int64, _P, _P, _P, _P, _P, C.c_int32, _P],

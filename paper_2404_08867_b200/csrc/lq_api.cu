@@ -77,6 +77,9 @@ struct lq_ctx {
     const void* fft_key_buf = nullptr;
     // device copies of orbit-plan tables by plan id (a 2^k rule has one plan per level)
     std::map<uint64_t, std::pair<void*, size_t>> orb_tabs;
+    // dynamic shared-memory opt-ins made on this context's device, per kernel
+    // (cudaFuncSetAttribute is per device; a context is one device and one thread)
+    std::map<const void*, int> smem_optin;
 };
 
 namespace {
@@ -140,6 +143,15 @@ int upload(lq_ctx* c, int which, const void* src, size_t bytes, void** dst) {
     c->hoff += need;
     memcpy(h, src, bytes);
     CK(cudaMemcpyAsync(*dst, h, bytes, cudaMemcpyHostToDevice, c->stream));
+    return LQ_OK;
+}
+
+// Opt kernel `fn` into `bytes` of dynamic shared memory on the context's device.
+int smem_optin(lq_ctx* c, const void* fn, size_t bytes) {
+    auto it = c->smem_optin.find(fn);
+    if (it != c->smem_optin.end() && it->second >= (int)bytes) return LQ_OK;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    c->smem_optin[fn] = (int)bytes;
     return LQ_OK;
 }
 
@@ -251,11 +263,8 @@ int launch_fam_s(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev)
     const int na = KIND == lq::FAM_QUADP ? 2 : 1;
     const size_t smem = S > 1 ? sizeof(double) * na * lq::fam_pts(KIND) * lq::kThreads : 0;
     if (S > 1) {
-        static bool attr_set = false;   // per template instance
-        if (!attr_set) {
-            CK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr_set = true;
-        }
+        int rc = smem_optin(c, (const void*)kern, smem);
+        if (rc) return rc;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)ntiles, S, 1);
@@ -1066,9 +1075,7 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     if ((rc = orbit_tables(c, p, &G, &Alo, &Ahi, &apow, &starts))) return rc;
     const int d = f->d;
     const size_t smem = lq::kFftSmem;
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute((const void*)lq::k_fft_coeffs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    {
         const void* fns[] = {(const void*)lq::k_orbit_fft<lq::OUT_EXP, false>,
                              (const void*)lq::k_orbit_fft<lq::OUT_SINCOS, false>,
                              (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, false>,
@@ -1081,12 +1088,13 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
                              (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, true, 12>,
                              (const void*)lq::k_orbit_fft<lq::OUT_EXP, true, 13>,
                              (const void*)lq::k_orbit_fft<lq::OUT_SINCOS, true, 13>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, true, 13>};
-        for (const void* fn : fns) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaFuncSetAttribute((const void*)lq::k_fft_coeffs_pm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft_quad<lq::OUT_EXP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaFuncSetAttribute((const void*)lq::k_orbit_fft_quad<lq::OUT_SINCOS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+                             (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, true, 13>,
+                             (const void*)lq::k_fft_coeffs,
+                             (const void*)lq::k_fft_coeffs_pm,
+                             (const void*)lq::k_orbit_fft_quad<lq::OUT_EXP>,
+                             (const void*)lq::k_orbit_fft_quad<lq::OUT_SINCOS>};
+        for (const void* fn : fns)
+            if ((rc = smem_optin(c, fn, smem))) return rc;
     }
     void *W, *Hc, *dc;
     if ((rc = dev_buf(c, B_FFTW, sizeof(double2) * lq::kFftN, &W))) return rc;
@@ -1696,13 +1704,15 @@ int lq_mc_sum(lq_ctx* c, const lq_program* pg, int32_t d, uint64_t n, const uint
     return read_scalar(c, r, sum_out);
 }
 
-int lq_tensor_sum(lq_ctx* c, const lq_program* pg, int32_t d, const int64_t* counts, const double* nodes,
-                  int32_t midpoint, uint64_t s_begin, uint64_t s_end, double* sum_out) {
+namespace {
+// Tile partials of the flat range [s_begin, s_end) (tiles of LQ_TILE nodes from
+// s_begin) into tiles_out, or -- tiles_out == NULL -- their fixed-tree sum.
+int tensor_tiles(lq_ctx* c, const lq_program* pg, int32_t d, const int64_t* counts, const double* nodes,
+                 int32_t midpoint, uint64_t s_begin, uint64_t s_end, double* tiles_out, double* sum_out) {
     int rc = set_dev(c);
     if (rc) return rc;
     if (!pg || !pg->insn || pg->n_insn < 1) return fail(LQ_ERR_VALUE, "null program");
     if (d < 0 || d > lq::kMaxAxes) return fail(LQ_ERR_UNSUPPORTED, "tensor sum supports 0..%d axes, got %d", lq::kMaxAxes, d);
-    if (!sum_out) return fail(LQ_ERR_VALUE, "null output");
     if (pg->n_vars > d) return fail(LQ_ERR_VALUE, "program uses %d axes, grid has %d", pg->n_vars, d);
     const int ns = pick_slots(pg->n_slots);
     if (ns < 0) return fail(LQ_ERR_UNSUPPORTED, "program needs %d slots (max %d)", pg->n_slots, LQ_MAX_SLOTS);
@@ -1713,7 +1723,7 @@ int lq_tensor_sum(lq_ctx* c, const lq_program* pg, int32_t d, const int64_t* cou
     }
     if (s_end < s_begin) return fail(LQ_ERR_VALUE, "bad flat range");
     if (s_end == s_begin) {
-        *sum_out = 0.0;
+        if (sum_out) *sum_out = 0.0;
         return LQ_OK;
     }
     void *dp, *dc, *doff, *dn;
@@ -1737,8 +1747,8 @@ int lq_tensor_sum(lq_ctx* c, const lq_program* pg, int32_t d, const int64_t* cou
         if ((rc = upload(c, B_AUX2, nodes, sizeof(double) * total_nodes, &dn))) return rc;
     }
     const int64_t ntiles = (int64_t)((s_end - s_begin + LQ_TILE - 1) / LQ_TILE);
-    void* tiles;
-    if ((rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
+    void* tiles = tiles_out;
+    if (!tiles && (rc = dev_buf(c, B_TILES, sizeof(double) * ntiles, &tiles))) return rc;
     const void* kern = ns == 32 ? (const void*)lq::k_prog_tensor<32> : (const void*)lq::k_prog_tensor<LQ_MAX_SLOTS>;
     int grid = grid_for(c, kern, ntiles);
     t_begin(c);
@@ -1753,9 +1763,27 @@ int lq_tensor_sum(lq_ctx* c, const lq_program* pg, int32_t d, const int64_t* cou
         lq::k_prog_tensor<LQ_MAX_SLOTS><<<grid, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, pg->n_insn, pg->result, d, (const int64_t*)dc, (const int64_t*)doff, (const double*)dn, s_begin, s_end, ntiles, (double*)tiles);
     t_end(c);
     CK(cudaGetLastError());
+    if (tiles_out) return LQ_OK;
     double* r;
     if ((rc = reduce_dev(c, (const double*)tiles, ntiles, &r))) return rc;
     return read_scalar(c, r, sum_out);
+}
+}  // namespace
+
+int lq_tensor_sum(lq_ctx* c, const lq_program* pg, int32_t d, const int64_t* counts, const double* nodes,
+                  int32_t midpoint, uint64_t s_begin, uint64_t s_end, double* sum_out) {
+    if (!sum_out) return fail(LQ_ERR_VALUE, "null output");
+    return tensor_tiles(c, pg, d, counts, nodes, midpoint, s_begin, s_end, nullptr, sum_out);
+}
+
+int lq_tensor_partials(lq_ctx* c, const lq_program* pg, int32_t d, const int64_t* counts, const double* nodes,
+                       int32_t midpoint, uint64_t total, int64_t t_begin, int64_t t_end, double* tiles_dev) {
+    if (!tiles_dev) return fail(LQ_ERR_VALUE, "null output");
+    const int64_t T = (int64_t)((total + LQ_TILE - 1) / LQ_TILE);
+    if (t_begin < 0 || t_end > T || t_end < t_begin) return fail(LQ_ERR_VALUE, "bad tile range [%lld, %lld) of %lld",
+                                                                 (long long)t_begin, (long long)t_end, (long long)T);
+    const uint64_t s0 = (uint64_t)t_begin * LQ_TILE, s1 = std::min<uint64_t>((uint64_t)t_end * LQ_TILE, total);
+    return tensor_tiles(c, pg, d, counts, nodes, midpoint, s0, s1, tiles_dev + t_begin, nullptr);
 }
 
 static int mdi_validate(const lq_insn* insn, int32_t n_insn, const lq_factor* fac, int32_t nf, int* nblk, int* ns) {
@@ -1851,37 +1879,48 @@ int lq_mdi_sum(lq_ctx* c, const lq_insn* insn, int32_t n_insn, const lq_factor* 
     return lq_mdi_combine(c, (const double*)part, fac, nf, nblk, term_ptr, term_fac, coef_re, coef_im, log_extra, n_terms, out4);
 }
 
+namespace {
+// Per-node terms of the characteristic-function integral for nodes [k0, k1):
+// vals[k], logmag[k] (device pointers indexed by the global node number).
+int expabs_nodes(lq_ctx* c, int32_t d, const double* beta, const int32_t* counts, double alpha, const double* wn,
+                 const double* ww, int32_t n_w, double kappa, int32_t k0, int32_t k1, double* vals, double* logmag) {
+    int rc;
+    void *db, *dc, *dw, *dww;
+    if ((rc = upload(c, B_AUX0, beta, sizeof(double) * d, &db))) return rc;
+    if ((rc = upload(c, B_AUX1, counts, sizeof(int32_t) * d, &dc))) return rc;
+    if ((rc = upload(c, B_AUX2, wn, sizeof(double) * n_w, &dw))) return rc;
+    if ((rc = upload(c, B_AUX3, ww, sizeof(double) * n_w, &dww))) return rc;
+    if (k1 <= k0) return LQ_OK;
+    // closed-form Dirichlet sums (default) or the direct N-term sums (LQ_CF_DIRECT=1)
+    const char* direct = std::getenv("LQ_CF_DIRECT");
+    const double *w0 = (const double*)dw + k0, *ww0 = (const double*)dww + k0;
+    t_begin(c);
+    if (direct && !std::strcmp(direct, "1")) {
+        lq::k_cf_expabs<<<k1 - k0, lq::kThreads, 0, c->stream>>>((const double*)db, (const int32_t*)dc, d, alpha, w0,
+                                                                 ww0, kappa, vals + k0, logmag + k0);
+    } else {
+        double bsum = 0.0;
+        for (int j = 0; j < d; ++j) bsum += beta[j];
+        lq::k_cf_expabs_closed<<<k1 - k0, lq::kThreads, 0, c->stream>>>((const double*)db, (const int32_t*)dc, d,
+                                                                        alpha + 0.5 * bsum, w0, ww0, kappa,
+                                                                        vals + k0, logmag + k0);
+    }
+    t_end(c);
+    CK(cudaGetLastError());
+    return LQ_OK;
+}
+}  // namespace
+
 int lq_mdi_expabs(lq_ctx* c, int32_t d, const double* beta, const int32_t* counts, double alpha, const double* wn,
                   const double* ww, int32_t n_w, double kappa, double* out2, double* logmag) {
     int rc = set_dev(c);
     if (rc) return rc;
     if (d < 1 || !beta || !counts || !wn || !ww || n_w < 1 || !out2) return fail(LQ_ERR_VALUE, "bad expabs arguments");
     if (!(kappa < 0.0)) return fail(LQ_ERR_VALUE, "kappa must be negative");
-    void *db, *dc, *dw, *dww, *dv;
-    if ((rc = upload(c, B_AUX0, beta, sizeof(double) * d, &db))) return rc;
-    if ((rc = upload(c, B_AUX1, counts, sizeof(int32_t) * d, &dc))) return rc;
-    if ((rc = upload(c, B_AUX2, wn, sizeof(double) * n_w, &dw))) return rc;
-    if ((rc = upload(c, B_AUX3, ww, sizeof(double) * n_w, &dww))) return rc;
-    void* dl;
+    void *dv, *dl;
     if ((rc = dev_buf(c, B_TILES, sizeof(double) * n_w, &dv))) return rc;
     if ((rc = dev_buf(c, B_PART, sizeof(double) * n_w, &dl))) return rc;
-    // closed-form Dirichlet sums (default) or the direct N-term sums (LQ_CF_DIRECT=1)
-    const char* direct = std::getenv("LQ_CF_DIRECT");
-    t_begin(c);
-    if (direct && !std::strcmp(direct, "1")) {
-        lq::k_cf_expabs<<<n_w, lq::kThreads, 0, c->stream>>>((const double*)db, (const int32_t*)dc, d, alpha,
-                                                             (const double*)dw, (const double*)dww, kappa,
-                                                             (double*)dv, (double*)dl);
-    } else {
-        double bsum = 0.0;
-        for (int j = 0; j < d; ++j) bsum += beta[j];
-        lq::k_cf_expabs_closed<<<n_w, lq::kThreads, 0, c->stream>>>((const double*)db, (const int32_t*)dc, d,
-                                                                    alpha + 0.5 * bsum, (const double*)dw,
-                                                                    (const double*)dww, kappa, (double*)dv,
-                                                                    (double*)dl);
-    }
-    t_end(c);
-    CK(cudaGetLastError());
+    if ((rc = expabs_nodes(c, d, beta, counts, alpha, wn, ww, n_w, kappa, 0, n_w, (double*)dv, (double*)dl))) return rc;
     double* r;
     if ((rc = reduce_dev(c, (const double*)dv, n_w, &r))) return rc;
     double s;
@@ -1893,6 +1932,19 @@ int lq_mdi_expabs(lq_ctx* c, int32_t d, const double* beta, const int32_t* count
     out2[0] = s == 0.0 ? -INFINITY : std::log(std::fabs(s));
     out2[1] = s > 0.0 ? 1.0 : (s < 0.0 ? -1.0 : 0.0);
     return LQ_OK;
+}
+
+int lq_mdi_expabs_partials(lq_ctx* c, int32_t d, const double* beta, const int32_t* counts, double alpha,
+                           const double* wn, const double* ww, int32_t n_w, double kappa, int32_t shard,
+                           int32_t nshards, double* out_dev) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (d < 1 || !beta || !counts || !wn || !ww || n_w < 1 || !out_dev) return fail(LQ_ERR_VALUE, "bad expabs arguments");
+    if (!(kappa < 0.0)) return fail(LQ_ERR_VALUE, "kappa must be negative");
+    if (nshards < 1 || shard < 0 || shard >= nshards) return fail(LQ_ERR_VALUE, "bad shard %d of %d", shard, nshards);
+    const int32_t k0 = (int32_t)((int64_t)shard * n_w / nshards), k1 = (int32_t)((int64_t)(shard + 1) * n_w / nshards);
+    CK(cudaMemsetAsync(out_dev, 0, sizeof(double) * 2 * n_w, c->stream));
+    return expabs_nodes(c, d, beta, counts, alpha, wn, ww, n_w, kappa, k0, k1, out_dev, out_dev + n_w);
 }
 
 // MDI level collapse for G(alpha + <beta, y>) (lq.h): the distribution of the
@@ -1933,8 +1985,7 @@ int lq_mdi_linform(lq_ctx* c, const lq_program* G, int32_t n_levels, const int64
     const char* force_global = std::getenv("LQ_LINFORM_SMEM");   // "0": global-memory levels (tests)
     t_begin(c);
     if (K <= kSmemCap && !(force_global && !std::strcmp(force_global, "0"))) {
-        CK(cudaFuncSetAttribute((const void*)lq::k_linform_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(2 * sizeof(double) * kSmemCap)));
+        if ((rc = smem_optin(c, (const void*)lq::k_linform_smem, 2 * sizeof(double) * kSmemCap))) return rc;
         lq::k_linform_smem<<<1, 1024, 2 * sizeof(double) * K, c->stream>>>((const lq::LinLevel*)dlv, n_levels, K,
                                                                            (double*)dp);
         c->launches++;

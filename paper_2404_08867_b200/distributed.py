@@ -9,9 +9,12 @@ is exact (x + 0 = x in IEEE arithmetic) whatever order NCCL reduces in, so
 every rank then holds the same vector and runs the same fixed pairwise tree:
 the estimate is bit-identical for any GPU count.
 
-MDI-LR: the node blocks of every direction's cluster sum are split across
-ranks the same way (lq_mdi_block_sums shard/nshards), exchanged with one
-all-reduce over disjoint slots, then combined in log-polar form on each rank.
+MDI-LR: the same front-end as one GPU (mdi.mdi_lr) with a Comm: the node
+blocks of every direction's cluster sum (separable), the frequency nodes of
+the characteristic-function integral (exp-abs past the cap), the support
+tiles of the level collapse (one commensurate linear form) and the flat-index
+tiles of the direct sweep are split across ranks, exchanged with one
+all-reduce over disjoint slots, and reduced by the same fixed trees.
 """
 
 from __future__ import annotations
@@ -19,16 +22,15 @@ from __future__ import annotations
 import ctypes as C
 import time
 
-import numpy as np
 
 from . import _native as N, engine
 from .expr import as_expr, evaluate, free_vars
 from .lattice import korobov_vector
-from .mdi import MdiConfig, _level_plan, _normalize, _det_a, mdi_lr as _mdi_lr_single, GridCapError
+from .mdi import GridCapError, mdi_lr as _mdi_lr_single
 from .quad import _result
 from .transform import midpoint_grids
 
-__all__ = ["shard_range", "exchange_disjoint", "slr_integrate", "mdi_lr", "world"]
+__all__ = ["shard_range", "exchange_disjoint", "slr_integrate", "mdi_lr", "implr_integrate", "world", "Comm"]
 
 
 def world(group=None):
@@ -84,6 +86,7 @@ def slr_integrate(f, rule, reference=None, group=None):
         from .quad import slr_integrate as single
         return single(e, rule, reference)
     pi = engine.plain_integrand(e, d)
+    engine.attach_jit(pi, n)     # the single-GPU path's code choice, a function of (f, n)
     h = N.lib()
     ctx = N.ctx(torch.cuda.current_device())
     _bind_stream(h, ctx)
@@ -101,42 +104,65 @@ def slr_integrate(f, rule, reference=None, group=None):
     return _result("slr", out.value / n, n, d, n, a, None, t0, reference)
 
 
+class Comm:
+    """The exchange step of a sharded call, for the engine (engine.py): this
+    rank's share of a fixed tiling, zeroed device vectors for the partials,
+    one all-reduce over disjoint slots, and liblq's fixed-tree reduction."""
+
+    def __init__(self, group=None):
+        import torch
+        self.group = group
+        self.rank, self.size = world(group)
+        self._torch = torch
+        self._ctx = None
+
+    def ctx(self):
+        if self._ctx is None:
+            h = N.lib()
+            self._ctx = N.ctx(self._torch.cuda.current_device())
+            _bind_stream(h, self._ctx)
+        return self._ctx
+
+    def shard(self, units):
+        return shard_range(units, self.rank, self.size)
+
+    def zeros(self, count):
+        self.ctx()
+        return self._torch.zeros(int(count), dtype=self._torch.float64, device="cuda")
+
+    def exchange(self, vec):
+        return exchange_disjoint(vec, self.group)
+
+    def reduce(self, vec, count=None):
+        out = C.c_double()
+        N.check(N.lib().lq_reduce_sum(self.ctx(), C.c_void_p(vec.data_ptr()),
+                                      int(vec.numel() if count is None else count), C.byref(out)))
+        return out.value
+
+
 def mdi_lr(f, d, a, n, cfg=None, rule=None, with_report=False, group=None):
-    """Multi-GPU MDI-LR: node blocks of every cluster sum sharded across ranks."""
-    import torch
+    """Multi-GPU MDI-LR: the single-GPU front-end (validation, branch choice,
+    report) with every branch's device work sharded -- node blocks of the
+    cluster sums, frequency nodes of the characteristic function, support
+    tiles of the level collapse, flat-index tiles of the direct sweep -- and
+    one exchange each."""
     rank, size = world(group)
-    if size == 1:
-        return _mdi_lr_single(f, d, a, n, cfg=cfg, rule=rule, with_report=with_report)
-    cfg = cfg if cfg is not None else MdiConfig()
-    rule = rule if rule is not None else korobov_vector(a, n, d)
+    comm = Comm(group) if size > 1 else None
+    return _mdi_lr_single(f, d, a, n, cfg=cfg, rule=rule, with_report=with_report, comm=comm)
+
+
+def implr_integrate(f, d, a, n, cap=None, rule=None, reference=None, group=None):
+    """Multi-GPU implr_integrate (quad.py:107-119): the direct sweep's tiles
+    sharded across ranks."""
+    from .mdi import DIRECT_CAP, direct_tensor_sum
+    t0 = time.perf_counter()
+    cap = DIRECT_CAP if cap is None else cap
+    if rule is None:
+        rule = korobov_vector(a, n, d)
     grids = midpoint_grids(rule)
-    e = as_expr(f)
-    plan = engine.separable_plan(e, grids.counts) if free_vars(e) else None
-    if plan is None or not plan.ok:
-        return _mdi_lr_single(f, d, a, n, cfg=cfg, rule=rule, with_report=with_report)
-    levels, base_axes = _level_plan(d, cfg)
-    base_total = int(np.prod([grids.counts[ax - 1] for ax in base_axes], dtype=object))
-    if base_total > cfg.direct_cap:
-        raise GridCapError(f"direct sweep needs {base_total} evaluations, cap is {cfg.direct_cap}")
-    h = N.lib()
-    ctx = N.ctx(torch.cuda.current_device())
-    _bind_stream(h, ctx)
-    nblk = max((int(plan.factors[k].count) + N.LQ_NODE_BLOCK - 1) // N.LQ_NODE_BLOCK
-               for k in range(plan.n_factors))
-    part = torch.zeros(plan.n_factors * nblk * 2, dtype=torch.float64, device="cuda")
-    N.check(h.lq_mdi_block_sums(ctx, N.as_ptr(plan.insn), plan.n_insn, C.cast(plan.factors, C.c_void_p),
-                                plan.n_factors, None, 0, rank, size, C.c_void_p(part.data_ptr())))
-    exchange_disjoint(part, group)
-    out = np.zeros(4)
-    N.check(h.lq_mdi_combine(ctx, C.c_void_p(part.data_ptr()), C.cast(plan.factors, C.c_void_p), plan.n_factors,
-                             nblk, N.as_ptr(plan.term_ptr), N.as_ptr(plan.term_fac), N.as_ptr(plan.coef_re),
-                             N.as_ptr(plan.coef_im), N.as_ptr(plan.log_extra), plan.n_terms, N.as_ptr(out)))
-    raw = float(out[2])
-    value = _normalize(raw, grids.counts)
-    if not with_report:
-        return value
-    from .mdi import MdiReport
-    rep = MdiReport(value=raw, levels=levels, base_dim=len(base_axes), level_nodes=(plan.n_factors,) * levels,
-                    level_seconds=(0.0,) * levels, fallback=False, det_a=_det_a(rule), log_raw=float(out[0]),
-                    sign=float(out[1]), method="separable", clusters=plan.n_factors)
-    return value, rep
+    total = grids.total
+    if total > cap:
+        raise GridCapError(f"improved rule needs {total} direct evaluations, cap is {cap}")
+    rank, size = world(group)
+    value = direct_tensor_sum(f, grids, cap, comm=Comm(group) if size > 1 else None) / total
+    return _result("implr", value, total, d, n, a, None, t0, reference)

@@ -98,12 +98,15 @@ def plain_integrand(f, d, force_program=False):
     return _plain_cache.get_or((e, d, force_program), make)
 
 
-def attach_jit(pi, n, npts):
+def attach_jit(pi, n):
     """Give an interpreted plain-sum integrand its NVRTC-compiled kernel when
-    the work is large enough to pay for the compile (jit.py)."""
+    the full lattice is large enough to pay for the compile (jit.py).  The
+    choice depends on (f, n) only -- not on the index range of the call -- so
+    every rank of a sharded sum and every sub-range call of the same lattice
+    run the same code."""
     from . import jit
     interpreted = pi.family is None or n > 2**31
-    if interpreted and not pi.struct.prog.jit and jit.jit_wanted(npts * max(len(pi.program), 1)):
+    if interpreted and not pi.struct.prog.jit and jit.jit_wanted(int(n) * max(len(pi.program), 1)):
         h = jit.compile_expr(pi.expr)
         if h:
             pi.struct.prog.jit = h
@@ -112,7 +115,7 @@ def attach_jit(pi, n, npts):
 def lattice_sum(pi, n, z_reduced, i_begin=0, i_end=None):
     """sum_{i in [i_begin, i_end)} f(x_i) on the GPU (not divided by n)."""
     i_end = n if i_end is None else i_end
-    attach_jit(pi, n, max(0, int(i_end) - int(i_begin)))
+    attach_jit(pi, n)
     out = C.c_double()
     N.check(N.lib().lq_lattice_sum(N.ctx(), C.byref(pi.struct), n, N.as_ptr(z_reduced),
                                    int(i_begin), int(i_end), C.byref(out)))
@@ -124,17 +127,14 @@ def tensor_program(g):
     return _prog_cache.get_or(e, lambda: compile_program(e))
 
 
-def tensor_sum(g, grids, s_begin=0, s_end=None):
-    """Direct grid sum of g (non-constant) on the GPU; flat index first-axis-fastest."""
+def _tensor_program_struct(g, grids):
     prog = tensor_program(g)
     d = grids.d
-    counts = np.asarray(grids.counts, dtype=np.int64)
-    total = grids.total
-    s_end = total if s_end is None else s_end
     ins = np.ascontiguousarray(prog.insn)
     from . import jit
     jh = None
-    if jit.jit_wanted((int(s_end) - int(s_begin)) * max(len(ins), 1)) and d <= 128:
+    # JIT choice from the whole grid (same code on every rank and sub-range)
+    if jit.jit_wanted(int(grids.total) * max(len(ins), 1)) and d <= 128:
         jh = jit.compile_expr(as_expr(g), n_axes=max(d, 1))
     p = N.Program(ins.ctypes.data, len(ins), prog.n_slots, prog.result, prog.n_vars, jh)
     if getattr(grids, "midpoint", False):
@@ -143,6 +143,25 @@ def tensor_sum(g, grids, s_begin=0, s_end=None):
         nodes = np.ascontiguousarray(np.concatenate([np.asarray(nd, dtype=np.float64) for nd in grids.nodes])
                                      if d else np.zeros(1))
         mid = 0
+    return ins, p, np.asarray(grids.counts, dtype=np.int64), nodes, mid
+
+
+def tensor_sum(g, grids, s_begin=0, s_end=None, comm=None):
+    """Direct grid sum of g (non-constant) on the GPU; flat index first-axis-fastest.
+    With ``comm`` (distributed.Comm, size > 1) the tiles of the full grid are
+    sharded across ranks and exchanged: bit-identical to one GPU."""
+    ins, p, counts, nodes, mid = _tensor_program_struct(g, grids)
+    d = grids.d
+    total = int(grids.total)
+    if comm is not None and comm.size > 1 and s_begin == 0 and s_end in (None, total):
+        T = -(-total // N.LQ_TILE)
+        lo, hi = comm.shard(T)
+        tiles = comm.zeros(T)
+        if hi > lo:
+            N.check(N.lib().lq_tensor_partials(comm.ctx(), C.byref(p), d, N.as_ptr(counts), N.as_ptr(nodes), mid,
+                                               total, lo, hi, C.c_void_p(tiles.data_ptr())))
+        return comm.reduce(comm.exchange(tiles))
+    s_end = total if s_end is None else s_end
     out = C.c_double()
     N.check(N.lib().lq_tensor_sum(N.ctx(), C.byref(p), d, N.as_ptr(counts), N.as_ptr(nodes), mid,
                                   int(s_begin), int(s_end), C.byref(out)))
@@ -230,10 +249,27 @@ def separable_plan(g, counts, nodes=None):
     return _sep_cache.get_or(key, lambda: SeparablePlan(e, counts, nodes))
 
 
-def mdi_separable_sum(plan):
-    """(log|raw|, sign, raw, im) of the full-grid sum via per-direction cluster sums."""
+def mdi_separable_sum(plan, comm=None):
+    """(log|raw|, sign, raw, im) of the full-grid sum via per-direction cluster
+    sums.  With ``comm`` (size > 1) the node blocks of every direction are
+    sharded across ranks ("cluster range of the current coordinate", SURVEY
+    §8e), exchanged once, and combined on every rank."""
     out = np.zeros(4)
     n_nodes = 0 if plan.nodes is None else len(plan.nodes)
+    if comm is not None and comm.size > 1:
+        nblk = max((int(plan.factors[k].count) + N.LQ_NODE_BLOCK - 1) // N.LQ_NODE_BLOCK
+                   for k in range(plan.n_factors))
+        part = comm.zeros(plan.n_factors * nblk * 2)
+        ctx = comm.ctx()
+        N.check(N.lib().lq_mdi_block_sums(ctx, N.as_ptr(plan.insn), plan.n_insn, C.cast(plan.factors, C.c_void_p),
+                                          plan.n_factors, N.as_ptr(plan.nodes), n_nodes, comm.rank, comm.size,
+                                          C.c_void_p(part.data_ptr())))
+        comm.exchange(part)
+        N.check(N.lib().lq_mdi_combine(ctx, C.c_void_p(part.data_ptr()), C.cast(plan.factors, C.c_void_p),
+                                       plan.n_factors, nblk, N.as_ptr(plan.term_ptr), N.as_ptr(plan.term_fac),
+                                       N.as_ptr(plan.coef_re), N.as_ptr(plan.coef_im), N.as_ptr(plan.log_extra),
+                                       plan.n_terms, N.as_ptr(out)))
+        return float(out[0]), float(out[1]), float(out[2]), float(out[3])
     N.check(N.lib().lq_mdi_sum(N.ctx(), N.as_ptr(plan.insn), plan.n_insn, C.cast(plan.factors, C.c_void_p),
                                plan.n_factors, N.as_ptr(plan.nodes), n_nodes,
                                N.as_ptr(plan.term_ptr), N.as_ptr(plan.term_fac),
@@ -284,11 +320,24 @@ def _cf_inputs(beta, counts, alpha, kappa):
     return _cf_cache.get_or(key, make)
 
 
-def mdi_expabs_cf(beta, counts, alpha, kappa):
+def mdi_expabs_cf(beta, counts, alpha, kappa, comm=None):
     """E = mean over the midpoint grid of exp(kappa |alpha + <beta, y>|), kappa < 0,
     by the characteristic function on the GPU (lq_mdi_expabs).  Returns
-    (E, tail_bound) where tail_bound bounds |prod_j phi_j| beyond Omega."""
+    (E, tail_bound) where tail_bound bounds |prod_j phi_j| beyond Omega.  With
+    ``comm`` (size > 1) the frequency nodes are sharded across ranks."""
     beta, cnt, wn, ww, n_nodes = _cf_inputs(beta, counts, alpha, kappa)
+    if comm is not None and comm.size > 1:
+        nw = len(wn)
+        buf = comm.zeros(2 * nw)
+        N.check(N.lib().lq_mdi_expabs_partials(comm.ctx(), len(beta), N.as_ptr(beta), N.as_ptr(cnt), float(alpha),
+                                               N.as_ptr(wn), N.as_ptr(ww), nw, float(kappa), comm.rank, comm.size,
+                                               C.c_void_p(buf.data_ptr())))
+        comm.exchange(buf)
+        s = comm.reduce(buf, count=nw)
+        logmag = buf[nw:].cpu().numpy()
+        E = s * 2.0 / math.pi
+        tail = float(np.exp(np.max(logmag[n_nodes:]))) if nw > n_nodes else 0.0
+        return E, tail
     out = np.zeros(2)
     logmag = np.zeros(len(wn))
     N.check(N.lib().lq_mdi_expabs(N.ctx(), len(beta), N.as_ptr(beta), N.as_ptr(cnt), float(alpha),
@@ -371,10 +420,20 @@ def linform_plan(g, counts):
     return _lin_cache.get_or((e, tuple(int(c) for c in counts)), lambda: LinformPlan(e, counts))
 
 
-def mdi_linform_mean(plan, shard=0, nshards=1, tiles_dev=None):
+def mdi_linform_mean(plan, shard=0, nshards=1, tiles_dev=None, comm=None):
     """Grid mean of G(<beta, y>) via the level-collapse kernels (single GPU), or
     this shard's tile partials into ``tiles_dev`` (a device pointer with
-    ``plan.tiles`` doubles)."""
+    ``plan.tiles`` doubles).  With ``comm`` (size > 1): every rank convolves
+    the level distributions (d small launches) and evaluates G on its share of
+    the support tiles; one exchange, then the fixed tree."""
+    if comm is not None and comm.size > 1:
+        tiles = comm.zeros(plan.tiles)
+        ins, p = plan.program_struct()
+        out = C.c_double()
+        N.check(N.lib().lq_mdi_linform(comm.ctx(), C.byref(p), len(plan.m), N.as_ptr(plan.m), N.as_ptr(plan.n),
+                                       0.0, plan.h, int(plan.m0), comm.rank, comm.size,
+                                       C.c_void_p(tiles.data_ptr()), plan.tiles, C.byref(out)))
+        return comm.reduce(comm.exchange(tiles))
     ins, p = plan.program_struct()
     out = C.c_double()
     N.check(N.lib().lq_mdi_linform(N.ctx(), C.byref(p), len(plan.m), N.as_ptr(plan.m), N.as_ptr(plan.n), 0.0,

@@ -139,8 +139,9 @@ def _const_levels(value, counts, cfg):
     return (_const_sweep(v, base) if base else v), levels, base_axes
 
 
-def direct_tensor_sum(g, grids, cap=DIRECT_CAP):
-    """Brute-force grid sum on the GPU (mdi.py:104-136); raises past ``cap``."""
+def direct_tensor_sum(g, grids, cap=DIRECT_CAP, comm=None):
+    """Brute-force grid sum on the GPU (mdi.py:104-136); raises past ``cap``.
+    ``comm`` (distributed.Comm): flat-index tiles sharded across ranks."""
     counts = list(grids.counts)
     total = math.prod(counts) if counts else 1
     if total > cap:
@@ -150,7 +151,7 @@ def direct_tensor_sum(g, grids, cap=DIRECT_CAP):
         if not counts:
             return evaluate(e, {})
         return _const_sweep(evaluate(e, {}), counts)
-    return engine.tensor_sum(e, grids)
+    return engine.tensor_sum(e, grids, comm=comm)
 
 
 def _level_plan(d, cfg):
@@ -163,8 +164,10 @@ def _level_plan(d, cfg):
     return levels, axes
 
 
-def mdi_sum(g, grids, cfg=None):
-    """Full grid sum of g by dimension iteration (mdi.py:139-192)."""
+def mdi_sum(g, grids, cfg=None, comm=None):
+    """Full grid sum of g by dimension iteration (mdi.py:139-192).  ``comm``
+    (distributed.Comm, size > 1) shards the device work of every branch across
+    ranks with one exchange; the result is the single-GPU one bit for bit."""
     cfg = cfg if cfg is not None else MdiConfig()
     d = grids.d
     e = as_expr(g)
@@ -193,17 +196,17 @@ def mdi_sum(g, grids, cfg=None):
         # extension, the reference has no |.|), functions of one commensurate
         # linear form by the distribution of the partial form (lq_mdi_linform)
         if total > cfg.direct_cap and cfg.fallback == "numeric":
-            rep = _characteristic(e, d, counts, levels, base_axes, t0)
+            rep = _characteristic(e, d, counts, levels, base_axes, t0, comm)
             if rep is not None:
                 return rep
-        rep = _linform(e, counts, levels, base_axes, cfg, t0)
+        rep = _linform(e, counts, levels, base_axes, cfg, t0, comm)
         if rep is not None:
             return rep
     if not usable:
         if cfg.fallback == "error":
             raise BudgetExceededError("integrand is not separable over the grid axes "
                                       f"(budget {cfg.budget}); no level reduction possible")
-        value = direct_tensor_sum(e, grids, cap=cfg.direct_cap)
+        value = direct_tensor_sum(e, grids, cap=cfg.direct_cap, comm=comm)
         return MdiReport(value=value, levels=0, base_dim=d, base_seconds=time.perf_counter() - t0,
                          fallback=True, log_raw=math.log(abs(value)) if value else -math.inf,
                          sign=math.copysign(1.0, value) if value else 0.0, method="direct")
@@ -211,7 +214,7 @@ def mdi_sum(g, grids, cfg=None):
     base_total = math.prod(counts[a - 1] for a in base_axes)
     if base_total > cfg.direct_cap:
         raise GridCapError(f"direct sweep needs {base_total} evaluations, cap is {cfg.direct_cap}")
-    log_raw, sign, raw, _ = engine.mdi_separable_sum(plan)
+    log_raw, sign, raw, _ = engine.mdi_separable_sum(plan, comm)
     secs = time.perf_counter() - t0
     return MdiReport(value=raw, levels=levels, base_dim=len(base_axes),
                      level_nodes=(plan.n_factors,) * levels, level_seconds=(0.0,) * levels,
@@ -219,7 +222,7 @@ def mdi_sum(g, grids, cfg=None):
                      method="separable", clusters=plan.n_factors)
 
 
-def _linform(e, counts, levels, base_axes, cfg, t0):
+def _linform(e, counts, levels, base_axes, cfg, t0, comm=None):
     """f = G(alpha + <beta, y>) with commensurate steps beta_j / (2 N_j): the
     level collapse the reference's partial sums perform by like-term
     collection (each level's partial sums take the values of the partial
@@ -228,9 +231,11 @@ def _linform(e, counts, levels, base_axes, cfg, t0):
     GPU (lq_mdi_linform), then G over its support.  None when e is not of
     this form or its support is too large."""
     plan = engine.linform_plan(e, counts)
-    if not plan.ok:
+    # the node budget bounds what a level may carry (exprcore.py:399-401); here
+    # a level carries its distinct partial-form values
+    if not plan.ok or max(plan.level_support, default=1) > cfg.budget:
         return None
-    mean = engine.mdi_linform_mean(plan)
+    mean = engine.mdi_linform_mean(plan, comm=comm)
     log_total = _log_total(counts)
     raw, log_raw, sign = _raw_from_mean(mean, counts, log_total)
     stripped = plan.level_support[:levels * cfg.m:cfg.m] if cfg.m > 1 else plan.level_support[:levels]
@@ -255,7 +260,7 @@ def _raw_from_mean(mean, counts, log_total):
     return raw, log_raw, sign
 
 
-def _characteristic(e, d, counts, levels, base_axes, t0):
+def _characteristic(e, d, counts, levels, base_axes, t0, comm=None):
     """K exp(kappa |alpha + <beta, x>|), kappa < 0, over the midpoint grid via
     e^{-k|L|} = (1/pi) int k/(k^2 + w^2) cos(w L) dw: the grid mean becomes a
     1-D integral of products of per-direction cluster sums
@@ -273,7 +278,7 @@ def _characteristic(e, d, counts, levels, base_axes, t0):
     else:
         if len(counts) < 2 or _grid_facts(counts).max_count > 2**31 - 1:
             return None
-        mean, tail = engine.mdi_expabs_cf(beta, counts, fam.alpha, fam.kappa)
+        mean, tail = engine.mdi_expabs_cf(beta, counts, fam.alpha, fam.kappa, comm)
         if not (mean > 0.0) or tail > 1e-16 * mean:
             return None
     log_raw = math.log(abs(fam.K)) + math.log(mean) + log_total
@@ -361,15 +366,16 @@ def _total(counts):
     return _grid_facts(counts).total
 
 
-def mdi_lr(f, d, a, n, cfg=None, rule=None, with_report=False):
-    """Improved-rule quadrature via dimension iteration (mdi.py:215-234)."""
+def mdi_lr(f, d, a, n, cfg=None, rule=None, with_report=False, comm=None):
+    """Improved-rule quadrature via dimension iteration (mdi.py:215-234);
+    ``comm`` shards the device work across ranks (distributed.mdi_lr)."""
     cfg = cfg if cfg is not None else MdiConfig()
     if rule is None:
         rule = korobov_vector(a, n, d)
     elif rule.d != d:
         raise ValueError(f"rule dimension {rule.d} != {d}")
     grids = midpoint_grids(rule)
-    report = mdi_sum(f, grids, cfg)
+    report = mdi_sum(f, grids, cfg, comm)
     report.det_a = _det_a(rule)
     report.log_total = _log_total(grids.counts)
     value = _normalize(report.value, grids.counts)

@@ -68,7 +68,8 @@ def test_invpow_matches_exact_multiset_oracle(d, a):
 @pytest.mark.parametrize("seed", range(6))
 @pytest.mark.parametrize("force_global", ["1", "0"])
 def test_random_commensurate_forms(seed, force_global, monkeypatch):
-    """Integer coefficients of both signs, zero coefficients, unequal counts;
+    """Integer coefficients of both signs, zero coefficients, unequal counts
+    (powers of two);
     both the shared-memory and the global-memory level kernels."""
     monkeypatch.setenv("LQ_LINFORM_SMEM", force_global)
     import paper_2404_08867_b200 as lq
@@ -77,7 +78,11 @@ def test_random_commensurate_forms(seed, force_global, monkeypatch):
     d = int(rng.integers(3, 9))
     coef = [int(v) for v in rng.integers(-4, 5, d)]
     coef[0] = coef[0] or 1
-    counts = tuple(int(v) for v in rng.integers(2, 40, d))
+    # commensurate node spacings (powers of two, or the Korobov (N, ..., N, N')
+    # shape): unrelated counts make the partial forms' values distinct, the
+    # support outgrows the node budget and the direct sweep runs, as in the
+    # reference, whose constants then do not coincide either
+    counts = tuple(int(v) for v in rng.choice([4, 8, 16, 32], d))
     alpha = 2.0 + float(sum(abs(c) for c in coef))
     text = f"({alpha!r} + " + " + ".join(f"{c}*x[{j + 1}]" for j, c in enumerate(coef)) + ")^(-2)"
     f = lq.parse(text, d)
@@ -90,10 +95,10 @@ def test_random_commensurate_forms(seed, force_global, monkeypatch):
 
 
 def test_large_support_global_path_equals_numpy_pmf():
-    """Support past shared memory (K > 12800): d = 60 directions with steps 1..5."""
+    """Support past shared memory (K > 12800): d = 80 directions with steps 1..5."""
     import paper_2404_08867_b200 as lq
     from oracle.np_oracle import linear_form_grid_mean_np
-    d, N = 60, 64
+    d, N = 80, 64
     coef = [1 + (j % 5) for j in range(d)]
     text = "1/(1 + " + " + ".join(f"{c}*x[{j + 1}]" for j, c in enumerate(coef)) + ")"
     f = lq.parse(text, d)
@@ -124,8 +129,8 @@ def test_sharded_tiles_sum_to_the_single_gpu_mean(nshards):
     import paper_2404_08867_b200 as lq
     from paper_2404_08867_b200 import _native as N
     from paper_2404_08867_b200 import engine
-    d, N_ = 40, 64
-    text = "1/(1 + " + " + ".join(f"{1 + j % 3}*x[{j + 1}]" for j in range(d)) + ")^2"
+    d, N_ = 100, 64
+    text = "1/(1 + " + " + ".join(f"{1 + j % 7}*x[{j + 1}]" for j in range(d)) + ")^2"
     plan = engine.linform_plan(lq.parse(text, d), (N_,) * d)
     assert plan.ok and plan.tiles >= nshards
     single = engine.mdi_linform_mean(plan)

@@ -128,8 +128,11 @@ def test_mdi_golden(lq, golden):
             assert abs(value - want) <= REL * abs(want), (case["tag"], value, want)
         else:
             assert value == 0.0, case["tag"]
-        if rep.method == "separable":
+        if rep.method in ("separable", "linform"):
+            # levels collapse (product form, or one commensurate linear form)
             assert (rep.levels, rep.base_dim) == (case["levels"], case["base_dim"]), case["tag"]
+            if rep.method == "linform":
+                assert not case["fallback"], case["tag"]
         else:   # non-separable: the reference's full-grid fallback sweep (mdi.py:167-179)
             assert rep.method in ("direct", "constant"), case["tag"]
         if "implr" in case:
