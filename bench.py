@@ -116,19 +116,55 @@ def cpu_model():
     return "unknown"
 
 
-def cpu_port_rate(cfg, npts, workers=1):
-    """The CPU oracle (numpy restatement of lattice.points_block + the
-    integrand, oracle/np_oracle.py) on the first ``npts`` points; pts/s."""
-    from oracle import cpu_baseline as cb
+def ref_rate(npts, workers):
+    """(pts/s, seconds, kind, what) of config 5's plain sum over its first
+    ``npts`` points on the host: the reference itself from baseline/_ref
+    (its lattice.points_block + the integrand in numpy) when installed, else
+    the oracle's numpy restatement of the same (oracle/cpu_baseline.py)."""
+    sys.path.insert(0, os.path.join(REPO, "baseline"))
+    import ref_cpu
     t0 = time.perf_counter()
-    s = cb.cfg5_range_sum(cfg, 0, npts, workers=workers)
+    if ref_cpu.available():
+        ref_cpu.cfg5_range_sum(0, npts, workers=workers)
+        kind, what = "reference", ("latquad.lattice.points_block from baseline/_ref (the reference itself) "
+                                   "+ exp(-|x c - c.w|) in numpy")
+    else:
+        from oracle import cpu_baseline as cb
+        from paper_2404_08867_b200.configs import make_config
+        cb.cfg5_range_sum(make_config(5), 0, npts, workers=workers)
+        kind, what = "port", "numpy restatement of lattice.points_block + integrand (oracle/np_oracle.py)"
     dt = time.perf_counter() - t0
-    return npts / dt, dt, s
+    return npts / dt, dt, kind, what
+
+
+def _suite_job(which):
+    sys.path.insert(0, os.path.join(REPO, "baseline"))
+    import ref_cpu
+    return ref_cpu.suite_one(which)
+
+
+def reference_suite():
+    """The reference's public API as is on configs 1-3 (slr_integrate) and 2, 1
+    (mdi_lr), each on one host core (five processes side by side); None when
+    baseline/_ref is not installed."""
+    sys.path.insert(0, os.path.join(REPO, "baseline"))
+    import ref_cpu
+    if not ref_cpu.available():
+        return None
+    import multiprocessing as mp
+    jobs = ["slr1", "slr2", "slr3", "mdi2", "mdi1"]
+    with mp.get_context("spawn").Pool(len(jobs)) as pool:
+        res = pool.map(_suite_job, jobs)
+    out = {}
+    for r in res:
+        out.update(r)
+    return out
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU path (oracle port; the reference is
-    pure Python and cannot travel to the GPU box) on all host cores."""
+    """--impl reference: the reference's CPU path for config 5 on all host
+    cores -- latquad itself from baseline/_ref (points_block + the integrand in
+    numpy; the grammar has no |.|), else the oracle's restatement."""
     if rank != 0:
         return
     from paper_2404_08867_b200.configs import make_config
@@ -136,10 +172,10 @@ def run_reference(args, rank, world):
     cores = os.cpu_count() or 1
     sample = args.ref_sample
     for _ in range(args.warmup):
-        cpu_port_rate(cfg, sample // 4, workers=cores)
+        ref_rate(sample // 4, cores)
     t = 0.0
     for _ in range(args.steps):
-        rate, dt, _ = cpu_port_rate(cfg, sample, workers=cores)
+        rate, dt, kind, what = ref_rate(sample, cores)
         t += dt
     value = args.steps * sample / t
     line = {
@@ -148,9 +184,9 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "cfg5_plain_sum", "d": cfg.d, "n": cfg.plain_n, "a": cfg.plain_a,
                    "integrand": "exp(-|sum c_j (x_j - w_j)|)", "sample_points_per_step": sample},
-        "cpu_baseline": {"value": value, "unit": "f-evals/s", "cores": cores, "kind": "port",
-                         "sample": f"first {sample} points of cfg5 per step, numpy restatement of "
-                                   f"lattice.points_block + integrand over {cores} processes",
+        "cpu_baseline": {"value": value, "unit": "f-evals/s", "cores": cores, "kind": kind,
+                         "sample": f"first {sample} points of cfg5 per step, {what}, contiguous index ranges "
+                                   f"over {cores} processes",
                          "cpu_model": cpu_model(), "host_cores": os.cpu_count()},
         "e2e": {"value": value, "unit": "f-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -166,6 +202,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 21)
     ap.add_argument("--ref-sample", type=int, default=1 << 21)
     ap.add_argument("--no-mdi", action="store_true")
+    ap.add_argument("--no-ref-suite", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -202,9 +239,16 @@ def main():
     torch.cuda.set_stream(stream)
     N.check(h.lq_ctx_set_stream(ctx, C.c_void_p(stream.cuda_stream)))
 
+    # cold first call of the public API in this process: text -> estimate,
+    # including lowering, the orbit plan (primality, ord(a), primitive root,
+    # chain-start tables), their upload, the coefficient transform and the sum
     cfg = make_config(5)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     f = lq.parse(cfg.text, cfg.d)
     rule = lq.korobov_vector(cfg.plain_a, cfg.plain_n, cfg.d)
+    cold_est = lq.slr_integrate(f, rule).value
+    cold_ms = (time.perf_counter() - t0) * 1e3
     n, d = rule.n, rule.d
     z = rule.z_reduced_array()
     pi = engine.plain_integrand(f, d)
@@ -319,24 +363,26 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    xfer0 = [C.c_int64() for _ in range(3)]
+    N.check(h.lq_ctx_transfer_bytes(ctx, *[C.byref(x) for x in xfer0]))
     t0 = time.perf_counter()
     for _ in range(args.steps):
         r = api(f, rule)
     e2e_s = time.perf_counter() - t0
+    xfer1 = [C.c_int64() for _ in range(3)]
+    N.check(h.lq_ctx_transfer_bytes(ctx, *[C.byref(x) for x in xfer1]))
+    h2d, d2h, params = [(b.value - a.value) / args.steps for a, b in zip(xfer0, xfer1)]
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    # H2D per call: the kernel-parameter struct (coefficient table + header);
-    # the orbit start tables are uploaded once per context and plan
-    if lay.mode == N.LAYOUT_ORBIT_FFT:
-        h2d = 8 * d + 216 + 32                               # coefficients + FftHead + launch arguments
-    elif lay.mode == N.LAYOUT_ORBIT:
-        h2d = 8 * (-(-d // ORB_M) * ORB_M) + 152 + 24          # OrbLinArgs<1008> + launch arguments
-    else:
-        h2d = 24 * d + 112 + 16                                # FamArgs<LinDim, 1000> + launch arguments
+    # bytes counted by liblq at its cudaMemcpy calls (lq_ctx_transfer_bytes):
+    # the coefficient upload and the 8-byte result per call; the FFT launch's
+    # parameter struct (FftHead, passed by value) is reported beside them
     e2e = {"value": args.steps * n / e2e_s, "unit": "f-evals/s",
-           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8,
+           "h2d_bytes_per_step": h2d + params, "d2h_bytes_per_step": d2h,
+           "h2d_breakdown": {"cudaMemcpy": h2d, "kernel_params": params},
+           "cold_first_call_ms": cold_ms, "cold_first_call_estimate": cold_est,
            "api": ("paper_2404_08867_b200.slr_integrate(f, rule)" if world == 1
                    else "paper_2404_08867_b200.distributed.slr_integrate(f, rule)"),
            "estimate": r.value}
@@ -350,10 +396,9 @@ def main():
 
     cpu = None
     if world == 1 and args.cpu_sample > 0:
-        rate, dt, _ = cpu_port_rate(cfg, args.cpu_sample, workers=1)
-        cpu = {"value": rate, "unit": "f-evals/s", "cores": 1, "kind": "port",
-               "sample": f"first {args.cpu_sample} points of cfg5 (numpy restatement of lattice.points_block "
-                         f"+ exp(-|.|), oracle/np_oracle.py), {dt:.1f} s on 1 core; "
+        rate, dt, kind, what = ref_rate(args.cpu_sample, 1)
+        cpu = {"value": rate, "unit": "f-evals/s", "cores": 1, "kind": kind,
+               "sample": f"first {args.cpu_sample} points of cfg5 ({what}), {dt:.1f} s on 1 core; "
                          f"{os.cpu_count()} host cores, numpy {np.__version__}",
                "cpu_model": cpu_model(), "host_cores": os.cpu_count()}
 
@@ -385,6 +430,19 @@ def main():
                 lq.slr_integrate(g, prule)
                 ts.append(time.perf_counter() - t0)
             mdi[f"plain_cfg{cid}_e2e_ms"] = min(ts) * 1e3
+        if not args.no_ref_suite:
+            # the reference as is, same box, same run (baseline/_ref; one core each)
+            ref = reference_suite()
+            if ref is None:
+                mdi["reference"] = "baseline/_ref not installed on this box"
+            else:
+                mdi["reference"] = ref
+                for key, ours in (("slr_cfg1_s", "plain_cfg1_e2e_ms"), ("slr_cfg2_s", "plain_cfg2_e2e_ms"),
+                                  ("slr_cfg3_s", "plain_cfg3_e2e_ms"), ("mdi_cfg2_s", "cfg2_ms"),
+                                  ("mdi_cfg1_s", "cfg1_ms")):
+                    if key in ref:
+                        mdi[f"speedup_{key[:-2]}"] = ref[key] / (mdi[ours] * 1e-3)
+                mdi["reference_cores"] = "1 core per config (5 processes side by side)"
 
     line = {
         "metric": METRIC, "value": value, "unit": "f-evals/s", "n_gpus": world,

@@ -104,6 +104,10 @@ int lq_device_info(lq_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);
 /* Device time (ms) of the main kernel of the last timed call (0 if none). */
 int lq_ctx_enable_timing(lq_ctx* ctx, int enable);
 int lq_last_kernel_ms(lq_ctx* ctx, float* ms, int64_t* launches);
+/* Cumulative bytes this context moved host->device and device->host with
+ * cudaMemcpy*, and the kernel-parameter bytes of its FFT-form lattice-sum
+ * launches (the e2e accounting of bench.py reads the difference per step). */
+int lq_ctx_transfer_bytes(lq_ctx* ctx, int64_t* h2d, int64_t* d2h, int64_t* params);
 
 /* ---- points: replaces lattice.points_block (lattice.py:96-105) ---------
  * out[(i-start)*d + j] = RN(((i * z_reduced[j]) mod n) / n), i in [start, stop),

@@ -66,6 +66,7 @@ _SIGS = {
     "lq_device_info": [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "lq_ctx_enable_timing": [_P, C.c_int],
     "lq_last_kernel_ms": [_P, C.POINTER(C.c_float), C.POINTER(C.c_int64)],
+    "lq_ctx_transfer_bytes": [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
     "lq_points_block": [_P, C.c_int32, C.c_uint64, _P, C.c_int64, C.c_int64, _P, C.c_int32],
     "lq_lattice_sum": [_P, C.POINTER(Integrand), C.c_uint64, _P, C.c_uint64, C.c_uint64, C.POINTER(C.c_double)],
     "lq_lattice_partials": [_P, C.POINTER(Integrand), C.c_uint64, _P, C.c_int64, C.c_int64, _P],

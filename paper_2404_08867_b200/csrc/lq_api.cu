@@ -80,6 +80,9 @@ struct lq_ctx {
     // dynamic shared-memory opt-ins made on this context's device, per kernel
     // (cudaFuncSetAttribute is per device; a context is one device and one thread)
     std::map<const void*, int> smem_optin;
+    // bytes moved between host and device by this context (cudaMemcpy*), and
+    // kernel-parameter bytes of the lattice-sum launches (lq_ctx_transfer_bytes)
+    int64_t h2d_bytes = 0, d2h_bytes = 0, param_bytes = 0;
 };
 
 namespace {
@@ -143,6 +146,7 @@ int upload(lq_ctx* c, int which, const void* src, size_t bytes, void** dst) {
     c->hoff += need;
     memcpy(h, src, bytes);
     CK(cudaMemcpyAsync(*dst, h, bytes, cudaMemcpyHostToDevice, c->stream));
+    c->h2d_bytes += (int64_t)bytes;
     return LQ_OK;
 }
 
@@ -208,6 +212,7 @@ int read_scalar(lq_ctx* c, const double* dev, double* out, int k = 1) {
     // (staged uploads still in flight read their slices before this copy
     // writes: same stream, in order)
     CK(cudaMemcpyAsync(h, dev, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+    c->d2h_bytes += (int64_t)(sizeof(double) * k);
     CK(cudaStreamSynchronize(c->stream));
     c->hoff = 0;
     memcpy(out, h, sizeof(double) * k);
@@ -943,6 +948,7 @@ int orbit_tables(lq_ctx* c, const OrbPlan& p, const uint32_t** G, const uint32_t
         void* d = nullptr;
         CK(cudaMalloc(&d, bytes));
         CK(cudaMemcpy(d, all.data(), bytes, cudaMemcpyHostToDevice));   // once per (context, plan)
+        c->h2d_bytes += (int64_t)bytes;
         it = c->orb_tabs.emplace(p.id, std::make_pair(d, bytes)).first;
     }
     const uint32_t* base = (const uint32_t*)it->second.first;
@@ -1061,6 +1067,13 @@ bool pair_fast_consts(const lq_integrand* f, double bsum, lq::PairFast& q) {
         q.ym = (double)lam; q.ya = (double)(lam * alpha); q.E = (double)(lam * D); q.post = f->K;
         split_exp(-lam * D, q.c0, q.k0);
         split_exp(lam * D, q.c1, q.k1);
+        // centred form (lq::pair_expabs_c): u = lam (l - sum beta / 2), c = |lam D| / 2
+        const long double cth = fabsl(lam * D) / 2.0L;
+        q.yc = (double)(lam * alpha - lam * D / 2.0L);
+        q.cth = (double)cth;
+        double cm;
+        split_exp(-cth, cm, q.ke);
+        split_exp(2.0L * cth, q.c2m, q.k2);
         q.on = 1;
         return true;
     }
@@ -1152,9 +1165,17 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     h.Hc = (const double2*)Hc;
     h.alpha = f->alpha; h.alphaB = f->alpha + bsum; h.K = f->K; h.A = f->A; h.Bc = f->B; h.C0 = f->C0;
     h.kappa = f->kappa; h.pw = f->power;
+    const int outer = lin_outer(f->kind);
+    const bool fast = !quad && pair_fast_consts(f, bsum, h.pf);
+    // the exp table of the pair outer; the centred exp-abs form folds e^{-c}
+    // into it (lq::pair_expabs_c)
+    long double tscale = 1.0L;
+    if (fast && outer == lq::OUT_EXPABS && LQ_FFT_CENTRED) {
+        tscale = expl(-(long double)h.pf.cth);   // e^{-c} >= e^{-700}: a normal double
+    }
     for (int j = 0; j < lq::kFftExpTab; ++j)
-        h.etab[j] = make_double2((double)exp2l(j / (long double)lq::kFftExpTab),
-                                 (double)exp2l(-(j / (long double)lq::kFftExpTab)));
+        h.etab[j] = make_double2((double)(exp2l(j / (long double)lq::kFftExpTab) * tscale),
+                                 (double)(exp2l(-(j / (long double)lq::kFftExpTab)) * tscale));
     // several tiles per CTA once there are many waves: the twiddle fill is
     // paid once per CTA
     const int per = (int)std::max<int64_t>(1, std::min<int64_t>(kFftTilesPerCta, ntiles / (2 * 148 * 16)));
@@ -1170,8 +1191,7 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
         CK(cudaGetLastError());
         return LQ_OK;
     }
-    const int outer = lin_outer(f->kind);
-    const bool fast = pair_fast_consts(f, bsum, h.pf);
+    c->param_bytes += (int64_t)(sizeof(h) + sizeof(unit0) + sizeof(ntiles) + sizeof(per) + sizeof(tiles_dev));
     t_begin(c);
     // positions per thread that can hold a chain point: B <= RM N/R
     const int rm = (int)((p.m + lq::kFftThreads - 1) / lq::kFftThreads);
@@ -1481,6 +1501,14 @@ int lq_ctx_enable_timing(lq_ctx* c, int enable) {
     return LQ_OK;
 }
 
+int lq_ctx_transfer_bytes(lq_ctx* c, int64_t* h2d, int64_t* d2h, int64_t* params) {
+    if (!c) return fail(LQ_ERR_VALUE, "null lq_ctx");
+    if (h2d) *h2d = c->h2d_bytes;
+    if (d2h) *d2h = c->d2h_bytes;
+    if (params) *params = c->param_bytes;
+    return LQ_OK;
+}
+
 int lq_last_kernel_ms(lq_ctx* c, float* ms, int64_t* launches) {
     int rc = set_dev(c);
     if (rc) return rc;
@@ -1538,6 +1566,7 @@ int lq_points_block(lq_ctx* c, int32_t d, uint64_t n, const uint64_t* z, int64_t
     CK(cudaGetLastError());
     if (!out_is_device) {
         CK(cudaMemcpyAsync(out, dst, n_elem * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        c->d2h_bytes += (int64_t)(n_elem * sizeof(double));
         CK(cudaStreamSynchronize(c->stream));
     }
     return LQ_OK;
@@ -1927,6 +1956,7 @@ int lq_mdi_expabs(lq_ctx* c, int32_t d, const double* beta, const int32_t* count
     if ((rc = read_scalar(c, r, &s))) return rc;
     if (logmag) {
         CK(cudaMemcpyAsync(logmag, dl, sizeof(double) * n_w, cudaMemcpyDeviceToHost, c->stream));
+        c->d2h_bytes += (int64_t)(sizeof(double) * n_w);
         CK(cudaStreamSynchronize(c->stream));
     }
     out2[0] = s == 0.0 ? -INFINITY : std::log(std::fabs(s));
@@ -2174,6 +2204,7 @@ int lq_cbc_construct(lq_ctx* c, uint64_t n, int32_t d, const double* gamma, doub
         t_end(c);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(vals.data(), dv, sizeof(double) * ncand, cudaMemcpyDeviceToHost, c->stream));
+        c->d2h_bytes += (int64_t)(sizeof(double) * ncand);
         CK(cudaStreamSynchronize(c->stream));
         int64_t best = -1;
         double best_val = INFINITY;
@@ -2218,6 +2249,7 @@ int lq_korobov_values(lq_ctx* c, uint64_t n, int32_t d, const double* gamma, dou
     t_end(c);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(sums_out, dv, sizeof(double) * ncand, cudaMemcpyDeviceToHost, c->stream));
+    c->d2h_bytes += (int64_t)(sizeof(double) * ncand);
     CK(cudaStreamSynchronize(c->stream));
     return LQ_OK;
 }

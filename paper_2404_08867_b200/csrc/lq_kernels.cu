@@ -184,6 +184,10 @@ struct PairFast {
     double post;         // multiplier after the sum (K; 1 for SINCOS)
     int32_t k0, k1;      // binary exponents of c0, c1
     int32_t on;          // the host enabled the form (else two outer evaluations)
+    // centred EXPABS form (pair_expabs_c): u = fma(l, ym, yc), threshold c = |E|/2,
+    // e^{-c} = cm 2^ke (cm folded into the exp table), e^{2c} = c2m 2^k2
+    int32_t ke, k2;
+    double yc, cth, c2m;
 };
 
 // v 2^j by exponent arithmetic (v 2^j must be a normal double)
@@ -272,6 +276,51 @@ __device__ __forceinline__ double pair_fast_tab(double l, const PairFast& q, con
         const bool s1 = y >= 0.0, s2 = y <= q.E, same = s1 == s2;
         return f1 + scale2((same ? m : p) * (s2 ? q.c0 : q.c1), (s2 ? q.k0 : q.k1) + (same ? -k : k));
     }
+}
+
+// Centred exp-abs pair: with u = y - E/2, w = |u| and c = |E|/2 the point and
+// its mirror give e^{-|y|} + e^{-|E-y|} = e^{-c} e^{-w} + (w >= c ? e^{c} e^{-w}
+// : e^{-c} e^{w}) -- one range reduction of -w, one comparison, one select.
+// T[j] = (2^(j/2^EB) e^{-c}, 2^(-j/2^EB) e^{-c}) (host; normal while c <= 700).
+__device__ __forceinline__ double pair_expabs_c(double l, const PairFast& q, const double2* __restrict__ T) {
+    constexpr int EB = kFftExpBits;
+    static_assert(EB >= 6, "degree-5 polynomial halves need |r| <= ln2/128");
+    const double u = fma(l, q.ym, q.yc);
+    const double t = fma(-fabs(u), (double)(1 << EB) * 1.4426950408889634, 6755399441055744.0);
+    const int K = __double2loint(t);
+    const double kf = t - 6755399441055744.0;
+    double r = fma(kf, -(6.93147180559945286e-01 / (1 << EB)), -fabs(u));
+    r = fma(kf, -(2.319046813846299558e-17 / (1 << EB)), r);
+    const int k = K >> EB;
+    const double2 tj = T[K & ((1 << EB) - 1)];
+    const double r2 = r * r;
+    double e = fma(r2, 4.1666666666666664e-02, 0.5);
+    double o = fma(r2, 8.3333333333333332e-03, 0.16666666666666666);
+    e = fma(r2, e, 1.0);
+    o = fma(r2, o, 1.0);
+    const double p = fma(r, o, e) * tj.x;    // e^{-w} e^{-c} 2^-k
+    const double m = fma(-r, o, e) * tj.y;   // e^{w} e^{-c} 2^k
+    const bool ge = fabs(u) >= q.cth;
+    const double t2 = ge ? p * q.c2m : m;
+    const int e2 = ge ? k + q.k2 : -k;
+    return scale2(p, k) + scale2(t2, e2);
+}
+
+#ifndef LQ_FFT_CENTRED
+#define LQ_FFT_CENTRED 1
+#endif
+#ifndef LQ_FFT_FULLTILE
+#define LQ_FFT_FULLTILE 1
+#endif
+
+template <int OUTER>
+__device__ __forceinline__ double pair_outer_fft(double l, const PairFast& q, const double2* __restrict__ T) {
+#if LQ_FFT_EXPTAB
+    if constexpr (OUTER == OUT_EXPABS && LQ_FFT_CENTRED) return pair_expabs_c(l, q, T);
+    else return pair_fast_tab<OUTER>(l, q, T);
+#else
+    return pair_fast<OUTER>(l, q);
+#endif
 }
 
 __global__ void __launch_bounds__(kThreads) k_fft_twiddles(double2* __restrict__ W) {
@@ -1016,17 +1065,34 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
         // directly, skipping warps whose positions are all past the chains
         fft4096_regs<false>(v, buf, Wt);
         const int v0 = fft_chain_valid(a, u0), v1 = fft_chain_valid(a, u1);
-        const int vmax = max(v0, v1), wbase = threadIdx.x & ~31;
-        #pragma unroll
-        for (int r = 0; r < RM; ++r) {
-            if (wbase + r * kFftThreads < vmax) {
-                const int k = threadIdx.x + r * kFftThreads;
 #if LQ_FFT_EXPTAB
-                const double g0 = pair_fast_tab<OUTER>(v[r].x, a.pf, et), g1 = pair_fast_tab<OUTER>(-v[r].y, a.pf, et);
+        const double2* T = et;
 #else
-                const double g0 = pair_fast<OUTER>(v[r].x, a.pf), g1 = pair_fast<OUTER>(-v[r].y, a.pf);
+        const double2* T = nullptr;
 #endif
-                s += (k < v0 ? g0 : 0.0) + (k < v1 ? g1 : 0.0);
+        const int B = (int)a.B;
+        if (LQ_FFT_FULLTILE && v0 == B && v1 == B && (RM - 1) * kFftThreads < B) {
+            // both chains full (every tile but the last of a coset): positions
+            // r < RM - 1 are all inside the chains -- no masks, no branches
+            #pragma unroll
+            for (int r = 0; r < RM - 1; ++r)
+                s += pair_outer_fft<OUTER>(v[r].x, a.pf, T) + pair_outer_fft<OUTER>(-v[r].y, a.pf, T);
+            if ((threadIdx.x & ~31) + (RM - 1) * kFftThreads < B) {
+                const int k = threadIdx.x + (RM - 1) * kFftThreads;
+                const double g = pair_outer_fft<OUTER>(v[RM - 1].x, a.pf, T) +
+                                 pair_outer_fft<OUTER>(-v[RM - 1].y, a.pf, T);
+                s += k < B ? g : 0.0;
+            }
+        } else {
+            const int vmax = max(v0, v1), wbase = threadIdx.x & ~31;
+            #pragma unroll
+            for (int r = 0; r < RM; ++r) {
+                if (wbase + r * kFftThreads < vmax) {
+                    const int k = threadIdx.x + r * kFftThreads;
+                    const double g0 = pair_outer_fft<OUTER>(v[r].x, a.pf, T),
+                                 g1 = pair_outer_fft<OUTER>(-v[r].y, a.pf, T);
+                    s += (k < v0 ? g0 : 0.0) + (k < v1 ? g1 : 0.0);
+                }
             }
         }
         s *= a.pf.post;
