@@ -439,6 +439,27 @@ def parser_cases():
     return out
 
 
+def suite7_cases():
+    """Suite test7 (bench.py:140-143: MDI-LR over d at n = 8^d + 1, a = 8) rows
+    with d <= 10 from the reference's own row runner: expalt, ratprod,
+    gaussian, coslin, expsq (separable) and invpow (collapses by like-term
+    collection; d = 10 takes ~7 min here)."""
+    from latquad import bench as rbench
+    out = []
+    for spec in rbench.suite_specs("test7"):
+        if spec[2] > 10:
+            continue
+        t0 = time.perf_counter()
+        rec = rbench._run_row(spec, 0, False)
+        out.append({"suite": "test7", "method": rec.method, "integrand": rec.integrand, "d": rec.d,
+                    "n": str(rec.n), "a": rec.a, "status": rec.status,
+                    "value": None if rec.value is None else hx(rec.value),
+                    "reference": None if rec.reference is None else hx(rec.reference),
+                    "ref_seconds": time.perf_counter() - t0})
+        print(f"suite7 {spec}: {time.perf_counter() - t0:.1f}s", flush=True)
+    return out
+
+
 def _cfg5_chunk(args):
     """Worker: the reference's own points_block (lattice.py:96-105) over
     [lo, hi) in blocks of 2^15 rows, integrand exp(-|x @ c - c.w|) in numpy
@@ -485,7 +506,7 @@ def cfg5_full_case(procs):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
-    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites", "cfg5_full", "linform", "fft", "parser"],
+    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites", "cfg5_full", "linform", "fft", "parser", "suites7"],
                     default=None)
     ap.add_argument("--procs", type=int, default=os.cpu_count())
     args = ap.parse_args()
@@ -495,9 +516,9 @@ def main():
             "mdi": lambda: mdi_cases(args.skip_slow), "quality": quality_cases, "mc": mc_cases,
             "suites": suite_cases, "cfg5_full": lambda: cfg5_full_case(args.procs),
             "linform": lambda: linform_cases(args.skip_slow), "fft": lambda: fft_cases_job(args.procs),
-            "parser": parser_cases}
+            "parser": parser_cases, "suites7": suite7_cases}
     for name, fn in jobs.items():
-        if args.only != name and (args.only or name in ("cfg5_full", "linform", "fft")):
+        if args.only != name and (args.only or name in ("cfg5_full", "linform", "fft", "suites7")):
             continue
         t0 = time.perf_counter()
         cases = fn()

@@ -111,3 +111,49 @@ def test_mc_oracle_pinned_to_reference():
         for i in (0, 1, first.shape[0] - 1):
             for j in range(d):
                 assert np_oracle.pcg64_draw(st["state"], st["inc"], i * d + j) == first[i, j], (case["tag"], i, j)
+
+
+def test_oracle_eval_matches_reference_eval_on_parser_corpus():
+    """The oracle's evaluator (np_oracle.eval_array, over the product's parse)
+    against the reference's exprcore.eval frozen at three points per text of
+    the parser corpus (tests/golden/parser.json)."""
+    import math
+    from paper_2404_08867_b200 import expr as E
+    from oracle import np_oracle
+    from conftest import load_golden, unhex
+    n = 0
+    for case in load_golden("parser"):
+        if "error" in case:
+            continue
+        f = E.parse(case["text"], case["d"])
+        tol = 1e-10 if E.free_vars(f) else 1e-8
+        for pt, want in zip(case["points"], case["values"]):
+            assign = {j + 1: np.array([unhex(v)]) for j, v in enumerate(pt)}
+            got = float(np.asarray(np_oracle.eval_array(f, assign)).reshape(-1)[0])
+            w = unhex(want)
+            assert got == w or math.isclose(got, w, rel_tol=tol, abs_tol=1e-300), (case["text"], got, w)
+            n += 1
+    assert n > 900
+
+
+def test_as_expr_accepts_real_latquad_expressions():
+    """The drop-in adapter on the reference's own Expr objects (build
+    container only: needs /root/reference importable)."""
+    import math
+    import os
+    import sys
+    if not os.path.isdir("/root/reference/pkg/src/latquad"):
+        import pytest
+        pytest.skip("reference not importable here")
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from latquad import corpus, exprcore
+    from paper_2404_08867_b200 import expr as E
+    rng = np.random.default_rng(3)
+    for entry in corpus.entries():
+        d = max(3, entry.min_d)
+        ref = exprcore.parse(entry.text, d)
+        ours = E.as_expr(ref)
+        for _ in range(3):
+            pt = {j: float(rng.random()) for j in range(1, d + 1)}
+            a, b = exprcore.eval(ref, pt), E.evaluate(ours, pt)
+            assert math.isclose(a, b, rel_tol=1e-13), (entry.id, a, b)
