@@ -39,14 +39,15 @@ constexpr int kFftExpTab = LQ_FFT_EXPTAB ? 1 << kFftExpBits : 0;   // (2^(j/2^EB
 constexpr int kFftSmem = (kFftPad + (kFftR == 16 ? kFftTwAll : 0) + kFftExpTab) * 16;   // bytes per CTA
 
 // Build the radix-16 tables from the global table W[k] = e^{-2 pi i k / N}.
-__device__ __forceinline__ void fft_load_twiddles(double2* __restrict__ tw, const double2* __restrict__ W) {
+__device__ __forceinline__ void fft_load_twiddles(double2* __restrict__ tw, const double2* __restrict__ W,
+                                                  int nthreads = kFftThreads) {
     if constexpr (kFftR != 16) return;   // radix 8 reads the global table directly
-    for (int i = threadIdx.x; i < kFftTw3; i += kFftThreads) {
+    for (int i = threadIdx.x; i < kFftTw3; i += nthreads) {
         const int q = i / 256 + 1, k = i & 255;
         tw[i] = __ldg(W + q * k);
         tw[kFftTw3 + i] = __ldg(W + ((4 * q * k) & (kFftN - 1)));
     }
-    for (int i = threadIdx.x; i < kFftTw2; i += kFftThreads) {
+    for (int i = threadIdx.x; i < kFftTw2; i += nthreads) {
         const int r = i / 16 + 1, k = i & 15;
         tw[2 * kFftTw3 + i] = __ldg(W + ((16 * r * k) & (kFftN - 1)));
     }
@@ -161,10 +162,18 @@ __host__ __device__ constexpr int dft_slot(int k) {
 //    + r Ns) or -- for the last pass, Ns = N/R, whose outputs are exactly
 //    j + (N/R) r -- stay in v in natural order.
 // A pass that loads must follow a __syncthreads() after the previous store.
-template <bool LOAD, bool STORE>
+// Barrier of the threads that share one transform: the whole CTA
+// (__syncthreads) or, NAMED, the 256-thread group with barrier id `bar`
+// (k_orbit_fft_dual runs two transforms per CTA).
+template <bool NAMED>
+__device__ __forceinline__ void fft_bar(int bar) {
+    if constexpr (NAMED) asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(kFftThreads) : "memory");
+    else __syncthreads();
+}
+
+template <bool LOAD, bool STORE, bool NAMED = false>
 __device__ __forceinline__ void fft_pass(double2 (&v)[kFftR], double2* __restrict__ buf, int Ns,
-                                         const double2* __restrict__ W) {
-    const int j = threadIdx.x;
+                                         const double2* __restrict__ W, int j = threadIdx.x, int bar = 0) {
     if (LOAD) {
         #pragma unroll
         for (int r = 0; r < kFftR; ++r) v[r] = buf[fpad(j + r * kFftThreads)];
@@ -200,11 +209,11 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[kFftR], double2* __restric
     }
     dftR<kFftR>(v);
     if (STORE) {
-        __syncthreads();   // every thread has read its inputs of this buffer
+        fft_bar<NAMED>(bar);   // every thread has read its inputs of this buffer
         const int idxD = (j / Ns) * Ns * kFftR + k;
         #pragma unroll
         for (int r = 0; r < kFftR; ++r) buf[fpad(idxD + r * Ns)] = v[dft_slot(r)];
-        __syncthreads();
+        fft_bar<NAMED>(bar);
     } else {
         double2 t[kFftR];
         #pragma unroll
@@ -216,13 +225,13 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[kFftR], double2* __restric
 
 // Forward FFT, inputs j + (N/R) r in v (registers).  The last pass leaves its
 // outputs -- the same positions -- in v, or stores them (natural order) to buf.
-template <bool LAST_TO_SMEM>
+template <bool LAST_TO_SMEM, bool NAMED = false>
 __device__ __forceinline__ void fft4096_regs(double2 (&v)[kFftR], double2* __restrict__ buf,
-                                             const double2* __restrict__ W) {
-    fft_pass<false, true>(v, buf, 1, W);
+                                             const double2* __restrict__ W, int j = threadIdx.x, int bar = 0) {
+    fft_pass<false, true, NAMED>(v, buf, 1, W, j, bar);
     #pragma unroll
-    for (int Ns = kFftR; Ns < kFftN / kFftR; Ns *= kFftR) fft_pass<true, true>(v, buf, Ns, W);
-    fft_pass<true, LAST_TO_SMEM>(v, buf, kFftN / kFftR, W);
+    for (int Ns = kFftR; Ns < kFftN / kFftR; Ns *= kFftR) fft_pass<true, true, NAMED>(v, buf, Ns, W, j, bar);
+    fft_pass<true, LAST_TO_SMEM, NAMED>(v, buf, kFftN / kFftR, W, j, bar);
 }
 
 // Forward FFT of the N values in buf (natural order in, natural order out).
