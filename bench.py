@@ -418,6 +418,27 @@ def main():
             mdi[f"cfg{cid}_mean"] = rep.mean
             mdi[f"cfg{cid}_log_mean"] = rep.log_raw - rep.log_total
             mdi[f"cfg{cid}_method"] = rep.method
+        # the level collapse of a non-separable integrand (suite test7's invpow,
+        # d = 10, n = 8^10 + 1): the reference needs minutes (its time from the
+        # build container is frozen in tests/golden/linform.json)
+        g = lq.parse("(1 + sum(i=1..d, x[i]))^(-(d+1))", 10)
+        lq.mdi_lr(g, 10, 8, 8**10 + 1)
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            v, rep = lq.mdi_lr(g, 10, 8, 8**10 + 1, with_report=True)
+            ts.append(time.perf_counter() - t0)
+        mdi["invpow_d10_ms"] = min(ts) * 1e3
+        mdi["invpow_d10_value"] = v
+        mdi["invpow_d10_method"] = rep.method
+        try:
+            with open(os.path.join(REPO, "tests", "golden", "linform.json")) as fh:
+                ref10 = next(c for c in json.load(fh)["cases"] if c["tag"] == "invpow_d10")
+            mdi["invpow_d10_reference_s"] = ref10["ref_seconds"]
+            mdi["invpow_d10_reference_value"] = float.fromhex(ref10["value"])
+            mdi["invpow_d10_reference_note"] = "reference mdi_lr timed in the build container (not this box)"
+        except (OSError, StopIteration, KeyError):
+            pass
         # the small BASELINE plain-sum configs (parity cases; launch/latency bound)
         for cid in (1, 2, 3):
             pc = make_config(cid)
