@@ -309,6 +309,7 @@ __device__ __forceinline__ double pair_expabs_c(double l, const PairFast& q, con
 #ifndef LQ_FFT_CENTRED
 #define LQ_FFT_CENTRED 1
 #endif
+
 #ifndef LQ_FFT_FULLTILE
 #define LQ_FFT_FULLTILE 1
 #endif

@@ -33,7 +33,7 @@ from . import engine
 from ._fp import blocked_const_sum, repeated_add
 from .expr import as_expr, evaluate, free_vars, var_bounds
 from .lattice import korobov_vector
-from .transform import midpoint_grids
+from .transform import AxisGridSet, midpoint_grids
 
 __all__ = ["MdiConfig", "MdiReport", "GridCapError", "BudgetExceededError", "mdi_sum", "mdi_lr",
            "direct_tensor_sum", "DIRECT_CAP", "DEFAULT_NODE_BUDGET"]
@@ -75,7 +75,7 @@ class MdiConfig:
 class MdiReport:
     """Observability record (mdi.py:79-101) plus GPU-side extras:
     log_raw (natural log of |value|, finite even when value under/overflows),
-    sign, method ('separable' | 'linform' | 'direct' | 'constant' |
+    sign, method ('separable' | 'linform' | 'subgrid' | 'direct' | 'constant' |
     'characteristic'), clusters (factor count, or support size for linform)."""
 
     value: float
@@ -203,6 +203,9 @@ def mdi_sum(g, grids, cfg=None, comm=None):
         if rep is not None:
             return rep
     if not usable:
+        rep = _subgrid(e, grids, counts, levels, base_axes, cfg, t0, comm)
+        if rep is not None:
+            return rep
         if cfg.fallback == "error":
             raise BudgetExceededError("integrand is not separable over the grid axes "
                                       f"(budget {cfg.budget}); no level reduction possible")
@@ -220,6 +223,41 @@ def mdi_sum(g, grids, cfg=None, comm=None):
                      level_nodes=(plan.n_factors,) * levels, level_seconds=(0.0,) * levels,
                      base_seconds=secs, fallback=False, log_raw=log_raw, sign=sign,
                      method="separable", clusters=plan.n_factors)
+
+
+def _subgrid(e, grids, counts, levels, base_axes, cfg, t0, comm=None):
+    """A non-separable integrand that leaves some axes unused: every level
+    that strips an unused axis only multiplies the carried expression by N
+    (make_sum of N equal terms, exprcore.py:139-169), so the grid sum is
+    prod_{j unused} N_j times the direct sweep over the used axes alone --
+    the sweep the reference's base case performs when the used axes are its
+    base axes.  None when every axis is used or that sweep exceeds the cap."""
+    used = free_vars(e)
+    d = len(counts)
+    if len(used) >= d:
+        return None
+    sub_counts = tuple(c if j + 1 in used else 1 for j, c in enumerate(counts))
+    sub_total = math.prod(sub_counts)
+    if sub_total > cfg.direct_cap:
+        return None
+    if getattr(grids, "midpoint", False):
+        sub = AxisGridSet(None, sub_counts, grids.n, grids.z, midpoint=True)
+    else:
+        sub = AxisGridSet(tuple(nd if j + 1 in used else nd[:1] for j, nd in enumerate(grids.nodes)),
+                          sub_counts, grids.n, grids.z)
+    part = direct_tensor_sum(e, sub, cap=cfg.direct_cap, comm=comm)
+    rest = math.prod(c for j, c in enumerate(counts) if j + 1 not in used)
+    if part == 0.0 or not math.isfinite(part):
+        raw, log_raw, sign = part * rest, (math.log(abs(part)) if part else -math.inf), \
+            (math.copysign(1.0, part) if part else 0.0)
+    else:
+        sign = math.copysign(1.0, part)
+        log_raw = math.log(abs(part)) + math.log(rest)
+        raw = part * float(rest) if rest.bit_length() <= 1000 else (
+            sign * math.exp(log_raw) if log_raw < 709.7 else sign * math.inf)
+    return MdiReport(value=raw, levels=levels, base_dim=len(base_axes), level_nodes=(sub_total,) * levels,
+                     level_seconds=(0.0,) * levels, base_seconds=time.perf_counter() - t0, fallback=False,
+                     log_raw=log_raw, sign=sign, method="subgrid", clusters=sub_total)
 
 
 def _linform(e, counts, levels, base_axes, cfg, t0, comm=None):

@@ -460,6 +460,24 @@ def suite7_cases():
     return out
 
 
+def subgrid_cases():
+    """MDI-LR of non-separable integrands that leave axes unused: the
+    reference's levels strip the unused axes (each multiplies the carried
+    expression by N) and sweep the rest (mdi.py:152-183)."""
+    out = []
+    for tag, text, d, a, n in (("expxy_d10", "exp(x[1]*x[2])", 10, 8, 8**10 + 1),
+                               ("corpus_expxy_d6", corpus.get("expxy").text, 6, 5, 5**6),
+                               ("recip3_d8", "1/(1 + x[1]*x[2] + x[3])", 8, 6, 6**8 + 7),
+                               ("exp_x1x9_d10", "exp(x[1]*x[9])", 10, 4, 4**10)):
+        f = exprcore.parse(text, d)
+        t0 = time.perf_counter()
+        value, rep = mdi_lr(f, d, a, n, with_report=True)
+        out.append({"tag": tag, "text": text, "d": d, "a": a, "n": str(n), "value": hx(value),
+                    "raw": hx(rep.value), "levels": rep.levels, "base_dim": rep.base_dim,
+                    "fallback": rep.fallback, "ref_seconds": time.perf_counter() - t0})
+    return out
+
+
 def _cfg5_chunk(args):
     """Worker: the reference's own points_block (lattice.py:96-105) over
     [lo, hi) in blocks of 2^15 rows, integrand exp(-|x @ c - c.w|) in numpy
@@ -506,7 +524,7 @@ def cfg5_full_case(procs):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
-    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites", "cfg5_full", "linform", "fft", "parser", "suites7"],
+    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites", "cfg5_full", "linform", "fft", "parser", "suites7", "subgrid"],
                     default=None)
     ap.add_argument("--procs", type=int, default=os.cpu_count())
     args = ap.parse_args()
@@ -516,7 +534,7 @@ def main():
             "mdi": lambda: mdi_cases(args.skip_slow), "quality": quality_cases, "mc": mc_cases,
             "suites": suite_cases, "cfg5_full": lambda: cfg5_full_case(args.procs),
             "linform": lambda: linform_cases(args.skip_slow), "fft": lambda: fft_cases_job(args.procs),
-            "parser": parser_cases, "suites7": suite7_cases}
+            "parser": parser_cases, "suites7": suite7_cases, "subgrid": subgrid_cases}
     for name, fn in jobs.items():
         if args.only != name and (args.only or name in ("cfg5_full", "linform", "fft", "suites7")):
             continue

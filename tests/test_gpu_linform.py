@@ -144,3 +144,20 @@ def test_sharded_tiles_sum_to_the_single_gpu_mean(nshards):
     out = C.c_double()
     N.check(N.lib().lq_reduce_sum(N.ctx(), C.c_void_p(acc.data_ptr()), plan.tiles, C.byref(out)))
     assert out.value == single
+
+
+SUBGRID = load_golden("subgrid")
+
+
+@pytest.mark.parametrize("case", SUBGRID, ids=lambda c: c["tag"])
+def test_unused_axes_reduce_to_a_subgrid_sweep(case):
+    """Non-separable integrands that leave axes unused (exp(x1 x2) at d = 10):
+    the reference strips the unused axes level by level and sweeps the rest;
+    here the used axes are swept alone and the unused ones multiply in."""
+    import paper_2404_08867_b200 as lq
+    f = lq.parse(case["text"], case["d"])
+    value, rep = lq.mdi_lr(f, case["d"], case["a"], int(case["n"]), with_report=True)
+    want = unhex(case["value"])
+    assert rep.method == "subgrid", rep.method
+    assert abs(value - want) <= 1e-10 * abs(want), (value, want)
+    assert (rep.levels, rep.base_dim, rep.fallback) == (case["levels"], case["base_dim"], case["fallback"])
