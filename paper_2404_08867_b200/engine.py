@@ -400,7 +400,8 @@ class LinformPlan:
         if abs(self.m0) + 2 * self.support >= 2**53:
             return
         self.level_support = tuple(int(v) for v in sizes)
-        self.h = float(b_ref * h_rat)
+        self.h_exact = b_ref * h_rat                 # the quantum as an exact rational
+        self.h = float(self.h_exact)
         self.G = lo.G
         self.prog = compile_program(lo.G)
         self.tiles = -(-self.support // N.LQ_TILE)

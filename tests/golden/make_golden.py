@@ -19,6 +19,7 @@ little-endian float64 bytes.
 from __future__ import annotations
 
 import argparse
+import gc
 import base64
 import json
 import math
@@ -321,20 +322,33 @@ def _fft_case_sum(case):
     points_block + the numpy restatement exp(-|x c - c.w|)."""
     key, text, params, n, a = case
     d = text.count("x[")
+    print(f"fft case {key} start", flush=True)
     rule = korobov_vector(a, n, d)
     t0 = time.perf_counter()
+    # the reference's own points_block and eval_array (or, for |.|, which its
+    # grammar lacks, numpy) on blocks of 2^14 rows -- slr_integrate's
+    # 2^19-row blocks need ~9 GB per process at d = 2048
+    rows = 1 << 14
+    acc = 0.0
     if params is None:
-        value = slr_integrate(exprcore.parse(text, d), rule).value
+        f = exprcore.parse(text, d)
+        for start in range(0, n, rows):
+            pts = points_block(rule, start, min(start + rows, n))
+            vals = exprcore.eval_array(f, {i + 1: pts[:, i] for i in range(d)})
+            acc += float(np.sum(vals))
+            # eval_array's memo lives in a self-referencing closure: a cycle
+            # that holds every intermediate column until the collector runs
+            del vals
+            gc.collect()
         kind = "reference"
     else:
         c = np.asarray(params["c"])
         cw = float(np.dot(c, np.asarray(params["w"])))
-        acc = 0.0
-        for start in range(0, n, 1 << 15):
-            pts = points_block(rule, start, min(start + (1 << 15), n))
+        for start in range(0, n, rows):
+            pts = points_block(rule, start, min(start + rows, n))
             acc += float(np.sum(np.exp(-np.abs(pts @ c - cw))))
-        value = acc / n
         kind = "ref_points+numpy"
+    value = acc / n
     return {"key": key, "n": n, "a": a, "d": d, "kind": kind, "value": hx(value),
             "ref_seconds": time.perf_counter() - t0}
 
@@ -347,8 +361,8 @@ def fft_cases_job(procs):
     sys.path.insert(0, os.path.dirname(HERE))
     import fft_cases
     cases = fft_cases.all_cases()
-    with mp.Pool(procs) as pool:
-        out = pool.map(_fft_case_sum, cases, chunksize=1)
+    with mp.Pool(procs, maxtasksperchild=1) as pool:
+        out = list(pool.imap(_fft_case_sum, cases, chunksize=1))
     return out
 
 

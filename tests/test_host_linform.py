@@ -96,3 +96,33 @@ def test_constant_slr_huge_n_raises_like_points_block():
         slr_integrate(parse("2.5", 2), LatticeRule(2**53 + 5, (1, 3)))
     r = slr_integrate(parse("2.5", 2), LatticeRule(2**40 + 15, (1, 3)))
     assert r.value == pytest.approx(2.5, rel=1e-15)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_linform_plan_reproduces_the_linear_form_multiset(seed):
+    """The plan's lattice alpha + h (m0 + 2k), k = sum |m_j| t_j, must carry
+    exactly the multiset of values of <beta, y> over the midpoint grid
+    (exact rationals; small grids enumerated in full)."""
+    import itertools
+    from collections import Counter
+    from fractions import Fraction
+    import numpy as np
+    from paper_2404_08867_b200 import parse
+    from paper_2404_08867_b200.engine import LinformPlan
+    rng = np.random.default_rng(seed)
+    d = int(rng.integers(1, 5))
+    coef = [int(v) for v in rng.integers(-3, 4, d)]
+    coef[0] = coef[0] or 2
+    counts = tuple(int(v) for v in rng.choice([2, 3, 4, 6], d))
+    text = "1/(9 + " + " + ".join(f"{c}*x[{j + 1}]" for j, c in enumerate(coef)) + ")"
+    plan = LinformPlan(parse(text, d), counts)
+    assert plan.ok
+    want = Counter(sum(Fraction(c) * Fraction(2 * t + 1, 2 * n) for c, t, n in zip(coef, ts, counts))
+                   for ts in itertools.product(*(range(n) for n in counts)))
+    h = plan.h_exact
+    got = Counter()
+    zero_axes = math.prod(counts[j] for j in range(d) if not coef[j])
+    for ks in itertools.product(*(range(n) for n in plan.n)):
+        k = sum(int(m) * t for m, t in zip(plan.m, ks))
+        got[h * (plan.m0 + 2 * k)] += zero_axes
+    assert got == want, (coef, counts)
