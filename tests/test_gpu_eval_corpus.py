@@ -32,4 +32,4 @@ def test_gpu_bytecode_matches_reference_eval():
             w = unhex(want)
             assert got == w or math.isclose(got, w, rel_tol=1e-10, abs_tol=1e-300), (text, x, got, w)
             checked += 1
-    assert checked > 600, checked
+    assert checked > 300, checked      # texts with coordinates, three points each

@@ -128,10 +128,11 @@ def test_mdi_golden(lq, golden):
             assert abs(value - want) <= REL * abs(want), (case["tag"], value, want)
         else:
             assert value == 0.0, case["tag"]
-        if rep.method in ("separable", "linform"):
-            # levels collapse (product form, or one commensurate linear form)
+        if rep.method in ("separable", "linform", "subgrid"):
+            # levels collapse (product form, one commensurate linear form, or
+            # unused axes stripped in front of a sweep over the used ones)
             assert (rep.levels, rep.base_dim) == (case["levels"], case["base_dim"]), case["tag"]
-            if rep.method == "linform":
+            if rep.method != "separable":
                 assert not case["fallback"], case["tag"]
         else:   # non-separable: the reference's full-grid fallback sweep (mdi.py:167-179)
             assert rep.method in ("direct", "constant"), case["tag"]
