@@ -161,3 +161,18 @@ def test_unused_axes_reduce_to_a_subgrid_sweep(case):
     assert rep.method == "subgrid", rep.method
     assert abs(value - want) <= 1e-10 * abs(want), (value, want)
     assert (rep.levels, rep.base_dim, rep.fallback) == (case["levels"], case["base_dim"], case["fallback"])
+
+
+@pytest.mark.parametrize("N", [12799, 12800, 12801])
+def test_shared_memory_capacity_boundary(N):
+    """Support K = N on one axis: 12 800 points is the last size the one-CTA
+    shared-memory kernel takes; 12 801 runs the global-memory levels.  Both
+    equal the direct sweep of the same grid."""
+    import paper_2404_08867_b200 as lq
+    from paper_2404_08867_b200 import engine
+    f = lq.parse("1/(2 + x[1])^3", 1)
+    assert engine.linform_plan(f, (N,)).support == N
+    rep = lq.mdi_sum(f, _grid((N,)))
+    assert rep.method == "linform"
+    direct = lq.direct_tensor_sum(f, _grid((N,)))
+    assert abs(rep.value - direct) <= 1e-13 * abs(direct), (rep.value, direct)
