@@ -160,11 +160,23 @@ class _Ctx:
             pass
 
 
+def _default_device():
+    """LQ_DEVICE if set; else torch's current device when the caller has
+    initialised CUDA through torch (torchrun scripts set it per rank); else
+    LOCAL_RANK, else 0."""
+    if "LQ_DEVICE" in os.environ:
+        return int(os.environ["LQ_DEVICE"])
+    import sys
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_initialized():
+        return torch.cuda.current_device()
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
 def ctx(device=None):
-    """The process's liblq context for ``device`` (default: current CUDA device
-    per LOCAL_RANK, else 0)."""
+    """The process's liblq context for ``device`` (default: _default_device)."""
     if device is None:
-        device = int(os.environ.get("LQ_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+        device = _default_device()
     key = (device, threading.get_ident())
     c = _ctxs.get(key)
     if c is None:
