@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define LQ_ABI_VERSION 5
+#define LQ_ABI_VERSION 6
 
 #define LQ_OK 0
 #define LQ_ERR_VALUE (-1)
@@ -189,8 +189,12 @@ typedef struct {
     int32_t n_slots;
     int32_t node_off;       /* < 0: midpoint nodes RN((t+0.5)/count); else
                                nodes[node_off + t] of the nodes table      */
-    int32_t reserved;
+    int32_t reserved;       /* 0, or LQ_FACTOR_SUPPLIED: a core factor of
+                               several axes whose cluster sum the caller
+                               supplies as (re, im) = nodes[node_off], nodes[node_off+1]
+                               (count must be 1)                           */
 } lq_factor;
+#define LQ_FACTOR_SUPPLIED 1
 
 /* Partial cluster sums of LQ_NODE_BLOCK-node blocks: part_dev[(f*nblk + b)*2 + {0,1}]
  * (re, im) for node blocks b of every factor with b*nshards/... owned by

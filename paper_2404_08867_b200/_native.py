@@ -23,8 +23,9 @@ LIB_PATH = os.environ.get("LQ_LIB_PATH") or os.path.join(os.path.dirname(os.path
 LQ_OK, LQ_ERR_VALUE, LQ_ERR_OVERFLOW, LQ_ERR_GRIDCAP = 0, -1, -2, -3
 LQ_ERR_CUDA, LQ_ERR_UNSUPPORTED, LQ_ERR_NOMEM = -4, -5, -6
 LQ_TILE, LQ_SUPER_TILES, LQ_NODE_BLOCK = 4096, 1024, 256
+LQ_FACTOR_SUPPLIED = 1
 
-ABI_VERSION = 5   # LQ_ABI_VERSION of include/lq.h these ctypes structs match
+ABI_VERSION = 6   # LQ_ABI_VERSION of include/lq.h these ctypes structs match
 FAM = {"program": 0, "lin_exp": 1, "lin_sincos": 2, "lin_expabs": 3, "quad_exp": 4, "lin_pow": 5, "quad_sincos": 6, "prod_quad": 7}
 
 

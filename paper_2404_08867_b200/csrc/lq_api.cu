@@ -1841,9 +1841,13 @@ int lq_mdi_block_sums(lq_ctx* c, const lq_insn* insn, int32_t n_insn, const lq_f
     if ((rc = mdi_validate(insn, n_insn, fac, nf, &nblk, &ns))) return rc;
     if (nshards < 1 || shard < 0 || shard >= nshards) return fail(LQ_ERR_VALUE, "bad shard %d of %d", shard, nshards);
     if (nf == 0) return LQ_OK;
-    for (int f = 0; f < nf; ++f)
-        if (fac[f].node_off >= 0 && (!nodes || (int64_t)fac[f].node_off + fac[f].count > n_nodes))
+    for (int f = 0; f < nf; ++f) {
+        const int64_t need = fac[f].reserved == LQ_FACTOR_SUPPLIED ? 2 : fac[f].count;
+        if (fac[f].reserved == LQ_FACTOR_SUPPLIED && (fac[f].count != 1 || fac[f].node_off < 0))
+            return fail(LQ_ERR_VALUE, "supplied factor %d needs count 1 and a node offset", f);
+        if (fac[f].node_off >= 0 && (!nodes || (int64_t)fac[f].node_off + need > n_nodes))
             return fail(LQ_ERR_VALUE, "factor %d node table out of range", f);
+    }
     void *dp, *dfac, *dn = nullptr;
     if ((rc = upload(c, B_PROG, insn, sizeof(lq_insn) * std::max(n_insn, 1), &dp))) return rc;
     if ((rc = upload(c, B_AUX0, fac, sizeof(lq_factor) * nf, &dfac))) return rc;

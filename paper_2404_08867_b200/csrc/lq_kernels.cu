@@ -1390,6 +1390,15 @@ __global__ void __launch_bounds__(kThreads) k_mdi_blocks(const lq_insn* __restri
     const int NB = (F.count + LQ_NODE_BLOCK - 1) / LQ_NODE_BLOCK;
     const int b_lo = (int)(((int64_t)shard * NB) / nshards), b_hi = (int)(((int64_t)(shard + 1) * NB) / nshards);
     if (b < b_lo || b >= b_hi) return;
+    if (F.reserved == LQ_FACTOR_SUPPLIED) {
+        // a core factor whose sum over its own sub-grid the host supplies
+        // as (re, im) at nodes[node_off] (one block)
+        if (threadIdx.x == 0) {
+            part[((int64_t)f * nblk + b) * 2 + 0] = nodes[F.node_off];
+            part[((int64_t)f * nblk + b) * 2 + 1] = nodes[F.node_off + 1];
+        }
+        return;
+    }
     const int t = b * LQ_NODE_BLOCK + threadIdx.x;
     double re = 0.0, im = 0.0;
     if (t < F.count) {

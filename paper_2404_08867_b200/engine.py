@@ -170,11 +170,21 @@ def tensor_sum(g, grids, s_begin=0, s_end=None, comm=None):
 
 # ------------------------------------------------------------------ MDI-LR
 
+CORE_MAX_AXES = 3            # coordinates a core factor may span (lower.separate)
+CORE_MAX_NODES = 10**8       # sub-grid nodes a core factor may sweep (the reference's DIRECT_CAP)
+
+
 class SeparablePlan:
-    """Factor table + term structure of a separable integrand on given axis counts."""
+    """Factor table + term structure of a (partially) separable integrand on
+    given axis counts.  Univariate factors become per-direction cluster sums
+    on the device (k_mdi_blocks); a core factor on 2-3 axes (a piece that does
+    not split, e.g. exp(x1 x2)) is swept over its own sub-grid by the direct
+    tensor kernel and enters the combine as a supplied cluster sum
+    (LQ_FACTOR_SUPPLIED) -- what the reference's levels do when they strip
+    the other axes and sweep the rest (mdi.py:152-183)."""
 
     def __init__(self, e, counts, nodes=None):
-        terms = separate(e)
+        terms = separate(e, max_axes=CORE_MAX_AXES)
         self.ok = terms is not None
         if not self.ok:
             return
@@ -184,40 +194,53 @@ class SeparablePlan:
         off = 0
         max_slots = 1
         fac_index = {}
+        node_vals = []
         if nodes is not None:
             node_offs = np.concatenate([[0], np.cumsum([len(nd) for nd in nodes])]).astype(np.int64)
             if node_offs[-1] >= 2**31:
                 raise ValueError("node table too large")
-            self.nodes = np.ascontiguousarray(np.concatenate([np.asarray(nd, dtype=np.float64) for nd in nodes]))
+            node_vals = [np.asarray(nd, dtype=np.float64) for nd in nodes]
         else:
             node_offs = None
-            self.nodes = None
+        n_node_vals = int(node_offs[-1]) if node_offs is not None else 0
+        self.cores = []        # (slot in the nodes table, Factor, sub-grid counts)
         for t in terms:
-            extra = 0.0
-            for ax in range(1, d + 1):
-                if ax not in t.factors:
-                    extra += math.log(counts[ax - 1])
-            for ax in sorted(t.factors):
-                fc = t.factors[ax]
-                key = (ax, fc.R, fc.P)
+            covered = {ax for key in t.factors for ax in key}
+            extra = sum(math.log(counts[ax - 1]) for ax in range(1, d + 1) if ax not in covered)
+            for axes in sorted(t.factors):
+                fc = t.factors[axes]
+                key = (axes, fc.R, fc.P)
                 idx = fac_index.get(key)
                 if idx is None:
                     rec = N.Factor()
-                    rec.count = int(counts[ax - 1])
-                    rec.node_off = -1 if node_offs is None else int(node_offs[ax - 1])
-                    for which, sub in (("r", fc.R), ("p", fc.P)):
-                        if sub is None:
-                            setattr(rec, f"{which}_off", 0)
-                            setattr(rec, f"{which}_len", 0)
-                            setattr(rec, f"{which}_result", 0)
-                            continue
-                        prog = compile_program(sub, var_map=lambda j: 0)
-                        insn_parts.append(prog.insn)
-                        setattr(rec, f"{which}_off", off)
-                        setattr(rec, f"{which}_len", len(prog.insn))
-                        setattr(rec, f"{which}_result", prog.result)
-                        off += len(prog.insn)
-                        max_slots = max(max_slots, prog.n_slots)
+                    if len(axes) > 1:
+                        sub = tuple(int(counts[j]) if j + 1 in axes else 1 for j in range(d))
+                        if math.prod(sub) > CORE_MAX_NODES:
+                            self.ok = False
+                            return
+                        rec.count = 1
+                        rec.reserved = N.LQ_FACTOR_SUPPLIED
+                        rec.node_off = n_node_vals
+                        self.cores.append((n_node_vals, fc, sub))
+                        n_node_vals += 2
+                        rec.r_off = rec.r_len = rec.r_result = rec.p_off = rec.p_len = rec.p_result = 0
+                    else:
+                        ax = axes[0]
+                        rec.count = int(counts[ax - 1])
+                        rec.node_off = -1 if node_offs is None else int(node_offs[ax - 1])
+                        for which, sub in (("r", fc.R), ("p", fc.P)):
+                            if sub is None:
+                                setattr(rec, f"{which}_off", 0)
+                                setattr(rec, f"{which}_len", 0)
+                                setattr(rec, f"{which}_result", 0)
+                                continue
+                            prog = compile_program(sub, var_map=lambda j: 0)
+                            insn_parts.append(prog.insn)
+                            setattr(rec, f"{which}_off", off)
+                            setattr(rec, f"{which}_len", len(prog.insn))
+                            setattr(rec, f"{which}_result", prog.result)
+                            off += len(prog.insn)
+                            max_slots = max(max_slots, prog.n_slots)
                     idx = len(factors)
                     fac_index[key] = idx
                     factors.append(rec)
@@ -229,6 +252,13 @@ class SeparablePlan:
         for rec in factors:
             rec.n_slots = max_slots
         from .lower import INSN_DTYPE
+        if node_vals or self.cores:
+            node_vals.append(np.zeros(n_node_vals - (int(node_offs[-1]) if node_offs is not None else 0)))
+            self.nodes = np.ascontiguousarray(np.concatenate(node_vals))
+        else:
+            self.nodes = None
+        self.grid_nodes = nodes
+        self.core_sums_done = False
         self.insn = (np.ascontiguousarray(np.concatenate(insn_parts)) if insn_parts
                      else np.zeros(1, dtype=INSN_DTYPE))
         self.n_insn = int(off)
@@ -240,6 +270,29 @@ class SeparablePlan:
         self.coef_im = np.asarray(coef_im, dtype=np.float64)
         self.log_extra = np.asarray(log_extra, dtype=np.float64)
         self.n_terms = len(terms)
+
+    def core_sums(self, comm=None):
+        """Sweep every core factor over its own sub-grid (direct tensor kernel,
+        sharded across ranks with ``comm``) into the supplied-sum slots."""
+        if self.core_sums_done or not self.cores:
+            return
+        from .expr import func as _func, mul as _mul
+        from .transform import AxisGridSet
+        for slot, fc, sub in self.cores:
+            if self.grid_nodes is None:
+                grid = AxisGridSet(None, sub, None, None, midpoint=True)
+            else:
+                grid = AxisGridSet(tuple(nd if c > 1 else nd[:1] for nd, c in zip(self.grid_nodes, sub)),
+                                   sub, None, None)
+            R = fc.R if fc.R is not None else None
+            if fc.P is None:
+                re, im = tensor_sum(R, grid, comm=comm), 0.0
+            else:
+                cos_p, sin_p = _func("cos", fc.P), _func("sin", fc.P)
+                re = tensor_sum(cos_p if R is None else _mul(1.0, [R, cos_p]), grid, comm=comm)
+                im = tensor_sum(sin_p if R is None else _mul(1.0, [R, sin_p]), grid, comm=comm)
+            self.nodes[slot], self.nodes[slot + 1] = re, im
+        self.core_sums_done = True
 
 
 def separable_plan(g, counts, nodes=None):
@@ -255,6 +308,7 @@ def mdi_separable_sum(plan, comm=None):
     sharded across ranks ("cluster range of the current coordinate", SURVEY
     §8e), exchanged once, and combined on every rank."""
     out = np.zeros(4)
+    plan.core_sums(comm)
     n_nodes = 0 if plan.nodes is None else len(plan.nodes)
     if comm is not None and comm.size > 1:
         nblk = max((int(plan.factors[k].count) + N.LQ_NODE_BLOCK - 1) // N.LQ_NODE_BLOCK

@@ -467,18 +467,25 @@ def compile_program(e, var_map=None):
 
 @dataclass(frozen=True)
 class Factor:
-    """Univariate factor U(y) = R(y) * exp(i P(y)) on one axis (1-based).
-    R or P may be None (meaning 1 and 0)."""
+    """Factor U(y) = R(y) * exp(i P(y)) of the coordinates ``axes`` (sorted,
+    1-based): one axis for the per-direction cluster sums; two or three for a
+    "core" -- a piece that does not split further, whose sum over its own
+    sub-grid is taken directly (``separate(..., max_axes > 1)``).  R or P may
+    be None (meaning 1 and 0)."""
 
-    axis: int
+    axes: tuple
     R: Expr = None
     P: Expr = None
+
+    @property
+    def axis(self):
+        return self.axes[0]
 
 
 @dataclass
 class SepTerm:
     coef: complex
-    factors: dict = field(default_factory=dict)   # axis -> Factor
+    factors: dict = field(default_factory=dict)   # axes tuple -> Factor, pairwise disjoint
 
 
 _TERM_CAP = 1024
@@ -489,41 +496,68 @@ def _univ(e):
     return next(iter(fv)) if len(fv) == 1 else (0 if not fv else None)
 
 
-def _fmul(f1, f2):
+def _fmul(f1, f2, axes):
     R = f1.R if f2.R is None else (f2.R if f1.R is None else mul(1.0, [f1.R, f2.R]))
     P = f1.P if f2.P is None else (f2.P if f1.P is None else add([(1.0, f1.P), (1.0, f2.P)]))
-    return Factor(f1.axis, R, P)
+    return Factor(axes, R, P)
 
 
-def _tmul(t1, t2):
+def _tmul(t1, t2, max_axes=1):
+    """Product of two terms: factors on overlapping axes merge into one factor
+    on the union; None when a union exceeds ``max_axes`` coordinates."""
     fac = dict(t1.factors)
-    for ax, f in t2.factors.items():
-        fac[ax] = _fmul(fac[ax], f) if ax in fac else f
+    for key, f in t2.factors.items():
+        axes = set(key)
+        merged = f
+        while True:
+            hit = next((k for k in fac if axes & set(k)), None)
+            if hit is None:
+                break
+            axes |= set(hit)
+            merged = _fmul(fac.pop(hit), merged, ())
+        if len(axes) > max_axes:
+            return None
+        key = tuple(sorted(axes))
+        fac[key] = Factor(key, merged.R, merged.P)
     return SepTerm(t1.coef * t2.coef, fac)
 
 
-def _additive_split(arg):
-    """arg = c + sum_j g_j(x_j) -> (c, {axis: g_j}) or None."""
+def _additive_split(arg, max_axes=1):
+    """arg = c + sum_G g_G(x_G) over disjoint coordinate groups of at most
+    ``max_axes`` axes -> (c, {axes: g_G}); None otherwise."""
     if arg.op == "add":
         pieces = [(c, t) for c, t in arg.terms]
         c0 = arg.val
     else:
         pieces, c0 = [(1.0, arg)], 0.0
-    groups = {}
+    groups = {}      # axes tuple -> [(coef, term)]
     for c, t in pieces:
-        ax = _univ(t)
-        if ax is None:
-            return None
-        if ax == 0:
+        fv = free_vars(t)
+        if not fv:
             from .expr import evaluate
             c0 += c * evaluate(t, {})
             continue
-        groups.setdefault(ax, []).append((c, t))
-    return c0, {ax: add(ps) for ax, ps in groups.items()}
+        axes = set(fv)
+        members = [(c, t)]
+        while True:
+            hit = next((k for k in groups if axes & set(k)), None)
+            if hit is None:
+                break
+            axes |= set(hit)
+            members = groups.pop(hit) + members
+        if len(axes) > max_axes:
+            return None
+        groups[tuple(sorted(axes))] = members
+    return c0, {key: add(ps) for key, ps in groups.items()}
 
 
-def separate(e, cap=_TERM_CAP):
-    """Factorise e into SepTerms, or None when e is not (finitely) separable."""
+def separate(e, cap=_TERM_CAP, max_axes=1):
+    """Factorise e into SepTerms, or None when e is not (finitely) separable.
+
+    max_axes = 1: every factor is univariate (the per-direction cluster sums
+    of the reference's level collapse).  max_axes > 1: a piece that does not
+    split further but depends on at most ``max_axes`` coordinates becomes one
+    core factor on them (e.g. exp(x1 x2) in exp(x1 x2) prod_j g(x_j))."""
     memo = {}
 
     def rec(node):
@@ -531,6 +565,11 @@ def separate(e, cap=_TERM_CAP):
         if hit is not None or node in memo:
             return hit
         out = _rec(node)
+        if out is None and max_axes > 1:
+            fv = free_vars(node)
+            if 2 <= len(fv) <= max_axes:
+                key = tuple(sorted(fv))
+                out = [SepTerm(1.0, {key: Factor(key, R=node)})]
         if out is not None and len(out) > cap:
             out = None
         memo[node] = out
@@ -542,7 +581,7 @@ def separate(e, cap=_TERM_CAP):
             from .expr import evaluate
             return [SepTerm(complex(evaluate(node, {})), {})]
         if ax is not None:
-            return [SepTerm(1.0, {ax: Factor(ax, R=node)})]
+            return [SepTerm(1.0, {(ax,): Factor((ax,), R=node)})]
         op = node.op
         if op == "add":
             terms = [SepTerm(complex(node.val), {})] if node.val != 0.0 else []
@@ -558,8 +597,8 @@ def separate(e, cap=_TERM_CAP):
                 sub = rec(f)
                 if sub is None:
                     return None
-                acc = [_tmul(a, b) for a in acc for b in sub]
-                if len(acc) > cap:
+                acc = [_tmul(a, b, max_axes) for a in acc for b in sub]
+                if any(t is None for t in acc) or len(acc) > cap:
                     return None
             return acc
         if op == "pow":
@@ -570,8 +609,8 @@ def separate(e, cap=_TERM_CAP):
             if k >= 2:
                 acc = [SepTerm(1.0, {})]
                 for _ in range(k):
-                    acc = [_tmul(a, b) for a in acc for b in sub]
-                    if len(acc) > cap:
+                    acc = [_tmul(a, b, max_axes) for a in acc for b in sub]
+                    if any(t is None for t in acc) or len(acc) > cap:
                         return None
                 return acc
             if len(sub) != 1:
@@ -580,21 +619,21 @@ def separate(e, cap=_TERM_CAP):
             if t.coef == 0:
                 return None
             fac = {}
-            for ax2, f in t.factors.items():
+            for key, f in t.factors.items():
                 R = power(f.R, k) if f.R is not None else None
                 P = mul(float(k), [f.P]) if f.P is not None else None
-                fac[ax2] = Factor(ax2, R, P)
+                fac[key] = Factor(key, R, P)
             return [SepTerm(t.coef ** k, fac)]
         if op in ("exp", "sin", "cos"):
-            sp = _additive_split(node.args[0])
+            sp = _additive_split(node.args[0], max_axes)
             if sp is None or not math.isfinite(sp[0]):
                 return None
             c0, groups = sp
             if op == "exp":
                 return [SepTerm(complex(math.exp(c0)),
-                                {ax2: Factor(ax2, R=func("exp", g)) for ax2, g in groups.items()})]
-            pos = {ax2: Factor(ax2, P=g) for ax2, g in groups.items()}
-            neg = {ax2: Factor(ax2, P=mul(-1.0, [g])) for ax2, g in groups.items()}
+                                {key: Factor(key, R=func("exp", g)) for key, g in groups.items()})]
+            pos = {key: Factor(key, P=g) for key, g in groups.items()}
+            neg = {key: Factor(key, P=mul(-1.0, [g])) for key, g in groups.items()}
             ep, en = cmath.exp(1j * c0), cmath.exp(-1j * c0)
             if op == "cos":   # (e^{i a} + e^{-i a}) / 2
                 return [SepTerm(0.5 * ep, pos), SepTerm(0.5 * en, neg)]

@@ -75,8 +75,8 @@ class MdiConfig:
 class MdiReport:
     """Observability record (mdi.py:79-101) plus GPU-side extras:
     log_raw (natural log of |value|, finite even when value under/overflows),
-    sign, method ('separable' | 'linform' | 'subgrid' | 'direct' | 'constant' |
-    'characteristic'), clusters (factor count, or support size for linform)."""
+    sign, method ('separable' | 'cores' | 'linform' | 'subgrid' | 'direct' |
+    'constant' | 'characteristic'), clusters (factor count, or support size for linform)."""
 
     value: float
     levels: int
@@ -189,8 +189,9 @@ def mdi_sum(g, grids, cfg=None, comm=None):
     midpoint = getattr(grids, "midpoint", False)
     plan = engine.separable_plan(e, counts, None if midpoint else grids.nodes)
     usable = plan.ok and (plan.n_factors + plan.n_terms) <= cfg.budget
+    pure = usable and not plan.cores
     total = _total(counts)
-    if not usable and midpoint:
+    if not pure and midpoint:
         # non-separable integrands whose levels still collapse: exp-abs of a
         # linear form past the direct cap by its characteristic function (an
         # extension, the reference has no |.|), functions of one commensurate
@@ -219,10 +220,12 @@ def mdi_sum(g, grids, cfg=None, comm=None):
         raise GridCapError(f"direct sweep needs {base_total} evaluations, cap is {cfg.direct_cap}")
     log_raw, sign, raw, _ = engine.mdi_separable_sum(plan, comm)
     secs = time.perf_counter() - t0
+    # "cores": product terms with a non-splitting piece on <= 3 axes, swept
+    # over its own sub-grid (the reference strips the other axes level by level)
     return MdiReport(value=raw, levels=levels, base_dim=len(base_axes),
                      level_nodes=(plan.n_factors,) * levels, level_seconds=(0.0,) * levels,
                      base_seconds=secs, fallback=False, log_raw=log_raw, sign=sign,
-                     method="separable", clusters=plan.n_factors)
+                     method="separable" if pure else "cores", clusters=plan.n_factors)
 
 
 def _subgrid(e, grids, counts, levels, base_axes, cfg, t0, comm=None):

@@ -475,14 +475,20 @@ def suite7_cases():
 
 
 def subgrid_cases():
-    """MDI-LR of non-separable integrands that leave axes unused: the
-    reference's levels strip the unused axes (each multiplies the carried
-    expression by N) and sweep the rest (mdi.py:152-183)."""
+    """MDI-LR of integrands that are not separable axis by axis: pieces on a
+    few axes (cores) times separable factors, and integrands that leave axes
+    unused.  The reference's levels strip the separable and unused axes and
+    sweep the rest (mdi.py:152-183)."""
     out = []
     for tag, text, d, a, n in (("expxy_d10", "exp(x[1]*x[2])", 10, 8, 8**10 + 1),
                                ("corpus_expxy_d6", corpus.get("expxy").text, 6, 5, 5**6),
                                ("recip3_d8", "1/(1 + x[1]*x[2] + x[3])", 8, 6, 6**8 + 7),
-                               ("exp_x1x9_d10", "exp(x[1]*x[9])", 10, 4, 4**10)):
+                               ("exp_x1x9_d10", "exp(x[1]*x[9])", 10, 4, 4**10),
+                               ("exp4_d8", "exp(x[1]*x[2]*x[3]*x[4])", 8, 4, 4**8),
+                               ("core_times_prod_d8", "exp(x[1]*x[2])*prod(i=3..d, 1/(1 + x[i]^2))", 8, 6, 6**8),
+                               ("core_phasor_d7", "cos(x[1]*x[7] + x[2]) + x[3]*x[4]*x[5]", 7, 5, 5**7),
+                               ("recip_core_d9", "(1 + x[1] + x[2] + x[3])^(-3)*exp(sum(i=4..d, x[i])/d)",
+                                9, 4, 4**9 + 1)):
         f = exprcore.parse(text, d)
         t0 = time.perf_counter()
         value, rep = mdi_lr(f, d, a, n, with_report=True)

@@ -128,7 +128,7 @@ def test_mdi_golden(lq, golden):
             assert abs(value - want) <= REL * abs(want), (case["tag"], value, want)
         else:
             assert value == 0.0, case["tag"]
-        if rep.method in ("separable", "linform", "subgrid"):
+        if rep.method in ("separable", "cores", "linform", "subgrid"):
             # levels collapse (product form, one commensurate linear form, or
             # unused axes stripped in front of a sweep over the used ones)
             assert (rep.levels, rep.base_dim) == (case["levels"], case["base_dim"]), case["tag"]

@@ -136,9 +136,10 @@ def _sep_eval(terms, x):
     tot = 0j
     for t in terms:
         v = complex(t.coef)
-        for ax, fc in t.factors.items():
-            R = E.evaluate(fc.R, {ax: x[ax - 1]}) if fc.R is not None else 1.0
-            P = E.evaluate(fc.P, {ax: x[ax - 1]}) if fc.P is not None else 0.0
+        for axes, fc in t.factors.items():
+            pt = {ax: x[ax - 1] for ax in axes}
+            R = E.evaluate(fc.R, pt) if fc.R is not None else 1.0
+            P = E.evaluate(fc.P, pt) if fc.P is not None else 0.0
             v *= R * complex(math.cos(P), math.sin(P))
         tot += v
     return tot
@@ -162,6 +163,36 @@ def test_separation_is_exact(text, d):
 def test_non_separable_detected():
     for text, d in [("x[2]*exp(x[1]*x[2])", 2), ("(1 + x[1] + x[2])^(-3)", 2), ("exp(-abs(x[1] - x[2]))", 2)]:
         assert L.separate(lq.parse(text, d)) is None
+
+
+@pytest.mark.parametrize("text,d,cores", [
+    ("exp(x[1]*x[2])*prod(i=3..d, 1/(1 + x[i]^2))", 6, {(1, 2)}),
+    ("exp(x[1]*x[2] + x[3] + sum(i=4..d, 0.5*x[i]))", 7, {(1, 2)}),
+    ("cos(x[1]*x[5] + x[2]) + x[3]*x[4]", 5, {(1, 5)}),
+    ("(1 + x[1] + x[2] + x[3])^(-3)*exp(x[4]) + sin(x[5])", 5, {(1, 2, 3)}),
+    ("x[2]*exp(x[1]*x[2])/(e-2)*prod(i=3..d, x[i])", 4, {(1, 2)}),
+])
+def test_separation_with_cores_is_exact(text, d, cores):
+    """max_axes = 3: non-splitting pieces on <= 3 coordinates become core
+    factors; the factorisation must still reproduce f exactly."""
+    f = lq.parse(text, d)
+    assert L.separate(f) is None
+    terms = L.separate(f, max_axes=3)
+    assert terms is not None
+    seen = {key for t in terms for key in t.factors if len(key) > 1}
+    assert seen == cores, seen
+    rng = np.random.default_rng(d)
+    for _ in range(6):
+        x = rng.uniform(0, 1, d)
+        want = E.evaluate(f, {j + 1: x[j] for j in range(d)})
+        got = _sep_eval(terms, x)
+        assert abs(got.imag) <= 1e-12 * max(1.0, abs(want))
+        assert got.real == pytest.approx(want, rel=1e-12, abs=1e-12)
+
+
+def test_cores_larger_than_three_axes_are_refused():
+    f = lq.parse("exp(x[1]*x[2]*x[3]*x[4])*x[5]", 5)
+    assert L.separate(f, max_axes=3) is None
 
 
 _coef = st.floats(min_value=-2, max_value=2, allow_nan=False)
