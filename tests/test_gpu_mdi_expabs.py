@@ -76,3 +76,24 @@ def test_config5_closed_form_equals_direct_sums(monkeypatch):
     _, b = lq.mdi_lr(f, cfg.d, cfg.mdi_a, cfg.mdi_n, with_report=True)
     assert a.method == b.method == "characteristic"
     assert math.isclose(a.mean, b.mean, rel_tol=1e-12), (a.mean, b.mean)
+
+
+@pytest.mark.parametrize("d,N,kappa,shift,seed", [(40, 8, -1.0, 0.0, 1), (32, 16, -2.5, 0.7, 2)])
+def test_characteristic_function_equals_level_collapse(d, N, kappa, shift, seed):
+    """Two independent GPU routes to the same grid mean of exp(kappa |alpha +
+    <beta, y>|) with rational beta: the characteristic-function integral
+    (what config 5's MDI-LR uses) and the exact distribution of the linear
+    form built level by level (lq_mdi_linform)."""
+    import paper_2404_08867_b200 as lq
+    from paper_2404_08867_b200 import engine
+    Q = 4096
+    rng = np.random.default_rng(seed)
+    k = rng.integers(1, 2 * Q + 1, d)
+    alpha = -float(np.sum(k)) / Q / 2.0 + shift
+    f = lq.parse(_text(k, Q, alpha, kappa), d)
+    value, rep = lq.mdi_lr(f, d, N, N**d, with_report=True)
+    assert rep.method == "characteristic"
+    plan = engine.linform_plan(f, (N,) * d)
+    assert plan.ok
+    lin = engine.mdi_linform_mean(plan)
+    assert abs(value - lin) <= 1e-10 * lin, (value, lin)
