@@ -27,6 +27,14 @@ lq.implr_integrate(lq.parse("(1 + x[1] + x[2] + x[3])^(-4)", 3), 3, 5, 125)
 lq.mdi_lr(lq.parse(make_config(2).text, 100), 100, 64, 64**100)
 lq.mdi_lr(lq.parse("exp(-abs(" + " + ".join(f"{0.1 + (k * 0.6180339887) % 1.0!r}*x[{k + 1}]" for k in range(40)) + " - 10.0))", 40),
           40, 8, 8**40)
+# round 2: level collapse (shared-memory and global levels), cores, sub-grids
+inv = lq.parse("(1 + sum(i=1..d, x[i]))^(-(d+1))", 10)
+lq.mdi_lr(inv, 10, 8, 8**10 + 1)
+os.environ["LQ_LINFORM_SMEM"] = "0"
+lq.mdi_lr(inv, 10, 8, 8**10 + 1)
+del os.environ["LQ_LINFORM_SMEM"]
+lq.mdi_lr(lq.parse("exp(x[1]*x[2])*prod(i=3..d, 1/(1 + x[i]^2))", 8), 8, 6, 6**8)
+lq.mdi_lr(lq.parse("exp(x[1]*x[2]*x[3]*x[4])", 8), 8, 4, 4**8)
 lq.p_alpha(lq.korobov_vector(76, 1009, 6), 4)
 lq.shift_avg_wce_sq(lq.korobov_vector(76, 1009, 6))
 lq.cbc_construct(101, 4)
