@@ -434,6 +434,8 @@ class LinformPlan:
         d = len(counts)
         if any(not 1 <= j <= d for j in lo.beta):
             return
+        if any(int(counts[j - 1]) > LINFORM_MAX_SUPPORT for j in lo.beta):
+            return                      # one axis alone would exceed the support cap
         axes = sorted(lo.beta)
         b_ref = Fraction(lo.beta[axes[0]])
         steps = []
