@@ -1088,27 +1088,9 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     if ((rc = orbit_tables(c, p, &G, &Alo, &Ahi, &apow, &starts))) return rc;
     const int d = f->d;
     const size_t smem = lq::kFftSmem;
-    {
-        const void* fns[] = {(const void*)lq::k_orbit_fft<lq::OUT_EXP, false>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_SINCOS, false>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, false>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_POW, false>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_EXP, true>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_SINCOS, true>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, true>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_EXP, true, 12>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_SINCOS, true, 12>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, true, 12>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_EXP, true, 13>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_SINCOS, true, 13>,
-                             (const void*)lq::k_orbit_fft<lq::OUT_EXPABS, true, 13>,
-                             (const void*)lq::k_fft_coeffs,
-                             (const void*)lq::k_fft_coeffs_pm,
-                             (const void*)lq::k_orbit_fft_quad<lq::OUT_EXP>,
-                             (const void*)lq::k_orbit_fft_quad<lq::OUT_SINCOS>};
-        for (const void* fn : fns)
-            if ((rc = smem_optin(c, fn, smem))) return rc;
-    }
+    // the dynamic shared-memory opt-in of each kernel right before its first
+    // launch: opting in all 17 instantiations up front made the lazy module
+    // loader bring every one of them in (36 ms of the cold first call)
     void *W, *Hc, *dc;
     if ((rc = dev_buf(c, B_FFTW, sizeof(double2) * lq::kFftN, &W))) return rc;
     if (!c->fft_w) {
@@ -1133,6 +1115,7 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
         bq.push_back((double)d);
         if (c->fft_key != bq || c->fft_key_buf != Hc) {
             if ((rc = upload(c, B_AUX0, bq.data(), sizeof(double) * 2 * d, &dc))) return rc;
+            if ((rc = smem_optin(c, (const void*)lq::k_fft_coeffs_pm, smem))) return rc;
             lq::k_fft_coeffs_pm<<<1, lq::kFftThreads, smem, c->stream>>>((const double*)dc, (const double*)dc + d, d,
                                                                         (const double2*)W, (double2*)Hc,
                                                                         (double2*)Hc + lq::kFftN);
@@ -1151,6 +1134,7 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
         cv.push_back((double)d);
         if (c->fft_key != cv || c->fft_key_buf != Hc) {
             if ((rc = upload(c, B_AUX0, cv.data(), sizeof(double) * d, &dc))) return rc;
+            if ((rc = smem_optin(c, (const void*)lq::k_fft_coeffs, smem))) return rc;
             lq::k_fft_coeffs<<<1, lq::kFftThreads, smem, c->stream>>>((const double*)dc, d, (const double2*)W,
                                                                       (double2*)Hc);
             c->launches++;   // the coefficient transform
@@ -1183,10 +1167,13 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     if (quad) {
         const double2* Hm = (const double2*)Hc + lq::kFftN;
         t_begin(c);
-        if (quad_outer_of(f->kind) == lq::OUT_SINCOS)
+        if (quad_outer_of(f->kind) == lq::OUT_SINCOS) {
+            if ((rc = smem_optin(c, (const void*)lq::k_orbit_fft_quad<lq::OUT_SINCOS>, smem))) return rc;
             lq::k_orbit_fft_quad<lq::OUT_SINCOS><<<g, b, smem, c->stream>>>(h, Hm, unit0, ntiles, per, tiles_dev);
-        else
+        } else {
+            if ((rc = smem_optin(c, (const void*)lq::k_orbit_fft_quad<lq::OUT_EXP>, smem))) return rc;
             lq::k_orbit_fft_quad<lq::OUT_EXP><<<g, b, smem, c->stream>>>(h, Hm, unit0, ntiles, per, tiles_dev);
+        }
         t_end(c);
         CK(cudaGetLastError());
         return LQ_OK;
@@ -1195,7 +1182,8 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     t_begin(c);
     // positions per thread that can hold a chain point: B <= RM N/R
     const int rm = (int)((p.m + lq::kFftThreads - 1) / lq::kFftThreads);
-#define LQ_FFT_LIN(O, F, RM) lq::k_orbit_fft<O, F, RM><<<g, b, smem, c->stream>>>(h, unit0, ntiles, per, tiles_dev)
+#define LQ_FFT_LIN(O, F, RM) do { if ((rc = smem_optin(c, (const void*)lq::k_orbit_fft<O, F, RM>, smem))) return rc; \
+                                  lq::k_orbit_fft<O, F, RM><<<g, b, smem, c->stream>>>(h, unit0, ntiles, per, tiles_dev); } while (0)
 #define LQ_FFT_FAST(O) do { if (rm <= 12) LQ_FFT_LIN(O, true, 12); else if (rm == 13) LQ_FFT_LIN(O, true, 13); \
                             else LQ_FFT_LIN(O, true, lq::kFftR); } while (0)
     if (outer == lq::OUT_EXP) { if (fast) LQ_FFT_FAST(lq::OUT_EXP); else LQ_FFT_LIN(lq::OUT_EXP, false, lq::kFftR); }
