@@ -189,7 +189,8 @@ int reduce_dev(lq_ctx* c, const double* vals, int64_t count, double** result) {
         *result = (double*)p;
         return LQ_OK;
     }
-    do {
+    // a single value is its own tree (k_reduce1024 would return it unchanged)
+    while (n > 1) {
         int64_t groups = (n + 1023) / 1024;
         void* p;
         int rc = dev_buf(c, which, groups * sizeof(double), &p);
@@ -200,7 +201,7 @@ int reduce_dev(lq_ctx* c, const double* vals, int64_t count, double** result) {
         cur = (const double*)p;
         n = groups;
         which = which == B_RED0 ? B_RED1 : B_RED0;
-    } while (n > 1);
+    }
     *result = const_cast<double*>(cur);
     return LQ_OK;
 }
