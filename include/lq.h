@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define LQ_ABI_VERSION 6
+#define LQ_ABI_VERSION 7
 
 #define LQ_OK 0
 #define LQ_ERR_VALUE (-1)
@@ -79,7 +79,9 @@ enum {
     LQ_FAM_QUAD_EXP = 4,    /* K exp(alpha + sum_j beta_j x_j + gamma_j x_j^2) */
     LQ_FAM_LIN_POW = 5,     /* K (alpha + <beta,x>)^power, integer power       */
     LQ_FAM_QUAD_SINCOS = 6, /* C0 + A sin(Q) + B cos(Q), Q = sum_j beta_j x_j + gamma_j x_j^2 */
-    LQ_FAM_PROD_QUAD = 7    /* K prod_j ((x_j - beta_j)^2 + gamma_j)^power; gamma_j = NaN: no factor */
+    LQ_FAM_PROD_QUAD = 7,   /* K prod_j ((x_j - beta_j)^2 + gamma_j)^power; gamma_j = NaN: no factor */
+    LQ_FAM_LIN_PROG = 8     /* G(<beta,x>), G any one-variable program (outer); prog = the whole
+                               expression (per-index kernels), outer = G (FFT-form chains)  */
 };
 
 typedef struct {
@@ -89,7 +91,8 @@ typedef struct {
     const double* gamma;    /* [d], host (QUAD_*)        */
     double alpha, K, A, B, C0, kappa;
     double power;           /* LIN_POW: integer-valued exponent */
-    lq_program prog;        /* LQ_FAM_PROGRAM */
+    lq_program prog;        /* LQ_FAM_PROGRAM, LQ_FAM_LIN_PROG: the whole expression */
+    lq_program outer;       /* LQ_FAM_LIN_PROG: G of one variable (variable 0 = <beta,x>) */
 } lq_integrand;
 
 /* ---- context ---------------------------------------------------------- */

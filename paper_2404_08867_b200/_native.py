@@ -25,8 +25,9 @@ LQ_ERR_CUDA, LQ_ERR_UNSUPPORTED, LQ_ERR_NOMEM = -4, -5, -6
 LQ_TILE, LQ_SUPER_TILES, LQ_NODE_BLOCK = 4096, 1024, 256
 LQ_FACTOR_SUPPLIED = 1
 
-ABI_VERSION = 6   # LQ_ABI_VERSION of include/lq.h these ctypes structs match
-FAM = {"program": 0, "lin_exp": 1, "lin_sincos": 2, "lin_expabs": 3, "quad_exp": 4, "lin_pow": 5, "quad_sincos": 6, "prod_quad": 7}
+ABI_VERSION = 7   # LQ_ABI_VERSION of include/lq.h these ctypes structs match
+FAM = {"program": 0, "lin_exp": 1, "lin_sincos": 2, "lin_expabs": 3, "quad_exp": 4, "lin_pow": 5, "quad_sincos": 6,
+       "prod_quad": 7, "lin_prog": 8}
 
 
 class NativeUnavailable(RuntimeError):
@@ -48,7 +49,8 @@ class Program(C.Structure):
 class Integrand(C.Structure):
     _fields_ = [("kind", C.c_int32), ("d", C.c_int32), ("beta", C.c_void_p), ("gamma", C.c_void_p),
                 ("alpha", C.c_double), ("K", C.c_double), ("A", C.c_double), ("B", C.c_double),
-                ("C0", C.c_double), ("kappa", C.c_double), ("power", C.c_double), ("prog", Program)]
+                ("C0", C.c_double), ("kappa", C.c_double), ("power", C.c_double), ("prog", Program),
+                ("outer", Program)]
 
 
 class Factor(C.Structure):

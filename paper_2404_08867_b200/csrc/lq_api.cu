@@ -246,7 +246,7 @@ bool is_lin_kind(int k) {
 }
 int lin_outer(int k) {
     return k == LQ_FAM_LIN_EXP ? lq::OUT_EXP : k == LQ_FAM_LIN_SINCOS ? lq::OUT_SINCOS
-         : k == LQ_FAM_LIN_EXPABS ? lq::OUT_EXPABS : lq::OUT_POW;
+         : k == LQ_FAM_LIN_EXPABS ? lq::OUT_EXPABS : k == LQ_FAM_LIN_PROG ? lq::OUT_PROG : lq::OUT_POW;
 }
 int quad_outer_of(int k) { return k == LQ_FAM_QUAD_SINCOS ? lq::OUT_SINCOS : lq::OUT_EXP; }
 
@@ -307,7 +307,9 @@ int launch_fam(lq_ctx* c, const Args& args, int64_t ntiles, double* tiles_dev, u
 bool pair_ok(const lq_integrand* f, uint64_t n, const uint64_t* z) {
     const char* e = std::getenv("LQ_PAIR");
     if (e && !std::strcmp(e, "0")) return false;
-    if (!z || f->kind == LQ_FAM_PROGRAM || f->kind == LQ_FAM_PROD_QUAD || n < 3 || n > (1ull << 31)) return false;
+    if (!z || f->kind == LQ_FAM_PROGRAM || f->kind == LQ_FAM_LIN_PROG || f->kind == LQ_FAM_PROD_QUAD || n < 3 ||
+        n > (1ull << 31))
+        return false;
     for (int j = 0; j < f->d; ++j) {
         uint64_t a = z[j], b = n;
         while (b) { const uint64_t t = a % b; a = b; b = t; }
@@ -378,8 +380,10 @@ int fam_dispatch(lq_ctx* c, const std::vector<Dim>& tab, int d, uint64_t n, uint
     return launch_fam<KIND, OUTER, PAIR>(c, args, ntiles, tiles_dev, units);
 }
 
+// LIN_PROG has no per-index family kernel: its sub-ranges and non-Korobov
+// rules run the whole expression's bytecode (f->prog) like PROGRAM.
 bool uses_family_kernel(const lq_integrand* f, uint64_t n) {
-    return n <= (1ull << 31) && f->kind != LQ_FAM_PROGRAM;
+    return n <= (1ull << 31) && f->kind != LQ_FAM_PROGRAM && f->kind != LQ_FAM_LIN_PROG;
 }
 
 // Product family (k_prod).  The coordinate comes out of the denormal residue
@@ -593,7 +597,10 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
 
 int check_integrand(const lq_integrand* f) {
     if (!f) return fail(LQ_ERR_VALUE, "null integrand");
-    if (f->kind < LQ_FAM_PROGRAM || f->kind > LQ_FAM_PROD_QUAD) return fail(LQ_ERR_VALUE, "bad family kind %d", f->kind);
+    if (f->kind < LQ_FAM_PROGRAM || f->kind > LQ_FAM_LIN_PROG) return fail(LQ_ERR_VALUE, "bad family kind %d", f->kind);
+    if (f->kind == LQ_FAM_LIN_PROG &&
+        (!f->beta || !f->outer.insn || f->outer.n_insn < 1 || f->outer.n_vars > 1 || f->outer.n_slots > 32))
+        return fail(LQ_ERR_VALUE, "LIN_PROG needs beta and a one-variable outer program of <= 32 slots");
     if ((f->kind == LQ_FAM_LIN_POW || f->kind == LQ_FAM_PROD_QUAD) &&
         (f->power != std::floor(f->power) || std::fabs(f->power) > 1e6))
         return fail(LQ_ERR_VALUE, "LIN_POW needs an integer power, got %g", f->power);
@@ -865,6 +872,7 @@ int orbit_mode() {
 constexpr uint64_t kFftMinN = 1ull << 18;
 int fft_min_d(const lq_integrand* f, uint64_t n) {
     if (is_quad_kind(f->kind)) return 64;
+    if (f->kind == LQ_FAM_LIN_PROG) return 16;   // the alternative is the per-index bytecode kernel
     return n >= (1ull << 22) ? 49 : 112;
 }
 // Accuracy guard: the FFT's norm-wise error on a linear form is about
@@ -889,7 +897,9 @@ bool fft_accurate(const lq_integrand* f) {
 bool fft_wanted(const lq_integrand* f, uint64_t n) {
     const char* e = std::getenv("LQ_FFT");
     if (e && !std::strcmp(e, "0")) return false;
-    if (!(is_lin_kind(f->kind) || is_quad_kind(f->kind)) || f->d > lq::kFftN / 2 || !f->beta) return false;
+    if (!(is_lin_kind(f->kind) || is_quad_kind(f->kind) || f->kind == LQ_FAM_LIN_PROG) || f->d > lq::kFftN / 2 ||
+        !f->beta)
+        return false;
     if (is_quad_kind(f->kind) && !f->gamma) return false;
     if (!fft_accurate(f)) return false;
     if (e && !std::strcmp(e, "always")) return f->d >= 2;
@@ -920,6 +930,7 @@ std::shared_ptr<const OrbPlan> orbit_for(const lq_integrand* f, uint64_t n, cons
             return p;
         }
     }
+    if (f->kind == LQ_FAM_LIN_PROG) return nullptr;     // no direct orbit kernel for a program outer
     if ((f->d + m - 1) / m * m > cap) return nullptr;   // direct form: tables in parameter space
     return orbit_plan((uint32_t)n, (uint32_t)a, m, !prod);
 }
@@ -1151,7 +1162,14 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     h.alpha = f->alpha; h.alphaB = f->alpha + bsum; h.K = f->K; h.A = f->A; h.Bc = f->B; h.C0 = f->C0;
     h.kappa = f->kappa; h.pw = f->power;
     const int outer = lin_outer(f->kind);
-    const bool fast = !quad && pair_fast_consts(f, bsum, h.pf);
+    const bool fast = !quad && outer != lq::OUT_PROG && pair_fast_consts(f, bsum, h.pf);
+    if (outer == lq::OUT_PROG) {
+        void* dg;
+        if ((rc = upload(c, B_PROG, f->outer.insn, sizeof(lq_insn) * f->outer.n_insn, &dg))) return rc;
+        h.g_insn = (const lq_insn*)dg;
+        h.g_n = f->outer.n_insn;
+        h.g_result = f->outer.result;
+    }
     // the exp table of the pair outer; the centred exp-abs form folds e^{-c}
     // into it (lq::pair_expabs_c)
     long double tscale = 1.0L;
@@ -1190,6 +1208,7 @@ int launch_orbit_fft(lq_ctx* c, const lq_integrand* f, const OrbPlan& p, uint64_
     if (outer == lq::OUT_EXP) { if (fast) LQ_FFT_FAST(lq::OUT_EXP); else LQ_FFT_LIN(lq::OUT_EXP, false, lq::kFftR); }
     else if (outer == lq::OUT_SINCOS) { if (fast) LQ_FFT_FAST(lq::OUT_SINCOS); else LQ_FFT_LIN(lq::OUT_SINCOS, false, lq::kFftR); }
     else if (outer == lq::OUT_EXPABS) { if (fast) LQ_FFT_FAST(lq::OUT_EXPABS); else LQ_FFT_LIN(lq::OUT_EXPABS, false, lq::kFftR); }
+    else if (outer == lq::OUT_PROG) LQ_FFT_LIN(lq::OUT_PROG, false, lq::kFftR);
     else LQ_FFT_LIN(lq::OUT_POW, false, lq::kFftR);
 #undef LQ_FFT_FAST
 #undef LQ_FFT_LIN

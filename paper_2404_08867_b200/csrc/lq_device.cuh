@@ -92,6 +92,12 @@ __device__ __forceinline__ double ipow(double b, int k) {
     return k == 2 ? b * b : pow(b, (double)k);
 }
 
+// One-variable program input (MDI factors, outer functions G(s)).
+struct UnivSrc {
+    double y;
+    __device__ __forceinline__ double x(int) const { return y; }
+};
+
 // Evaluate a program; Src::x(b) supplies variable b.  NS = slot capacity.
 template <int NS, class Src>
 __device__ __forceinline__ double run_program(const lq_insn* __restrict__ prog, int n_insn, int result,

@@ -122,7 +122,7 @@ struct LinParams {
 
 // Outer functions g(s) of the families' inner sums s:
 //   EXP K e^s | SINCOS C0 + A sin s + B cos s | EXPABS K e^(kappa |s|) | POW K s^pw
-enum : int { OUT_EXP = 0, OUT_SINCOS = 1, OUT_EXPABS = 2, OUT_POW = 3 };
+enum : int { OUT_EXP = 0, OUT_SINCOS = 1, OUT_EXPABS = 2, OUT_POW = 3, OUT_PROG = 4 };
 
 // numpy's b**k for integer k (exprcore.py:466-468; square for k == 2, libm pow
 // otherwise; a negative k is 1 / b**(-k), as the reference's pow nodes).
@@ -931,6 +931,8 @@ struct FftHead {
     const double2* Hc;                 // conj(FFT(c zero-padded)) / N, c_j = beta_j / n
     double alpha, alphaB, K, A, Bc, C0, kappa, pw;
     PairFast pf;
+    const lq_insn* g_insn;             // OUT_PROG: the outer G as bytecode (variable 0)
+    int32_t g_n, g_result;
     int32_t zero;                      // unit 0 also adds the point x = 0
     double2 etab[kFftExpTab > 0 ? kFftExpTab : 1];          // (2^(j/2^EB), 2^(-j/2^EB)), correctly rounded on the host
 };
@@ -1102,6 +1104,25 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
     // so the out-of-line outer function runs with no transform state live
     fft4096_regs<true>(v, buf, Wt);
     const int v0 = fft_chain_valid(a, u0), v1 = fft_chain_valid(a, u1);   // recomputed: not live across the FFTs
+    if constexpr (OUTER == OUT_PROG) {
+        // G(s) + G(sum beta - s) by the bytecode interpreter: nothing of the
+        // transforms is live here, so its slots cost only local memory
+        double slot[32];
+        #pragma unroll 1
+        for (int k = threadIdx.x; k < v0 || k < v1; k += kFftThreads) {
+            const double2 y = buf[fpad(k)];
+            const double l0 = y.x, l1 = -y.y;
+            double g = 0.0;
+            if (k < v0)
+                g += run_program<32>(a.g_insn, a.g_n, a.g_result, UnivSrc{l0}, slot) +
+                     run_program<32>(a.g_insn, a.g_n, a.g_result, UnivSrc{a.alphaB - l0}, slot);
+            if (k < v1)
+                g += run_program<32>(a.g_insn, a.g_n, a.g_result, UnivSrc{l1}, slot) +
+                     run_program<32>(a.g_insn, a.g_n, a.g_result, UnivSrc{a.alphaB - l1}, slot);
+            s += g;
+        }
+        if (u0 == 0 && a.zero && threadIdx.x == 0) s += run_program<32>(a.g_insn, a.g_n, a.g_result, UnivSrc{0.0}, slot);
+    } else {
     #pragma unroll 1
     for (int k = threadIdx.x; k < v0 || k < v1; k += kFftThreads) {
         const double2 y = buf[fpad(k)];             // conj of the correlation: (L0, -L1)
@@ -1112,7 +1133,9 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_orbit_fft(const __grid_const
         s += (k < v0 ? f00 + f01 : 0.0) + (k < v1 ? f10 + f11 : 0.0);
     }
     }
-    if (u0 == 0 && a.zero && threadIdx.x == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
+    }
+    if constexpr (OUTER != OUT_PROG)
+        if (u0 == 0 && a.zero && threadIdx.x == 0) s += outer_fn<OUTER>(0.0, prm);   // point 0
 #if LQ_FFT_DEFER
     #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -1371,11 +1394,6 @@ __global__ void k_midpoint_nodes(const int64_t* __restrict__ counts, const int64
 }
 
 // ============================================================ MDI cluster sums
-struct UnivSrc {
-    double y;
-    __device__ __forceinline__ double x(int) const { return y; }
-};
-
 // One CTA per (factor, node block): evaluates U_f(y_t) = R(y_t) e^{i P(y_t)}
 // on the block's 256 midpoint nodes and writes the (re, im) block sums.
 template <int NS>

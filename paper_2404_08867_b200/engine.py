@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _native as N
 from .expr import Expr, as_expr, free_vars
-from .lower import Program, compile_program, linear_outer, recognize_plain, separate
+from .lower import Program, compile_program, linear_outer, recognize_linear_program, recognize_plain, separate
 
 __all__ = ["PlainIntegrand", "plain_integrand", "lattice_sum", "tensor_program", "SeparablePlan",
            "separable_plan", "mdi_separable_sum"]
@@ -69,6 +69,14 @@ class PlainIntegrand:
                 s.gamma = gamma.ctypes.data
             s.alpha, s.K, s.A, s.B = family.alpha, family.K, family.A, family.B
             s.C0, s.kappa, s.power = family.C0, family.kappa, float(family.power)
+            if family.outer is not None:
+                g = np.ascontiguousarray(family.outer.insn)
+                self._keep.append(g)
+                s.outer.insn = g.ctypes.data
+                s.outer.n_insn = len(g)
+                s.outer.n_slots = family.outer.n_slots
+                s.outer.result = family.outer.result
+                s.outer.n_vars = family.outer.n_vars
         if program is not None:
             if family is None:
                 s.kind = 0
@@ -91,7 +99,7 @@ def plain_integrand(f, d, force_program=False):
     e = as_expr(f)
 
     def make():
-        fam = None if force_program else recognize_plain(e, d)
+        fam = None if force_program else (recognize_plain(e, d) or recognize_linear_program(e, d))
         prog = compile_program(e)
         return PlainIntegrand(e, d, fam, prog)
 
@@ -105,7 +113,7 @@ def attach_jit(pi, n):
     every rank of a sharded sum and every sub-range call of the same lattice
     run the same code."""
     from . import jit
-    interpreted = pi.family is None or n > 2**31
+    interpreted = pi.family is None or pi.family.kind == "lin_prog" or n > 2**31
     if interpreted and not pi.struct.prog.jit and jit.jit_wanted(int(n) * max(len(pi.program), 1)):
         h = jit.compile_expr(pi.expr)
         if h:

@@ -33,7 +33,7 @@ from .expr import Expr, add, const, free_vars, func, mul, power, topo, var
 __all__ = [
     "linear_form", "quad_form", "recognize_plain", "PlainFamily",
     "Program", "compile_program", "separate", "SepTerm", "Factor",
-    "MAX_SLOTS", "INSN_DTYPE", "LinearOuter", "linear_outer",
+    "MAX_SLOTS", "INSN_DTYPE", "LinearOuter", "linear_outer", "recognize_linear_program",
 ]
 
 # ------------------------------------------------------------ polynomial view
@@ -154,6 +154,8 @@ class PlainFamily:
           'quad_exp'    f = K exp(alpha + sum_j beta_j x_j + gamma_j x_j^2)
           'quad_sincos' f = C0 + A sin(Q) + B cos(Q), Q = sum_j beta_j x_j + gamma_j x_j^2
           'prod_quad'   f = K prod_j ((x_j - beta_j)^2 + gamma_j)^power  (gamma_j NaN: no factor)
+          'lin_prog'    f = G(<beta, x>), G any expression of one variable (``outer``:
+                        its bytecode); the FFT-form chains evaluate G per linear form
     """
 
     kind: str
@@ -167,6 +169,7 @@ class PlainFamily:
     C0: float = 0.0
     kappa: float = -1.0
     power: int = 0
+    outer: object = None      # lin_prog: Program of G (variable 0 = <beta, x>)
 
 
 def _vec(coefs, d):
@@ -312,6 +315,22 @@ def recognize_plain(e, d):
         if fam is not None:
             return fam
     return None
+
+
+def recognize_linear_program(e, d, max_slots=32):
+    """f = G(<beta, x>) for an expression no closed family matches (e.g.
+    1/(1 + L^2), exp(-L^2) with L a full linear form, or sums of functions of
+    one form): PlainFamily 'lin_prog' with G's bytecode, or None."""
+    lo = linear_outer(e)
+    if lo is None or len(lo.beta) < 2:
+        return None
+    beta = _vec(lo.beta, d)
+    if beta is None:
+        return None
+    prog = compile_program(lo.G)
+    if prog.n_slots > max_slots or prog.n_vars > 1:
+        return None
+    return PlainFamily("lin_prog", d, beta, outer=prog)
 
 
 def _trig_family(terms, C0, d, form, kind):

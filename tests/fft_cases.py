@@ -14,6 +14,10 @@ PAIR = [("expabs", 10.0, 0), ("expabs", 0.01, 0), ("expabs", 350.0, 0), ("expabs
         ("exp", 3.0, 0.25), ("exp", 600.0, 0.25), ("exp", 100.0, -650.0), ("sincos", 9.0, 0),
         ("sincos", 400.0, 0)]
 RM_FAMILIES = ["exp", "expabs", "sincos"]
+# functions of one linear form no closed family covers (PlainFamily 'lin_prog':
+# the FFT-form chains with the outer G run as bytecode)
+LINPROG = [("recip_sq", 100003, 64), ("gauss_lin", 1000003, 300), ("trig_mix", 100003, 150),
+           ("recip_sq", 1000003, 1000)]
 RM_DS = [768, 769, 1024, 1025]
 _FACTORS = {100003: (2, 3, 7, 2381), 1000003: (2, 3, 166667)}
 
@@ -86,8 +90,24 @@ def rm_case(family, d):
     return f"rm/{family}/{d}", text, params, n, primitive_root(n)
 
 
+def linprog_text(kind, d, rng):
+    c = [float(v) for v in rng.uniform(0, 1, d)]
+    L = " + ".join(f"{c[j] / d!r}*x[{j + 1}]" for j in range(d))
+    if kind == "recip_sq":
+        return f"1/(1 + (2*({L}) - 0.8)^2)"
+    if kind == "gauss_lin":
+        return f"exp(-(3*({L}) - 1.5)^2)"
+    return f"cos({L})^2 + 0.5*sin(3*({L}))"
+
+
+def linprog_case(kind, n, d):
+    rng = np.random.default_rng(zlib.crc32(f"linprog/{kind}/{n}/{d}".encode()))
+    return f"linprog/{kind}/{n}/{d}", linprog_text(kind, d, rng), None, n, primitive_root(n)
+
+
 def all_cases():
     out = [main_case(f, n, d, k) for f in FAMILIES for (n, d, k) in MAIN]
     out += [pair_case(*p) for p in PAIR]
     out += [rm_case(f, d) for f in RM_FAMILIES for d in RM_DS]
+    out += [linprog_case(*c) for c in LINPROG]
     return out

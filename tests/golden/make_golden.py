@@ -353,7 +353,7 @@ def _fft_case_sum(case):
             "ref_seconds": time.perf_counter() - t0}
 
 
-def fft_cases_job(procs):
+def fft_cases_job(procs, only_new=False):
     """Reference sums of every case of tests/test_gpu_fft.py (cases from
     tests/fft_cases.py), so that the FFT-form kernel meets the reference and
     not only the direct orbit kernel."""
@@ -361,8 +361,18 @@ def fft_cases_job(procs):
     sys.path.insert(0, os.path.dirname(HERE))
     import fft_cases
     cases = fft_cases.all_cases()
+    if only_new:
+        have = set()
+        path = os.path.join(HERE, "fft.json")
+        if os.path.exists(path):
+            with open(path) as fh:
+                old = json.load(fh)["cases"]
+            have = {c["key"] for c in old}
+        cases = [c for c in cases if c[0] not in have]
     with mp.Pool(procs, maxtasksperchild=1) as pool:
         out = list(pool.imap(_fft_case_sum, cases, chunksize=1))
+    if only_new:
+        out = old + out if have else out
     return out
 
 
@@ -547,13 +557,14 @@ def main():
     ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites", "cfg5_full", "linform", "fft", "parser", "suites7", "subgrid"],
                     default=None)
     ap.add_argument("--procs", type=int, default=os.cpu_count())
+    ap.add_argument("--only-new", action="store_true", help="fft: compute only cases missing from fft.json")
     args = ap.parse_args()
     meta = {"generator": "tests/golden/make_golden.py", "numpy": np.__version__,
             "python": sys.version.split()[0], "reference": "/root/reference/pkg (latquad 0.1.0)"}
     jobs = {"points": lambda: points_cases(), "slr": lambda: slr_cases(args.skip_slow),
             "mdi": lambda: mdi_cases(args.skip_slow), "quality": quality_cases, "mc": mc_cases,
             "suites": suite_cases, "cfg5_full": lambda: cfg5_full_case(args.procs),
-            "linform": lambda: linform_cases(args.skip_slow), "fft": lambda: fft_cases_job(args.procs),
+            "linform": lambda: linform_cases(args.skip_slow), "fft": lambda: fft_cases_job(args.procs, args.only_new),
             "parser": parser_cases, "suites7": suite7_cases, "subgrid": subgrid_cases}
     for name, fn in jobs.items():
         if args.only != name and (args.only or name in ("cfg5_full", "linform", "fft", "suites7")):

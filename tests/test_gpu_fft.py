@@ -162,3 +162,24 @@ def test_fft_position_bound_boundaries(env, family, d, monkeypatch):
     assert math.isclose(fft, direct, rel_tol=1e-12, abs_tol=1e-12 * n), (family, d, fft, direct)
     ref = _ref_sum(key)
     assert math.isclose(fft, ref, rel_tol=REL, abs_tol=1e-10 * n), (family, d, fft, ref)
+
+
+@pytest.mark.parametrize("kind,n,d", fft_cases.LINPROG)
+def test_fft_program_outer_matches_index_kernel_and_reference(env, kind, n, d, monkeypatch):
+    """Functions of one linear form outside the closed families (PlainFamily
+    'lin_prog': 1/(1 + L^2), exp(+-L^2) of a full form, mixed trig of one
+    form): the FFT-form chains with G run as bytecode, against the per-index
+    bytecode kernel over the whole expression and the reference's own sum."""
+    lq, N, engine = env
+    key, text, _, n, a = fft_cases.linprog_case(kind, n, d)
+    f = lq.parse(text, d)
+    rule = lq.korobov_vector(a, n, d)
+    pi = engine.plain_integrand(f, d)
+    assert pi.kind == "lin_prog"
+    z = rule.z_reduced_array()
+    got = _sums(engine, N, pi, n, z, monkeypatch)
+    assert N.LAYOUT_ORBIT_FFT in got and N.LAYOUT_INDEX in got, got.keys()
+    fft, index = got[N.LAYOUT_ORBIT_FFT], got[N.LAYOUT_INDEX]
+    assert math.isclose(fft, index, rel_tol=1e-12, abs_tol=1e-12 * n), (key, fft, index)
+    ref = _ref_sum(key)
+    assert math.isclose(fft, ref, rel_tol=REL, abs_tol=1e-10 * n), (key, fft, ref)
