@@ -114,7 +114,8 @@ def attach_jit(pi, n):
     run the same code."""
     from . import jit
     interpreted = pi.family is None or pi.family.kind == "lin_prog" or n > 2**31
-    if interpreted and not pi.struct.prog.jit and jit.jit_wanted(int(n) * max(len(pi.program), 1)):
+    n_insn = max(len(pi.program), 1)
+    if interpreted and not pi.struct.prog.jit and jit.jit_wanted(int(n) * n_insn, n_insn):
         h = jit.compile_expr(pi.expr)
         if h:
             pi.struct.prog.jit = h
@@ -142,7 +143,7 @@ def _tensor_program_struct(g, grids):
     from . import jit
     jh = None
     # JIT choice from the whole grid (same code on every rank and sub-range)
-    if jit.jit_wanted(int(grids.total) * max(len(ins), 1)) and d <= 128:
+    if jit.jit_wanted(int(grids.total) * max(len(ins), 1), max(len(ins), 1)) and d <= 128:
         jh = jit.compile_expr(as_expr(g), n_axes=max(d, 1))
     p = N.Program(ins.ctypes.data, len(ins), prog.n_slots, prog.result, prog.n_vars, jh)
     if getattr(grids, "midpoint", False):

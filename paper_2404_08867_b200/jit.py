@@ -197,16 +197,29 @@ _lock = threading.Lock()
 
 
 # interpreter instruction-points above which compiling pays for itself
-# (NVRTC takes ~0.3 s per expression; the interpreter runs ~2e9 insn-points/s)
+# (NVRTC takes ~0.3 s for a small expression; the interpreter runs ~2e9
+# insn-points/s)
 JIT_THRESHOLD = 1e9
+# NVRTC time grows faster than quadratically with the straight-line body
+# (tools/jit_compile_probe.py on the B200 box: 37/69/133/261 bytecode
+# instructions -> 0.36/0.82/2.6/11.6 s; ~3000 -> 620 s), while the
+# interpreter is only ~4x slower than the compiled kernel: past this size the
+# interpreter always wins
+JIT_MAX_INSN = 160
 
 
-def jit_wanted(work):
-    """LQ_JIT=0 never, =always for any size, default: only past JIT_THRESHOLD."""
+def jit_wanted(work, n_insn=1):
+    """LQ_JIT=0 never, =always for any size; default: programs of at most
+    JIT_MAX_INSN instructions whose work pays for the compile (the threshold
+    grows with the square of the program length, as the compile time does)."""
     mode = os.environ.get("LQ_JIT", "auto")
     if mode == "0":
         return False
-    return mode == "always" or work >= JIT_THRESHOLD
+    if mode == "always":
+        return True
+    if n_insn > JIT_MAX_INSN:
+        return False
+    return work >= JIT_THRESHOLD * max(1.0, (n_insn / 32.0) ** 2)
 
 
 def compile_expr(e, n_axes=1):

@@ -17,7 +17,7 @@ RM_FAMILIES = ["exp", "expabs", "sincos"]
 # functions of one linear form no closed family covers (PlainFamily 'lin_prog':
 # the FFT-form chains with the outer G run as bytecode)
 LINPROG = [("recip_sq", 100003, 64), ("gauss_lin", 1000003, 300), ("trig_mix", 100003, 150),
-           ("recip_sq", 1000003, 1000)]
+           ("recip_sq", 100003, 700)]
 RM_DS = [768, 769, 1024, 1025]
 _FACTORS = {100003: (2, 3, 7, 2381), 1000003: (2, 3, 166667)}
 

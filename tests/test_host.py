@@ -384,3 +384,19 @@ def test_pow2_layout_without_gpu():
     assert _native.lattice_layout(pi.struct, r.n, r.z_reduced_array()).mode != _native.LAYOUT_ORBIT_POW2
     r = lq.korobov_vector(12346, 1 << 24, cfg.d)
     assert _native.lattice_layout(pi.struct, r.n, r.z_reduced_array()).mode != _native.LAYOUT_ORBIT_POW2
+
+
+def test_jit_policy_refuses_long_programs(monkeypatch):
+    """NVRTC time grows faster than quadratically with the expression (a
+    3000-instruction body took 620 s on the box, the interpreter 3.4 ms):
+    past JIT_MAX_INSN the interpreter always runs."""
+    from paper_2404_08867_b200 import jit
+    monkeypatch.delenv("LQ_JIT", raising=False)
+    assert jit.jit_wanted(1e12, 40)
+    assert not jit.jit_wanted(1e8, 40)
+    assert not jit.jit_wanted(1e15, jit.JIT_MAX_INSN + 1)
+    assert not jit.jit_wanted(2e9, 128)            # 16x the base threshold at 128 instructions
+    monkeypatch.setenv("LQ_JIT", "always")
+    assert jit.jit_wanted(1.0, 10**6)
+    monkeypatch.setenv("LQ_JIT", "0")
+    assert not jit.jit_wanted(1e15, 10)
