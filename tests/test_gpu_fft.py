@@ -183,3 +183,22 @@ def test_fft_program_outer_matches_index_kernel_and_reference(env, kind, n, d, m
     assert math.isclose(fft, index, rel_tol=1e-12, abs_tol=1e-12 * n), (key, fft, index)
     ref = _ref_sum(key)
     assert math.isclose(fft, ref, rel_tol=REL, abs_tol=1e-10 * n), (key, fft, ref)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fft_full_size_random_multipliers(env, seed, monkeypatch):
+    """Config 5's integrand on n = 2^31 - 1 with other seeded multipliers a
+    (other orders and coset structures of <a>): FFT form against the direct
+    orbit kernel, full lattice, 1e-12."""
+    lq, N, engine = env
+    from paper_2404_08867_b200.configs import make_config
+    import numpy as np
+    cfg = make_config(5)
+    n = cfg.plain_n
+    a = int(np.random.default_rng(1000 + seed).integers(2, n - 1))
+    f = lq.parse(cfg.text, cfg.d)
+    rule = lq.korobov_vector(a, n, cfg.d)
+    pi = engine.plain_integrand(f, cfg.d)
+    got = _sums(engine, N, pi, n, rule.z_reduced_array(), monkeypatch)
+    fft, direct = got[N.LAYOUT_ORBIT_FFT], got[N.LAYOUT_ORBIT]
+    assert math.isclose(fft, direct, rel_tol=1e-12), (a, fft, direct)
