@@ -20,6 +20,8 @@ def repeated_add(v, count, acc=0.0):
     count = int(count)
     if count <= 0 or v == 0.0:
         return acc
+    if not (math.isfinite(v) and math.isfinite(acc)):
+        return acc + v          # inf / nan absorb every further addition
     if v < 0.0:
         return -repeated_add(-v, count, -acc)
     while count > 0:

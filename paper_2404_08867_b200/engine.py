@@ -441,7 +441,7 @@ class LinformPlan:
         if lo is None:
             return
         d = len(counts)
-        if any(not 1 <= j <= d for j in lo.beta):
+        if any(not 1 <= j <= d for j in lo.beta) or not all(math.isfinite(c) for c in lo.beta.values()):
             return
         if any(int(counts[j - 1]) > LINFORM_MAX_SUPPORT for j in lo.beta):
             return                      # one axis alone would exceed the support cap
