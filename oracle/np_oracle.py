@@ -1,9 +1,9 @@
 """Numpy restatement of the reference hot path (CPU ORACLE, test-only).
 
 Each function cites the reference code it restates
-(/root/reference/pkg/src/latquad/...).  Expressions are the repo's own
-``paper_2404_08867_b200.expr.Expr`` (the reference's Expr cannot travel to the
-GPU box); ``eval_array`` below follows the reference evaluator's order.
+(/root/reference/pkg/src/latquad/...).  Integrands are source text in the
+reference's language, evaluated by the oracle's own literal evaluator
+(``oracle/np_expr.py``): nothing here imports the product package.
 """
 
 from __future__ import annotations
@@ -12,7 +12,7 @@ import math
 
 import numpy as np
 
-from paper_2404_08867_b200.expr import as_expr, topo
+from oracle import np_expr
 
 _MAX_ENUM = 2**53
 
@@ -30,41 +30,14 @@ def points_block(n, z, start, stop):
     return out
 
 
-def eval_array(e, assignment):
-    """exprcore.py:442-480 over the repo's Expr: sums v = const; v = v + c*t,
-    products v = coeff; v = v*f; pow 1/b or b**k; numpy exp/sin/cos (+abs)."""
-    e = as_expr(e)
-    memo = {}
-    for node in topo(e):
-        op = node.op
-        if op == "const":
-            v = node.val
-        elif op == "var":
-            v = assignment[node.idx]
-        elif op == "add":
-            v = node.val
-            for c, t in node.terms:
-                v = v + c * memo[t]
-        elif op == "mul":
-            v = node.val
-            for f in node.args:
-                v = v * memo[f]
-        elif op == "pow":
-            b = memo[node.args[0]]
-            k = node.idx
-            v = b ** k if k > 0 else (1.0 / b if k == -1 else 1.0 / (b ** -k))
-        elif op == "exp":
-            v = np.exp(memo[node.args[0]])
-        elif op == "sin":
-            v = np.sin(memo[node.args[0]])
-        elif op == "cos":
-            v = np.cos(memo[node.args[0]])
-        elif op == "abs":
-            v = np.abs(memo[node.args[0]])
-        else:
-            raise ValueError(op)
-        memo[node] = v
-    return memo[e]
+def eval_array(text, d, assignment):
+    """exprcore.py:442-480's job -- the integrand's values over numpy columns
+    -- done by the oracle's own literal evaluator (np_expr: the source text as
+    written, no canonical DAG), so the oracle shares nothing with the
+    product's front end."""
+    if not isinstance(text, str):
+        raise TypeError("the oracle evaluates integrand source text (not a product Expr)")
+    return np_expr.evaluate(text, d, assignment)
 
 
 def slr_sum(f, n, z, i_begin=0, i_end=None, rows=1 << 19):
@@ -76,7 +49,7 @@ def slr_sum(f, n, z, i_begin=0, i_end=None, rows=1 << 19):
     for start in range(i_begin, i_end, rows):
         stop = min(start + rows, i_end)
         pts = points_block(n, z, start, stop)
-        vals = eval_array(f, {i + 1: pts[:, i] for i in range(d)})
+        vals = eval_array(f, d, {i + 1: pts[:, i] for i in range(d)})
         acc += float(vals) * len(pts) if np.ndim(vals) == 0 else float(np.sum(vals))
     return acc
 
@@ -93,7 +66,7 @@ def mc_value(f, d, n, seed=0, rows=1 << 19):
     while done < n:
         m = min(rows, n - done)
         pts = rng.random((m, d))
-        vals = eval_array(f, {i + 1: pts[:, i] for i in range(d)})
+        vals = eval_array(f, d, {i + 1: pts[:, i] for i in range(d)})
         acc += float(vals) * m if np.ndim(vals) == 0 else float(np.sum(vals))
         done += m
     return acc / n
@@ -145,7 +118,7 @@ def direct_tensor_sum(f, nodes, chunk=1 << 19):
         for k, (ct, arr) in enumerate(zip(counts, nodes)):
             assign[k + 1] = arr[rem % ct]
             rem = rem // ct
-        vals = eval_array(f, assign)
+        vals = eval_array(f, len(counts), assign)
         acc += float(vals) * len(idx) if np.ndim(vals) == 0 else float(np.sum(vals))
     return acc
 

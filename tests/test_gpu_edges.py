@@ -51,7 +51,8 @@ def test_negative_start_points(lq):
 def test_modulus_boundary_family_vs_bytecode(lq, n):
     from paper_2404_08867_b200 import engine
     d = 6
-    f = lq.parse("exp(-abs(0.3*x[1] - 0.2*x[2] + 0.5*x[3] - 0.1*x[4] + 0.25*x[5] - 0.4*x[6] + 0.05))", d)
+    text = "exp(-abs(0.3*x[1] - 0.2*x[2] + 0.5*x[3] - 0.1*x[4] + 0.25*x[5] - 0.4*x[6] + 0.05))"
+    f = lq.parse(text, d)
     z = np.array([1, 1234567, 987654321 % n, 5, 2**30 + 3, 77], dtype=np.uint64)
     fam = engine.plain_integrand(f, d)
     prog = engine.plain_integrand(f, d, force_program=True)
@@ -60,7 +61,7 @@ def test_modulus_boundary_family_vs_bytecode(lq, n):
     b = engine.lattice_sum(prog, n, z, lo, hi)
     assert abs(a - b) <= 1e-12 * abs(b)
     from oracle import np_oracle as orc
-    want = orc.slr_sum(f, n, [int(v) for v in z], lo, lo + 4096)
+    want = orc.slr_sum(text, n, [int(v) for v in z], lo, lo + 4096)
     got = engine.lattice_sum(fam, n, z, lo, lo + 4096)
     assert abs(got - want) <= 1e-12 * abs(want)
 

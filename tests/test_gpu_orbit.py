@@ -68,7 +68,7 @@ def test_orbit_configs_vs_oracle(env, cid, monkeypatch):
     idx = _sum(lq, engine, f, rule, "0", monkeypatch)
     assert math.isclose(orb, idx, rel_tol=1e-12), (orb, idx)
     if cfg.plain_n <= 20000:
-        ref = np_oracle.slr_sum(f, rule.n, list(rule.z_reduced))
+        ref = np_oracle.slr_sum(cfg.text, rule.n, list(rule.z_reduced))
         assert math.isclose(orb, ref, rel_tol=REL), (orb, ref)
 
 
@@ -94,7 +94,7 @@ def test_orbit_group_structures(env, kind, family, monkeypatch):
     assert lay.mode == N.LAYOUT_ORBIT, (kind, o)
     orb = _sum(lq, engine, f, rule, "always", monkeypatch)
     idx = _sum(lq, engine, f, rule, "0", monkeypatch)
-    ref = np_oracle.slr_sum(f, rule.n, list(rule.z_reduced))
+    ref = np_oracle.slr_sum(text, rule.n, list(rule.z_reduced))
     assert math.isclose(orb, ref, rel_tol=REL), (kind, family, orb, ref)
     assert math.isclose(orb, idx, rel_tol=1e-12), (kind, family, orb, idx)
 
@@ -165,7 +165,8 @@ def test_paired_layout_vs_oracle(env, n, family, monkeypatch):
     from oracle import np_oracle
     d = 96 if family in ("gauss", "qtrig") else 40       # 96: the cluster split runs too
     rng = np.random.default_rng(zlib.crc32(f"{n}/{family}".encode()))
-    f = lq.parse(_family_text(family, d, rng), d)
+    text = _family_text(family, d, rng)
+    f = lq.parse(text, d)
     rule = lq.LatticeRule(n, _unit_vector(n, d, rng))
     monkeypatch.delenv("LQ_PAIR", raising=False)
     assert _layout(N, engine, f, rule).mode == N.LAYOUT_PAIRED
@@ -175,7 +176,7 @@ def test_paired_layout_vs_oracle(env, n, family, monkeypatch):
     monkeypatch.setenv("LQ_PAIR", "0")
     assert _layout(N, engine, f, rule).mode == N.LAYOUT_INDEX
     plain = engine.lattice_sum(pi, n, z)
-    ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
+    ref = np_oracle.slr_sum(text, n, list(rule.z_reduced))
     assert math.isclose(paired, ref, rel_tol=REL), (n, family, paired, ref)
     assert math.isclose(paired, plain, rel_tol=1e-12), (n, family, paired, plain)
 
@@ -199,7 +200,8 @@ def test_paired_partials_sharded_bit_identical(env, monkeypatch):
     monkeypatch.delenv("LQ_PAIR", raising=False)
     n, d = 1 << 26, 64
     rng = np.random.default_rng(11)
-    f = lq.parse(_family_text("expabs", d, rng), d)
+    text = _family_text("expabs", d, rng)
+    f = lq.parse(text, d)
     rule = lq.LatticeRule(n, _unit_vector(n, d, rng))
     pi = engine.plain_integrand(f, d)
     z = rule.z_reduced_array()
@@ -231,7 +233,8 @@ def test_new_families_match_bytecode(env, family, kind, monkeypatch):
     lq, N, engine = env
     d, n = 50, 1000003
     rng = np.random.default_rng(9)
-    f = lq.parse(_family_text(family, d, rng), d)
+    text = _family_text(family, d, rng)
+    f = lq.parse(text, d)
     rule = lq.korobov_vector(76543, n, d)
     fam = engine.plain_integrand(f, d)
     prog = engine.plain_integrand(f, d, force_program=True)
@@ -252,7 +255,8 @@ def test_layout_edges_vs_index_kernel(env, n, d, a, monkeypatch):
     # equals the plain per-index sum
     lq, N, engine = env
     rng = np.random.default_rng(n + d)
-    f = lq.parse(_family_text("expabs", d, rng), d)
+    text = _family_text("expabs", d, rng)
+    f = lq.parse(text, d)
     rule = lq.korobov_vector(a, n, d)
     pi = engine.plain_integrand(f, d)
     z = rule.z_reduced_array()
@@ -267,7 +271,7 @@ def test_layout_edges_vs_index_kernel(env, n, d, a, monkeypatch):
     assert math.isclose(got, want, rel_tol=1e-12), (n, d, lay, got, want)
     if n * d <= 200000:
         from oracle import np_oracle
-        ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
+        ref = np_oracle.slr_sum(text, n, list(rule.z_reduced))
         assert math.isclose(got, ref, rel_tol=REL), (n, d, got, ref)
 
 
@@ -292,7 +296,7 @@ def test_product_family_vs_bytecode_and_oracle(env, text, d, monkeypatch):
         want = engine.lattice_sum(prog, n, z)
         assert math.isclose(got, want, rel_tol=1e-12), (text, n, got, want)
         if n * d <= 200000:
-            ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
+            ref = np_oracle.slr_sum(text, n, list(rule.z_reduced))
             assert math.isclose(got, ref, rel_tol=REL), (text, n, got, ref)
 
 
@@ -369,7 +373,8 @@ def test_pow2_levels_vs_paired(env, k, a, d, family, monkeypatch):
     lq, N, engine = env
     n = 1 << k
     rng = np.random.default_rng(zlib.crc32(f"pow2/{k}/{a}/{d}/{family}".encode()))
-    f = lq.parse(_family_text(family, d, rng), d)
+    text = _family_text(family, d, rng)
+    f = lq.parse(text, d)
     rule = lq.korobov_vector(a % n, n, d)
     pi = engine.plain_integrand(f, d)
     z = rule.z_reduced_array()
@@ -384,7 +389,7 @@ def test_pow2_levels_vs_paired(env, k, a, d, family, monkeypatch):
     assert math.isclose(got, want, rel_tol=1e-11, abs_tol=1e-9 * n), (k, a, d, family, got, want)
     if n * d <= 200000:
         from oracle import np_oracle
-        ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
+        ref = np_oracle.slr_sum(text, n, list(rule.z_reduced))
         assert math.isclose(got, ref, rel_tol=REL, abs_tol=1e-9 * n), (k, a, d, family, got, ref)
 
 
@@ -433,7 +438,8 @@ def test_pair_fast_direct_kernels(env, layout, family, scale, offset, monkeypatc
     from oracle import np_oracle
     n, d = 100003, 40
     rng = np.random.default_rng(zlib.crc32(f"pairdirect/{family}/{scale}".encode()))
-    f = lq.parse(_pair_text(family, d, rng, scale, offset), d)
+    text = _pair_text(family, d, rng, scale, offset)
+    f = lq.parse(text, d)
     if layout == "orbit":
         rule = lq.korobov_vector(2, n, d)
         want = N.LAYOUT_ORBIT
@@ -448,5 +454,5 @@ def test_pair_fast_direct_kernels(env, layout, family, scale, offset, monkeypatc
     monkeypatch.setenv("LQ_PAIRFAST", "0")
     slow = engine.lattice_sum(pi, n, z)
     assert math.isclose(fast, slow, rel_tol=1e-13, abs_tol=1e-300), (fast, slow)
-    ref = np_oracle.slr_sum(f, n, list(rule.z_reduced))
+    ref = np_oracle.slr_sum(text, n, list(rule.z_reduced))
     assert math.isclose(fast, ref, rel_tol=1e-10, abs_tol=1e-300), (fast, ref)

@@ -31,17 +31,15 @@ def test_points_overflow_guard():
                                  "expalt7", "poly_mix", "recip_sum", "sin_of_prod", "cfg1", "cfg2"])
 def test_slr_matches_reference(golden, tag):
     case = next(c for c in golden["slr"] if c["tag"] == tag)
-    f = parse(case["text"], case["d"])
     n = int(case["n"])
-    got = orc.slr_value(f, n, [int(c) for c in case["z"]])
+    got = orc.slr_value(case["text"], n, [int(c) for c in case["z"]])
     want = unhex(case["value"])
     assert abs(got - want) <= 1e-13 * max(abs(want), 1e-3), (tag, got, want)
 
 
 def test_cfg5_range_restatement(golden):
     case = next(c for c in golden["slr"] if c["tag"] == "cfg5_range_0_16384")
-    f = parse(case["text"], case["d"])
-    got = orc.slr_sum(f, int(case["n"]), [int(c) for c in case["z"]], 0, 1 << 14)
+    got = orc.slr_sum(case["text"], int(case["n"]), [int(c) for c in case["z"]], 0, 1 << 14)
     assert abs(got - unhex(case["range_sum"])) <= 1e-12 * unhex(case["range_sum"])
 
 
@@ -65,8 +63,7 @@ def test_direct_tensor_sum_matches_reference(golden):
         counts = [int(c) for c in case["counts"]]
         if math.prod(counts) > 200_000:
             continue
-        f = parse(case["text"], case["d"])
-        got = orc.direct_tensor_sum(f, orc.midpoint_nodes(counts))
+        got = orc.direct_tensor_sum(case["text"], orc.midpoint_nodes(counts))
         want = unhex(case["direct_sum"])
         assert abs(got - want) <= 1e-13 * abs(want), case["tag"]
         checked += 1
@@ -102,8 +99,7 @@ def test_mc_oracle_pinned_to_reference():
     from conftest import load_golden, unb64, unhex
     from oracle import np_oracle
     for case in load_golden("mc"):
-        f = lq.parse(case["text"], case["d"])
-        got = np_oracle.mc_value(f, case["d"], case["n"], case["seed"])
+        got = np_oracle.mc_value(case["text"], case["d"], case["n"], case["seed"])
         assert abs(got - unhex(case["value"])) <= 1e-13 * abs(unhex(case["value"])), case["tag"]
         first = unb64(case["first_rows"], case["first_shape"])
         st = np.random.default_rng(case["seed"]).bit_generator.state["state"]
@@ -114,46 +110,46 @@ def test_mc_oracle_pinned_to_reference():
 
 
 def test_oracle_eval_matches_reference_eval_on_parser_corpus():
-    """The oracle's evaluator (np_oracle.eval_array, over the product's parse)
-    against the reference's exprcore.eval frozen at three points per text of
-    the parser corpus (tests/golden/parser.json)."""
+    """The oracle's own literal evaluator (np_oracle.eval_array -> np_expr, no
+    product code) against the reference's exprcore.eval frozen at three points
+    per accepted text of the parser corpus (tests/golden/parser.json).  The
+    reference canonicalises before evaluating (angle addition, quadratic
+    expansion, constant folding), the oracle evaluates the text as written:
+    1e-10, or 1e-8 for constant texts whose huge trig arguments amplify the
+    folding order."""
     import math
-    from paper_2404_08867_b200 import expr as E
     from oracle import np_oracle
     from conftest import load_golden, unhex
     n = 0
     for case in load_golden("parser"):
         if "error" in case:
             continue
-        f = E.parse(case["text"], case["d"])
-        tol = 1e-10 if E.free_vars(f) else 1e-8
+        d = case["d"]
+        tol = 1e-10 if "x[" in case["text"] else 1e-8
         for pt, want in zip(case["points"], case["values"]):
+            if not want.startswith(("0x", "-0x", "inf", "-inf", "nan")):
+                continue   # the reference raised at this point (e.g. a zero base to a negative power)
             assign = {j + 1: np.array([unhex(v)]) for j, v in enumerate(pt)}
-            got = float(np.asarray(np_oracle.eval_array(f, assign)).reshape(-1)[0])
+            with np.errstate(all="ignore"):
+                got = float(np.asarray(np_oracle.eval_array(case["text"], d, assign)).reshape(-1)[0])
             w = unhex(want)
-            assert got == w or math.isclose(got, w, rel_tol=tol, abs_tol=1e-300), (case["text"], got, w)
+            assert got == w or math.isclose(got, w, rel_tol=tol, abs_tol=1e-300) or (math.isnan(got) and math.isnan(w)), \
+                (case["text"], got, w)
             n += 1
-    assert n > 900
+    assert n > 800
 
 
-def test_as_expr_accepts_real_latquad_expressions():
-    """The drop-in adapter on the reference's own Expr objects (build
-    container only: needs /root/reference importable)."""
-    import math
+def test_oracle_takes_text_only():
+    """The oracle shares nothing with the product front end: a product Expr is
+    refused, and nothing under oracle/ imports the product package."""
     import os
-    import sys
-    if not os.path.isdir("/root/reference/pkg/src/latquad"):
-        import pytest
-        pytest.skip("reference not importable here")
-    sys.path.insert(0, "/root/reference/pkg/src")
-    from latquad import corpus, exprcore
-    from paper_2404_08867_b200 import expr as E
-    rng = np.random.default_rng(3)
-    for entry in corpus.entries():
-        d = max(3, entry.min_d)
-        ref = exprcore.parse(entry.text, d)
-        ours = E.as_expr(ref)
-        for _ in range(3):
-            pt = {j: float(rng.random()) for j in range(1, d + 1)}
-            a, b = exprcore.eval(ref, pt), E.evaluate(ours, pt)
-            assert math.isclose(a, b, rel_tol=1e-13), (entry.id, a, b)
+    import re
+    import paper_2404_08867_b200 as lq
+    from oracle import np_oracle
+    with pytest.raises(TypeError):
+        np_oracle.eval_array(lq.parse("x[1]", 1), 1, {1: np.array([0.5])})
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "oracle")
+    for name in os.listdir(here):
+        if name.endswith(".py"):
+            src = open(os.path.join(here, name)).read()
+            assert not re.search(r"^\s*(from|import)\s+paper_2404_08867_b200", src, re.M), name
