@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define LQ_ABI_VERSION 7
+#define LQ_ABI_VERSION 8
 
 #define LQ_OK 0
 #define LQ_ERR_VALUE (-1)
@@ -178,6 +178,15 @@ int lq_tensor_sum(lq_ctx* ctx, const lq_program* prog, int32_t d, const int64_t*
 int lq_tensor_partials(lq_ctx* ctx, const lq_program* prog, int32_t d, const int64_t* counts,
                        const double* nodes, int32_t midpoint, uint64_t total, int64_t t_begin,
                        int64_t t_end, double* tiles_dev);
+
+/* ---- element-wise evaluation: replaces exprcore.eval_array
+ * (exprcore.py:442-480) on m rows, out[i] = f(x_1[i], ..., x_V[i]) in the
+ * reference's evaluation order (the bytecode of lower.compile_program).
+ * cols[b] holds the m values of variable b (b < prog->n_vars; NULL for a
+ * variable the program never reads).  The table cols is host memory; the
+ * columns and out are host memory, or device memory when on_device != 0.     */
+int lq_eval_array(lq_ctx* ctx, const lq_program* prog, const double* const* cols, int64_t m,
+                  int32_t on_device, double* out);
 
 /* ---- MDI-LR cluster sums: replaces the symbolic level loop of
  * mdi.mdi_sum (mdi.py:139-192) for separable integrands.  Factor f is a

@@ -10,10 +10,11 @@ from __future__ import annotations
 
 import cmath
 import math
+from dataclasses import dataclass
 
 from .expr import parse
 
-__all__ = ["all_ids", "corpus_expr", "reference_value", "text_of"]
+__all__ = ["CorpusEntry", "all_ids", "corpus_expr", "entries", "get", "reference_value", "text_of"]
 
 
 def _one(d):
@@ -59,6 +60,49 @@ _TABLE = {
     "invpow": ("(1 + sum(i=1..d, x[i]))^(-(d+1))", 1, lambda d: 1.0 / math.factorial(d + 1)),
     "one": ("1", 1, _one),
 }
+
+
+# benchmark families each integrand appears in (the reference's suites, bench.py)
+_SUITES = {
+    "expxy": ("test1",), "sinsq": ("test1", "test2"), "expsum": ("test2",),
+    "gaussian": ("test3", "test5", "test6", "test7"), "expalt": ("test4", "test7"),
+    "ratprod": ("test4", "test5", "test6", "test7"), "coslin": ("test5", "test6", "test7"),
+    "expsq": ("test7",), "invpow": ("test7",), "one": (),
+}
+
+
+@dataclass(frozen=True)
+class CorpusEntry:
+    """One named integrand (corpus.py:68-86): id, source text in d, exact
+    integral as a function of d, the suites it appears in, minimum d."""
+
+    id: str
+    text: str
+    reference: object
+    suites: tuple
+    min_d: int = 1
+
+    def expr(self, d):
+        if d < self.min_d:
+            raise ValueError(f"{self.id} needs d >= {self.min_d}, got {d}")
+        return parse(self.text, d)
+
+    def ref(self, d):
+        return float(self.reference(d))
+
+
+_ENTRIES = {k: CorpusEntry(k, text, fn, _SUITES[k], min_d) for k, (text, min_d, fn) in _TABLE.items()}
+
+
+def entries():
+    return list(_ENTRIES.values())
+
+
+def get(name):
+    try:
+        return _ENTRIES[name]
+    except KeyError:
+        raise KeyError(f"unknown integrand {name!r}; known: {', '.join(_TABLE)}") from None
 
 
 def all_ids():

@@ -1807,6 +1807,65 @@ int tensor_tiles(lq_ctx* c, const lq_program* pg, int32_t d, const int64_t* coun
 }
 }  // namespace
 
+int lq_eval_array(lq_ctx* c, const lq_program* pg, const double* const* cols, int64_t m, int32_t on_device,
+                  double* out) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (!pg || !pg->insn || pg->n_insn < 1) return fail(LQ_ERR_VALUE, "null program");
+    if (m < 0) return fail(LQ_ERR_VALUE, "negative row count %lld", (long long)m);
+    if (m == 0) return LQ_OK;
+    if (!out) return fail(LQ_ERR_VALUE, "null output");
+    if (pg->n_vars > 0 && !cols) return fail(LQ_ERR_VALUE, "null column table");
+    const int ns = pick_slots(pg->n_slots);
+    if (ns < 0) return fail(LQ_ERR_UNSUPPORTED, "program needs %d slots (max %d)", pg->n_slots, LQ_MAX_SLOTS);
+    // every variable the bytecode reads must have a column
+    for (int k = 0; k < pg->n_insn; ++k) {
+        const lq_insn& in = pg->insn[k];
+        if (in.op == lq::OP_VAR || in.op == lq::OP_ACC_ADDVAR) {
+            if (in.b < 0 || in.b >= pg->n_vars || !cols[in.b])
+                return fail(LQ_ERR_VALUE, "variable x[%d] has no column", in.b + 1);
+        }
+    }
+    const int V = std::max(pg->n_vars, 1);
+    const size_t bytes = sizeof(double) * (size_t)m;
+    void *dp, *dptr, *dcols = nullptr, *dout = out;
+    if ((rc = upload(c, B_PROG, pg->insn, sizeof(lq_insn) * pg->n_insn, &dp))) return rc;
+    std::vector<const double*> ptrs(V, nullptr);
+    if (on_device) {
+        for (int b = 0; b < pg->n_vars; ++b) ptrs[b] = cols[b];
+    } else {
+        // host columns: one device block, V columns of m rows (pageable copies)
+        if ((rc = dev_buf(c, B_AUX2, bytes * V, &dcols))) return rc;
+        for (int b = 0; b < pg->n_vars; ++b) {
+            if (!cols[b]) continue;
+            ptrs[b] = (const double*)dcols + (size_t)b * m;
+            CK(cudaMemcpyAsync((void*)ptrs[b], cols[b], bytes, cudaMemcpyHostToDevice, c->stream));
+            c->h2d_bytes += (int64_t)bytes;
+        }
+        if ((rc = dev_buf(c, B_OUT, bytes, &dout))) return rc;
+    }
+    if ((rc = upload(c, B_AUX3, ptrs.data(), sizeof(void*) * V, &dptr))) return rc;
+    const int64_t blocks = (m + lq::kThreads - 1) / lq::kThreads;
+    const void* kern = ns == 32 ? (const void*)lq::k_prog_eval<32> : (const void*)lq::k_prog_eval<LQ_MAX_SLOTS>;
+    const int grid = grid_for(c, kern, blocks);
+    t_begin(c);
+    if (ns == 32)
+        lq::k_prog_eval<32><<<grid, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, pg->n_insn, pg->result,
+                                                                  (const double* const*)dptr, m, (double*)dout);
+    else
+        lq::k_prog_eval<LQ_MAX_SLOTS><<<grid, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, pg->n_insn, pg->result,
+                                                                            (const double* const*)dptr, m, (double*)dout);
+    t_end(c);
+    CK(cudaGetLastError());
+    if (!on_device) {
+        CK(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, c->stream));
+        c->d2h_bytes += (int64_t)bytes;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    c->hoff = 0;
+    return LQ_OK;
+}
+
 int lq_tensor_sum(lq_ctx* c, const lq_program* pg, int32_t d, const int64_t* counts, const double* nodes,
                   int32_t midpoint, uint64_t s_begin, uint64_t s_end, double* sum_out) {
     if (!sum_out) return fail(LQ_ERR_VALUE, "null output");

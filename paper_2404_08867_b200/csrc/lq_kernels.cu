@@ -1382,6 +1382,26 @@ __global__ void __launch_bounds__(kThreads) k_prog_tensor(const lq_insn* __restr
     }
 }
 
+// ============================================================ element-wise
+// eval_array (exprcore.py:442-480): one row per thread, grid-stride; variable
+// b of row i is cols[b][i] (coalesced across the warp)
+struct ColSrc {
+    const double* const* __restrict__ cols;
+    int64_t i;
+    __device__ __forceinline__ double x(int b) const { return __ldg(cols[b] + i); }
+};
+
+template <int NS>
+__global__ void __launch_bounds__(kThreads) k_prog_eval(const lq_insn* __restrict__ prog, int n_insn, int result,
+                                                        const double* const* __restrict__ cols, int64_t m,
+                                                        double* __restrict__ out) {
+    double slot[NS];
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < m; i += (int64_t)gridDim.x * kThreads) {
+        ColSrc src{cols, i};
+        out[i] = run_program<NS>(prog, n_insn, result, src, slot);
+    }
+}
+
 __global__ void k_midpoint_nodes(const int64_t* __restrict__ counts, const int64_t* __restrict__ off, int d,
                                  double* __restrict__ nodes) {
     // nodes of axis k: RN((t + 0.5) / n_k), transform.py:177

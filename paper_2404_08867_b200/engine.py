@@ -14,10 +14,10 @@ from collections import OrderedDict
 import numpy as np
 
 from . import _native as N
-from .expr import Expr, as_expr, free_vars
+from .expr import Expr, UnassignedVariableError, as_expr, evaluate, free_vars
 from .lower import Program, compile_program, linear_outer, recognize_linear_program, recognize_plain, separate
 
-__all__ = ["PlainIntegrand", "plain_integrand", "lattice_sum", "tensor_program", "SeparablePlan",
+__all__ = ["PlainIntegrand", "plain_integrand", "lattice_sum", "tensor_program", "eval_array", "SeparablePlan",
            "separable_plan", "mdi_separable_sum"]
 
 
@@ -175,6 +175,38 @@ def tensor_sum(g, grids, s_begin=0, s_end=None, comm=None):
     N.check(N.lib().lq_tensor_sum(N.ctx(), C.byref(p), d, N.as_ptr(counts), N.as_ptr(nodes), mid,
                                   int(s_begin), int(s_end), C.byref(out)))
     return out.value
+
+
+def eval_array(g, assignment):
+    """exprcore.eval_array (exprcore.py:442-480) on the GPU: the values of g
+    with x[j] = assignment[j] (numpy arrays broadcast together, or scalars),
+    evaluated row by row by the bytecode interpreter (k_prog_eval) in the
+    reference's evaluation order.  A constant g returns its float value, as
+    the reference does; a missing coordinate raises UnassignedVariableError."""
+    e = as_expr(g)
+    fv = sorted(free_vars(e))
+    if not fv:
+        return evaluate(e, {})
+    cols = []
+    for j in fv:
+        if j not in assignment:
+            raise UnassignedVariableError(j)
+        cols.append(np.asarray(assignment[j], dtype=np.float64))
+    shaped = np.broadcast_arrays(*cols)
+    shape = shaped[0].shape
+    m = int(np.prod(shape)) if shape else 1
+    out = np.empty(m, dtype=np.float64)
+    if m == 0:
+        return out.reshape(shape)
+    prog = tensor_program(e)
+    ins = np.ascontiguousarray(prog.insn)
+    p = N.Program(ins.ctypes.data, len(ins), prog.n_slots, prog.result, prog.n_vars, None)
+    flat = {j: np.ascontiguousarray(a.reshape(-1)) for j, a in zip(fv, shaped)}
+    table = (C.c_void_p * max(prog.n_vars, 1))()
+    for j, a in flat.items():
+        table[j - 1] = a.ctypes.data
+    N.check(N.lib().lq_eval_array(N.ctx(), C.byref(p), table, m, 0, out.ctypes.data))
+    return out.reshape(shape) if shape else float(out[0])
 
 
 # ------------------------------------------------------------------ MDI-LR

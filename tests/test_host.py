@@ -400,3 +400,31 @@ def test_jit_policy_refuses_long_programs(monkeypatch):
     assert jit.jit_wanted(1.0, 10**6)
     monkeypatch.setenv("LQ_JIT", "0")
     assert not jit.jit_wanted(1e15, 10)
+
+
+# names of latquad.__all__ deliberately not provided: the symbolic algebra and
+# the transform validation path (SURVEY §2 / DESIGN §8: never on the value path)
+OUT_OF_SCOPE = {"bind", "partial_sum", "substitute", "NonCartesianStructureError", "TransformedIntegrand",
+                "build_axis_grids", "forward_transform", "grid_completion", "inverse_substitution",
+                "make_transformed_integrand"}
+
+
+def test_top_level_api_covers_the_reference_exports():
+    """A drop-in user's `from latquad import X` works for every value-path name
+    the reference exports (/root/reference/pkg/src/latquad/__init__.py)."""
+    src = "/root/reference/pkg/src"
+    if not os.path.isdir(os.path.join(src, "latquad")):
+        pytest.skip("reference not importable here")
+    import sys
+    sys.path.insert(0, src)
+    try:
+        import latquad
+    finally:
+        sys.path.remove(src)
+    missing = sorted(set(latquad.__all__) - OUT_OF_SCOPE - set(dir(lq)))
+    assert not missing, missing
+    assert set(lq.__all__) >= set(latquad.__all__) - OUT_OF_SCOPE
+    e = lq.get("invpow")
+    assert e.ref(4) == latquad.get("invpow").ref(4) and e.suites == latquad.get("invpow").suites
+    assert [x.id for x in lq.entries()] == [x.id for x in latquad.entries()]
+    assert lq.eval(lq.parse("exp(1) + 2*pi", 1), {}) == latquad.eval(latquad.parse("exp(1) + 2*pi", 1), {})
