@@ -79,6 +79,73 @@ __device__ __forceinline__ double block_sum(double v, double* sh /* >= 8 */) {
     return v;
 }
 
+// ------------------------------------------------ exact (order-free) sums
+// A 192-bit two's-complement fixed-point accumulator with 2^-S resolution:
+// every term is truncated to the grid once (deterministically), after which
+// integer addition is associative, so the sum is the same for any order of
+// the terms -- a permutation of the points, a reflected or inverted lattice
+// (the reference sorts its terms for the same purpose, lattice.py:236-239)
+// -- and for any tiling, block shape or rank count.  The host picks S so that
+// n * max|term| < 2^188 (fix_scale) and rounds the result once (fix_to_double).
+struct Fix3 {
+    uint64_t w0, w1, w2;   // little-endian limbs
+};
+
+__device__ __forceinline__ Fix3 fix_zero() { return Fix3{0ull, 0ull, 0ull}; }
+
+__device__ __forceinline__ void fix_add(Fix3& a, const Fix3& b) {
+    asm("add.cc.u64 %0, %0, %3;\n\t"
+        "addc.cc.u64 %1, %1, %4;\n\t"
+        "addc.u64 %2, %2, %5;"
+        : "+l"(a.w0), "+l"(a.w1), "+l"(a.w2)
+        : "l"(b.w0), "l"(b.w1), "l"(b.w2));
+}
+
+// v * 2^S truncated toward zero, as 192-bit two's complement
+__device__ __forceinline__ Fix3 fix_of(double v, int S) {
+    const uint64_t bits = (uint64_t)__double_as_longlong(v);
+    const int ex = (int)((bits >> 52) & 0x7ff);
+    uint64_t m = bits & 0xfffffffffffffull;
+    int sh;                                   // v = m 2^(sh - S) after the next two lines
+    if (ex == 0) sh = -1074 + S;
+    else { m |= 1ull << 52; sh = ex - 1075 + S; }
+    Fix3 t = fix_zero();
+    if (ex == 0x7ff || m == 0) return t;      // inf/nan never occur (finite products); zero
+    if (sh < 0) {
+        m = sh <= -64 ? 0ull : m >> -sh;
+        sh = 0;
+    }
+    const int limb = sh >> 6, off = sh & 63;
+    const uint64_t lo = m << off, hi = off ? m >> (64 - off) : 0ull;
+    if (limb == 0) { t.w0 = lo; t.w1 = hi; }
+    else if (limb == 1) { t.w1 = lo; t.w2 = hi; }
+    else { t.w2 = lo; }
+    if (bits >> 63) {                         // negate: ~t + 1
+        t.w0 = ~t.w0; t.w1 = ~t.w1; t.w2 = ~t.w2;
+        fix_add(t, Fix3{1ull, 0ull, 0ull});
+    }
+    return t;
+}
+
+__device__ __forceinline__ Fix3 fix_shfl_xor(const Fix3& a, int o) {
+    return Fix3{__shfl_xor_sync(0xffffffffu, a.w0, o), __shfl_xor_sync(0xffffffffu, a.w1, o),
+                __shfl_xor_sync(0xffffffffu, a.w2, o)};
+}
+
+// CTA sum of a Fix3 (NT threads); the result is valid in thread 0
+template <int NT>
+__device__ __forceinline__ Fix3 fix_block_sum(Fix3 a, Fix3* sh /* >= NT / 32 */) {
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) fix_add(a, fix_shfl_xor(a, o));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[warp] = a;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int w = 1; w < NT / 32; ++w) fix_add(a, sh[w]);
+    return a;
+}
+
 // ----------------------------------------------------------- interpreter
 
 enum : int32_t {

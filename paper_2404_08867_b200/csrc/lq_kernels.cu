@@ -1773,11 +1773,13 @@ struct QDim {
 
 // sum over points of prod_j (1 + g_j (B_alpha(x_j) + beta)), x_j = RN(r/n)
 // exactly: shift_avg_wce_sq (lattice.py:225-245) and p_alpha (:167-181).
+// Each product is added to an exact fixed-point tile sum (Fix3, scale 2^S),
+// so the total does not depend on the order of the points.
 template <int ALPHA>
 __global__ void __launch_bounds__(kThreads) k_bprod(const QDim* __restrict__ dims, int d, uint32_t n, double n_d,
-                                                    double inv_n, double beta, uint64_t base, uint64_t end,
-                                                    double* __restrict__ tile_out) {
-    __shared__ double sh[8];
+                                                    double inv_n, double beta, uint64_t base, uint64_t end, int S,
+                                                    Fix3* __restrict__ tile_out) {
+    __shared__ Fix3 sh[8];
     const uint64_t i0_64 = base + (uint64_t)blockIdx.x * kTile + (uint64_t)threadIdx.x * kPts;
     const uint32_t i0 = (uint32_t)i0_64;
     double prod[kPts];
@@ -1795,11 +1797,22 @@ __global__ void __launch_bounds__(kThreads) k_bprod(const QDim* __restrict__ dim
             r = step_mod(r, dm.z, zm);
         }
     }
-    double s = 0.0;
+    Fix3 acc = fix_zero();
     #pragma unroll
-    for (int p = 0; p < kPts; ++p) s += (i0_64 + p < end) ? prod[p] : 0.0;
-    s = block_sum(s, sh);
-    if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
+    for (int p = 0; p < kPts; ++p)
+        if (i0_64 + p < end) fix_add(acc, fix_of(prod[p], S));
+    acc = fix_block_sum<kThreads>(acc, sh);
+    if (threadIdx.x == 0) tile_out[blockIdx.x] = acc;
+}
+
+// exact sum of count Fix3 partials (one CTA; integer addition, any order)
+__global__ void __launch_bounds__(kThreads) k_fix_reduce(const Fix3* __restrict__ in, int64_t count,
+                                                         Fix3* __restrict__ out) {
+    __shared__ Fix3 sh[8];
+    Fix3 acc = fix_zero();
+    for (int64_t i = threadIdx.x; i < count; i += kThreads) fix_add(acc, in[i]);
+    acc = fix_block_sum<kThreads>(acc, sh);
+    if (threadIdx.x == 0) out[0] = acc;
 }
 
 // B2 of every residue: b2[r] = B2(RN(r/n)), as bernoulli_poly(np.arange(n)/n, 2)
@@ -1817,15 +1830,18 @@ __global__ void k_cbc_init(uint32_t n, const double* __restrict__ b2, double g, 
 }
 
 // CBC candidate sweep (lattice.py:280-287): for every candidate c,
-// val[c] = sum_k base[k] * (1 + g (b2[(k c) mod n] + beta)).  Persistent CTAs
-// hold the B2 table in shared memory when it fits and walk the candidates.
+// val[c] = sum_k base[k] * (1 + g (b2[(k c) mod n] + beta)), summed exactly
+// (Fix3, scale 2^S): reflected candidates, whose terms are a permutation of
+// each other, tie exactly (the reference sorts its terms for this,
+// lattice.py:284).  Persistent CTAs hold the B2 table in shared memory when
+// it fits and walk the candidates.
 template <bool SMEM>
 __global__ void __launch_bounds__(kThreads) k_cbc_eval(uint32_t n, const double* __restrict__ b2g,
                                                        const double* __restrict__ basev, double g, double beta,
-                                                       const int64_t* __restrict__ cands, int64_t ncand,
-                                                       double* __restrict__ vals) {
+                                                       const int64_t* __restrict__ cands, int64_t ncand, int S,
+                                                       Fix3* __restrict__ vals) {
     extern __shared__ double b2s[];
-    __shared__ double sh[8];
+    __shared__ Fix3 sh[8];
     const double* b2 = b2g;
     if (SMEM) {
         for (uint32_t r = threadIdx.x; r < n; r += kThreads) b2s[r] = b2g[r];
@@ -1836,13 +1852,13 @@ __global__ void __launch_bounds__(kThreads) k_cbc_eval(uint32_t n, const double*
         const uint32_t c = (uint32_t)cands[ci];
         const uint32_t step = (uint32_t)(((uint64_t)c * kThreads) % n), stepm = step - n;
         uint32_t r = (uint32_t)(((uint64_t)threadIdx.x * c) % n);
-        double s = 0.0;
+        Fix3 acc = fix_zero();
         for (uint32_t k = threadIdx.x; k < n; k += kThreads) {
-            s += __dmul_rn(basev[k], bfactor(b2[r], g, beta));
+            fix_add(acc, fix_of(__dmul_rn(basev[k], bfactor(b2[r], g, beta)), S));
             r = step_mod(r, step, stepm);
         }
-        s = block_sum(s, sh);
-        if (threadIdx.x == 0) vals[ci] = s;
+        acc = fix_block_sum<kThreads>(acc, sh);
+        if (threadIdx.x == 0) vals[ci] = acc;
     }
 }
 
@@ -1855,15 +1871,15 @@ __global__ void k_cbc_update(uint32_t n, const double* __restrict__ b2, double g
 }
 
 // Korobov search (lattice.py:292-311): for every candidate a, sum over points
-// k of prod_j (1 + g_j (b2[k a^j mod n] + beta)); residues advance along j by
-// a Shoup modmul with the candidate's constant.
+// k of prod_j (1 + g_j (b2[k a^j mod n] + beta)), exact (Fix3, scale 2^S);
+// residues advance along j by a Shoup modmul with the candidate's constant.
 template <bool SMEM>
 __global__ void __launch_bounds__(kThreads) k_korobov(uint32_t n, int d, const double* __restrict__ b2g,
                                                       const double* __restrict__ gam, double beta,
-                                                      const int64_t* __restrict__ cands, int64_t ncand,
-                                                      double* __restrict__ vals) {
+                                                      const int64_t* __restrict__ cands, int64_t ncand, int S,
+                                                      Fix3* __restrict__ vals) {
     extern __shared__ double b2s[];
-    __shared__ double sh[8];
+    __shared__ Fix3 sh[8];
     const double* b2 = b2g;
     if (SMEM) {
         for (uint32_t r = threadIdx.x; r < n; r += kThreads) b2s[r] = b2g[r];
@@ -1873,7 +1889,7 @@ __global__ void __launch_bounds__(kThreads) k_korobov(uint32_t n, int d, const d
     for (int64_t ci = blockIdx.x; ci < ncand; ci += gridDim.x) {
         const uint32_t a = (uint32_t)(cands[ci] % n);
         const uint32_t as = (uint32_t)(((uint64_t)a << 32) / n);
-        double s = 0.0;
+        Fix3 acc = fix_zero();
         for (uint32_t k = threadIdx.x; k < n; k += kThreads) {
             uint32_t r = k;
             double prod = 1.0;
@@ -1881,10 +1897,10 @@ __global__ void __launch_bounds__(kThreads) k_korobov(uint32_t n, int d, const d
                 prod = __dmul_rn(prod, bfactor(b2[r], __ldg(gam + j), beta));
                 r = mulmod_shoup(r, a, as, n);
             }
-            s += prod;
+            fix_add(acc, fix_of(prod, S));
         }
-        s = block_sum(s, sh);
-        if (threadIdx.x == 0) vals[ci] = s;
+        acc = fix_block_sum<kThreads>(acc, sh);
+        if (threadIdx.x == 0) vals[ci] = acc;
     }
 }
 

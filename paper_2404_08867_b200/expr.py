@@ -20,6 +20,7 @@ like-term merging) keeps that analysis simple.
 from __future__ import annotations
 
 import math
+import weakref
 import re
 
 __all__ = [
@@ -48,7 +49,7 @@ class Expr:
     'exp', 'sin', 'cos', 'abs' (args = (arg,)).
     """
 
-    __slots__ = ("op", "val", "idx", "args", "terms", "_key", "_hash", "_fv", "_fvb")
+    __slots__ = ("op", "val", "idx", "args", "terms", "_key", "_hash", "_fv", "_fvb", "__weakref__")
 
     def __init__(self, op, val=0.0, idx=0, args=(), terms=()):
         self.op = op
@@ -97,6 +98,26 @@ class Expr:
     def __pow__(self, k):
         return power(self, int(k))
 
+    # latquad's field names (exprcore.py:80-91), read-only views of this node
+    # for callers that inspect a parsed expression
+    @property
+    def kind(self):
+        return {"add": "sum", "mul": "prod"}.get(self.op, self.op)
+
+    @property
+    def value(self):
+        return self.val
+
+    @property
+    def index(self):
+        return self.idx
+
+    @property
+    def children(self):
+        if self.op == "add":
+            return tuple((t, c) for c, t in self.terms)
+        return self.args
+
 
 def _lift(o):
     return o if isinstance(o, Expr) else const(o)
@@ -104,14 +125,24 @@ def _lift(o):
 
 # ------------------------------------------------------------------ factories
 
+# One live object per distinct node (the reference hash-conses its DAG the
+# same way, exprcore.py:94-106, and callers may rely on `parse(t) is parse(t)`)
+_INTERN = weakref.WeakValueDictionary()
+
+
+def _node(op, val=0.0, idx=0, args=(), terms=()):
+    e = Expr(op, val, idx, args, terms)
+    return _INTERN.setdefault(e._key, e)
+
+
 def const(v):
-    return Expr("const", float(v))
+    return _node("const", float(v))
 
 
 def var(i):
     if int(i) < 1:
         raise ValueError(f"variable index must be >= 1, got {i}")
-    return Expr("var", idx=int(i))
+    return _node("var", idx=int(i))
 
 
 def add(pairs, constant=0.0):
@@ -149,7 +180,7 @@ def add(pairs, constant=0.0):
     if len(items) == 1 and constant == 0.0:
         c, t = items[0]
         return t if c == 1.0 else mul(c, [t])
-    return Expr("add", constant, terms=items)
+    return _node("add", constant, terms=items)
 
 
 def mul(coef, factors):
@@ -196,7 +227,7 @@ def mul(coef, factors):
             return f
         if f.op == "add":  # distribute a scalar over a lone sum (exprcore.py:198-202)
             return add([(coef * c, t) for c, t in f.terms], coef * f.val)
-    return Expr("mul", coef, args=out)
+    return _node("mul", coef, args=out)
 
 
 def power(base, k):
@@ -212,7 +243,7 @@ def power(base, k):
     if base.op == "mul":
         c = base.val ** k if k > 0 else 1.0 / (base.val ** -k)
         return mul(c, [power(f, k) for f in base.args])
-    return Expr("pow", idx=k, args=(base,))
+    return _node("pow", idx=k, args=(base,))
 
 
 def func(name, arg):
@@ -221,7 +252,7 @@ def func(name, arg):
     if arg.op == "const":
         v = arg.val
         return const({"exp": math.exp, "sin": math.sin, "cos": math.cos, "abs": abs}[name](v))
-    return Expr(name, args=(arg,))
+    return _node(name, args=(arg,))
 
 
 # -------------------------------------------------------------------- queries
@@ -301,26 +332,47 @@ def evaluate(e, assignment):
     return float(vals[e])
 
 
+def _num(v):
+    """Integers without a fraction part, anything else as repr (exprcore.py:778-781)."""
+    return str(int(v)) if v == int(v) and abs(v) < 1e15 else repr(v)
+
+
 def to_text(e, maxlen=None):
-    def r(n):
+    """Readable rendering for diagnostics, in latquad's conventions
+    (exprcore.py:771-818): variables as x1, powers b^k, a product's
+    coefficient in front, sums joined by + / -, parentheses by precedence
+    (0 sum, 1 product, 2 atom).  Not meant to be parsed back."""
+    def atom(n):
+        return n.op not in ("add", "mul")
+
+    def r(n, prec):
         op = n.op
         if op == "const":
-            return repr(n.val)
+            return _num(n.val)
         if op == "var":
-            return f"x[{n.idx}]"
-        if op == "add":
-            parts = [f"{c!r}*{r(t)}" if c != 1.0 else r(t) for c, t in n.terms]
-            if n.val != 0.0:
-                parts.append(repr(n.val))
-            return "(" + " + ".join(parts) + ")"
-        if op == "mul":
-            body = "*".join(r(f) for f in n.args)
-            return body if n.val == 1.0 else f"{n.val!r}*{body}"
+            return f"x{n.idx}"
         if op == "pow":
-            return f"{r(n.args[0])}^({n.idx})"
-        return f"{op}({r(n.args[0])})"
+            b = r(n.args[0], 2)
+            if not atom(n.args[0]):
+                b = f"({b})"
+            return f"{b}^{n.idx}" if n.idx != -1 else f"{b}^-1"
+        if op == "mul":
+            body = "*".join(r(f, 2) if f.op != "add" else f"({r(f, 0)})" for f in n.args)
+            if n.val != 1.0:
+                body = f"{_num(n.val)}*{body}"
+            return f"({body})" if prec > 1 else body
+        if op == "add":
+            parts = []
+            for c, t in n.terms:
+                rt = r(t, 1)
+                parts.append(rt if c == 1.0 else f"-{rt}" if c == -1.0 else f"{_num(c)}*{rt}")
+            if n.val != 0.0 or not parts:
+                parts.append(_num(n.val))
+            body = " + ".join(parts).replace("+ -", "- ")
+            return f"({body})" if prec > 0 else body
+        return f"{op}({r(n.args[0], 0)})"
 
-    s = r(e)
+    s = r(e, 0)
     if maxlen is not None and len(s) > maxlen:
         s = s[: maxlen - 3] + "..."
     return s

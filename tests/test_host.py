@@ -428,3 +428,29 @@ def test_top_level_api_covers_the_reference_exports():
     assert e.ref(4) == latquad.get("invpow").ref(4) and e.suites == latquad.get("invpow").suites
     assert [x.id for x in lq.entries()] == [x.id for x in latquad.entries()]
     assert lq.eval(lq.parse("exp(1) + 2*pi", 1), {}) == latquad.eval(latquad.parse("exp(1) + 2*pi", 1), {})
+
+
+def test_reference_import_shim_resolves():
+    """tools/refcompat/latquad (the shim that runs the reference's own test
+    suite against this package, tools/run_reference_tests.py) imports every
+    submodule the reference's tests use, without a GPU."""
+    import importlib
+    import sys
+    shim = os.path.join(REPO, "tools", "refcompat")
+    saved = {k: sys.modules.pop(k) for k in [k for k in sys.modules if k == "latquad" or k.startswith("latquad.")]}
+    sys.path.insert(0, shim)
+    try:
+        for name in ("latquad", "latquad.exprcore", "latquad.lattice", "latquad.quad", "latquad.mdi",
+                     "latquad.transform", "latquad.corpus", "latquad.bench", "latquad.cli"):
+            importlib.import_module(name)
+        import latquad
+        assert latquad.slr_integrate is lq.slr_integrate
+        from latquad.exprcore import make_sum, parse, var
+        e = make_sum([(var(1), 2.0), (var(2), 1.0)], 0.5)
+        assert e is parse("2*x[1] + x[2] + 0.5", 2)
+        assert e.kind == "sum" and e.value == 0.5 and len(e.children) == 2
+    finally:
+        sys.path.remove(shim)
+        for k in [k for k in sys.modules if k == "latquad" or k.startswith("latquad.")]:
+            del sys.modules[k]
+        sys.modules.update(saved)
