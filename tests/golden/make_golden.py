@@ -463,6 +463,114 @@ def parser_cases():
     return out
 
 
+def _family_texts(rng):
+    """Random members of the closed families the plain-sum kernels recognise
+    (linear-form exp / cos / sin / integer powers, diagonal quadratics, shifted
+    quadratic products), written in the reference grammar."""
+    out = []
+    for d in (3, 8, 20, 40):
+        for kind in ("exp", "cos", "sin", "pow", "quad", "prodq"):
+            c = [round(rng.uniform(-1.5, 1.5) / max(1.0, d / 8), 6) for _ in range(d)]
+            lin = " + ".join(f"{cj!r}*x[{j + 1}]" for j, cj in enumerate(c))
+            a0 = round(rng.uniform(-1, 1), 4)
+            if kind == "exp":
+                t = f"exp({a0!r} + {lin})"
+            elif kind in ("cos", "sin"):
+                t = f"{round(rng.uniform(0.5, 2), 3)!r}*{kind}({a0!r} + {lin})"
+            elif kind == "pow":
+                k = rng.choice([-3, -2, -1, 2, 3])
+                t = f"(2.5 + {lin})^({k})"
+            elif kind == "quad":
+                q = " + ".join(f"{round(rng.uniform(-1, 0.3) / max(1.0, d / 8), 6)!r}*x[{j + 1}]^2" for j in range(d))
+                t = f"exp({lin} + {q})"
+            else:
+                t = "prod(i=1..d, 1/(0.8 + (x[i] - 0.4)^2))" if d <= 8 else \
+                    " * ".join(f"(({round(rng.uniform(0.5, 2), 3)!r} + (x[{j + 1}] - {round(rng.uniform(0, 1), 3)!r})^2)^(-1))"
+                               for j in range(min(d, 12)))
+            out.append((t, d))
+    return out
+
+
+def slr_fuzz_cases():
+    """slr_integrate of the reference (quad.py:96-104) for every accepted text
+    of the parser corpus (parser.json) and for random members of the closed
+    families, on Korobov rules over primes (the orbit and FFT-form layouts),
+    over n = 2^12 (lattice-sequence levels) and a composite n, and on a random
+    non-Korobov z: the GPU's family recognition, bytecode and kernels against
+    the reference's full sums.  `scale` = mean |f| over the same points (the
+    abs tolerance for sums that cancel)."""
+    import random
+    rng = random.Random(8867)
+    with open(os.path.join(HERE, "parser.json")) as fh:
+        parsed = [c for c in json.load(fh)["cases"] if "error" not in c]
+    texts = [(c["text"], c["d"]) for c in parsed] + _family_texts(rng)
+    out = []
+    for i, (text, d) in enumerate(texts):
+        try:
+            f = exprcore.parse(text, d)
+        except Exception:
+            continue
+        if not exprcore.free_vars(f):
+            continue
+        lats = [("korobov", 4099 if d <= 8 else 10007), ("korobov", 4096), ("korobov", 3003), ("random", 2039)]
+        for kind, n in lats[i % 2: i % 2 + 3]:
+            if kind == "korobov":
+                a = rng.randrange(2, n)
+                while math.gcd(a, n) != 1:
+                    a = rng.randrange(2, n)
+                rule = korobov_vector(a, n, d)
+            else:
+                rule = LatticeRule(n, tuple([1] + [rng.randrange(1, n) for _ in range(d - 1)]))
+            with np.errstate(all="ignore"):
+                try:
+                    val = slr_integrate(f, rule).value
+                except Exception:
+                    continue
+                pts = points_block(rule, 0, n)
+                vals = exprcore.eval_array(f, {j + 1: pts[:, j] for j in range(d)})
+                scale = float(np.mean(np.abs(vals))) if np.ndim(vals) else abs(float(vals))
+            if not (math.isfinite(val) and math.isfinite(scale)):
+                continue
+            out.append({"text": text, "d": d, "n": n, "z": [str(v) for v in rule.z], "kind": kind,
+                        "value": hx(val), "scale": hx(scale)})
+    # the closed families on prime n >= 2^18, where the orbit (direct) and
+    # FFT-form (d >= 49 at n >= 2^22) layouts take the full lattice
+    for (text, d), n in zip(_family_texts_big(rng), _BIG_N * 100):
+        a = rng.randrange(2, n)
+        rule = korobov_vector(a, n, d)
+        f = exprcore.parse(text, d)
+        val = slr_integrate(f, rule).value
+        acc = 0.0
+        for start in range(0, n, 1 << 18):
+            pts = points_block(rule, start, min(n, start + (1 << 18)))
+            acc += float(np.sum(np.abs(exprcore.eval_array(f, {j + 1: pts[:, j] for j in range(d)}))))
+        out.append({"text": text, "d": d, "n": n, "z": [str(v) for v in rule.z], "kind": "korobov_big",
+                    "value": hx(val), "scale": hx(acc / n)})
+    return out
+
+
+_BIG_N = [262147, 1048583, 4194319]
+
+
+def _family_texts_big(rng):
+    out = []
+    for d in (8, 40, 64, 100):
+        for kind in ("exp", "cos", "sin", "pow", "quad"):
+            c = [round(rng.uniform(0.0, 1.0) * 3.0 / d, 6) for _ in range(d)]
+            lin = " + ".join(f"{cj!r}*x[{j + 1}]" for j, cj in enumerate(c))
+            if kind == "exp":
+                t = f"exp(-0.5 + {lin})"
+            elif kind in ("cos", "sin"):
+                t = f"{kind}(0.25 + {lin})"
+            elif kind == "pow":
+                t = f"(1.5 + {lin})^(-2)"
+            else:
+                q = " + ".join(f"{round(-rng.uniform(0.0, 1.0) * 3.0 / d, 6)!r}*x[{j + 1}]^2" for j in range(d))
+                t = f"exp({lin} + {q})"
+            out.append((t, d))
+    return out
+
+
 def suite7_cases():
     """Suite test7 (bench.py:140-143: MDI-LR over d at n = 8^d + 1, a = 8) rows
     with d <= 10 from the reference's own row runner: expalt, ratprod,
@@ -554,7 +662,7 @@ def cfg5_full_case(procs):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
-    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites", "cfg5_full", "linform", "fft", "parser", "suites7", "subgrid"],
+    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites", "cfg5_full", "linform", "fft", "parser", "suites7", "subgrid", "slr_fuzz"],
                     default=None)
     ap.add_argument("--procs", type=int, default=os.cpu_count())
     ap.add_argument("--only-new", action="store_true", help="fft: compute only cases missing from fft.json")
@@ -565,7 +673,8 @@ def main():
             "mdi": lambda: mdi_cases(args.skip_slow), "quality": quality_cases, "mc": mc_cases,
             "suites": suite_cases, "cfg5_full": lambda: cfg5_full_case(args.procs),
             "linform": lambda: linform_cases(args.skip_slow), "fft": lambda: fft_cases_job(args.procs, args.only_new),
-            "parser": parser_cases, "suites7": suite7_cases, "subgrid": subgrid_cases}
+            "parser": parser_cases, "suites7": suite7_cases, "subgrid": subgrid_cases,
+            "slr_fuzz": slr_fuzz_cases}
     for name, fn in jobs.items():
         if args.only != name and (args.only or name in ("cfg5_full", "linform", "fft", "suites7")):
             continue
