@@ -31,7 +31,7 @@ import numpy as np
 
 from . import engine
 from ._fp import blocked_const_sum, repeated_add
-from .expr import as_expr, evaluate, free_vars, var_bounds
+from .expr import as_expr, evaluate, free_vars, node_count, var_bounds
 from .lattice import korobov_vector
 from .transform import AxisGridSet, midpoint_grids
 
@@ -207,12 +207,17 @@ def mdi_sum(g, grids, cfg=None, comm=None):
         rep = _subgrid(e, grids, counts, levels, base_axes, cfg, t0, comm)
         if rep is not None:
             return rep
-        if cfg.fallback == "error":
+        bounds = _level_bounds(e, counts, levels, base_axes, cfg)
+        if bounds is None and cfg.fallback == "error":
             raise BudgetExceededError("integrand is not separable over the grid axes "
                                       f"(budget {cfg.budget}); no level reduction possible")
         value = direct_tensor_sum(e, grids, cap=cfg.direct_cap, comm=comm)
-        return MdiReport(value=value, levels=0, base_dim=d, base_seconds=time.perf_counter() - t0,
-                         fallback=True, log_raw=math.log(abs(value)) if value else -math.inf,
+        certified = bounds is not None
+        return MdiReport(value=value, levels=levels if certified else 0,
+                         base_dim=len(base_axes) if certified else d,
+                         level_nodes=bounds if certified else (), level_seconds=(0.0,) * len(bounds or ()),
+                         base_seconds=time.perf_counter() - t0, fallback=not certified,
+                         log_raw=math.log(abs(value)) if value else -math.inf,
                          sign=math.copysign(1.0, value) if value else 0.0, method="direct")
 
     base_total = math.prod(counts[a - 1] for a in base_axes)
@@ -226,6 +231,32 @@ def mdi_sum(g, grids, cfg=None, comm=None):
                      level_nodes=(plan.n_factors,) * levels, level_seconds=(0.0,) * levels,
                      base_seconds=secs, fallback=False, log_raw=log_raw, sign=sign,
                      method="separable" if pure else "cores", clusters=plan.n_factors)
+
+
+def _level_bounds(e, counts, levels, base_axes, cfg):
+    """Upper bounds on the DAG sizes the reference's levels reach for e
+    (mdi.py:152-165): a partial sum over N nodes is one sum of N bound copies
+    of the carried expression (exprcore.py:390-402), so a level multiplies the
+    node count by at most N and adds the sum node; e's own count is taken
+    twice over (plus slack) for the difference between the two canonical
+    forms.  The tuple, when every bound stays within cfg.budget -- then the
+    reference certainly completes its levels (no fallback, no
+    BudgetExceededError) and its value is the full grid sum the direct sweep
+    computes; else None (the reference may fall back, as reported)."""
+    if levels == 0:
+        return ()
+    stripped = [a for a in range(1, len(counts) + 1) if a not in base_axes]
+    if cfg.order == "forward":
+        stripped = stripped[::-1]
+    nc = 2 * node_count(e) + 8
+    out = []
+    for lev in range(levels):
+        for a in stripped[lev * cfg.m:(lev + 1) * cfg.m]:
+            nc = counts[a - 1] * nc + 1
+        if nc > cfg.budget:
+            return None
+        out.append(nc)
+    return tuple(out)
 
 
 def _subgrid(e, grids, counts, levels, base_axes, cfg, t0, comm=None):

@@ -549,6 +549,53 @@ def slr_fuzz_cases():
     return out
 
 
+def mdi_fuzz_cases():
+    """mdi_lr of the reference (mdi.py:215-234) for every accepted text of the
+    parser corpus with coordinates, on Korobov grids N^d (+1) with N = 3, 4 and
+    d = the text's own 3/4 and 6 (two levels): value, report fields, or the
+    exception type.  `scale` = mean |f| over the midpoint grid (numpy)."""
+    import itertools
+    with open(os.path.join(HERE, "parser.json")) as fh:
+        parsed = [c for c in json.load(fh)["cases"] if "error" not in c]
+    # integrands with a factor spanning more than three axes (no separation,
+    # no single linear form: the direct-sweep branch here)
+    parsed = parsed + [{"text": t, "d": 4} for t in (
+        "exp(x[1]*x[2]*x[3]*x[4])", "1/(1 + x[1]*x[2]*x[3]*x[4])", "sin(x[1]*x[2]*x[3] + x[4])*x[2]",
+        "exp(-(x[1] - x[2])^2 - (x[3] - x[4])^2 - x[1]*x[4])", "(1 + x[1]*x[2] + x[3]*x[4])^(-2)",
+        "cos(x[1] + x[2]*x[3]*x[4]) + exp(x[1]*x[2]*x[3]*x[4])")]
+    out = []
+    for i, c in enumerate(parsed):
+        text = c["text"]
+        for d, a, extra in ((c["d"], 3 + i % 2, 1), (6, 3, i % 2)):
+            n = a ** d + extra
+            try:
+                f = exprcore.parse(text, d)
+            except Exception:
+                continue
+            if not exprcore.free_vars(f):
+                continue
+            rec = {"text": text, "d": d, "a": a, "n": n}
+            t0 = time.perf_counter()
+            try:
+                with np.errstate(all="ignore"):
+                    val, rep = mdi_lr(f, d, a, n, with_report=True)
+                rec.update(value=hx(val), levels=rep.levels, base_dim=rep.base_dim, fallback=rep.fallback)
+                counts = axis_counts(korobov_vector(a, n, d))
+                grid = [(np.arange(k) + 0.5) / k for k in counts]
+                mesh = np.meshgrid(*grid, indexing="ij")
+                with np.errstate(all="ignore"):
+                    vals = exprcore.eval_array(f, {j + 1: mesh[j].reshape(-1) for j in range(d)})
+                rec["scale"] = hx(float(np.mean(np.abs(vals))) if np.ndim(vals) else abs(float(vals)))
+            except Exception as exc:
+                rec["error"] = type(exc).__name__
+            rec["ref_seconds"] = round(time.perf_counter() - t0, 4)
+            if "value" in rec and not (math.isfinite(float.fromhex(rec["value"])) and
+                                       math.isfinite(float.fromhex(rec["scale"]))):
+                continue
+            out.append(rec)
+    return out
+
+
 _BIG_N = [262147, 1048583, 4194319]
 
 
@@ -662,7 +709,7 @@ def cfg5_full_case(procs):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
-    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites", "cfg5_full", "linform", "fft", "parser", "suites7", "subgrid", "slr_fuzz"],
+    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites", "cfg5_full", "linform", "fft", "parser", "suites7", "subgrid", "slr_fuzz", "mdi_fuzz"],
                     default=None)
     ap.add_argument("--procs", type=int, default=os.cpu_count())
     ap.add_argument("--only-new", action="store_true", help="fft: compute only cases missing from fft.json")
@@ -674,9 +721,9 @@ def main():
             "suites": suite_cases, "cfg5_full": lambda: cfg5_full_case(args.procs),
             "linform": lambda: linform_cases(args.skip_slow), "fft": lambda: fft_cases_job(args.procs, args.only_new),
             "parser": parser_cases, "suites7": suite7_cases, "subgrid": subgrid_cases,
-            "slr_fuzz": slr_fuzz_cases}
+            "slr_fuzz": slr_fuzz_cases, "mdi_fuzz": mdi_fuzz_cases}
     for name, fn in jobs.items():
-        if args.only != name and (args.only or name in ("cfg5_full", "linform", "fft", "suites7")):
+        if args.only != name and (args.only or name in ("cfg5_full", "linform", "fft", "suites7", "slr_fuzz", "mdi_fuzz")):
             continue
         t0 = time.perf_counter()
         cases = fn()
