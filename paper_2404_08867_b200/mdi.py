@@ -211,8 +211,16 @@ def mdi_sum(g, grids, cfg=None, comm=None):
         if bounds is None and cfg.fallback == "error":
             raise BudgetExceededError("integrand is not separable over the grid axes "
                                       f"(budget {cfg.budget}); no level reduction possible")
-        value = direct_tensor_sum(e, grids, cap=cfg.direct_cap, comm=comm)
         certified = bounds is not None
+        cap = cfg.direct_cap
+        if certified:
+            # the reference completes its levels and sweeps only its base axes
+            # (mdi.py:181-183): the cap applies to those, the GPU sweeps the grid
+            base_total = math.prod(counts[a - 1] for a in base_axes)
+            if base_total > cfg.direct_cap:
+                raise GridCapError(f"direct sweep needs {base_total} evaluations, cap is {cfg.direct_cap}")
+            cap = max(cap, total)
+        value = direct_tensor_sum(e, grids, cap=cap, comm=comm)
         return MdiReport(value=value, levels=levels if certified else 0,
                          base_dim=len(base_axes) if certified else d,
                          level_nodes=bounds if certified else (), level_seconds=(0.0,) * len(bounds or ()),

@@ -593,6 +593,16 @@ def mdi_fuzz_cases():
                                        math.isfinite(float.fromhex(rec["scale"]))):
                 continue
             out.append(rec)
+    # past the direct cap, where the reference's levels still fit the node
+    # budget: it sweeps only its base axes (no GridCapError)
+    for text, d, a in (("exp(x[1]*x[2]*x[3]*x[4]*x[5])", 5, 45),
+                       ("exp(-(x[1] - x[2])^2 - (x[3] - x[4])^2 - x[1]*x[4] - x[5])", 5, 42)):
+        f = exprcore.parse(text, d)
+        t0 = time.perf_counter()
+        val, rep = mdi_lr(f, d, a, a ** d, with_report=True)
+        out.append({"text": text, "d": d, "a": a, "n": a ** d, "value": hx(val), "levels": rep.levels,
+                    "base_dim": rep.base_dim, "fallback": rep.fallback, "scale": hx(abs(val)),
+                    "ref_seconds": round(time.perf_counter() - t0, 4), "over_cap": True})
     return out
 
 
