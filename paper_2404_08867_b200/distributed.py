@@ -82,6 +82,8 @@ def slr_integrate(f, rule, reference=None, group=None):
     e = as_expr(f)
     rank, size = world(group)
     d, n = rule.d, rule.n
+    from .quad import check_plain
+    check_plain(e, rule)
     if not free_vars(e) or size == 1:
         from .quad import slr_integrate as single
         return single(e, rule, reference)
