@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define LQ_ABI_VERSION 8
+#define LQ_ABI_VERSION 9
 
 #define LQ_OK 0
 #define LQ_ERR_VALUE (-1)
@@ -267,6 +267,13 @@ int lq_mdi_expabs_partials(lq_ctx* ctx, int32_t d, const double* beta, const int
 int lq_mdi_linform(lq_ctx* ctx, const lq_program* G, int32_t n_levels, const int64_t* m, const int32_t* counts,
                    double alpha, double h, int64_t m0, int32_t shard, int32_t nshards, double* tiles_dev,
                    int64_t tiles_cap, double* out);
+/* Weighted form (f = G(alpha + <beta, y>) prod_j phi_j(y_j)): level l's
+ * distribution update is p'(k) = (1/N_l) sum_t w_(l,t) p(k - |m_l| t), with
+ * weights[] the levels' node weights concatenated in level order (N_l each,
+ * in the order of the level's t; NULL: uniform, = lq_mdi_linform).          */
+int lq_mdi_linform_w(lq_ctx* ctx, const lq_program* G, int32_t n_levels, const int64_t* m, const int32_t* counts,
+                     const double* weights, double alpha, double h, int64_t m0, int32_t shard, int32_t nshards,
+                     double* tiles_dev, int64_t tiles_cap, double* out);
 
 /* ---- lattice quality measures and constructions (
  * lattice.py:140-311).  B_alpha and the factors 1 + g_j (B + beta) follow

@@ -2053,6 +2053,13 @@ int lq_mdi_expabs_partials(lq_ctx* c, int32_t d, const double* beta, const int32
 int lq_mdi_linform(lq_ctx* c, const lq_program* G, int32_t n_levels, const int64_t* m, const int32_t* counts,
                    double alpha, double h, int64_t m0, int32_t shard, int32_t nshards, double* tiles_dev,
                    int64_t tiles_cap, double* out) {
+    return lq_mdi_linform_w(c, G, n_levels, m, counts, nullptr, alpha, h, m0, shard, nshards, tiles_dev, tiles_cap,
+                            out);
+}
+
+int lq_mdi_linform_w(lq_ctx* c, const lq_program* G, int32_t n_levels, const int64_t* m, const int32_t* counts,
+                     const double* weights, double alpha, double h, int64_t m0, int32_t shard, int32_t nshards,
+                     double* tiles_dev, int64_t tiles_cap, double* out) {
     int rc = set_dev(c);
     if (rc) return rc;
     if (!G || !G->insn || G->n_insn < 1) return fail(LQ_ERR_VALUE, "null program");
@@ -2064,22 +2071,24 @@ int lq_mdi_linform(lq_ctx* c, const lq_program* G, int32_t n_levels, const int64
     const int ns = pick_slots(G->n_slots);
     if (ns < 0) return fail(LQ_ERR_UNSUPPORTED, "program needs %d slots (max %d)", G->n_slots, LQ_MAX_SLOTS);
     std::vector<lq::LinLevel> lv;
-    int64_t K = 1;
+    int64_t K = 1, wtotal = 0;
     for (int l = 0; l < n_levels; ++l) {
         if (m[l] < 1 || counts[l] < 1)
             return fail(LQ_ERR_VALUE, "level %d: m = %lld, N = %d", l, (long long)m[l], counts[l]);
         if (m[l] > LQ_LINFORM_MAX_SUPPORT / counts[l]) return fail(LQ_ERR_UNSUPPORTED, "level %d step too large", l);
         K += m[l] * (counts[l] - 1);
         if (K > LQ_LINFORM_MAX_SUPPORT) return fail(LQ_ERR_UNSUPPORTED, "support exceeds %lld points", (long long)LQ_LINFORM_MAX_SUPPORT);
-        lv.push_back({m[l], counts[l], 0});
+        lv.push_back({m[l], counts[l], 0, weights ? wtotal : -1});
+        wtotal += counts[l];
     }
     if (std::fabs((double)m0) + 2.0 * (double)K > 9007199254740992.0)
         return fail(LQ_ERR_UNSUPPORTED, "support positions exceed 2^53");
     const int64_t T = (K + LQ_TILE - 1) / LQ_TILE;
     if (tiles_dev && tiles_cap < T)
         return fail(LQ_ERR_VALUE, "tiles_dev holds %lld tiles, need %lld", (long long)tiles_cap, (long long)T);
-    void *dlv = nullptr, *dp, *dq = nullptr, *dg;
+    void *dlv = nullptr, *dp, *dq = nullptr, *dg, *dw = nullptr;
     if (!lv.empty() && (rc = upload(c, B_AUX0, lv.data(), sizeof(lq::LinLevel) * lv.size(), &dlv))) return rc;
+    if (weights && wtotal > 0 && (rc = upload(c, B_AUX3, weights, sizeof(double) * wtotal, &dw))) return rc;
     if ((rc = upload(c, B_PROG, G->insn, sizeof(lq_insn) * G->n_insn, &dg))) return rc;
     if ((rc = dev_buf(c, B_AUX1, sizeof(double) * K, &dp))) return rc;
     constexpr int64_t kSmemCap = (200 * 1024) / (2 * (int64_t)sizeof(double));   // 12800 support points
@@ -2088,7 +2097,7 @@ int lq_mdi_linform(lq_ctx* c, const lq_program* G, int32_t n_levels, const int64
     if (K <= kSmemCap && !(force_global && !std::strcmp(force_global, "0"))) {
         if ((rc = smem_optin(c, (const void*)lq::k_linform_smem, 2 * sizeof(double) * kSmemCap))) return rc;
         lq::k_linform_smem<<<1, 1024, 2 * sizeof(double) * K, c->stream>>>((const lq::LinLevel*)dlv, n_levels, K,
-                                                                           (double*)dp);
+                                                                           (const double*)dw, (double*)dp);
         c->launches++;
         CK(cudaGetLastError());
     } else {
@@ -2102,7 +2111,8 @@ int lq_mdi_linform(lq_ctx* c, const lq_program* G, int32_t n_levels, const int64
         for (int l = 0; l < n_levels; ++l) {
             const int64_t kn = k_old + lv[l].m * (lv[l].n - 1);
             const int grid = (int)std::min<int64_t>((kn + lq::kThreads - 1) / lq::kThreads, (int64_t)c->sm_count * 8);
-            lq::k_linform_level<<<grid, lq::kThreads, 0, c->stream>>>(cur, k_old, lv[l].m, lv[l].n, nxt);
+            const double* w = lv[l].woff >= 0 ? (const double*)dw + lv[l].woff : nullptr;
+            lq::k_linform_level<<<grid, lq::kThreads, 0, c->stream>>>(cur, k_old, lv[l].m, lv[l].n, w, nxt);
             c->launches++;
             CK(cudaGetLastError());
             std::swap(cur, nxt);

@@ -1541,29 +1541,41 @@ struct LinLevel {
     int64_t m;     // |m_j| >= 1
     int32_t n;     // N_j nodes
     int32_t pad;
+    int64_t woff;  // offset of the level's N_j node weights, or -1 (uniform)
 };
 
+// p_new[s] = (1/n) sum_t w_t p_old[s - m t] (w_t = 1 without weights)
 __device__ __forceinline__ double lin_conv_point(const double* __restrict__ p, int64_t k_old, int64_t s,
-                                                 int64_t m, int n) {
+                                                 int64_t m, int n, const double* __restrict__ w) {
     const int64_t t_lo = s < k_old ? 0 : (s - k_old + m) / m;   // s - m t <= k_old - 1
     const int64_t t_hi = min((int64_t)n - 1, s / m);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int64_t t = t_lo;
     const double* q = p + (s - m * t_lo);
-    for (; t + 3 <= t_hi; t += 4, q -= 4 * m) {
-        a0 += q[0];
-        a1 += q[-m];
-        a2 += q[-2 * m];
-        a3 += q[-3 * m];
+    if (w) {
+        for (; t + 3 <= t_hi; t += 4, q -= 4 * m) {
+            a0 = fma(w[t], q[0], a0);
+            a1 = fma(w[t + 1], q[-m], a1);
+            a2 = fma(w[t + 2], q[-2 * m], a2);
+            a3 = fma(w[t + 3], q[-3 * m], a3);
+        }
+        for (; t <= t_hi; ++t, q -= m) a0 = fma(w[t], q[0], a0);
+    } else {
+        for (; t + 3 <= t_hi; t += 4, q -= 4 * m) {
+            a0 += q[0];
+            a1 += q[-m];
+            a2 += q[-2 * m];
+            a3 += q[-3 * m];
+        }
+        for (; t <= t_hi; ++t, q -= m) a0 += q[0];
     }
-    for (; t <= t_hi; ++t, q -= m) a0 += q[0];
     return ((a0 + a1) + (a2 + a3)) / (double)n;
 }
 
 // Every level in one CTA with both distributions in shared memory (support
 // <= k_cap doubles each); the final distribution goes to p_out.
 __global__ void __launch_bounds__(1024) k_linform_smem(const LinLevel* __restrict__ lv, int n_lv, int64_t k_cap,
-                                                       double* __restrict__ p_out) {
+                                                       const double* __restrict__ wts, double* __restrict__ p_out) {
     extern __shared__ double lin_sm[];
     double* a = lin_sm;
     double* b = lin_sm + k_cap;
@@ -1573,7 +1585,8 @@ __global__ void __launch_bounds__(1024) k_linform_smem(const LinLevel* __restric
     for (int l = 0; l < n_lv; ++l) {
         const LinLevel L = lv[l];
         const int64_t Kn = K + L.m * (L.n - 1);
-        for (int64_t s = threadIdx.x; s < Kn; s += blockDim.x) b[s] = lin_conv_point(a, K, s, L.m, L.n);
+        const double* w = L.woff >= 0 ? wts + L.woff : nullptr;
+        for (int64_t s = threadIdx.x; s < Kn; s += blockDim.x) b[s] = lin_conv_point(a, K, s, L.m, L.n, w);
         __syncthreads();
         double* t = a;
         a = b;
@@ -1590,10 +1603,11 @@ __global__ void k_fill(double* __restrict__ p, int64_t count, double v) {
 
 // One level in global memory (support past the shared-memory capacity).
 __global__ void __launch_bounds__(kThreads) k_linform_level(const double* __restrict__ p, int64_t k_old,
-                                                            int64_t m, int n, double* __restrict__ q) {
+                                                            int64_t m, int n, const double* __restrict__ w,
+                                                            double* __restrict__ q) {
     const int64_t Kn = k_old + m * (n - 1);
     for (int64_t s = blockIdx.x * (int64_t)kThreads + threadIdx.x; s < Kn; s += (int64_t)gridDim.x * kThreads)
-        q[s] = lin_conv_point(p, k_old, s, m, n);
+        q[s] = lin_conv_point(p, k_old, s, m, n, w);
 }
 
 // sum_k p[k] G(alpha + h (m0 + 2k)) over tiles of kTile support points

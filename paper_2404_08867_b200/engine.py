@@ -15,7 +15,8 @@ import numpy as np
 
 from . import _native as N
 from .expr import Expr, UnassignedVariableError, as_expr, evaluate, free_vars
-from .lower import Program, compile_program, linear_outer, recognize_linear_program, recognize_plain, separate
+from .lower import (Program, compile_program, linear_outer, recognize_linear_program, recognize_plain, separate,
+                    weighted_linear_outer)
 
 __all__ = ["PlainIntegrand", "plain_integrand", "lattice_sum", "tensor_program", "eval_array", "SeparablePlan",
            "separable_plan", "mdi_separable_sum"]
@@ -469,10 +470,16 @@ class LinformPlan:
     def __init__(self, e, counts):
         from fractions import Fraction
         self.ok = False
+        self.weights = None          # weighted form: axis -> phi_j Expr
         lo = linear_outer(e)
         if lo is None:
-            return
+            lo = weighted_linear_outer(e)
+            if lo is None:
+                return
+            self.weights = lo.weights
         d = len(counts)
+        if self.weights is not None and any(not 1 <= j <= d for j in self.weights):
+            return
         if any(not 1 <= j <= d for j in lo.beta) or not all(math.isfinite(c) for c in lo.beta.values()):
             return
         if any(int(counts[j - 1]) > LINFORM_MAX_SUPPORT for j in lo.beta):
@@ -507,12 +514,52 @@ class LinformPlan:
         if abs(self.m0) + 2 * self.support >= 2**53:
             return
         self.level_support = tuple(int(v) for v in sizes)
+        self.wts, self.log_scale, self.sign = None, 0.0, 1.0
+        if self.weights is not None and not self._node_weights(counts, [axes[i] for i in order],
+                                                                [m[i] for i in order]):
+            return
         self.h_exact = b_ref * h_rat                 # the quantum as an exact rational
         self.h = float(self.h_exact)
         self.G = lo.G
         self.prog = compile_program(lo.G)
         self.tiles = -(-self.support // N.LQ_TILE)
         self.ok = True
+
+    def _node_weights(self, counts, level_axes, level_m):
+        """phi_j at the midpoint nodes y_t = RN((t + 1/2)/N_j), evaluated on
+        the GPU (eval_array), each axis scaled by its mean |phi_j| (the
+        scales go to log_scale, so the level distributions stay O(1));
+        levels with a negative step take their nodes in reverse (the plan's
+        t' = N - 1 - t).  Axes weighted but outside the linear form contribute
+        their scaled node mean to log_scale / sign.  False when some phi_j is
+        zero or non-finite on every node."""
+        per_axis = {}
+        for ax, phi in self.weights.items():
+            nn = int(counts[ax - 1])
+            y = (np.arange(nn, dtype=np.float64) + 0.5) / nn
+            with np.errstate(all="ignore"):
+                v = np.asarray(eval_array(phi, {ax: y}), dtype=np.float64) * np.ones(nn)
+            if not np.all(np.isfinite(v)):
+                return False
+            scale = float(np.mean(np.abs(v)))
+            if scale == 0.0:
+                return False
+            per_axis[ax] = v / scale
+            self.log_scale += math.log(scale)
+        in_form = set(level_axes)
+        for ax, v in per_axis.items():
+            if ax not in in_form:
+                mean = float(np.mean(v))
+                if mean == 0.0:
+                    return False
+                self.log_scale += math.log(abs(mean))
+                self.sign *= math.copysign(1.0, mean)
+        cols = []
+        for ax, mj in zip(level_axes, level_m):
+            v = per_axis.get(ax, np.ones(int(counts[ax - 1])))
+            cols.append(v[::-1] if mj < 0 else v)
+        self.wts = np.ascontiguousarray(np.concatenate(cols))
+        return True
 
     def program_struct(self):
         ins = np.ascontiguousarray(self.prog.insn)
@@ -538,14 +585,14 @@ def mdi_linform_mean(plan, shard=0, nshards=1, tiles_dev=None, comm=None):
         tiles = comm.zeros(plan.tiles)
         ins, p = plan.program_struct()
         out = C.c_double()
-        N.check(N.lib().lq_mdi_linform(comm.ctx(), C.byref(p), len(plan.m), N.as_ptr(plan.m), N.as_ptr(plan.n),
-                                       0.0, plan.h, int(plan.m0), comm.rank, comm.size,
-                                       C.c_void_p(tiles.data_ptr()), plan.tiles, C.byref(out)))
+        N.check(N.lib().lq_mdi_linform_w(comm.ctx(), C.byref(p), len(plan.m), N.as_ptr(plan.m), N.as_ptr(plan.n),
+                                         N.as_ptr(plan.wts), 0.0, plan.h, int(plan.m0), comm.rank, comm.size,
+                                         C.c_void_p(tiles.data_ptr()), plan.tiles, C.byref(out)))
         return comm.reduce(comm.exchange(tiles))
     ins, p = plan.program_struct()
     out = C.c_double()
-    N.check(N.lib().lq_mdi_linform(N.ctx(), C.byref(p), len(plan.m), N.as_ptr(plan.m), N.as_ptr(plan.n), 0.0,
-                                   plan.h, int(plan.m0), shard, nshards,
-                                   None if tiles_dev is None else C.c_void_p(tiles_dev), plan.tiles,
-                                   C.byref(out)))
+    N.check(N.lib().lq_mdi_linform_w(N.ctx(), C.byref(p), len(plan.m), N.as_ptr(plan.m), N.as_ptr(plan.n),
+                                     N.as_ptr(plan.wts), 0.0, plan.h, int(plan.m0), shard, nshards,
+                                     None if tiles_dev is None else C.c_void_p(tiles_dev), plan.tiles,
+                                     C.byref(out)))
     return out.value

@@ -32,7 +32,7 @@ from .expr import Expr, add, const, free_vars, func, mul, power, topo, var
 
 __all__ = [
     "linear_form", "quad_form", "recognize_plain", "PlainFamily",
-    "Program", "compile_program", "separate", "SepTerm", "Factor",
+    "Program", "compile_program", "separate", "SepTerm", "Factor", "weighted_linear_outer", "WeightedOuter",
     "MAX_SLOTS", "INSN_DTYPE", "LinearOuter", "linear_outer", "recognize_linear_program",
 ]
 
@@ -740,3 +740,40 @@ def linear_outer(e, rel_tol=4.0 * 2.0**-52):
     if free_vars(G) != frozenset({1}):
         return None
     return LinearOuter(G, beta0)
+
+
+@dataclass
+class WeightedOuter:
+    """e = coef * G(<beta, x>) * prod_j phi_j(x_j): the factors of a product
+    that separate into one real univariate term each (the weights phi_j, one
+    Expr per axis) times a function of one linear form.  ``G`` includes coef."""
+
+    G: Expr
+    beta: dict
+    weights: dict
+
+
+def weighted_linear_outer(e):
+    """Split a product into separable real weights and a function of one
+    linear form (None otherwise, or when either part is missing) -- the
+    integrands whose MDI levels the reference collapses by like-term
+    collection with node-dependent coefficients (exprcore.py:139-206)."""
+    if e.op != "mul":
+        return None
+    coef = e.val
+    rest, weights = [], {}
+    for f in e.args:
+        sep = separate(f) if len(free_vars(f)) > 0 else None
+        if sep is not None and len(sep) == 1 and sep[0].coef.imag == 0.0 and \
+                all(fac.P is None and len(fac.axes) == 1 and fac.R is not None for fac in sep[0].factors.values()):
+            coef *= sep[0].coef.real
+            for fac in sep[0].factors.values():
+                weights.setdefault(fac.axis, []).append(fac.R)
+        else:
+            rest.append(f)
+    if not rest or not weights or not math.isfinite(coef):
+        return None
+    lo = linear_outer(mul(coef, rest))
+    if lo is None:
+        return None
+    return WeightedOuter(lo.G, lo.beta, {ax: mul(1.0, fs) for ax, fs in weights.items()})

@@ -200,7 +200,7 @@ def mdi_sum(g, grids, cfg=None, comm=None):
             rep = _characteristic(e, d, counts, levels, base_axes, t0, comm)
             if rep is not None:
                 return rep
-        rep = _linform(e, counts, levels, base_axes, cfg, t0, comm)
+        rep = _linform(e, counts, levels, base_axes, cfg, t0, comm, weighted=not usable)
         if rep is not None:
             return rep
     if not usable:
@@ -302,8 +302,9 @@ def _subgrid(e, grids, counts, levels, base_axes, cfg, t0, comm=None):
                      log_raw=log_raw, sign=sign, method="subgrid", clusters=sub_total)
 
 
-def _linform(e, counts, levels, base_axes, cfg, t0, comm=None):
-    """f = G(alpha + <beta, y>) with commensurate steps beta_j / (2 N_j): the
+def _linform(e, counts, levels, base_axes, cfg, t0, comm=None, weighted=True):
+    """f = G(alpha + <beta, y>), or G(...) prod_j phi_j(y_j) (weighted: each
+    level's nodes carry phi_j(y_t)), with commensurate steps beta_j / (2 N_j): the
     level collapse the reference's partial sums perform by like-term
     collection (each level's partial sums take the values of the partial
     linear form, exprcore.py:139-169, 390-402; mdi.py:152-165), here as the
@@ -312,12 +313,23 @@ def _linform(e, counts, levels, base_axes, cfg, t0, comm=None):
     this form or its support is too large."""
     plan = engine.linform_plan(e, counts)
     # the node budget bounds what a level may carry (exprcore.py:399-401); here
-    # a level carries its distinct partial-form values
-    if not plan.ok or max(plan.level_support, default=1) > cfg.budget:
+    # a level carries its distinct partial-form values.  A weighted form that
+    # also splits into cores takes the separable combine instead (weighted=False).
+    if not plan.ok or max(plan.level_support, default=1) > cfg.budget or (plan.weights is not None and not weighted):
         return None
     mean = engine.mdi_linform_mean(plan, comm=comm)
     log_total = _log_total(counts)
-    raw, log_raw, sign = _raw_from_mean(mean, counts, log_total)
+    if plan.weights is not None and mean != 0.0 and math.isfinite(mean):
+        # weighted form: the distribution carried scaled weights (plan.log_scale)
+        sign = math.copysign(1.0, mean) * plan.sign
+        log_mean = math.log(abs(mean)) + plan.log_scale
+        if -700.0 < log_mean < 700.0:
+            raw, log_raw, sign = _raw_from_mean(sign * math.exp(log_mean), counts, log_total)
+        else:
+            log_raw = log_mean + log_total
+            raw = sign * (math.exp(log_raw) if log_raw < 709.7 else math.inf)
+    else:
+        raw, log_raw, sign = _raw_from_mean(mean, counts, log_total)
     stripped = plan.level_support[:levels * cfg.m:cfg.m] if cfg.m > 1 else plan.level_support[:levels]
     return MdiReport(value=raw, levels=levels, base_dim=len(base_axes), level_nodes=tuple(stripped),
                      level_seconds=(0.0,) * levels, base_seconds=time.perf_counter() - t0, fallback=False,

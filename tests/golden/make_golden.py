@@ -606,6 +606,32 @@ def mdi_fuzz_cases():
     return out
 
 
+def linform_w_cases():
+    """mdi_lr of the reference for products of separable real weights and a
+    function of one commensurate linear form (its like-term collection carries
+    node-dependent coefficients, exprcore.py:139-206): value and report,
+    including grids past the direct cap (d = 10, 12) and weights on axes the
+    linear form does not use."""
+    cases = [("exp(-sum(i=1..d, x[i]^2))*(1 + sum(i=1..d, x[i]))^(-2)", 6, 8, 8**6 + 1),
+             ("exp(-sum(i=1..d, x[i]^2))*(1 + sum(i=1..d, x[i]))^(-2)", 10, 8, 8**10 + 1),
+             ("exp(-sum(i=1..d, x[i]^2))*(1 + sum(i=1..d, x[i]))^(-2)", 12, 8, 8**12 + 1),
+             ("x[1]*x[2]*(1 + sum(i=1..d, x[i]))^(-3)", 5, 4, 4**5 + 1),
+             ("prod(i=1..d, 1 + x[i])*exp(-(sum(i=1..d, x[i]))^2)", 7, 6, 6**7 + 1),
+             ("prod(i=1..d, 1 + x[i])*exp(-((sum(i=1..d, x[i]))^2))", 9, 6, 6**9 + 1),
+             ("x[5]^2*(1 + x[1] + x[2] + x[3])^(-2)", 5, 5, 5**5 + 1),
+             ("exp(-sum(i=1..d, x[i]^2))*(3 + x[1] - x[2] + x[3] - 0.5*x[4])^(-1)", 6, 8, 8**6),
+             ("(x[1] - 0.5)*cos(x[2])*(2 + x[1] + 2*x[2] + x[3])^(-2)", 4, 6, 6**4 + 1)]
+    out = []
+    for text, d, a, n in cases:
+        f = exprcore.parse(text, d)
+        t0 = time.perf_counter()
+        val, rep = mdi_lr(f, d, a, n, with_report=True)
+        out.append({"text": text, "d": d, "a": a, "n": n, "value": hx(val), "levels": rep.levels,
+                    "base_dim": rep.base_dim, "fallback": rep.fallback,
+                    "ref_seconds": round(time.perf_counter() - t0, 3)})
+    return out
+
+
 _BIG_N = [262147, 1048583, 4194319]
 
 
@@ -719,7 +745,7 @@ def cfg5_full_case(procs):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
-    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites", "cfg5_full", "linform", "fft", "parser", "suites7", "subgrid", "slr_fuzz", "mdi_fuzz"],
+    ap.add_argument("--only", choices=["points", "slr", "mdi", "quality", "mc", "suites", "cfg5_full", "linform", "fft", "parser", "suites7", "subgrid", "slr_fuzz", "mdi_fuzz", "linform_w"],
                     default=None)
     ap.add_argument("--procs", type=int, default=os.cpu_count())
     ap.add_argument("--only-new", action="store_true", help="fft: compute only cases missing from fft.json")
@@ -731,9 +757,9 @@ def main():
             "suites": suite_cases, "cfg5_full": lambda: cfg5_full_case(args.procs),
             "linform": lambda: linform_cases(args.skip_slow), "fft": lambda: fft_cases_job(args.procs, args.only_new),
             "parser": parser_cases, "suites7": suite7_cases, "subgrid": subgrid_cases,
-            "slr_fuzz": slr_fuzz_cases, "mdi_fuzz": mdi_fuzz_cases}
+            "slr_fuzz": slr_fuzz_cases, "mdi_fuzz": mdi_fuzz_cases, "linform_w": linform_w_cases}
     for name, fn in jobs.items():
-        if args.only != name and (args.only or name in ("cfg5_full", "linform", "fft", "suites7", "slr_fuzz", "mdi_fuzz")):
+        if args.only != name and (args.only or name in ("cfg5_full", "linform", "fft", "suites7", "slr_fuzz", "mdi_fuzz", "linform_w")):
             continue
         t0 = time.perf_counter()
         cases = fn()

@@ -162,3 +162,25 @@ def test_cores_and_unused_axes_match_reference(case):
     assert rep.method == ("subgrid" if case["tag"] == "exp4_d8" else "cores"), rep.method
     assert abs(value - want) <= 1e-10 * abs(want), (value, want)
     assert (rep.levels, rep.base_dim, rep.fallback) == (case["levels"], case["base_dim"], case["fallback"])
+
+
+def test_weighted_level_collapse_matches_reference():
+    """Products of separable real weights and a function of one commensurate
+    linear form (tests/golden/linform_w.json, frozen from the reference's
+    mdi_lr): each level's nodes carry phi_j(y_t) in the distribution update
+    (lq_mdi_linform_w), including grids past the direct cap (d = 10, 12),
+    weights on an axis outside the form and mixed-sign steps."""
+    methods = set()
+    import paper_2404_08867_b200 as lq
+    from conftest import load_golden, unhex
+    for c in load_golden("linform_w"):
+        f = lq.parse(c["text"], c["d"])
+        got, rep = lq.mdi_lr(f, c["d"], c["a"], c["n"], with_report=True)
+        want = unhex(c["value"])
+        # a weighted form whose non-splitting piece spans <= 3 axes takes the
+        # separable combine with a core instead (same collapse, same value)
+        assert rep.method in ("linform", "cores"), (c["text"], rep.method)
+        assert abs(got - want) <= 1e-10 * abs(want), (c["text"], c["d"], got, want)
+        assert (rep.levels, rep.base_dim, rep.fallback) == (c["levels"], c["base_dim"], c["fallback"]), c["text"]
+        methods.add(rep.method)
+    assert "linform" in methods
