@@ -207,6 +207,9 @@ def mdi_sum(g, grids, cfg=None, comm=None):
         rep = _subgrid(e, grids, counts, levels, base_axes, cfg, t0, comm)
         if rep is not None:
             return rep
+        rep = _term_sum(e, grids, counts, levels, base_axes, cfg, t0, comm)
+        if rep is not None:
+            return rep
         bounds = _level_bounds(e, counts, levels, base_axes, cfg)
         if bounds is None and cfg.fallback == "error":
             raise BudgetExceededError("integrand is not separable over the grid axes "
@@ -265,6 +268,42 @@ def _level_bounds(e, counts, levels, base_axes, cfg):
             return None
         out.append(nc)
     return tuple(out)
+
+
+def _term_sum(e, grids, counts, levels, base_axes, cfg, t0, comm=None):
+    """A sum whose terms collapse separately (e.g. (1 + sum x)^-2 + exp(-sum
+    x^2)): the reference's levels act on each term of the sum
+    (exprcore.py:390-402 distributes partial_sum over a sum), so the grid mean
+    is the constant plus the coefficient-weighted term means, each by its own
+    branch.  None unless every term collapses without a fallback."""
+    if e.op != "add" or len(e.terms) < 2 or not midpoint_of(grids):
+        return None
+    mean = e.val
+    parts = 0
+    log_total = _log_total(counts)
+    for c, t in e.terms:
+        if not free_vars(t):
+            mean += c * evaluate(t, {})
+            continue
+        try:
+            rep = mdi_sum(t, grids, cfg, comm)
+        except (GridCapError, BudgetExceededError):
+            return None
+        if rep.fallback or rep.method == "direct" or rep.log_raw is None:
+            return None
+        if rep.log_raw > -math.inf and rep.sign:
+            mean += c * rep.sign * math.exp(rep.log_raw - log_total)
+        parts += 1
+    if parts < 2:
+        return None
+    raw, log_raw, sign = _raw_from_mean(mean, counts, log_total)
+    return MdiReport(value=raw, levels=levels, base_dim=len(base_axes), level_nodes=(len(e.terms),) * levels,
+                     level_seconds=(0.0,) * levels, base_seconds=time.perf_counter() - t0, fallback=False,
+                     log_raw=log_raw, sign=sign, method="terms", clusters=parts)
+
+
+def midpoint_of(grids):
+    return getattr(grids, "midpoint", False)
 
 
 def _subgrid(e, grids, counts, levels, base_axes, cfg, t0, comm=None):

@@ -620,7 +620,11 @@ def linform_w_cases():
              ("prod(i=1..d, 1 + x[i])*exp(-((sum(i=1..d, x[i]))^2))", 9, 6, 6**9 + 1),
              ("x[5]^2*(1 + x[1] + x[2] + x[3])^(-2)", 5, 5, 5**5 + 1),
              ("exp(-sum(i=1..d, x[i]^2))*(3 + x[1] - x[2] + x[3] - 0.5*x[4])^(-1)", 6, 8, 8**6),
-             ("(x[1] - 0.5)*cos(x[2])*(2 + x[1] + 2*x[2] + x[3])^(-2)", 4, 6, 6**4 + 1)]
+             ("(x[1] - 0.5)*cos(x[2])*(2 + x[1] + 2*x[2] + x[3])^(-2)", 4, 6, 6**4 + 1),
+             # sums whose terms collapse by different branches
+             ("(1 + sum(i=1..d, x[i]))^(-2) + exp(-sum(i=1..d, x[i]^2))", 10, 8, 8**10 + 1),
+             ("3*(2 + sum(i=1..d, x[i]))^(-1) - 0.5*prod(i=1..d, 1 + x[i]) + 1.25", 8, 8, 8**8 + 1),
+             ("x[1]*x[2]*(1 + sum(i=1..d, x[i]))^(-3) + cos(sum(i=1..d, x[i]))", 9, 6, 6**9 + 1)]
     out = []
     for text, d, a, n in cases:
         f = exprcore.parse(text, d)
