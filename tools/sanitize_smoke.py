@@ -39,4 +39,14 @@ lq.p_alpha(lq.korobov_vector(76, 1009, 6), 4)
 lq.shift_avg_wce_sq(lq.korobov_vector(76, 1009, 6))
 lq.cbc_construct(101, 4)
 lq.korobov_search(101, 4)
+# session 2: eval_array, weighted level collapse, term sums, exact quality sums
+f3 = lq.parse("exp(x[1]) * cos(x[2] + 2*x[3])", 3)
+lq.eval_array(f3, {1: np.linspace(0, 1, 1000), 2: 0.25, 3: np.linspace(1, 0, 1000)})
+w = lq.parse("exp(-sum(i=1..d, x[i]^2))*(1 + sum(i=1..d, x[i]))^(-2)", 8)
+lq.mdi_lr(w, 8, 8, 8**8 + 1)
+os.environ["LQ_LINFORM_SMEM"] = "0"
+lq.mdi_lr(w, 8, 8, 8**8 + 1)
+del os.environ["LQ_LINFORM_SMEM"]
+lq.mdi_lr(lq.parse("(1 + sum(i=1..d, x[i]))^(-2) + exp(-sum(i=1..d, x[i]^2))", 6), 6, 6, 6**6 + 1)
+lq.p_alpha(lq.LatticeRule(1009, (1, 400)), 2)
 print("sanitize smoke ok")
