@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define LQ_ABI_VERSION 9
+#define LQ_ABI_VERSION 10
 
 #define LQ_OK 0
 #define LQ_ERR_VALUE (-1)
@@ -154,6 +154,12 @@ int lq_lattice_layout(const lq_integrand* f, uint64_t n, const uint64_t* z_reduc
 int lq_lattice_partials(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_t* z_reduced,
                         int64_t s_begin, int64_t s_end, double* out_dev);
 /* Fixed pairwise tree over vals_dev[0..count); result to host *out. */
+/* Host-only check of the full-lattice layout of (f, n, z) (n <= 2^26): how
+ * many lattice indices the layout's units (chains and their mirrors, levels,
+ * the small lattice, mirror pairs or plain indices) miss and how many they
+ * cover more than once -- both 0 for a correct plan.                        */
+int lq_layout_cover(const lq_integrand* f, uint64_t n, const uint64_t* z_reduced, int64_t* missed,
+                    int64_t* repeated);
 int lq_reduce_sum(lq_ctx* ctx, const double* vals_dev, int64_t count, double* out);
 
 /* ---- Monte Carlo: replaces quad.mc_integrate's loop (quad.py:79-93).  Sums

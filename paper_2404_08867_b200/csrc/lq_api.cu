@@ -13,6 +13,8 @@
 #include <tuple>
 #include <string>
 #include <vector>
+#include <unordered_map>
+#include <algorithm>
 
 #include "lq_kernels.cu"
 
@@ -677,7 +679,10 @@ constexpr uint32_t kOrbMaxCosets = 4096;
 // kernel can enumerate (caller then uses the per-index kernels).
 // mirror: enumerate half of the nonzero points (their mirrors n - i are summed
 // with them); otherwise every nonzero point once (product family).
-std::shared_ptr<const OrbPlan> build_orbit_plan(uint32_t n, uint32_t a, int m, bool mirror) {
+// relaxed (composite-n levels): chains may be shorter than m and the cosets
+// many (kOrbMaxCosetsLevel); the kernels mask a chain's tail either way.
+constexpr uint32_t kOrbMaxCosetsLevel = 1u << 20;
+std::shared_ptr<const OrbPlan> build_orbit_plan(uint32_t n, uint32_t a, int m, bool mirror, bool relaxed = false) {
     if (!is_prime32(n) || a < 1 || a >= n) return nullptr;
     std::vector<uint32_t> primes;
     uint32_t rest = n - 1;
@@ -702,7 +707,8 @@ std::shared_ptr<const OrbPlan> build_orbit_plan(uint32_t n, uint32_t a, int m, b
     if (!mirror) { cosets = C; h = o; }                 // every coset, every exponent
     else if (o % 2 == 0) { cosets = C; h = o / 2; }     // -1 lies in <a>: half of each coset
     else { cosets = C / 2; h = o; }                     // -coset(s) = coset(s + C/2)
-    if (cosets < 1 || cosets > kOrbMaxCosets || h < (uint32_t)m) return nullptr;
+    if (cosets < 1 || cosets > (relaxed ? kOrbMaxCosetsLevel : kOrbMaxCosets) || h < (relaxed ? 1u : (uint32_t)m))
+        return nullptr;
     static std::atomic<uint64_t> next_id{1};
     auto p = std::make_shared<OrbPlan>();
     p->id = next_id++;
@@ -817,9 +823,14 @@ std::shared_ptr<const OrbPlan> build_orbit_plan_pow2(int m, uint32_t a_full, int
     return p;
 }
 
+// Levels + small lattice (n = 2^k here; composite n below, DivPlan): every
+// level is the orbit sum of one class of points (a unit group mod its own
+// modulus), and the small lattice -- modulus small_n, the per-index kernel --
+// holds the classes too short for chains and the point 0.
 struct Pow2Plan {
     int k = 0, m0 = 0;                                  // levels m0+1 .. k; small lattice mod 2^m0
     bool fft = false;
+    uint64_t small_n = 1;                               // modulus of the small lattice
     std::vector<std::shared_ptr<const OrbPlan>> levels; // m = k, k-1, ..., m0+1
 };
 
@@ -840,7 +851,332 @@ std::shared_ptr<const Pow2Plan> pow2_plan(uint32_t a, int k, int len, bool fft) 
         P->levels.push_back(lp);
     }
     P->m0 = m;
+    P->small_n = 1ull << m;
     std::shared_ptr<const Pow2Plan> out = P->levels.empty() ? nullptr : P;
+    if (cache.size() > 64) cache.clear();
+    cache[key] = out;
+    return out;
+}
+
+// ---- Korobov rules with composite n.  Point i with
+// gcd(i, n) = n/m is (n/m) u, u a unit mod m, and its coordinates are
+// frac(u a^(j-1) / m): the class is the unit group U(m) of the Korobov lattice
+// mod m.  U(m) is a product of cyclic groups (a primitive root per odd prime
+// power, -1 and 5 for 2^e); in those exponent coordinates <a> (with -1 for the
+// mirror pairs) is a subgroup, and the box of a triangular (Hermite) basis of
+// the relation lattice is a complete set of coset representatives.
+struct UnitComp {
+    uint64_t q;      // prime-power modulus of the component
+    uint64_t ord;    // cyclic order
+    uint64_t gen;    // generator mod q
+    int two;         // 0 odd prime power; 1 the -1 factor of 2^e; 2 the <5> factor of 2^e
+};
+
+uint64_t mulmod64(uint64_t x, uint64_t y, uint64_t m) { return (uint64_t)((unsigned __int128)x * y % m); }
+uint64_t powmod64(uint64_t b, uint64_t e, uint64_t m) {
+    uint64_t r = 1 % m;
+    b %= m;
+    for (; e; e >>= 1, b = mulmod64(b, b, m))
+        if (e & 1) r = mulmod64(r, b, m);
+    return r;
+}
+uint64_t gcd64(uint64_t x, uint64_t y) { while (y) { uint64_t t = x % y; x = y; y = t; } return x; }
+
+std::vector<std::pair<uint64_t, int>> factor64(uint64_t n) {
+    std::vector<std::pair<uint64_t, int>> out;
+    for (uint64_t p = 2; p * p <= n; ++p)
+        if (n % p == 0) {
+            int e = 0;
+            while (n % p == 0) { n /= p; ++e; }
+            out.push_back({p, e});
+        }
+    if (n > 1) out.push_back({n, 1});
+    return out;
+}
+
+// discrete log of x to base g in the cyclic group of order ord mod q (baby-step
+// giant-step); ord < 2^32
+uint64_t dlog_bsgs(uint64_t g, uint64_t x, uint64_t ord, uint64_t q) {
+    const uint64_t s = (uint64_t)std::ceil(std::sqrt((double)ord)) + 1;
+    std::unordered_map<uint64_t, uint64_t> baby;
+    baby.reserve(2 * s);
+    uint64_t cur = 1 % q;
+    for (uint64_t j = 0; j < s; ++j) {
+        baby.emplace(cur, j);
+        cur = mulmod64(cur, g, q);
+    }
+    const uint64_t ginv_s = powmod64(powmod64(g, ord - 1, q), s, q);   // g^-s
+    cur = x % q;
+    for (uint64_t i = 0; i <= s; ++i) {
+        auto it = baby.find(cur);
+        if (it != baby.end()) return (i * s + it->second) % ord;
+        cur = mulmod64(cur, ginv_s, q);
+    }
+    return UINT64_MAX;
+}
+
+uint64_t primitive_root_pe(uint64_t p, int e) {
+    const uint64_t pm1 = p - 1;
+    auto fs = factor64(pm1);
+    for (uint64_t g = 2;; ++g) {
+        bool prim = true;
+        for (auto& f : fs)
+            if (powmod64(g, pm1 / f.first, p) == 1) { prim = false; break; }
+        if (!prim) continue;
+        if (e >= 2 && powmod64(g, pm1, p * p) == 1) continue;   // lifts to p^e unless g^(p-1) = 1 mod p^2
+        return g;
+    }
+}
+
+// Orbit plan of the unit group U(m) (m composite or a prime power) under
+// multiplication by a, mirror pairs u, -u summed together; nullptr when the
+// chains would be shorter than len or the cosets too many.
+std::shared_ptr<const OrbPlan> build_orbit_plan_units(uint32_t m, uint32_t a_full, int len, bool fft) {
+    if (m < 3) return nullptr;
+    const uint64_t a = a_full % m;
+    if (gcd64(a, m) != 1) return nullptr;
+    // cyclic components and the exponent vectors of a and -1
+    std::vector<UnitComp> comp;
+    std::vector<uint64_t> al, be;
+    for (auto& pe : factor64(m)) {
+        uint64_t q = 1;
+        for (int i = 0; i < pe.second; ++i) q *= pe.first;
+        if (pe.first == 2) {
+            if (pe.second == 1) {            // U(2) is trivial, but u must still be odd (CRT)
+                comp.push_back({2, 1, 1, 1});
+                al.push_back(0);
+                be.push_back(0);
+                continue;
+            }
+            const uint64_t ar = a % q;
+            const bool neg = (ar & 3) == 3;
+            comp.push_back({q, 2, q - 1, 1});
+            al.push_back(neg ? 1 : 0);
+            be.push_back(1);
+            if (pe.second >= 3) {
+                const int e = pe.second;
+                const uint64_t ord5 = q >> 2, b = neg ? (q - ar) % q : ar;   // +-a = 5^k
+                uint64_t k = 0, cur = b, p5 = 5;
+                for (int i = 0; i < e - 2; ++i) {
+                    if ((cur & ((1ull << (i + 3)) - 1)) != 1) {
+                        k |= 1ull << i;
+                        cur = mulmod64(cur, inv_pow2(p5, 64) & (q - 1), q);
+                    }
+                    p5 = mulmod64(p5, p5, q);
+                }
+                comp.push_back({q, ord5, 5, 2});
+                al.push_back(k);
+                be.push_back(0);
+            }
+        } else {
+            const uint64_t ord = q / pe.first * (pe.first - 1);
+            const uint64_t g = primitive_root_pe(pe.first, pe.second);
+            const uint64_t k = dlog_bsgs(g, a % q, ord, q);
+            if (k == UINT64_MAX) return nullptr;
+            comp.push_back({q, ord, g, 0});
+            al.push_back(k);
+            be.push_back(ord / 2);          // -1 = g^(ord/2)
+        }
+    }
+    const int r = (int)comp.size();
+    if (r == 0) return nullptr;
+    uint64_t o = 1, phi = 1;                  // ord(a), |U(m)|
+    for (int c = 0; c < r; ++c) {
+        const uint64_t oc = comp[c].ord / gcd64(comp[c].ord, al[c]);
+        o = o / gcd64(o, oc) * oc;
+        phi *= comp[c].ord;
+    }
+    const bool neg_in = (o % 2 == 0) && powmod64(a, o / 2, m) == m - 1;
+    const uint64_t h = neg_in ? o / 2 : o;
+    const uint64_t hsize = neg_in ? o : 2 * o;   // |H|, H = <a> or <a, -1>
+    if (phi % hsize) return nullptr;
+    const uint64_t cosets = phi / hsize;
+    if (cosets > kOrbMaxCosetsLevel || h < 1) return nullptr;
+    // triangular basis of the relation lattice span{ord_c e_c, alpha (, beta)}
+    std::vector<std::vector<int64_t>> rows;
+    rows.push_back(std::vector<int64_t>(al.begin(), al.end()));
+    if (!neg_in) rows.push_back(std::vector<int64_t>(be.begin(), be.end()));
+    auto modc = [&](int64_t v, int c) { const int64_t M = (int64_t)comp[c].ord; v %= M; return v < 0 ? v + M : v; };
+    std::vector<int64_t> diag(r);
+    for (int c = 0; c < r; ++c) {
+        std::vector<int64_t> piv(r, 0);
+        piv[c] = (int64_t)comp[c].ord;        // the relation ord_c e_c
+        for (auto& R : rows) {
+            if (R[c] == 0) continue;
+            // extended gcd of (piv[c], R[c]): [piv; R] <- [[s, t], [-R_c/g, piv_c/g]] [piv; R]
+            int64_t x0 = piv[c], x1 = R[c], s0 = 1, s1 = 0, t0 = 0, t1 = 1;
+            while (x1) {
+                const int64_t qq = x0 / x1;
+                int64_t tmp = x0 - qq * x1; x0 = x1; x1 = tmp;
+                tmp = s0 - qq * s1; s0 = s1; s1 = tmp;
+                tmp = t0 - qq * t1; t0 = t1; t1 = tmp;
+            }
+            const int64_t g = x0, u = piv[c] / g, v = R[c] / g;
+            std::vector<int64_t> np(r), nr(r);
+            for (int k = 0; k < r; ++k) {
+                const __int128 pk = piv[k], rk = R[k];
+                const __int128 a1 = (__int128)s0 * pk + (__int128)t0 * rk, a2 = -(__int128)v * pk + (__int128)u * rk;
+                if (k == c) { np[k] = (int64_t)a1; nr[k] = (int64_t)a2; continue; }
+                const __int128 M = (__int128)comp[k].ord;
+                __int128 b1 = a1 % M, b2 = a2 % M;
+                np[k] = (int64_t)(b1 < 0 ? b1 + M : b1);
+                nr[k] = (int64_t)(b2 < 0 ? b2 + M : b2);
+            }
+            piv.swap(np);
+            R.swap(nr);
+        }
+        // piv is the basis vector b_c = (0, .., 0, g, *, ..); every remaining
+        // row now has a zero in column c
+        diag[c] = piv[c] < 0 ? -piv[c] : piv[c];
+    }
+    uint64_t box = 1;
+    for (int c = 0; c < r; ++c) {
+        if (diag[c] < 1) return nullptr;
+        box *= (uint64_t)diag[c];
+    }
+    if (box != cosets) return nullptr;        // the basis must index exactly |U(m)/H| cosets
+    // representatives: x in the box -> prod_c gen_c^(x_c), CRT over the prime powers
+    static std::atomic<uint64_t> next_id{1ull << 50};
+    auto p = std::make_shared<OrbPlan>();
+    p->id = next_id++;
+    p->n = m; p->a = (uint32_t)a; p->m = len; p->h = (uint32_t)h; p->mirror = true; p->zero = false;
+    p->as = (uint32_t)((a << 32) / m);
+    p->qc = (uint32_t)((h + len - 1) / len);
+    p->units = cosets * p->qc;
+    p->G.resize(cosets);
+    std::vector<int64_t> x(r, 0);
+    for (uint64_t idx = 0; idx < cosets; ++idx) {
+        uint64_t u = 0, M = 1;   // CRT accumulation
+        int c = 0;
+        while (c < r) {
+            const uint64_t q = comp[c].q;
+            uint64_t v = 1 % q;
+            int c2 = c;
+            for (; c2 < r && comp[c2].q == q; ++c2) v = mulmod64(v, powmod64(comp[c2].gen, (uint64_t)x[c2], q), q);
+            // u mod M and v mod q -> u mod M q
+            uint64_t t = (v + q - u % q) % q;
+            // M^-1 mod q by extended Euclid
+            int64_t e0 = (int64_t)(M % q), e1 = (int64_t)q, s0 = 1, s1 = 0;
+            while (e1) { const int64_t qq = e0 / e1; int64_t tmp = e0 - qq * e1; e0 = e1; e1 = tmp; tmp = s0 - qq * s1; s0 = s1; s1 = tmp; }
+            const uint64_t inv = (uint64_t)((s0 % (int64_t)q + (int64_t)q) % (int64_t)q);
+            t = mulmod64(t, inv, q);
+            u += M * t;
+            M *= q;
+            c = c2;
+        }
+        p->G[idx] = (uint32_t)(u % m);
+        for (int k = r - 1; k >= 0; --k) {   // mixed-radix increment over the box
+            if (++x[k] < diag[k]) break;
+            x[k] = 0;
+        }
+    }
+    auto mulm = [&](uint64_t xx, uint64_t yy) { return mulmod64(xx, yy, m); };
+    uint64_t am = 1;
+    for (int i = 0; i < len; ++i) am = mulm(am, a);
+    p->Alo.resize(4096);
+    uint64_t t = 1;
+    for (int q = 0; q < 4096; ++q) { p->Alo[q] = (uint32_t)t; t = mulm(t, am); }
+    const uint64_t am4096 = t;
+    p->Ahi.resize(p->qc / 4096 + 1);
+    t = 1;
+    for (size_t q = 0; q < p->Ahi.size(); ++q) { p->Ahi[q] = (uint32_t)t; t = mulm(t, am4096); }
+    if (fft) {
+        p->apow.resize(2 * lq::kFftN);
+        t = 1;
+        for (int k = 0; k < lq::kFftN; ++k) {
+            p->apow[2 * k] = (uint32_t)t;
+            p->apow[2 * k + 1] = (uint32_t)((t << 32) / m);
+            t = mulm(t, a);
+        }
+        fill_chain_starts(*p);
+    }
+    return p;
+}
+
+// Composite n: a level for every divisor m of n whose unit group has chains
+// (the prime plan for prime m), the small lattice mod m0 for the rest.  m0 is
+// grown (lcm) by every divisor without a plan, so its divisors are exactly the
+// classes left to the per-index kernel.  nullptr when m0 would exceed n / 4.
+std::shared_ptr<const Pow2Plan> div_plan(uint32_t n, uint32_t a, int len, bool fft, int len_direct) {
+    static std::mutex mu;
+    static std::map<std::tuple<uint32_t, uint32_t, int, bool, int>, std::shared_ptr<const Pow2Plan>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(n, a, len, fft, len_direct);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    std::vector<uint64_t> divs{1};
+    for (auto& pe : factor64(n)) {
+        const size_t k = divs.size();
+        uint64_t q = 1;
+        for (int e = 1; e <= pe.second; ++e) {
+            q *= pe.first;
+            for (size_t i = 0; i < k; ++i) divs.push_back(divs[i] * q);
+        }
+    }
+    std::sort(divs.rbegin(), divs.rend());
+    std::map<uint64_t, std::shared_ptr<const OrbPlan>> plans;
+    // one class: FFT-form chains when its orbits fill at least half a tile,
+    // else direct chains (len_direct; 0 = no direct form for this integrand)
+    auto build = [&](uint64_t m, int ln, bool f) -> std::shared_ptr<const OrbPlan> {
+        std::shared_ptr<const OrbPlan> pl;
+        if (is_prime32((uint32_t)m)) {
+            auto q = build_orbit_plan((uint32_t)m, (uint32_t)(a % m), ln, true, true);
+            if (q) {
+                auto w = std::make_shared<OrbPlan>(*q);
+                w->zero = false;   // the point 0 belongs to the small lattice
+                if (f) {
+                    w->apow.resize(2 * lq::kFftN);
+                    uint64_t t = 1 % m;
+                    for (int k = 0; k < lq::kFftN; ++k) {
+                        w->apow[2 * k] = (uint32_t)t;
+                        w->apow[2 * k + 1] = (uint32_t)((t << 32) / m);
+                        t = t * (a % m) % m;
+                    }
+                    fill_chain_starts(*w);
+                }
+                pl = w;
+            }
+        } else {
+            pl = build_orbit_plan_units((uint32_t)m, a, ln, f);
+        }
+        return pl;
+    };
+    auto plan_of = [&](uint64_t m) -> std::shared_ptr<const OrbPlan> {
+        auto hit = plans.find(m);
+        if (hit != plans.end()) return hit->second;
+        std::shared_ptr<const OrbPlan> pl;
+        if (fft) {
+            pl = build(m, len, true);
+            if (pl && 2 * (uint64_t)pl->h < (uint64_t)len) pl = nullptr;
+        }
+        if (!pl && len_direct > 0) pl = build(m, len_direct, false);
+        plans[m] = pl;
+        return pl;
+    };
+    uint64_t m0 = (n % 2 == 0) ? 2 : 1;
+    for (bool grew = true; grew;) {
+        grew = false;
+        for (uint64_t m : divs) {
+            if (m0 % m == 0) continue;
+            if (!plan_of(m)) {
+                m0 = m0 / gcd64(m0, m) * m;
+                grew = true;
+                break;
+            }
+        }
+        if (m0 > n / 4) break;
+    }
+    std::shared_ptr<const Pow2Plan> out;
+    if (m0 <= n / 4) {
+        auto P = std::make_shared<Pow2Plan>();
+        P->small_n = m0;
+        for (uint64_t m : divs)
+            if (m0 % m) {
+                P->levels.push_back(plan_of(m));
+                P->fft = P->fft || !P->levels.back()->apow.empty();
+            }
+        if (!P->levels.empty()) out = P;
+    }
     if (cache.size() > 64) cache.clear();
     cache[key] = out;
     return out;
@@ -1336,19 +1672,47 @@ std::shared_ptr<const Pow2Plan> pow2_for(const lq_integrand* f, uint64_t n, cons
     return P;
 }
 
+// Chains per tile of one level: two per FFT tile (one for the Gaussian form),
+// one per thread of the direct orbit kernel.
+uint64_t level_units_per_tile(const lq_integrand* f, const OrbPlan& lp) {
+    return lp.apow.empty() ? lq::kThreads : (is_quad_kind(f->kind) ? 1 : 2);
+}
+
+// Composite n (not a power of two) Korobov rules of the linear and Gaussian
+// families with gcd(a, n) = 1: the divisor-class levels of div_plan.
+std::shared_ptr<const Pow2Plan> divplan_for(const lq_integrand* f, uint64_t n, const uint64_t* z, bool* fft) {
+    *fft = false;
+    if (orbit_mode() == 0 || !z || f->d < 2 || !(is_lin_kind(f->kind) || is_quad_kind(f->kind))) return nullptr;
+    if (n < (1ull << 12) || n > (1ull << 31) || !(n & (n - 1)) || is_prime32((uint32_t)n)) return nullptr;
+    if (!f->beta || (is_quad_kind(f->kind) && !f->gamma)) return nullptr;
+    if (z[0] != 1) return nullptr;
+    const uint64_t a = z[1];
+    if (a < 2 || gcd64(a, n) != 1) return nullptr;
+    for (int j = 2; j < f->d; ++j)
+        if (z[j] != z[j - 1] * a % n) return nullptr;
+    const bool quad = is_quad_kind(f->kind);
+    const bool use_fft = fft_wanted(f, n);
+    int len_direct = lq::orb_len(quad ? lq::FAM_QUAD : lq::FAM_LIN);
+    const int cap = quad ? lq::kOrbQuadDims : lq::kOrbLinDims;
+    if (f->kind == LQ_FAM_LIN_PROG || (f->d + len_direct - 1) / len_direct * len_direct > cap) len_direct = 0;
+    if (!use_fft && len_direct == 0) return nullptr;
+    auto P = div_plan((uint32_t)n, (uint32_t)a, use_fft ? lq::kFftN - f->d + 1 : len_direct, use_fft, len_direct);
+    if (P) *fft = P->fft;
+    return P;
+}
+
 Layout layout_of(const lq_integrand* f, uint64_t n, const uint64_t* z) {
     Layout L;
     bool fft2 = false;
-    if ((L.p2 = pow2_for(f, n, z, &fft2))) {
+    if ((L.p2 = pow2_for(f, n, z, &fft2)) || (L.p2 = divplan_for(f, n, z, &fft2))) {
         L.fft = fft2;
-        const bool quad = is_quad_kind(f->kind);
-        const uint64_t tu = fft2 ? (quad ? 1 : 2) : lq::kThreads;
         int64_t t = 0;
-        for (const auto& lp : L.p2->levels) {
+        for (const auto& lp : L.p2->levels) {   // each level: FFT-form or direct chains
+            const uint64_t tu = level_units_per_tile(f, *lp);
             L.seg.push_back(t);
             t += (int64_t)((lp->units + tu - 1) / tu);
         }
-        L.small_n = 1ull << L.p2->m0;
+        L.small_n = L.p2->small_n;
         L.small_tp = tile_points(f, L.small_n);
         L.seg.push_back(t);
         t += (int64_t)((L.small_n + L.small_tp - 1) / L.small_tp);
@@ -1404,20 +1768,20 @@ int launch_pow2_tiles(lq_ctx* c, const lq_integrand* f, const uint64_t* z, const
                       double* tiles_dev) {
     int rc;
     const int nl = (int)L.p2->levels.size();
-    const bool quad = is_quad_kind(f->kind);
-    const uint64_t tu = L.fft ? (quad ? 1 : 2) : lq::kThreads;
     for (int l = 0; l <= nl; ++l) {
         const int64_t lo = std::max(T0, L.seg[l]), hi = std::min(T1, L.seg[l + 1]);
         if (hi <= lo) continue;
         double* out = tiles_dev + (lo - T0);
         if (l < nl) {
             const OrbPlan& lp = *L.p2->levels[l];
-            const uint64_t unit0 = (uint64_t)(lo - L.seg[l]) * tu;
-            rc = L.fft ? launch_orbit_fft(c, f, lp, unit0, hi - lo, out) : launch_orbit(c, f, lp, unit0, hi - lo, out);
+            const uint64_t unit0 = (uint64_t)(lo - L.seg[l]) * level_units_per_tile(f, lp);
+            rc = lp.apow.empty() ? launch_orbit(c, f, lp, unit0, hi - lo, out)
+                                 : launch_orbit_fft(c, f, lp, unit0, hi - lo, out);
         } else {
-            // the lattice mod 2^m0: every level too short for chains, and the point 0
+            // the small lattice (mod 2^m0, or m0 for composite n): every class
+            // too short for chains, and the point 0
             std::vector<uint64_t> zs(f->d);
-            for (int j = 0; j < f->d; ++j) zs[j] = z[j] & (L.small_n - 1);
+            for (int j = 0; j < f->d; ++j) zs[j] = z[j] % L.small_n;
             const uint64_t base = (uint64_t)(lo - L.seg[l]) * L.small_tp;
             const uint64_t end = std::min<uint64_t>((uint64_t)(hi - L.seg[l]) * L.small_tp, L.small_n);
             rc = launch_tiles(c, f, L.small_n, zs.data(), base, end, hi - lo, out);
@@ -1620,6 +1984,47 @@ int lq_lattice_partials(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint
         if ((rc = launch_tiles(c, f, n, z, base, end, ntiles, (double*)tiles, L.pair))) return rc;
     }
     return super_partials(c, L, (const double*)tiles, ntiles, s_end - s_begin, out_dev);
+}
+
+int lq_layout_cover(const lq_integrand* f, uint64_t n, const uint64_t* z, int64_t* missed, int64_t* repeated) {
+    int rc;
+    if ((rc = check_integrand(f)) || (rc = check_lattice(n, z, f->d))) return rc;
+    if (!missed || !repeated) return fail(LQ_ERR_VALUE, "null output");
+    if (n > (1ull << 26)) return fail(LQ_ERR_UNSUPPORTED, "cover check supports n <= 2^26");
+    const Layout L = layout_of(f, n, z);
+    std::vector<uint8_t> hits(n, 0);
+    auto mark = [&](uint64_t i) { if (hits[i] < 255) ++hits[i]; };
+    auto mark_plan = [&](const OrbPlan& p, uint64_t scale) {   // points scale * u, u in the plan's unit classes
+        const uint64_t m = p.n;
+        for (uint64_t cs = 0; cs < p.G.size(); ++cs) {
+            uint64_t u = p.G[cs];
+            for (uint64_t t = 0; t < p.h; ++t) {
+                const uint64_t i = scale * u % n;
+                mark(i);
+                if (p.mirror) mark((n - i) % n);
+                u = u * p.a % m;
+            }
+        }
+        if (p.zero) mark(0);
+    };
+    if (L.p2) {
+        for (const auto& lp : L.p2->levels) mark_plan(*lp, n / lp->n);
+        for (uint64_t t = 0; t < L.small_n; ++t) mark(n / L.small_n * t);
+    } else if (L.orb) {
+        mark_plan(*L.orb, 1);
+    } else if (L.pair) {
+        for (uint64_t i = 0; i <= n / 2; ++i) { mark(i); if (i && 2 * i != n) mark(n - i); }
+    } else {
+        for (uint64_t i = 0; i < n; ++i) mark(i);
+    }
+    int64_t miss = 0, rep = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (hits[i] == 0) ++miss;
+        else if (hits[i] > 1) ++rep;
+    }
+    *missed = miss;
+    *repeated = rep;
+    return LQ_OK;
 }
 
 int lq_reduce_sum(lq_ctx* c, const double* vals, int64_t count, double* out) {

@@ -454,3 +454,36 @@ def test_reference_import_shim_resolves():
         for k in [k for k in sys.modules if k == "latquad" or k.startswith("latquad.")]:
             del sys.modules[k]
         sys.modules.update(saved)
+
+
+def test_composite_modulus_layouts_cover_the_lattice():
+    """Korobov rules over composite n: the divisor-class plan (a unit-group
+    orbit plan per divisor m of n, plus the small lattice mod m0)
+    covers every lattice index exactly once, point and mirror counted
+    together (lq_layout_cover, host only) -- for odd, even, prime-power and
+    many-factor moduli, direct chains (d = 8) and FFT chains (d = 120)."""
+    import ctypes as C
+    import math
+    import random
+    from paper_2404_08867_b200 import _native as N, engine
+    if not os.path.exists(N.LIB_PATH):
+        pytest.skip("liblq.so not built")
+    h = N.lib()
+    rng = random.Random(41)
+    used = set()
+    cases = [(n, 8) for n in (2 * 5**4 * 4, 2 * 3**7, 10000, 4 * 7**5, 12289 * 3, 30030, 65535, 3**10, 5**7,
+                              7 * 11 * 13 * 17 * 19, 1000000, 2**20 - 1, 1009 * 1013)]
+    cases += [(n, 120) for n in (1000000, 3 * 5 * 7 * 11 * 13 * 17 * 19, 2**22 - 2)]
+    for n, d in cases:
+        for _ in range(3):
+            a = rng.randrange(2, n)
+            while math.gcd(a, n) != 1:
+                a = rng.randrange(2, n)
+            text = "exp(" + " + ".join(f"{0.3 + 0.01 * j}*x[{j + 1}]" for j in range(d)) + ")"
+            pi = engine.plain_integrand(lq.parse(text, d), d)
+            z = lq.korobov_vector(a, n, d).z_reduced_array()
+            miss, rep = C.c_int64(), C.c_int64()
+            N.check(h.lq_layout_cover(C.byref(pi.struct), n, N.as_ptr(z), C.byref(miss), C.byref(rep)))
+            assert (miss.value, rep.value) == (0, 0), (n, a, d, miss.value, rep.value)
+            used.add(N.lattice_layout(pi.struct, n, z).mode)
+    assert N.LAYOUT_ORBIT_POW2 in used
