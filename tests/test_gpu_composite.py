@@ -85,3 +85,37 @@ def test_composite_cfg5_scale(lq, monkeypatch):
     mode, got, ref = _sums(lq, cfg.text, cfg.d, n, a, monkeypatch)
     assert mode == N.LAYOUT_ORBIT_POW2
     assert math.isclose(got, ref, rel_tol=1e-12), (got, ref)
+
+
+@pytest.mark.parametrize("n,d", [(10**8, 1000), (3 * 5 * 7 * 11 * 13 * 17 * 19 * 4, 40)])
+def test_composite_partials_sharded_bit_identical(lq, n, d, monkeypatch):
+    """The divisor-class layout through the multi-GPU building blocks: three
+    shards of its super-chunks (levels with FFT-form and direct chains, the
+    small lattice) reproduce the one-launch sum bit for bit."""
+    import ctypes as C
+    import torch
+    from paper_2404_08867_b200 import _native as N, engine
+    from paper_2404_08867_b200.distributed import shard_range
+    rng = random.Random(n)
+    a = rng.randrange(2, n)
+    while math.gcd(a, n) != 1:
+        a = rng.randrange(2, n)
+    f = lq.parse(_text("expabs", d, rng), d)
+    z = lq.korobov_vector(a, n, d).z_reduced_array()
+    pi = engine.plain_integrand(f, d)
+    lay = N.lattice_layout(pi.struct, n, z)
+    assert lay.mode == N.LAYOUT_ORBIT_POW2 and lay.n_supers >= 2, lay
+    h, ctx = N.lib(), N.ctx()
+    S = lay.n_supers
+    one = torch.zeros(S, dtype=torch.float64, device="cuda")
+    N.check(h.lq_lattice_partials(ctx, C.byref(pi.struct), n, N.as_ptr(z), 0, S, C.c_void_p(one.data_ptr())))
+    many = torch.zeros(S, dtype=torch.float64, device="cuda")
+    for r in range(3):
+        lo, hi = shard_range(S, r, 3)
+        N.check(h.lq_lattice_partials(ctx, C.byref(pi.struct), n, N.as_ptr(z), lo, hi,
+                                      C.c_void_p(many.data_ptr() + 8 * lo)))
+    torch.cuda.synchronize()
+    assert torch.equal(one.view(torch.int64), many.view(torch.int64))
+    out = C.c_double()
+    N.check(h.lq_reduce_sum(ctx, C.c_void_p(one.data_ptr()), S, C.byref(out)))
+    assert out.value == engine.lattice_sum(pi, n, z)
