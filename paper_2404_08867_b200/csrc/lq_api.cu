@@ -970,8 +970,25 @@ std::shared_ptr<const OrbPlan> build_orbit_plan_units(uint32_t m, uint32_t a_ful
             }
         } else {
             const uint64_t ord = q / pe.first * (pe.first - 1);
-            const uint64_t g = primitive_root_pe(pe.first, pe.second);
-            const uint64_t k = dlog_bsgs(g, a % q, ord, q);
+            // (generator, log of a) per prime power, shared by every divisor
+            // of n that contains it (div_plan builds ~all of them)
+            static std::mutex dl_mu;
+            static std::map<std::pair<uint64_t, uint64_t>, std::pair<uint64_t, uint64_t>> dl_cache;
+            uint64_t g, k;
+            {
+                std::lock_guard<std::mutex> lk(dl_mu);
+                auto key = std::make_pair(q, a % q);
+                auto hit = dl_cache.find(key);
+                if (hit != dl_cache.end()) {
+                    g = hit->second.first;
+                    k = hit->second.second;
+                } else {
+                    g = primitive_root_pe(pe.first, pe.second);
+                    k = dlog_bsgs(g, a % q, ord, q);
+                    if (dl_cache.size() > 4096) dl_cache.clear();
+                    dl_cache[key] = {g, k};
+                }
+            }
             if (k == UINT64_MAX) return nullptr;
             comp.push_back({q, ord, g, 0});
             al.push_back(k);
@@ -1044,33 +1061,43 @@ std::shared_ptr<const OrbPlan> build_orbit_plan_units(uint32_t m, uint32_t a_ful
     p->qc = (uint32_t)((h + len - 1) / len);
     p->units = cosets * p->qc;
     p->G.resize(cosets);
+    // CRT idempotents e_q (e_q = 1 mod q, 0 mod the other prime powers) and
+    // the per-component powers gen_c^(x_c), advanced incrementally with the
+    // mixed-radix counter over the box
+    std::vector<uint64_t> qs, eq;
+    std::vector<int> comp_q(r);
+    for (int c = 0; c < r; ++c) {
+        if (c == 0 || comp[c].q != comp[c - 1].q) qs.push_back(comp[c].q);
+        comp_q[c] = (int)qs.size() - 1;
+    }
+    for (uint64_t q : qs) {
+        const uint64_t Mq = m / q;
+        int64_t e0 = (int64_t)(Mq % q), e1 = (int64_t)q, s0 = 1, s1 = 0;
+        while (e1) { const int64_t qq = e0 / e1; int64_t tmp = e0 - qq * e1; e0 = e1; e1 = tmp; tmp = s0 - qq * s1; s0 = s1; s1 = tmp; }
+        const uint64_t inv = (uint64_t)((s0 % (int64_t)q + (int64_t)q) % (int64_t)q);
+        eq.push_back(mulmod64(Mq % m, inv, m));
+    }
     std::vector<int64_t> x(r, 0);
+    std::vector<uint64_t> pw(r, 1);   // gen_c^(x_c) mod q_c
+    for (int c = 0; c < r; ++c) pw[c] = 1 % comp[c].q;
     for (uint64_t idx = 0; idx < cosets; ++idx) {
-        uint64_t u = 0, M = 1;   // CRT accumulation
-        int c = 0;
-        while (c < r) {
-            const uint64_t q = comp[c].q;
+        uint64_t u = 0;
+        size_t c = 0;
+        for (size_t qi = 0; qi < qs.size(); ++qi) {
+            const uint64_t q = qs[qi];
             uint64_t v = 1 % q;
-            int c2 = c;
-            for (; c2 < r && comp[c2].q == q; ++c2) v = mulmod64(v, powmod64(comp[c2].gen, (uint64_t)x[c2], q), q);
-            // u mod M and v mod q -> u mod M q
-            uint64_t t = (v + q - u % q) % q;
-            // M^-1 mod q by extended Euclid
-            int64_t e0 = (int64_t)(M % q), e1 = (int64_t)q, s0 = 1, s1 = 0;
-            while (e1) { const int64_t qq = e0 / e1; int64_t tmp = e0 - qq * e1; e0 = e1; e1 = tmp; tmp = s0 - qq * s1; s0 = s1; s1 = tmp; }
-            const uint64_t inv = (uint64_t)((s0 % (int64_t)q + (int64_t)q) % (int64_t)q);
-            t = mulmod64(t, inv, q);
-            u += M * t;
-            M *= q;
-            c = c2;
+            for (; c < (size_t)r && comp[c].q == q; ++c) v = v * pw[c] % q;
+            u = (u + v * eq[qi]) % m;
         }
-        p->G[idx] = (uint32_t)(u % m);
+        p->G[idx] = (uint32_t)u;
         for (int k = r - 1; k >= 0; --k) {   // mixed-radix increment over the box
-            if (++x[k] < diag[k]) break;
+            if (++x[k] < diag[k]) { pw[k] = pw[k] * comp[k].gen % comp[k].q; break; }
             x[k] = 0;
+            pw[k] = 1 % comp[k].q;
         }
     }
-    auto mulm = [&](uint64_t xx, uint64_t yy) { return mulmod64(xx, yy, m); };
+    (void)comp_q;
+    auto mulm = [&](uint64_t xx, uint64_t yy) { return xx * yy % m; };   // operands < m < 2^32
     uint64_t am = 1;
     for (int i = 0; i < len; ++i) am = mulm(am, a);
     p->Alo.resize(4096);
