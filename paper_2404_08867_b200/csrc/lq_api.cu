@@ -1307,7 +1307,11 @@ int orbit_tables(lq_ctx* c, const OrbPlan& p, const uint32_t** G, const uint32_t
     const size_t bytes = 4 * (nG + nlo + nhi + pad + np + ns);
     auto it = c->orb_tabs.find(p.id);
     if (it == c->orb_tabs.end()) {
-        if (c->orb_tabs.size() >= 64) {   // bounded cache: drop everything (plans are rebuilt cheaply)
+        // bounded cache (a composite-n layout holds one plan per divisor class,
+        // 2^31 - 2: ~190): drop everything past 1024 plans or 512 MB
+        size_t held = 0;
+        for (auto& kv : c->orb_tabs) held += kv.second.second;
+        if (c->orb_tabs.size() >= 1024 || held + bytes > (512u << 20)) {
             CK(cudaStreamSynchronize(c->stream));
             for (auto& kv : c->orb_tabs) cudaFree(kv.second.first);
             c->orb_tabs.clear();
