@@ -1713,7 +1713,8 @@ uint64_t level_units_per_tile(const lq_integrand* f, const OrbPlan& lp) {
 // families with gcd(a, n) = 1: the divisor-class levels of div_plan.
 std::shared_ptr<const Pow2Plan> divplan_for(const lq_integrand* f, uint64_t n, const uint64_t* z, bool* fft) {
     *fft = false;
-    if (orbit_mode() == 0 || !z || f->d < 2 || !(is_lin_kind(f->kind) || is_quad_kind(f->kind))) return nullptr;
+    if (orbit_mode() == 0 || !z || f->d < 2) return nullptr;
+    if (!(is_lin_kind(f->kind) || is_quad_kind(f->kind) || f->kind == LQ_FAM_LIN_PROG)) return nullptr;
     if (n < (1ull << 12) || n > (1ull << 31) || !(n & (n - 1)) || is_prime32((uint32_t)n)) return nullptr;
     if (!f->beta || (is_quad_kind(f->kind) && !f->gamma)) return nullptr;
     if (z[0] != 1) return nullptr;

@@ -119,3 +119,20 @@ def test_composite_partials_sharded_bit_identical(lq, n, d, monkeypatch):
     out = C.c_double()
     N.check(h.lq_reduce_sum(ctx, C.c_void_p(one.data_ptr()), S, C.byref(out)))
     assert out.value == engine.lattice_sum(pi, n, z)
+
+
+def test_composite_modulus_program_outer(lq, monkeypatch):
+    """A function of one linear form outside the closed families (the outer G
+    as bytecode, FFT-form chains only) over a composite modulus: the classes
+    with long orbits take FFT chains, the rest the small lattice."""
+    from paper_2404_08867_b200 import _native as N
+    rng = random.Random(77)
+    n, d = 10**8, 200
+    a = rng.randrange(2, n)
+    while math.gcd(a, n) != 1:
+        a = rng.randrange(2, n)
+    c = [rng.uniform(0.2, 1.0) * 3.0 / d for _ in range(d)]
+    lin = " + ".join(f"{cj!r}*x[{j + 1}]" for j, cj in enumerate(c))
+    mode, got, ref = _sums(lq, f"1/(1 + (2*({lin}) - 0.8)^2)", d, n, a, monkeypatch)
+    assert mode == N.LAYOUT_ORBIT_POW2, mode
+    assert math.isclose(got, ref, rel_tol=1e-12), (got, ref)
