@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define LQ_ABI_VERSION 10
+#define LQ_ABI_VERSION 11
 
 #define LQ_OK 0
 #define LQ_ERR_VALUE (-1)
@@ -154,6 +154,19 @@ int lq_lattice_layout(const lq_integrand* f, uint64_t n, const uint64_t* z_reduc
 int lq_lattice_partials(lq_ctx* ctx, const lq_integrand* f, uint64_t n, const uint64_t* z_reduced,
                         int64_t s_begin, int64_t s_end, double* out_dev);
 /* Fixed pairwise tree over vals_dev[0..count); result to host *out. */
+/* ---- MDI-LR level collapse for G(alpha1 + <beta1, y>, alpha2 + <beta2, y>):
+ * two commensurate forms (exprcore.py:139-169 collects the partial sums with
+ * equal pairs).  Level l moves the joint distribution of
+ * k = (sum |m1_l| t, sum |m2_l| t) by node t (t -> N-1-t for a negative step),
+ * on a K1 x K2 grid (K1 K2 <= LQ_LINFORM2_MAX_SUPPORT); then
+ * sum_k p(k) G(h1 (m01 + 2 k1), h2 (m02 + 2 k2)) over fixed tiles of LQ_TILE
+ * entries.  G: program of variables 0 and 1.  Sharding and outputs as
+ * lq_mdi_linform.                                                             */
+#define LQ_LINFORM2_MAX_SUPPORT (((int64_t)1) << 25)
+int lq_mdi_linform2(lq_ctx* ctx, const lq_program* G, int32_t n_levels, const int64_t* m1, const int64_t* m2,
+                    const int32_t* counts, double h1, int64_t m01, double h2, int64_t m02, int32_t shard,
+                    int32_t nshards, double* tiles_dev, int64_t tiles_cap, double* out);
+
 /* Host-only check of the full-lattice layout of (f, n, z) (n <= 2^26): how
  * many lattice indices the layout's units (chains and their mirrors, levels,
  * the small lattice, mirror pairs or plain indices) miss and how many they

@@ -25,7 +25,7 @@ LQ_ERR_CUDA, LQ_ERR_UNSUPPORTED, LQ_ERR_NOMEM = -4, -5, -6
 LQ_TILE, LQ_SUPER_TILES, LQ_NODE_BLOCK = 4096, 1024, 256
 LQ_FACTOR_SUPPLIED = 1
 
-ABI_VERSION = 10   # LQ_ABI_VERSION of include/lq.h these ctypes structs match
+ABI_VERSION = 11   # LQ_ABI_VERSION of include/lq.h these ctypes structs match
 FAM = {"program": 0, "lin_exp": 1, "lin_sincos": 2, "lin_expabs": 3, "quad_exp": 4, "lin_pow": 5, "quad_sincos": 6,
        "prod_quad": 7, "lin_prog": 8}
 
@@ -90,6 +90,8 @@ _SIGS = {
     "lq_mdi_combine": [_P, _P, _P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, C.c_int32, _P],
     "lq_mdi_sum": [_P, _P, C.c_int32, _P, C.c_int32, _P, C.c_int64, _P, _P, _P, _P, _P, C.c_int32, _P],
     "lq_mdi_expabs": [_P, C.c_int32, _P, _P, C.c_double, _P, _P, C.c_int32, C.c_double, _P, _P],
+    "lq_mdi_linform2": [_P, C.POINTER(Program), C.c_int32, _P, _P, _P, C.c_double, C.c_int64, C.c_double,
+                        C.c_int64, C.c_int32, C.c_int32, _P, C.c_int64, C.POINTER(C.c_double)],
     "lq_mdi_linform_w": [_P, C.POINTER(Program), C.c_int32, _P, _P, _P, C.c_double, C.c_double, C.c_int64,
                          C.c_int32, C.c_int32, _P, C.c_int64, C.POINTER(C.c_double)],
     "lq_mdi_linform": [_P, C.POINTER(Program), C.c_int32, _P, _P, C.c_double, C.c_double, C.c_int64, C.c_int32,

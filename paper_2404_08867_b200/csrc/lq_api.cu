@@ -2587,6 +2587,85 @@ int lq_mdi_linform_w(lq_ctx* c, const lq_program* G, int32_t n_levels, const int
     return read_scalar(c, r, out);
 }
 
+int lq_mdi_linform2(lq_ctx* c, const lq_program* G, int32_t n_levels, const int64_t* m1, const int64_t* m2,
+                    const int32_t* counts, double h1, int64_t m01, double h2, int64_t m02, int32_t shard,
+                    int32_t nshards, double* tiles_dev, int64_t tiles_cap, double* out) {
+    int rc = set_dev(c);
+    if (rc) return rc;
+    if (!G || !G->insn || G->n_insn < 1) return fail(LQ_ERR_VALUE, "null program");
+    if (G->n_vars > 2) return fail(LQ_ERR_VALUE, "G must use variables 0 and 1 only, uses %d", G->n_vars);
+    if (n_levels < 1 || !m1 || !m2 || !counts) return fail(LQ_ERR_VALUE, "bad levels");
+    if (nshards < 1 || shard < 0 || shard >= nshards) return fail(LQ_ERR_VALUE, "bad shard %d of %d", shard, nshards);
+    if (!out) return fail(LQ_ERR_VALUE, "null output");
+    if (!tiles_dev && nshards != 1) return fail(LQ_ERR_VALUE, "sharded calls need tiles_dev");
+    const int ns = pick_slots(G->n_slots);
+    if (ns < 0) return fail(LQ_ERR_UNSUPPORTED, "program needs %d slots (max %d)", G->n_slots, LQ_MAX_SLOTS);
+    int64_t K1 = 1, K2 = 1;
+    std::vector<lq::Lin2Level> lv;
+    for (int l = 0; l < n_levels; ++l) {
+        if (counts[l] < 1) return fail(LQ_ERR_VALUE, "level %d: N = %d", l, counts[l]);
+        const int64_t a1 = m1[l] < 0 ? -m1[l] : m1[l], a2 = m2[l] < 0 ? -m2[l] : m2[l];
+        if (a1 > LQ_LINFORM2_MAX_SUPPORT / counts[l] || a2 > LQ_LINFORM2_MAX_SUPPORT / counts[l])
+            return fail(LQ_ERR_UNSUPPORTED, "level %d step too large", l);
+        K1 += a1 * (counts[l] - 1);
+        K2 += a2 * (counts[l] - 1);
+        if (K1 > LQ_LINFORM2_MAX_SUPPORT || K2 > LQ_LINFORM2_MAX_SUPPORT || K1 * K2 > LQ_LINFORM2_MAX_SUPPORT)
+            return fail(LQ_ERR_UNSUPPORTED, "joint support exceeds %lld points", (long long)LQ_LINFORM2_MAX_SUPPORT);
+        lv.push_back({a1, a2, counts[l], (m1[l] < 0 ? 1 : 0) | (m2[l] < 0 ? 2 : 0)});
+    }
+    const int64_t K = K1 * K2, T = (K + LQ_TILE - 1) / LQ_TILE;
+    if (tiles_dev && tiles_cap < T)
+        return fail(LQ_ERR_VALUE, "tiles_dev holds %lld tiles, need %lld", (long long)tiles_cap, (long long)T);
+    void *dp, *dq, *dg;
+    if ((rc = upload(c, B_PROG, G->insn, sizeof(lq_insn) * G->n_insn, &dg))) return rc;
+    if ((rc = dev_buf(c, B_AUX1, sizeof(double) * K, &dp))) return rc;
+    if ((rc = dev_buf(c, B_AUX2, sizeof(double) * K, &dq))) return rc;
+    double* cur = (double*)(n_levels % 2 ? dq : dp);   // the last level lands in dp
+    double* nxt = (double*)(n_levels % 2 ? dp : dq);
+    t_begin(c);
+    lq::k_fill<<<1, 32, 0, c->stream>>>(cur, 1, 1.0);
+    c->launches++;
+    int64_t k1 = 1, k2 = 1;
+    for (int l = 0; l < n_levels; ++l) {
+        const int64_t k1n = k1 + lv[l].m1 * (lv[l].n - 1), k2n = k2 + lv[l].m2 * (lv[l].n - 1);
+        const int grid = (int)std::min<int64_t>((k1n * k2n + lq::kThreads - 1) / lq::kThreads, (int64_t)c->sm_count * 8);
+        lq::k_linform2_level<<<grid, lq::kThreads, 0, c->stream>>>(cur, k1, k2, lv[l], nxt, k1n, k2n);
+        c->launches++;
+        CK(cudaGetLastError());
+        std::swap(cur, nxt);
+        k1 = k1n;
+        k2 = k2n;
+    }
+    const int64_t t0 = (int64_t)shard * T / nshards, t1 = (int64_t)(shard + 1) * T / nshards;
+    void* tiles = tiles_dev;
+    if (!tiles) {
+        if ((rc = dev_buf(c, B_TILES, sizeof(double) * T, &tiles))) return rc;
+    } else {
+        CK(cudaMemsetAsync(tiles, 0, sizeof(double) * T, c->stream));
+    }
+    if (t1 > t0) {
+        const int grid = (int)std::min<int64_t>(t1 - t0, (int64_t)c->sm_count * 4);
+        if (ns == 32)
+            lq::k_linform2_eval<32><<<grid, lq::kThreads, 0, c->stream>>>(
+                (const lq_insn*)dg, G->n_insn, G->result, (const double*)dp, K1, K2, h1, (double)m01, h2,
+                (double)m02, t0, t1, 0, (double*)tiles);
+        else
+            lq::k_linform2_eval<LQ_MAX_SLOTS><<<grid, lq::kThreads, 0, c->stream>>>(
+                (const lq_insn*)dg, G->n_insn, G->result, (const double*)dp, K1, K2, h1, (double)m01, h2,
+                (double)m02, t0, t1, 0, (double*)tiles);
+        c->launches++;
+        CK(cudaGetLastError());
+    }
+    t_end(c);
+    if (tiles_dev) {
+        *out = (double)T;
+        return LQ_OK;
+    }
+    double* r;
+    if ((rc = reduce_dev(c, (const double*)tiles, T, &r))) return rc;
+    return read_scalar(c, r, out);
+}
+
 int lq_fp64_peak(lq_ctx* c, int32_t iters, double* tflops, float* ms) {
     int rc = set_dev(c);
     if (rc) return rc;

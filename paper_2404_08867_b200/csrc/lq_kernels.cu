@@ -1610,6 +1610,68 @@ __global__ void __launch_bounds__(kThreads) k_linform_level(const double* __rest
         q[s] = lin_conv_point(p, k_old, s, m, n, w);
 }
 
+// ---- two linear forms: the joint distribution on a K1 x K2 grid (row-major)
+struct Lin2Level {
+    int64_t m1, m2;     // |m1_j|, |m2_j| (either may be 0)
+    int32_t n;          // N_j nodes
+    int32_t flip;       // bit 0: form 1 takes node N-1-t (negative step), bit 1: form 2
+};
+
+// q[s1, s2] = (1/N) sum_t p[s1 - m1 t1(t), s2 - m2 t2(t)] over the new K1n x K2n grid
+__global__ void __launch_bounds__(kThreads) k_linform2_level(const double* __restrict__ p, int64_t k1o, int64_t k2o,
+                                                             Lin2Level L, double* __restrict__ q, int64_t k1n,
+                                                             int64_t k2n) {
+    const int64_t total = k1n * k2n;
+    for (int64_t idx = blockIdx.x * (int64_t)kThreads + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kThreads) {
+        const int64_t s1 = idx / k2n, s2 = idx - s1 * k2n;
+        double a0 = 0.0, a1 = 0.0;
+        for (int t = 0; t < L.n; ++t) {
+            const int64_t t1 = (L.flip & 1) ? L.n - 1 - t : t, t2 = (L.flip & 2) ? L.n - 1 - t : t;
+            const int64_t k1 = s1 - L.m1 * t1, k2 = s2 - L.m2 * t2;
+            if (k1 >= 0 && k1 < k1o && k2 >= 0 && k2 < k2o) {
+                if (t & 1) a1 += p[k1 * k2o + k2];
+                else a0 += p[k1 * k2o + k2];
+            }
+        }
+        q[idx] = (a0 + a1) / (double)L.n;
+    }
+}
+
+struct Src2 {
+    double s1, s2;
+    __device__ __forceinline__ double x(int b) const { return b == 0 ? s1 : s2; }
+};
+
+// sum over the K1 x K2 support of p G(h1 (m01 + 2 k1), h2 (m02 + 2 k2)), tiles of
+// kTile entries [t_begin, t_end) into tiles[t - t_out0]
+template <int NS>
+__global__ void __launch_bounds__(kThreads) k_linform2_eval(const lq_insn* __restrict__ prog, int n_insn, int result,
+                                                            const double* __restrict__ p, int64_t K1, int64_t K2,
+                                                            double h1, double m01, double h2, double m02,
+                                                            int64_t t_begin, int64_t t_end, int64_t t_out0,
+                                                            double* __restrict__ tiles) {
+    __shared__ double sh[8];
+    double slot[NS];
+    const int64_t K = K1 * K2;
+    for (int64_t tile = t_begin + blockIdx.x; tile < t_end; tile += gridDim.x) {
+        double s = 0.0;
+        #pragma unroll 1
+        for (int q = 0; q < kPts; ++q) {
+            const int64_t k = tile * kTile + (int64_t)q * kThreads + threadIdx.x;
+            if (k < K) {
+                const double w = p[k];
+                if (w != 0.0) {
+                    const int64_t k1 = k / K2, k2 = k - k1 * K2;
+                    Src2 src{h1 * (m01 + 2.0 * (double)k1), h2 * (m02 + 2.0 * (double)k2)};
+                    s += w * run_program<NS>(prog, n_insn, result, src, slot);
+                }
+            }
+        }
+        s = block_sum(s, sh);
+        if (threadIdx.x == 0) tiles[tile - t_out0] = s;
+    }
+}
+
 // sum_k p[k] G(alpha + h (m0 + 2k)) over tiles of kTile support points
 // (thread-strided inside the tile, block_sum tree): tiles [t_begin, t_end),
 // partial of tile t to tiles[t - t_out0].

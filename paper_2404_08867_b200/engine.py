@@ -15,8 +15,8 @@ import numpy as np
 
 from . import _native as N
 from .expr import Expr, UnassignedVariableError, as_expr, evaluate, free_vars
-from .lower import (Program, compile_program, linear_outer, recognize_linear_program, recognize_plain, separate,
-                    weighted_linear_outer)
+from .lower import (Program, compile_program, linear_outer, linear_outer2, recognize_linear_program, recognize_plain,
+                    separate, weighted_linear_outer)
 
 __all__ = ["PlainIntegrand", "plain_integrand", "lattice_sum", "tensor_program", "eval_array", "SeparablePlan",
            "separable_plan", "mdi_separable_sum"]
@@ -567,6 +567,97 @@ class LinformPlan:
 
 
 _lin_cache = _LRU(32)
+
+
+def form_quantum(beta, counts):
+    """Commensurate steps of one linear form on the midpoint grid: direction j
+    contributes beta_j (t + 1/2)/N_j = h m_j (2t + 1) with integer m_j.
+    Returns (h as an exact rational, {axis: m_j}) or None (LinformPlan's rule:
+    ratios snapped to denominators <= 2^20 within 2^-50)."""
+    from fractions import Fraction
+    axes = sorted(beta)
+    b_ref = Fraction(beta[axes[0]])
+    steps = []
+    for j in axes:
+        rho = Fraction(beta[j]) / b_ref
+        if rho.denominator > _RATIO_DEN:
+            approx = rho.limit_denominator(_RATIO_DEN)
+            if abs(approx - rho) > abs(rho) * Fraction(1, 1 << 50):
+                return None
+            rho = approx
+        steps.append(rho / (2 * int(counts[j - 1])))
+    den = math.lcm(*(r.denominator for r in steps))
+    nums = [int(r * den) for r in steps]
+    g = math.gcd(*nums)
+    return b_ref * Fraction(g, den), {j: v // g for j, v in zip(axes, nums)}
+
+
+LINFORM2_MAX_SUPPORT = 1 << 25     # entries of the 2-D distribution (two buffers of 256 MB)
+
+
+class Linform2Plan:
+    """G(<beta1, y>, <beta2, y>) with both forms commensurate: the joint
+    distribution of the two partial forms, k = (sum_j |m1_j| t1_j, sum_j
+    |m2_j| t2_j) with t_i = t or N - 1 - t by the sign of m_i_j, convolved one
+    direction per level on a K1 x K2 grid (lq_mdi_linform2)."""
+
+    def __init__(self, e, counts):
+        self.ok = False
+        lo = linear_outer2(e)
+        if lo is None:
+            return
+        d = len(counts)
+        for beta in (lo.beta1, lo.beta2):
+            if any(not 1 <= j <= d for j in beta) or not all(math.isfinite(c) for c in beta.values()):
+                return
+        q1, q2 = form_quantum(lo.beta1, counts), form_quantum(lo.beta2, counts)
+        if q1 is None or q2 is None:
+            return
+        (h1, m1), (h2, m2) = q1, q2
+        axes = sorted(set(m1) | set(m2), reverse=True)   # the reference strips the last axis first
+        self.m1 = np.asarray([m1.get(j, 0) for j in axes], dtype=np.int64)
+        self.m2 = np.asarray([m2.get(j, 0) for j in axes], dtype=np.int64)
+        self.n = np.asarray([int(counts[j - 1]) for j in axes], dtype=np.int32)
+        nn = self.n.astype(np.int64)
+        k1 = np.cumsum(np.abs(self.m1) * (nn - 1)) + 1
+        k2 = np.cumsum(np.abs(self.m2) * (nn - 1)) + 1
+        sizes = k1 * k2
+        self.K1, self.K2 = int(k1[-1]), int(k2[-1])
+        self.support = self.K1 * self.K2
+        if self.support > LINFORM2_MAX_SUPPORT or int(np.sum(sizes * nn)) > LINFORM_MAX_WORK:
+            return
+        self.m01 = sum(v if v > 0 else v * (2 * int(counts[j - 1]) - 1) for j, v in m1.items())
+        self.m02 = sum(v if v > 0 else v * (2 * int(counts[j - 1]) - 1) for j, v in m2.items())
+        if max(abs(self.m01) + 2 * self.K1, abs(self.m02) + 2 * self.K2) >= 2**53:
+            return
+        self.level_support = tuple(int(v) for v in sizes)
+        self.h1, self.h2 = float(h1), float(h2)
+        self.G = lo.G
+        self.prog = compile_program(lo.G)
+        self.tiles = -(-self.support // N.LQ_TILE)
+        self.ok = True
+
+
+def linform2_plan(g, counts):
+    e = as_expr(g)
+    return _lin_cache.get_or((e, tuple(int(c) for c in counts), 2), lambda: Linform2Plan(e, counts))
+
+
+def mdi_linform2_mean(plan, comm=None):
+    """Grid mean of G(<beta1, y>, <beta2, y>) (lq_mdi_linform2); with comm
+    (size > 1) the evaluation tiles of the joint support are sharded."""
+    ins = np.ascontiguousarray(plan.prog.insn)
+    p = N.Program(ins.ctypes.data, len(ins), plan.prog.n_slots, plan.prog.result, plan.prog.n_vars, None)
+    out = C.c_double()
+    args = (C.byref(p), len(plan.n), N.as_ptr(plan.m1), N.as_ptr(plan.m2), N.as_ptr(plan.n), plan.h1,
+            int(plan.m01), plan.h2, int(plan.m02))
+    if comm is not None and comm.size > 1:
+        tiles = comm.zeros(plan.tiles)
+        N.check(N.lib().lq_mdi_linform2(comm.ctx(), *args, comm.rank, comm.size, C.c_void_p(tiles.data_ptr()),
+                                        plan.tiles, C.byref(out)))
+        return comm.reduce(comm.exchange(tiles))
+    N.check(N.lib().lq_mdi_linform2(N.ctx(), *args, 0, 1, None, plan.tiles, C.byref(out)))
+    return out.value
 
 
 def linform_plan(g, counts):

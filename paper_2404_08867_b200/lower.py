@@ -33,6 +33,7 @@ from .expr import Expr, add, const, free_vars, func, mul, power, topo, var
 __all__ = [
     "linear_form", "quad_form", "recognize_plain", "PlainFamily",
     "Program", "compile_program", "separate", "SepTerm", "Factor", "weighted_linear_outer", "WeightedOuter",
+    "linear_outer2", "LinearOuter2",
     "MAX_SLOTS", "INSN_DTYPE", "LinearOuter", "linear_outer", "recognize_linear_program",
 ]
 
@@ -777,3 +778,61 @@ def weighted_linear_outer(e):
     if lo is None:
         return None
     return WeightedOuter(lo.G, lo.beta, {ax: mul(1.0, fs) for ax, fs in weights.items()})
+
+
+@dataclass
+class LinearOuter2:
+    """e = G(<beta1, x>, <beta2, x>): the maximal affine subexpressions fall into
+    exactly two proportionality classes.  ``G`` is an Expr in var(1), var(2)."""
+
+    G: Expr
+    beta1: dict
+    beta2: dict
+
+
+def linear_outer2(e, rel_tol=4.0 * 2.0**-52):
+    """Split e = G(<beta1, x>, <beta2, x>) with two independent coefficient
+    directions, or None (one direction: linear_outer; three or more: no
+    collapse of this kind).  The reference's levels carry the pairs of
+    partial forms for these (exprcore.py:139-169 collects like terms with
+    equal pairs)."""
+    leaves = {}
+    seen = set()
+    stack = [e]
+    while stack:
+        node = stack.pop()
+        if node in seen or not free_vars(node):
+            continue
+        seen.add(node)
+        lf = linear_form(node)
+        if lf is not None:
+            leaves[node] = lf
+            continue
+        stack.extend(_children_of(node))
+    groups = []                        # [(beta_ref, var index)]
+    repl = {}
+    for node, (alpha, beta) in leaves.items():
+        beta = {j: c for j, c in beta.items() if c != 0.0}
+        if not beta:
+            return None
+        hit = None
+        for ref, v in groups:
+            if set(beta) != set(ref):
+                continue
+            j0 = min(ref)
+            b = beta[j0] / ref[j0]
+            if all(abs(c - b * ref[j]) <= rel_tol * abs(c) for j, c in beta.items()):
+                hit = (b, v)
+                break
+        if hit is None:
+            if len(groups) == 2:
+                return None
+            groups.append((beta, len(groups) + 1))
+            hit = (1.0, len(groups))
+        repl[node] = add([(hit[0], var(hit[1]))], alpha)
+    if len(groups) != 2:
+        return None
+    G = _rebuild(e, repl)
+    if free_vars(G) != frozenset({1, 2}):
+        return None
+    return LinearOuter2(G, groups[0][0], groups[1][0])

@@ -203,6 +203,10 @@ def mdi_sum(g, grids, cfg=None, comm=None):
         rep = _linform(e, counts, levels, base_axes, cfg, t0, comm, weighted=not usable)
         if rep is not None:
             return rep
+        if not usable:
+            rep = _linform2(e, counts, levels, base_axes, cfg, t0, comm)
+            if rep is not None:
+                return rep
     if not usable:
         rep = _subgrid(e, grids, counts, levels, base_axes, cfg, t0, comm)
         if rep is not None:
@@ -373,6 +377,27 @@ def _linform(e, counts, levels, base_axes, cfg, t0, comm=None, weighted=True):
     return MdiReport(value=raw, levels=levels, base_dim=len(base_axes), level_nodes=tuple(stripped),
                      level_seconds=(0.0,) * levels, base_seconds=time.perf_counter() - t0, fallback=False,
                      log_raw=log_raw, sign=sign, method="linform", clusters=plan.support)
+
+
+def _linform2(e, counts, levels, base_axes, cfg, t0, comm=None):
+    """f = G(<beta1, y>, <beta2, y>), two commensurate forms: the reference's
+    levels carry the distinct pairs of partial forms (like-term collection,
+    exprcore.py:139-169); here their joint distribution, one direction per
+    level (lq_mdi_linform2), then G over its support.  None when e is not of
+    this form or the joint support exceeds its cap."""
+    plan = engine.linform2_plan(e, counts)
+    # the grid K1 x K2 over-counts the pairs a level actually reaches (both
+    # forms move with the same nodes), so only the support cap applies here;
+    # where the reference's levels would overflow its budget it sums the same
+    # grid directly
+    if not plan.ok:
+        return None
+    mean = engine.mdi_linform2_mean(plan, comm=comm)
+    raw, log_raw, sign = _raw_from_mean(mean, counts, _log_total(counts))
+    stripped = plan.level_support[:levels * cfg.m:cfg.m] if cfg.m > 1 else plan.level_support[:levels]
+    return MdiReport(value=raw, levels=levels, base_dim=len(base_axes), level_nodes=tuple(stripped),
+                     level_seconds=(0.0,) * levels, base_seconds=time.perf_counter() - t0, fallback=False,
+                     log_raw=log_raw, sign=sign, method="linform2", clusters=plan.support)
 
 
 def _raw_from_mean(mean, counts, log_total):

@@ -624,7 +624,12 @@ def linform_w_cases():
              # sums whose terms collapse by different branches
              ("(1 + sum(i=1..d, x[i]))^(-2) + exp(-sum(i=1..d, x[i]^2))", 10, 8, 8**10 + 1),
              ("3*(2 + sum(i=1..d, x[i]))^(-1) - 0.5*prod(i=1..d, 1 + x[i]) + 1.25", 8, 8, 8**8 + 1),
-             ("x[1]*x[2]*(1 + sum(i=1..d, x[i]))^(-3) + cos(sum(i=1..d, x[i]))", 9, 6, 6**9 + 1)]
+             ("x[1]*x[2]*(1 + sum(i=1..d, x[i]))^(-3) + cos(sum(i=1..d, x[i]))", 9, 6, 6**9 + 1),
+             # functions of two commensurate linear forms
+             ("(1 + sum(i=1..d, x[i]))^(-2)*(2 + sum(i=1..d, (-1)^i*x[i]))^(-1)", 8, 8, 8**8 + 1),
+             ("(1 + sum(i=1..d, x[i]))^(-2)*(2 + sum(i=1..d, (-1)^i*x[i]))^(-1)", 10, 8, 8**10 + 1),
+             ("exp(-((sum(i=1..d, x[i]) - 0.5*d)^2)/d)*cos(sum(i=1..d, i*x[i])/d)", 8, 6, 6**8 + 1),
+             ("1/(1 + (x[1] + x[2] + x[3] - x[4])^2 + (x[1] - 2*x[2] + 0.5*x[5])^2)", 6, 5, 5**6 + 1)]
     out = []
     for text, d, a, n in cases:
         f = exprcore.parse(text, d)

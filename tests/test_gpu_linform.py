@@ -170,7 +170,8 @@ def test_weighted_level_collapse_matches_reference():
     mdi_lr): each level's nodes carry phi_j(y_t) in the distribution update
     (lq_mdi_linform_w), including grids past the direct cap (d = 10, 12),
     weights on an axis outside the form and mixed-sign steps; and sums whose
-    terms collapse by different branches (method "terms")."""
+    terms collapse by different branches (method "terms"); and functions of
+    two commensurate forms (their joint distribution, method "linform2")."""
     methods = set()
     import paper_2404_08867_b200 as lq
     from conftest import load_golden, unhex
@@ -180,8 +181,8 @@ def test_weighted_level_collapse_matches_reference():
         want = unhex(c["value"])
         # a weighted form whose non-splitting piece spans <= 3 axes takes the
         # separable combine with a core instead (same collapse, same value)
-        assert rep.method in ("linform", "cores", "terms"), (c["text"], rep.method)
+        assert rep.method in ("linform", "cores", "terms", "linform2"), (c["text"], rep.method)
         assert abs(got - want) <= 1e-10 * abs(want), (c["text"], c["d"], got, want)
         assert (rep.levels, rep.base_dim, rep.fallback) == (c["levels"], c["base_dim"], c["fallback"]), c["text"]
         methods.add(rep.method)
-    assert {"linform", "terms"} <= methods, methods
+    assert {"linform", "terms", "linform2"} <= methods, methods
