@@ -5,7 +5,8 @@ shard, then the host-staged all-reduce) -- against the single-rank results of
 quad/mdi, bit for bit.  Covers every sharded branch: plain sums (index and
 FFT-form orbit layouts), separable MDI (node blocks), core factors (their
 sub-grid sweeps), the characteristic function (frequency nodes), the level
-collapse (support tiles) and the direct sweep (flat-index tiles).  (VERDICT r1 next-round item 5.)"""
+collapse (support tiles; weighted, two-form), term sums, the direct sweep
+(flat-index tiles) and a composite-modulus plain sum.  (VERDICT r1 next-round item 5.)"""
 
 import os
 import socket
@@ -32,6 +33,13 @@ def _jobs():
                                        4, 60, 60**4)))
     jobs.append(("mdi_cores", "mdi", ("exp(x[1]*x[2])*prod(i=3..d, 1/(1 + x[i]^2))", 8, 40, 40**8)))
     jobs.append(("implr_ratprod", "implr", ("prod(i=1..d, 1/(0.81 + (x[i]-0.6)^2))", 4, 30, 30**4)))
+    # round 2, session 2: weighted and two-form level collapse, term sums,
+    # a composite-modulus plain sum (divisor-class levels)
+    jobs.append(("mdi_weighted", "mdi", ("exp(-sum(i=1..d, x[i]^2))*(1 + sum(i=1..d, x[i]))^(-2)", 10, 8, 8**10 + 1)))
+    jobs.append(("mdi_two_forms", "mdi", ("(1 + sum(i=1..d, x[i]))^(-2)*(2 + sum(i=1..d, (-1)^i*x[i]))^(-1)",
+                                          8, 8, 8**8 + 1)))
+    jobs.append(("mdi_terms", "mdi", ("(1 + sum(i=1..d, x[i]))^(-2) + exp(-sum(i=1..d, x[i]^2))", 8, 8, 8**8 + 1)))
+    jobs.append(("slr_composite", "slr", (make_config(5).text, 1000, 12345679, 10**8)))
     return jobs
 
 
@@ -96,4 +104,5 @@ def test_ranks_reproduce_the_single_gpu_results(single, size):
             assert got[r][tag] == want, (size, r, tag, got[r][tag], want)
     methods = {tag: v[1][0] for tag, v in single.items() if v[1] is not None}
     assert methods == {"mdi_cfg2": "separable", "mdi_cfg4": "separable", "mdi_cfg5": "characteristic",
-                       "mdi_invpow_d10": "linform", "mdi_direct": "direct", "mdi_cores": "cores"}, methods
+                       "mdi_invpow_d10": "linform", "mdi_direct": "direct", "mdi_cores": "cores",
+                       "mdi_weighted": "linform", "mdi_two_forms": "linform2", "mdi_terms": "terms"}, methods

@@ -49,4 +49,7 @@ lq.mdi_lr(w, 8, 8, 8**8 + 1)
 del os.environ["LQ_LINFORM_SMEM"]
 lq.mdi_lr(lq.parse("(1 + sum(i=1..d, x[i]))^(-2) + exp(-sum(i=1..d, x[i]^2))", 6), 6, 6, 6**6 + 1)
 lq.p_alpha(lq.LatticeRule(1009, (1, 400)), 2)
+lq.mdi_lr(lq.parse("(1 + sum(i=1..d, x[i]))^(-2)*(2 + sum(i=1..d, (-1)^i*x[i]))^(-1)", 6), 6, 6, 6**6 + 1)
+cfg = make_config(5)
+lq.slr_integrate(lq.parse(cfg.text, cfg.d), lq.korobov_vector(12345679, 10**8, cfg.d))
 print("sanitize smoke ok")
