@@ -167,7 +167,19 @@ def _level_plan(d, cfg):
 def mdi_sum(g, grids, cfg=None, comm=None):
     """Full grid sum of g by dimension iteration (mdi.py:139-192).  ``comm``
     (distributed.Comm, size > 1) shards the device work of every branch across
-    ranks with one exchange; the result is the single-GPU one bit for bit."""
+    ranks with one exchange; the result is the single-GPU one bit for bit.
+
+    The collapse the reference's symbolic levels perform is taken by the first
+    branch that applies (``MdiReport.method``):
+      constant      -- closed form;
+      characteristic-- exp-abs of a linear form past the cap (extension);
+      linform       -- G(one commensurate form), or G times separable weights;
+      linform2      -- G(two commensurate forms);
+      separable / cores -- product-separable terms, pieces on <= 3 axes swept;
+      subgrid       -- unused axes multiply a sweep of the used ones;
+      terms         -- a sum whose terms collapse by different branches;
+      direct        -- the full sweep (the reference's fallback), reported
+                       without fallback where its levels certainly fit."""
     cfg = cfg if cfg is not None else MdiConfig()
     d = grids.d
     e = as_expr(g)
