@@ -24,7 +24,7 @@ import time
 
 
 from . import _native as N, engine
-from .expr import as_expr, evaluate, free_vars
+from .expr import as_expr, free_vars
 from .lattice import korobov_vector
 from .mdi import GridCapError, mdi_lr as _mdi_lr_single
 from .quad import _result

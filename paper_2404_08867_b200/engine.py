@@ -14,8 +14,8 @@ from collections import OrderedDict
 import numpy as np
 
 from . import _native as N
-from .expr import Expr, UnassignedVariableError, as_expr, evaluate, free_vars
-from .lower import (Program, compile_program, linear_outer, linear_outer2, recognize_linear_program, recognize_plain,
+from .expr import UnassignedVariableError, as_expr, evaluate, free_vars
+from .lower import (compile_program, linear_outer, linear_outer2, recognize_linear_program, recognize_plain,
                     separate, weighted_linear_outer)
 
 __all__ = ["PlainIntegrand", "plain_integrand", "lattice_sum", "tensor_program", "eval_array", "SeparablePlan",

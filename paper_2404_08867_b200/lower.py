@@ -28,7 +28,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .expr import Expr, add, const, free_vars, func, mul, power, topo, var
+from .expr import Expr, add, free_vars, func, mul, power, topo, var
 
 __all__ = [
     "linear_form", "quad_form", "recognize_plain", "PlainFamily",

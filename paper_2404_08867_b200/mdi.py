@@ -22,7 +22,6 @@ has no symbolic DAG).
 
 from __future__ import annotations
 
-import functools
 import math
 import time
 from dataclasses import dataclass
