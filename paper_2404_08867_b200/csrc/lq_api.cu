@@ -1168,15 +1168,29 @@ std::shared_ptr<const Pow2Plan> div_plan(uint32_t n, uint32_t a, int len, bool f
         }
         return pl;
     };
+    // a global bound on the chains of all levels (short orbits on many
+    // classes: one unit per few points) -- past it the whole plan is refused
+    // and the paired index kernel runs; it also bounds the host tables
+    const uint64_t unit_budget = 4 * ((uint64_t)n / (uint64_t)std::max(len, 1) + 1) + (1u << 20);
+    uint64_t units_total = 0;
+    bool over = false;
     auto plan_of = [&](uint64_t m) -> std::shared_ptr<const OrbPlan> {
         auto hit = plans.find(m);
         if (hit != plans.end()) return hit->second;
+        if (over) return nullptr;
         std::shared_ptr<const OrbPlan> pl;
         if (fft) {
             pl = build(m, len, true);
             if (pl && 2 * (uint64_t)pl->h < (uint64_t)len) pl = nullptr;
         }
         if (!pl && len_direct > 0) pl = build(m, len_direct, false);
+        if (pl) {
+            units_total += pl->units;
+            if (units_total > unit_budget) {
+                over = true;
+                pl = nullptr;
+            }
+        }
         plans[m] = pl;
         return pl;
     };
@@ -1194,7 +1208,7 @@ std::shared_ptr<const Pow2Plan> div_plan(uint32_t n, uint32_t a, int len, bool f
         if (m0 > n / 4) break;
     }
     std::shared_ptr<const Pow2Plan> out;
-    if (m0 <= n / 4) {
+    if (m0 <= n / 4 && !over) {
         auto P = std::make_shared<Pow2Plan>();
         P->small_n = m0;
         for (uint64_t m : divs)
