@@ -638,6 +638,14 @@ def linform_w_cases():
         out.append({"text": text, "d": d, "a": a, "n": n, "value": hx(val), "levels": rep.levels,
                     "base_dim": rep.base_dim, "fallback": rep.fallback,
                     "ref_seconds": round(time.perf_counter() - t0, 3)})
+    # the level-plan options (m axes per level, stripping order) on the same branches
+    for text, d, a, n in cases[:1] + cases[3:5] + cases[9:10] + cases[12:13]:
+        for m, order in ((2, "forward"), (1, "reverse"), (3, "reverse")):
+            f = exprcore.parse(text, d)
+            cfg = MdiConfig(m=m, order=order)
+            val, rep = mdi_lr(f, d, a, n, cfg=cfg, with_report=True)
+            out.append({"text": text, "d": d, "a": a, "n": n, "m": m, "order": order, "value": hx(val),
+                        "levels": rep.levels, "base_dim": rep.base_dim, "fallback": rep.fallback})
     return out
 
 

@@ -177,7 +177,8 @@ def test_weighted_level_collapse_matches_reference():
     from conftest import load_golden, unhex
     for c in load_golden("linform_w"):
         f = lq.parse(c["text"], c["d"])
-        got, rep = lq.mdi_lr(f, c["d"], c["a"], c["n"], with_report=True)
+        cfg = lq.MdiConfig(m=c.get("m", 1), order=c.get("order", "forward"))
+        got, rep = lq.mdi_lr(f, c["d"], c["a"], c["n"], cfg=cfg, with_report=True)
         want = unhex(c["value"])
         # a weighted form whose non-splitting piece spans <= 3 axes takes the
         # separable combine with a core instead (same collapse, same value)
