@@ -104,8 +104,10 @@ def run_row(spec, seed=0, unbounded=False):
                      seed if method == "mc" else None)
 
 
-def run_suite(suite, out_path, seed=0, unbounded=False, verbose=False):
-    """Every row of a suite on the GPU, written to ``out_path``; returns the records."""
+def run_suite(suite, out_path, seed=0, unbounded=False, figures=False, verbose=False):
+    """Every row of a suite on the GPU, written to ``out_path``; returns the
+    records.  ``figures`` is accepted for latquad's signature (bench.py:226);
+    rendering them is out of scope (matplotlib), so it is ignored."""
     records = []
     for spec in suite_specs(suite, unbounded=unbounded):
         rec = run_row(spec, seed, unbounded)

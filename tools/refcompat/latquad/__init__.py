@@ -8,7 +8,7 @@ when called."""
 from paper_2404_08867_b200 import *  # noqa: F401,F403
 from paper_2404_08867_b200 import __all__, __version__  # noqa: F401
 
-from . import bench, cli, corpus, exprcore, lattice, mdi, quad, transform  # noqa: F401,E402
+from . import bench, cli, corpus, exprcore, lattice, mdi, plots, quad, transform  # noqa: F401,E402
 
 from ._oos import (NonCartesianStructureError, TransformedIntegrand, bind, build_axis_grids,  # noqa: F401,E402
                    forward_transform, grid_completion, inverse_substitution, make_transformed_integrand,
