@@ -15,30 +15,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2404_08867_b200 as lq  # noqa: E402
 from oracle import np_expr, np_oracle  # noqa: E402
 
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden"))
-
-
-def texts(rng, count):
-    def index(depth, names):
-        if depth > 1 or rng.random() < 0.4:
-            return rng.choice([str(rng.randint(1, 3)), "d"] + list(names))
-        return f"({index(depth + 1, names)}{rng.choice(['+', '-', '*'])}{index(depth + 1, names)})"
-
-    def real(depth, names):
-        r = rng.random()
-        if depth > 3 or r < 0.25:
-            return rng.choice([f"x[{index(1, names)}]", repr(round(rng.uniform(-2, 2), 3)), "pi", "e"] + list(names))
-        if r < 0.55:
-            return f"{real(depth + 1, names)} {rng.choice(['+', '-', '*'])} {real(depth + 1, names)}"
-        if r < 0.65:
-            return f"({real(depth + 1, names)})^{rng.choice(['2', '3', '(1+1)'])}"
-        if r < 0.8:
-            return f"{rng.choice(['exp', 'sin', 'cos'])}({real(depth + 1, names)})"
-        if r < 0.9:
-            v = rng.choice(["i", "j", "k"])
-            return f"{rng.choice(['sum', 'prod'])}({v}=1..{rng.choice(['d', '2'])}, {real(depth + 1, names | {v})})"
-        return f"-{real(depth + 1, names)}"
-    return [real(0, frozenset()) for _ in range(count)]
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from fuzz_texts import texts  # noqa: E402
 
 
 rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
