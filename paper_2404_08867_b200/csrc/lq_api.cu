@@ -1135,7 +1135,58 @@ std::shared_ptr<const Pow2Plan> divplan_for(const lq_integrand* f, uint64_t n, c
     return P;
 }
 
+Layout plan_layout(const lq_integrand* f, uint64_t n, const uint64_t* z);
+
+// The layout of (f, n, z) is a pure function of n, z, f's kind, d, beta and
+// gamma and the LQ_ORBIT / LQ_FFT / LQ_PAIR switches.  Deciding it costs
+// O(d) 64-bit modular checks plus the planners' cache lookups (11 us at
+// d = 1000), paid on every call; a repeated call (the e2e loop, sub-range
+// calls of one sum) matches the last few inputs by bytes instead (~1 us).
+struct LayoutMemo {
+    uint64_t n = 0;
+    int kind = -1, d = -1, has_gamma = 0;
+    std::string env;
+    std::vector<uint64_t> z;
+    std::vector<double> beta, gamma;
+    Layout L;
+};
+
+std::string layout_env() {
+    std::string s;
+    for (const char* k : {"LQ_ORBIT", "LQ_FFT", "LQ_PAIR"}) {
+        const char* e = std::getenv(k);
+        s += e ? e : "";
+        s += '\x1f';
+    }
+    return s;
+}
+
 Layout layout_of(const lq_integrand* f, uint64_t n, const uint64_t* z) {
+    constexpr int kMemo = 4;
+    static thread_local LayoutMemo memo[kMemo];
+    static thread_local int next = 0;
+    if (!z || !f->beta || f->d < 1) return plan_layout(f, n, z);
+    const int d = f->d;
+    const int hg = f->gamma != nullptr;
+    std::string env = layout_env();
+    for (auto& m : memo)
+        if (m.n == n && m.kind == f->kind && m.d == d && m.has_gamma == hg && m.env == env &&
+            !std::memcmp(m.z.data(), z, sizeof(uint64_t) * d) &&
+            !std::memcmp(m.beta.data(), f->beta, sizeof(double) * d) &&
+            (!hg || !std::memcmp(m.gamma.data(), f->gamma, sizeof(double) * d)))
+            return m.L;
+    Layout L = plan_layout(f, n, z);
+    LayoutMemo& m = memo[next];
+    next = (next + 1) % kMemo;
+    m.n = n; m.kind = f->kind; m.d = d; m.has_gamma = hg; m.env = std::move(env);
+    m.z.assign(z, z + d);
+    m.beta.assign(f->beta, f->beta + d);
+    if (hg) m.gamma.assign(f->gamma, f->gamma + d); else m.gamma.clear();
+    m.L = L;
+    return L;
+}
+
+Layout plan_layout(const lq_integrand* f, uint64_t n, const uint64_t* z) {
     Layout L;
     bool fft2 = false;
     if ((L.p2 = pow2_for(f, n, z, &fft2)) || (L.p2 = divplan_for(f, n, z, &fft2))) {

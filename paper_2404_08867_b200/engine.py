@@ -13,7 +13,7 @@ from collections import OrderedDict
 
 import numpy as np
 
-from . import _native as N
+from . import _native as N, jit
 from .expr import UnassignedVariableError, as_expr, evaluate, free_vars
 from .lower import (compile_program, linear_outer, linear_outer2, recognize_linear_program, recognize_plain,
                     separate, weighted_linear_outer)
@@ -113,8 +113,9 @@ def attach_jit(pi, n):
     choice depends on (f, n) only -- not on the index range of the call -- so
     every rank of a sharded sum and every sub-range call of the same lattice
     run the same code."""
-    from . import jit
     interpreted = pi.family is None or pi.family.kind == "lin_prog" or n > 2**31
+    if not interpreted:
+        return
     n_insn = max(len(pi.program), 1)
     if interpreted and not pi.struct.prog.jit and jit.jit_wanted(int(n) * n_insn, n_insn):
         h = jit.compile_expr(pi.expr)
