@@ -309,6 +309,45 @@ def test_error_mapping_without_gpu():
         _native.ctx(0)
 
 
+def test_layout_memo_tracks_inputs(monkeypatch):
+    # layout_of memoises by input bytes: the same buffers rewritten in place,
+    # a different z, and the LQ_FFT / LQ_ORBIT / LQ_PAIR switches must each
+    # give a fresh decision, never the remembered one
+    import numpy as np
+    from paper_2404_08867_b200 import _native, engine
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("liblq.so not built")
+    cfg = make_config(5)
+    pi = engine.plain_integrand(lq.parse(cfg.text, cfg.d), cfg.d)
+    rule = lq.korobov_vector(cfg.plain_a, cfg.plain_n, cfg.d)
+    z = rule.z_reduced_array()
+    lay = lambda: _native.lattice_layout(pi.struct, rule.n, z)   # noqa: E731
+    assert lay().mode == _native.LAYOUT_ORBIT_FFT
+    assert lay().mode == _native.LAYOUT_ORBIT_FFT                 # memo hit
+    monkeypatch.setenv("LQ_FFT", "0")
+    assert lay().mode == _native.LAYOUT_ORBIT
+    monkeypatch.setenv("LQ_ORBIT", "0")
+    assert lay().mode == _native.LAYOUT_PAIRED
+    monkeypatch.setenv("LQ_PAIR", "0")
+    assert lay().mode == _native.LAYOUT_INDEX
+    monkeypatch.delenv("LQ_FFT")
+    monkeypatch.delenv("LQ_ORBIT")
+    monkeypatch.delenv("LQ_PAIR")
+    assert lay().mode == _native.LAYOUT_ORBIT_FFT
+    beta = pi._keep[0]
+    saved = beta.copy()
+    try:
+        beta *= 1e6                      # fails the FFT accuracy guard: direct orbit kernel
+        assert lay().mode == _native.LAYOUT_ORBIT
+    finally:
+        beta[:] = saved
+    assert lay().mode == _native.LAYOUT_ORBIT_FFT
+    z2 = z.copy()
+    z2[2] = (z2[2] + 1) % rule.n         # no longer a Korobov vector: mirror pairs
+    assert _native.lattice_layout(pi.struct, rule.n, z2).mode == _native.LAYOUT_PAIRED
+    assert lay().mode == _native.LAYOUT_ORBIT_FFT
+
+
 def test_layout_selection_without_gpu():
     # host-side layout decisions (no GPU needed): FFT form for cfg5, the
     # accuracy guard keeps huge-coefficient linear forms on the direct orbit
