@@ -74,6 +74,10 @@ struct LqLat64 {
         return lq_exact_div((double)lq_mulmod64(i, __ldg(z + j), n, inv), nd, inv);
     }
 };
+struct LqArr {
+    const double* v;
+    __device__ __forceinline__ double operator()(int k) const { return v[k]; }
+};
 struct LqTen {
     const double* nodes; const i64* off; const u32* digit;
     __device__ __forceinline__ double operator()(int j) const { return __ldg(nodes + off[j] + digit[j]); }
@@ -88,11 +92,62 @@ extern "C" __global__ void __launch_bounds__(256) lq_jit_lattice(const void* zt,
     __shared__ double sh[8];
     const u64 i0 = base + (u64)blockIdx.x * 4096ull + (u64)threadIdx.x * 16ull;
     double s = 0.0;
+#ifdef LQ_STEP
+    // the coordinates a point uses, stepped from point to point of the
+    // thread's run: r_k(i + 1) = r_k(i) + z_k mod n (one add and one wrap per
+    // coordinate instead of a modular product), each fed to the same exactly
+    // rounded division -- the coordinates, and so the sum, are unchanged
+    if (i0 < end) {
+        if (wide) {
+            const u64* z = (const u64*)zt;
+            const u64 im = i0 < n ? i0 : i0 % n;
+            u64 r[LQ_NU];
+#pragma unroll
+            for (int k = 0; k < LQ_NU; ++k) r[k] = lq_mulmod64(im, __ldg(z + lq_use[k]), n, inv);
+            for (int p = 0; p < 16; ++p) {
+                if (i0 + p < end) {
+                    double xv[LQ_NU];
+#pragma unroll
+                    for (int k = 0; k < LQ_NU; ++k) xv[k] = lq_exact_div((double)r[k], nd, inv);
+                    s += lq_fc(LqArr{xv});
+                }
+#pragma unroll
+                for (int k = 0; k < LQ_NU; ++k) {
+                    const u64 t = r[k] + __ldg(z + lq_use[k]);
+                    r[k] = t >= n ? t - n : t;
+                }
+            }
+        } else {
+            const LqZZ* zz = (const LqZZ*)zt;
+            const u32 n32 = (u32)n;
+            u32 r[LQ_NU];
+#pragma unroll
+            for (int k = 0; k < LQ_NU; ++k) {
+                const LqZZ t = zz[lq_use[k]];
+                r[k] = lq_shoup((u32)i0, t.z, t.zs, n32);
+            }
+            for (int p = 0; p < 16; ++p) {
+                if (i0 + p < end) {
+                    double xv[LQ_NU];
+#pragma unroll
+                    for (int k = 0; k < LQ_NU; ++k) xv[k] = lq_exact_div((double)r[k], nd, inv);
+                    s += lq_fc(LqArr{xv});
+                }
+#pragma unroll
+                for (int k = 0; k < LQ_NU; ++k) {
+                    const u32 t = r[k] + zz[lq_use[k]].z;
+                    const u32 w = t - n32;
+                    r[k] = w < t ? w : t;
+                }
+            }
+        }
+    }
+#else
     for (int p = 0; p < 16; ++p) {
         const u64 i = i0 + p;
         if (i < end) {
             if (wide) {
-                LqLat64 x{i % n, n, nd, inv, (const u64*)zt};
+                LqLat64 x{i < n ? i : i % n, n, nd, inv, (const u64*)zt};
                 s += lq_f(x);
             } else {
                 LqLat32 x{(u32)i, (u32)n, nd, inv, (const LqZZ*)zt};
@@ -100,6 +155,7 @@ extern "C" __global__ void __launch_bounds__(256) lq_jit_lattice(const void* zt,
             }
         }
     }
+#endif
     s = lq_block_sum(s, sh);
     if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
 }
@@ -117,8 +173,28 @@ extern "C" __global__ void __launch_bounds__(256) lq_jit_tensor(int d, const i64
         digit[k] = (u32)(rem % c);
         rem /= c;
     }
-    LqTen x{nodes, off, digit};
     double s = 0.0;
+#ifdef LQ_STEP
+    // the used axes' node values stay in registers; after each odometer step
+    // only the axes up to the highest one that moved are re-read (mostly the
+    // first axis alone) -- same node values, same sum
+    double xv[LQ_NU];
+#pragma unroll
+    for (int k = 0; k < LQ_NU; ++k) xv[k] = __ldg(nodes + off[lq_use[k]] + digit[lq_use[k]]);
+    for (int p = 0; p < 16; ++p) {
+        if (s0 + p < end) s += lq_fc(LqArr{xv});
+        int moved = 0;
+        for (int k = 0; k < d; ++k) {
+            moved = k;
+            if (++digit[k] < (u64)counts[k]) break;
+            digit[k] = 0;
+        }
+#pragma unroll
+        for (int k = 0; k < LQ_NU; ++k)
+            if (lq_use[k] <= moved) xv[k] = __ldg(nodes + off[lq_use[k]] + digit[lq_use[k]]);
+    }
+#else
+    LqTen x{nodes, off, digit};
     for (int p = 0; p < 16; ++p) {
         if (s0 + p < end) s += lq_f(x);
         for (int k = 0; k < d; ++k) {
@@ -126,6 +202,7 @@ extern "C" __global__ void __launch_bounds__(256) lq_jit_tensor(int d, const i64
             digit[k] = 0;
         }
     }
+#endif
     s = lq_block_sum(s, sh);
     if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
 }
@@ -139,12 +216,33 @@ def _lit(v):
     return v.hex()
 
 
+# stepped coordinates in the lattice kernel for expressions of at most this
+# many distinct coordinates (their residues live in registers)
+STEP_MAX_VARS = 24
+
+
 def source_for(e, var_map=None, n_axes=1):
-    """CUDA source of an expression: ``lq_f(x)`` plus both kernel bodies."""
+    """CUDA source of an expression: ``lq_f(x)`` (coordinates by index),
+    ``lq_fc(x)`` (coordinates by their rank among the used ones, for the
+    stepped lattice kernel) plus both kernel bodies."""
     vm = var_map if var_map is not None else (lambda j: j - 1)
+    order = list(topo(e))
+    uses = sorted({vm(node.idx) for node in order if node.op == "var"})
+    body = _body(order, e, vm)
+    src = _PRELUDE + (f"template <class X> __device__ __forceinline__ double lq_f(const X& x) {{\n{body}\n}}\n")
+    if 0 < len(uses) <= STEP_MAX_VARS:
+        rank = {j: k for k, j in enumerate(uses)}
+        bodyc = _body(order, e, lambda j: rank[vm(j)])
+        src += (f"template <class X> __device__ __forceinline__ double lq_fc(const X& x) {{\n{bodyc}\n}}\n"
+                f"#define LQ_STEP 1\n#define LQ_NU {len(uses)}\n"
+                f"__constant__ int lq_use[LQ_NU] = {{{', '.join(str(j) for j in uses)}}};\n")
+    return src + f"#define LQ_AXES {max(1, int(n_axes))}\n" + _KERNELS
+
+
+def _body(order, e, vm):
     names = {}
     lines = []
-    for k, node in enumerate(topo(e)):
+    for k, node in enumerate(order):
         t = f"t{k}"
         names[node] = t
         op = node.op
@@ -171,10 +269,8 @@ def source_for(e, var_map=None, n_axes=1):
         else:
             fn = {"exp": "exp", "sin": "sin", "cos": "cos", "abs": "fabs"}[op]
             lines.append(f"    const double {t} = {fn}({names[node.args[0]]});")
-    body = "\n".join(lines)
-    fdef = (f"template <class X> __device__ __forceinline__ double lq_f(const X& x) {{\n{body}\n"
-            f"    return {names[e]};\n}}\n")
-    return _PRELUDE + fdef + f"#define LQ_AXES {max(1, int(n_axes))}\n" + _KERNELS
+    lines.append(f"    return {names[e]};")
+    return "\n".join(lines)
 
 
 class _Module:
