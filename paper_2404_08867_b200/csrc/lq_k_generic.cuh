@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kThreads) k_prog_lattice(const lq_insn* __rest
             double f = 0.0;
             if (i < end) {
                 if (WIDE) {
-                    LatSrc64 src{i % n, n, n_d, inv_n, ninv_mm, (const uint64_t*)ztab};
+                    LatSrc64 src{i < n ? i : i % n, n, n_d, inv_n, ninv_mm, (const uint64_t*)ztab};
                     f = run_program<NS>(prog, n_insn, result, src, slot);
                 } else {
                     LatSrc32 src{(uint32_t)i, (uint32_t)n, n_d, inv_n, (const uint2*)ztab};
