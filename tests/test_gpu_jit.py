@@ -76,3 +76,50 @@ def test_jit_wide_modulus(lq, monkeypatch):
     pts = np.array([[float((i * zj) % n) / n for zj in z] for i in range(lo, lo + 8192)])
     ref = float(np.sum(pts[:, 1] * np.exp(pts[:, 0] * pts[:, 2]) + np.sin(pts[:, 0] ** 2)))
     assert abs(s - ref) <= 1e-12 * abs(ref)
+
+
+@pytest.mark.parametrize("n,lo,hi", [(2**40 + 15, 2**40 + 15 - 3000, 2**40 + 15 + 3001),   # wraps past n
+                                     (2**40 + 15, 12345, 12345 + 70001),
+                                     (2147483647, 2147483647 - 40003, 2147483647),
+                                     (1000003, 7, 1000003)])
+def test_jit_stepped_coordinates(lq, monkeypatch, n, lo, hi):
+    # the JIT lattice kernel steps each used coordinate's residue from point
+    # to point (r += z mod n) instead of forming i*z mod n: same coordinates as
+    # the interpreter's per-point products, over unaligned sub-ranges and
+    # ranges that cross i = n
+    from paper_2404_08867_b200 import engine, jit
+    d = 5
+    f = lq.parse("x[2]*exp(x[1]*x[5]) + sin(x[1]^2) - x[4]^3", d)
+    z = np.asarray([1, 123456789013 % n, (2**39 + 7) % n, 0, 977 % n], dtype=np.uint64)
+    monkeypatch.setenv("LQ_JIT", "0")
+    engine._plain_cache.clear()
+    interp = engine.plain_integrand(f, d, force_program=True)
+    a = engine.lattice_sum(interp, n, z, lo, hi)
+    monkeypatch.setenv("LQ_JIT", "always")
+    engine._plain_cache.clear()
+    jitted = engine.plain_integrand(f, d, force_program=True)
+    b = engine.lattice_sum(jitted, n, z, lo, hi)
+    assert jitted.struct.prog.jit and "#define LQ_STEP" in jit.source_for(jitted.expr)
+    assert abs(a - b) <= 1e-13 * max(abs(a), 1.0), (a, b)
+    idx = np.arange(lo, hi, dtype=object) % n
+    if len(idx) <= 80000:
+        cols = [np.array([float(int(i) * int(zj) % n) / n for i in idx]) for zj in z]
+        ref = float(np.sum(cols[1] * np.exp(cols[0] * cols[4]) + np.sin(cols[0] ** 2) - cols[3] ** 3))
+        assert abs(b - ref) <= 1e-12 * abs(ref)
+
+
+def test_jit_many_coordinates_unstepped(lq, monkeypatch):
+    # past STEP_MAX_VARS used coordinates the kernel keeps per-point products
+    from paper_2404_08867_b200 import engine, jit
+    d = 30
+    f = lq.parse("exp(-sum(i=1..d, x[i]^2)/7) + x[3]*x[30]", d)
+    rule = lq.korobov_vector(4567, 2**35 + 3, d)
+    monkeypatch.setenv("LQ_JIT", "0")
+    engine._plain_cache.clear()
+    a = engine.lattice_sum(engine.plain_integrand(f, d, force_program=True), rule.n, rule.z_reduced_array(), 0, 300000)
+    monkeypatch.setenv("LQ_JIT", "always")
+    engine._plain_cache.clear()
+    pj = engine.plain_integrand(f, d, force_program=True)
+    b = engine.lattice_sum(pj, rule.n, rule.z_reduced_array(), 0, 300000)
+    assert pj.struct.prog.jit and "#define LQ_STEP" not in jit.source_for(pj.expr)
+    assert abs(a - b) <= 1e-13 * abs(a)

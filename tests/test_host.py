@@ -526,3 +526,17 @@ def test_composite_modulus_layouts_cover_the_lattice():
             assert (miss.value, rep.value) == (0, 0), (n, a, d, miss.value, rep.value)
             used.add(N.lattice_layout(pi.struct, n, z).mode)
     assert N.LAYOUT_ORBIT_POW2 in used
+
+
+def test_jit_source_step_selection():
+    # the JIT lattice kernel steps coordinates for expressions of at most
+    # STEP_MAX_VARS distinct coordinates: lq_use lists them (0-based, sorted)
+    # and lq_fc reads them by rank
+    from paper_2404_08867_b200 import jit
+    src = jit.source_for(lq.parse("x[7]*exp(x[2]) + x[7]^2", 9))
+    assert "#define LQ_STEP 1" in src and "#define LQ_NU 2" in src
+    assert "lq_use[LQ_NU] = {1, 6}" in src
+    assert "x(0)" in src and "x(1)" in src and "x(6)" in src    # lq_fc by rank, lq_f by index
+    wide = jit.source_for(lq.parse("sum(i=1..d, x[i]^2)", jit.STEP_MAX_VARS + 1))
+    assert "#define LQ_STEP" not in wide
+    assert "#define LQ_STEP" not in jit.source_for(lq.parse("2.5", 3))
