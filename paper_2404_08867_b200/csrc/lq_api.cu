@@ -161,9 +161,12 @@ int smem_optin(lq_ctx* c, const void* fn, size_t bytes) {
     return LQ_OK;
 }
 
-int grid_for(lq_ctx* c, const void* kernel, int64_t work) {
+int grid_for(lq_ctx* c, const void* kernel, int64_t work, int fallback_per_sm = 1) {
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, lq::kThreads, 0);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, lq::kThreads, 0) != cudaSuccess) {
+        cudaGetLastError();
+        per_sm = fallback_per_sm;   // (a grid larger than resident only queues)
+    }
     if (per_sm < 1) per_sm = 1;
     int64_t g = (int64_t)c->sm_count * per_sm;
     if (work < g) g = work;
@@ -578,9 +581,13 @@ int launch_tiles(lq_ctx* c, const lq_integrand* f, uint64_t n, const uint64_t* z
     if (cudaKernel_t jk = lq_jit_lattice_kernel(pg->jit)) {
         const void* ztab = dz;
         int wide_i = wide ? 1 : 0;
-        void* args[] = {(void*)&ztab, (void*)&n, (void*)&n_d, (void*)&inv_n, (void*)&base, (void*)&end, (void*)&wide_i, (void*)&tiles_dev};
+        int64_t nt = ntiles;
+        void* args[] = {(void*)&ztab, (void*)&n, (void*)&n_d, (void*)&inv_n, (void*)&base, (void*)&end, (void*)&wide_i, (void*)&tiles_dev, (void*)&nt};
+        // a resident grid striding over the tiles: each thread's coordinate
+        // residues are set up once and carried from tile to tile
+        const int grid = grid_for(c, (const void*)jk, ntiles, 2048 / lq::kThreads);
         t_begin(c);
-        CK(cudaLaunchKernel((const void*)jk, dim3((unsigned)ntiles), dim3(lq::kThreads), args, 0, c->stream));
+        CK(cudaLaunchKernel((const void*)jk, dim3((unsigned)grid), dim3(lq::kThreads), args, 0, c->stream));
         t_end(c);
         return LQ_OK;
     }
@@ -1682,8 +1689,12 @@ int tensor_tiles(lq_ctx* c, const lq_program* pg, int32_t d, const int64_t* coun
     if (cudaKernel_t jk = lq_jit_tensor_kernel(pg->jit)) {
         const void *pc = dc, *po = doff, *pn = dn;
         void* tp = tiles;
-        void* args[] = {(void*)&d, (void*)&pc, (void*)&po, (void*)&pn, (void*)&s_begin, (void*)&s_end, (void*)&tp};
-        CK(cudaLaunchKernel((const void*)jk, dim3((unsigned)ntiles), dim3(lq::kThreads), args, 0, c->stream));
+        int64_t nt = ntiles;
+        void* args[] = {(void*)&d, (void*)&pc, (void*)&po, (void*)&pn, (void*)&s_begin, (void*)&s_end, (void*)&tp, (void*)&nt};
+        // a resident grid striding over the tiles: the odometers are set up
+        // once by division and carried from tile to tile
+        const int jgrid = grid_for(c, (const void*)jk, ntiles, 2048 / lq::kThreads);
+        CK(cudaLaunchKernel((const void*)jk, dim3((unsigned)jgrid), dim3(lq::kThreads), args, 0, c->stream));
     } else if (ns == 32)
         lq::k_prog_tensor<32><<<grid, lq::kThreads, 0, c->stream>>>((const lq_insn*)dp, pg->n_insn, pg->result, d, (const int64_t*)dc, (const int64_t*)doff, (const double*)dn, s_begin, s_end, ntiles, (double*)tiles);
     else

@@ -136,16 +136,30 @@ __global__ void __launch_bounds__(kThreads) k_prog_tensor(const lq_insn* __restr
                                                           uint64_t base, uint64_t end, int64_t ntiles,
                                                           double* __restrict__ tile_out) {
     __shared__ double sh[8];
+    __shared__ uint32_t gapd[kMaxAxes];
     double slot[NS];
     uint32_t digit[kMaxAxes];
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t s0 = base + (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kPts;
-        uint64_t rem = s0;
+    // each thread's odometer is set up once by division and carried to the
+    // CTA's next tile by adding the mixed-radix digits of G kTile - kPts
+    if (threadIdx.x == 0) {
+        uint64_t rem = (uint64_t)gridDim.x * kTile - kPts;
+        for (int k = 0; k < d; ++k) {
+            const uint64_t c = (uint64_t)counts[k];
+            gapd[k] = (uint32_t)(rem % c);
+            rem /= c;
+        }
+    }
+    __syncthreads();
+    {
+        uint64_t rem = base + (uint64_t)blockIdx.x * kTile + (uint64_t)threadIdx.x * kPts;
         for (int k = 0; k < d; ++k) {
             const uint64_t c = (uint64_t)counts[k];
             digit[k] = (uint32_t)(rem % c);
             rem /= c;
         }
+    }
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t s0 = base + (uint64_t)tile * kTile + (uint64_t)threadIdx.x * kPts;
         TensorSrc src{nodes, off, digit};
         double s = 0.0;
         for (int p = 0; p < kPts; ++p) {
@@ -157,6 +171,13 @@ __global__ void __launch_bounds__(kThreads) k_prog_tensor(const lq_insn* __restr
         }
         s = block_sum(s, sh);
         if (threadIdx.x == 0) tile_out[tile] = s;
+        uint32_t carry = 0;
+        for (int k = 0; k < d; ++k) {
+            const uint64_t c = (uint64_t)counts[k];
+            const uint64_t t = (uint64_t)digit[k] + gapd[k] + carry;
+            carry = t >= c;
+            digit[k] = (uint32_t)(carry ? t - c : t);
+        }
     }
 }
 

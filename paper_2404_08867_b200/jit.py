@@ -85,126 +85,159 @@ struct LqTen {
 """
 
 _KERNELS = r"""
-// plain lattice sum: 256 threads x 16 consecutive points per tile (the
-// interpreter's tiling, so partials line up with k_prog_lattice)
-extern "C" __global__ void __launch_bounds__(256) lq_jit_lattice(const void* zt, u64 n, double nd, double inv,
-                                                                u64 base, u64 end, int wide, double* tile_out) {
-    __shared__ double sh[8];
-    const u64 i0 = base + (u64)blockIdx.x * 4096ull + (u64)threadIdx.x * 16ull;
-    double s = 0.0;
-#ifdef LQ_STEP
-    // the coordinates a point uses, stepped from point to point of the
-    // thread's run: r_k(i + 1) = r_k(i) + z_k mod n (one add and one wrap per
-    // coordinate instead of a modular product), each fed to the same exactly
-    // rounded division -- the coordinates, and so the sum, are unchanged
-    if (i0 < end) {
-        if (wide) {
-            const u64* z = (const u64*)zt;
-            const u64 im = i0 < n ? i0 : i0 % n;
-            u64 r[LQ_NU];
-#pragma unroll
-            for (int k = 0; k < LQ_NU; ++k) r[k] = lq_mulmod64(im, __ldg(z + lq_use[k]), n, inv);
-            for (int p = 0; p < 16; ++p) {
-                if (i0 + p < end) {
-                    double xv[LQ_NU];
-#pragma unroll
-                    for (int k = 0; k < LQ_NU; ++k) xv[k] = lq_exact_div((double)r[k], nd, inv);
-                    s += lq_fc(LqArr{xv});
-                }
-#pragma unroll
-                for (int k = 0; k < LQ_NU; ++k) {
-                    const u64 t = r[k] + __ldg(z + lq_use[k]);
-                    r[k] = t >= n ? t - n : t;
-                }
-            }
-        } else {
-            const LqZZ* zz = (const LqZZ*)zt;
-            const u32 n32 = (u32)n;
-            u32 r[LQ_NU];
-#pragma unroll
-            for (int k = 0; k < LQ_NU; ++k) {
-                const LqZZ t = zz[lq_use[k]];
-                r[k] = lq_shoup((u32)i0, t.z, t.zs, n32);
-            }
-            for (int p = 0; p < 16; ++p) {
-                if (i0 + p < end) {
-                    double xv[LQ_NU];
-#pragma unroll
-                    for (int k = 0; k < LQ_NU; ++k) xv[k] = lq_exact_div((double)r[k], nd, inv);
-                    s += lq_fc(LqArr{xv});
-                }
-#pragma unroll
-                for (int k = 0; k < LQ_NU; ++k) {
-                    const u32 t = r[k] + zz[lq_use[k]].z;
-                    const u32 w = t - n32;
-                    r[k] = w < t ? w : t;
-                }
-            }
-        }
-    }
-#else
-    for (int p = 0; p < 16; ++p) {
-        const u64 i = i0 + p;
-        if (i < end) {
-            if (wide) {
-                LqLat64 x{i < n ? i : i % n, n, nd, inv, (const u64*)zt};
-                s += lq_f(x);
-            } else {
-                LqLat32 x{(u32)i, (u32)n, nd, inv, (const LqZZ*)zt};
-                s += lq_f(x);
-            }
-        }
-    }
-#endif
-    s = lq_block_sum(s, sh);
-    if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
+__device__ __forceinline__ u64 lq_addmod64(u64 a, u64 b, u64 n) {   // a, b < n < 2^53
+    const u64 t = a + b;
+    return t >= n ? t - n : t;
+}
+__device__ __forceinline__ u32 lq_addmod32(u32 a, u32 b, u32 n) {   // a, b < n <= 2^31
+    const u32 t = a + b, w = t - n;
+    return w < t ? w : t;
 }
 
-// direct tensor-grid sum, flat index first axis fastest (odometer per thread)
-extern "C" __global__ void __launch_bounds__(256) lq_jit_tensor(int d, const i64* counts, const i64* off,
-                                                               const double* nodes, u64 base, u64 end,
-                                                               double* tile_out) {
+// plain lattice sum: 256 threads x 16 consecutive points per tile (the
+// interpreter's tiling, so the tile partials line up with k_prog_lattice);
+// CTAs stride over the tiles
+extern "C" __global__ void __launch_bounds__(256) lq_jit_lattice(const void* zt, u64 n, double nd, double inv,
+                                                                u64 base, u64 end, int wide, double* tile_out,
+                                                                i64 ntiles) {
     __shared__ double sh[8];
-    u32 digit[LQ_AXES];
-    const u64 s0 = base + (u64)blockIdx.x * 4096ull + (u64)threadIdx.x * 16ull;
-    u64 rem = s0;
-    for (int k = 0; k < d; ++k) {
-        const u64 c = (u64)counts[k];
-        digit[k] = (u32)(rem % c);
-        rem /= c;
-    }
-    double s = 0.0;
 #ifdef LQ_STEP
-    // the used axes' node values stay in registers; after each odometer step
-    // only the axes up to the highest one that moved are re-read (mostly the
-    // first axis alone) -- same node values, same sum
-    double xv[LQ_NU];
+    // the coordinates a point uses are stepped from point to point of the
+    // thread's run, r_k(i + 1) = r_k(i) + z_k mod n, and from one tile of the
+    // CTA to its next by jump_k = (G 4096 - 16) z_k mod n: one add and one wrap
+    // per coordinate instead of a modular product, each fed to the same
+    // exactly rounded division -- the coordinates, and so the sums, are those
+    // of the per-point products
+    __shared__ u64 jump[LQ_NU];
+    const u64 gap = (u64)gridDim.x * 4096ull - 16ull;
+    if (threadIdx.x < LQ_NU) {
+        const int j = lq_use[threadIdx.x];
+        jump[threadIdx.x] = wide ? lq_mulmod64(gap % n, ((const u64*)zt)[j], n, inv)
+                                 : (gap % n) * (u64)((const LqZZ*)zt)[j].z % n;
+    }
+    __syncthreads();
+    const u64 i00 = base + (u64)blockIdx.x * 4096ull + (u64)threadIdx.x * 16ull;
+    if (wide) {
+        const u64* z = (const u64*)zt;
+        u64 r[LQ_NU];
+        const u64 im = i00 < n ? i00 : i00 % n;
 #pragma unroll
-    for (int k = 0; k < LQ_NU; ++k) xv[k] = __ldg(nodes + off[lq_use[k]] + digit[lq_use[k]]);
-    for (int p = 0; p < 16; ++p) {
-        if (s0 + p < end) s += lq_fc(LqArr{xv});
-        int moved = 0;
-        for (int k = 0; k < d; ++k) {
-            moved = k;
-            if (++digit[k] < (u64)counts[k]) break;
-            digit[k] = 0;
+        for (int k = 0; k < LQ_NU; ++k) r[k] = lq_mulmod64(im, __ldg(z + lq_use[k]), n, inv);
+        for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const u64 i0 = base + (u64)tile * 4096ull + (u64)threadIdx.x * 16ull;
+            double s = 0.0;
+            for (int p = 0; p < 16; ++p) {
+                if (i0 + p < end) {
+                    double xv[LQ_NU];
+#pragma unroll
+                    for (int k = 0; k < LQ_NU; ++k) xv[k] = lq_exact_div((double)r[k], nd, inv);
+                    s += lq_fc(LqArr{xv});
+                }
+#pragma unroll
+                for (int k = 0; k < LQ_NU; ++k) r[k] = lq_addmod64(r[k], __ldg(z + lq_use[k]), n);
+            }
+            s = lq_block_sum(s, sh);
+            if (threadIdx.x == 0) tile_out[tile] = s;
+#pragma unroll
+            for (int k = 0; k < LQ_NU; ++k) r[k] = lq_addmod64(r[k], jump[k], n);
         }
+    } else {
+        const LqZZ* zz = (const LqZZ*)zt;
+        const u32 n32 = (u32)n;
+        u32 r[LQ_NU];
 #pragma unroll
-        for (int k = 0; k < LQ_NU; ++k)
-            if (lq_use[k] <= moved) xv[k] = __ldg(nodes + off[lq_use[k]] + digit[lq_use[k]]);
+        for (int k = 0; k < LQ_NU; ++k) {
+            const LqZZ t = zz[lq_use[k]];
+            r[k] = lq_shoup((u32)i00, t.z, t.zs, n32);
+        }
+        for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const u64 i0 = base + (u64)tile * 4096ull + (u64)threadIdx.x * 16ull;
+            double s = 0.0;
+            for (int p = 0; p < 16; ++p) {
+                if (i0 + p < end) {
+                    double xv[LQ_NU];
+#pragma unroll
+                    for (int k = 0; k < LQ_NU; ++k) xv[k] = lq_exact_div((double)r[k], nd, inv);
+                    s += lq_fc(LqArr{xv});
+                }
+#pragma unroll
+                for (int k = 0; k < LQ_NU; ++k) r[k] = lq_addmod32(r[k], zz[lq_use[k]].z, n32);
+            }
+            s = lq_block_sum(s, sh);
+            if (threadIdx.x == 0) tile_out[tile] = s;
+#pragma unroll
+            for (int k = 0; k < LQ_NU; ++k) r[k] = lq_addmod32(r[k], (u32)jump[k], n32);
+        }
     }
 #else
-    LqTen x{nodes, off, digit};
-    for (int p = 0; p < 16; ++p) {
-        if (s0 + p < end) s += lq_f(x);
-        for (int k = 0; k < d; ++k) {
-            if (++digit[k] < (u64)counts[k]) break;
-            digit[k] = 0;
+    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const u64 i0 = base + (u64)tile * 4096ull + (u64)threadIdx.x * 16ull;
+        double s = 0.0;
+        for (int p = 0; p < 16; ++p) {
+            const u64 i = i0 + p;
+            if (i < end) {
+                if (wide) {
+                    LqLat64 x{i < n ? i : i % n, n, nd, inv, (const u64*)zt};
+                    s += lq_f(x);
+                } else {
+                    LqLat32 x{(u32)i, (u32)n, nd, inv, (const LqZZ*)zt};
+                    s += lq_f(x);
+                }
+            }
         }
+        s = lq_block_sum(s, sh);
+        if (threadIdx.x == 0) tile_out[tile] = s;
     }
 #endif
-    s = lq_block_sum(s, sh);
-    if (threadIdx.x == 0) tile_out[blockIdx.x] = s;
+}
+
+// direct tensor-grid sum, flat index first axis fastest: an odometer per
+// thread, set up once by division and carried from one tile of the CTA to its
+// next by adding the mixed-radix digits of G 4096 - 16
+extern "C" __global__ void __launch_bounds__(256) lq_jit_tensor(int d, const i64* counts, const i64* off,
+                                                               const double* nodes, u64 base, u64 end,
+                                                               double* tile_out, i64 ntiles) {
+    __shared__ double sh[8];
+    __shared__ u32 gapd[LQ_AXES];
+    if (threadIdx.x == 0) {
+        u64 rem = (u64)gridDim.x * 4096ull - 16ull;
+        for (int k = 0; k < d; ++k) {
+            const u64 c = (u64)counts[k];
+            gapd[k] = (u32)(rem % c);
+            rem /= c;
+        }
+    }
+    __syncthreads();
+    u32 digit[LQ_AXES];
+    {
+        u64 rem = base + (u64)blockIdx.x * 4096ull + (u64)threadIdx.x * 16ull;
+        for (int k = 0; k < d; ++k) {
+            const u64 c = (u64)counts[k];
+            digit[k] = (u32)(rem % c);
+            rem /= c;
+        }
+    }
+    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const u64 s0 = base + (u64)tile * 4096ull + (u64)threadIdx.x * 16ull;
+        double s = 0.0;
+        LqTen x{nodes, off, digit};
+        for (int p = 0; p < 16; ++p) {
+            if (s0 + p < end) s += lq_f(x);
+            for (int k = 0; k < d; ++k) {
+                if (++digit[k] < (u64)counts[k]) break;
+                digit[k] = 0;
+            }
+        }
+        s = lq_block_sum(s, sh);
+        if (threadIdx.x == 0) tile_out[tile] = s;
+        u32 carry = 0;
+        for (int k = 0; k < d; ++k) {
+            const u64 c = (u64)counts[k];
+            u64 t = (u64)digit[k] + gapd[k] + carry;
+            carry = t >= c;
+            digit[k] = (u32)(carry ? t - c : t);
+        }
+    }
 }
 """
 
