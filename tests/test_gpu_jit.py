@@ -123,3 +123,42 @@ def test_jit_many_coordinates_unstepped(lq, monkeypatch):
     b = engine.lattice_sum(pj, rule.n, rule.z_reduced_array(), 0, 300000)
     assert pj.struct.prog.jit and "#define LQ_STEP" not in jit.source_for(pj.expr)
     assert abs(a - b) <= 1e-13 * abs(a)
+
+
+def test_carried_state_across_tiles_lattice(lq, monkeypatch):
+    # 2^25 indices: past one resident grid's worth of tiles (148 SMs x up to
+    # 8 CTAs x 4096), so every thread carries its residues to further tiles;
+    # the interpreter forms every coordinate by a modular product per point
+    from paper_2404_08867_b200 import engine
+    d = 4
+    n = 2**41 + 21
+    f = lq.parse("exp(-x[1]*x[2]) + cos(3*x[3] - x[4]^2)", d)
+    z = np.asarray([1, 987654321987 % n, (2**40 + 3) % n, 55555], dtype=np.uint64)
+    lo, hi = 12345, 12345 + (1 << 25)
+    monkeypatch.setenv("LQ_JIT", "0")
+    engine._plain_cache.clear()
+    a = engine.lattice_sum(engine.plain_integrand(f, d, force_program=True), n, z, lo, hi)
+    monkeypatch.setenv("LQ_JIT", "always")
+    engine._plain_cache.clear()
+    pj = engine.plain_integrand(f, d, force_program=True)
+    b = engine.lattice_sum(pj, n, z, lo, hi)
+    assert pj.struct.prog.jit
+    assert abs(a - b) <= 1e-13 * abs(a), (a, b)
+
+
+@pytest.mark.parametrize("jit_mode", ["0", "always"])
+def test_carried_odometer_across_tiles_tensor(lq, monkeypatch, jit_mode):
+    # a 2.1e7-node grid (more tiles than one resident grid holds): the carried
+    # odometers of the interpreter and JIT tensor kernels against the oracle's
+    # direct grid sum
+    from oracle import np_oracle as orc
+    from paper_2404_08867_b200 import engine
+    from paper_2404_08867_b200.transform import AxisGridSet
+    monkeypatch.setenv("LQ_JIT", jit_mode)
+    text = "x[2]*exp(x[1]*x[2]) + sin(x[1] + x[3]^2)"
+    counts = (277, 271, 281)
+    f = lq.parse(text, 3)
+    grids = AxisGridSet(None, counts, None, None, midpoint=True)
+    got = engine.tensor_sum(f, grids)
+    want = orc.direct_tensor_sum(text, orc.midpoint_nodes(list(counts)))
+    assert abs(got - want) <= 1e-12 * abs(want), (got, want)
