@@ -95,7 +95,10 @@ typedef struct {
     lq_program outer;       /* LQ_FAM_LIN_PROG: G of one variable (variable 0 = <beta,x>) */
 } lq_integrand;
 
-/* ---- context ---------------------------------------------------------- */
+/* ---- context ----------------------------------------------------------
+ * Plumbing with no reference counterpart: latquad is single-process numpy
+ * (quad.py:96-131 runs its loops on the host); a context holds what those
+ * loops keep implicitly -- the device, a stream, scratch and cached plans.  */
 int lq_ctx_create(int device, lq_ctx** out);
 int lq_ctx_destroy(lq_ctx* ctx);
 /* Order all work on this cudaStream_t (NULL: the context's own stream). */
@@ -236,13 +239,16 @@ int lq_mdi_block_sums(lq_ctx* ctx, const lq_insn* insn, int32_t n_insn, const lq
                       int32_t nshards, double* part_dev);
 /* Combine: S_f = fixed tree over blocks; term t = coef_t * prod_{f in term t} S_f
  * * exp(log_extra_t), evaluated in log-polar form (sum log|S|, sum arg S).
- * term_ptr[n_terms+1] indexes term_fac.  out[0]=log|raw|, out[1]=sign(Re raw)
+ * term_ptr[n_terms+1] indexes term_fac (replaces the level loop's folded
+ * coefficients, mdi.py:152-165, and the base sweep, mdi.py:166-179).
+ * out[0]=log|raw|, out[1]=sign(Re raw)
  * (0 if raw == 0), out[2]=Re raw as a double (may under/overflow), out[3]=Im raw. */
 int lq_mdi_combine(lq_ctx* ctx, const double* part_dev, const lq_factor* factors, int32_t n_factors, int32_t nblk,
                    const int32_t* term_ptr, const int32_t* term_fac, const double* coef_re,
                    const double* coef_im, const double* log_extra, int32_t n_terms,
                    double* out4);
-/* Single-GPU convenience: block sums + combine. */
+/* Single-GPU convenience: block sums + combine -- the whole of mdi_sum
+ * (mdi.py:139-192) for a separable integrand.                               */
 int lq_mdi_sum(lq_ctx* ctx, const lq_insn* insn, int32_t n_insn, const lq_factor* factors,
                int32_t n_factors, const double* nodes, int64_t n_nodes, const int32_t* term_ptr, const int32_t* term_fac,
                const double* coef_re, const double* coef_im, const double* log_extra,
@@ -250,7 +256,7 @@ int lq_mdi_sum(lq_ctx* ctx, const lq_insn* insn, int32_t n_insn, const lq_factor
 
 /* ---- characteristic-function MDI for K exp(kappa |alpha + <beta,y>|),
  * kappa < 0 (BASELINE config 5; the reference cannot express |.|, so this is
- * an extension):  sum_grid = K prod_j N_j (|kappa|/pi) int_R Re[e^{i w alpha}
+ * an extension of mdi_sum, mdi.py:139-192):  sum_grid = K prod_j N_j (|kappa|/pi) int_R Re[e^{i w alpha}
  * prod_j phi_j(w)] / (kappa^2 + w^2) dw,  phi_j(w) = (1/N_j) sum_t e^{i w beta_j y_t}.
  * w_nodes/w_weights: host quadrature on [0, W] (even integrand, factor 2
  * applied by the caller).  out2[0] = log|sum_k w_k |kappa|/(kappa^2+w_k^2)
@@ -316,13 +322,15 @@ int lq_korobov_values(lq_ctx* ctx, uint64_t n, int32_t d, const double* gamma, d
 /* ---- JIT: the lowering step before the path ------
  * Compile CUDA source that defines extern "C" kernels lq_jit_lattice and/or
  * lq_jit_tensor (generated from an expression by paper_2404_08867_b200/jit.py)
- * with NVRTC for sm_100a.  Attach the handle to lq_program.jit: lattice and
+ * with NVRTC for sm_100a (replaces eval_array inside the sums,
+ * exprcore.py:442-480).  Attach the handle to lq_program.jit: lattice and
  * tensor sums then launch the compiled kernel instead of the interpreter,
  * with the same tiles and reduction tree.  NVRTC is loaded with dlopen.     */
 int lq_jit_create(const char* source, const char* name, lq_jit** out, char* log, int64_t log_cap);
 int lq_jit_destroy(lq_jit* jit);
 
-/* ---- FP64 roofline probe: DFMA chains on every SM; returns TFLOP/s ----- */
+/* ---- FP64 roofline probe: DFMA chains on every SM; returns TFLOP/s -----
+ * (measurement only; bench.py's roofline denominator, no reference twin) */
 int lq_fp64_peak(lq_ctx* ctx, int32_t iters, double* tflops, float* ms);
 
 #ifdef __cplusplus
