@@ -509,6 +509,9 @@ def main():
                                                        else ""))},
                      "fp64_pipe_busy_ncu": prof.get({N.LAYOUT_ORBIT_FFT: "k_orbit_fft", N.LAYOUT_ORBIT: "k_orbit"}
                                                     .get(lay.mode, "k_fam_index_kernel"), {}).get("fp64_pipe_pct_of_peak"),
+                     # integer work is not counted in flops; its pipe shares beside FP64's
+                     "pipes_pct_ncu": prof.get({N.LAYOUT_ORBIT_FFT: "k_orbit_fft", N.LAYOUT_ORBIT: "k_orbit"}
+                                               .get(lay.mode, "k_fam_index_kernel"), {}).get("pipes_pct_of_peak"),
                      "executed_dfma_tflops": executed, "executed_frac": executed / fp64_peak,
                      "peak_source": "measured in-run by lq_fp64_peak (DFMA chains, ~1 s); "
                                     "MEASURED_PEAKS.json has no FP64 entry"},
