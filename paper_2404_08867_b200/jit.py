@@ -220,6 +220,29 @@ extern "C" __global__ void __launch_bounds__(256) lq_jit_tensor(int d, const i64
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const u64 s0 = base + (u64)tile * 4096ull + (u64)threadIdx.x * 16ull;
         double s = 0.0;
+#ifdef LQ_STEP
+        // the used axes' node values stay in registers: a step of the first
+        // axis re-reads one node, a carry re-reads them all -- same nodes
+        double xv[LQ_NU];
+#pragma unroll
+        for (int k = 0; k < LQ_NU; ++k) xv[k] = __ldg(nodes + off[lq_use[k]] + digit[lq_use[k]]);
+        const u32 c0 = (u32)counts[0];
+        const double* node0 = nodes + off[0];
+        for (int p = 0; p < 16; ++p) {
+            if (s0 + p < end) s += lq_fc(LqArr{xv});
+            if (++digit[0] < c0) {
+                if (lq_use[0] == 0) xv[0] = __ldg(node0 + digit[0]);
+            } else {
+                digit[0] = 0;
+                for (int k = 1; k < d; ++k) {
+                    if (++digit[k] < (u64)counts[k]) break;
+                    digit[k] = 0;
+                }
+#pragma unroll
+                for (int k = 0; k < LQ_NU; ++k) xv[k] = __ldg(nodes + off[lq_use[k]] + digit[lq_use[k]]);
+            }
+        }
+#else
         LqTen x{nodes, off, digit};
         for (int p = 0; p < 16; ++p) {
             if (s0 + p < end) s += lq_f(x);
@@ -228,6 +251,7 @@ extern "C" __global__ void __launch_bounds__(256) lq_jit_tensor(int d, const i64
                 digit[k] = 0;
             }
         }
+#endif
         s = lq_block_sum(s, sh);
         if (threadIdx.x == 0) tile_out[tile] = s;
         u32 carry = 0;
