@@ -4,10 +4,13 @@ SURVEY.md §8(f) item 1).
 An integrand outside the closed families becomes straight-line device code in
 the reference's evaluation order (sums ``v = const; v = v + c*t``, products
 ``v = coeff; v = v*f``, /root/reference/pkg/src/latquad/exprcore.py:442-480),
-with every constant as an exact hex literal and every coordinate fetched once
-per point.  liblq compiles it for sm_100a (``lq_jit_create``) and launches it
-with the same tiles and fixed reduction tree as the bytecode interpreter it
-replaces, so the two agree to rounding and the JIT is purely a speed-up.
+with every constant as an exact hex literal and every coordinate formed once
+per point -- for expressions of at most STEP_MAX_VARS coordinates by stepping
+its residue from the thread's previous point (r + z_j mod n) instead of a
+modular product, the same integer either way.  liblq compiles it for sm_100a
+(``lq_jit_create``) and launches it over a resident grid with the same tiles
+and fixed reduction tree as the bytecode interpreter it replaces, so the two
+agree to rounding and the JIT is purely a speed-up.
 """
 
 from __future__ import annotations
