@@ -88,13 +88,12 @@ struct LqTen {
 """
 
 _KERNELS = r"""
-__device__ __forceinline__ u64 lq_addmod64(u64 a, u64 b, u64 n) {   // a, b < n < 2^53
-    const u64 t = a + b;
-    return t >= n ? t - n : t;
-}
-__device__ __forceinline__ u32 lq_addmod32(u32 a, u32 b, u32 n) {   // a, b < n <= 2^31
-    const u32 t = a + b, w = t - n;
-    return w < t ? w : t;
+// (r + b) mod n for an integer r in [0, n) and bm = b - n with b in [0, n),
+// n < 2^53, all exact doubles: r + bm is exact and lies in [-n, n); the sign
+// bit (high word) says whether n goes back on.  r + bm == 0 rounds to +0.0.
+__device__ __forceinline__ double lq_addmod_d(double r, double bm, double nd) {
+    const double t = r + bm;
+    return __double2hiint(t) < 0 ? t + nd : t;
 }
 
 // plain lattice sum: 256 threads x 16 consecutive points per tile (the
@@ -107,70 +106,59 @@ extern "C" __global__ void __launch_bounds__(256) lq_jit_lattice(const void* zt,
 #ifdef LQ_STEP
     // the coordinates a point uses are stepped from point to point of the
     // thread's run, r_k(i + 1) = r_k(i) + z_k mod n, and from one tile of the
-    // CTA to its next by jump_k = (G 4096 - 16) z_k mod n: one add and one wrap
-    // per coordinate instead of a modular product, each fed to the same
+    // CTA to its next by jump_k = (G 4096 - 16) z_k mod n, each fed to the same
     // exactly rounded division -- the coordinates, and so the sums, are those
-    // of the per-point products
-    __shared__ u64 jump[LQ_NU];
+    // of the per-point products.  The residues are integers below n < 2^53 and
+    // are carried as exact doubles: one add of z_k - n, a sign test on the
+    // high word and a conditional add of n per coordinate, with no integer
+    // carry chain and no int -> double conversion (issue-bound before:
+    // profiles/r02_jit_lattice_step.md)
+    __shared__ double jmn[LQ_NU];
     const u64 gap = (u64)gridDim.x * 4096ull - 16ull;
     if (threadIdx.x < LQ_NU) {
         const int j = lq_use[threadIdx.x];
-        jump[threadIdx.x] = wide ? lq_mulmod64(gap % n, ((const u64*)zt)[j], n, inv)
-                                 : (gap % n) * (u64)((const LqZZ*)zt)[j].z % n;
+        const u64 jump = wide ? lq_mulmod64(gap % n, ((const u64*)zt)[j], n, inv)
+                              : (gap % n) * (u64)((const LqZZ*)zt)[j].z % n;
+        jmn[threadIdx.x] = (double)jump - nd;
     }
     __syncthreads();
     const u64 i00 = base + (u64)blockIdx.x * 4096ull + (u64)threadIdx.x * 16ull;
+    double r[LQ_NU], zmn[LQ_NU];
     if (wide) {
         const u64* z = (const u64*)zt;
-        u64 r[LQ_NU];
         const u64 im = i00 < n ? i00 : i00 % n;
 #pragma unroll
-        for (int k = 0; k < LQ_NU; ++k) r[k] = lq_mulmod64(im, __ldg(z + lq_use[k]), n, inv);
-        for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const u64 i0 = base + (u64)tile * 4096ull + (u64)threadIdx.x * 16ull;
-            double s = 0.0;
-            for (int p = 0; p < 16; ++p) {
-                if (i0 + p < end) {
-                    double xv[LQ_NU];
-#pragma unroll
-                    for (int k = 0; k < LQ_NU; ++k) xv[k] = lq_exact_div((double)r[k], nd, inv);
-                    s += lq_fc(LqArr{xv});
-                }
-#pragma unroll
-                for (int k = 0; k < LQ_NU; ++k) r[k] = lq_addmod64(r[k], __ldg(z + lq_use[k]), n);
-            }
-            s = lq_block_sum(s, sh);
-            if (threadIdx.x == 0) tile_out[tile] = s;
-#pragma unroll
-            for (int k = 0; k < LQ_NU; ++k) r[k] = lq_addmod64(r[k], jump[k], n);
+        for (int k = 0; k < LQ_NU; ++k) {
+            const u64 zk = __ldg(z + lq_use[k]);
+            r[k] = (double)lq_mulmod64(im, zk, n, inv);
+            zmn[k] = (double)zk - nd;
         }
     } else {
         const LqZZ* zz = (const LqZZ*)zt;
-        const u32 n32 = (u32)n;
-        u32 r[LQ_NU];
 #pragma unroll
         for (int k = 0; k < LQ_NU; ++k) {
             const LqZZ t = zz[lq_use[k]];
-            r[k] = lq_shoup((u32)i00, t.z, t.zs, n32);
+            r[k] = (double)lq_shoup((u32)i00, t.z, t.zs, (u32)n);
+            zmn[k] = (double)t.z - nd;
         }
-        for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const u64 i0 = base + (u64)tile * 4096ull + (u64)threadIdx.x * 16ull;
-            double s = 0.0;
-            for (int p = 0; p < 16; ++p) {
-                if (i0 + p < end) {
-                    double xv[LQ_NU];
+    }
+    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const u64 i0 = base + (u64)tile * 4096ull + (u64)threadIdx.x * 16ull;
+        double s = 0.0;
+        for (int p = 0; p < 16; ++p) {
+            if (i0 + p < end) {
+                double xv[LQ_NU];
 #pragma unroll
-                    for (int k = 0; k < LQ_NU; ++k) xv[k] = lq_exact_div((double)r[k], nd, inv);
-                    s += lq_fc(LqArr{xv});
-                }
-#pragma unroll
-                for (int k = 0; k < LQ_NU; ++k) r[k] = lq_addmod32(r[k], zz[lq_use[k]].z, n32);
+                for (int k = 0; k < LQ_NU; ++k) xv[k] = lq_exact_div(r[k], nd, inv);
+                s += lq_fc(LqArr{xv});
             }
-            s = lq_block_sum(s, sh);
-            if (threadIdx.x == 0) tile_out[tile] = s;
 #pragma unroll
-            for (int k = 0; k < LQ_NU; ++k) r[k] = lq_addmod32(r[k], (u32)jump[k], n32);
+            for (int k = 0; k < LQ_NU; ++k) r[k] = lq_addmod_d(r[k], zmn[k], nd);
         }
+        s = lq_block_sum(s, sh);
+        if (threadIdx.x == 0) tile_out[tile] = s;
+#pragma unroll
+        for (int k = 0; k < LQ_NU; ++k) r[k] = lq_addmod_d(r[k], jmn[k], nd);
     }
 #else
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
